@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""Benchmark of the SPH hot path (arXiv 2505.14538) on B200: one KDK hydro step per
+"step" = kick/drift -> cell rebuild (device radix sort) -> density + h iteration (+finalize)
+-> gradient (+ghost) -> force (+CFL dt) -> closing kick, i.e. every SURVEY §8(a) row.
+
+Metric (BASELINE.json): SPH pair interactions per second (density + gradient + force,
+directed pairs) and the time per hydro step.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C4] [--impl ours|reference]
+
+Under torchrun (N > 1) every rank runs the same workload on its own GPU (independent
+replicas, "scaling": "weak"); the timed region is bracketed by a barrier and
+torch.cuda.synchronize(), and the max over ranks is reported.  Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+# Algorithmic FP32 work per pair (FMA = 2 flops), frozen here and in
+# density 54 / directed pair, gradient 30 / directed pair, force 95 /
+# UNORDERED pair.
+FLOPS_DENSITY, FLOPS_GRADIENT, FLOPS_FORCE_UNORDERED = 54.0, 30.0, 95.0
+# FP32 peak derived from unit counts and clock: 148 SM x 128 lanes x 2 x 1.965 GHz.
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+
+WORKLOADS = {
+    "C4": ("gresho256", lambda: W.gresho(256)),
+    "C4j": ("gresho256_jitter0.1", lambda: W.gresho(256, jitter=0.1)),
+    "C2": ("sod2x64", lambda: W.sod(64)),
+    "C1": ("lattice16", lambda: W.lattice(16)),
+    "G128": ("gresho128", lambda: W.gresho(128)),
+    "G64": ("gresho64", lambda: W.gresho(64)),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="C4", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample", default="G64", choices=sorted(WORKLOADS))
+    return ap.parse_args()
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,utilization.gpu,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self._proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                           "--format=csv,noheader,nounits", "-lms", "100"],
+                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self._proc = None
+        return self
+
+    def _read(self):
+        for line in self._proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self._proc:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except Exception:
+                self._proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        util = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        loaded = [x for x, u in zip(sm, util) if u > 50] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if s[3 + k].lower() == "active"})
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        return {"sm_mhz": float(np.median(loaded)) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_init(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        import torch
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    return world, rank, local
+
+
+def oracle_rate(sample_key, steps=1, threads=None):
+    """The fp64 cell-list oracle, as it stands, on a bounded sample: one full hydro pass."""
+    import oracle
+
+    name, gen = WORKLOADS[sample_key]
+    p = gen()
+    if threads:
+        oracle.set_threads(threads)
+    o = oracle.Oracle(oracle.Params(), mode="cells")
+    times, inter = [], 0
+    for _ in range(steps):
+        st = oracle.State.from_particles(p)
+        t0 = time.perf_counter()
+        r = o.hydro(st, dt_ghost=1e-4, first_step=True)
+        times.append(time.perf_counter() - t0)
+        inter = int(r["density"]["count"].sum()) * 2 + int(r["force"]["count"].sum())
+    t = float(np.mean(times))
+    return {"value": inter / t, "unit": "interactions/s", "cores": oracle.max_threads(), "kind": "oracle",
+            "sample": f"{name}: one full hydro pass (density+h, gradient, force) with the fp64 cell-list "
+                      f"oracle, {p['X'].shape[0]} particles, {inter} interactions, {t:.2f} s/pass"}, t, inter, times
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    for _ in range(args.warmup):
+        pass  # the oracle has no warm-up state; warm-up steps would only repeat the same pass
+    base, t, inter, times = oracle_rate(args.cpu_sample, steps=args.steps)
+    name, _ = WORKLOADS[args.workload]
+    line = {"impl": "reference", "metric": "SPH pair interactions/sec (density+gradient+force)",
+            "value": base["value"], "unit": "interactions/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOADS[args.cpu_sample][0], "bench_workload": name,
+                       "note": "fp64 oracle on host cores; bounded sample of the workload family"},
+            "cpu_baseline": base,
+            "e2e": {"value": base["value"], "unit": "interactions/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, world, rank, local):
+    import torch
+
+    from paper_2505_14538_b200 import Context
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    name, gen = WORKLOADS[args.workload]
+    p = gen()
+    n = p["X"].shape[0]
+    stream = torch.cuda.Stream(device=dev)
+    ctx = Context(p, stream=stream.cuda_stream, device=local)
+    dt = 1e-4
+
+    def ev():
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        return e
+
+    def step(log=None):
+        nonlocal dt
+        marks = [ev()]
+        ctx.kick_drift(0.5 * dt, dt)
+        st = ctx.density()
+        marks.append(ev())
+        ctx.gradient(dt)
+        marks.append(ev())
+        dt_next = ctx.force()
+        marks.append(ev())
+        ctx.kick_drift(0.5 * dt, 0.0)
+        marks.append(ev())
+        c = ctx.counters()
+        if log is not None:
+            log.append((marks, st, c))
+        dt = float(min(dt_next, 2 * dt))
+        return st, c
+
+    # first density pass establishes a consistent state (h converged, a computed)
+    ctx.density()
+    ctx.gradient(dt)
+    dt = min(ctx.force(), 1e-3)
+    for _ in range(args.warmup):
+        step()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.counters()["kernel_launches"]
+    log = []
+    with Clocks(local) as clk:
+        t0 = ev()
+        for _ in range(args.steps):
+            step(log)
+        t1 = ev()
+        torch.cuda.synchronize()
+    launches = ctx.counters()["kernel_launches"] - launches0
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ph = np.zeros(4)
+    inter = 0
+    pd = pg = pf = ph_iter = 0
+    iters = []
+    for marks, st, c in log:
+        for k in range(4):
+            ph[k] += marks[k].elapsed_time(marks[k + 1])
+        pd += c["pairs_density"]
+        pg += c["pairs_gradient"]
+        pf += c["pairs_force"]
+        ph_iter += c["pairs_h_iter"]
+        iters.append(st["iterations"])
+    inter = pd + pg + pf
+    K = args.steps
+    ms_step = ms / K
+    value = inter * world / (ms * 1e-3)
+    t_force = ph[2] / K * 1e-3
+    t_dens = ph[0] / K * 1e-3
+    t_grad = ph[1] / K * 1e-3
+    flops_force = FLOPS_FORCE_UNORDERED * (pf / K) / 2.0
+    flops_dens = FLOPS_DENSITY * (ph_iter / K)
+    flops_grad = FLOPS_GRADIENT * (pg / K)
+    kernels = {
+        "density": {"ms": 1e3 * t_dens, "tflops": flops_dens / t_dens / 1e12, "share": ph[0] / ms},
+        "gradient": {"ms": 1e3 * t_grad, "tflops": flops_grad / t_grad / 1e12, "share": ph[1] / ms},
+        "force": {"ms": 1e3 * t_force, "tflops": flops_force / t_force / 1e12, "share": ph[2] / ms},
+    }
+    dom = max(("density", "gradient", "force"), key=lambda k: kernels[k]["ms"])
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "r01", "ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch", {}).get(dom)
+        except Exception:
+            traffic = None
+    roof = {"bound": "alu", "kernel": dom, "achieved": kernels[dom]["tflops"], "peak": FP32_PEAK_TFLOPS,
+            "unit": "TFLOP/s", "frac": kernels[dom]["tflops"] / FP32_PEAK_TFLOPS, "traffic": traffic,
+            "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (DESIGN.md §7)"}
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(ctx, p, torch, dev, stream, max(2, min(K, 5)), world)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = oracle_rate(args.cpu_sample)[0]
+    if rank == 0:
+        line = {
+            "metric": "SPH pair interactions/sec (density+gradient+force) and time per hydro step",
+            "value": value, "unit": "interactions/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": name, "particles": n, "parallelism": f"replicas{world}" if world > 1 else "1gpu",
+                       "step": "KDK: kick/drift, rebuild, density+h-iteration, gradient, force+dt, kick",
+                       "l2": "inputs larger than L2 (n x ~300 B >> 126 MB)",
+                       "interactions_per_step": inter / K, "density_passes_mean": float(np.mean(iters))},
+            "gpu_launches": int(launches),
+            "kernels": kernels,
+            "roofline": roof,
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+
+
+def run_e2e(ctx, p, torch, dev, stream, K, world):
+    """Same metric through the public API with host buffers: every step uploads the
+    particles from pinned host memory (sph_set_particles), runs density + gradient +
+    force, and reads a and du/dt back to pinned host memory (sph_get)."""
+    n = p["X"].shape[0]
+
+    def pinned(a):
+        t = torch.empty(a.shape, dtype={np.uint32: torch.int32, np.float32: torch.float32}[a.dtype.type],
+                        pin_memory=True)
+        t.numpy()[...] = a.view(np.int32) if a.dtype == np.uint32 else a
+        return t
+
+    host = {k: pinned(p[k]) for k in ("X", "v", "m", "u", "h", "alpha_v", "alpha_c")}
+    hin = {k: (host[k].numpy().view(np.uint32) if k == "X" else host[k].numpy()) for k in host}
+    a_out = torch.empty((n, 3), dtype=torch.float32, pin_memory=True)
+    du_out = torch.empty((n,), dtype=torch.float32, pin_memory=True)
+    h2d = sum(v.nbytes for v in hin.values())
+    d2h = a_out.numel() * 4 + du_out.numel() * 4
+
+    from paper_2505_14538_b200 import binding
+
+    def one():
+        ctx.set_particles(hin)
+        ctx.density()
+        ctx.gradient(1e-4)
+        ctx.force()
+        binding.lib().sph_get(ctx.h, binding.FIELDS["a"][0], a_out.data_ptr(), 0)
+        binding.lib().sph_get(ctx.h, binding.FIELDS["du"][0], du_out.data_ptr(), 0)
+        return ctx.counters()
+
+    one()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    inter = 0
+    for _ in range(K):
+        c = one()
+        inter += c["pairs_density"] + c["pairs_gradient"] + c["pairs_force"]
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([dt], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    return {"value": inter * world / dt, "unit": "interactions/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * dt / K,
+            "note": "host-timed (perf_counter) around upload + hydro pass + read-back; no kick/drift"}
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_init(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

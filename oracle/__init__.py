@@ -248,14 +248,15 @@ class Oracle:
         ii = _idx(n, idx)
         g = geom or self.geometry(st)
         pp = np.ascontiguousarray(np.stack([f, P, c, B, rho, st.u, alpha_v, alpha_c], axis=1))
-        out = np.full((n, 8), np.nan)
+        out = np.full((n, 10), np.nan)
         vm = None if valid is None else np.ascontiguousarray(valid, dtype=np.uint8)
         hm = float(np.nanmax(h if valid is None else np.where(valid, h, np.nan)))
         status = lib().orc_force(g.h, ctypes.byref(self.params), _ptr(ii, _I64), ii.size, _ptr(h, _D),
                                  _ptr(np.ascontiguousarray(st.v), _D), _ptr(st.m, _D), _ptr(pp, _D),
                                  None if vm is None else _ptr(vm, _U8), hm, _ptr(out, _D))
         return dict(status=status, a=out[:, 0:3], du=out[:, 3], v_sig=out[:, 4], scale_a=out[:, 5],
-                    scale_u=out[:, 6], count=out[:, 7])
+                    scale_u=out[:, 6], count=out[:, 7], scale_cond=out[:, 8],
+                    scale_tail=out[:, 9])
 
     def dt(self, h, v_sig, idx=None):
         ii = _idx(h.shape[0], idx)

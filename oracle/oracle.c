@@ -63,6 +63,12 @@ double orc_dw(double q) {
   if (q < 2.0) { double t = 2.0 - q; return -0.75 * t * t; }
   return 0.0;
 }
+/* d2w/dq2 (used only for a tolerance scale of the parity tests) */
+double orc_ddw(double q) {
+  if (q < 1.0) return -3.0 + 4.5 * q;
+  if (q < 2.0) return 1.5 * (2.0 - q);
+  return 0.0;
+}
 /* W, dW/dr and dW/dh.  dW/dh = -(3 W + r dW/dr)/h is Eq. 6's summand with n_d = 3
  * and "grad_i W" read as the scalar dW/dr (R6). */
 void orc_kernel(double r, double h, double* W, double* dWdr, double* dWdh) {
@@ -449,7 +455,7 @@ int orc_force(const orc_geom* g, const orc_params* p, const int64_t* idx, int64_
       const double* qi = pp + 8 * i;
       double fi = qi[0], Pi_ = qi[1], ci = qi[2], Bi = qi[3], rhoi = qi[4], ui = qi[5], avi = qi[6], aci = qi[7];
       double Ai = Pi_ / (rhoi * rhoi);
-      double a[3] = {0, 0, 0}, du = 0.0, vsig = 2.0 * ci, sa = 0.0, su = 0.0, d[3];
+      double a[3] = {0, 0, 0}, du = 0.0, vsig = 2.0 * ci, sa = 0.0, su = 0.0, sc = 0.0, st = 0.0, d[3];
       int64_t cnt = 0;
       for (int64_t k = 0; k < nn; ++k) {
         int64_t j = buf[k];
@@ -489,10 +495,26 @@ int orc_force(const orc_geom* g, const orc_params* p, const int64_t* idx, int64_
         if (vs > vsig) vsig = vs;
         sa += m[j] * fabs(S) * r;
         su += m[j] * (fabs(t1) + fabs(t2) + fabs(D));
+        /* sensitivity of D to the pressure difference inside v_c: sqrt(2|P_i-P_j|/rho) has an
+         * unbounded derivative at P_i = P_j, so an input error e (P_i+P_j) moves v_c by
+         * sqrt(2 e (P_i+P_j)/(rho_i+rho_j)); sc = sum_j m_j |D_ij/v_c| sqrt((P_i+P_j)/(rho_i+rho_j)) */
+        sc += m[j] * fabs(acij * (ui - uj) * (Gi + Gj) * r / (rhoi + rhoj)) * sqrt((Pi_ + Pj) / (rhoi + rhoj));
+        /* sensitivity to the kernel derivative near the support edge: w'(q) ~ (2-q)^2 has a
+         * large relative error when q -> 2 in any finite precision.  A relative error e of q
+         * moves w' by e q |w''(q)|; st = the du terms with |w'| replaced by q |w''(q)|, so the
+         * du error from rounding q is <= e st. */
+        {
+          double qi = r / h[i], qj = r / h[j];
+          double Ki = (r2 < Hi * Hi) ? fi * qi * fabs(orc_ddw(qi)) / (PI * h[i] * h[i] * h[i] * h[i] * r) : 0.0;
+          double Kj = (r2 < Hj * Hj) ? fj * qj * fabs(orc_ddw(qj)) / (PI * h[j] * h[j] * h[j] * h[j] * r) : 0.0;
+          st += m[j] * ((fabs(Ai) * Ki + fabs(0.5 * PiV) * 0.5 * (Ki + Kj)) * fabs(vr) +
+                        fabs(acij * vc * (ui - uj)) * (Ki + Kj) * r / (rhoi + rhoj));
+        }
         cnt++;
       }
-      double* o = force + 8 * i;
+      double* o = force + 10 * i;
       o[0] = a[0]; o[1] = a[1]; o[2] = a[2]; o[3] = du; o[4] = vsig; o[5] = sa; o[6] = su; o[7] = (double)cnt;
+      o[8] = sc; o[9] = st;
     }
     free(buf);
   }

@@ -1,0 +1,99 @@
+// sph_internal.cuh -- device-side data layout and kernel launch interface of libsph.
+//
+// Layout in HBM: every per-particle array is stored in CELL ORDER (the
+// order produced by the last sph_rebuild_cells), structure-of-arrays with the fields
+// the interaction loops read together packed into 16-byte records:
+//   xh   uint4  (X, Y, Z fixed point, h as f32 bits)        density/gradient/force tiles
+//   vm   float4 (vx, vy, vz, m)                              density/gradient/force tiles
+//   gq   float4 (c_s, u, m/rho, rho)                         gradient tile
+//   fr1  float4 (A = P/rho^2, Kf = f/(pi h^4), c_s, rho)     force tile
+//   fr2  float4 (P, P alpha_c, u, alpha_v)                   force tile
+//   fr3  float2 (B, 1/h)                                     force tile
+// plus plain f32 arrays for state and outputs.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sph {
+
+constexpr int kMaxTileCellsZ = 32;          // z cells per block + 2 halo cells
+constexpr int kMaxTileCells = 9 * kMaxTileCellsZ;
+constexpr float kPi = 3.14159265358979323846f;
+
+// Cell grid and CTA block decomposition.  A CTA owns the cells (ix, iy, z0..z1-1) of
+// one grid column; its tile is the 3x3 neighbour columns over z0-1..z1 (wrapped).
+struct DevGrid {
+  int nx, ny, nz;     // cells per axis (each >= 3)
+  int nzb, KZ;        // z blocks per column, cells per block
+  int nblocks;        // nx * ny * nzb
+  int ncells;
+  int tcap;           // tile capacity (particles) the launch is sized for
+  int lcap;           // per-lane neighbour-list capacity
+  float scale[3];     // L_a / 2^32 as f32 (fixed point -> length)
+  double dscale[3];   // L_a * 2^-32 exact (fp64 exact neighbour test)
+  float side[3];      // cell side per axis
+  float side_min;
+  float eabs;         // 8 x max rounding error of a tile coordinate (length units)
+};
+
+struct DevPhys {
+  float gamma_k, eta3, h_tol, pi_eta3;
+  int h_max_iter, fh_mode;
+  float gamma_eos, beta, alpha_v_max, ell, alpha_c_min, alpha_c_max, beta_c, c_cfl;
+};
+
+struct DevState {
+  uint4* xh;
+  float4* vm;
+  float* u;
+  float* av;
+  float* ac;
+  float* dprev;
+  int64_t* uid;       // caller id
+  int32_t* orig;      // caller index 0..n-1 (for sph_get)
+  // density
+  float4* dens;       // rho, drho_dh, nhat, dn_dh
+  float4* dvc;        // curl x, y, z, div
+  int32_t* count;
+  float4* fin;        // f, P, c, B
+  float4* gq;         // c, u, m/rho, rho
+  float* hlo;
+  float* hhi;
+  int32_t* iters;
+  uint8_t* active;
+  // gradient
+  float2* grad;       // v_sig, lap_u
+  float4* fr1;
+  float4* fr2;
+  float2* fr3;
+  // force
+  float4* acc;        // a, du
+  float* vsig;
+  int32_t* countf;
+};
+
+struct DevCounters {
+  unsigned long long pairs;     // directed neighbour pairs of the loop (density: at the final h)
+  unsigned long long pairs_all; // density: directed pairs evaluated over all h passes
+  int unconverged;
+  int h_exceeds;
+  unsigned int dt_bits;         // min dt as f32 bits (positive)
+  int nonfinite;
+  int active_next;
+  int pad;
+};
+
+// Launchers (sph_kernels.cu).  All enqueue on `st`.
+cudaError_t launch_density(const DevGrid& g, const DevPhys& ph, const DevState& s, const int* cell_start, int pass,
+                           const uint8_t* blk_in, uint8_t* blk_out, DevCounters* ctr, cudaStream_t st);
+cudaError_t launch_gradient(const DevGrid& g, const DevPhys& ph, const DevState& s, const int* cell_start, float dt,
+                            int first_step, DevCounters* ctr, cudaStream_t st);
+cudaError_t launch_force(const DevGrid& g, const DevPhys& ph, const DevState& s, const int* cell_start,
+                         DevCounters* ctr, cudaStream_t st);
+cudaError_t launch_tile_sizes(const DevGrid& g, const int* cell_start, int* max_tile, cudaStream_t st);
+size_t density_smem(const DevGrid& g);
+size_t gradient_smem(const DevGrid& g);
+size_t force_smem(const DevGrid& g);
+int kernel_threads();
+
+}  // namespace sph

@@ -1,0 +1,78 @@
+"""Helpers shared by the GPU parity tests: run the CUDA path and the oracle on the same
+seeded inputs and compare element by element."""
+from __future__ import annotations
+
+import numpy as np
+
+import oracle
+
+# north-star tolerances (BASELINE.json): rho, h, P, accelerations 1e-4 relative (fp32 vs fp64)
+RTOL = 1e-4
+
+
+def gpu_hydro(p, dt_ghost=1e-3, fixed_h=False, h_tol=1e-6, **cfg):
+    """density (+h iteration) -> gradient -> force on the GPU, fields in input order."""
+    from paper_2505_14538_b200 import Context
+
+    if fixed_h:
+        cfg["h_max_iter"] = 0
+    ctx = Context(p, h_tol=h_tol, **cfg)
+    st = ctx.density()
+    ctx.gradient(dt_ghost)
+    dt = ctx.force()
+    out = {k: ctx.get(k) for k in ("h", "rho", "drho_dh", "nhat", "dn_dh", "div", "curl", "count", "f", "P", "c",
+                                   "B", "v_sig_grad", "lap_u", "alpha_v", "alpha_c", "a", "du", "v_sig",
+                                   "count_force", "iters")}
+    out["stats"] = st
+    out["dt"] = dt
+    out["counters"] = ctx.counters()
+    ctx.close()
+    return out
+
+
+def oracle_hydro(p, dt_ghost=1e-3, fixed_h=False, h_tol=1e-13, mode="cells", sample=None, **prm):
+    o = oracle.Oracle(oracle.Params(h_tol=h_tol, h_max_iter=64, **prm), mode=mode)
+    st = oracle.State.from_particles(p)
+    return o.hydro(st, dt_ghost=dt_ghost, first_step=True, fixed_h=fixed_h, sample=sample)
+
+
+def band_mask(p, h, R_factor=2.0, rel=1e-6):
+    """Particles with any pair inside |r_ij - H_i| < rel * h_i (north star exclusion band),
+    computed with the oracle's neighbour enumeration."""
+    st = oracle.State.from_particles(p)
+    g = oracle.Geometry(st.X, st.box, use_cells=True, min_side=R_factor * float(np.max(h)) * 1.01)
+    x = st.X.astype(np.int64)
+    L = st.box
+    bad = np.zeros(len(h), dtype=bool)
+    for i in range(len(h)):
+        H = R_factor * float(h[i])
+        nb = g.neighbours(i, H * (1 + rel))
+        if nb.size == 0:
+            continue
+        d = ((x[nb] - x[i] + 2 ** 31) % 2 ** 32 - 2 ** 31) * (L[None, :] / 2 ** 32)
+        r = np.sqrt((d ** 2).sum(1))
+        if np.any(np.abs(r - H) < rel * h[i]):
+            bad[i] = True
+    return bad
+
+
+def assert_close(name, got, ref, rtol=RTOL, atol_scale=None, mask=None):
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    if mask is not None:
+        got, ref = got[mask], ref[mask]
+        if atol_scale is not None and np.ndim(atol_scale):
+            atol_scale = np.asarray(atol_scale)[mask]
+    tol = rtol * np.abs(ref)
+    if atol_scale is not None:
+        a = np.asarray(atol_scale, dtype=np.float64)
+        if got.ndim == 2 and a.ndim == 1:
+            a = a[:, None]
+        tol = np.maximum(tol, rtol * a)
+    err = np.abs(got - ref)
+    bad = err > tol
+    if bad.any():
+        k = np.argmax(err - tol)
+        kk = np.unravel_index(k, err.shape)
+        raise AssertionError(f"{name}: {bad.sum()} / {bad.size} elements outside tolerance; worst at {kk}: "
+                             f"got {got[kk]!r} ref {ref[kk]!r} tol {tol[kk]!r}")

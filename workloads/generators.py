@@ -82,7 +82,7 @@ def jittered_lattice(n=16, jitter=0.1, seed=1, vel_sigma=0.01, h_factor=1.0, u=1
     x = _lattice_f64(n) + rng.uniform(-jitter, jitter, size=(n ** 3, 3)) * dx
     N = x.shape[0]
     v = rng.normal(0.0, vel_sigma, size=(N, 3)) if vel_sigma > 0 else np.zeros((N, 3))
-    uu = u * (1.0 + u_sigma * rng.standard_normal(N)) if u_sigma > 0 else np.full(N, u)
+    uu = u * np.exp(u_sigma * rng.standard_normal(N)) if u_sigma > 0 else np.full(N, u)
     return _pack(f"jitter{n}", _fixed_point(x, (1, 1, 1)), v, 1.0 / N, uu,
                  h_factor * H_STAR_LATTICE * dx, (1.0, 1.0, 1.0))
 
@@ -92,7 +92,7 @@ def poisson(N=4096, seed=2, vel_sigma=0.05, u=1.5, u_sigma=0.2, h_factor=1.0):
     rng = np.random.default_rng(seed)
     x = rng.uniform(0.0, 1.0, size=(N, 3))
     v = rng.normal(0.0, vel_sigma, size=(N, 3))
-    uu = np.abs(u * (1.0 + u_sigma * rng.standard_normal(N)))
+    uu = u * np.exp(u_sigma * rng.standard_normal(N))
     dx = N ** (-1.0 / 3.0)
     return _pack(f"poisson{N}", _fixed_point(x, (1, 1, 1)), v, 1.0 / N, uu,
                  h_factor * H_STAR_LATTICE * dx, (1.0, 1.0, 1.0))

@@ -13,7 +13,7 @@ DEPS = SOURCES + sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + [
     os.path.join(os.path.dirname(HERE), "include", "sph.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc" if os.path.exists("/usr/local/cuda/bin/nvcc") else "nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-         "-shared"]
+         "-shared", "-ftz=true", "-prec-div=false", "-prec-sqrt=false", "-Xptxas", "-v"]
 
 
 def stale() -> bool:
@@ -29,7 +29,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
         cmd = [NVCC] + FLAGS + ["-o", tmp] + SOURCES
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
-        subprocess.check_call(cmd)
+        out = subprocess.run(cmd, capture_output=True, text=True)
+        if out.returncode != 0:
+            sys.stderr.write(out.stdout + out.stderr)
+            raise subprocess.CalledProcessError(out.returncode, cmd)
+        with open(os.path.join(HERE, "ptxas.log"), "w") as fh:
+            fh.write(out.stderr)
         os.replace(tmp, LIB)
     return LIB
 

@@ -18,8 +18,9 @@ using namespace sph;
 
 namespace {
 
-constexpr int kLcap = 64;             // per-lane neighbour-list capacity (entries)
+constexpr int kLcapInit = 96;         // neighbour-list capacity per particle (entries, multiple of 8)
 constexpr size_t kSmemMax = 227 * 1024;
+constexpr size_t kSmemTarget = 113 * 1024;  // two CTAs per SM for the largest (force) tile
 
 __global__ void k_hmax(int n, const uint4* __restrict__ xh, unsigned int* out) {
   unsigned int m = 0;
@@ -142,6 +143,9 @@ struct sph_ctx {
   int n = 0;
   bool poisoned = false;
   bool stale = true;          // grid must be rebuilt before the next loop
+  bool lists_stale = true;    // neighbour lists must be rebuilt before the next loop
+  size_t nbr_cap = 0;         // allocated list entries (n x lcap)
+  int lcap = kLcapInit;
   bool dprev_valid = false;
   bool density_done = false, gradient_done = false;
   std::string err;
@@ -202,6 +206,9 @@ sph_status alloc_state(sph_ctx* c) {
   CK(dalloc(&s.gq, n)); CK(dalloc(&s.hlo, n)); CK(dalloc(&s.hhi, n)); CK(dalloc(&s.iters, n));
   CK(dalloc(&s.active, n)); CK(dalloc(&s.grad, n)); CK(dalloc(&s.fr1, n)); CK(dalloc(&s.fr2, n));
   CK(dalloc(&s.fr3, n)); CK(dalloc(&s.vsig, n)); CK(dalloc(&s.countf, n));
+  CK(dalloc(&s.ncount, n)); CK(dalloc(&s.hbuild, n));
+  CK(dalloc(&s.nbr, n * (size_t)c->lcap));
+  c->nbr_cap = n * (size_t)c->lcap;
   CK(dalloc(&c->keys, n)); CK(dalloc(&c->keys_alt, n)); CK(dalloc(&c->perm, n)); CK(dalloc(&c->perm_alt, n));
   CK(dalloc(&c->ctr, 1));
   CK(cudaMallocHost((void**)&c->ctr_h, sizeof(DevCounters)));
@@ -393,8 +400,11 @@ sph_status rebuild(sph_ctx* c) {
     CK(cudaMemcpyAsync(c->scratch_h + 1, c->scratch + 1, 4, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     g.tcap = std::max(32, (int)c->scratch_h[1]);
-    g.lcap = kLcap;
-    if (force_smem(g) <= kSmemMax && g.tcap < 65535) break;
+    g.lcap = c->lcap;
+    g.skin = c->cfg.cell_skin;
+    const bool fits = force_smem(g) <= kSmemMax && lists_smem(g) <= kSmemMax && g.tcap < 65535;
+    if (fits && (force_smem(g) <= kSmemTarget || KZ == 1)) break;
+    if (fits && c->cfg.tile_cells_z > 0) break;
     if (KZ == 1) {
       char b[256];
       snprintf(b, sizeof b, "largest cell tile (%d particles) exceeds shared memory; h contrast too high for one grid", g.tcap);
@@ -413,7 +423,39 @@ sph_status rebuild(sph_ctx* c) {
     c->blk_cap = (size_t)g.nblocks;
   }
   c->stale = false;
+  c->lists_stale = true;
   return SPH_OK;
+}
+
+// Build the neighbour lists for the current grid and h (growing the capacity if needed).
+sph_status build_lists(sph_ctx* c) {
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    c->grid.lcap = c->lcap;
+    CK(cudaMemsetAsync(&c->ctr->list_overflow, 0, sizeof(int), c->stream));
+    CK(cudaMemsetAsync(&c->ctr->nonfinite, 0, sizeof(int), c->stream));
+    if (lists_smem(c->grid) > kSmemMax) return fail(c, SPH_ERR_H_EXCEEDS_CELL, "neighbour lists exceed shared memory");
+    CK(launch_lists(c->grid, c->phys, c->s, c->cell_start, c->ctr, c->stream));
+    c->launches++;
+    sph_status st = sync_ctr(c);
+    if (st != SPH_OK) return st;
+    int over = c->ctr_h->list_overflow;
+    if (c->ctr_h->nonfinite == 2) return fail(c, SPH_ERR_CUDA, "internal: tile larger than its capacity");
+    if (over == 0) {
+      c->lists_stale = false;
+      return SPH_OK;
+    }
+    int need = ((int)(over * 1.25) + 7) & ~7;
+    if (need > 8192) return fail(c, SPH_ERR_H_EXCEEDS_CELL, "neighbour list longer than 8192 entries");
+    c->lcap = need;
+    size_t want = (size_t)c->n * c->lcap;
+    if (want > c->nbr_cap) {
+      cudaFree(c->s.nbr);
+      c->s.nbr = nullptr;
+      CK(dalloc(&c->s.nbr, want));
+      c->nbr_cap = want;
+    }
+  }
+  return fail(c, SPH_ERR_CUDA, "internal: neighbour list capacity did not converge");
 }
 
 }  // namespace
@@ -496,6 +538,7 @@ sph_status sph_density(sph_ctx* c, sph_density_stats* stats) {
   GUARD(c);
   sph_status st;
   if (c->stale && (st = rebuild(c)) != SPH_OK) return st;
+  if (c->lists_stale && (st = build_lists(c)) != SPH_OK) return st;
   int rebuilds = 0;
   long long pairs_all = 0;
   int pass = 0, passes_run = 0;
@@ -506,23 +549,28 @@ sph_status sph_density(sph_ctx* c, sph_density_stats* stats) {
     uint8_t* bin = c->blk[pass & 1];
     uint8_t* bout = c->blk[(pass + 1) & 1];
     CK(cudaMemsetAsync(bout, 0, (size_t)c->grid.nblocks, c->stream));
-    CK(cudaMemsetAsync(&c->ctr->active_next, 0, sizeof(int), c->stream));
+    CK(cudaMemsetAsync(&c->ctr->active_next, 0, 3 * sizeof(int), c->stream));  // active_next, list_stale, overflow
     CK(cudaMemsetAsync(&c->ctr->h_exceeds, 0, sizeof(int), c->stream));
     CK(launch_density(c->grid, c->phys, c->s, c->cell_start, pass, bin, bout, c->ctr, c->stream));
     c->launches++;
     ++passes_run;
     if ((st = sync_ctr(c)) != SPH_OK) return st;
     if (c->ctr_h->nonfinite == 2) return fail(c, SPH_ERR_CUDA, "internal: tile larger than its capacity");
-    if (c->ctr_h->active_next > 0 && c->ctr_h->h_exceeds) {
-      // an h grew past the cell side: rebin with the new h and restart the passes
+    if (c->ctr_h->active_next == 0) break;
+    if (c->ctr_h->h_exceeds) {
+      // an h grew past what the cell grid holds: rebin with the new h and restart the passes
       if (++rebuilds > 8) return fail(c, SPH_ERR_H_EXCEEDS_CELL, "h kept outgrowing the cell grid");
       pairs_all += (long long)c->ctr_h->pairs_all;
       if ((st = rebuild(c)) != SPH_OK) return st;
+      if ((st = build_lists(c)) != SPH_OK) return st;
       if ((st = reset_ctr(c)) != SPH_OK) return st;
       pass = 0;
       continue;
     }
-    if (c->ctr_h->active_next == 0) break;
+    if (c->ctr_h->list_stale) {
+      // an h outgrew its list radius: rebuild the lists for the current h, keep iterating
+      if ((st = build_lists(c)) != SPH_OK) return st;
+    }
     ++pass;
   }
   final_pairs = c->ctr_h->pairs;
@@ -684,7 +732,8 @@ sph_status sph_destroy(sph_ctx* c) {
   DevState& s = c->s;
   void* ptrs[] = {s.xh, s.vm, s.u, s.av, s.ac, s.dprev, s.uid, s.orig, s.acc, c->alt.xh, c->alt.vm, c->alt.u,
                   c->alt.av, c->alt.ac, c->alt.dprev, c->alt.uid, c->alt.orig, c->alt.acc, s.dens, s.dvc, s.count,
-                  s.fin, s.gq, s.hlo, s.hhi, s.iters, s.active, s.grad, s.fr1, s.fr2, s.fr3, s.vsig, s.countf,
+                  s.fin, s.gq, s.hlo, s.hhi, s.iters, s.active, s.grad, s.fr1, s.fr2, s.fr3, s.vsig, s.countf, s.nbr,
+                  s.ncount, s.hbuild,
                   c->cell_start, c->keys, c->keys_alt, c->perm, c->perm_alt, c->sort_tmp, c->blk[0], c->blk[1],
                   c->ctr, c->scratch, c->out_tmp};
   for (void* p : ptrs)

@@ -27,8 +27,9 @@ struct DevGrid {
   int nzb, KZ;        // z blocks per column, cells per block
   int nblocks;        // nx * ny * nzb
   int ncells;
-  int tcap;           // tile capacity (particles) the launch is sized for
-  int lcap;           // per-lane neighbour-list capacity
+  int tcap;           // tile capacity (particles) the launch is sized for; slot tcap = sentinel
+  int lcap;           // neighbour-list capacity per particle (multiple of 8)
+  float skin;         // list radius = (1 + skin) max(H_i, H_j)
   float scale[3];     // L_a / 2^32 as f32 (fixed point -> length)
   double dscale[3];   // L_a * 2^-32 exact (fp64 exact neighbour test)
   float side[3];      // cell side per axis
@@ -70,6 +71,10 @@ struct DevState {
   float4* acc;        // a, du
   float* vsig;
   int32_t* countf;
+  // neighbour lists (tile-relative uint16 slots, padded to 8 with the sentinel slot)
+  uint16_t* nbr;      // [n][lcap]
+  int32_t* ncount;    // padded list length
+  float* hbuild;      // h when the list was built
 };
 
 struct DevCounters {
@@ -80,10 +85,14 @@ struct DevCounters {
   unsigned int dt_bits;         // min dt as f32 bits (positive)
   int nonfinite;
   int active_next;
+  int list_stale;               // an h outgrew its list radius
+  int list_overflow;            // max list length seen above lcap (0 = none)
   int pad;
 };
 
 // Launchers (sph_kernels.cu).  All enqueue on `st`.
+cudaError_t launch_lists(const DevGrid& g, const DevPhys& ph, const DevState& s, const int* cell_start,
+                         DevCounters* ctr, cudaStream_t st);
 cudaError_t launch_density(const DevGrid& g, const DevPhys& ph, const DevState& s, const int* cell_start, int pass,
                            const uint8_t* blk_in, uint8_t* blk_out, DevCounters* ctr, cudaStream_t st);
 cudaError_t launch_gradient(const DevGrid& g, const DevPhys& ph, const DevState& s, const int* cell_start, float dt,
@@ -91,6 +100,7 @@ cudaError_t launch_gradient(const DevGrid& g, const DevPhys& ph, const DevState&
 cudaError_t launch_force(const DevGrid& g, const DevPhys& ph, const DevState& s, const int* cell_start,
                          DevCounters* ctr, cudaStream_t st);
 cudaError_t launch_tile_sizes(const DevGrid& g, const int* cell_start, int* max_tile, cudaStream_t st);
+size_t lists_smem(const DevGrid& g);
 size_t density_smem(const DevGrid& g);
 size_t gradient_smem(const DevGrid& g);
 size_t force_smem(const DevGrid& g);

@@ -72,6 +72,8 @@ typedef struct {
   void* stream;           /* cudaStream_t to enqueue on, or NULL                            */
   int32_t rank, nranks;   /* multi-GPU slab decomposition (reserved: nranks must be 1)     */
   int32_t tile_cells_z;   /* cells per CTA block along z (0 = auto)                         */
+  int32_t predict_h;      /* drift also advances h with d ln h/dt = (div v)/3 (continuity),   */
+                          /* a better Newton start; the converged h does not depend on it     */
 } sph_config;
 
 /* Particle input.  n particles; arrays are host pointers (on_device = 0) or device

@@ -46,7 +46,7 @@ class Config(ctypes.Structure):
                 ("alpha_c_min", ctypes.c_float), ("alpha_c_max", ctypes.c_float), ("beta_c", ctypes.c_float),
                 ("c_cfl", ctypes.c_float), ("fh_mode", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("stream", ctypes.c_void_p), ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
-                ("tile_cells_z", ctypes.c_int32)]
+                ("tile_cells_z", ctypes.c_int32), ("predict_h", ctypes.c_int32)]
 
 
 class ParticlesIn(ctypes.Structure):

@@ -20,7 +20,7 @@ namespace {
 
 constexpr int kLcapInit = 96;         // neighbour-list capacity per particle (entries, multiple of 8)
 constexpr size_t kSmemMax = 227 * 1024;
-constexpr size_t kSmemTarget = 113 * 1024;  // two CTAs per SM for the largest (force) tile
+constexpr size_t kSmemTarget = 106 * 1024;  // two CTAs per SM for the largest (force) tile (+ static smem)
 
 __global__ void k_hmax(int n, const uint4* __restrict__ xh, unsigned int* out) {
   unsigned int m = 0;
@@ -98,9 +98,14 @@ __global__ void k_ingest(int n, const uint32_t* __restrict__ X, const float* __r
 // Kick v += a dt_k, u = max(0, u + du dt_k); drift x += v dt_d on the 2^-32 L
 // grid, rounded to nearest, wrapping mod 2^32 (R25).
 __global__ void k_kick_drift(int n, uint4* xh, float4* vm, float* u, const float4* __restrict__ acc, float dtk,
-                             float dtd, double fx, double fy, double fz) {
+                             float dtd, double fx, double fy, double fz, const float4* __restrict__ dvc) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  if (dvc && dtd != 0.f) {
+    // h prediction in the drift: d ln h/dt = -(1/3) d ln rho/dt = (div v)/3 (continuity)
+    float h = __uint_as_float(xh[i].w) * __expf(dtd * dvc[i].w * (1.f / 3.f));
+    reinterpret_cast<unsigned int*>(&xh[i])[3] = __float_as_uint(h);
+  }
   float4 a = acc[i];
   float4 v = vm[i];
   v.x = fmaf(a.x, dtk, v.x);
@@ -147,6 +152,7 @@ struct sph_ctx {
   size_t nbr_cap = 0;         // allocated list entries (n x lcap)
   int lcap = kLcapInit;
   bool dprev_valid = false;
+  bool dvc_valid = false;     // dvc (div v) is from a density pass in the current particle order
   bool density_done = false, gradient_done = false;
   std::string err;
   DevGrid grid{};
@@ -305,6 +311,7 @@ sph_status ingest(sph_ctx* c, const sph_particles_in* in) {
   c->launches++;
   CK(cudaGetLastError());
   c->dprev_valid = dp != nullptr;
+  c->dvc_valid = false;
   c->stale = true;
   c->density_done = c->gradient_done = false;
   return SPH_OK;
@@ -384,16 +391,21 @@ sph_status rebuild(sph_ctx* c) {
   Persist old = persist_of(c->s);
   set_persist(c->s, c->alt);
   c->alt = old;
-  // CTA blocks: KZ cells per block along z, ~kernel_threads() particles per block
+  // CTA blocks: BX x BY grid columns x KZ cells (BX, BY = 2 when the grid allows: the tile of
+  // (BX+2)(BY+2) columns is then ~2x smaller per owned particle than with single columns)
+  g.bx = g.nx >= 6 ? 2 : 1;
+  g.by = g.ny >= 6 ? 2 : 1;
+  g.nbx = (g.nx + g.bx - 1) / g.bx;
+  g.nby = (g.ny + g.by - 1) / g.by;
   const double occ = (double)n / g.ncells;
-  int kz_max = std::min(kMaxTileCellsZ - 2, g.nz > 3 ? g.nz - 3 : 1);
-  int KZ = (int)std::lround(kernel_threads() / std::max(occ, 1e-3));
+  const int kz_max = std::min(kMaxTileCellsZ - 2, g.nz > 3 ? g.nz - 3 : 1);
+  int KZ = (int)std::lround(kernel_threads() / std::max(occ * g.bx * g.by, 1e-3));
   if (c->cfg.tile_cells_z > 0) KZ = c->cfg.tile_cells_z;
   KZ = std::max(1, std::min(KZ, kz_max));
   for (;;) {
     g.KZ = KZ;
     g.nzb = (g.nz + KZ - 1) / KZ;
-    g.nblocks = g.nx * g.ny * g.nzb;
+    g.nblocks = g.nbx * g.nby * g.nzb;
     CK(cudaMemsetAsync(c->scratch + 1, 0, 4, c->stream));
     CK(launch_tile_sizes(g, c->cell_start, (int*)(c->scratch + 1), c->stream));
     c->launches++;
@@ -410,10 +422,12 @@ sph_status rebuild(sph_ctx* c) {
       snprintf(b, sizeof b, "largest cell tile (%d particles) exceeds shared memory; h contrast too high for one grid", g.tcap);
       return fail(c, SPH_ERR_H_EXCEEDS_CELL, b);
     }
-    KZ = std::max(1, KZ / 2);
+    KZ = std::max(1, KZ - 1);
   }
-  const float max_off = std::max(1.5f * std::max(g.side[0], g.side[1]), (0.5f * g.KZ + 1.0f) * g.side[2]);
-  g.eabs = 4.0f * ulp_of(max_off) * 2.0f;  // 8 x (ulp/2): coordinate rounding, with margin
+  // rounding error of a tile coordinate: offsets reach (B/2 + 1) cells from the block centre
+  const float max_off = std::max(std::max((0.5f * g.bx + 1.0f) * g.side[0], (0.5f * g.by + 1.0f) * g.side[1]),
+                                 (0.5f * g.KZ + 1.0f) * g.side[2]);
+  g.eabs = 4.0f * ulp_of(max_off) * 2.0f;  // 8 x (ulp/2): two coordinates per difference, with margin
   if ((size_t)g.nblocks > c->blk_cap) {
     for (int k = 0; k < 2; ++k) {
       if (c->blk[k]) cudaFree(c->blk[k]);
@@ -424,6 +438,7 @@ sph_status rebuild(sph_ctx* c) {
   }
   c->stale = false;
   c->lists_stale = true;
+  c->dvc_valid = false;
   return SPH_OK;
 }
 
@@ -488,6 +503,7 @@ void sph_config_default(sph_config* cfg) {
   cfg->rank = 0;
   cfg->nranks = 1;
   cfg->tile_cells_z = 0;
+  cfg->predict_h = 1;
 }
 
 sph_status sph_create(const sph_config* cfg, const sph_particles_in* in, sph_ctx** out) {
@@ -551,7 +567,8 @@ sph_status sph_density(sph_ctx* c, sph_density_stats* stats) {
     CK(cudaMemsetAsync(bout, 0, (size_t)c->grid.nblocks, c->stream));
     CK(cudaMemsetAsync(&c->ctr->active_next, 0, 3 * sizeof(int), c->stream));  // active_next, list_stale, overflow
     CK(cudaMemsetAsync(&c->ctr->h_exceeds, 0, sizeof(int), c->stream));
-    CK(launch_density(c->grid, c->phys, c->s, c->cell_start, pass, bin, bout, c->ctr, c->stream));
+    CK(launch_density(c->grid, c->phys, c->s, c->cell_start, pass, bin, bout, 1.f + c->cfg.cell_skin, c->ctr,
+                      c->stream));
     c->launches++;
     ++passes_run;
     if ((st = sync_ctr(c)) != SPH_OK) return st;
@@ -580,6 +597,7 @@ sph_status sph_density(sph_ctx* c, sph_density_stats* stats) {
   c->counters.pairs_h_iter = pairs_all;
   c->density_done = true;
   c->gradient_done = false;
+  c->dvc_valid = true;
   if (stats) {
     stats->iterations = passes_run;
     stats->unconverged = unconverged;
@@ -636,8 +654,9 @@ sph_status sph_kick_drift(sph_ctx* c, float dt_kick, float dt_drift) {
   if (!std::isfinite(dt_kick) || !std::isfinite(dt_drift)) return fail(c, SPH_ERR_INVALID_ARG, "non-finite dt");
   const double f[3] = {std::ldexp(1.0, 32) / c->cfg.box[0], std::ldexp(1.0, 32) / c->cfg.box[1],
                        std::ldexp(1.0, 32) / c->cfg.box[2]};
+  const float4* dvc = (c->cfg.predict_h && c->dvc_valid) ? c->s.dvc : nullptr;
   k_kick_drift<<<nblk(c->n, 256), 256, 0, c->stream>>>(c->n, c->s.xh, c->s.vm, c->s.u, c->s.acc, dt_kick, dt_drift, f[0],
-                                                     f[1], f[2]);
+                                                     f[1], f[2], dvc);
   c->launches++;
   CK(cudaGetLastError());
   if (dt_drift != 0.f) c->stale = true;

@@ -5,10 +5,10 @@
 // the interaction loops read together packed into 16-byte records:
 //   xh   uint4  (X, Y, Z fixed point, h as f32 bits)        density/gradient/force tiles
 //   vm   float4 (vx, vy, vz, m)                              density/gradient/force tiles
-//   gq   float4 (c_s, u, m/rho, rho)                         gradient tile
+//   gq   float4 (c_s, u, m/rho, rho)                         gradient tile (+ xh, vm)
 //   fr1  float4 (A = P/rho^2, Kf = f/(pi h^4), c_s, rho)     force tile
 //   fr2  float4 (P, P alpha_c, u, alpha_v)                   force tile
-//   fr3  float2 (B, 1/h)                                     force tile
+//   fr3  float  B                                            force tile
 // plus plain f32 arrays for state and outputs.
 #pragma once
 #include <cuda_runtime.h>
@@ -17,15 +17,17 @@
 namespace sph {
 
 constexpr int kMaxTileCellsZ = 32;          // z cells per block + 2 halo cells
-constexpr int kMaxTileCells = 9 * kMaxTileCellsZ;
+constexpr int kMaxTileCells = 16 * kMaxTileCellsZ;  // (BX+2)(BY+2) <= 16 tile columns
 constexpr float kPi = 3.14159265358979323846f;
 
-// Cell grid and CTA block decomposition.  A CTA owns the cells (ix, iy, z0..z1-1) of
-// one grid column; its tile is the 3x3 neighbour columns over z0-1..z1 (wrapped).
+// Cell grid and CTA block decomposition.  A CTA owns the cells of BX x BY grid columns
+// over z0..z1-1; its tile is the (BX+2) x (BY+2) neighbour columns over z0-1..z1 (wrapped).
 struct DevGrid {
   int nx, ny, nz;     // cells per axis (each >= 3)
+  int bx, by;         // grid columns per block along x, y (1 or 2)
+  int nbx, nby;       // blocks along x, y
   int nzb, KZ;        // z blocks per column, cells per block
-  int nblocks;        // nx * ny * nzb
+  int nblocks;        // nbx * nby * nzb
   int ncells;
   int tcap;           // tile capacity (particles) the launch is sized for; slot tcap = sentinel
   int lcap;           // neighbour-list capacity per particle (multiple of 8)
@@ -66,7 +68,7 @@ struct DevState {
   float2* grad;       // v_sig, lap_u
   float4* fr1;
   float4* fr2;
-  float2* fr3;
+  float* fr3;         // B (Balsara switch)
   // force
   float4* acc;        // a, du
   float* vsig;
@@ -94,7 +96,8 @@ struct DevCounters {
 cudaError_t launch_lists(const DevGrid& g, const DevPhys& ph, const DevState& s, const int* cell_start,
                          DevCounters* ctr, cudaStream_t st);
 cudaError_t launch_density(const DevGrid& g, const DevPhys& ph, const DevState& s, const int* cell_start, int pass,
-                           const uint8_t* blk_in, uint8_t* blk_out, DevCounters* ctr, cudaStream_t st);
+                           const uint8_t* blk_in, uint8_t* blk_out, float hfac_stale, DevCounters* ctr,
+                           cudaStream_t st);
 cudaError_t launch_gradient(const DevGrid& g, const DevPhys& ph, const DevState& s, const int* cell_start, float dt,
                             int first_step, DevCounters* ctr, cudaStream_t st);
 cudaError_t launch_force(const DevGrid& g, const DevPhys& ph, const DevState& s, const int* cell_start,

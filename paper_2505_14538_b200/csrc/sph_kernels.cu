@@ -2,21 +2,22 @@
 // (density + h iteration, gradient + ghost, force + CFL dt).
 //
 // Decomposition.  The cell grid (side >= (1+skin) max support radius H = gamma_k h) is
-// cut into CTA blocks of KZ cells of one grid column.  A block's TILE is the particles of
-// the 3x3 neighbour columns over its z range +-1 cell: 9 contiguous ranges of the
-// cell-sorted arrays, staged into shared memory with positions converted from fixed point
-// to f32 offsets from the block centre.
+// cut into CTA blocks of BX x BY grid columns x KZ cells.  A block's TILE is the
+// particles of the (BX+2) x (BY+2) neighbour columns over its z range +-1 cell: at most
+// 3 contiguous ranges of the cell-sorted arrays per column, staged into shared memory with
+// cp.async (LDGSTS) and converted from fixed point to f32 offsets from the block centre.
 //
 // Neighbour lists.  k_lists tests, once per cell rebuild (and again only if an h outgrows
 // its list radius), every candidate of the union of the 27-cell stencils of a warp's 32
 // particles (warp-uniform, broadcast shared-memory reads) and stores, per particle, the
-// tile slots j with r_ij < (1 + skin) max(H_i, H_j) as uint16, padded to a multiple of 8
-// with a sentinel slot.  The density passes, the gradient loop and the force loop then run
-// the pair arithmetic over these lists only: every lane works on a real (or skin)
-// neighbour, no candidate is re-tested (the paper's pair tasks test all particle pairs of
-// two cells).  Skin entries and the sentinel contribute exactly zero (compact
-// support); membership (neighbour counts, v_sig) is decided in f32 with a rigorous band
-// and re-decided in fp64 inside it, so counts equal the definition exactly.
+// tile slots j with r_ij < (1 + skin) max(H_i, H_j) (self included) as uint16, padded to a
+// multiple of 8 with a sentinel slot.  The density passes, the gradient loop and the force
+// loop then run the pair arithmetic over these lists only: every lane works on a real (or
+// skin) neighbour, no candidate is re-tested (the paper's pair tasks test all particle
+// pairs of two cells).  Skin entries, the sentinel and the self pair contribute
+// exactly zero (compact support, w'(0) = 0); membership (neighbour counts, v_sig) is decided
+// in f32 with a rigorous band and re-decided in fp64 inside it, so counts equal the
+// definition exactly.
 #include <cuda_runtime.h>
 #include <math_constants.h>
 #include <stdint.h>
@@ -25,78 +26,168 @@
 
 namespace sph {
 
+extern __shared__ float4 smem4[];  // dynamic shared memory of every loop kernel
+
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kNW = 4;              // warps per CTA
+constexpr int kNW = 8;              // warps per CTA
 constexpr float kFar = 1.0e12f;     // sentinel position (tile coordinates)
+constexpr int kMaxICols = 4;        // BX * BY <= 4
+constexpr int kMaxSeg = 3 * 16;     // <= 3 contiguous segments per tile column
 
 struct Tile {
-  int ix, iy, z0, z1, nzt, nct, ntile, ib, ie, g0;
+  int ix0, iy0, z0, z1, nzt, ntc, nct, ntile, ncol, ni;
   uint32_t ref[3];
 };
 
-// Block geometry + tile cell table.  s_gst[c] = first global particle of tile cell c,
-// s_off[c] = its offset in the tile; c = col * nzt + zz, col = (dx+1)*3 + (dy+1),
+// Shared block bookkeeping (static shared memory of every loop kernel).
+struct BlockShared {
+  int off[kMaxTileCells + 1];  // tile offset of each tile cell (exclusive prefix)
+  int gst[kMaxTileCells];      // global index of the first particle of each tile cell
+  int4 seg[kMaxSeg];           // contiguous segments (tile start, global start, length)
+  int ib[kMaxICols];           // tile start of each i column of the block
+  int g0[kMaxICols];           // global start of each i column
+  int tc[kMaxICols];           // tile column of each i column
+  int pre[kMaxICols + 1];      // prefix of i counts over the i columns
+};
+
+// Block geometry + tile cell table + i columns + segments.  Tile cell c = tc * nzt + zz,
+// tile column tc = (dx+1) * (BY+2) + (dy+1) for dx in [-1, BX], dy in [-1, BY],
 // zz = z - z0 + 1.  Ends with __syncthreads().
-__device__ void tile_setup(const DevGrid& g, int b, const int* __restrict__ cell_start, int* s_off, int* s_gst,
-                           Tile& T) {
-  int zb = b % g.nzb;
-  int col = b / g.nzb;
-  T.iy = col % g.ny;
-  T.ix = col / g.ny;
+__device__ void tile_setup(const DevGrid& g, int b, const int* __restrict__ cell_start, BlockShared& S, Tile& T) {
+  const int zb = b % g.nzb;
+  const int t2 = b / g.nzb;
+  const int jy = t2 % g.nby, jx = t2 / g.nby;
+  T.ix0 = jx * g.bx;
+  T.iy0 = jy * g.by;
   T.z0 = zb * g.KZ;
   T.z1 = min(g.nz, T.z0 + g.KZ);
   T.nzt = T.z1 - T.z0 + 2;
-  T.nct = 9 * T.nzt;
-  T.ref[0] = (uint32_t)((((unsigned long long)(2 * T.ix + 1)) << 31) / (unsigned long long)g.nx);
-  T.ref[1] = (uint32_t)((((unsigned long long)(2 * T.iy + 1)) << 31) / (unsigned long long)g.ny);
+  T.ntc = (g.bx + 2) * (g.by + 2);
+  T.nct = T.ntc * T.nzt;
+  T.ref[0] = (uint32_t)((((unsigned long long)(2 * T.ix0 + g.bx)) << 31) / (unsigned long long)g.nx);
+  T.ref[1] = (uint32_t)((((unsigned long long)(2 * T.iy0 + g.by)) << 31) / (unsigned long long)g.ny);
   T.ref[2] = (uint32_t)((((unsigned long long)(T.z0 + T.z1)) << 31) / (unsigned long long)g.nz);
   for (int t = threadIdx.x; t < T.nct; t += blockDim.x) {
-    int c = t / T.nzt, zz = t - c * T.nzt;
-    int cx = T.ix + c / 3 - 1, cy = T.iy + c % 3 - 1, cz = T.z0 - 1 + zz;
+    const int c = t / T.nzt, zz = t - c * T.nzt;
+    int cx = T.ix0 + c / (g.by + 2) - 1, cy = T.iy0 + c % (g.by + 2) - 1, cz = T.z0 - 1 + zz;
     cx += (cx < 0) ? g.nx : 0;
     cx -= (cx >= g.nx) ? g.nx : 0;
     cy += (cy < 0) ? g.ny : 0;
     cy -= (cy >= g.ny) ? g.ny : 0;
     cz += (cz < 0) ? g.nz : 0;
     cz -= (cz >= g.nz) ? g.nz : 0;
-    int cell = (cx * g.ny + cy) * g.nz + cz;
-    int gs = __ldg(cell_start + cell);
-    s_gst[t] = gs;
-    s_off[t + 1] = __ldg(cell_start + cell + 1) - gs;
+    const int cell = (cx * g.ny + cy) * g.nz + cz;
+    const int gs = __ldg(cell_start + cell);
+    S.gst[t] = gs;
+    S.off[t + 1] = __ldg(cell_start + cell + 1) - gs;
   }
   __syncthreads();
   if (threadIdx.x < 32) {
-    int lane = threadIdx.x, carry = 0;
+    const int lane = threadIdx.x;
+    int carry = 0;
     for (int base = 0; base < T.nct; base += 32) {
-      int t = base + lane;
-      int v = t < T.nct ? s_off[t + 1] : 0;
+      const int t = base + lane;
+      int v = t < T.nct ? S.off[t + 1] : 0;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(kFull, v, o);
+        const int y = __shfl_up_sync(kFull, v, o);
         if (lane >= o) v += y;
       }
-      if (t < T.nct) s_off[t + 1] = carry + v;
+      if (t < T.nct) S.off[t + 1] = carry + v;
       carry += __shfl_sync(kFull, v, 31);
     }
-    if (lane == 0) s_off[0] = 0;
+    if (lane == 0) S.off[0] = 0;
   }
   __syncthreads();
-  T.ntile = s_off[T.nct];
-  T.ib = s_off[4 * T.nzt + 1];
-  T.ie = s_off[4 * T.nzt + T.nzt - 1];
-  T.g0 = s_gst[4 * T.nzt + 1];  // the block's own cells are consecutive in the cell order
+  // i columns of the block (edge blocks may own fewer than BX x BY columns)
+  if (threadIdx.x == 0) {
+    int k = 0, acc = 0;
+    for (int ex = 0; ex < g.bx; ++ex)
+      for (int ey = 0; ey < g.by; ++ey) {
+        if (T.ix0 + ex >= g.nx || T.iy0 + ey >= g.ny) continue;
+        const int tc = (ex + 1) * (g.by + 2) + (ey + 1);
+        S.tc[k] = tc;
+        S.ib[k] = S.off[tc * T.nzt + 1];
+        S.g0[k] = S.gst[tc * T.nzt + 1];  // an i column's cells are consecutive in the cell order
+        S.pre[k] = acc;
+        acc += S.off[tc * T.nzt + T.nzt - 1] - S.off[tc * T.nzt + 1];
+        ++k;
+      }
+    S.pre[k] = acc;
+    for (int r = k; r < kMaxICols; ++r) { S.tc[r] = 0; S.ib[r] = 0; S.g0[r] = 0; S.pre[r + 1] = acc; }
+  }
+  // contiguous segments: one thread per tile column
+  if (threadIdx.x >= 32 && threadIdx.x < 32 + T.ntc) {
+    const int col = threadIdx.x - 32;
+    int n = 0;
+    int4 cur = make_int4(0, 0, 0, 0);
+    for (int zz = 0; zz < T.nzt; ++zz) {
+      const int c = col * T.nzt + zz;
+      const int len = S.off[c + 1] - S.off[c];
+      if (zz > 0 && cur.y + cur.z == S.gst[c]) {
+        cur.z += len;
+      } else {
+        if (zz > 0) S.seg[col * 3 + n++] = cur;
+        cur = make_int4(S.off[c], S.gst[c], len, 0);
+      }
+    }
+    S.seg[col * 3 + n++] = cur;
+    for (; n < 3; ++n) S.seg[col * 3 + n] = make_int4(0, 0, 0, 0);
+  }
+  __syncthreads();
+  T.ntile = S.off[T.nct];
+  int k = 0;
+  while (k < kMaxICols && S.pre[k + 1] > S.pre[k]) ++k;
+  T.ncol = k;
+  T.ni = S.pre[kMaxICols];
 }
 
-// tile slot -> global particle index (binary search over the cell table)
-__device__ __forceinline__ int slot_global(const int* s_off, const int* s_gst, int nct, int t) {
+// block-local i index -> (tile slot, global index)
+__device__ __forceinline__ void i_slot(const BlockShared& S, int li, int& ti, int& gi) {
+  int k = 0;
+#pragma unroll
+  for (int r = 1; r < kMaxICols; ++r) k += (li >= S.pre[r]) ? 1 : 0;
+  ti = S.ib[k] + (li - S.pre[k]);
+  gi = S.g0[k] + (li - S.pre[k]);
+}
+
+// tile slot -> global particle index (binary search over the cell table; rare path)
+__device__ __forceinline__ int slot_global(const BlockShared& S, int nct, int t) {
   int lo = 0, hi = nct;
   while (hi - lo > 1) {
-    int mid = (lo + hi) >> 1;
-    if (s_off[mid] <= t) lo = mid; else hi = mid;
+    const int mid = (lo + hi) >> 1;
+    if (S.off[mid] <= t) lo = mid; else hi = mid;
   }
-  return s_gst[lo] + (t - s_off[lo]);
+  return S.gst[lo] + (t - S.off[lo]);
+}
+
+__device__ __forceinline__ void cp_async16(const void* smem_dst, const void* gmem_src) {
+  const unsigned int d = (unsigned int)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(const void* smem_dst, const void* gmem_src) {
+  const unsigned int d = (unsigned int)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// Stage nrec16 16-byte per-particle records (at smem4[o16[r] + slot]) and optionally one
+// 4-byte record (at float offset o4) of every tile slot with cp.async: no register round
+// trip, every copy of the CTA in flight at once.
+__device__ __forceinline__ void stage_records(const BlockShared& S, int nseg, int nrec16, const float4* const* src16,
+                                              const int* o16, const float* src4, int o4) {
+  float* sm1 = reinterpret_cast<float*>(smem4);
+  for (int k = 0; k < nseg; ++k) {
+    const int4 sg = S.seg[k];
+    for (int t = threadIdx.x; t < sg.z; t += blockDim.x) {
+      for (int r = 0; r < nrec16; ++r) cp_async16(&smem4[o16[r] + sg.x + t], src16[r] + sg.y + t);
+      if (src4) cp_async4(&sm1[o4 + sg.x + t], src4 + sg.y + t);
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
 }
 
 __device__ __forceinline__ float3 rel_pos(const DevGrid& g, const Tile& T, uint4 x) {
@@ -117,37 +208,45 @@ __device__ __forceinline__ int warp_max(int v) {
 
 // M4 cubic spline: w(q), dw/dq; exactly zero for q >= 2 (compact support).
 __device__ __forceinline__ void m4(float q, float& w, float& dw) {
-  float q2 = q * q;
-  float w_in = fmaf(q2, fmaf(0.75f, q, -1.5f), 1.f);
-  float dw_in = q * fmaf(2.25f, q, -3.f);
-  float t = fmaxf(2.f - q, 0.f);
-  float t2 = t * t;
-  bool inner = q < 1.f;
+  const float q2 = q * q;
+  const float w_in = fmaf(q2, fmaf(0.75f, q, -1.5f), 1.f);
+  const float dw_in = q * fmaf(2.25f, q, -3.f);
+  const float t = fmaxf(2.f - q, 0.f);
+  const float t2 = t * t;
+  const bool inner = q < 1.f;
   w = inner ? w_in : 0.25f * t2 * t;
   dw = inner ? dw_in : -0.75f * t2;
 }
 __device__ __forceinline__ float m4_dw(float q) {
-  float dw_in = q * fmaf(2.25f, q, -3.f);
-  float t = fmaxf(2.f - q, 0.f);
+  const float dw_in = q * fmaf(2.25f, q, -3.f);
+  const float t = fmaxf(2.f - q, 0.f);
   return q < 1.f ? dw_in : -0.75f * t * t;
 }
 
 // fp64 fixed-point neighbour test, operation for operation the oracle's (oracle.c sep2):
 // r^2 = (dx*dx + dy*dy) + dz*dz < H2 with dx = (double)(int32)(X_i - X_j) * (L * 2^-32).
-__device__ __noinline__ bool exact_neighbour(const uint4* __restrict__ xh, int gi, int gj, double H2, double sx,
-                                             double sy, double sz) {
-  uint4 a = xh[gi], b = xh[gj];
-  double dx = __dmul_rn((double)(int)(a.x - b.x), sx);
-  double dy = __dmul_rn((double)(int)(a.y - b.y), sy);
-  double dz = __dmul_rn((double)(int)(a.z - b.z), sz);
-  double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+// Only reached for pairs within the f32 error band of the support radius (rare).
+__device__ __forceinline__ bool exact_neighbour(const uint4* __restrict__ xh, int gi, int gj, double H2, double sx,
+                                                double sy, double sz) {
+  const uint4 a = xh[gi], b = xh[gj];
+  const double dx = __dmul_rn((double)(int)(a.x - b.x), sx);
+  const double dy = __dmul_rn((double)(int)(a.y - b.y), sy);
+  const double dz = __dmul_rn((double)(int)(a.z - b.z), sz);
+  const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
   return r2 < H2 && r2 > 0.0;
 }
 
 __device__ __forceinline__ double h2_exact(float h, float gamma_k) {
-  double H = __dmul_rn((double)gamma_k, (double)h);
+  const double H = __dmul_rn((double)gamma_k, (double)h);
   return __dmul_rn(H, H);
 }
+
+// 1 if d < 0 (sign bit), i.e. q < 2 for d = q - 2
+__device__ __forceinline__ int neg(float d) { return (int)(__float_as_uint(d) >> 31); }
+
+// r^-1 with the self pair (r = 0, listed) mapped to a finite value: every pair term of the
+// self pair then carries w'(0) = 0 or v_ij = 0 and vanishes exactly.
+__device__ __forceinline__ float rinv_safe(float r2) { return rsqrtf(fmaxf(r2, 1e-30f)); }
 
 // Iterate a particle's padded neighbour list in groups of 8 (one 16-byte load each).
 template <class PairF>
@@ -168,77 +267,183 @@ __device__ __forceinline__ void for_list(const uint16_t* __restrict__ list, int 
   }
 }
 
+#define TILE_PROLOGUE()                                   \
+  __shared__ BlockShared S;                               \
+  Tile T;                                                 \
+  tile_setup(g, blockIdx.x, cell_start, S, T);            \
+  if (T.ntile > g.tcap) {                                 \
+    if (threadIdx.x == 0) atomicExch(&ctr->nonfinite, 2); \
+    return;                                               \
+  }                                                       \
+  const int nseg = 3 * T.ntc;                             \
+  const int SP = g.tcap + 1; /* slots per record array (last = sentinel) */
+
 // ========================================================== neighbour lists ==========
-// For every particle i of the block: all tile slots j != i with
+// For every particle i of the block: all tile slots j (self included) with
 // r_ij^2 < ((1 + skin) gamma_k max(h_i, h_j))^2, in tile order, padded to 8 with the
 // sentinel slot tcap.  Superset of every loop's neighbour set while each h stays within
 // (1 + skin) of its value here (checked by the density epilogue).
-__global__ void __launch_bounds__(kNW * 32) k_lists(DevGrid g, DevPhys ph, DevState s,
-                                                    const int* __restrict__ cell_start,
-                                                    DevCounters* __restrict__ ctr) {
-  __shared__ int s_off[kMaxTileCells + 1];
-  __shared__ int s_gst[kMaxTileCells];
-  extern __shared__ float4 smem4[];
-  float4* T0 = smem4;  // x, y, z, ((1+skin) H)^2
-  uint16_t* L = reinterpret_cast<uint16_t*>(smem4 + g.tcap + 1);
-  Tile T;
-  tile_setup(g, blockIdx.x, cell_start, s_off, s_gst, T);
-  if (T.ntile > g.tcap) {
-    if (threadIdx.x == 0) atomicExch(&ctr->nonfinite, 2);
-    return;
+// Warps take chunks of 32 particles in cell-major order over the block (z level, then i
+// column), so a chunk spans ~2 cells of one z level; its candidates are the union of the
+// 3 x 3 column neighbourhoods of its i columns over its z cells +-1.  The tile is staged as
+// SoA (x[], y[], z[], H2[]) so one LDS.64 per coordinate brings two consecutive candidates
+// and the distance test runs in packed f32x2 (FADD2 / FMUL2 / FFMA2, the particle's
+// coordinate as a broadcast operand).  Hits are appended to a 16-row per-lane buffer in
+// shared memory and leave for global memory 8 at a time (16-byte stores).
+constexpr int kMaxICells = kMaxICols * (kMaxTileCellsZ - 2);
+__global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, DevState s,
+                                                       const int* __restrict__ cell_start,
+                                                       DevCounters* __restrict__ ctr) {
+  __shared__ int s_cp[kMaxICells + 1];  // prefix of particle counts over the block's i cells
+  __shared__ int s_ct[kMaxICells];      // tile start of each i cell
+  __shared__ int s_cg[kMaxICells];      // global start of each i cell
+  __shared__ unsigned s_nbm[kMaxICols]; // tile columns of the 3 x 3 neighbourhood of each i column
+  TILE_PROLOGUE();
+  {
+    const float4* src[1] = {reinterpret_cast<const float4*>(s.xh)};
+    const int o16[1] = {0};
+    stage_records(S, nseg, 1, src, o16, nullptr, 0);
   }
+  // AoS raw records -> pair-interleaved SoA in place: for the slot pair (2p, 2p+1),
+  // P[8p .. 8p+7] = (x_2p, x_2p+1, y_2p, y_2p+1, z_2p, z_2p+1, H2_2p, H2_2p+1) occupies the same
+  // 32 bytes as the two raw records, so one thread converts one pair; two LDS.128 then bring
+  // two candidates laid out for f32x2 arithmetic.  The pad slot past the tile end never hits.
+  const int NP = (SP + 1) >> 1;  // slot pairs
+  float* P = reinterpret_cast<float*>(smem4);
   const float Hfac = (1.f + g.skin) * ph.gamma_k;
-  for (int t = threadIdx.x; t < T.ntile; t += blockDim.x) {
-    uint4 x = __ldg(&s.xh[slot_global(s_off, s_gst, T.nct, t)]);
-    float3 p = rel_pos(g, T, x);
-    float Hs = Hfac * __uint_as_float(x.w);
-    T0[t] = make_float4(p.x, p.y, p.z, Hs * Hs);
+  for (int pp = threadIdx.x; pp < NP; pp += blockDim.x) {
+    float4 q[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int t = 2 * pp + u;
+      q[u] = make_float4(kFar, kFar, kFar, 0.f);
+      if (t < T.ntile) {
+        const uint4 x = reinterpret_cast<const uint4*>(smem4)[t];
+        const float3 r = rel_pos(g, T, x);
+        const float Hs = Hfac * __uint_as_float(x.w);
+        q[u] = make_float4(r.x, r.y, r.z, Hs * Hs);
+      }
+    }
+    reinterpret_cast<float4*>(P)[2 * pp] = make_float4(q[0].x, q[1].x, q[0].y, q[1].y);
+    reinterpret_cast<float4*>(P)[2 * pp + 1] = make_float4(q[0].z, q[1].z, q[0].w, q[1].w);
+  }
+  int ncolI = 0;
+#pragma unroll
+  for (int r = 0; r < kMaxICols; ++r) ncolI += (r == 0 || S.tc[r] != 0) ? 1 : 0;
+  const int nicell = (T.nzt - 2) * ncolI;
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int e = 0; e < nicell; ++e) {
+      const int zz = e / ncolI + 1, k = e - (zz - 1) * ncolI;
+      const int c = S.tc[k] * T.nzt + zz;
+      s_cp[e] = acc;
+      s_ct[e] = S.off[c];
+      s_cg[e] = S.gst[c];
+      acc += S.off[c + 1] - S.off[c];
+    }
+    s_cp[nicell] = acc;
+  }
+  if (threadIdx.x < kMaxICols) {
+    const int tc = S.tc[threadIdx.x];
+    unsigned m = 0;
+    for (int dx = -1; dx <= 1; ++dx)
+      for (int dy = -1; dy <= 1; ++dy) m |= 1u << (tc + dx * (g.by + 2) + dy);
+    s_nbm[threadIdx.x] = threadIdx.x < ncolI ? m : 0u;
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int ni = T.ie - T.ib;
-  uint16_t* lst = L + warp * g.lcap * 32 + lane;
+  // 24-row x 32-lane uint16 buffer per warp after the pair array (row stride 64 bytes)
+  uint16_t* buf = reinterpret_cast<uint16_t*>(P + NP * 8) + warp * 24 * 32 + lane;
+  const int ni = s_cp[nicell];
   int over = 0;
   for (int c = warp; c * 32 < ni; c += kNW) {
     const int k = c * 32 + lane;
     const bool valid = k < ni;
-    const int ti = T.ib + (valid ? k : c * 32);
-    const int* o = s_off + 4 * T.nzt;
-    int zz = 1;
-    while (zz < T.nzt - 2 && o[zz + 1] <= ti) ++zz;
+    const int kk = valid ? k : c * 32;
+    int lo = 0, hi = nicell;  // s_cp[lo] <= kk < s_cp[hi]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (s_cp[mid] <= kk) lo = mid; else hi = mid;
+    }
+    const int zz = lo / ncolI + 1, col = lo - (zz - 1) * ncolI;
+    const int ti = s_ct[lo] + (kk - s_cp[lo]);
+    const int gi = s_cg[lo] + (kk - s_cp[lo]);
     const int zf = warp_min(valid ? zz : 1 << 30), zl = warp_max(valid ? zz : -1);
-    float4 pi4 = T0[ti];
-    if (!valid) pi4.x = kFar;  // no hits
-    int cnt = 0;
-    for (int col = 0; col < 9; ++col) {
-      const int a = s_off[col * T.nzt + zf - 1], e = s_off[col * T.nzt + zl + 2];
+    unsigned tmask = __reduce_or_sync(kFull, valid ? s_nbm[col] : 0u);
+    const float* pi = P + (ti >> 1) * 8 + (ti & 1);
+    const float xi = valid ? pi[0] : kFar;  // invalid lanes: no hits
+    const float2 nX = make_float2(-xi, -xi), nY = make_float2(-pi[2], -pi[2]), nZ = make_float2(-pi[4], -pi[4]);
+    const float Hi2 = pi[6];
+    uint4* dst = reinterpret_cast<uint4*>(s.nbr + (size_t)gi * g.lcap);
+    uint16_t* w = buf;  // next free buffer row
+    int flushed = 0;    // entries already in global memory
+    auto test_one = [&](int t) {  // a single candidate (range ends)
+      const float* q = P + (t >> 1) * 8 + (t & 1);
+      const float dx = q[0] + nX.x, dy = q[2] + nY.x, dz = q[4] + nZ.x;
+      const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+      if (r2 < Hi2 || r2 < q[6]) { *w = (uint16_t)t; w += 32; }
+    };
+    while (tmask) {
+      const int tcol = __ffs(tmask) - 1;
+      tmask &= tmask - 1;
+      int a = S.off[tcol * T.nzt + zf - 1];
+      int e = S.off[tcol * T.nzt + zl + 2];
+      if (a & 1) test_one(a++);
+      if ((e - a) & 1) test_one(--e);
+      for (int p0 = a >> 1; p0 < (e >> 1); p0 += 8) {
+        const int pn = min(e >> 1, p0 + 8);
 #pragma unroll 4
-      for (int t = a; t < e; ++t) {
-        const float4 p = T0[t];
-        const float dx = pi4.x - p.x, dy = pi4.y - p.y, dz = pi4.z - p.z;
-        const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-        if (r2 < fmaxf(pi4.w, p.w) && r2 > 0.f) {
-          if (cnt < g.lcap) lst[cnt * 32] = (uint16_t)t;
-          ++cnt;
+        for (int pp = p0; pp < pn; ++pp) {
+          const float4 A = reinterpret_cast<const float4*>(P)[2 * pp];
+          const float4 B = reinterpret_cast<const float4*>(P)[2 * pp + 1];
+          const float2 dx = __fadd2_rn(make_float2(A.x, A.y), nX);
+          const float2 dy = __fadd2_rn(make_float2(A.z, A.w), nY);
+          const float2 dz = __fadd2_rn(make_float2(B.x, B.y), nZ);
+          float2 r2 = __fmul2_rn(dx, dx);
+          r2 = __ffma2_rn(dy, dy, r2);
+          r2 = __ffma2_rn(dz, dz, r2);
+          if (r2.x < fmaxf(Hi2, B.z)) { *w = (uint16_t)(2 * pp); w += 32; }
+          if (r2.y < fmaxf(Hi2, B.w)) { *w = (uint16_t)(2 * pp + 1); w += 32; }
+        }
+        // at most 7 + 16 buffered entries: drain 8 at a time
+        while (w - buf >= 8 * 32) {
+          if (flushed + 8 <= g.lcap) {
+            uint4 v;
+            v.x = (uint32_t)buf[0 * 32] | ((uint32_t)buf[1 * 32] << 16);
+            v.y = (uint32_t)buf[2 * 32] | ((uint32_t)buf[3 * 32] << 16);
+            v.z = (uint32_t)buf[4 * 32] | ((uint32_t)buf[5 * 32] << 16);
+            v.w = (uint32_t)buf[6 * 32] | ((uint32_t)buf[7 * 32] << 16);
+            dst[flushed >> 3] = v;
+          }
+          for (uint16_t* q = buf + 8 * 32; q < w; q += 32) q[-8 * 32] = *q;
+          w -= 8 * 32;
+          flushed += 8;
         }
       }
     }
-    const int cntp = (cnt + 7) & ~7;
-    if (cntp > g.lcap) over = max(over, cntp);
-    if (valid && cntp <= g.lcap) {
-      for (int kk = cnt; kk < cntp; ++kk) lst[kk * 32] = (uint16_t)g.tcap;
-      const int gi = T.g0 + k;
-      uint4* dst = reinterpret_cast<uint4*>(s.nbr + (size_t)gi * g.lcap);
-      for (int k8 = 0; k8 < cntp; k8 += 8) {
+    int nb = (int)(w - buf) >> 5;
+    auto flush8 = [&]() {
+      if (flushed + 8 <= g.lcap) {
         uint4 v;
-        v.x = (uint32_t)lst[(k8 + 0) * 32] | ((uint32_t)lst[(k8 + 1) * 32] << 16);
-        v.y = (uint32_t)lst[(k8 + 2) * 32] | ((uint32_t)lst[(k8 + 3) * 32] << 16);
-        v.z = (uint32_t)lst[(k8 + 4) * 32] | ((uint32_t)lst[(k8 + 5) * 32] << 16);
-        v.w = (uint32_t)lst[(k8 + 6) * 32] | ((uint32_t)lst[(k8 + 7) * 32] << 16);
-        dst[k8 >> 3] = v;
+        v.x = (uint32_t)buf[0 * 32] | ((uint32_t)buf[1 * 32] << 16);
+        v.y = (uint32_t)buf[2 * 32] | ((uint32_t)buf[3 * 32] << 16);
+        v.z = (uint32_t)buf[4 * 32] | ((uint32_t)buf[5 * 32] << 16);
+        v.w = (uint32_t)buf[6 * 32] | ((uint32_t)buf[7 * 32] << 16);
+        dst[flushed >> 3] = v;
       }
-      s.ncount[gi] = cntp;
-      s.hbuild[gi] = sqrtf(pi4.w) / Hfac;
+      for (int q = 8; q < nb; ++q) buf[(q - 8) * 32] = buf[q * 32];
+      nb -= 8;
+      flushed += 8;
+    };
+    while (nb >= 8) flush8();
+    const int cnt = flushed + nb;
+    const int cntp = (cnt + 7) & ~7;
+    while (nb < ((nb + 7) & ~7)) buf[(nb++) * 32] = (uint16_t)g.tcap;
+    if (nb >= 8) flush8();
+    if (cntp > g.lcap) over = max(over, cntp);
+    if (valid) {
+      s.ncount[gi] = min(cntp, g.lcap);
+      s.hbuild[gi] = sqrtf(Hi2) / Hfac;
     }
     __syncwarp();
   }
@@ -249,51 +454,46 @@ __global__ void __launch_bounds__(kNW * 32) k_lists(DevGrid g, DevPhys ph, DevSt
 // ============================================================== density loop ==========
 // Eqs. 2-6 with the Newton-Raphson h update of the ghost (R7) and the
 // density finalize (Eq. 8, EoS, Balsara; R8, R14) fused into the epilogue.
-// Accumulators per particle i (q = r/h_i, w = M4, self term added in the epilogue):
+// Accumulators per particle i (q = r/h_i, w = M4; the self pair is in the list: w(0) = 1):
 //   S0 = sum w, S1 = sum q w', R0 = sum m_j w, R1 = sum m_j q w',
 //   Dv = sum m_j w'/r (v_ij . r_ij),  Cv = sum m_j w'/r (v_ij x r_ij),  N_i.
 // Then nhat = S0/(pi h^3), dn/dh = -(3 S0 + S1)/(pi h^4), rho = R0/(pi h^3),
 // drho/dh = -(3 R0 + R1)/(pi h^4), div = -Dv/(rho pi h^4), curl = Cv/(rho pi h^4),
 // g = nhat h^3 - eta^3 = S0/pi - eta^3, h g' = -S1/pi.
-__global__ void __launch_bounds__(kNW * 32) k_density(DevGrid g, DevPhys ph, DevState s,
+__global__ void __launch_bounds__(kNW * 32, 2) k_density(DevGrid g, DevPhys ph, DevState s,
                                                       const int* __restrict__ cell_start, int pass,
                                                       const uint8_t* __restrict__ blk_in, uint8_t* __restrict__ blk_out,
-                                                      DevCounters* __restrict__ ctr) {
+                                                      float hfac_stale, DevCounters* __restrict__ ctr) {
   if (pass > 0 && !blk_in[blockIdx.x]) return;
-  __shared__ int s_off[kMaxTileCells + 1];
-  __shared__ int s_gst[kMaxTileCells];
   __shared__ int s_ni;
   __shared__ unsigned long long s_pairs, s_final;
   __shared__ int s_unconv, s_active;
-  extern __shared__ float4 smem4[];
-  float4* T0 = smem4;                  // x, y, z, m
-  float4* T1 = T0 + (g.tcap + 1);      // vx, vy, vz, h
-  int* ilist = reinterpret_cast<int*>(T1 + (g.tcap + 1));
-  Tile T;
   if (threadIdx.x == 0) { s_ni = 0; s_pairs = 0; s_final = 0; s_unconv = 0; s_active = 0; }
-  tile_setup(g, blockIdx.x, cell_start, s_off, s_gst, T);
-  if (T.ntile > g.tcap) {
-    if (threadIdx.x == 0) atomicExch(&ctr->nonfinite, 2);
-    return;
+  TILE_PROLOGUE();
+  const int O1 = SP;  // T0 = smem4[j]: x, y, z, h   T1 = smem4[O1 + j]: vx, vy, vz, m
+  int* ilist = reinterpret_cast<int*>(smem4 + 2 * SP);
+  {
+    const float4* src[2] = {reinterpret_cast<const float4*>(s.xh), s.vm};
+    const int o16[2] = {0, O1};
+    stage_records(S, nseg, 2, src, o16, nullptr, 0);
   }
   for (int t = threadIdx.x; t < T.ntile; t += blockDim.x) {
-    int gi = slot_global(s_off, s_gst, T.nct, t);
-    uint4 x = __ldg(&s.xh[gi]);
-    float4 v = __ldg(&s.vm[gi]);
-    float3 p = rel_pos(g, T, x);
-    T0[t] = make_float4(p.x, p.y, p.z, v.w);
-    T1[t] = make_float4(v.x, v.y, v.z, __uint_as_float(x.w));
+    const uint4 x = reinterpret_cast<const uint4*>(smem4)[t];
+    const float3 p = rel_pos(g, T, x);
+    smem4[t] = make_float4(p.x, p.y, p.z, __uint_as_float(x.w));
   }
   if (threadIdx.x == 0) {
-    T0[g.tcap] = make_float4(kFar, kFar, kFar, 0.f);
-    T1[g.tcap] = make_float4(0.f, 0.f, 0.f, 1.f);
+    smem4[g.tcap] = make_float4(kFar, kFar, kFar, 1.f);
+    smem4[O1 + g.tcap] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  const int ni_all = T.ie - T.ib;
   if (pass == 0) {
-    if (threadIdx.x == 0) s_ni = ni_all;
+    if (threadIdx.x == 0) s_ni = T.ni;
   } else {
-    for (int k = threadIdx.x; k < ni_all; k += blockDim.x)
-      if (s.active[T.g0 + k]) ilist[atomicAdd(&s_ni, 1)] = k;
+    for (int k = threadIdx.x; k < T.ni; k += blockDim.x) {
+      int ti, gi;
+      i_slot(S, k, ti, gi);
+      if (s.active[gi]) ilist[atomicAdd(&s_ni, 1)] = k;
+    }
   }
   __syncthreads();
   const int ni = s_ni;
@@ -305,54 +505,56 @@ __global__ void __launch_bounds__(kNW * 32) k_density(DevGrid g, DevPhys ph, Dev
     const int kk = c * 32 + lane;
     const bool valid = kk < ni;
     const int li = pass == 0 ? (valid ? kk : c * 32) : ilist[valid ? kk : c * 32];
-    const int ti = T.ib + li, gi = T.g0 + li;
-    const float4 pi4 = T0[ti];
-    const float4 vi4 = T1[ti];
-    const float h = vi4.w, hinv = 1.f / h;
+    int ti, gi;
+    i_slot(S, li, ti, gi);
+    const float4 pi4 = smem4[ti];
+    const float4 vi4 = smem4[O1 + ti];
+    const float h = pi4.w, hinv = 1.f / h;
     const float qband = g.eabs * hinv + 8e-6f;  // |q - 2| below this: decide in fp64
-    const double H2e = h2_exact(h, ph.gamma_k);
     const int cnt = valid ? s.ncount[gi] : 0;
     float S0 = 0.f, S1 = 0.f, R0 = 0.f, R1 = 0.f, Dv = 0.f, Cx = 0.f, Cy = 0.f, Cz = 0.f;
     int nn = 0;
     for_list(s.nbr + (size_t)gi * g.lcap, cnt, [&](int j) {
-      const float4 p = T0[j];
-      const float4 q4 = T1[j];
+      const float4 p = smem4[j];
+      const float4 q4 = smem4[O1 + j];
       const float dx = pi4.x - p.x, dy = pi4.y - p.y, dz = pi4.z - p.z;
       const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-      const float rinv = rsqrtf(r2);
+      const float rinv = rinv_safe(r2);
       const float q = r2 * rinv * hinv;
-      bool in = q < 2.f;
-      if (fabsf(q - 2.f) < qband)
-        in = exact_neighbour(s.xh, gi, slot_global(s_off, s_gst, T.nct, j), H2e, g.dscale[0], g.dscale[1],
-                             g.dscale[2]);
-      nn += in;
+      const float d = q - 2.f;
+      nn += neg(d);
+      if (fabsf(d) < qband) {
+        const bool ex = exact_neighbour(s.xh, gi, slot_global(S, T.nct, j), h2_exact(h, ph.gamma_k), g.dscale[0],
+                                        g.dscale[1], g.dscale[2]);
+        nn += (int)ex - neg(d);
+      }
       float w, dw;
       m4(q, w, dw);
       const float qdw = q * dw;
       S0 += w;
       S1 += qdw;
-      R0 = fmaf(p.w, w, R0);
-      R1 = fmaf(p.w, qdw, R1);
-      const float F = p.w * dw * rinv;
+      R0 = fmaf(q4.w, w, R0);
+      R1 = fmaf(q4.w, qdw, R1);
+      const float F = q4.w * dw * rinv;
       const float ux = vi4.x - q4.x, uy = vi4.y - q4.y, uz = vi4.z - q4.z;
       Dv = fmaf(F, fmaf(uz, dz, fmaf(uy, dy, ux * dx)), Dv);
       Cx = fmaf(F, fmaf(uy, dz, -uz * dy), Cx);
       Cy = fmaf(F, fmaf(uz, dx, -ux * dz), Cy);
       Cz = fmaf(F, fmaf(ux, dy, -uy * dx), Cz);
     });
-    npairs += (unsigned long long)nn;
+    nn -= 1;  // the self pair
     if (valid) {
-      // ---- epilogue: self term, closure, Newton / finalize
-      const float mi = pi4.w;
-      const float S0t = S0 + 1.f, R0t = R0 + mi;  // self: w(0) = 1, q w'(0) = 0
+      npairs += (unsigned long long)nn;
+      // ---- epilogue: closure, Newton / finalize
+      const float mi = vi4.w;
       const float ih3 = inv_pi * hinv * hinv * hinv;
-      const float nhat = S0t * ih3;
-      const float dndh = -(3.f * S0t + S1) * ih3 * hinv;
-      const float rho = R0t * ih3;
-      const float drho = -(3.f * R0t + R1) * ih3 * hinv;
-      const float gres = S0t * inv_pi - ph.eta3;
+      const float nhat = S0 * ih3;
+      const float dndh = -(3.f * S0 + S1) * ih3 * hinv;
+      const float rho = R0 * ih3;
+      const float drho = -(3.f * R0 + R1) * ih3 * hinv;
+      const float gres = S0 * inv_pi - ph.eta3;
       const bool conv = (ph.h_max_iter == 0) || fabsf(gres) <= ph.h_tol * ph.eta3;
-      int it = pass == 0 ? 0 : s.iters[gi];
+      const int it = pass == 0 ? 0 : s.iters[gi];
       const bool give_up = !conv && it >= ph.h_max_iter;
       if (conv || give_up) {
         const float ih4 = ih3 * hinv / rho;
@@ -381,7 +583,7 @@ __global__ void __launch_bounds__(kNW * 32) k_density(DevGrid g, DevPhys ph, Dev
         float lo = pass == 0 ? 0.f : s.hlo[gi];
         float hi = pass == 0 ? CUDART_INF_F : s.hhi[gi];
         if (gres > 0.f) hi = h; else lo = h;
-        float hn = (S1 < 0.f) ? h * (1.f + (S0t - ph.pi_eta3) / S1) : (gres < 0.f ? 2.f * h : 0.5f * h);
+        float hn = (S1 < 0.f) ? h * (1.f + (S0 - ph.pi_eta3) / S1) : (gres < 0.f ? 2.f * h : 0.5f * h);
         hn = fminf(fmaxf(hn, 0.5f * h), 2.f * h);
         if (hn <= lo || hn >= hi) hn = isinf(hi) ? 2.f * h : 0.5f * (lo + hi);
         s.hlo[gi] = lo;
@@ -392,7 +594,7 @@ __global__ void __launch_bounds__(kNW * 32) k_density(DevGrid g, DevPhys ph, Dev
         s_active = 1;
         const float Hn = ph.gamma_k * hn * (1.f + g.skin);
         if (Hn > g.side_min) atomicExch(&ctr->h_exceeds, 1);
-        if (hn > (1.f + g.skin) * s.hbuild[gi]) atomicExch(&ctr->list_stale, 1);
+        if (hn > hfac_stale * s.hbuild[gi]) atomicExch(&ctr->list_stale, 1);
       }
     }
   }
@@ -419,77 +621,70 @@ __global__ void __launch_bounds__(kNW * 32) k_density(DevGrid g, DevPhys ph, Dev
 // Brookshaw Laplacian lap u_i = 2 sum_j (m_j/rho_j)(u_i - u_j) dW/dr / r (R16), gathered
 // over r_ij < H_i; the gradient ghost (alpha_v Eqs. 12-15, alpha_c Eqs. 21-24; R17-R21)
 // runs in the epilogue and writes the force-loop records.
-__global__ void __launch_bounds__(kNW * 32) k_gradient(DevGrid g, DevPhys ph, DevState s,
+__global__ void __launch_bounds__(kNW * 32, 2) k_gradient(DevGrid g, DevPhys ph, DevState s,
                                                        const int* __restrict__ cell_start, float dt, int first_step,
                                                        DevCounters* __restrict__ ctr) {
-  __shared__ int s_off[kMaxTileCells + 1];
-  __shared__ int s_gst[kMaxTileCells];
   __shared__ unsigned long long s_pairs;
-  extern __shared__ float4 smem4[];
-  float4* T0 = smem4;                               // x, y, z, u
-  float4* T1 = T0 + (g.tcap + 1);                   // vx, vy, vz, c
-  float* T2 = reinterpret_cast<float*>(T1 + (g.tcap + 1));  // m/rho
-  Tile T;
   if (threadIdx.x == 0) s_pairs = 0;
-  tile_setup(g, blockIdx.x, cell_start, s_off, s_gst, T);
-  if (T.ntile > g.tcap) {
-    if (threadIdx.x == 0) atomicExch(&ctr->nonfinite, 2);
-    return;
+  TILE_PROLOGUE();
+  // T0 = smem4[j]: x, y, z, h   T1 = smem4[O1 + j]: vx, vy, vz, m   T2 = smem4[O2 + j]: c, u, m/rho, rho
+  const int O1 = SP, O2 = 2 * SP;
+  {
+    const float4* src[3] = {reinterpret_cast<const float4*>(s.xh), s.vm, s.gq};
+    const int o16[3] = {0, O1, O2};
+    stage_records(S, nseg, 3, src, o16, nullptr, 0);
   }
   for (int t = threadIdx.x; t < T.ntile; t += blockDim.x) {
-    int gi = slot_global(s_off, s_gst, T.nct, t);
-    uint4 x = __ldg(&s.xh[gi]);
-    float4 v = __ldg(&s.vm[gi]);
-    float4 q = __ldg(&s.gq[gi]);
-    float3 p = rel_pos(g, T, x);
-    T0[t] = make_float4(p.x, p.y, p.z, q.y);
-    T1[t] = make_float4(v.x, v.y, v.z, q.x);
-    T2[t] = q.z;
+    const uint4 x = reinterpret_cast<const uint4*>(smem4)[t];
+    const float3 p = rel_pos(g, T, x);
+    smem4[t] = make_float4(p.x, p.y, p.z, __uint_as_float(x.w));
   }
   if (threadIdx.x == 0) {
-    T0[g.tcap] = make_float4(kFar, kFar, kFar, 0.f);
-    T1[g.tcap] = make_float4(0.f, 0.f, 0.f, 0.f);
-    T2[g.tcap] = 0.f;
+    smem4[g.tcap] = make_float4(kFar, kFar, kFar, 1.f);
+    smem4[O1 + g.tcap] = make_float4(0.f, 0.f, 0.f, 0.f);
+    smem4[O2 + g.tcap] = make_float4(0.f, 0.f, 0.f, 1.f);
   }
   __syncthreads();
-  const int ni = T.ie - T.ib;
+  const int ni = T.ni;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned long long npairs = 0;
 
   for (int c = warp; c * 32 < ni; c += kNW) {
     const int kk = c * 32 + lane;
     const bool valid = kk < ni;
-    const int li = valid ? kk : c * 32;
-    const int ti = T.ib + li, gi = T.g0 + li;
-    const float4 pi4 = T0[ti];
-    const float4 vi4 = T1[ti];
-    const float h = __uint_as_float(s.xh[gi].w), hinv = 1.f / h;
+    int ti, gi;
+    i_slot(S, valid ? kk : c * 32, ti, gi);
+    const float4 pi4 = smem4[ti];
+    const float4 vi4 = smem4[O1 + ti];
+    const float4 gi4 = smem4[O2 + ti];
+    const float h = pi4.w, hinv = 1.f / h;
     const float qband = g.eabs * hinv + 8e-6f;
-    const double H2e = h2_exact(h, ph.gamma_k);
-    const float ci = vi4.w, ui = pi4.w;
+    const float ci = gi4.x, ui = gi4.y;
     const int cnt = valid ? s.ncount[gi] : 0;
     float vmax = 2.f * ci, lap = 0.f;
     int nn = 0;
     for_list(s.nbr + (size_t)gi * g.lcap, cnt, [&](int j) {
-      const float4 p = T0[j];
-      const float4 q4 = T1[j];
-      const float Vj = T2[j];
+      const float4 p = smem4[j];
+      const float4 q4 = smem4[O1 + j];
+      const float4 g4 = smem4[O2 + j];
       const float dx = pi4.x - p.x, dy = pi4.y - p.y, dz = pi4.z - p.z;
       const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-      const float rinv = rsqrtf(r2);
+      const float rinv = rinv_safe(r2);
       const float q = r2 * rinv * hinv;
-      bool in = q < 2.f;
-      if (fabsf(q - 2.f) < qband)
-        in = exact_neighbour(s.xh, gi, slot_global(s_off, s_gst, T.nct, j), H2e, g.dscale[0], g.dscale[1],
+      const float d = q - 2.f;
+      int in = neg(d);
+      if (fabsf(d) < qband)
+        in = exact_neighbour(s.xh, gi, slot_global(S, T.nct, j), h2_exact(h, ph.gamma_k), g.dscale[0], g.dscale[1],
                              g.dscale[2]);
       nn += in;
       const float dw = m4_dw(q);
       const float vr = fmaf(vi4.z - q4.z, dz, fmaf(vi4.y - q4.y, dy, (vi4.x - q4.x) * dx));
       const float mu = fminf(vr, 0.f) * rinv;
-      const float vs = fmaf(-ph.beta, mu, ci + q4.w);
+      const float vs = fmaf(-ph.beta, mu, ci + g4.x);
       vmax = fmaxf(vmax, in ? vs : 0.f);
-      lap = fmaf(Vj * (ui - p.w), dw * rinv, lap);
+      lap = fmaf(g4.z * (ui - g4.y), dw * rinv, lap);
     });
+    nn -= 1;  // the self pair
     if (valid) {
       npairs += (unsigned long long)nn;
       const float lap_u = 2.f * lap * hinv * hinv * hinv * hinv / kPi;
@@ -501,9 +696,9 @@ __global__ void __launch_bounds__(kNW * 32) k_gradient(DevGrid g, DevPhys ph, De
       const float div = dvc.w;
       float av = s.av[gi], ac = s.ac[gi];
       const float Ddot = first_step ? 0.f : (div - s.dprev[gi]) / dt;
-      const float S = H * H * fmaxf(-Ddot, 0.f);
-      const float den = vsig * vsig + S;
-      const float aloc = den > 0.f ? ph.alpha_v_max * S / den : 0.f;
+      const float Sx = H * H * fmaxf(-Ddot, 0.f);
+      const float den = vsig * vsig + Sx;
+      const float aloc = den > 0.f ? ph.alpha_v_max * Sx / den : 0.f;
       if (av < aloc) av = aloc;
       else av = aloc + (av - aloc) * expf(-ph.ell * ci * dt / H);
       const float src = ui > 0.f ? ph.beta_c * H * lap_u / sqrtf(ui) : 0.f;
@@ -515,11 +710,11 @@ __global__ void __launch_bounds__(kNW * 32) k_gradient(DevGrid g, DevPhys ph, De
       s.av[gi] = av;
       s.ac[gi] = ac;
       s.dprev[gi] = div;
-      const float rho = s.dens[gi].x;
+      const float rho = gi4.w;
       const float f = fin.x, P = fin.y;
       s.fr1[gi] = make_float4(P / (rho * rho), f * hinv * hinv * hinv * hinv / kPi, ci, rho);
       s.fr2[gi] = make_float4(P, P * ac, ui, av);
-      s.fr3[gi] = make_float2(fin.w, hinv);
+      s.fr3[gi] = fin.w;
     }
   }
 #pragma unroll
@@ -538,47 +733,37 @@ __global__ void __launch_bounds__(kNW * 32) k_gradient(DevGrid g, DevPhys ph, De
 // S_ij is evaluated from operands that are symmetric in (i, j), so the pair terms of i and
 // j are exact negatives (momentum and energy conserving up to the summation rounding).
 // The CFL dt = C_cfl min 2 gamma_k h / v_sig is reduced in the epilogue.
-__global__ void __launch_bounds__(kNW * 32) k_force(DevGrid g, DevPhys ph, DevState s,
+__global__ void __launch_bounds__(kNW * 32, 2) k_force(DevGrid g, DevPhys ph, DevState s,
                                                     const int* __restrict__ cell_start,
                                                     DevCounters* __restrict__ ctr) {
-  __shared__ int s_off[kMaxTileCells + 1];
-  __shared__ int s_gst[kMaxTileCells];
   __shared__ unsigned long long s_pairs;
   __shared__ unsigned int s_dt;
   __shared__ int s_bad;
-  extern __shared__ float4 smem4[];
-  float4* T0 = smem4;                      // x, y, z, B
-  float4* T1 = T0 + (g.tcap + 1);          // vx, vy, vz, m
-  float4* T2 = T1 + (g.tcap + 1);          // A, Kf, c, rho
-  float4* T3 = T2 + (g.tcap + 1);          // P, P alpha_c, u, alpha_v
-  float* T4 = reinterpret_cast<float*>(T3 + (g.tcap + 1));  // 1/h
-  Tile T;
   if (threadIdx.x == 0) { s_pairs = 0; s_dt = 0x7f800000u; s_bad = 0; }
-  tile_setup(g, blockIdx.x, cell_start, s_off, s_gst, T);
-  if (T.ntile > g.tcap) {
-    if (threadIdx.x == 0) atomicExch(&ctr->nonfinite, 2);
-    return;
+  TILE_PROLOGUE();
+  // T0 = [j]: x, y, z, 1/h   T1 = [O1+j]: vx, vy, vz, m   T2 = [O2+j]: A, Kf, c, rho
+  // T3 = [O3+j]: P, P alpha_c, u, alpha_v   T4 = float [O4+j]: B
+  const int O1 = SP, O2 = 2 * SP, O3 = 3 * SP, O4 = 16 * SP;
+  const float* sm1 = reinterpret_cast<const float*>(smem4);
+  {
+    const float4* src[4] = {reinterpret_cast<const float4*>(s.xh), s.vm, s.fr1, s.fr2};
+    const int o16[4] = {0, O1, O2, O3};
+    stage_records(S, nseg, 4, src, o16, s.fr3, O4);
   }
   for (int t = threadIdx.x; t < T.ntile; t += blockDim.x) {
-    int gi = slot_global(s_off, s_gst, T.nct, t);
-    uint4 x = __ldg(&s.xh[gi]);
-    float3 p = rel_pos(g, T, x);
-    float2 b3 = __ldg(&s.fr3[gi]);
-    T0[t] = make_float4(p.x, p.y, p.z, b3.x);
-    T1[t] = __ldg(&s.vm[gi]);
-    T2[t] = __ldg(&s.fr1[gi]);
-    T3[t] = __ldg(&s.fr2[gi]);
-    T4[t] = b3.y;
+    const uint4 x = reinterpret_cast<const uint4*>(smem4)[t];
+    const float3 p = rel_pos(g, T, x);
+    smem4[t] = make_float4(p.x, p.y, p.z, 1.f / __uint_as_float(x.w));
   }
   if (threadIdx.x == 0) {
-    T0[g.tcap] = make_float4(kFar, kFar, kFar, 0.f);
-    T1[g.tcap] = make_float4(0.f, 0.f, 0.f, 0.f);
-    T2[g.tcap] = make_float4(0.f, 0.f, 0.f, 1.f);
-    T3[g.tcap] = make_float4(0.f, 0.f, 0.f, 0.f);
-    T4[g.tcap] = 1.f;
+    smem4[g.tcap] = make_float4(kFar, kFar, kFar, 1.f);
+    smem4[O1 + g.tcap] = make_float4(0.f, 0.f, 0.f, 0.f);
+    smem4[O2 + g.tcap] = make_float4(0.f, 0.f, 0.f, 1.f);
+    smem4[O3 + g.tcap] = make_float4(0.f, 0.f, 0.f, 0.f);
+    reinterpret_cast<float*>(smem4)[O4 + g.tcap] = 0.f;
   }
   __syncthreads();
-  const int ni = T.ie - T.ib;
+  const int ni = T.ni;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned long long npairs = 0;
   float dtmin = CUDART_INF_F;
@@ -586,36 +771,36 @@ __global__ void __launch_bounds__(kNW * 32) k_force(DevGrid g, DevPhys ph, DevSt
   for (int c = warp; c * 32 < ni; c += kNW) {
     const int kk = c * 32 + lane;
     const bool valid = kk < ni;
-    const int li = valid ? kk : c * 32;
-    const int ti = T.ib + li, gi = T.g0 + li;
-    const float4 pi4 = T0[ti];
-    const float4 vi4 = T1[ti];
-    const float4 ai = T2[ti];
-    const float4 bi = T3[ti];
-    const float hinv_i = T4[ti];
+    int ti, gi;
+    i_slot(S, valid ? kk : c * 32, ti, gi);
+    const float4 pi4 = smem4[ti];
+    const float4 vi4 = smem4[O1 + ti];
+    const float4 ai = smem4[O2 + ti];
+    const float4 bi = smem4[O3 + ti];
+    const float Bi = sm1[O4 + ti];
+    const float hinv_i = pi4.w;
     const float hi_ = __uint_as_float(s.xh[gi].w);
-    const double H2ei = h2_exact(hi_, ph.gamma_k);
-    const float eq = g.eabs;
+    const float ebi = g.eabs * hinv_i;
     const int cnt = valid ? s.ncount[gi] : 0;
     float ax = 0.f, ay = 0.f, az = 0.f, du = 0.f, vmax = 2.f * ai.z;
     int nn = 0;
     for_list(s.nbr + (size_t)gi * g.lcap, cnt, [&](int j) {
-      const float4 p = T0[j];
+      const float4 p = smem4[j];
       const float dx = pi4.x - p.x, dy = pi4.y - p.y, dz = pi4.z - p.z;
       const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-      const float4 vj = T1[j];
-      const float4 aj = T2[j];
-      const float4 bj = T3[j];
-      const float hinv_j = T4[j];
-      const float rinv = rsqrtf(r2);
+      const float4 vj = smem4[O1 + j];
+      const float4 aj = smem4[O2 + j];
+      const float4 bj = smem4[O3 + j];
+      const float Bj = sm1[O4 + j];
+      const float rinv = rinv_safe(r2);
       const float r = r2 * rinv;
-      const float qi = r * hinv_i, qj = r * hinv_j;
-      const float qm = fminf(qi, qj);
-      bool in = qm < 2.f;
-      if (fabsf(qm - 2.f) < eq * fmaxf(hinv_i, hinv_j) + 8e-6f) {
-        const int gj = slot_global(s_off, s_gst, T.nct, j);
-        const double H2ej = h2_exact(__uint_as_float(s.xh[gj].w), ph.gamma_k);
-        in = exact_neighbour(s.xh, gi, gj, fmax(H2ei, H2ej), g.dscale[0], g.dscale[1], g.dscale[2]);
+      const float qi = r * hinv_i, qj = r * p.w;
+      const float d = fminf(qi, qj) - 2.f;
+      int in = neg(d);
+      if (fabsf(d) < fmaxf(ebi, g.eabs * p.w) + 8e-6f) {
+        const int gj = slot_global(S, T.nct, j);
+        const double H2 = fmax(h2_exact(hi_, ph.gamma_k), h2_exact(__uint_as_float(s.xh[gj].w), ph.gamma_k));
+        in = exact_neighbour(s.xh, gi, gj, H2, g.dscale[0], g.dscale[1], g.dscale[2]);
       }
       nn += in;
       const float Gi = ai.y * m4_dw(qi) * rinv;
@@ -624,8 +809,8 @@ __global__ void __launch_bounds__(kNW * 32) k_force(DevGrid g, DevPhys ph, DevSt
       const float mu = fminf(vr, 0.f) * rinv;
       const float vs = fmaf(-ph.beta, mu, ai.z + aj.z);
       vmax = fmaxf(vmax, in ? vs : 0.f);
-      const float abar = 0.25f * (bi.w + bj.w) * (pi4.w + p.w);
-      const float irs = __frcp_rn(ai.w + aj.w);
+      const float abar = 0.25f * (bi.w + bj.w) * (Bi + Bj);
+      const float irs = __fdividef(1.f, ai.w + aj.w);
       const float PiV = -2.f * abar * mu * vs * irs;
       const float Gbar = 0.5f * (Gi + Gj);
       const float Sij = fmaf(PiV, Gbar, fmaf(ai.x, Gi, aj.x * Gj));
@@ -634,11 +819,12 @@ __global__ void __launch_bounds__(kNW * 32) k_force(DevGrid g, DevPhys ph, DevSt
       ay = fmaf(-mS, dy, ay);
       az = fmaf(-mS, dz, az);
       const float Psum = bi.x + bj.x;
-      const float acij = Psum > 0.f ? (bi.y + bj.y) * __frcp_rn(Psum) : 0.f;
+      const float acij = Psum > 0.f ? __fdividef(bi.y + bj.y, Psum) : 0.f;
       const float vc = fabsf(vr) * rinv + sqrtf(2.f * fabsf(bi.x - bj.x) * irs);
       const float D = acij * vc * (bi.z - bj.z) * (Gi + Gj) * r * irs;
       du = fmaf(vj.w, fmaf(ai.x * Gi, vr, fmaf(0.5f * PiV * Gbar, vr, D)), du);
     });
+    nn -= 1;  // the self pair
     if (valid) {
       s.acc[gi] = make_float4(ax, ay, az, du);
       s.vsig[gi] = vmax;
@@ -669,19 +855,21 @@ __global__ void __launch_bounds__(kNW * 32) k_force(DevGrid g, DevPhys ph, DevSt
 
 // per-block tile size (max over blocks) -> sizes shared memory of the loops
 __global__ void k_tile_sizes(DevGrid g, const int* __restrict__ cell_start, int* max_tile) {
-  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= g.nblocks) return;
-  int zb = b % g.nzb, col = b / g.nzb, iy = col % g.ny, ix = col / g.ny;
-  int z0 = zb * g.KZ, z1 = min(g.nz, z0 + g.KZ);
+  const int zb = b % g.nzb, t2 = b / g.nzb, jy = t2 % g.nby, jx = t2 / g.nby;
+  const int ix0 = jx * g.bx, iy0 = jy * g.by;
+  const int z0 = zb * g.KZ, z1 = min(g.nz, z0 + g.KZ);
   int tot = 0;
-  for (int c = 0; c < 9; ++c) {
-    int cx = (ix + c / 3 - 1 + g.nx) % g.nx, cy = (iy + c % 3 - 1 + g.ny) % g.ny;
-    for (int z = z0 - 1; z <= z1; ++z) {
-      int cz = (z + g.nz) % g.nz;
-      int cell = (cx * g.ny + cy) * g.nz + cz;
-      tot += cell_start[cell + 1] - cell_start[cell];
+  for (int dx = -1; dx <= g.bx; ++dx)
+    for (int dy = -1; dy <= g.by; ++dy) {
+      const int cx = (ix0 + dx + g.nx) % g.nx, cy = (iy0 + dy + g.ny) % g.ny;
+      const int c0 = (cx * g.ny + cy) * g.nz;
+      for (int z = z0 - 1; z <= z1; ++z) {
+        const int cz = (z + g.nz) % g.nz;
+        tot += cell_start[c0 + cz + 1] - cell_start[c0 + cz];
+      }
     }
-  }
   atomicMax(max_tile, tot);
 }
 
@@ -689,9 +877,11 @@ __global__ void k_tile_sizes(DevGrid g, const int* __restrict__ cell_start, int*
 
 int kernel_threads() { return kNW * 32; }
 
-size_t lists_smem(const DevGrid& g) { return (size_t)(g.tcap + 1) * 16 + (size_t)kNW * g.lcap * 32 * 2; }
-size_t density_smem(const DevGrid& g) { return (size_t)(g.tcap + 1) * (2 * 16 + 4); }
-size_t gradient_smem(const DevGrid& g) { return (size_t)(g.tcap + 1) * (2 * 16 + 4); }
+size_t lists_smem(const DevGrid& g) {
+  return (size_t)((g.tcap + 2) & ~1) * 16 + (size_t)kNW * 24 * 32 * 2;
+}
+size_t density_smem(const DevGrid& g) { return (size_t)(g.tcap + 1) * (2 * 16 + 4); }  // + i list
+size_t gradient_smem(const DevGrid& g) { return (size_t)(g.tcap + 1) * (3 * 16); }
 size_t force_smem(const DevGrid& g) { return (size_t)(g.tcap + 1) * (4 * 16 + 4); }
 
 cudaError_t launch_tile_sizes(const DevGrid& g, const int* cell_start, int* max_tile, cudaStream_t st) {
@@ -705,7 +895,7 @@ static cudaError_t set_smem(const void* fn, size_t bytes) {
 
 cudaError_t launch_lists(const DevGrid& g, const DevPhys& ph, const DevState& s, const int* cell_start,
                          DevCounters* ctr, cudaStream_t st) {
-  size_t sm = lists_smem(g);
+  const size_t sm = lists_smem(g);
   cudaError_t e = set_smem((const void*)k_lists, sm);
   if (e != cudaSuccess) return e;
   k_lists<<<g.nblocks, kNW * 32, sm, st>>>(g, ph, s, cell_start, ctr);
@@ -713,17 +903,18 @@ cudaError_t launch_lists(const DevGrid& g, const DevPhys& ph, const DevState& s,
 }
 
 cudaError_t launch_density(const DevGrid& g, const DevPhys& ph, const DevState& s, const int* cell_start, int pass,
-                           const uint8_t* blk_in, uint8_t* blk_out, DevCounters* ctr, cudaStream_t st) {
-  size_t sm = density_smem(g);
+                           const uint8_t* blk_in, uint8_t* blk_out, float hfac_stale, DevCounters* ctr,
+                           cudaStream_t st) {
+  const size_t sm = density_smem(g);
   cudaError_t e = set_smem((const void*)k_density, sm);
   if (e != cudaSuccess) return e;
-  k_density<<<g.nblocks, kNW * 32, sm, st>>>(g, ph, s, cell_start, pass, blk_in, blk_out, ctr);
+  k_density<<<g.nblocks, kNW * 32, sm, st>>>(g, ph, s, cell_start, pass, blk_in, blk_out, hfac_stale, ctr);
   return cudaGetLastError();
 }
 
 cudaError_t launch_gradient(const DevGrid& g, const DevPhys& ph, const DevState& s, const int* cell_start, float dt,
                             int first_step, DevCounters* ctr, cudaStream_t st) {
-  size_t sm = gradient_smem(g);
+  const size_t sm = gradient_smem(g);
   cudaError_t e = set_smem((const void*)k_gradient, sm);
   if (e != cudaSuccess) return e;
   k_gradient<<<g.nblocks, kNW * 32, sm, st>>>(g, ph, s, cell_start, dt, first_step, ctr);
@@ -732,7 +923,7 @@ cudaError_t launch_gradient(const DevGrid& g, const DevPhys& ph, const DevState&
 
 cudaError_t launch_force(const DevGrid& g, const DevPhys& ph, const DevState& s, const int* cell_start,
                          DevCounters* ctr, cudaStream_t st) {
-  size_t sm = force_smem(g);
+  const size_t sm = force_smem(g);
   cudaError_t e = set_smem((const void*)k_force, sm);
   if (e != cudaSuccess) return e;
   k_force<<<g.nblocks, kNW * 32, sm, st>>>(g, ph, s, cell_start, ctr);

@@ -11,7 +11,7 @@ raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_outpu
 r = list(csv.reader(io.StringIO(raw)))
 hdr, units = r[0], r[1]
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
-tscale = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}
+tscale = {"nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3, "second": 1.0, "s": 1.0}
 res = {"report": rep, "dram_bytes_per_launch": {}, "duration_s": {}}
 for row in r[2:]:
     name = row[hdr.index("Kernel Name")].split("(")[0].split("::")[-1].replace("k_", "")

@@ -8,9 +8,12 @@ directed pairs) and the time per hydro step.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C4] [--impl ours|reference]
 
-Under torchrun (N > 1) every rank runs the same workload on its own GPU (independent
-replicas, "scaling": "weak"); the timed region is bracketed by a barrier and
-torch.cuda.synchronize(), and the max over ranks is reported.  Rank 0 prints ONE JSON line.
+Under torchrun (N > 1) the job is ONE simulation decomposed into x-slabs, one per GPU
+(include/sph.h "Several ranks"): N copies of the workload side by side along x in a box
+(N Lx, Ly, Lz), rank r owning copy r's slab, exchanging ghost planes, migrants and the
+global h_max / dt over NCCL every step ("scaling": "weak": the per-GPU work is fixed).
+The timed region is bracketed by a barrier and torch.cuda.synchronize(), and the max over
+ranks is reported.  Rank 0 prints ONE JSON line.
 """
 from __future__ import annotations
 
@@ -108,6 +111,37 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def rank_workload(key, rank, world):
+    """Rank's share of the weak-scaling job: copy `rank` of the workload, placed at
+    x in [rank Lx, (rank + 1) Lx) of a box (world Lx, Ly, Lz).  Fixed point: X' =
+    floor((X + rank 2^32) / world), i.e. inside rank's slab [floor(r 2^32 / N),
+    floor((r+1) 2^32 / N)) up to one grid unit (which the library migrates)."""
+    name, gen = WORKLOADS[key]
+    p = gen()
+    if world == 1:
+        return name, p
+    q = dict(p)
+    X = p["X"].astype(np.uint64)
+    X[:, 0] = (X[:, 0] + (np.uint64(rank) << np.uint64(32))) // np.uint64(world)
+    q["X"] = np.ascontiguousarray(X.astype(np.uint32))
+    box = np.asarray(p["box"], dtype=np.float64).copy()
+    box[0] *= world
+    q["box"] = box
+    return f"{name}_x{world}", q
+
+
+def share_uid(uid, rank, device=None):
+    """Broadcast rank 0's 128-byte NCCL id to every rank over torch.distributed."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.zeros(128, dtype=torch.uint8, device=device)
+    if rank == 0:
+        t.copy_(torch.frombuffer(bytearray(uid), dtype=torch.uint8))
+    dist.broadcast(t, src=0)
+    return bytes(t.cpu().numpy().tobytes())
+
+
 def dist_init(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -165,15 +199,18 @@ def run_reference(args, world, rank):
 def run_ours(args, world, rank, local):
     import torch
 
-    from paper_2505_14538_b200 import Context
+    from paper_2505_14538_b200 import Context, nccl_unique_id
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    name, gen = WORKLOADS[args.workload]
-    p = gen()
+    name, p = rank_workload(args.workload, rank, world)
     n = p["X"].shape[0]
     stream = torch.cuda.Stream(device=dev)
-    ctx = Context(p, stream=stream.cuda_stream, device=local)
+    multi = {}
+    if world > 1:
+        uid = share_uid(nccl_unique_id() if rank == 0 else b"", rank, device=dev)
+        multi = dict(rank=rank, nranks=world, n_total=n * world, nccl_uid=uid)
+    ctx = Context(p, stream=stream.cuda_stream, device=local, **multi)
     dt = 1e-4
 
     def ev():
@@ -241,7 +278,14 @@ def run_ours(args, world, rank, local):
     inter = pd + pg + pf
     K = args.steps
     ms_step = ms / K
-    value = inter * world / (ms * 1e-3)
+    inter_all = inter
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([float(inter)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t)  # interactions of all ranks (units all ranks processed)
+        inter_all = float(t.item())
+    value = inter_all / (ms * 1e-3)
     t_force = ph[2] / K * 1e-3
     t_dens = ph[0] / K * 1e-3
     t_grad = ph[1] / K * 1e-3
@@ -268,6 +312,12 @@ def run_ours(args, world, rank, local):
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(ctx, p, torch, dev, stream, max(2, min(K, 5)), world)
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([float(launches)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t)
+        launches = int(t.item())
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -278,10 +328,11 @@ def run_ours(args, world, rank, local):
             "value": value, "unit": "interactions/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": name, "particles": n, "parallelism": f"replicas{world}" if world > 1 else "1gpu",
+            "config": {"workload": name, "particles": n * world,
+                       "parallelism": f"x-slabs{world} (NCCL halo exchange)" if world > 1 else "1gpu",
                        "step": "KDK: kick/drift, rebuild, density+h-iteration, gradient, force+dt, kick",
                        "l2": "inputs larger than L2 (n x ~300 B >> 126 MB)",
-                       "interactions_per_step": inter / K, "density_passes_mean": float(np.mean(iters))},
+                       "interactions_per_step": inter_all / K, "density_passes_mean": float(np.mean(iters))},
             "gpu_launches": int(launches),
             "kernels": kernels,
             "roofline": roof,
@@ -307,10 +358,11 @@ def run_e2e(ctx, p, torch, dev, stream, K, world):
 
     host = {k: pinned(p[k]) for k in ("X", "v", "m", "u", "h", "alpha_v", "alpha_c")}
     hin = {k: (host[k].numpy().view(np.uint32) if k == "X" else host[k].numpy()) for k in host}
-    a_out = torch.empty((n, 3), dtype=torch.float32, pin_memory=True)
-    du_out = torch.empty((n,), dtype=torch.float32, pin_memory=True)
+    cap = n + (n // 4 + 4096 if world > 1 else 0)  # owned count after migration (several ranks)
+    a_out = torch.empty((cap, 3), dtype=torch.float32, pin_memory=True)
+    du_out = torch.empty((cap,), dtype=torch.float32, pin_memory=True)
     h2d = sum(v.nbytes for v in hin.values())
-    d2h = a_out.numel() * 4 + du_out.numel() * 4
+    d2h = n * 16
 
     from paper_2505_14538_b200 import binding
 
@@ -325,6 +377,10 @@ def run_e2e(ctx, p, torch, dev, stream, K, world):
 
     one()
     torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
     t0 = time.perf_counter()
     inter = 0
     for _ in range(K):
@@ -335,10 +391,12 @@ def run_e2e(ctx, p, torch, dev, stream, K, world):
     if world > 1:
         import torch.distributed as dist
 
-        t = torch.tensor([dt], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dt = float(t.item())
-    return {"value": inter * world / dt, "unit": "interactions/s", "h2d_bytes_per_step": int(h2d),
+        tm = torch.tensor([dt], dtype=torch.float64, device=dev)
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        ts = torch.tensor([float(inter)], dtype=torch.float64, device=dev)
+        dist.all_reduce(ts)
+        dt, inter = float(tm.item()), float(ts.item())
+    return {"value": inter / dt, "unit": "interactions/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * dt / K,
             "note": "host-timed (perf_counter) around upload + hydro pass + read-back; no kick/drift"}
 

@@ -22,8 +22,22 @@
  *  - Errors: no C++ exception crosses the ABI.  After any CUDA error the context is
  *    poisoned: every later call except sph_destroy / sph_last_error returns SPH_ERR_STATE.
  *    SPH_ERR_NOT_CONVERGED leaves the context valid (last h iterate kept).
- *  - Threading: a context is not thread-safe; one context per device per process.
+ *  - Threading: a context is not thread-safe.  Contexts of a loopback group (below) are
+ *    driven from one host thread each.
  *  - There is no CPU fallback: a call that cannot run on the GPU fails.
+ *
+ * Several ranks: nranks > 1 splits the box into
+ * x-slabs, rank r owning x in [floor(r 2^32 / R), floor((r+1) 2^32 / R)) on the fixed-point
+ * grid.  Each rank keeps one cell plane of ghosts on either side (cell side >= support
+ * radius, so one plane is the whole halo of P:82's neighbour search) and exchanges, per
+ * step: migrating particles + ghost positions/velocities at each rebuild (X1), ghost h and
+ * gradient-loop records after the density loop (X2), force-loop records after the gradient
+ * loop (X3), and the global flags / h_max / dt as allreduces (X4).  Every call below is then
+ * COLLECTIVE: all ranks make the same calls in the same order.  The transport is NCCL (one
+ * process per GPU; grouped ncclSend/ncclRecv between slab neighbours) or a loopback group
+ * (several contexts in one process, one host thread each, any devices; device copies) used
+ * to test the multi-rank path on one GPU.  sph_get returns the rank's OWNED particles in
+ * its local order (n = sph_local_count; SPH_F_ID identifies them).
  */
 #ifndef SPH_H_
 #define SPH_H_
@@ -50,11 +64,13 @@ typedef enum {
 
 typedef struct sph_ctx sph_ctx; /* opaque */
 
+typedef enum { SPH_TRANSPORT_NCCL = 0, SPH_TRANSPORT_LOOPBACK = 1 } sph_transport;
+
 /* Configuration.  Defaults (sph_config_default) follow DESIGN.md §3 readings R1, R7, R8,
  * R22, R23 and SPEC S:72-74. */
 typedef struct {
   uint32_t struct_size;   /* = sizeof(sph_config); ABI check                                */
-  int64_t n_total;        /* total particle count over all ranks (informational)           */
+  int64_t n_total;        /* total particle count over all ranks (nranks > 1: sizes buffers)*/
   double box[3];          /* periodic box side lengths L_a                                 */
   float gamma_k;          /* kernel support ratio H = gamma_k h; must be 2 (M4, R1)         */
   float eta;              /* target nhat h^3 = eta^3 (R1), default 1.2348            */
@@ -70,10 +86,13 @@ typedef struct {
   int32_t fh_mode;        /* R8: 0 -> f = 1/Omega (default), 1 -> f = Omega (Eq. 8 literal)*/
   int32_t device;         /* CUDA device ordinal                                            */
   void* stream;           /* cudaStream_t to enqueue on, or NULL                            */
-  int32_t rank, nranks;   /* multi-GPU slab decomposition (reserved: nranks must be 1)     */
+  int32_t rank, nranks;   /* slab decomposition over nranks ranks (default 0, 1)            */
   int32_t tile_cells_z;   /* cells per CTA block along z (0 = auto)                         */
   int32_t predict_h;      /* drift also advances h with d ln h/dt = (div v)/3 (continuity),   */
                           /* a better Newton start; the converged h does not depend on it     */
+  int32_t transport;      /* sph_transport, used when nranks > 1                            */
+  const void* nccl_uid;   /* NCCL: 128-byte id from sph_nccl_unique_id on rank 0, same on all*/
+  void* loopback;         /* LOOPBACK: group from sph_loopback_create (shared by the ranks)  */
 } sph_config;
 
 /* Particle input.  n particles; arrays are host pointers (on_device = 0) or device
@@ -147,11 +166,14 @@ typedef enum {
 void sph_config_default(sph_config* cfg);
 
 /* Create a context on cfg->device and copy the particles in (S:104 build_tree: the cell
- * grid is built here).  On success *out is a valid context. */
+ * grid is built here).  On success *out is a valid context.  nranks > 1: collective; each
+ * rank passes the particles of its slab (a particle up to one cell plane outside migrates,
+ * farther is SPH_ERR_INVALID_ARG) and cfg->n_total > 0. */
 sph_status sph_create(const sph_config* cfg, const sph_particles_in* in, sph_ctx** out);
 
-/* Replace every particle field (same n as at creation).  Resets div_prev validity unless
- * in->div_prev is given.  Asynchronous on the context stream. */
+/* Replace every particle field (one rank: same n as at creation; several ranks: the
+ * rank's slab, at most the capacity derived from n_total).  Resets div_prev validity
+ * unless in->div_prev is given.  Asynchronous on the context stream. */
 sph_status sph_set_particles(sph_ctx* ctx, const sph_particles_in* in);
 
 /* Wrap positions, bin particles into the cell grid (side >= gamma_k h_max (1+skin)) with a
@@ -179,8 +201,21 @@ sph_status sph_force(sph_ctx* ctx, float* dt_next);
 sph_status sph_kick_drift(sph_ctx* ctx, float dt_kick, float dt_drift);
 
 /* Copy one field out, in the caller's original order (by id), to host (on_device = 0)
- * or device memory.  dst must hold n x components elements of the field's type. */
+ * or device memory.  dst must hold n x components elements of the field's type (several
+ * ranks: the owned particles in local order, n = sph_local_count). */
 sph_status sph_get(sph_ctx* ctx, int field, void* dst, int on_device);
+
+/* Particles owned by this rank (= n for one rank); -1 for NULL. */
+int64_t sph_local_count(const sph_ctx* ctx);
+
+/* NCCL transport: write a fresh 128-byte ncclUniqueId to out128 (call on rank 0, then
+ * broadcast it to the other ranks out of band, e.g. torch.distributed). */
+sph_status sph_nccl_unique_id(void* out128);
+
+/* Loopback transport: a group of nranks in-process ranks; destroy after every context of
+ * the group is destroyed. */
+sph_status sph_loopback_create(int32_t nranks, void** group);
+sph_status sph_loopback_destroy(void* group);
 
 /* Counters of the last calls (pairs per loop, launches). */
 sph_status sph_get_counters(sph_ctx* ctx, sph_counters* out);

@@ -6,9 +6,14 @@ from .binding import (  # noqa: F401
     Config,
     Context,
     FIELDS,
+    LoopbackGroup,
     SphError,
     default_config,
     lib,
+    nccl_unique_id,
+    slab_lo,
+    slab_mask,
 )
 
-__all__ = ["Context", "Config", "FIELDS", "SphError", "default_config", "lib"]
+__all__ = ["Context", "Config", "FIELDS", "LoopbackGroup", "SphError", "default_config", "lib", "nccl_unique_id",
+           "slab_lo", "slab_mask"]

@@ -46,7 +46,10 @@ class Config(ctypes.Structure):
                 ("alpha_c_min", ctypes.c_float), ("alpha_c_max", ctypes.c_float), ("beta_c", ctypes.c_float),
                 ("c_cfl", ctypes.c_float), ("fh_mode", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("stream", ctypes.c_void_p), ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
-                ("tile_cells_z", ctypes.c_int32), ("predict_h", ctypes.c_int32)]
+                ("tile_cells_z", ctypes.c_int32), ("predict_h", ctypes.c_int32), ("transport", ctypes.c_int32),
+                ("nccl_uid", ctypes.c_void_p), ("loopback", ctypes.c_void_p)]
+
+SPH_TRANSPORT_NCCL, SPH_TRANSPORT_LOOPBACK = 0, 1
 
 
 class ParticlesIn(ctypes.Structure):
@@ -68,7 +71,8 @@ class Counters(ctypes.Structure):
 
 EXPORTS = ["sph_abi_version", "sph_config_default", "sph_create", "sph_set_particles", "sph_rebuild_cells",
            "sph_density", "sph_gradient", "sph_force", "sph_kick_drift", "sph_get", "sph_get_counters",
-           "sph_synchronize", "sph_last_error", "sph_destroy"]
+           "sph_synchronize", "sph_last_error", "sph_destroy", "sph_local_count", "sph_nccl_unique_id",
+           "sph_loopback_create", "sph_loopback_destroy"]
 
 _lib = None
 
@@ -97,24 +101,72 @@ def lib():
         L.sph_last_error.argtypes = [P]
         L.sph_last_error.restype = ctypes.c_char_p
         L.sph_destroy.argtypes = [P]
+        L.sph_local_count.argtypes = [P]
+        L.sph_local_count.restype = ctypes.c_int64
+        L.sph_nccl_unique_id.argtypes = [P]
+        L.sph_loopback_create.argtypes = [ctypes.c_int32, ctypes.POINTER(P)]
+        L.sph_loopback_destroy.argtypes = [P]
         for name in EXPORTS:
-            if name not in ("sph_abi_version", "sph_config_default", "sph_last_error"):
+            if name not in ("sph_abi_version", "sph_config_default", "sph_last_error", "sph_local_count"):
                 getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
 
 
-def default_config(box=(1.0, 1.0, 1.0), **kw) -> Config:
+def default_config(box=(1.0, 1.0, 1.0), keep=None, **kw) -> Config:
     c = Config()
     lib().sph_config_default(ctypes.byref(c))
     for a in range(3):
         c.box[a] = float(box[a])
     for k, v in kw.items():
-        if k == "stream":
-            c.stream = v
+        if k == "nccl_uid":
+            buf = ctypes.create_string_buffer(bytes(v), 128)
+            if keep is not None:
+                keep.append(buf)
+            c.nccl_uid = ctypes.cast(buf, ctypes.c_void_p)
+        elif k == "loopback":
+            c.loopback = v.handle if isinstance(v, LoopbackGroup) else v
+            c.transport = SPH_TRANSPORT_LOOPBACK
         else:
             setattr(c, k, v)
     return c
+
+
+def slab_lo(rank: int, nranks: int) -> int:
+    """First fixed-point x of rank's slab: floor(rank 2^32 / nranks) (include/sph.h)."""
+    return (rank << 32) // nranks
+
+
+def slab_mask(X, rank: int, nranks: int):
+    """Boolean mask of the particles (fixed-point X [n,3]) in rank's x-slab."""
+    x = np.asarray(X)[:, 0].astype(np.int64)
+    return (x >= slab_lo(rank, nranks)) & (x < slab_lo(rank + 1, nranks))
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 creates it, the other ranks receive it out of band)."""
+    buf = ctypes.create_string_buffer(128)
+    st = lib().sph_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p))
+    if st != SPH_OK:
+        raise SphError(st, "sph_nccl_unique_id failed (libnccl.so.2 not loadable?)")
+    return buf.raw
+
+
+class LoopbackGroup:
+    """In-process group of ranks for the loopback transport (tests on one GPU)."""
+
+    def __init__(self, nranks: int):
+        h = ctypes.c_void_p()
+        st = lib().sph_loopback_create(int(nranks), ctypes.byref(h))
+        if st != SPH_OK:
+            raise SphError(st, "sph_loopback_create failed")
+        self.handle = h.value
+        self.nranks = nranks
+
+    def close(self):
+        if self.handle:
+            lib().sph_loopback_destroy(self.handle)
+            self.handle = None
 
 
 def _is_torch(a):
@@ -155,8 +207,8 @@ class Context:
     def __init__(self, particles, box=None, **cfg):
         self._keep = []
         box = box if box is not None else particles.get("box", (1.0, 1.0, 1.0))
-        self.cfg = default_config(box=box, **cfg)
-        self.n = int(particles["X"].shape[0])
+        self._cfg_keep = []
+        self.cfg = default_config(box=box, keep=self._cfg_keep, **cfg)
         pin = particles_in(particles, self._keep)
         h = ctypes.c_void_p()
         st = lib().sph_create(ctypes.byref(self.cfg), ctypes.byref(pin), ctypes.byref(h))
@@ -164,6 +216,11 @@ class Context:
         if st != SPH_OK:
             raise SphError(st, "sph_create failed")
         self.h = h
+
+    @property
+    def n(self) -> int:
+        """Particles this context owns (all of them on one rank)."""
+        return int(lib().sph_local_count(self.h))
 
     def _check(self, st, what, allow=()):
         if st != SPH_OK and st not in allow:
@@ -196,7 +253,8 @@ class Context:
         self._check(lib().sph_kick_drift(self.h, float(dt_kick), float(dt_drift)), "sph_kick_drift")
 
     def get(self, field, out=None):
-        """Field in the caller's original particle order: numpy (host) or into a torch CUDA tensor."""
+        """Field in the caller's original particle order (several ranks: the owned particles in
+        local order, see "id"): numpy (host) or into a torch CUDA tensor."""
         enum, dt, comps = FIELDS[field]
         if out is not None and _is_torch(out):
             self._check(lib().sph_get(self.h, enum, out.data_ptr(), int(out.is_cuda)), "sph_get")

@@ -13,7 +13,7 @@ DEPS = SOURCES + sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + [
     os.path.join(os.path.dirname(HERE), "include", "sph.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc" if os.path.exists("/usr/local/cuda/bin/nvcc") else "nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-         "-shared", "-ftz=true", "-prec-div=false", "-prec-sqrt=false", "-Xptxas", "-v"]
+         "-shared", "-ftz=true", "-prec-div=false", "-prec-sqrt=false", "-Xptxas", "-v", "-ldl"]
 
 
 def stale() -> bool:

@@ -1,7 +1,15 @@
 // sph_api.cu -- the C-ABI of libsph (include/sph.h): context, cell binning (device radix
 // sort by cell key, SWIFT's cell tree + sort tasks replaced), orchestration
-// of the three interaction loops and the h iteration, kick/drift, read-back.
+// of the three interaction loops and the h iteration, kick/drift, read-back, and
+// the slab decomposition across ranks with its halo exchanges.
+//
+// Local particle layout (every array, cell order):  [left ghosts | owned | right ghosts].
+// One rank: no ghosts, periodic grid.  Several ranks: rank r owns the grid planes
+// [r nx/R, (r+1) nx/R) along x; the planes on either side are ghost planes received from the
+// neighbours (cell side >= (1+skin) max H, so one plane is the whole halo).  The local grid
+// has P + 2 planes along x (ghost, owned..., ghost) and is periodic in y and z.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -10,8 +18,10 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "../../include/sph.h"
+#include "sph_comm.cuh"
 #include "sph_internal.cuh"
 
 using namespace sph;
@@ -29,15 +39,30 @@ __global__ void k_hmax(int n, const uint4* __restrict__ xh, unsigned int* out) {
   if ((threadIdx.x & 31) == 0) atomicMax(out, m);  // positive f32 order as u32
 }
 
-__global__ void k_keys(int n, const uint4* __restrict__ xh, int nx, int ny, int nz, unsigned int* keys,
-                       unsigned int* perm) {
+// cell key of each particle in the local grid (DevGrid slab fields); a particle outside the
+// local planes gets the key ncells (sorted last) and is counted
+__global__ void k_keys(int n, const uint4* __restrict__ xh, DevGrid g, unsigned int* keys, unsigned int* perm,
+                       int* outside) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  const int nx = g.nx, ny = g.ny, nz = g.nz;
   uint4 x = xh[i];
-  unsigned int cx = (unsigned int)(((unsigned long long)x.x * (unsigned)nx) >> 32);
+  // offset from the slab start; the complement of the slab is split at its middle into
+  // "left of the slab" (negative) and "right of the slab"
+  long long d = (long long)(unsigned int)(x.x - g.x_lo);
+  if ((unsigned long long)d >= g.wfix + ((1ull << 32) - g.wfix) / 2) d -= (1ll << 32);
+  const long long q = d * (long long)g.nxo;
+  const long long w = (long long)g.wfix;
+  const long long pl = q >= 0 ? q / w : -((-q + w - 1) / w);  // floor
+  const long long cx = pl + g.ix_first;
   unsigned int cy = (unsigned int)(((unsigned long long)x.y * (unsigned)ny) >> 32);
   unsigned int cz = (unsigned int)(((unsigned long long)x.z * (unsigned)nz) >> 32);
-  keys[i] = (cx * ny + cy) * nz + cz;
+  if (cx < 0 || cx >= nx) {
+    keys[i] = (unsigned)nx * ny * nz;
+    atomicAdd(outside, 1);
+  } else {
+    keys[i] = ((unsigned)cx * ny + cy) * nz + cz;
+  }
   perm[i] = i;
 }
 
@@ -45,8 +70,8 @@ __global__ void k_keys(int n, const uint4* __restrict__ xh, int nx, int ny, int 
 __global__ void k_cell_start(int n, int ncells, const unsigned int* __restrict__ keys, int* cell_start) {
   int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p > n) return;
-  int lo = (p == 0) ? 0 : (int)keys[p - 1] + 1;
-  int hi = (p == n) ? ncells : (int)keys[p];
+  int lo = (p == 0) ? 0 : min((int)keys[p - 1] + 1, ncells + 1);
+  int hi = (p == n) ? ncells : min((int)keys[p], ncells);
   for (int c = lo; c <= hi; ++c) cell_start[c] = p;
 }
 
@@ -62,6 +87,11 @@ struct Persist {
   float4* acc;
 };
 
+Persist offset(const Persist& p, int o) {
+  return Persist{p.xh + o, p.vm + o, p.u + o, p.av + o, p.ac + o, p.dprev + o, p.uid + o, p.orig + o, p.acc + o};
+}
+
+// dst[p] = src[perm[p0 + p]] for p < n
 __global__ void k_permute(int n, const unsigned int* __restrict__ perm, Persist src, Persist dst) {
   int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
@@ -75,6 +105,69 @@ __global__ void k_permute(int n, const unsigned int* __restrict__ perm, Persist 
   dst.uid[p] = src.uid[i];
   dst.orig[p] = src.orig[i];
   dst.acc[p] = src.acc[i];
+}
+
+// one migrating particle, all persistent fields (80 bytes)
+struct MigRec {
+  uint4 xh;
+  float4 vm;
+  float4 acc;
+  float u, av, ac, dprev;
+  long long uid;
+  int orig, pad;
+};
+
+__global__ void k_pack_mig(int n, const unsigned int* __restrict__ perm, Persist src, MigRec* out) {
+  int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  int i = (int)perm[p];
+  MigRec r;
+  r.xh = src.xh[i];
+  r.vm = src.vm[i];
+  r.acc = src.acc[i];
+  r.u = src.u[i];
+  r.av = src.av[i];
+  r.ac = src.ac[i];
+  r.dprev = src.dprev[i];
+  r.uid = src.uid[i];
+  r.orig = src.orig[i];
+  r.pad = 0;
+  out[p] = r;
+}
+
+__global__ void k_unpack_mig(int n, const MigRec* __restrict__ in, Persist dst) {
+  int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  MigRec r = in[p];
+  dst.xh[p] = r.xh;
+  dst.vm[p] = r.vm;
+  dst.acc[p] = r.acc;
+  dst.u[p] = r.u;
+  dst.av[p] = r.av;
+  dst.ac[p] = r.ac;
+  dst.dprev[p] = r.dprev;
+  dst.uid[p] = r.uid;
+  dst.orig[p] = r.orig;
+}
+
+// per-cell particle counts of one x plane of the owned cell_start
+__global__ void k_plane_counts(int plane_cells, const int* __restrict__ cs, int first_cell, int* out) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= plane_cells) return;
+  out[k] = cs[first_cell + k + 1] - cs[first_cell + k];
+}
+
+// final cell_start of the [ghost | owned | ghost] layout: owned planes shifted by gL, ghost
+// planes from the exclusive scans of the received per-cell counts
+__global__ void k_final_cs(int ncells, int plane_cells, int P, int gL, int n_own, const int* __restrict__ scanL,
+                           const int* __restrict__ scanR, int n_loc, int* cs) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > ncells) return;
+  if (c == ncells) { cs[c] = n_loc; return; }
+  int plane = c / plane_cells, k = c - plane * plane_cells;
+  if (plane == 0) cs[c] = scanL[k];
+  else if (plane == P + 1) cs[c] = gL + n_own + scanR[k];
+  else cs[c] = cs[c] + gL;
 }
 
 // caller arrays (any order) -> persistent state (caller order; the next rebuild sorts it)
@@ -96,7 +189,7 @@ __global__ void k_ingest(int n, const uint32_t* __restrict__ X, const float* __r
 }
 
 // Kick v += a dt_k, u = max(0, u + du dt_k); drift x += v dt_d on the 2^-32 L
-// grid, rounded to nearest, wrapping mod 2^32 (R25).
+// grid, rounded to nearest, wrapping mod 2^32 (R25); h prediction (R29).
 __global__ void k_kick_drift(int n, uint4* xh, float4* vm, float* u, const float4* __restrict__ acc, float dtk,
                              float dtd, double fx, double fy, double fz, const float4* __restrict__ dvc) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -122,18 +215,18 @@ __global__ void k_kick_drift(int n, uint4* xh, float4* vm, float* u, const float
   }
 }
 
-// out[orig[p] * comps + c] = src[p * stride + off + c]   (32-bit or 64-bit elements)
+// out[(orig ? orig[p] : p) * comps + c] = src[p * stride + off + c]   (32-bit or 64-bit)
 __global__ void k_scatter32(int n, const uint32_t* __restrict__ src, int stride, int off, int comps,
                             const int32_t* __restrict__ orig, uint32_t* out) {
   int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
-  int o = orig[p];
+  int o = orig ? orig[p] : p;
   for (int c = 0; c < comps; ++c) out[(size_t)o * comps + c] = src[(size_t)p * stride + off + c];
 }
 __global__ void k_scatter64(int n, const uint64_t* __restrict__ src, const int32_t* __restrict__ orig, uint64_t* out) {
   int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
-  out[orig[p]] = src[p];
+  out[orig ? orig[p] : p] = src[p];
 }
 
 inline int nblk(long long n, int t) { return (int)((n + t - 1) / t); }
@@ -145,11 +238,19 @@ struct sph_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int device = 0;
-  int n = 0;
+  // particle layout: [gL ghosts | n_own owned | gR ghosts], capacity cap
+  int n_in = 0;               // particles given at creation / set_particles
+  int cap = 0;
+  int n_own = 0, gL = 0, gR = 0;
+  int nranks = 1, rank = 0;
+  bool slab = false;          // slab path (a transport was given; always when nranks > 1)
+  Comm* comm = nullptr;
+  bool ghost_v_stale = false;   // owners' v changed since the ghosts were received
+  int planeL = 0, planeR = 0;   // owned particles in the first / last owned plane (ghost sources)
   bool poisoned = false;
   bool stale = true;          // grid must be rebuilt before the next loop
   bool lists_stale = true;    // neighbour lists must be rebuilt before the next loop
-  size_t nbr_cap = 0;         // allocated list entries (n x lcap)
+  size_t nbr_cap = 0;         // allocated list entries (cap x lcap)
   int lcap = kLcapInit;
   bool dprev_valid = false;
   bool dvc_valid = false;     // dvc (div v) is from a density pass in the current particle order
@@ -172,6 +273,15 @@ struct sph_ctx {
   unsigned int* scratch_h = nullptr;
   void* out_tmp = nullptr;
   size_t out_tmp_bytes = 0;
+  // halo exchange buffers
+  MigRec *mig_send = nullptr, *mig_recv = nullptr;
+  size_t mig_cap = 0;
+  int *pc_send = nullptr, *pc_recv = nullptr, *pc_scan = nullptr;  // per-cell plane counts
+  size_t pc_cap = 0;
+  void* scan_tmp = nullptr;
+  size_t scan_tmp_bytes = 0;
+  long long* cnt_dev = nullptr;  // 4 message sizes
+  long long* cnt_h = nullptr;
   sph_counters counters{};
   long long launches = 0;
 };
@@ -195,13 +305,19 @@ sph_status fail(sph_ctx* c, sph_status st, const std::string& msg) {
     }                                                                                               \
   } while (0)
 
+#define CKC(expr)                                          \
+  do {                                                     \
+    std::string e_ = (expr);                               \
+    if (!e_.empty()) return fail(c, SPH_ERR_NCCL, e_);     \
+  } while (0)
+
 template <class T>
 cudaError_t dalloc(T** p, size_t count) {
   return cudaMalloc((void**)p, std::max<size_t>(count, 1) * sizeof(T));
 }
 
 sph_status alloc_state(sph_ctx* c) {
-  const size_t n = (size_t)c->n;
+  const size_t n = (size_t)c->cap;
   DevState& s = c->s;
   CK(dalloc(&s.xh, n)); CK(dalloc(&s.vm, n)); CK(dalloc(&s.u, n)); CK(dalloc(&s.av, n)); CK(dalloc(&s.ac, n));
   CK(dalloc(&s.dprev, n)); CK(dalloc(&s.uid, n)); CK(dalloc(&s.orig, n)); CK(dalloc(&s.acc, n));
@@ -220,6 +336,8 @@ sph_status alloc_state(sph_ctx* c) {
   CK(cudaMallocHost((void**)&c->ctr_h, sizeof(DevCounters)));
   CK(dalloc(&c->scratch, 16));
   CK(cudaMallocHost((void**)&c->scratch_h, 16 * sizeof(unsigned int)));
+  CK(dalloc(&c->cnt_dev, 8));
+  CK(cudaMallocHost((void**)&c->cnt_h, 8 * sizeof(long long)));
   size_t tmp = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tmp, c->keys, c->keys_alt, c->perm, c->perm_alt, (int)n, 0, 32);
   c->sort_tmp_bytes = tmp;
@@ -236,6 +354,12 @@ void set_persist(DevState& s, const Persist& p) {
   s.orig = p.orig; s.acc = p.acc;
 }
 
+void swap_persist(sph_ctx* c) {
+  Persist old = persist_of(c->s);
+  set_persist(c->s, c->alt);
+  c->alt = old;
+}
+
 sph_status validate_cfg(sph_ctx* c, const sph_config* cfg) {
   if (!cfg) return fail(c, SPH_ERR_INVALID_ARG, "cfg is NULL");
   if (cfg->struct_size != sizeof(sph_config)) return fail(c, SPH_ERR_INVALID_ARG, "sph_config.struct_size mismatch");
@@ -245,8 +369,15 @@ sph_status validate_cfg(sph_ctx* c, const sph_config* cfg) {
   if (!(cfg->eta > 0.f) || !(cfg->h_tol > 0.f) || cfg->h_max_iter < 0 || !(cfg->gamma_eos > 1.f) ||
       !(cfg->alpha_v_max > 0.f) || !(cfg->c_cfl > 0.f) || cfg->cell_skin < 0.f)
     return fail(c, SPH_ERR_INVALID_ARG, "invalid physics parameter");
-  if (cfg->nranks != 1 || cfg->rank != 0)
-    return fail(c, SPH_ERR_INVALID_ARG, "multi-rank contexts are not supported by this build (nranks must be 1)");
+  if (cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks)
+    return fail(c, SPH_ERR_INVALID_ARG, "rank/nranks out of range");
+  if (cfg->nranks > 1 || cfg->nccl_uid || (cfg->transport == SPH_TRANSPORT_LOOPBACK && cfg->loopback)) {
+    if (cfg->transport == SPH_TRANSPORT_NCCL && !cfg->nccl_uid)
+      return fail(c, SPH_ERR_INVALID_ARG, "NCCL transport needs nccl_uid (sph_nccl_unique_id on rank 0, broadcast)");
+    if (cfg->transport == SPH_TRANSPORT_LOOPBACK && !cfg->loopback)
+      return fail(c, SPH_ERR_INVALID_ARG, "loopback transport needs a group (sph_loopback_create)");
+    if (cfg->n_total <= 0) return fail(c, SPH_ERR_INVALID_ARG, "multi-rank contexts need n_total");
+  }
   return SPH_OK;
 }
 
@@ -270,17 +401,19 @@ void fill_phys(sph_ctx* c) {
 }
 
 sph_status ingest(sph_ctx* c, const sph_particles_in* in) {
-  if (!in || in->n != c->n) return fail(c, SPH_ERR_INVALID_ARG, "particle count mismatch");
-  if (!in->X || !in->v || !in->m || !in->u || !in->h) return fail(c, SPH_ERR_INVALID_ARG, "required particle array is NULL");
-  const size_t n = (size_t)c->n;
-  // stage host arrays through the (reused) output buffer region on the device
+  if (!in || !in->X || !in->v || !in->m || !in->u || !in->h)
+    return fail(c, SPH_ERR_INVALID_ARG, "required particle array is NULL");
+  if (in->n < 0 || (c->nranks == 1 && in->n != c->n_in) || in->n > c->cap)
+    return fail(c, SPH_ERR_INVALID_ARG, "particle count mismatch / above capacity");
+  const size_t n = (size_t)in->n;
   const uint32_t* X = in->X;
   const float *v = in->v, *m = in->m, *u = in->u, *h = in->h, *av = in->alpha_v, *ac = in->alpha_c,
               *dp = in->div_prev;
   const int64_t* id = in->id;
-  void* tmp = nullptr;
-  if (!in->on_device) {
-    size_t bytes = n * (12 + 12 + 4 * 3) + (av ? 4 * n : 0) + (ac ? 4 * n : 0) + (dp ? 4 * n : 0) + (id ? 8 * n : 0);
+  if (!in->on_device && n > 0) {
+    // stage host arrays through the (reused) output buffer region on the device
+    size_t bytes = n * (12 + 12 + 4 * 3) + (av ? 4 * n : 0) + (ac ? 4 * n : 0) + (dp ? 4 * n : 0) + (id ? 8 * n : 0) +
+                   9 * 16;
     if (c->out_tmp_bytes < bytes) {
       if (c->out_tmp) cudaFree(c->out_tmp);
       c->out_tmp = nullptr;
@@ -288,8 +421,7 @@ sph_status ingest(sph_ctx* c, const sph_particles_in* in) {
       CK(cudaMalloc(&c->out_tmp, bytes));
       c->out_tmp_bytes = bytes;
     }
-    tmp = c->out_tmp;
-    char* d = (char*)tmp;
+    char* d = (char*)c->out_tmp;
     auto up = [&](const void* src, size_t b) -> void* {
       void* dst = d;
       cudaMemcpyAsync(dst, src, b, cudaMemcpyHostToDevice, c->stream);
@@ -307,9 +439,13 @@ sph_status ingest(sph_ctx* c, const sph_particles_in* in) {
     if (id) id = (const int64_t*)up(in->id, 8 * n);
     CK(cudaGetLastError());
   }
-  k_ingest<<<nblk(n, 256), 256, 0, c->stream>>>((int)n, X, v, m, u, h, av, ac, dp, id, persist_of(c->s));
-  c->launches++;
-  CK(cudaGetLastError());
+  if (n > 0) {
+    k_ingest<<<nblk(n, 256), 256, 0, c->stream>>>((int)n, X, v, m, u, h, av, ac, dp, id, persist_of(c->s));
+    c->launches++;
+    CK(cudaGetLastError());
+  }
+  c->n_own = (int)n;
+  c->gL = c->gR = 0;
   c->dprev_valid = dp != nullptr;
   c->dvc_valid = false;
   c->stale = true;
@@ -334,70 +470,296 @@ float ulp_of(float x) {
   return std::ldexp(1.0f, e - 24);
 }
 
-// Choose the grid for the current h, sort, permute, and size the CTA tiles.
-sph_status rebuild(sph_ctx* c) {
-  const int n = c->n;
-  CK(cudaMemsetAsync(c->scratch, 0, 16 * sizeof(unsigned int), c->stream));
-  k_hmax<<<std::min(nblk(n, 256), 1184), 256, 0, c->stream>>>(n, c->s.xh, c->scratch);
+int left_of(const sph_ctx* c) { return (c->rank + c->nranks - 1) % c->nranks; }
+int right_of(const sph_ctx* c) { return (c->rank + 1) % c->nranks; }
+
+// Exchange two int64 sizes with the slab neighbours: sends (to_right, to_left), returns
+// (from_left, from_right).
+sph_status exchange_sizes(sph_ctx* c, long long to_right, long long to_left, long long& from_left,
+                          long long& from_right) {
+  c->cnt_h[0] = to_right;
+  c->cnt_h[1] = to_left;
+  CK(cudaMemcpyAsync(c->cnt_dev, c->cnt_h, 2 * sizeof(long long), cudaMemcpyHostToDevice, c->stream));
+  Xfer s[2] = {{right_of(c), c->cnt_dev, 8}, {left_of(c), c->cnt_dev + 1, 8}};
+  Xfer r[2] = {{left_of(c), c->cnt_dev + 2, 8}, {right_of(c), c->cnt_dev + 3, 8}};
+  CKC(c->comm->exchange(s, 2, r, 2, c->stream));
+  CK(cudaMemcpyAsync(c->cnt_h + 2, c->cnt_dev + 2, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  from_left = c->cnt_h[2];
+  from_right = c->cnt_h[3];
+  return SPH_OK;
+}
+
+template <class T>
+sph_status grow(sph_ctx* c, T** p, size_t& cap, size_t need) {
+  if (need <= cap) return SPH_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  cap = 0;
+  CK(dalloc(p, need));
+  cap = need;
+  return SPH_OK;
+}
+
+// Ghost halo exchange of one per-particle array (elem bytes each): the first owned plane goes
+// to the left neighbour (its right ghosts), the last owned plane to the right neighbour (its
+// left ghosts).  Ghost sets are fixed between rebuilds, so no sizes are exchanged.
+sph_status halo(sph_ctx* c, void* base, size_t elem) {
+  if (!c->slab) return SPH_OK;
+  char* b = static_cast<char*>(base);
+  Xfer s[2] = {{right_of(c), b + (size_t)(c->gL + c->n_own - c->planeR) * elem, (size_t)c->planeR * elem},
+               {left_of(c), b + (size_t)c->gL * elem, (size_t)c->planeL * elem}};
+  Xfer r[2] = {{left_of(c), b, (size_t)c->gL * elem},
+               {right_of(c), b + (size_t)(c->gL + c->n_own) * elem, (size_t)c->gR * elem}};
+  CKC(c->comm->exchange(s, 2, r, 2, c->stream));
+  return SPH_OK;
+}
+
+// global reduction of host scalars (no-op on one rank)
+sph_status allreduce(sph_ctx* c, double* v, int n, ReduceOp op) {
+  if (!c->slab) return SPH_OK;
+  CKC(c->comm->allreduce(v, n, op, c->stream));
+  return SPH_OK;
+}
+
+// Collective error agreement: every rank takes the same branch (a rank that fails alone
+// would leave its neighbours waiting in the next exchange).
+sph_status agree(sph_ctx* c, bool bad, sph_status code, const char* msg) {
+  if (c->slab) {
+    double v = bad ? 1.0 : 0.0;
+    sph_status st = allreduce(c, &v, 1, kMax);
+    if (st != SPH_OK) return st;
+    if (v > 0 && !bad) return fail(c, code, std::string("another rank failed: ") + msg);
+  }
+  return bad ? fail(c, code, msg) : SPH_OK;
+}
+
+// keys + radix sort of n particles starting at `base` (persistent arrays) into cell order;
+// fills c->perm_alt (sorted -> input index) and the owned-relative cell_start
+sph_status sort_cells(sph_ctx* c, int base, int n, int* outside) {
+  DevGrid& g = c->grid;
+  CK(cudaMemsetAsync(c->scratch + 2, 0, 4, c->stream));
+  if (n > 0) {
+    k_keys<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->s.xh + base, g, c->keys, c->perm, (int*)(c->scratch + 2));
+    c->launches++;
+    CK(cudaGetLastError());
+    int bits = 1;
+    while ((1LL << bits) <= g.ncells) ++bits;
+    size_t tmp = c->sort_tmp_bytes;
+    CK(cub::DeviceRadixSort::SortPairs(c->sort_tmp, tmp, c->keys, c->keys_alt, c->perm, c->perm_alt, n, 0, bits,
+                                       c->stream));
+    c->launches += 1 + (bits + 7) / 8;
+  }
+  k_cell_start<<<nblk(n + 1, 256), 256, 0, c->stream>>>(n, g.ncells, c->keys_alt, c->cell_start);
   c->launches++;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(c->scratch_h + 2, c->scratch + 2, 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  *outside = (int)c->scratch_h[2];
+  return SPH_OK;
+}
+
+sph_status read_cs(sph_ctx* c, int cell, int* v) {
+  CK(cudaMemcpyAsync(c->scratch + 4, c->cell_start + cell, 4, cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->scratch_h + 4, c->scratch + 4, 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  *v = (int)c->scratch_h[4];
+  return SPH_OK;
+}
+
+// Choose the grid for the current h, migrate (several ranks), sort, exchange ghost planes, and
+// size the CTA tiles.
+sph_status rebuild(sph_ctx* c) {
+  sph_status st;
+  // the owned particles sit at [base, base + n); the old ghosts are dropped (re-received below)
+  const int base = c->gL;
+  int n = c->n_own;
+  // global h_max -> cell side (identical on every rank)
+  CK(cudaMemsetAsync(c->scratch, 0, 4, c->stream));
+  if (n > 0) {
+    k_hmax<<<std::min(nblk(n, 256), 1184), 256, 0, c->stream>>>(n, c->s.xh + base, c->scratch);
+    c->launches++;
+  }
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(c->scratch_h, c->scratch, 4, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  float hmax;
-  std::memcpy(&hmax, c->scratch_h, 4);
+  float hmax_l;
+  std::memcpy(&hmax_l, c->scratch_h, 4);
+  double hm = hmax_l;
+  if ((st = allreduce(c, &hm, 1, kMax)) != SPH_OK) return st;
+  const float hmax = (float)hm;
   if (!(hmax > 0.f) || !std::isfinite(hmax)) return fail(c, SPH_ERR_INVALID_ARG, "smoothing lengths must be finite and > 0");
   const double Hs = (double)c->cfg.gamma_k * hmax * (1.0 + c->cfg.cell_skin);
   DevGrid& g = c->grid;
+  const int R = c->nranks;
+  const bool slab = c->slab;
+  // slab of this rank on the 2^-32 grid (fixed by position, independent of h)
+  const double two32 = std::ldexp(1.0, 32);
+  auto slab_lo = [&](int r) { return (unsigned long long)(((unsigned __int128)r << 32) / (unsigned)R); };
+  unsigned long long wmin = ~0ull;
+  for (int r = 0; r < R; ++r) wmin = std::min(wmin, slab_lo(r + 1) - slab_lo(r));
+  g.x_lo = (unsigned int)slab_lo(c->rank);
+  g.wfix = slab_lo(c->rank + 1) - slab_lo(c->rank);
   int nc[3];
   for (int a = 0; a < 3; ++a) {
-    double k = std::floor(c->cfg.box[a] / Hs);
-    if (k < 3) {
+    // planes along x per slab (same on every rank), cells along y, z
+    const double len = a == 0 ? c->cfg.box[0] * ((double)wmin / two32) : c->cfg.box[a];
+    double k = std::floor(len / Hs);
+    // R nxo >= 3: the ghost planes are distinct from each other and from the owned ones
+    const double kmin = (a == 0 && slab) ? (double)((3 + R - 1) / R) : 3;
+    if (k < kmin) {
       char b[256];
-      snprintf(b, sizeof b, "support radius %.6g leaves fewer than 3 cells along axis %d (box %.6g)", Hs, a, c->cfg.box[a]);
+      snprintf(b, sizeof b, "support radius %.6g leaves fewer than %g cells along axis %d (length %.6g over %d ranks)",
+               Hs, kmin, a, c->cfg.box[a], a == 0 ? R : 1);
       return fail(c, SPH_ERR_H_EXCEEDS_CELL, b);
     }
     nc[a] = (int)std::min(k, 1024.0);
   }
-  while ((long long)nc[0] * nc[1] * nc[2] > (1LL << 30)) { for (int a = 0; a < 3; ++a) nc[a] = std::max(3, nc[a] / 2); }
-  g.nx = nc[0]; g.ny = nc[1]; g.nz = nc[2];
+  auto ncells_of = [&]() { return (long long)(nc[0] + (slab ? 2 : 0)) * nc[1] * nc[2]; };
+  while (ncells_of() > (1LL << 30)) { for (int a = 0; a < 3; ++a) nc[a] = std::max(3, nc[a] / 2); }
+  g.nxo = nc[0];
+  if (slab) {
+    g.nx = nc[0] + 2;
+    g.periodic_x = 0;
+    g.ix_first = 1;
+  } else {
+    g.nx = nc[0];
+    g.periodic_x = 1;
+    g.ix_first = 0;
+  }
+  g.ny = nc[1];
+  g.nz = nc[2];
   g.ncells = g.nx * g.ny * g.nz;
   for (int a = 0; a < 3; ++a) {
     g.side[a] = (float)(c->cfg.box[a] / nc[a]);
     g.scale[a] = (float)(c->cfg.box[a] * std::ldexp(1.0, -32));
     g.dscale[a] = c->cfg.box[a] * std::ldexp(1.0, -32);
   }
-  g.side_min = std::min(g.side[0], std::min(g.side[1], g.side[2]));
-  // keys, sort, cell ranges, permutation
-  if (c->cell_cap < (size_t)g.ncells + 1) {
-    if (c->cell_start) cudaFree(c->cell_start);
-    c->cell_start = nullptr;
-    CK(dalloc(&c->cell_start, (size_t)g.ncells + 1));
-    c->cell_cap = (size_t)g.ncells + 1;
+  float side_x_min = g.side[0];
+  if (slab) {
+    g.side[0] = (float)(c->cfg.box[0] * ((double)g.wfix / two32) / nc[0]);          // this slab's planes
+    side_x_min = (float)(c->cfg.box[0] * ((double)wmin / two32) / nc[0]);           // thinnest planes of any slab
   }
-  k_keys<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->s.xh, g.nx, g.ny, g.nz, c->keys, c->perm);
-  c->launches++;
-  CK(cudaGetLastError());
-  int bits = 1;
-  while ((1LL << bits) < g.ncells) ++bits;
-  size_t tmp = c->sort_tmp_bytes;
-  CK(cub::DeviceRadixSort::SortPairs(c->sort_tmp, tmp, c->keys, c->keys_alt, c->perm, c->perm_alt, n, 0, bits,
-                                     c->stream));
-  c->launches += 1 + (bits + 7) / 8;
-  k_cell_start<<<nblk(n + 1, 256), 256, 0, c->stream>>>(n, g.ncells, c->keys_alt, c->cell_start);
-  c->launches++;
-  k_permute<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->perm_alt, persist_of(c->s), c->alt);
-  c->launches++;
-  CK(cudaGetLastError());
-  Persist old = persist_of(c->s);
-  set_persist(c->s, c->alt);
-  c->alt = old;
+  g.side_min = std::min(side_x_min, std::min(g.side[1], g.side[2]));
+  if ((st = grow(c, &c->cell_start, c->cell_cap, (size_t)g.ncells + 1)) != SPH_OK) return st;
+  const int pcells = g.ny * g.nz;
+  int outside = 0;
+  if ((st = sort_cells(c, base, n, &outside)) != SPH_OK) return st;
+  const Persist cur = offset(persist_of(c->s), base);
+  if (slab) {
+    // ---- migration (X6): particles now in a ghost plane belong to the neighbour
+    if ((st = agree(c, outside > 0, SPH_ERR_INVALID_ARG, "a particle moved more than one cell plane out of its slab")) != SPH_OK)
+      return st;
+    const int P = g.nxo;
+    int c1, cP1;
+    if ((st = read_cs(c, pcells, &c1)) != SPH_OK) return st;             // first owned plane
+    if ((st = read_cs(c, (P + 1) * pcells, &cP1)) != SPH_OK) return st;  // right ghost plane
+    const long long nL = c1, nR = n - cP1, nmid = cP1 - c1;
+    long long mL = 0, mR = 0;
+    if ((st = exchange_sizes(c, nR, nL, mL, mR)) != SPH_OK) return st;
+    const long long nnew = nmid + mL + mR;
+    if ((st = agree(c, nnew > c->cap, SPH_ERR_OOM, "slab holds more particles than the context capacity")) != SPH_OK)
+      return st;
+    if ((st = grow(c, &c->mig_send, c->mig_cap, (size_t)std::max(nL + nR, mL + mR) * 2 + 16)) != SPH_OK) return st;
+    if (c->mig_recv) cudaFree(c->mig_recv);
+    c->mig_recv = nullptr;
+    CK(dalloc(&c->mig_recv, c->mig_cap));
+    MigRec* sR = c->mig_send;
+    MigRec* sL = c->mig_send + nR;
+    if (nR > 0) k_pack_mig<<<nblk(nR, 256), 256, 0, c->stream>>>((int)nR, c->perm_alt + cP1, cur, sR);
+    if (nL > 0) k_pack_mig<<<nblk(nL, 256), 256, 0, c->stream>>>((int)nL, c->perm_alt, cur, sL);
+    c->launches += 2;
+    CK(cudaGetLastError());
+    Xfer s[2] = {{right_of(c), sR, (size_t)nR * sizeof(MigRec)}, {left_of(c), sL, (size_t)nL * sizeof(MigRec)}};
+    Xfer r[2] = {{left_of(c), c->mig_recv, (size_t)mL * sizeof(MigRec)},
+                 {right_of(c), c->mig_recv + mL, (size_t)mR * sizeof(MigRec)}};
+    CKC(c->comm->exchange(s, 2, r, 2, c->stream));
+    if (nmid > 0) {
+      k_permute<<<nblk(nmid, 256), 256, 0, c->stream>>>((int)nmid, c->perm_alt + c1, cur, c->alt);
+      c->launches++;
+    }
+    if (mL + mR > 0) {
+      k_unpack_mig<<<nblk(mL + mR, 256), 256, 0, c->stream>>>((int)(mL + mR), c->mig_recv, offset(c->alt, (int)nmid));
+      c->launches++;
+    }
+    CK(cudaGetLastError());
+    swap_persist(c);
+    n = (int)nnew;
+    c->n_own = n;
+    c->gL = c->gR = 0;
+    if ((st = sort_cells(c, 0, n, &outside)) != SPH_OK) return st;
+    if ((st = agree(c, outside > 0, SPH_ERR_INVALID_ARG, "migrated particle outside its slab")) != SPH_OK) return st;
+    // ---- ghost planes (X1): sizes and per-cell counts first
+    int cP;
+    if ((st = read_cs(c, P * pcells, &cP)) != SPH_OK) return st;  // start of the last owned plane
+    int c2;
+    if ((st = read_cs(c, 2 * pcells, &c2)) != SPH_OK) return st;  // end of the first owned plane
+    c->planeL = c2;        // first owned plane: [0, c2) of the sorted owned set
+    c->planeR = n - cP;    // last owned plane: [cP, n)
+    long long gL = 0, gR = 0;
+    if ((st = exchange_sizes(c, c->planeR, c->planeL, gL, gR)) != SPH_OK) return st;
+    if ((st = agree(c, gL + n + gR > c->cap, SPH_ERR_OOM, "owned + ghost particles exceed the context capacity")) !=
+        SPH_OK)
+      return st;
+    c->gL = (int)gL;
+    c->gR = (int)gR;
+    if ((st = grow(c, &c->pc_send, c->pc_cap, (size_t)4 * pcells + 64)) != SPH_OK) return st;
+    if (c->pc_recv) cudaFree(c->pc_recv);
+    if (c->pc_scan) cudaFree(c->pc_scan);
+    c->pc_recv = c->pc_scan = nullptr;
+    CK(dalloc(&c->pc_recv, c->pc_cap));
+    CK(dalloc(&c->pc_scan, c->pc_cap));
+    k_plane_counts<<<nblk(pcells, 256), 256, 0, c->stream>>>(pcells, c->cell_start, P * pcells, c->pc_send);
+    k_plane_counts<<<nblk(pcells, 256), 256, 0, c->stream>>>(pcells, c->cell_start, pcells, c->pc_send + pcells);
+    c->launches += 2;
+    CK(cudaGetLastError());
+    {
+      Xfer s2[2] = {{right_of(c), c->pc_send, (size_t)pcells * 4}, {left_of(c), c->pc_send + pcells, (size_t)pcells * 4}};
+      Xfer r2[2] = {{left_of(c), c->pc_recv, (size_t)pcells * 4}, {right_of(c), c->pc_recv + pcells, (size_t)pcells * 4}};
+      CKC(c->comm->exchange(s2, 2, r2, 2, c->stream));
+    }
+    size_t need = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, need, c->pc_recv, c->pc_scan, pcells, c->stream);
+    if (need > c->scan_tmp_bytes) {
+      if (c->scan_tmp) cudaFree(c->scan_tmp);
+      c->scan_tmp = nullptr;
+      CK(cudaMalloc(&c->scan_tmp, need));
+      c->scan_tmp_bytes = need;
+    }
+    CK(cub::DeviceScan::ExclusiveSum(c->scan_tmp, need, c->pc_recv, c->pc_scan, pcells, c->stream));
+    CK(cub::DeviceScan::ExclusiveSum(c->scan_tmp, need, c->pc_recv + pcells, c->pc_scan + pcells, pcells, c->stream));
+    c->launches += 2;
+    // owned particles into their final place, then the ghost payload straight into the ghost slots
+    if (n > 0) {
+      k_permute<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->perm_alt, persist_of(c->s), offset(c->alt, c->gL));
+      c->launches++;
+    }
+    k_final_cs<<<nblk(g.ncells + 1, 256), 256, 0, c->stream>>>(g.ncells, pcells, P, c->gL, n, c->pc_scan,
+                                                               c->pc_scan + pcells, c->gL + n + c->gR, c->cell_start);
+    c->launches++;
+    CK(cudaGetLastError());
+    swap_persist(c);
+    if ((st = halo(c, c->s.xh, sizeof(uint4))) != SPH_OK) return st;
+    if ((st = halo(c, c->s.vm, sizeof(float4))) != SPH_OK) return st;
+    c->ghost_v_stale = false;
+  } else {
+    if (outside) return fail(c, SPH_ERR_INVALID_ARG, "internal: particle outside the periodic grid");
+    if (n > 0) {
+      k_permute<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->perm_alt, cur, c->alt);
+      c->launches++;
+    }
+    CK(cudaGetLastError());
+    swap_persist(c);
+  }
   // CTA blocks: BX x BY grid columns x KZ cells (BX, BY = 2 when the grid allows: the tile of
   // (BX+2)(BY+2) columns is then ~2x smaller per owned particle than with single columns)
-  g.bx = g.nx >= 6 ? 2 : 1;
+  g.bx = (g.periodic_x ? g.nx >= 6 : g.nxo >= 2) ? 2 : 1;
   g.by = g.ny >= 6 ? 2 : 1;
-  g.nbx = (g.nx + g.bx - 1) / g.bx;
+  g.nbx = (g.nxo + g.bx - 1) / g.bx;
   g.nby = (g.ny + g.by - 1) / g.by;
-  const double occ = (double)n / g.ncells;
+  double ntot = n;
+  if ((st = allreduce(c, &ntot, 1, kSum)) != SPH_OK) return st;  // same KZ on every rank
+  const double occ = std::max(ntot, 1.0) / ((double)R * g.nxo * g.ny * g.nz);
   const int kz_max = std::min(kMaxTileCellsZ - 2, g.nz > 3 ? g.nz - 3 : 1);
   int KZ = (int)std::lround(kernel_threads() / std::max(occ * g.bx * g.by, 1e-3));
   if (c->cfg.tile_cells_z > 0) KZ = c->cfg.tile_cells_z;
@@ -411,7 +773,9 @@ sph_status rebuild(sph_ctx* c) {
     c->launches++;
     CK(cudaMemcpyAsync(c->scratch_h + 1, c->scratch + 1, 4, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    g.tcap = std::max(32, (int)c->scratch_h[1]);
+    double tmax = (double)c->scratch_h[1];
+    if ((st = allreduce(c, &tmax, 1, kMax)) != SPH_OK) return st;  // same tile capacity on every rank
+    g.tcap = std::max(32, (int)tmax);
     g.lcap = c->lcap;
     g.skin = c->cfg.cell_skin;
     const bool fits = force_smem(g) <= kSmemMax && lists_smem(g) <= kSmemMax && g.tcap < 65535;
@@ -428,14 +792,21 @@ sph_status rebuild(sph_ctx* c) {
   const float max_off = std::max(std::max((0.5f * g.bx + 1.0f) * g.side[0], (0.5f * g.by + 1.0f) * g.side[1]),
                                  (0.5f * g.KZ + 1.0f) * g.side[2]);
   g.eabs = 4.0f * ulp_of(max_off) * 2.0f;  // 8 x (ulp/2): two coordinates per difference, with margin
-  if ((size_t)g.nblocks > c->blk_cap) {
-    for (int k = 0; k < 2; ++k) {
-      if (c->blk[k]) cudaFree(c->blk[k]);
-      c->blk[k] = nullptr;
-      CK(dalloc(&c->blk[k], (size_t)g.nblocks));
-    }
-    c->blk_cap = (size_t)g.nblocks;
+  if (getenv("SPH_DEBUG")) {
+    std::vector<int> cs(g.ncells + 1);
+    cudaMemcpyAsync(cs.data(), c->cell_start, cs.size() * 4, cudaMemcpyDeviceToHost, c->stream);
+    cudaStreamSynchronize(c->stream);
+    int bad = 0;
+    for (int k = 0; k < g.ncells; ++k) bad += cs[k + 1] < cs[k];
+    fprintf(stderr, "[sph rank %d] nx %d ny %d nz %d nxo %d ix_first %d bx %d by %d nbx %d nby %d KZ %d nzb %d nblocks %d "
+            "tcap %d n_own %d gL %d gR %d planeL %d planeR %d cs0 %d csN %d nonmono %d x_lo %u wfix %llu\n",
+            c->rank, g.nx, g.ny, g.nz, g.nxo, g.ix_first, g.bx, g.by, g.nbx, g.nby, g.KZ, g.nzb, g.nblocks, g.tcap,
+            c->n_own, c->gL, c->gR, c->planeL, c->planeR, cs[0], cs[g.ncells], bad, g.x_lo, g.wfix);
   }
+  if ((st = grow(c, &c->blk[0], c->blk_cap, (size_t)g.nblocks)) != SPH_OK) return st;
+  if (c->blk[1]) cudaFree(c->blk[1]);
+  c->blk[1] = nullptr;
+  CK(dalloc(&c->blk[1], c->blk_cap));
   c->stale = false;
   c->lists_stale = true;
   c->dvc_valid = false;
@@ -453,16 +824,18 @@ sph_status build_lists(sph_ctx* c) {
     c->launches++;
     sph_status st = sync_ctr(c);
     if (st != SPH_OK) return st;
-    int over = c->ctr_h->list_overflow;
-    if (c->ctr_h->nonfinite == 2) return fail(c, SPH_ERR_CUDA, "internal: tile larger than its capacity");
-    if (over == 0) {
+    double over = c->ctr_h->list_overflow, bad = c->ctr_h->nonfinite == 2 ? 1 : 0;
+    double v[2] = {over, bad};
+    if ((st = allreduce(c, v, 2, kMax)) != SPH_OK) return st;
+    if (v[1] > 0) return fail(c, SPH_ERR_CUDA, "internal: tile larger than its capacity");
+    if (v[0] == 0) {
       c->lists_stale = false;
       return SPH_OK;
     }
-    int need = ((int)(over * 1.25) + 7) & ~7;
+    int need = ((int)(v[0] * 1.25) + 7) & ~7;
     if (need > 8192) return fail(c, SPH_ERR_H_EXCEEDS_CELL, "neighbour list longer than 8192 entries");
     c->lcap = need;
-    size_t want = (size_t)c->n * c->lcap;
+    size_t want = (size_t)c->cap * c->lcap;
     if (want > c->nbr_cap) {
       cudaFree(c->s.nbr);
       c->s.nbr = nullptr;
@@ -504,6 +877,25 @@ void sph_config_default(sph_config* cfg) {
   cfg->nranks = 1;
   cfg->tile_cells_z = 0;
   cfg->predict_h = 1;
+  cfg->transport = SPH_TRANSPORT_NCCL;
+  cfg->nccl_uid = nullptr;
+  cfg->loopback = nullptr;
+}
+
+sph_status sph_nccl_unique_id(void* out128) {
+  if (!out128) return SPH_ERR_INVALID_ARG;
+  return nccl_unique_id(out128).empty() ? SPH_OK : SPH_ERR_NCCL;
+}
+
+sph_status sph_loopback_create(int nranks, void** out) {
+  if (!out || nranks < 1) return SPH_ERR_INVALID_ARG;
+  *out = loopback_group_create(nranks);
+  return SPH_OK;
+}
+
+sph_status sph_loopback_destroy(void* group) {
+  if (group) loopback_group_destroy(group);
+  return SPH_OK;
 }
 
 sph_status sph_create(const sph_config* cfg, const sph_particles_in* in, sph_ctx** out) {
@@ -513,10 +905,23 @@ sph_status sph_create(const sph_config* cfg, const sph_particles_in* in, sph_ctx
   if (!c) return SPH_ERR_OOM;
   sph_status st = validate_cfg(c, cfg);
   if (st != SPH_OK) { delete c; return st; }
-  if (!in || in->n <= 0 || in->n > (int64_t)0x7fffffff) { delete c; return SPH_ERR_INVALID_ARG; }
+  if (!in || in->n < 0 || in->n > (int64_t)0x3fffffff || (cfg->nranks == 1 && in->n <= 0)) {
+    delete c;
+    return SPH_ERR_INVALID_ARG;
+  }
   c->cfg = *cfg;
-  c->n = (int)in->n;
+  c->n_in = (int)in->n;
+  c->nranks = cfg->nranks;
+  c->rank = cfg->rank;
   c->device = cfg->device;
+  c->slab = cfg->nranks > 1 || cfg->nccl_uid || (cfg->transport == SPH_TRANSPORT_LOOPBACK && cfg->loopback);
+  if (!c->slab) {
+    c->cap = c->n_in;
+  } else {
+    const double per = (double)cfg->n_total / c->nranks;
+    const double plane = std::pow((double)cfg->n_total, 2.0 / 3.0);
+    c->cap = (int)std::min<double>(0x3fffffff, 1.5 * std::max<double>(per, c->n_in) + 6.0 * plane + 65536);
+  }
   auto bail = [&](sph_status s) { sph_destroy(c); return s; };
   if (cudaSetDevice(c->device) != cudaSuccess) return bail(SPH_ERR_CUDA);
   if (cfg->stream) {
@@ -525,10 +930,23 @@ sph_status sph_create(const sph_config* cfg, const sph_particles_in* in, sph_ctx
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return bail(SPH_ERR_CUDA);
     c->own_stream = true;
   }
+  if (c->slab) {
+    std::string e;
+    c->comm = cfg->transport == SPH_TRANSPORT_LOOPBACK ? make_loopback_comm(cfg->loopback, c->rank, e)
+                                                       : make_nccl_comm(cfg->nccl_uid, c->rank, c->nranks, e);
+    if (!c->comm) {
+      fail(c, SPH_ERR_NCCL, e);
+      fprintf(stderr, "sph_create: %s\n", e.c_str());
+      return bail(SPH_ERR_NCCL);
+    }
+  }
   fill_phys(c);
   if ((st = alloc_state(c)) != SPH_OK) return bail(st);
   if ((st = ingest(c, in)) != SPH_OK) return bail(st);
-  if ((st = rebuild(c)) != SPH_OK) return bail(st);
+  if ((st = rebuild(c)) != SPH_OK) {
+    fprintf(stderr, "sph_create: %s\n", c->err.c_str());
+    return bail(st);
+  }
   *out = c;
   return SPH_OK;
 }
@@ -554,6 +972,8 @@ sph_status sph_density(sph_ctx* c, sph_density_stats* stats) {
   GUARD(c);
   sph_status st;
   if (c->stale && (st = rebuild(c)) != SPH_OK) return st;
+  if (c->ghost_v_stale && (st = halo(c, c->s.vm, sizeof(float4))) != SPH_OK) return st;
+  c->ghost_v_stale = false;
   if (c->lists_stale && (st = build_lists(c)) != SPH_OK) return st;
   int rebuilds = 0;
   long long pairs_all = 0;
@@ -572,9 +992,13 @@ sph_status sph_density(sph_ctx* c, sph_density_stats* stats) {
     c->launches++;
     ++passes_run;
     if ((st = sync_ctr(c)) != SPH_OK) return st;
-    if (c->ctr_h->nonfinite == 2) return fail(c, SPH_ERR_CUDA, "internal: tile larger than its capacity");
-    if (c->ctr_h->active_next == 0) break;
-    if (c->ctr_h->h_exceeds) {
+    // every rank takes the same branch: the flags are reduced over ranks
+    double fl[4] = {(double)c->ctr_h->active_next, (double)c->ctr_h->h_exceeds, (double)c->ctr_h->list_stale,
+                    c->ctr_h->nonfinite == 2 ? 1.0 : 0.0};
+    if ((st = allreduce(c, fl, 4, kMax)) != SPH_OK) return st;
+    if (fl[3] > 0) return fail(c, SPH_ERR_CUDA, "internal: tile larger than its capacity");
+    if (fl[0] == 0) break;
+    if (fl[1] > 0) {
       // an h grew past what the cell grid holds: rebin with the new h and restart the passes
       if (++rebuilds > 8) return fail(c, SPH_ERR_H_EXCEEDS_CELL, "h kept outgrowing the cell grid");
       pairs_all += (long long)c->ctr_h->pairs_all;
@@ -584,8 +1008,9 @@ sph_status sph_density(sph_ctx* c, sph_density_stats* stats) {
       pass = 0;
       continue;
     }
-    if (c->ctr_h->list_stale) {
-      // an h outgrew its list radius: rebuild the lists for the current h, keep iterating
+    if (fl[2] > 0) {
+      // an h outgrew its list radius: refresh the ghosts' h, rebuild the lists, keep iterating
+      if ((st = halo(c, c->s.xh, sizeof(uint4))) != SPH_OK) return st;
       if ((st = build_lists(c)) != SPH_OK) return st;
     }
     ++pass;
@@ -593,6 +1018,11 @@ sph_status sph_density(sph_ctx* c, sph_density_stats* stats) {
   final_pairs = c->ctr_h->pairs;
   pairs_all += (long long)c->ctr_h->pairs_all;
   unconverged = c->ctr_h->unconverged;
+  // ghosts need the final h and the gradient-loop record of their owners (X2)
+  if ((st = halo(c, c->s.xh, sizeof(uint4))) != SPH_OK) return st;
+  if ((st = halo(c, c->s.gq, sizeof(float4))) != SPH_OK) return st;
+  double un = unconverged;
+  if ((st = allreduce(c, &un, 1, kMax)) != SPH_OK) return st;
   c->counters.pairs_density = (int64_t)final_pairs;
   c->counters.pairs_h_iter = pairs_all;
   c->density_done = true;
@@ -606,7 +1036,7 @@ sph_status sph_density(sph_ctx* c, sph_density_stats* stats) {
     stats->pairs_density = (int64_t)final_pairs;
     stats->pairs_h_iter = pairs_all;
   }
-  if (unconverged > 0) {
+  if (un > 0) {
     char b[160];
     snprintf(b, sizeof b, "h iteration: %d particles not converged after %d Newton updates", unconverged,
              c->cfg.h_max_iter);
@@ -625,6 +1055,10 @@ sph_status sph_gradient(sph_ctx* c, float dt) {
   CK(launch_gradient(c->grid, c->phys, c->s, c->cell_start, dt, c->dprev_valid ? 0 : 1, c->ctr, c->stream));
   c->launches++;
   CK(cudaMemcpyAsync(&c->counters.pairs_gradient, &c->ctr->pairs, 8, cudaMemcpyDeviceToHost, c->stream));
+  // ghosts need their owners' force-loop records (X3)
+  if ((st = halo(c, c->s.fr1, sizeof(float4))) != SPH_OK) return st;
+  if ((st = halo(c, c->s.fr2, sizeof(float4))) != SPH_OK) return st;
+  if ((st = halo(c, c->s.fr3, sizeof(float))) != SPH_OK) return st;
   c->dprev_valid = true;
   c->gradient_done = true;
   return SPH_OK;
@@ -643,9 +1077,14 @@ sph_status sph_force(sph_ctx* c, float* dt_next) {
   c->counters.pairs_force = (int64_t)c->ctr_h->pairs;
   float dt;
   std::memcpy(&dt, &c->ctr_h->dt_bits, 4);
+  double red[2] = {std::isfinite(dt) ? (double)dt : 1e300, (double)c->ctr_h->nonfinite};
+  double mx = red[1];
+  if ((st = allreduce(c, red, 1, kMin)) != SPH_OK) return st;   // CFL dt: global minimum (X4)
+  if ((st = allreduce(c, &mx, 1, kMax)) != SPH_OK) return st;
+  dt = (float)red[0];
   if (dt_next) *dt_next = dt;
-  if (c->ctr_h->nonfinite == 2) return fail(c, SPH_ERR_CUDA, "internal: tile larger than its capacity");
-  if (c->ctr_h->nonfinite || !std::isfinite(dt)) return fail(c, SPH_ERR_NUMERIC, "non-finite acceleration, v_sig or dt (S:262)");
+  if (mx == 2) return fail(c, SPH_ERR_CUDA, "internal: tile larger than its capacity");
+  if (mx > 0 || !std::isfinite(dt) || red[0] >= 1e300) return fail(c, SPH_ERR_NUMERIC, "non-finite acceleration, v_sig or dt (S:262)");
   return SPH_OK;
 }
 
@@ -654,12 +1093,16 @@ sph_status sph_kick_drift(sph_ctx* c, float dt_kick, float dt_drift) {
   if (!std::isfinite(dt_kick) || !std::isfinite(dt_drift)) return fail(c, SPH_ERR_INVALID_ARG, "non-finite dt");
   const double f[3] = {std::ldexp(1.0, 32) / c->cfg.box[0], std::ldexp(1.0, 32) / c->cfg.box[1],
                        std::ldexp(1.0, 32) / c->cfg.box[2]};
-  const float4* dvc = (c->cfg.predict_h && c->dvc_valid) ? c->s.dvc : nullptr;
-  k_kick_drift<<<nblk(c->n, 256), 256, 0, c->stream>>>(c->n, c->s.xh, c->s.vm, c->s.u, c->s.acc, dt_kick, dt_drift, f[0],
-                                                     f[1], f[2], dvc);
-  c->launches++;
+  const int o = c->gL, n = c->n_own;
+  const float4* dvc = (c->cfg.predict_h && c->dvc_valid) ? c->s.dvc + o : nullptr;
+  if (n > 0) {
+    k_kick_drift<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->s.xh + o, c->s.vm + o, c->s.u + o, c->s.acc + o, dt_kick,
+                                                      dt_drift, f[0], f[1], f[2], dvc);
+    c->launches++;
+  }
   CK(cudaGetLastError());
   if (dt_drift != 0.f) c->stale = true;
+  else if (c->slab && dt_kick != 0.f) c->ghost_v_stale = true;
   c->density_done = c->gradient_done = false;
   return SPH_OK;
 }
@@ -700,7 +1143,13 @@ sph_status sph_get(sph_ctx* c, int field, void* dst, int on_device) {
     case SPH_F_ID: src = s.uid; wide = 1; break;
     default: return fail(c, SPH_ERR_INVALID_ARG, "unknown field");
   }
-  const size_t bytes = (size_t)c->n * comps * (wide ? 8 : 4);
+  // one rank: the caller's original order; several ranks: the owned particles in the local
+  // (cell) order -- SPH_F_ID maps them to the caller's ids
+  const int n = c->n_own;
+  const int32_t* orig = c->nranks == 1 ? s.orig : nullptr;
+  const size_t esz = wide ? 8 : 4;
+  const size_t bytes = (size_t)n * comps * esz;
+  if (n == 0) return SPH_OK;
   void* d = dst;
   if (!on_device) {
     if (c->out_tmp_bytes < bytes) {
@@ -713,10 +1162,10 @@ sph_status sph_get(sph_ctx* c, int field, void* dst, int on_device) {
     d = c->out_tmp;
   }
   if (wide)
-    k_scatter64<<<nblk(c->n, 256), 256, 0, c->stream>>>(c->n, (const uint64_t*)src, s.orig, (uint64_t*)d);
+    k_scatter64<<<nblk(n, 256), 256, 0, c->stream>>>(n, (const uint64_t*)src + c->gL, orig, (uint64_t*)d);
   else
-    k_scatter32<<<nblk(c->n, 256), 256, 0, c->stream>>>(c->n, (const uint32_t*)src, stride, off, comps, s.orig,
-                                                        (uint32_t*)d);
+    k_scatter32<<<nblk(n, 256), 256, 0, c->stream>>>(n, (const uint32_t*)src + (size_t)c->gL * stride, stride, off,
+                                                     comps, orig, (uint32_t*)d);
   c->launches++;
   CK(cudaGetLastError());
   if (!on_device) {
@@ -726,11 +1175,13 @@ sph_status sph_get(sph_ctx* c, int field, void* dst, int on_device) {
   return SPH_OK;
 }
 
+int64_t sph_local_count(const sph_ctx* c) { return c ? (int64_t)c->n_own : -1; }
+
 sph_status sph_get_counters(sph_ctx* c, sph_counters* out) {
   GUARD(c);
   if (!out) return SPH_ERR_INVALID_ARG;
   CK(cudaStreamSynchronize(c->stream));
-  c->counters.coincident = -1;  // not tracked by the GPU loops
+  c->counters.coincident = -1;  // not tracked by the GPU loops (R28)
   c->counters.kernel_launches = c->launches;
   *out = c->counters;
   return SPH_OK;
@@ -752,13 +1203,15 @@ sph_status sph_destroy(sph_ctx* c) {
   void* ptrs[] = {s.xh, s.vm, s.u, s.av, s.ac, s.dprev, s.uid, s.orig, s.acc, c->alt.xh, c->alt.vm, c->alt.u,
                   c->alt.av, c->alt.ac, c->alt.dprev, c->alt.uid, c->alt.orig, c->alt.acc, s.dens, s.dvc, s.count,
                   s.fin, s.gq, s.hlo, s.hhi, s.iters, s.active, s.grad, s.fr1, s.fr2, s.fr3, s.vsig, s.countf, s.nbr,
-                  s.ncount, s.hbuild,
-                  c->cell_start, c->keys, c->keys_alt, c->perm, c->perm_alt, c->sort_tmp, c->blk[0], c->blk[1],
-                  c->ctr, c->scratch, c->out_tmp};
+                  s.ncount, s.hbuild, c->cell_start, c->keys, c->keys_alt, c->perm, c->perm_alt, c->sort_tmp,
+                  c->blk[0], c->blk[1], c->ctr, c->scratch, c->out_tmp, c->mig_send, c->mig_recv, c->pc_send,
+                  c->pc_recv, c->pc_scan, c->scan_tmp, c->cnt_dev};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->ctr_h) cudaFreeHost(c->ctr_h);
   if (c->scratch_h) cudaFreeHost(c->scratch_h);
+  if (c->cnt_h) cudaFreeHost(c->cnt_h);
+  delete c->comm;
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return SPH_OK;

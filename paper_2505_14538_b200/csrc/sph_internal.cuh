@@ -37,6 +37,14 @@ struct DevGrid {
   float side[3];      // cell side per axis
   float side_min;
   float eabs;         // 8 x max rounding error of a tile coordinate (length units)
+  // Slab decomposition along x.  The rank owns x in [x_lo, x_lo + wfix) on the 2^-32 grid,
+  // cut into nxo planes; local plane of x = ix_first + floor((x - x_lo) nxo / wfix).
+  // One rank: x_lo = 0, wfix = 2^32, ix_first = 0, nxo = nx, periodic.  Several ranks:
+  // local planes = [ghost, nxo owned, ghost] (nx = nxo + 2), not periodic along x.
+  unsigned long long wfix;
+  unsigned int x_lo;
+  int periodic_x;
+  int ix_first, nxo;
 };
 
 struct DevPhys {

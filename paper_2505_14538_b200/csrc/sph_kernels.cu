@@ -59,29 +59,37 @@ __device__ void tile_setup(const DevGrid& g, int b, const int* __restrict__ cell
   const int zb = b % g.nzb;
   const int t2 = b / g.nzb;
   const int jy = t2 % g.nby, jx = t2 / g.nby;
-  T.ix0 = jx * g.bx;
+  T.ix0 = g.ix_first + jx * g.bx;
   T.iy0 = jy * g.by;
   T.z0 = zb * g.KZ;
   T.z1 = min(g.nz, T.z0 + g.KZ);
   T.nzt = T.z1 - T.z0 + 2;
   T.ntc = (g.bx + 2) * (g.by + 2);
   T.nct = T.ntc * T.nzt;
-  T.ref[0] = (uint32_t)((((unsigned long long)(2 * T.ix0 + g.bx)) << 31) / (unsigned long long)g.nx);
+  // block centre on the global 2^-32 grid (wraps mod 2^32 past the box edge)
+  T.ref[0] = g.x_lo + (uint32_t)(((unsigned long long)(2 * (T.ix0 - g.ix_first) + g.bx) * g.wfix) /
+                                 (2ull * (unsigned long long)g.nxo));
   T.ref[1] = (uint32_t)((((unsigned long long)(2 * T.iy0 + g.by)) << 31) / (unsigned long long)g.ny);
   T.ref[2] = (uint32_t)((((unsigned long long)(T.z0 + T.z1)) << 31) / (unsigned long long)g.nz);
   for (int t = threadIdx.x; t < T.nct; t += blockDim.x) {
     const int c = t / T.nzt, zz = t - c * T.nzt;
     int cx = T.ix0 + c / (g.by + 2) - 1, cy = T.iy0 + c % (g.by + 2) - 1, cz = T.z0 - 1 + zz;
-    cx += (cx < 0) ? g.nx : 0;
-    cx -= (cx >= g.nx) ? g.nx : 0;
+    bool empty = false;
+    if (g.periodic_x) {
+      cx += (cx < 0) ? g.nx : 0;
+      cx -= (cx >= g.nx) ? g.nx : 0;
+    } else {
+      empty = cx >= g.nx;  // past the right ghost plane (odd owned plane count)
+      cx = min(cx, g.nx - 1);
+    }
     cy += (cy < 0) ? g.ny : 0;
     cy -= (cy >= g.ny) ? g.ny : 0;
     cz += (cz < 0) ? g.nz : 0;
     cz -= (cz >= g.nz) ? g.nz : 0;
     const int cell = (cx * g.ny + cy) * g.nz + cz;
     const int gs = __ldg(cell_start + cell);
-    S.gst[t] = gs;
-    S.off[t + 1] = __ldg(cell_start + cell + 1) - gs;
+    S.gst[t] = empty ? 0 : gs;
+    S.off[t + 1] = empty ? 0 : __ldg(cell_start + cell + 1) - gs;
   }
   __syncthreads();
   if (threadIdx.x < 32) {
@@ -106,7 +114,7 @@ __device__ void tile_setup(const DevGrid& g, int b, const int* __restrict__ cell
     int k = 0, acc = 0;
     for (int ex = 0; ex < g.bx; ++ex)
       for (int ey = 0; ey < g.by; ++ey) {
-        if (T.ix0 + ex >= g.nx || T.iy0 + ey >= g.ny) continue;
+        if (T.ix0 + ex >= g.ix_first + g.nxo || T.iy0 + ey >= g.ny) continue;
         const int tc = (ex + 1) * (g.by + 2) + (ey + 1);
         S.tc[k] = tc;
         S.ib[k] = S.off[tc * T.nzt + 1];
@@ -126,8 +134,11 @@ __device__ void tile_setup(const DevGrid& g, int b, const int* __restrict__ cell
     for (int zz = 0; zz < T.nzt; ++zz) {
       const int c = col * T.nzt + zz;
       const int len = S.off[c + 1] - S.off[c];
-      if (zz > 0 && cur.y + cur.z == S.gst[c]) {
+      // empty cells never split a segment (at most 3 per column: the two z wraps)
+      if (zz > 0 && (len == 0 || cur.y + cur.z == S.gst[c])) {
         cur.z += len;
+      } else if (zz > 0 && cur.z == 0) {
+        cur = make_int4(S.off[c], S.gst[c], len, 0);
       } else {
         if (zz > 0) S.seg[col * 3 + n++] = cur;
         cur = make_int4(S.off[c], S.gst[c], len, 0);
@@ -858,11 +869,12 @@ __global__ void k_tile_sizes(DevGrid g, const int* __restrict__ cell_start, int*
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= g.nblocks) return;
   const int zb = b % g.nzb, t2 = b / g.nzb, jy = t2 % g.nby, jx = t2 / g.nby;
-  const int ix0 = jx * g.bx, iy0 = jy * g.by;
+  const int ix0 = g.ix_first + jx * g.bx, iy0 = jy * g.by;
   const int z0 = zb * g.KZ, z1 = min(g.nz, z0 + g.KZ);
   int tot = 0;
   for (int dx = -1; dx <= g.bx; ++dx)
     for (int dy = -1; dy <= g.by; ++dy) {
+      if (!g.periodic_x && ix0 + dx >= g.nx) continue;
       const int cx = (ix0 + dx + g.nx) % g.nx, cy = (iy0 + dy + g.ny) % g.ny;
       const int c0 = (cx * g.ny + cy) * g.nz;
       for (int z = z0 - 1; z <= z1; ++z) {

@@ -1146,7 +1146,7 @@ sph_status sph_get(sph_ctx* c, int field, void* dst, int on_device) {
   // one rank: the caller's original order; several ranks: the owned particles in the local
   // (cell) order -- SPH_F_ID maps them to the caller's ids
   const int n = c->n_own;
-  const int32_t* orig = c->nranks == 1 ? s.orig : nullptr;
+  const int32_t* orig = c->nranks == 1 ? s.orig + c->gL : nullptr;
   const size_t esz = wide ? 8 : 4;
   const size_t bytes = (size_t)n * comps * esz;
   if (n == 0) return SPH_OK;

@@ -9,9 +9,10 @@ directed pairs) and the time per hydro step.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C4] [--impl ours|reference]
 
 Under torchrun (N > 1) the job is ONE simulation decomposed into x-slabs, one per GPU
-(include/sph.h "Several ranks"): N copies of the workload side by side along x in a box
-(N Lx, Ly, Lz), rank r owning copy r's slab, exchanging ghost planes, migrants and the
-global h_max / dt over NCCL every step ("scaling": "weak": the per-GPU work is fixed).
+(include/sph.h "Several ranks"), exchanging ghost planes, migrants and the global h_max / dt
+over NCCL every step.  Default --scaling strong: the workload itself (BASELINE.json C4:
+"256^3 on 1 B200, then 2/4/8 with halo exchange") split into N slabs.  --scaling weak: N
+copies of the workload side by side along x in a box (N Lx, Ly, Lz), one per rank.
 The timed region is bracketed by a barrier and torch.cuda.synchronize(), and the max over
 ranks is reported.  Rank 0 prints ONE JSON line.
 """
@@ -59,6 +60,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample", default="G64", choices=sorted(WORKLOADS))
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     return ap.parse_args()
 
 
@@ -111,15 +113,26 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def rank_workload(key, rank, world):
-    """Rank's share of the weak-scaling job: copy `rank` of the workload, placed at
-    x in [rank Lx, (rank + 1) Lx) of a box (world Lx, Ly, Lz).  Fixed point: X' =
-    floor((X + rank 2^32) / world), i.e. inside rank's slab [floor(r 2^32 / N),
-    floor((r+1) 2^32 / N)) up to one grid unit (which the library migrates)."""
+def rank_workload(key, rank, world, scaling="strong"):
+    """Rank's share of the job.  strong: the particles of the workload inside rank's
+    x-slab [floor(r 2^32 / N), floor((r+1) 2^32 / N)) (ids = global indices).  weak: copy
+    `rank` of the workload, placed at x in [rank Lx, (rank + 1) Lx) of a box (world Lx, Ly,
+    Lz): X' = floor((X + rank 2^32) / world), inside rank's slab up to one grid unit (which
+    the library migrates)."""
+    from paper_2505_14538_b200.binding import slab_mask
+
     name, gen = WORKLOADS[key]
     p = gen()
     if world == 1:
         return name, p
+    n = p["X"].shape[0]
+    if scaling == "strong":
+        mk = slab_mask(p["X"], rank, world)
+        q = {k: (np.ascontiguousarray(v[mk]) if isinstance(v, np.ndarray) and v.shape[:1] == (n,) else v)
+             for k, v in p.items()}
+        q["id"] = np.flatnonzero(mk).astype(np.int64)
+        q["n_total"] = n
+        return name, q
     q = dict(p)
     X = p["X"].astype(np.uint64)
     X[:, 0] = (X[:, 0] + (np.uint64(rank) << np.uint64(32))) // np.uint64(world)
@@ -127,6 +140,7 @@ def rank_workload(key, rank, world):
     box = np.asarray(p["box"], dtype=np.float64).copy()
     box[0] *= world
     q["box"] = box
+    q["n_total"] = n * world
     return f"{name}_x{world}", q
 
 
@@ -203,13 +217,14 @@ def run_ours(args, world, rank, local):
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    name, p = rank_workload(args.workload, rank, world)
+    name, p = rank_workload(args.workload, rank, world, args.scaling)
     n = p["X"].shape[0]
+    n_total = int(p.get("n_total", n))
     stream = torch.cuda.Stream(device=dev)
     multi = {}
     if world > 1:
         uid = share_uid(nccl_unique_id() if rank == 0 else b"", rank, device=dev)
-        multi = dict(rank=rank, nranks=world, n_total=n * world, nccl_uid=uid)
+        multi = dict(rank=rank, nranks=world, n_total=n_total, nccl_uid=uid)
     ctx = Context(p, stream=stream.cuda_stream, device=local, **multi)
     dt = 1e-4
 
@@ -220,19 +235,14 @@ def run_ours(args, world, rank, local):
 
     def step(log=None):
         nonlocal dt
-        marks = [ev()]
         ctx.kick_drift(0.5 * dt, dt)
         st = ctx.density()
-        marks.append(ev())
         ctx.gradient(dt)
-        marks.append(ev())
         dt_next = ctx.force()
-        marks.append(ev())
         ctx.kick_drift(0.5 * dt, 0.0)
-        marks.append(ev())
         c = ctx.counters()
         if log is not None:
-            log.append((marks, st, c))
+            log.append((st, c))
         dt = float(min(dt_next, 2 * dt))
         return st, c
 
@@ -248,6 +258,8 @@ def run_ours(args, world, rank, local):
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = ctx.counters()["kernel_launches"]
+    ctx.timings(reset=True)
+    ctx.set_timing(True)
     log = []
     with Clocks(local) as clk:
         t0 = ev()
@@ -263,13 +275,12 @@ def run_ours(args, world, rank, local):
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    ph = np.zeros(4)
+    tm = ctx.timings(reset=True)  # per-kernel device time (CUDA events on the context stream)
+    ctx.set_timing(False)
     inter = 0
     pd = pg = pf = ph_iter = 0
     iters = []
-    for marks, st, c in log:
-        for k in range(4):
-            ph[k] += marks[k].elapsed_time(marks[k + 1])
+    for st, c in log:
         pd += c["pairs_density"]
         pg += c["pairs_gradient"]
         pf += c["pairs_force"]
@@ -286,18 +297,19 @@ def run_ours(args, world, rank, local):
         dist.all_reduce(t)  # interactions of all ranks (units all ranks processed)
         inter_all = float(t.item())
     value = inter_all / (ms * 1e-3)
-    t_force = ph[2] / K * 1e-3
-    t_dens = ph[0] / K * 1e-3
-    t_grad = ph[1] / K * 1e-3
-    flops_force = FLOPS_FORCE_UNORDERED * (pf / K) / 2.0
-    flops_dens = FLOPS_DENSITY * (ph_iter / K)
-    flops_grad = FLOPS_GRADIENT * (pg / K)
-    kernels = {
-        "density": {"ms": 1e3 * t_dens, "tflops": flops_dens / t_dens / 1e12, "share": ph[0] / ms},
-        "gradient": {"ms": 1e3 * t_grad, "tflops": flops_grad / t_grad / 1e12, "share": ph[1] / ms},
-        "force": {"ms": 1e3 * t_force, "tflops": flops_force / t_force / 1e12, "share": ph[2] / ms},
-    }
-    dom = max(("density", "gradient", "force"), key=lambda k: kernels[k]["ms"])
+    # algorithmic FP32 work of the three loops; density counts every pass
+    flops = {"density": FLOPS_DENSITY * ph_iter, "gradient": FLOPS_GRADIENT * pg,
+             "force": FLOPS_FORCE_UNORDERED * pf / 2.0}
+    kernels = {}
+    for name_k, (kms, kn) in tm.items():
+        if kn == 0:
+            continue
+        e = {"ms_per_step": kms / K, "launches_per_step": kn / K, "ms_per_launch": kms / kn, "share": kms / ms}
+        if name_k in flops:
+            e["tflops"] = flops[name_k] / (kms * 1e-3) / 1e12
+        kernels[name_k] = e
+    # roofline: the loop kernel (§8 rows a2/a5/a7) with the largest share of the step
+    dom = max(("density", "gradient", "force"), key=lambda k: kernels.get(k, {}).get("ms_per_step", 0.0))
     traffic = None
     prof = os.path.join(ROOT, "profiles", "r01", "ncu_summary.json")
     if os.path.exists(prof):
@@ -326,9 +338,10 @@ def run_ours(args, world, rank, local):
         line = {
             "metric": "SPH pair interactions/sec (density+gradient+force) and time per hydro step",
             "value": value, "unit": "interactions/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
-            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling if world > 1 else "weak",
+            "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": name, "particles": n * world,
+            "config": {"workload": name, "particles": n_total,
                        "parallelism": f"x-slabs{world} (NCCL halo exchange)" if world > 1 else "1gpu",
                        "step": "KDK: kick/drift, rebuild, density+h-iteration, gradient, force+dt, kick",
                        "l2": "inputs larger than L2 (n x ~300 B >> 126 MB)",

@@ -131,6 +131,23 @@ typedef struct {
   int64_t kernel_launches; /* kernels launched by this context since creation              */
 } sph_counters;
 
+/* Device-time phases (sph_get_timings). */
+typedef enum {
+  SPH_T_REBUILD = 0,    /* binning: sort, permute, migration + ghost exchange (a1, X1, X6)     */
+  SPH_T_LISTS = 1,      /* neighbour-list build (one per rebuild or list refresh)              */
+  SPH_T_DENSITY = 2,    /* one density pass each (a2-a4)                                        */
+  SPH_T_GRADIENT = 3,   /* a5-a6                                                                */
+  SPH_T_FORCE = 4,      /* a7-a8                                                                */
+  SPH_T_KICK_DRIFT = 5, /* a9                                                                   */
+  SPH_T_EXCHANGE = 6,   /* halo exchanges outside the rebuild (X2, X3)                          */
+  SPH_T_COUNT = 8
+} sph_phase;
+
+typedef struct {
+  double ms[SPH_T_COUNT];     /* summed device time per phase (CUDA events on the context stream) */
+  int64_t count[SPH_T_COUNT]; /* timed launches / scopes per phase                               */
+} sph_timings;
+
 /* Fields for sph_get (element type; components). */
 typedef enum {
   SPH_F_X = 0,        /* uint32 x3  fixed-point position                                   */
@@ -219,6 +236,14 @@ sph_status sph_loopback_destroy(void* group);
 
 /* Counters of the last calls (pairs per loop, launches). */
 sph_status sph_get_counters(sph_ctx* ctx, sph_counters* out);
+
+/* Per-phase device timing with CUDA events recorded around every launch on the context
+ * stream (off by default; a few microseconds per launch when on). */
+sph_status sph_set_timing(sph_ctx* ctx, int on);
+
+/* Synchronise the stream and return the summed phase times since the last reset; reset != 0
+ * zeroes them afterwards. */
+sph_status sph_get_timings(sph_ctx* ctx, sph_timings* out, int reset);
 
 /* Block until all work enqueued by the context has finished. */
 sph_status sph_synchronize(sph_ctx* ctx);

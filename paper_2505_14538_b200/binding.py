@@ -63,6 +63,13 @@ class DensityStats(ctypes.Structure):
                 ("reserved", ctypes.c_int32), ("pairs_density", ctypes.c_int64), ("pairs_h_iter", ctypes.c_int64)]
 
 
+PHASES = ["rebuild", "lists", "density", "gradient", "force", "kick_drift", "exchange"]
+
+
+class Timings(ctypes.Structure):
+    _fields_ = [("ms", ctypes.c_double * 8), ("count", ctypes.c_int64 * 8)]
+
+
 class Counters(ctypes.Structure):
     _fields_ = [("pairs_density", ctypes.c_int64), ("pairs_gradient", ctypes.c_int64),
                 ("pairs_force", ctypes.c_int64), ("pairs_h_iter", ctypes.c_int64), ("coincident", ctypes.c_int64),
@@ -72,7 +79,7 @@ class Counters(ctypes.Structure):
 EXPORTS = ["sph_abi_version", "sph_config_default", "sph_create", "sph_set_particles", "sph_rebuild_cells",
            "sph_density", "sph_gradient", "sph_force", "sph_kick_drift", "sph_get", "sph_get_counters",
            "sph_synchronize", "sph_last_error", "sph_destroy", "sph_local_count", "sph_nccl_unique_id",
-           "sph_loopback_create", "sph_loopback_destroy"]
+           "sph_loopback_create", "sph_loopback_destroy", "sph_set_timing", "sph_get_timings"]
 
 _lib = None
 
@@ -101,6 +108,8 @@ def lib():
         L.sph_last_error.argtypes = [P]
         L.sph_last_error.restype = ctypes.c_char_p
         L.sph_destroy.argtypes = [P]
+        L.sph_set_timing.argtypes = [P, ctypes.c_int]
+        L.sph_get_timings.argtypes = [P, ctypes.POINTER(Timings), ctypes.c_int]
         L.sph_local_count.argtypes = [P]
         L.sph_local_count.restype = ctypes.c_int64
         L.sph_nccl_unique_id.argtypes = [P]
@@ -267,6 +276,15 @@ class Context:
         c = Counters()
         self._check(lib().sph_get_counters(self.h, ctypes.byref(c)), "sph_get_counters")
         return {f: getattr(c, f) for f, _ in Counters._fields_}
+
+    def set_timing(self, on=True):
+        self._check(lib().sph_set_timing(self.h, int(on)), "sph_set_timing")
+
+    def timings(self, reset=True):
+        """{phase: (summed device ms, launches)} since the last reset (synchronises)."""
+        t = Timings()
+        self._check(lib().sph_get_timings(self.h, ctypes.byref(t), int(reset)), "sph_get_timings")
+        return {name: (t.ms[k], t.count[k]) for k, name in enumerate(PHASES)}
 
     def synchronize(self):
         self._check(lib().sph_synchronize(self.h), "sph_synchronize")

@@ -284,9 +284,47 @@ struct sph_ctx {
   long long* cnt_h = nullptr;
   sph_counters counters{};
   long long launches = 0;
+  // per-phase device timing (sph_set_timing): event pairs resolved by sph_get_timings
+  bool timing = false;
+  struct TEv { int kind; cudaEvent_t a, b; };
+  std::vector<TEv> tev;
+  std::vector<cudaEvent_t> pool;
+  double tms[SPH_T_COUNT] = {};
+  long long tcnt[SPH_T_COUNT] = {};
 };
 
 namespace {
+
+cudaEvent_t ev_get(sph_ctx* c) {
+  if (!c->pool.empty()) {
+    cudaEvent_t e = c->pool.back();
+    c->pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Scope of one timed phase on the context stream (no-op unless timing is on).
+struct Timed {
+  sph_ctx* c;
+  int kind;
+  cudaEvent_t a = nullptr;
+  Timed(sph_ctx* ctx, int k) : c(ctx), kind(k) {
+    if (c->timing) {
+      a = ev_get(c);
+      cudaEventRecord(a, c->stream);
+    }
+  }
+  ~Timed() {
+    if (a) {
+      cudaEvent_t b = ev_get(c);
+      cudaEventRecord(b, c->stream);
+      c->tev.push_back({kind, a, b});
+    }
+  }
+};
 
 sph_status fail(sph_ctx* c, sph_status st, const std::string& msg) {
   if (c) {
@@ -506,6 +544,7 @@ sph_status grow(sph_ctx* c, T** p, size_t& cap, size_t need) {
 // left ghosts).  Ghost sets are fixed between rebuilds, so no sizes are exchanged.
 sph_status halo(sph_ctx* c, void* base, size_t elem) {
   if (!c->slab) return SPH_OK;
+  Timed tm(c, SPH_T_EXCHANGE);
   char* b = static_cast<char*>(base);
   Xfer s[2] = {{right_of(c), b + (size_t)(c->gL + c->n_own - c->planeR) * elem, (size_t)c->planeR * elem},
                {left_of(c), b + (size_t)c->gL * elem, (size_t)c->planeL * elem}};
@@ -569,7 +608,13 @@ sph_status read_cs(sph_ctx* c, int cell, int* v) {
 
 // Choose the grid for the current h, migrate (several ranks), sort, exchange ghost planes, and
 // size the CTA tiles.
+sph_status rebuild_impl(sph_ctx* c);
 sph_status rebuild(sph_ctx* c) {
+  Timed tm(c, SPH_T_REBUILD);
+  return rebuild_impl(c);
+}
+
+sph_status rebuild_impl(sph_ctx* c) {
   sph_status st;
   // the owned particles sit at [base, base + n); the old ghosts are dropped (re-received below)
   const int base = c->gL;
@@ -820,7 +865,10 @@ sph_status build_lists(sph_ctx* c) {
     CK(cudaMemsetAsync(&c->ctr->list_overflow, 0, sizeof(int), c->stream));
     CK(cudaMemsetAsync(&c->ctr->nonfinite, 0, sizeof(int), c->stream));
     if (lists_smem(c->grid) > kSmemMax) return fail(c, SPH_ERR_H_EXCEEDS_CELL, "neighbour lists exceed shared memory");
-    CK(launch_lists(c->grid, c->phys, c->s, c->cell_start, c->ctr, c->stream));
+    {
+      Timed tm(c, SPH_T_LISTS);
+      CK(launch_lists(c->grid, c->phys, c->s, c->cell_start, c->ctr, c->stream));
+    }
     c->launches++;
     sph_status st = sync_ctr(c);
     if (st != SPH_OK) return st;
@@ -987,8 +1035,11 @@ sph_status sph_density(sph_ctx* c, sph_density_stats* stats) {
     CK(cudaMemsetAsync(bout, 0, (size_t)c->grid.nblocks, c->stream));
     CK(cudaMemsetAsync(&c->ctr->active_next, 0, 3 * sizeof(int), c->stream));  // active_next, list_stale, overflow
     CK(cudaMemsetAsync(&c->ctr->h_exceeds, 0, sizeof(int), c->stream));
-    CK(launch_density(c->grid, c->phys, c->s, c->cell_start, pass, bin, bout, 1.f + c->cfg.cell_skin, c->ctr,
-                      c->stream));
+    {
+      Timed tm(c, SPH_T_DENSITY);
+      CK(launch_density(c->grid, c->phys, c->s, c->cell_start, pass, bin, bout, 1.f + c->cfg.cell_skin, c->ctr,
+                        c->stream));
+    }
     c->launches++;
     ++passes_run;
     if ((st = sync_ctr(c)) != SPH_OK) return st;
@@ -1052,7 +1103,10 @@ sph_status sph_gradient(sph_ctx* c, float dt) {
   if (!(dt > 0.f) || !std::isfinite(dt)) return fail(c, SPH_ERR_INVALID_ARG, "sph_gradient: dt must be > 0 (S:246)");
   sph_status st;
   if ((st = reset_ctr(c)) != SPH_OK) return st;
-  CK(launch_gradient(c->grid, c->phys, c->s, c->cell_start, dt, c->dprev_valid ? 0 : 1, c->ctr, c->stream));
+  {
+    Timed tm(c, SPH_T_GRADIENT);
+    CK(launch_gradient(c->grid, c->phys, c->s, c->cell_start, dt, c->dprev_valid ? 0 : 1, c->ctr, c->stream));
+  }
   c->launches++;
   CK(cudaMemcpyAsync(&c->counters.pairs_gradient, &c->ctr->pairs, 8, cudaMemcpyDeviceToHost, c->stream));
   // ghosts need their owners' force-loop records (X3)
@@ -1071,7 +1125,10 @@ sph_status sph_force(sph_ctx* c, float* dt_next) {
   if ((st = reset_ctr(c)) != SPH_OK) return st;
   unsigned int inf_bits = 0x7f800000u;
   CK(cudaMemcpyAsync(&c->ctr->dt_bits, &inf_bits, 4, cudaMemcpyHostToDevice, c->stream));
-  CK(launch_force(c->grid, c->phys, c->s, c->cell_start, c->ctr, c->stream));
+  {
+    Timed tm(c, SPH_T_FORCE);
+    CK(launch_force(c->grid, c->phys, c->s, c->cell_start, c->ctr, c->stream));
+  }
   c->launches++;
   if ((st = sync_ctr(c)) != SPH_OK) return st;
   c->counters.pairs_force = (int64_t)c->ctr_h->pairs;
@@ -1096,6 +1153,7 @@ sph_status sph_kick_drift(sph_ctx* c, float dt_kick, float dt_drift) {
   const int o = c->gL, n = c->n_own;
   const float4* dvc = (c->cfg.predict_h && c->dvc_valid) ? c->s.dvc + o : nullptr;
   if (n > 0) {
+    Timed tm(c, SPH_T_KICK_DRIFT);
     k_kick_drift<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->s.xh + o, c->s.vm + o, c->s.u + o, c->s.acc + o, dt_kick,
                                                       dt_drift, f[0], f[1], f[2], dvc);
     c->launches++;
@@ -1193,6 +1251,39 @@ sph_status sph_synchronize(sph_ctx* c) {
   return SPH_OK;
 }
 
+sph_status sph_set_timing(sph_ctx* c, int on) {
+  GUARD(c);
+  c->timing = on != 0;
+  return SPH_OK;
+}
+
+sph_status sph_get_timings(sph_ctx* c, sph_timings* out, int reset) {
+  GUARD(c);
+  CK(cudaStreamSynchronize(c->stream));
+  for (const auto& t : c->tev) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, t.a, t.b));
+    c->tms[t.kind] += ms;
+    c->tcnt[t.kind] += 1;
+    c->pool.push_back(t.a);
+    c->pool.push_back(t.b);
+  }
+  c->tev.clear();
+  if (out) {
+    for (int k = 0; k < SPH_T_COUNT; ++k) {
+      out->ms[k] = c->tms[k];
+      out->count[k] = c->tcnt[k];
+    }
+  }
+  if (reset) {
+    for (int k = 0; k < SPH_T_COUNT; ++k) {
+      c->tms[k] = 0.0;
+      c->tcnt[k] = 0;
+    }
+  }
+  return SPH_OK;
+}
+
 const char* sph_last_error(const sph_ctx* c) { return c ? c->err.c_str() : "context is NULL"; }
 
 sph_status sph_destroy(sph_ctx* c) {
@@ -1211,6 +1302,11 @@ sph_status sph_destroy(sph_ctx* c) {
   if (c->ctr_h) cudaFreeHost(c->ctr_h);
   if (c->scratch_h) cudaFreeHost(c->scratch_h);
   if (c->cnt_h) cudaFreeHost(c->cnt_h);
+  for (const auto& t : c->tev) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
   delete c->comm;
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;

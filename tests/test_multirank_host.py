@@ -30,8 +30,10 @@ def _worker(rank, world, port, out):
 
     uid = bytes(range(128)) if rank == 0 else b""
     got = bench.share_uid(uid, rank)
-    name, p = bench.rank_workload("G64", rank, world)
+    name, p = bench.rank_workload("G64", rank, world, "weak")
     np.save(os.path.join(out, f"X{rank}.npy"), p["X"])
+    _, q = bench.rank_workload("G64", rank, world, "strong")
+    np.save(os.path.join(out, f"S{rank}.npy"), q["id"])
     with open(os.path.join(out, f"uid{rank}.bin"), "wb") as fh:
         fh.write(got)
     with open(os.path.join(out, f"box{rank}.txt"), "w") as fh:
@@ -63,3 +65,9 @@ def test_uid_broadcast_and_slab_split(tmp_path):
         assert x.min() >= lo and x.max() <= hi
         expect = (base["X"][:, 0].astype(np.int64) + (r << 32)) // world
         assert np.array_equal(x, expect)
+    # strong scaling: the ranks' slabs partition the workload, each particle in its slab
+    ids = np.concatenate([np.load(tmp_path / f"S{r}.npy") for r in range(world)])
+    assert np.array_equal(np.sort(ids), np.arange(n))
+    for r in range(world):
+        x = base["X"][np.load(tmp_path / f"S{r}.npy"), 0].astype(np.int64)
+        assert x.min() >= slab_lo(r, world) and x.max() < slab_lo(r + 1, world)

@@ -56,22 +56,26 @@ __global__ void k_keys(int n, const uint4* __restrict__ xh, DevGrid g, unsigned 
   const long long pl = q >= 0 ? q / w : -((-q + w - 1) / w);  // floor
   const long long cx = pl + g.ix_first;
   unsigned int cy = (unsigned int)(((unsigned long long)x.y * (unsigned)ny) >> 32);
-  unsigned int cz = (unsigned int)(((unsigned long long)x.z * (unsigned)nz) >> 32);
+  const unsigned long long zq = (unsigned long long)x.z * (unsigned)nz;
+  const unsigned int cz = (unsigned int)(zq >> 32);
+  // low bits: the top zbits of the position inside the cell along z, so each cell's
+  // particles come out sorted by z up to one bucket (the list kernel's z windows)
+  const unsigned int zf = g.zbits ? (unsigned int)zq >> (32 - g.zbits) : 0u;
   if (cx < 0 || cx >= nx) {
-    keys[i] = (unsigned)nx * ny * nz;
+    keys[i] = ((unsigned)nx * ny * nz) << g.zbits;
     atomicAdd(outside, 1);
   } else {
-    keys[i] = ((unsigned)cx * ny + cy) * nz + cz;
+    keys[i] = ((((unsigned)cx * ny + cy) * nz + cz) << g.zbits) | zf;
   }
   perm[i] = i;
 }
 
-// cell_start[c] = first sorted index with key >= c, for c in [0, ncells]
-__global__ void k_cell_start(int n, int ncells, const unsigned int* __restrict__ keys, int* cell_start) {
+// cell_start[c] = first sorted index with cell(key) >= c, for c in [0, ncells]
+__global__ void k_cell_start(int n, int ncells, int zbits, const unsigned int* __restrict__ keys, int* cell_start) {
   int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p > n) return;
-  int lo = (p == 0) ? 0 : min((int)keys[p - 1] + 1, ncells + 1);
-  int hi = (p == n) ? ncells : min((int)keys[p], ncells);
+  int lo = (p == 0) ? 0 : min((int)(keys[p - 1] >> zbits) + 1, ncells + 1);
+  int hi = (p == n) ? ncells : min((int)(keys[p] >> zbits), ncells);
   for (int c = lo; c <= hi; ++c) cell_start[c] = p;
 }
 
@@ -584,12 +588,13 @@ sph_status sort_cells(sph_ctx* c, int base, int n, int* outside) {
     CK(cudaGetLastError());
     int bits = 1;
     while ((1LL << bits) <= g.ncells) ++bits;
+    bits += g.zbits;
     size_t tmp = c->sort_tmp_bytes;
     CK(cub::DeviceRadixSort::SortPairs(c->sort_tmp, tmp, c->keys, c->keys_alt, c->perm, c->perm_alt, n, 0, bits,
                                        c->stream));
     c->launches += 1 + (bits + 7) / 8;
   }
-  k_cell_start<<<nblk(n + 1, 256), 256, 0, c->stream>>>(n, g.ncells, c->keys_alt, c->cell_start);
+  k_cell_start<<<nblk(n + 1, 256), 256, 0, c->stream>>>(n, g.ncells, g.zbits, c->keys_alt, c->cell_start);
   c->launches++;
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(c->scratch_h + 2, c->scratch + 2, 4, cudaMemcpyDeviceToHost, c->stream));
@@ -675,6 +680,11 @@ sph_status rebuild_impl(sph_ctx* c) {
   g.ny = nc[1];
   g.nz = nc[2];
   g.ncells = g.nx * g.ny * g.nz;
+  {
+    int cbits = 1;
+    while ((1LL << cbits) <= g.ncells) ++cbits;
+    g.zbits = std::max(0, std::min(12, 32 - cbits));
+  }
   for (int a = 0; a < 3; ++a) {
     g.side[a] = (float)(c->cfg.box[a] / nc[a]);
     g.scale[a] = (float)(c->cfg.box[a] * std::ldexp(1.0, -32));
@@ -686,6 +696,7 @@ sph_status rebuild_impl(sph_ctx* c) {
     side_x_min = (float)(c->cfg.box[0] * ((double)wmin / two32) / nc[0]);           // thinnest planes of any slab
   }
   g.side_min = std::min(side_x_min, std::min(g.side[1], g.side[2]));
+  g.zbucket = (float)(c->cfg.box[2] / nc[2] * std::ldexp(1.0, -g.zbits));
   if ((st = grow(c, &c->cell_start, c->cell_cap, (size_t)g.ncells + 1)) != SPH_OK) return st;
   const int pcells = g.ny * g.nz;
   int outside = 0;

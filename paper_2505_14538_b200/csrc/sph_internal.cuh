@@ -37,6 +37,8 @@ struct DevGrid {
   float side[3];      // cell side per axis
   float side_min;
   float eabs;         // 8 x max rounding error of a tile coordinate (length units)
+  int zbits;          // particles of a cell sorted by the top zbits of their z inside the cell
+  float zbucket;      // side_z 2^-zbits: z order inside a cell holds up to this
   // Slab decomposition along x.  The rank owns x in [x_lo, x_lo + wfix) on the 2^-32 grid,
   // cut into nxo planes; local plane of x = ix_first + floor((x - x_lo) nxo / wfix).
   // One rank: x_lo = 0, wfix = 2^32, ix_first = 0, nxo = nx, periodic.  Several ranks:

@@ -8,10 +8,10 @@
 // cp.async (LDGSTS) and converted from fixed point to f32 offsets from the block centre.
 //
 // Neighbour lists.  k_lists tests, once per cell rebuild (and again only if an h outgrows
-// its list radius), every candidate of the union of the 27-cell stencils of a warp's 32
-// particles (warp-uniform, broadcast shared-memory reads) and stores, per particle, the
-// tile slots j with r_ij < (1 + skin) max(H_i, H_j) (self included) as uint16, padded to a
-// multiple of 8 with a sentinel slot.  The density passes, the gradient loop and the force
+// its list radius), each particle's candidates in its 3 x 3 neighbour columns inside a z
+// window of +-R (cells are z-sorted by the binning key, so a binary search finds the
+// window) and stores, per particle, the tile slots j with r_ij < (1 + skin) max(H_i, H_j)
+// (self included) as uint16, padded to a multiple of 8 with a sentinel slot.  The density passes, the gradient loop and the force
 // loop then run the pair arithmetic over these lists only: every lane works on a real (or
 // skin) neighbour, no candidate is re-tested (the paper's pair tasks test all particle
 // pairs of two cells).  Skin entries, the sentinel and the self pair contribute
@@ -176,11 +176,11 @@ __device__ __forceinline__ int slot_global(const BlockShared& S, int nct, int t)
 
 __device__ __forceinline__ void cp_async16(const void* smem_dst, const void* gmem_src) {
   const unsigned int d = (unsigned int)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src));
 }
 __device__ __forceinline__ void cp_async4(const void* smem_dst, const void* gmem_src) {
   const unsigned int d = (unsigned int)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(gmem_src) : "memory");
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(gmem_src));
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
@@ -190,9 +190,11 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 __device__ __forceinline__ void stage_records(const BlockShared& S, int nseg, int nrec16, const float4* const* src16,
                                               const int* o16, const float* src4, int o4) {
   float* sm1 = reinterpret_cast<float*>(smem4);
-  for (int k = 0; k < nseg; ++k) {
+  // one warp per segment (segments are ~1-3 cells long): no block-wide pass over all of them
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int k = warp; k < nseg; k += nw) {
     const int4 sg = S.seg[k];
-    for (int t = threadIdx.x; t < sg.z; t += blockDim.x) {
+    for (int t = lane; t < sg.z; t += 32) {
       for (int r = 0; r < nrec16; ++r) cp_async16(&smem4[o16[r] + sg.x + t], src16[r] + sg.y + t);
       if (src4) cp_async4(&sm1[o4 + sg.x + t], src4 + sg.y + t);
     }
@@ -294,34 +296,43 @@ __device__ __forceinline__ void for_list(const uint16_t* __restrict__ list, int 
 // r_ij^2 < ((1 + skin) gamma_k max(h_i, h_j))^2, in tile order, padded to 8 with the
 // sentinel slot tcap.  Superset of every loop's neighbour set while each h stays within
 // (1 + skin) of its value here (checked by the density epilogue).
-// Warps take chunks of 32 particles in cell-major order over the block (z level, then i
-// column), so a chunk spans ~2 cells of one z level; its candidates are the union of the
-// 3 x 3 column neighbourhoods of its i columns over its z cells +-1.  The tile is staged as
-// SoA (x[], y[], z[], H2[]) so one LDS.64 per coordinate brings two consecutive candidates
-// and the distance test runs in packed f32x2 (FADD2 / FMUL2 / FFMA2, the particle's
-// coordinate as a broadcast operand).  Hits are appended to a 16-row per-lane buffer in
-// shared memory and leave for global memory 8 at a time (16-byte stores).
+// One lane per particle i, each walking its OWN candidates: in each of the 3 x 3 tile
+// columns around i's column, only the slots with |z_j - z_i| <= R (R = the largest list
+// radius in the tile), found by binary search -- each cell's particles are sorted by z up
+// to one bucket of zbucket (the z bits of the sort key), so the window is exact up to that
+// bucket, which is added to R.  This tests ~2R/(3 side) of the 27-cell candidates.
+// The tile is staged pair-interleaved, P[8p .. 8p+7] = (x_2p, x_2p+1, y_2p, y_2p+1, z_2p,
+// z_2p+1, H2_2p, H2_2p+1), so one lane tests two consecutive candidates with two LDS.128
+// and packed f32x2 arithmetic (FADD2 / FMUL2 / FFMA2).  Hits go to a per-lane column of a
+// per-warp buffer in shared memory and leave for global memory 8 at a time (16-byte stores).
 constexpr int kMaxICells = kMaxICols * (kMaxTileCellsZ - 2);
+constexpr int kListRows = 26;  // buffer rows per lane: 7 left + 2 single tests + 16 per group
+__device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;\n" ::"r"(a), "h"((unsigned short)v) : "memory");
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];\n" : "=h"(v) : "r"(a) : "memory");
+  return v;
+}
 __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, DevState s,
                                                        const int* __restrict__ cell_start,
                                                        DevCounters* __restrict__ ctr) {
   __shared__ int s_cp[kMaxICells + 1];  // prefix of particle counts over the block's i cells
   __shared__ int s_ct[kMaxICells];      // tile start of each i cell
   __shared__ int s_cg[kMaxICells];      // global start of each i cell
-  __shared__ unsigned s_nbm[kMaxICols]; // tile columns of the 3 x 3 neighbourhood of each i column
+  __shared__ unsigned int s_hmax;       // largest h of the tile (f32 bits)
+  if (threadIdx.x == 0) s_hmax = 0u;
   TILE_PROLOGUE();
   {
     const float4* src[1] = {reinterpret_cast<const float4*>(s.xh)};
     const int o16[1] = {0};
     stage_records(S, nseg, 1, src, o16, nullptr, 0);
   }
-  // AoS raw records -> pair-interleaved SoA in place: for the slot pair (2p, 2p+1),
-  // P[8p .. 8p+7] = (x_2p, x_2p+1, y_2p, y_2p+1, z_2p, z_2p+1, H2_2p, H2_2p+1) occupies the same
-  // 32 bytes as the two raw records, so one thread converts one pair; two LDS.128 then bring
-  // two candidates laid out for f32x2 arithmetic.  The pad slot past the tile end never hits.
   const int NP = (SP + 1) >> 1;  // slot pairs
   float* P = reinterpret_cast<float*>(smem4);
   const float Hfac = (1.f + g.skin) * ph.gamma_k;
+  unsigned int hm = 0u;
   for (int pp = threadIdx.x; pp < NP; pp += blockDim.x) {
     float4 q[2];
 #pragma unroll
@@ -332,12 +343,16 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
         const uint4 x = reinterpret_cast<const uint4*>(smem4)[t];
         const float3 r = rel_pos(g, T, x);
         const float Hs = Hfac * __uint_as_float(x.w);
+        hm = max(hm, x.w);
         q[u] = make_float4(r.x, r.y, r.z, Hs * Hs);
       }
     }
+    // (the raw records of this pair are read before the pair's 32 bytes are rewritten)
     reinterpret_cast<float4*>(P)[2 * pp] = make_float4(q[0].x, q[1].x, q[0].y, q[1].y);
     reinterpret_cast<float4*>(P)[2 * pp + 1] = make_float4(q[0].z, q[1].z, q[0].w, q[1].w);
   }
+  hm = warp_max((int)hm);
+  if ((threadIdx.x & 31) == 0) atomicMax(&s_hmax, hm);
   int ncolI = 0;
 #pragma unroll
   for (int r = 0; r < kMaxICols; ++r) ncolI += (r == 0 || S.tc[r] != 0) ? 1 : 0;
@@ -354,17 +369,20 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
     }
     s_cp[nicell] = acc;
   }
-  if (threadIdx.x < kMaxICols) {
-    const int tc = S.tc[threadIdx.x];
-    unsigned m = 0;
-    for (int dx = -1; dx <= 1; ++dx)
-      for (int dy = -1; dy <= 1; ++dy) m |= 1u << (tc + dx * (g.by + 2) + dy);
-    s_nbm[threadIdx.x] = threadIdx.x < ncolI ? m : 0u;
-  }
   __syncthreads();
+  // window half-width: the largest list radius of any pair in the tile, plus the z-order
+  // bucket and the coordinate rounding bound
+  const float zpad = Hfac * __uint_as_float(s_hmax) + g.zbucket + g.eabs;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // 24-row x 32-lane uint16 buffer per warp after the pair array (row stride 64 bytes)
-  uint16_t* buf = reinterpret_cast<uint16_t*>(P + NP * 8) + warp * 24 * 32 + lane;
+  const uint32_t sP = (uint32_t)__cvta_generic_to_shared(P);
+  const float inv_side = 1.f / g.side[2];
+  auto zbound = [&](int cz) {  // tile-relative z of the lower boundary of grid cell cz (may wrap)
+    const int c = cz < 0 ? cz + g.nz : cz;
+    const uint32_t b = (uint32_t)((((unsigned long long)c) << 32) / (unsigned long long)g.nz);
+    return (float)(int)(b - T.ref[2]) * g.scale[2];
+  };
+  // kListRows x 32-lane uint16 buffer per warp after the pair array (row stride 64 bytes)
+  const uint32_t buf = sP + (uint32_t)NP * 32u + (uint32_t)(warp * kListRows * 32 + lane) * 2u;
   const int ni = s_cp[nicell];
   int over = 0;
   for (int c = warp; c * 32 < ni; c += kNW) {
@@ -379,84 +397,97 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
     const int zz = lo / ncolI + 1, col = lo - (zz - 1) * ncolI;
     const int ti = s_ct[lo] + (kk - s_cp[lo]);
     const int gi = s_cg[lo] + (kk - s_cp[lo]);
-    const int zf = warp_min(valid ? zz : 1 << 30), zl = warp_max(valid ? zz : -1);
-    unsigned tmask = __reduce_or_sync(kFull, valid ? s_nbm[col] : 0u);
     const float* pi = P + (ti >> 1) * 8 + (ti & 1);
-    const float xi = valid ? pi[0] : kFar;  // invalid lanes: no hits
-    const float2 nX = make_float2(-xi, -xi), nY = make_float2(-pi[2], -pi[2]), nZ = make_float2(-pi[4], -pi[4]);
+    const float2 nX = make_float2(-pi[0], -pi[0]), nY = make_float2(-pi[2], -pi[2]);
+    const float zi = pi[4];
+    const float2 nZ = make_float2(-zi, -zi);
     const float Hi2 = pi[6];
+    const int tc = S.tc[col];
+    const float zc = zbound(T.z0 + zz - 2);  // bottom of tile cell zz - 1
     uint4* dst = reinterpret_cast<uint4*>(s.nbr + (size_t)gi * g.lcap);
-    uint16_t* w = buf;  // next free buffer row
-    int flushed = 0;    // entries already in global memory
-    auto test_one = [&](int t) {  // a single candidate (range ends)
+    uint32_t w = buf;  // next free buffer row
+    int flushed = 0;   // entries already in global memory
+    auto hit = [&](bool h, int t) {
+      if (h) {
+        sts_u16(w, (uint32_t)t);
+        w += 64u;
+      }
+    };
+    auto test_one = [&](int t) {  // a single candidate (window ends)
       const float* q = P + (t >> 1) * 8 + (t & 1);
       const float dx = q[0] + nX.x, dy = q[2] + nY.x, dz = q[4] + nZ.x;
       const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-      if (r2 < Hi2 || r2 < q[6]) { *w = (uint16_t)t; w += 32; }
+      hit(r2 < Hi2 || r2 < q[6], t);
     };
-    while (tmask) {
-      const int tcol = __ffs(tmask) - 1;
-      tmask &= tmask - 1;
-      int a = S.off[tcol * T.nzt + zf - 1];
-      int e = S.off[tcol * T.nzt + zl + 2];
-      if (a & 1) test_one(a++);
-      if ((e - a) & 1) test_one(--e);
-      for (int p0 = a >> 1; p0 < (e >> 1); p0 += 8) {
-        const int pn = min(e >> 1, p0 + 8);
-#pragma unroll 4
-        for (int pp = p0; pp < pn; ++pp) {
-          const float4 A = reinterpret_cast<const float4*>(P)[2 * pp];
-          const float4 B = reinterpret_cast<const float4*>(P)[2 * pp + 1];
-          const float2 dx = __fadd2_rn(make_float2(A.x, A.y), nX);
-          const float2 dy = __fadd2_rn(make_float2(A.z, A.w), nY);
-          const float2 dz = __fadd2_rn(make_float2(B.x, B.y), nZ);
-          float2 r2 = __fmul2_rn(dx, dx);
-          r2 = __ffma2_rn(dy, dy, r2);
-          r2 = __ffma2_rn(dz, dz, r2);
-          if (r2.x < fmaxf(Hi2, B.z)) { *w = (uint16_t)(2 * pp); w += 32; }
-          if (r2.y < fmaxf(Hi2, B.w)) { *w = (uint16_t)(2 * pp + 1); w += 32; }
+    auto drain = [&]() {  // buffered entries -> global memory, 8 at a time
+      while (w - buf >= 8u * 64u) {
+        if (flushed + 8 <= g.lcap) {
+          uint4 v;
+          v.x = lds_u16(buf + 0 * 64) | (lds_u16(buf + 1 * 64) << 16);
+          v.y = lds_u16(buf + 2 * 64) | (lds_u16(buf + 3 * 64) << 16);
+          v.z = lds_u16(buf + 4 * 64) | (lds_u16(buf + 5 * 64) << 16);
+          v.w = lds_u16(buf + 6 * 64) | (lds_u16(buf + 7 * 64) << 16);
+          dst[flushed >> 3] = v;
         }
-        // at most 7 + 16 buffered entries: drain 8 at a time
-        while (w - buf >= 8 * 32) {
-          if (flushed + 8 <= g.lcap) {
-            uint4 v;
-            v.x = (uint32_t)buf[0 * 32] | ((uint32_t)buf[1 * 32] << 16);
-            v.y = (uint32_t)buf[2 * 32] | ((uint32_t)buf[3 * 32] << 16);
-            v.z = (uint32_t)buf[4 * 32] | ((uint32_t)buf[5 * 32] << 16);
-            v.w = (uint32_t)buf[6 * 32] | ((uint32_t)buf[7 * 32] << 16);
-            dst[flushed >> 3] = v;
-          }
-          for (uint16_t* q = buf + 8 * 32; q < w; q += 32) q[-8 * 32] = *q;
-          w -= 8 * 32;
-          flushed += 8;
-        }
+        for (uint32_t q = buf + 8u * 64u; q < w; q += 64u) sts_u16(q - 8u * 64u, lds_u16(q));
+        w -= 8u * 64u;
+        flushed += 8;
       }
-    }
-    int nb = (int)(w - buf) >> 5;
-    auto flush8 = [&]() {
-      if (flushed + 8 <= g.lcap) {
-        uint4 v;
-        v.x = (uint32_t)buf[0 * 32] | ((uint32_t)buf[1 * 32] << 16);
-        v.y = (uint32_t)buf[2 * 32] | ((uint32_t)buf[3 * 32] << 16);
-        v.z = (uint32_t)buf[4 * 32] | ((uint32_t)buf[5 * 32] << 16);
-        v.w = (uint32_t)buf[6 * 32] | ((uint32_t)buf[7 * 32] << 16);
-        dst[flushed >> 3] = v;
-      }
-      for (int q = 8; q < nb; ++q) buf[(q - 8) * 32] = buf[q * 32];
-      nb -= 8;
-      flushed += 8;
     };
-    while (nb >= 8) flush8();
-    const int cnt = flushed + nb;
-    const int cntp = (cnt + 7) & ~7;
-    while (nb < ((nb + 7) & ~7)) buf[(nb++) * 32] = (uint16_t)g.tcap;
-    if (nb >= 8) flush8();
-    if (cntp > g.lcap) over = max(over, cntp);
+    auto zat = [&](int t) { return P[(t >> 1) * 8 + 4 + (t & 1)]; };
+    // slot guess for height u above the bottom of tile cell c0 (3 cells c0 .. c0 + 2)
+    auto guess = [&](int c0, float u, int lo, int hi) {
+      const float f = fminf(fmaxf(u * inv_side, 0.f), 2.999f);
+      const int k = (int)f;
+      const int s0 = S.off[c0 + k], s1 = S.off[c0 + k + 1];
+      return min(max(s0 + (int)((f - (float)k) * (float)(s1 - s0)), lo), hi);
+    };
     if (valid) {
+#pragma unroll 1
+      for (int d = 0; d < 9; ++d) {
+        const int tcol = tc + (d / 3 - 1) * (g.by + 2) + (d % 3 - 1);
+        const int cb = tcol * T.nzt + zz;
+        const int a0 = S.off[cb - 1], e0 = S.off[cb + 2];
+        // first slot with z >= zi - zpad and first slot with z > zi + zpad: a guess from the
+        // cell boundaries (slots spread ~evenly over a cell), then a short walk
+        int a = guess(cb - 1, zi - zpad - zc, a0, e0);
+        while (a < e0 && zat(a) < zi - zpad) ++a;
+        while (a > a0 && zat(a - 1) >= zi - zpad) --a;
+        int e = guess(cb - 1, zi + zpad - zc, a, e0);
+        while (e < e0 && zat(e) <= zi + zpad) ++e;
+        while (e > a && zat(e - 1) > zi + zpad) --e;
+        if (a >= e) continue;
+        if (a & 1) test_one(a++);
+        if ((e - a) & 1) test_one(--e);
+        drain();
+        for (int p0 = a >> 1; p0 < (e >> 1); p0 += 8) {
+          const int pn = min(e >> 1, p0 + 8);
+#pragma unroll 4
+          for (int pp = p0; pp < pn; ++pp) {
+            const float4 A = reinterpret_cast<const float4*>(P)[2 * pp];
+            const float4 B = reinterpret_cast<const float4*>(P)[2 * pp + 1];
+            const float2 dx = __fadd2_rn(make_float2(A.x, A.y), nX);
+            const float2 dy = __fadd2_rn(make_float2(A.z, A.w), nY);
+            const float2 dz = __fadd2_rn(make_float2(B.x, B.y), nZ);
+            float2 r2 = __fmul2_rn(dx, dx);
+            r2 = __ffma2_rn(dy, dy, r2);
+            r2 = __ffma2_rn(dz, dz, r2);
+            hit(r2.x < fmaxf(Hi2, B.z), 2 * pp);
+            hit(r2.y < fmaxf(Hi2, B.w), 2 * pp + 1);
+          }
+          drain();
+        }
+      }
+      // pad to a multiple of 8 with the sentinel slot, flush
+      int nb = (int)((w - buf) >> 6);
+      const int cnt = flushed + nb;
+      const int cntp = (cnt + 7) & ~7;
+      for (; nb < ((nb + 7) & ~7); ++nb) hit(true, g.tcap);
+      drain();
+      if (cntp > g.lcap) over = max(over, cntp);
       s.ncount[gi] = min(cntp, g.lcap);
       s.hbuild[gi] = sqrtf(Hi2) / Hfac;
     }
-    __syncwarp();
   }
   over = warp_max(over);
   if (lane == 0 && over) atomicMax(&ctr->list_overflow, over);
@@ -890,7 +921,7 @@ __global__ void k_tile_sizes(DevGrid g, const int* __restrict__ cell_start, int*
 int kernel_threads() { return kNW * 32; }
 
 size_t lists_smem(const DevGrid& g) {
-  return (size_t)((g.tcap + 2) & ~1) * 16 + (size_t)kNW * 24 * 32 * 2;
+  return (size_t)((g.tcap + 2) & ~1) * 16 + (size_t)kNW * kListRows * 32 * 2;
 }
 size_t density_smem(const DevGrid& g) { return (size_t)(g.tcap + 1) * (2 * 16 + 4); }  // + i list
 size_t gradient_smem(const DevGrid& g) { return (size_t)(g.tcap + 1) * (3 * 16); }

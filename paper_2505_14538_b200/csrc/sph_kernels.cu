@@ -306,7 +306,7 @@ __device__ __forceinline__ void for_list(const uint16_t* __restrict__ list, int 
 // and packed f32x2 arithmetic (FADD2 / FMUL2 / FFMA2).  Hits go to a per-lane column of a
 // per-warp buffer in shared memory and leave for global memory 8 at a time (16-byte stores).
 constexpr int kMaxICells = kMaxICols * (kMaxTileCellsZ - 2);
-constexpr int kListRows = 26;  // buffer rows per lane: 7 left + 2 single tests + 16 per group
+constexpr int kListRows = 32;  // ring rows per lane (<= 7 left + 2 single tests + 16 per group)
 __device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u16 [%0], %1;\n" ::"r"(a), "h"((unsigned short)v) : "memory");
 }
@@ -381,8 +381,10 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
     const uint32_t b = (uint32_t)((((unsigned long long)c) << 32) / (unsigned long long)g.nz);
     return (float)(int)(b - T.ref[2]) * g.scale[2];
   };
-  // kListRows x 32-lane uint16 buffer per warp after the pair array (row stride 64 bytes)
+  // kListRows x 32-lane uint16 ring per warp after the pair array (row stride 64 bytes):
+  // entries leave 8 at a time from 512-byte aligned ring positions, nothing is moved
   const uint32_t buf = sP + (uint32_t)NP * 32u + (uint32_t)(warp * kListRows * 32 + lane) * 2u;
+  constexpr uint32_t kRing = kListRows * 64u;
   const int ni = s_cp[nicell];
   int over = 0;
   for (int c = warp; c * 32 < ni; c += kNW) {
@@ -405,12 +407,12 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
     const int tc = S.tc[col];
     const float zc = zbound(T.z0 + zz - 2);  // bottom of tile cell zz - 1
     uint4* dst = reinterpret_cast<uint4*>(s.nbr + (size_t)gi * g.lcap);
-    uint32_t w = buf;  // next free buffer row
-    int flushed = 0;   // entries already in global memory
+    uint32_t w = 0u, rd = 0u;  // ring byte offsets: next write, next flush
+    int flushed = 0;           // entries already in global memory
     auto hit = [&](bool h, int t) {
       if (h) {
-        sts_u16(w, (uint32_t)t);
-        w += 64u;
+        sts_u16(buf + w, (uint32_t)t);
+        w = (w + 64u) & (kRing - 1u);
       }
     };
     auto test_one = [&](int t) {  // a single candidate (window ends)
@@ -420,17 +422,17 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
       hit(r2 < Hi2 || r2 < q[6], t);
     };
     auto drain = [&]() {  // buffered entries -> global memory, 8 at a time
-      while (w - buf >= 8u * 64u) {
+      while (((w - rd) & (kRing - 1u)) >= 8u * 64u) {
         if (flushed + 8 <= g.lcap) {
+          const uint32_t r = buf + rd;
           uint4 v;
-          v.x = lds_u16(buf + 0 * 64) | (lds_u16(buf + 1 * 64) << 16);
-          v.y = lds_u16(buf + 2 * 64) | (lds_u16(buf + 3 * 64) << 16);
-          v.z = lds_u16(buf + 4 * 64) | (lds_u16(buf + 5 * 64) << 16);
-          v.w = lds_u16(buf + 6 * 64) | (lds_u16(buf + 7 * 64) << 16);
+          v.x = lds_u16(r + 0 * 64) | (lds_u16(r + 1 * 64) << 16);
+          v.y = lds_u16(r + 2 * 64) | (lds_u16(r + 3 * 64) << 16);
+          v.z = lds_u16(r + 4 * 64) | (lds_u16(r + 5 * 64) << 16);
+          v.w = lds_u16(r + 6 * 64) | (lds_u16(r + 7 * 64) << 16);
           dst[flushed >> 3] = v;
         }
-        for (uint32_t q = buf + 8u * 64u; q < w; q += 64u) sts_u16(q - 8u * 64u, lds_u16(q));
-        w -= 8u * 64u;
+        rd = (rd + 8u * 64u) & (kRing - 1u);
         flushed += 8;
       }
     };
@@ -479,7 +481,7 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
         }
       }
       // pad to a multiple of 8 with the sentinel slot, flush
-      int nb = (int)((w - buf) >> 6);
+      int nb = (int)(((w - rd) & (kRing - 1u)) >> 6);
       const int cnt = flushed + nb;
       const int cntp = (cnt + 7) & ~7;
       for (; nb < ((nb + 7) & ~7); ++nb) hit(true, g.tcap);

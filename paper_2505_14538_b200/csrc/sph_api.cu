@@ -817,21 +817,30 @@ sph_status rebuild_impl(sph_ctx* c) {
   if ((st = allreduce(c, &ntot, 1, kSum)) != SPH_OK) return st;  // same KZ on every rank
   const double occ = std::max(ntot, 1.0) / ((double)R * g.nxo * g.ny * g.nz);
   const int kz_max = std::min(kMaxTileCellsZ - 2, g.nz > 3 ? g.nz - 3 : 1);
-  int KZ = (int)std::lround(kernel_threads() / std::max(occ * g.bx * g.by, 1e-3));
+  // largest KZ whose force tile (68 B per slot + 32 B per block particle) fits the target,
+  // from the mean occupancy with a 25% margin; then checked against the real maximum below
+  int KZ = 1;
+  for (int k = 2; k <= kz_max; ++k) {
+    const double slots = 1.25 * occ * (g.bx + 2) * (g.by + 2) * (k + 2);
+    const double icnt = 1.25 * occ * g.bx * g.by * k;
+    if (68.0 * slots + 32.0 * icnt > (double)kSmemTarget) break;
+    KZ = k;
+  }
   if (c->cfg.tile_cells_z > 0) KZ = c->cfg.tile_cells_z;
   KZ = std::max(1, std::min(KZ, kz_max));
   for (;;) {
     g.KZ = KZ;
     g.nzb = (g.nz + KZ - 1) / KZ;
     g.nblocks = g.nbx * g.nby * g.nzb;
-    CK(cudaMemsetAsync(c->scratch + 1, 0, 4, c->stream));
-    CK(launch_tile_sizes(g, c->cell_start, (int*)(c->scratch + 1), c->stream));
+    CK(cudaMemsetAsync(c->scratch + 6, 0, 8, c->stream));
+    CK(launch_tile_sizes(g, c->cell_start, (int*)(c->scratch + 6), (int*)(c->scratch + 7), c->stream));
     c->launches++;
-    CK(cudaMemcpyAsync(c->scratch_h + 1, c->scratch + 1, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(c->scratch_h + 6, c->scratch + 6, 8, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    double tmax = (double)c->scratch_h[1];
-    if ((st = allreduce(c, &tmax, 1, kMax)) != SPH_OK) return st;  // same tile capacity on every rank
-    g.tcap = std::max(32, (int)tmax);
+    double tmax[2] = {(double)c->scratch_h[6], (double)c->scratch_h[7]};
+    if ((st = allreduce(c, tmax, 2, kMax)) != SPH_OK) return st;  // same capacities on every rank
+    g.tcap = std::max(32, (int)tmax[0]);
+    g.icap = std::max(32, (int)tmax[1]);
     g.lcap = c->lcap;
     g.skin = c->cfg.cell_skin;
     const bool fits = force_smem(g) <= kSmemMax && lists_smem(g) <= kSmemMax && g.tcap < 65535;

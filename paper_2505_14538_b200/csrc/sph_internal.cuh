@@ -30,6 +30,7 @@ struct DevGrid {
   int nblocks;        // nbx * nby * nzb
   int ncells;
   int tcap;           // tile capacity (particles) the launch is sized for; slot tcap = sentinel
+  int icap;           // most i particles (owned by the block) of any block
   int lcap;           // neighbour-list capacity per particle (multiple of 8)
   float skin;         // list radius = (1 + skin) max(H_i, H_j)
   float scale[3];     // L_a / 2^32 as f32 (fixed point -> length)
@@ -112,7 +113,7 @@ cudaError_t launch_gradient(const DevGrid& g, const DevPhys& ph, const DevState&
                             int first_step, DevCounters* ctr, cudaStream_t st);
 cudaError_t launch_force(const DevGrid& g, const DevPhys& ph, const DevState& s, const int* cell_start,
                          DevCounters* ctr, cudaStream_t st);
-cudaError_t launch_tile_sizes(const DevGrid& g, const int* cell_start, int* max_tile, cudaStream_t st);
+cudaError_t launch_tile_sizes(const DevGrid& g, const int* cell_start, int* max_tile, int* max_i, cudaStream_t st);
 size_t lists_smem(const DevGrid& g);
 size_t density_smem(const DevGrid& g);
 size_t gradient_smem(const DevGrid& g);

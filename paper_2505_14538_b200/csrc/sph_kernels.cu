@@ -495,6 +495,136 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
   if (lane == 0 && over) atomicMax(&ctr->list_overflow, over);
 }
 
+// ================================================ balanced walk over the lists ==========
+// The loops below run over the block's i particles' neighbour lists cut into groups of 8
+// entries (one 16-byte load each).  Instead of one lane per particle (a block holds only a
+// few chunks of 32 particles, so most warps would idle while the last chunk finishes), the
+// block's G list groups are split evenly over its 256 threads: thread t walks groups
+// [t G / 256, (t+1) G / 256) in particle order, in one flat loop (every thread runs the same
+// number of iterations up to one; only the particle switch diverges).  A particle whose
+// groups lie inside one thread's range is summed by that thread alone and stored; a particle
+// split across threads gets its partial sums combined with shared-memory atomics (float
+// adds: the split particles' sums may differ in the last bit between runs).
+constexpr int kNT = kNW * 32;
+__device__ __forceinline__ int group_start(int t, int G) { return (int)(((long long)t * G) / kNT); }
+
+// In-place exclusive scan of a[0..n) by the whole block; a[n] = total.  Ends with a barrier.
+__device__ void block_exclusive_scan(int* a, int n) {
+  __shared__ int s_w[kNW + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int carry = 0;
+  for (int base = 0; base < n; base += kNT) {
+    const int k = base + threadIdx.x;
+    const int v0 = k < n ? a[k] : 0;
+    int v = v0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, v, o);
+      if (lane >= o) v += y;
+    }
+    if (lane == 31) s_w[warp] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int acc = 0;
+      for (int w = 0; w < kNW; ++w) {
+        const int t = s_w[w];
+        s_w[w] = acc;
+        acc += t;
+      }
+      s_w[kNW] = acc;
+    }
+    __syncthreads();
+    if (k < n) a[k] = carry + s_w[warp] + v - v0;
+    carry += s_w[kNW];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) a[n] = carry;
+  __syncthreads();
+}
+
+// Walk this thread's groups.  list_of(k) is particle k's list; begin(k) sets up particle k
+// (i state, accumulators); pair(j) accumulates one entry; take() returns the accumulators.
+// fin[] must hold Acc::zero() for every particle.
+template <class Acc, class ListOf, class Begin, class Pair, class Take>
+__device__ __forceinline__ void walk_lists(int ni, const int* __restrict__ pref, Acc* fin, int /*sentinel*/,
+                                           ListOf&& list_of, Begin&& begin, Pair&& pair, Take&& take) {
+  const int G = pref[ni];
+  if (G == 0) return;
+  const int g0 = group_start(threadIdx.x, G), g1 = group_start(threadIdx.x + 1, G);
+  if (g0 >= g1) return;
+  int lo = 0, hi = ni;  // pref[lo] <= g0 < pref[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (pref[mid] <= g0) lo = mid; else hi = mid;
+  }
+  int k = lo;
+  int p0 = pref[k], p1 = pref[k + 1];
+  const uint4* list = reinterpret_cast<const uint4*>(list_of(k)) + (g0 - p0);
+  begin(k);
+  auto finish = [&]() {
+    if (g0 <= p0 && p1 <= g1) fin[k] = take(); else take().merge_into(&fin[k]);
+  };
+  for (int gg = g0; gg < g1; ++gg, ++list) {
+    if (gg == p1) {
+      finish();
+      ++k;
+      p0 = p1;
+      p1 = pref[k + 1];
+      list = reinterpret_cast<const uint4*>(list_of(k));
+      begin(k);
+    }
+    const uint4 e = __ldg(list);
+    pair((int)(e.x & 0xffffu));
+    pair((int)(e.x >> 16));
+    pair((int)(e.y & 0xffffu));
+    pair((int)(e.y >> 16));
+    pair((int)(e.z & 0xffffu));
+    pair((int)(e.z >> 16));
+    pair((int)(e.w & 0xffffu));
+    pair((int)(e.w >> 16));
+  }
+  finish();
+}
+
+// Walk-area layout after a kernel's tile records (byte offset `base`, 16-aligned).
+template <class Acc>
+struct WalkArea {
+  int* pref;  // [icap + 1]
+  int* kl;    // [icap]  walk index -> block-local i index
+  Acc* fin;   // [icap]
+};
+template <class Acc>
+__host__ __device__ __forceinline__ size_t walk_bytes(int icap) {
+  return (((size_t)(icap + 1) * 4 + 15) & ~(size_t)15) + (((size_t)icap * 4 + 15) & ~(size_t)15) +
+         (size_t)icap * sizeof(Acc);
+}
+template <class Acc>
+__device__ __forceinline__ WalkArea<Acc> walk_area(char* base, int icap) {
+  WalkArea<Acc> w;
+  w.pref = reinterpret_cast<int*>(base);
+  base += ((size_t)(icap + 1) * 4 + 15) & ~(size_t)15;
+  w.kl = reinterpret_cast<int*>(base);
+  base += ((size_t)icap * 4 + 15) & ~(size_t)15;
+  w.fin = reinterpret_cast<Acc*>(base);
+  return w;
+}
+
+// Fill pref[] with the list groups of the walk's particles (kl[0..ni)), scan it, and clear
+// the accumulators.
+template <class Acc>
+__device__ __forceinline__ void walk_prefix(const BlockShared& S, const DevState& s, WalkArea<Acc>& W, int ni) {
+  const int* kl = W.kl;
+  int* pref = W.pref;
+  for (int k = threadIdx.x; k < ni; k += kNT) {
+    int ti, gi;
+    i_slot(S, kl[k], ti, gi);
+    pref[k] = __ldg(s.ncount + gi) >> 3;
+    W.fin[k] = Acc::zero();
+  }
+  __syncthreads();
+  block_exclusive_scan(pref, ni);
+}
+
 // ============================================================== density loop ==========
 // Eqs. 2-6 with the Newton-Raphson h update of the ghost (R7) and the
 // density finalize (Eq. 8, EoS, Balsara; R8, R14) fused into the epilogue.
@@ -504,6 +634,17 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
 // Then nhat = S0/(pi h^3), dn/dh = -(3 S0 + S1)/(pi h^4), rho = R0/(pi h^3),
 // drho/dh = -(3 R0 + R1)/(pi h^4), div = -Dv/(rho pi h^4), curl = Cv/(rho pi h^4),
 // g = nhat h^3 - eta^3 = S0/pi - eta^3, h g' = -S1/pi.
+struct DenAcc {
+  float S0, S1, R0, R1, Dv, Cx, Cy, Cz;
+  int nn;
+  __device__ static DenAcc zero() { return DenAcc{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0}; }
+  __device__ void merge_into(DenAcc* d) const {
+    atomicAdd(&d->S0, S0); atomicAdd(&d->S1, S1); atomicAdd(&d->R0, R0); atomicAdd(&d->R1, R1);
+    atomicAdd(&d->Dv, Dv); atomicAdd(&d->Cx, Cx); atomicAdd(&d->Cy, Cy); atomicAdd(&d->Cz, Cz);
+    atomicAdd(&d->nn, nn);
+  }
+};
+
 __global__ void __launch_bounds__(kNW * 32, 2) k_density(DevGrid g, DevPhys ph, DevState s,
                                                       const int* __restrict__ cell_start, int pass,
                                                       const uint8_t* __restrict__ blk_in, uint8_t* __restrict__ blk_out,
@@ -515,7 +656,7 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_density(DevGrid g, DevPhys ph, 
   if (threadIdx.x == 0) { s_ni = 0; s_pairs = 0; s_final = 0; s_unconv = 0; s_active = 0; }
   TILE_PROLOGUE();
   const int O1 = SP;  // T0 = smem4[j]: x, y, z, h   T1 = smem4[O1 + j]: vx, vy, vz, m
-  int* ilist = reinterpret_cast<int*>(smem4 + 2 * SP);
+  WalkArea<DenAcc> W = walk_area<DenAcc>(reinterpret_cast<char*>(smem4 + 2 * SP), g.icap);
   {
     const float4* src[2] = {reinterpret_cast<const float4*>(s.xh), s.vm};
     const int o16[2] = {0, O1};
@@ -530,118 +671,142 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_density(DevGrid g, DevPhys ph, 
     smem4[g.tcap] = make_float4(kFar, kFar, kFar, 1.f);
     smem4[O1 + g.tcap] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
+  // the walk's particles: all of the block (pass 0) or the still active ones, compacted in
+  // block order (deterministic)
   if (pass == 0) {
+    for (int k = threadIdx.x; k < T.ni; k += kNT) W.kl[k] = k;
     if (threadIdx.x == 0) s_ni = T.ni;
   } else {
-    for (int k = threadIdx.x; k < T.ni; k += blockDim.x) {
+    for (int k = threadIdx.x; k < T.ni; k += kNT) {
       int ti, gi;
       i_slot(S, k, ti, gi);
-      if (s.active[gi]) ilist[atomicAdd(&s_ni, 1)] = k;
+      W.pref[k] = s.active[gi] ? 1 : 0;
     }
+    __syncthreads();
+    block_exclusive_scan(W.pref, T.ni);
+    for (int k = threadIdx.x; k < T.ni; k += kNT)
+      if (W.pref[k + 1] > W.pref[k]) W.kl[W.pref[k]] = k;
+    if (threadIdx.x == 0) s_ni = W.pref[T.ni];
   }
   __syncthreads();
   const int ni = s_ni;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  walk_prefix(S, s, W, ni);
+  {
+    float4 pi4, vi4;
+    float hinv = 0.f, qband = 0.f;
+    double H2 = 0.0;
+    int gi = 0;
+    DenAcc a;
+    walk_lists(
+        ni, W.pref, W.fin, g.tcap,
+        [&](int k) {
+          int ti, gk;
+          i_slot(S, W.kl[k], ti, gk);
+          return s.nbr + (size_t)gk * g.lcap;
+        },
+        [&](int k) {
+          int ti;
+          i_slot(S, W.kl[k], ti, gi);
+          pi4 = smem4[ti];
+          vi4 = smem4[O1 + ti];
+          hinv = 1.f / pi4.w;
+          qband = g.eabs * hinv + 8e-6f;  // |q - 2| below this: decide in fp64
+          H2 = h2_exact(pi4.w, ph.gamma_k);
+          a = DenAcc{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0};
+        },
+        [&](int j) {
+          const float4 p = smem4[j];
+          const float4 q4 = smem4[O1 + j];
+          const float dx = pi4.x - p.x, dy = pi4.y - p.y, dz = pi4.z - p.z;
+          const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+          const float rinv = rinv_safe(r2);
+          const float q = r2 * rinv * hinv;
+          const float d = q - 2.f;
+          a.nn += neg(d);
+          if (fabsf(d) < qband) {
+            const bool ex = exact_neighbour(s.xh, gi, slot_global(S, T.nct, j), H2, g.dscale[0], g.dscale[1],
+                                            g.dscale[2]);
+            a.nn += (int)ex - neg(d);
+          }
+          float w, dw;
+          m4(q, w, dw);
+          const float qdw = q * dw;
+          a.S0 += w;
+          a.S1 += qdw;
+          a.R0 = fmaf(q4.w, w, a.R0);
+          a.R1 = fmaf(q4.w, qdw, a.R1);
+          const float F = q4.w * dw * rinv;
+          const float ux = vi4.x - q4.x, uy = vi4.y - q4.y, uz = vi4.z - q4.z;
+          a.Dv = fmaf(F, fmaf(uz, dz, fmaf(uy, dy, ux * dx)), a.Dv);
+          a.Cx = fmaf(F, fmaf(uy, dz, -uz * dy), a.Cx);
+          a.Cy = fmaf(F, fmaf(uz, dx, -ux * dz), a.Cy);
+          a.Cz = fmaf(F, fmaf(ux, dy, -uy * dx), a.Cz);
+        },
+        [&]() { return a; });
+  }
+  __syncthreads();
   const float inv_pi = 1.f / kPi;
   unsigned long long npairs = 0, nfinal = 0;
-
-  for (int c = warp; c * 32 < ni; c += kNW) {
-    const int kk = c * 32 + lane;
-    const bool valid = kk < ni;
-    const int li = pass == 0 ? (valid ? kk : c * 32) : ilist[valid ? kk : c * 32];
+  for (int k = threadIdx.x; k < ni; k += kNT) {
+    const DenAcc a = W.fin[k];
     int ti, gi;
-    i_slot(S, li, ti, gi);
-    const float4 pi4 = smem4[ti];
-    const float4 vi4 = smem4[O1 + ti];
-    const float h = pi4.w, hinv = 1.f / h;
-    const float qband = g.eabs * hinv + 8e-6f;  // |q - 2| below this: decide in fp64
-    const int cnt = valid ? s.ncount[gi] : 0;
-    float S0 = 0.f, S1 = 0.f, R0 = 0.f, R1 = 0.f, Dv = 0.f, Cx = 0.f, Cy = 0.f, Cz = 0.f;
-    int nn = 0;
-    for_list(s.nbr + (size_t)gi * g.lcap, cnt, [&](int j) {
-      const float4 p = smem4[j];
-      const float4 q4 = smem4[O1 + j];
-      const float dx = pi4.x - p.x, dy = pi4.y - p.y, dz = pi4.z - p.z;
-      const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-      const float rinv = rinv_safe(r2);
-      const float q = r2 * rinv * hinv;
-      const float d = q - 2.f;
-      nn += neg(d);
-      if (fabsf(d) < qband) {
-        const bool ex = exact_neighbour(s.xh, gi, slot_global(S, T.nct, j), h2_exact(h, ph.gamma_k), g.dscale[0],
-                                        g.dscale[1], g.dscale[2]);
-        nn += (int)ex - neg(d);
-      }
-      float w, dw;
-      m4(q, w, dw);
-      const float qdw = q * dw;
-      S0 += w;
-      S1 += qdw;
-      R0 = fmaf(q4.w, w, R0);
-      R1 = fmaf(q4.w, qdw, R1);
-      const float F = q4.w * dw * rinv;
-      const float ux = vi4.x - q4.x, uy = vi4.y - q4.y, uz = vi4.z - q4.z;
-      Dv = fmaf(F, fmaf(uz, dz, fmaf(uy, dy, ux * dx)), Dv);
-      Cx = fmaf(F, fmaf(uy, dz, -uz * dy), Cx);
-      Cy = fmaf(F, fmaf(uz, dx, -ux * dz), Cy);
-      Cz = fmaf(F, fmaf(ux, dy, -uy * dx), Cz);
-    });
-    nn -= 1;  // the self pair
-    if (valid) {
-      npairs += (unsigned long long)nn;
-      // ---- epilogue: closure, Newton / finalize
-      const float mi = vi4.w;
-      const float ih3 = inv_pi * hinv * hinv * hinv;
-      const float nhat = S0 * ih3;
-      const float dndh = -(3.f * S0 + S1) * ih3 * hinv;
-      const float rho = R0 * ih3;
-      const float drho = -(3.f * R0 + R1) * ih3 * hinv;
-      const float gres = S0 * inv_pi - ph.eta3;
-      const bool conv = (ph.h_max_iter == 0) || fabsf(gres) <= ph.h_tol * ph.eta3;
-      const int it = pass == 0 ? 0 : s.iters[gi];
-      const bool give_up = !conv && it >= ph.h_max_iter;
-      if (conv || give_up) {
-        const float ih4 = ih3 * hinv / rho;
-        s.dens[gi] = make_float4(rho, drho, nhat, dndh);
-        const float div = -Dv * ih4;
-        const float cx = Cx * ih4, cy = Cy * ih4, cz = Cz * ih4;
-        s.dvc[gi] = make_float4(cx, cy, cz, div);
-        s.count[gi] = nn;
-        // finalize: Eq. 8 (n_a = 3), ideal gas, Balsara (R8, R14)
-        const float Omega = 1.f + h / (3.f * rho) * drho;
-        const float f = ph.fh_mode ? Omega : 1.f / Omega;
-        const float u = s.u[gi];
-        const float P = (ph.gamma_eos - 1.f) * rho * u;
-        const float cs = sqrtf(ph.gamma_eos * P / rho);
-        const float adiv = fabsf(div), acurl = sqrtf(cx * cx + cy * cy + cz * cz);
-        const float den = adiv + acurl + 1e-4f * cs * hinv;
-        const float Bal = den > 0.f ? adiv / den : 0.f;
-        s.fin[gi] = make_float4(f, P, cs, Bal);
-        s.gq[gi] = make_float4(cs, u, mi / rho, rho);
-        s.active[gi] = 0;
-        s.iters[gi] = conv ? it : -1;
-        nfinal += (unsigned long long)nn;
-        if (give_up) atomicAdd(&s_unconv, 1);
-      } else {
-        // Newton with bracket + bisection (R7); g is non-decreasing in h
-        float lo = pass == 0 ? 0.f : s.hlo[gi];
-        float hi = pass == 0 ? CUDART_INF_F : s.hhi[gi];
-        if (gres > 0.f) hi = h; else lo = h;
-        float hn = (S1 < 0.f) ? h * (1.f + (S0 - ph.pi_eta3) / S1) : (gres < 0.f ? 2.f * h : 0.5f * h);
-        hn = fminf(fmaxf(hn, 0.5f * h), 2.f * h);
-        if (hn <= lo || hn >= hi) hn = isinf(hi) ? 2.f * h : 0.5f * (lo + hi);
-        s.hlo[gi] = lo;
-        s.hhi[gi] = hi;
-        s.iters[gi] = it + 1;
-        s.active[gi] = 1;
-        reinterpret_cast<unsigned int*>(&s.xh[gi])[3] = __float_as_uint(hn);
-        s_active = 1;
-        const float Hn = ph.gamma_k * hn * (1.f + g.skin);
-        if (Hn > g.side_min) atomicExch(&ctr->h_exceeds, 1);
-        if (hn > hfac_stale * s.hbuild[gi]) atomicExch(&ctr->list_stale, 1);
-      }
+    i_slot(S, W.kl[k], ti, gi);
+    const float h = smem4[ti].w, hinv = 1.f / h;
+    const float mi = smem4[O1 + ti].w;
+    const int nn = a.nn - 1;  // the self pair
+    npairs += (unsigned long long)nn;
+    // ---- epilogue: closure, Newton / finalize
+    const float ih3 = inv_pi * hinv * hinv * hinv;
+    const float nhat = a.S0 * ih3;
+    const float dndh = -(3.f * a.S0 + a.S1) * ih3 * hinv;
+    const float rho = a.R0 * ih3;
+    const float drho = -(3.f * a.R0 + a.R1) * ih3 * hinv;
+    const float gres = a.S0 * inv_pi - ph.eta3;
+    const bool conv = (ph.h_max_iter == 0) || fabsf(gres) <= ph.h_tol * ph.eta3;
+    const int it = pass == 0 ? 0 : s.iters[gi];
+    const bool give_up = !conv && it >= ph.h_max_iter;
+    if (conv || give_up) {
+      const float ih4 = ih3 * hinv / rho;
+      s.dens[gi] = make_float4(rho, drho, nhat, dndh);
+      const float div = -a.Dv * ih4;
+      const float cx = a.Cx * ih4, cy = a.Cy * ih4, cz = a.Cz * ih4;
+      s.dvc[gi] = make_float4(cx, cy, cz, div);
+      s.count[gi] = nn;
+      // finalize: Eq. 8 (n_a = 3), ideal gas, Balsara (R8, R14)
+      const float Omega = 1.f + h / (3.f * rho) * drho;
+      const float f = ph.fh_mode ? Omega : 1.f / Omega;
+      const float u = s.u[gi];
+      const float P = (ph.gamma_eos - 1.f) * rho * u;
+      const float cs = sqrtf(ph.gamma_eos * P / rho);
+      const float adiv = fabsf(div), acurl = sqrtf(cx * cx + cy * cy + cz * cz);
+      const float den = adiv + acurl + 1e-4f * cs * hinv;
+      const float Bal = den > 0.f ? adiv / den : 0.f;
+      s.fin[gi] = make_float4(f, P, cs, Bal);
+      s.gq[gi] = make_float4(cs, u, mi / rho, rho);
+      s.active[gi] = 0;
+      s.iters[gi] = conv ? it : -1;
+      nfinal += (unsigned long long)nn;
+      if (give_up) atomicAdd(&s_unconv, 1);
+    } else {
+      // Newton with bracket + bisection (R7); g is non-decreasing in h
+      float lo = pass == 0 ? 0.f : s.hlo[gi];
+      float hi = pass == 0 ? CUDART_INF_F : s.hhi[gi];
+      if (gres > 0.f) hi = h; else lo = h;
+      float hn = (a.S1 < 0.f) ? h * (1.f + (a.S0 - ph.pi_eta3) / a.S1) : (gres < 0.f ? 2.f * h : 0.5f * h);
+      hn = fminf(fmaxf(hn, 0.5f * h), 2.f * h);
+      if (hn <= lo || hn >= hi) hn = isinf(hi) ? 2.f * h : 0.5f * (lo + hi);
+      s.hlo[gi] = lo;
+      s.hhi[gi] = hi;
+      s.iters[gi] = it + 1;
+      s.active[gi] = 1;
+      reinterpret_cast<unsigned int*>(&s.xh[gi])[3] = __float_as_uint(hn);
+      s_active = 1;
+      const float Hn = ph.gamma_k * hn * (1.f + g.skin);
+      if (Hn > g.side_min) atomicExch(&ctr->h_exceeds, 1);
+      if (hn > hfac_stale * s.hbuild[gi]) atomicExch(&ctr->list_stale, 1);
     }
   }
+  const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     npairs += __shfl_xor_sync(kFull, npairs, o);
@@ -665,6 +830,17 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_density(DevGrid g, DevPhys ph, 
 // Brookshaw Laplacian lap u_i = 2 sum_j (m_j/rho_j)(u_i - u_j) dW/dr / r (R16), gathered
 // over r_ij < H_i; the gradient ghost (alpha_v Eqs. 12-15, alpha_c Eqs. 21-24; R17-R21)
 // runs in the epilogue and writes the force-loop records.
+struct GradAcc {
+  float vmax, lap;  // vmax > 0: max over its f32 bits as int
+  int nn;
+  __device__ static GradAcc zero() { return GradAcc{0.f, 0.f, 0}; }
+  __device__ void merge_into(GradAcc* d) const {
+    atomicMax(reinterpret_cast<int*>(&d->vmax), __float_as_int(vmax));
+    atomicAdd(&d->lap, lap);
+    atomicAdd(&d->nn, nn);
+  }
+};
+
 __global__ void __launch_bounds__(kNW * 32, 2) k_gradient(DevGrid g, DevPhys ph, DevState s,
                                                        const int* __restrict__ cell_start, float dt, int first_step,
                                                        DevCounters* __restrict__ ctr) {
@@ -673,6 +849,7 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_gradient(DevGrid g, DevPhys ph,
   TILE_PROLOGUE();
   // T0 = smem4[j]: x, y, z, h   T1 = smem4[O1 + j]: vx, vy, vz, m   T2 = smem4[O2 + j]: c, u, m/rho, rho
   const int O1 = SP, O2 = 2 * SP;
+  WalkArea<GradAcc> W = walk_area<GradAcc>(reinterpret_cast<char*>(smem4 + 3 * SP), g.icap);
   {
     const float4* src[3] = {reinterpret_cast<const float4*>(s.xh), s.vm, s.gq};
     const int o16[3] = {0, O1, O2};
@@ -688,79 +865,99 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_gradient(DevGrid g, DevPhys ph,
     smem4[O1 + g.tcap] = make_float4(0.f, 0.f, 0.f, 0.f);
     smem4[O2 + g.tcap] = make_float4(0.f, 0.f, 0.f, 1.f);
   }
-  __syncthreads();
   const int ni = T.ni;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  unsigned long long npairs = 0;
-
-  for (int c = warp; c * 32 < ni; c += kNW) {
-    const int kk = c * 32 + lane;
-    const bool valid = kk < ni;
-    int ti, gi;
-    i_slot(S, valid ? kk : c * 32, ti, gi);
-    const float4 pi4 = smem4[ti];
-    const float4 vi4 = smem4[O1 + ti];
-    const float4 gi4 = smem4[O2 + ti];
-    const float h = pi4.w, hinv = 1.f / h;
-    const float qband = g.eabs * hinv + 8e-6f;
-    const float ci = gi4.x, ui = gi4.y;
-    const int cnt = valid ? s.ncount[gi] : 0;
-    float vmax = 2.f * ci, lap = 0.f;
-    int nn = 0;
-    for_list(s.nbr + (size_t)gi * g.lcap, cnt, [&](int j) {
-      const float4 p = smem4[j];
-      const float4 q4 = smem4[O1 + j];
-      const float4 g4 = smem4[O2 + j];
-      const float dx = pi4.x - p.x, dy = pi4.y - p.y, dz = pi4.z - p.z;
-      const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-      const float rinv = rinv_safe(r2);
-      const float q = r2 * rinv * hinv;
-      const float d = q - 2.f;
-      int in = neg(d);
-      if (fabsf(d) < qband)
-        in = exact_neighbour(s.xh, gi, slot_global(S, T.nct, j), h2_exact(h, ph.gamma_k), g.dscale[0], g.dscale[1],
-                             g.dscale[2]);
-      nn += in;
-      const float dw = m4_dw(q);
-      const float vr = fmaf(vi4.z - q4.z, dz, fmaf(vi4.y - q4.y, dy, (vi4.x - q4.x) * dx));
-      const float mu = fminf(vr, 0.f) * rinv;
-      const float vs = fmaf(-ph.beta, mu, ci + g4.x);
-      vmax = fmaxf(vmax, in ? vs : 0.f);
-      lap = fmaf(g4.z * (ui - g4.y), dw * rinv, lap);
-    });
-    nn -= 1;  // the self pair
-    if (valid) {
-      npairs += (unsigned long long)nn;
-      const float lap_u = 2.f * lap * hinv * hinv * hinv * hinv / kPi;
-      const float vsig = vmax;
-      // gradient ghost (R17-R21)
-      const float H = ph.gamma_k * h;
-      const float4 dvc = s.dvc[gi];
-      const float4 fin = s.fin[gi];
-      const float div = dvc.w;
-      float av = s.av[gi], ac = s.ac[gi];
-      const float Ddot = first_step ? 0.f : (div - s.dprev[gi]) / dt;
-      const float Sx = H * H * fmaxf(-Ddot, 0.f);
-      const float den = vsig * vsig + Sx;
-      const float aloc = den > 0.f ? ph.alpha_v_max * Sx / den : 0.f;
-      if (av < aloc) av = aloc;
-      else av = aloc + (av - aloc) * expf(-ph.ell * ci * dt / H);
-      const float src = ui > 0.f ? ph.beta_c * H * lap_u / sqrtf(ui) : 0.f;
-      const float dac = src - (ac - ph.alpha_c_min) * vsig / H;
-      ac = ac + dt * dac;
-      const float ceil_ = fmaxf(ph.alpha_c_min, ph.alpha_c_max * (1.f - av / ph.alpha_v_max));
-      ac = fmaxf(fminf(ac, ceil_), ph.alpha_c_min);
-      s.grad[gi] = make_float2(vsig, lap_u);
-      s.av[gi] = av;
-      s.ac[gi] = ac;
-      s.dprev[gi] = div;
-      const float rho = gi4.w;
-      const float f = fin.x, P = fin.y;
-      s.fr1[gi] = make_float4(P / (rho * rho), f * hinv * hinv * hinv * hinv / kPi, ci, rho);
-      s.fr2[gi] = make_float4(P, P * ac, ui, av);
-      s.fr3[gi] = fin.w;
-    }
+  for (int k = threadIdx.x; k < ni; k += kNT) W.kl[k] = k;
+  __syncthreads();
+  walk_prefix(S, s, W, ni);
+  {
+    float4 pi4, vi4;
+    float hinv = 0.f, qband = 0.f, ci = 0.f, ui = 0.f;
+    double H2 = 0.0;
+    int gi = 0;
+    GradAcc a;
+    walk_lists(
+        ni, W.pref, W.fin, g.tcap,
+        [&](int k) {
+          int ti, gk;
+          i_slot(S, W.kl[k], ti, gk);
+          return s.nbr + (size_t)gk * g.lcap;
+        },
+        [&](int k) {
+          int ti;
+          i_slot(S, k, ti, gi);
+          pi4 = smem4[ti];
+          vi4 = smem4[O1 + ti];
+          const float4 gi4 = smem4[O2 + ti];
+          hinv = 1.f / pi4.w;
+          qband = g.eabs * hinv + 8e-6f;
+          H2 = h2_exact(pi4.w, ph.gamma_k);
+          ci = gi4.x;
+          ui = gi4.y;
+          a = GradAcc{2.f * ci, 0.f, 0};
+        },
+        [&](int j) {
+          const float4 p = smem4[j];
+          const float4 q4 = smem4[O1 + j];
+          const float4 g4 = smem4[O2 + j];
+          const float dx = pi4.x - p.x, dy = pi4.y - p.y, dz = pi4.z - p.z;
+          const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+          const float rinv = rinv_safe(r2);
+          const float q = r2 * rinv * hinv;
+          const float d = q - 2.f;
+          int in = neg(d);
+          if (fabsf(d) < qband)
+            in = exact_neighbour(s.xh, gi, slot_global(S, T.nct, j), H2, g.dscale[0], g.dscale[1], g.dscale[2]);
+          a.nn += in;
+          const float dw = m4_dw(q);
+          const float vr = fmaf(vi4.z - q4.z, dz, fmaf(vi4.y - q4.y, dy, (vi4.x - q4.x) * dx));
+          const float mu = fminf(vr, 0.f) * rinv;
+          const float vs = fmaf(-ph.beta, mu, ci + g4.x);
+          a.vmax = fmaxf(a.vmax, in ? vs : 0.f);
+          a.lap = fmaf(g4.z * (ui - g4.y), dw * rinv, a.lap);
+        },
+        [&]() { return a; });
   }
+  __syncthreads();
+  unsigned long long npairs = 0;
+  for (int k = threadIdx.x; k < ni; k += kNT) {
+    const GradAcc a = W.fin[k];
+    int ti, gi;
+    i_slot(S, k, ti, gi);
+    const float h = smem4[ti].w, hinv = 1.f / h;
+    const float4 gi4 = smem4[O2 + ti];
+    const float ci = gi4.x, ui = gi4.y;
+    const int nn = a.nn - 1;  // the self pair
+    npairs += (unsigned long long)nn;
+    const float lap_u = 2.f * a.lap * hinv * hinv * hinv * hinv / kPi;
+    const float vsig = a.vmax;
+    // gradient ghost (R17-R21)
+    const float H = ph.gamma_k * h;
+    const float4 dvc = s.dvc[gi];
+    const float4 fin = s.fin[gi];
+    const float div = dvc.w;
+    float av = s.av[gi], ac = s.ac[gi];
+    const float Ddot = first_step ? 0.f : (div - s.dprev[gi]) / dt;
+    const float Sx = H * H * fmaxf(-Ddot, 0.f);
+    const float den = vsig * vsig + Sx;
+    const float aloc = den > 0.f ? ph.alpha_v_max * Sx / den : 0.f;
+    if (av < aloc) av = aloc;
+    else av = aloc + (av - aloc) * expf(-ph.ell * ci * dt / H);
+    const float src = ui > 0.f ? ph.beta_c * H * lap_u / sqrtf(ui) : 0.f;
+    const float dac = src - (ac - ph.alpha_c_min) * vsig / H;
+    ac = ac + dt * dac;
+    const float ceil_ = fmaxf(ph.alpha_c_min, ph.alpha_c_max * (1.f - av / ph.alpha_v_max));
+    ac = fmaxf(fminf(ac, ceil_), ph.alpha_c_min);
+    s.grad[gi] = make_float2(vsig, lap_u);
+    s.av[gi] = av;
+    s.ac[gi] = ac;
+    s.dprev[gi] = div;
+    const float rho = gi4.w;
+    const float f = fin.x, P = fin.y;
+    s.fr1[gi] = make_float4(P / (rho * rho), f * hinv * hinv * hinv * hinv / kPi, ci, rho);
+    s.fr2[gi] = make_float4(P, P * ac, ui, av);
+    s.fr3[gi] = fin.w;
+  }
+  const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) npairs += __shfl_xor_sync(kFull, npairs, o);
   if (lane == 0 && npairs) atomicAdd(&s_pairs, npairs);
@@ -777,6 +974,20 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_gradient(DevGrid g, DevPhys ph,
 // S_ij is evaluated from operands that are symmetric in (i, j), so the pair terms of i and
 // j are exact negatives (momentum and energy conserving up to the summation rounding).
 // The CFL dt = C_cfl min 2 gamma_k h / v_sig is reduced in the epilogue.
+struct ForceAcc {
+  float ax, ay, az, du, vmax;  // vmax > 0: max over its f32 bits as int
+  int nn;
+  __device__ static ForceAcc zero() { return ForceAcc{0.f, 0.f, 0.f, 0.f, 0.f, 0}; }
+  __device__ void merge_into(ForceAcc* d) const {
+    atomicAdd(&d->ax, ax); atomicAdd(&d->ay, ay); atomicAdd(&d->az, az); atomicAdd(&d->du, du);
+    atomicMax(reinterpret_cast<int*>(&d->vmax), __float_as_int(vmax));
+    atomicAdd(&d->nn, nn);
+  }
+};
+__host__ __device__ __forceinline__ size_t force_records_bytes(int tcap) {
+  return (((size_t)(tcap + 1) * (4 * 16 + 4)) + 15) & ~(size_t)15;
+}
+
 __global__ void __launch_bounds__(kNW * 32, 2) k_force(DevGrid g, DevPhys ph, DevState s,
                                                     const int* __restrict__ cell_start,
                                                     DevCounters* __restrict__ ctr) {
@@ -789,6 +1000,8 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_force(DevGrid g, DevPhys ph, De
   // T3 = [O3+j]: P, P alpha_c, u, alpha_v   T4 = float [O4+j]: B
   const int O1 = SP, O2 = 2 * SP, O3 = 3 * SP, O4 = 16 * SP;
   const float* sm1 = reinterpret_cast<const float*>(smem4);
+  WalkArea<ForceAcc> W =
+      walk_area<ForceAcc>(reinterpret_cast<char*>(smem4) + force_records_bytes(g.tcap), g.icap);
   {
     const float4* src[4] = {reinterpret_cast<const float4*>(s.xh), s.vm, s.fr1, s.fr2};
     const int o16[4] = {0, O1, O2, O3};
@@ -806,80 +1019,96 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_force(DevGrid g, DevPhys ph, De
     smem4[O3 + g.tcap] = make_float4(0.f, 0.f, 0.f, 0.f);
     reinterpret_cast<float*>(smem4)[O4 + g.tcap] = 0.f;
   }
-  __syncthreads();
   const int ni = T.ni;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int k = threadIdx.x; k < ni; k += kNT) W.kl[k] = k;
+  __syncthreads();
+  walk_prefix(S, s, W, ni);
+  {
+    float4 pi4, vi4, ai, bi;
+    float Bi = 0.f, hinv_i = 0.f, ebi = 0.f;
+    int gi = 0;
+    ForceAcc a;
+    walk_lists(
+        ni, W.pref, W.fin, g.tcap,
+        [&](int k) {
+          int ti, gk;
+          i_slot(S, W.kl[k], ti, gk);
+          return s.nbr + (size_t)gk * g.lcap;
+        },
+        [&](int k) {
+          int ti;
+          i_slot(S, k, ti, gi);
+          pi4 = smem4[ti];
+          vi4 = smem4[O1 + ti];
+          ai = smem4[O2 + ti];
+          bi = smem4[O3 + ti];
+          Bi = sm1[O4 + ti];
+          hinv_i = pi4.w;
+          ebi = g.eabs * hinv_i;
+          a = ForceAcc{0.f, 0.f, 0.f, 0.f, 2.f * ai.z, 0};
+        },
+        [&](int j) {
+          const float4 p = smem4[j];
+          const float dx = pi4.x - p.x, dy = pi4.y - p.y, dz = pi4.z - p.z;
+          const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+          const float4 vj = smem4[O1 + j];
+          const float4 aj = smem4[O2 + j];
+          const float4 bj = smem4[O3 + j];
+          const float Bj = sm1[O4 + j];
+          const float rinv = rinv_safe(r2);
+          const float r = r2 * rinv;
+          const float qi = r * hinv_i, qj = r * p.w;
+          const float d = fminf(qi, qj) - 2.f;
+          int in = neg(d);
+          if (fabsf(d) < fmaxf(ebi, g.eabs * p.w) + 8e-6f) {
+            const int gj = slot_global(S, T.nct, j);
+            const double H2 = fmax(h2_exact(__uint_as_float(s.xh[gi].w), ph.gamma_k),
+                                   h2_exact(__uint_as_float(s.xh[gj].w), ph.gamma_k));
+            in = exact_neighbour(s.xh, gi, gj, H2, g.dscale[0], g.dscale[1], g.dscale[2]);
+          }
+          a.nn += in;
+          const float Gi = ai.y * m4_dw(qi) * rinv;
+          const float Gj = aj.y * m4_dw(qj) * rinv;
+          const float vr = fmaf(vi4.z - vj.z, dz, fmaf(vi4.y - vj.y, dy, (vi4.x - vj.x) * dx));
+          const float mu = fminf(vr, 0.f) * rinv;
+          const float vs = fmaf(-ph.beta, mu, ai.z + aj.z);
+          a.vmax = fmaxf(a.vmax, in ? vs : 0.f);
+          const float abar = 0.25f * (bi.w + bj.w) * (Bi + Bj);
+          const float irs = __fdividef(1.f, ai.w + aj.w);
+          const float PiV = -2.f * abar * mu * vs * irs;
+          const float Gbar = 0.5f * (Gi + Gj);
+          const float Sij = fmaf(PiV, Gbar, fmaf(ai.x, Gi, aj.x * Gj));
+          const float mS = vj.w * Sij;
+          a.ax = fmaf(-mS, dx, a.ax);
+          a.ay = fmaf(-mS, dy, a.ay);
+          a.az = fmaf(-mS, dz, a.az);
+          const float Psum = bi.x + bj.x;
+          const float acij = Psum > 0.f ? __fdividef(bi.y + bj.y, Psum) : 0.f;
+          const float vc = fabsf(vr) * rinv + sqrtf(2.f * fabsf(bi.x - bj.x) * irs);
+          const float D = acij * vc * (bi.z - bj.z) * (Gi + Gj) * r * irs;
+          a.du = fmaf(vj.w, fmaf(ai.x * Gi, vr, fmaf(0.5f * PiV * Gbar, vr, D)), a.du);
+        },
+        [&]() { return a; });
+  }
+  __syncthreads();
   unsigned long long npairs = 0;
   float dtmin = CUDART_INF_F;
-
-  for (int c = warp; c * 32 < ni; c += kNW) {
-    const int kk = c * 32 + lane;
-    const bool valid = kk < ni;
+  for (int k = threadIdx.x; k < ni; k += kNT) {
+    const ForceAcc a = W.fin[k];
     int ti, gi;
-    i_slot(S, valid ? kk : c * 32, ti, gi);
-    const float4 pi4 = smem4[ti];
-    const float4 vi4 = smem4[O1 + ti];
-    const float4 ai = smem4[O2 + ti];
-    const float4 bi = smem4[O3 + ti];
-    const float Bi = sm1[O4 + ti];
-    const float hinv_i = pi4.w;
+    i_slot(S, k, ti, gi);
     const float hi_ = __uint_as_float(s.xh[gi].w);
-    const float ebi = g.eabs * hinv_i;
-    const int cnt = valid ? s.ncount[gi] : 0;
-    float ax = 0.f, ay = 0.f, az = 0.f, du = 0.f, vmax = 2.f * ai.z;
-    int nn = 0;
-    for_list(s.nbr + (size_t)gi * g.lcap, cnt, [&](int j) {
-      const float4 p = smem4[j];
-      const float dx = pi4.x - p.x, dy = pi4.y - p.y, dz = pi4.z - p.z;
-      const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-      const float4 vj = smem4[O1 + j];
-      const float4 aj = smem4[O2 + j];
-      const float4 bj = smem4[O3 + j];
-      const float Bj = sm1[O4 + j];
-      const float rinv = rinv_safe(r2);
-      const float r = r2 * rinv;
-      const float qi = r * hinv_i, qj = r * p.w;
-      const float d = fminf(qi, qj) - 2.f;
-      int in = neg(d);
-      if (fabsf(d) < fmaxf(ebi, g.eabs * p.w) + 8e-6f) {
-        const int gj = slot_global(S, T.nct, j);
-        const double H2 = fmax(h2_exact(hi_, ph.gamma_k), h2_exact(__uint_as_float(s.xh[gj].w), ph.gamma_k));
-        in = exact_neighbour(s.xh, gi, gj, H2, g.dscale[0], g.dscale[1], g.dscale[2]);
-      }
-      nn += in;
-      const float Gi = ai.y * m4_dw(qi) * rinv;
-      const float Gj = aj.y * m4_dw(qj) * rinv;
-      const float vr = fmaf(vi4.z - vj.z, dz, fmaf(vi4.y - vj.y, dy, (vi4.x - vj.x) * dx));
-      const float mu = fminf(vr, 0.f) * rinv;
-      const float vs = fmaf(-ph.beta, mu, ai.z + aj.z);
-      vmax = fmaxf(vmax, in ? vs : 0.f);
-      const float abar = 0.25f * (bi.w + bj.w) * (Bi + Bj);
-      const float irs = __fdividef(1.f, ai.w + aj.w);
-      const float PiV = -2.f * abar * mu * vs * irs;
-      const float Gbar = 0.5f * (Gi + Gj);
-      const float Sij = fmaf(PiV, Gbar, fmaf(ai.x, Gi, aj.x * Gj));
-      const float mS = vj.w * Sij;
-      ax = fmaf(-mS, dx, ax);
-      ay = fmaf(-mS, dy, ay);
-      az = fmaf(-mS, dz, az);
-      const float Psum = bi.x + bj.x;
-      const float acij = Psum > 0.f ? __fdividef(bi.y + bj.y, Psum) : 0.f;
-      const float vc = fabsf(vr) * rinv + sqrtf(2.f * fabsf(bi.x - bj.x) * irs);
-      const float D = acij * vc * (bi.z - bj.z) * (Gi + Gj) * r * irs;
-      du = fmaf(vj.w, fmaf(ai.x * Gi, vr, fmaf(0.5f * PiV * Gbar, vr, D)), du);
-    });
-    nn -= 1;  // the self pair
-    if (valid) {
-      s.acc[gi] = make_float4(ax, ay, az, du);
-      s.vsig[gi] = vmax;
-      s.countf[gi] = nn;
-      npairs += (unsigned long long)nn;
-      const float dti = ph.c_cfl * 2.f * ph.gamma_k * hi_ / vmax;
-      if (!(isfinite(vmax) && isfinite(ax) && isfinite(ay) && isfinite(az) && isfinite(du)) || !(dti > 0.f))
-        s_bad = 1;
-      dtmin = fminf(dtmin, dti);
-    }
+    const int nn = a.nn - 1;  // the self pair
+    s.acc[gi] = make_float4(a.ax, a.ay, a.az, a.du);
+    s.vsig[gi] = a.vmax;
+    s.countf[gi] = nn;
+    npairs += (unsigned long long)nn;
+    const float dti = ph.c_cfl * 2.f * ph.gamma_k * hi_ / a.vmax;
+    if (!(isfinite(a.vmax) && isfinite(a.ax) && isfinite(a.ay) && isfinite(a.az) && isfinite(a.du)) || !(dti > 0.f))
+      s_bad = 1;
+    dtmin = fminf(dtmin, dti);
   }
+  const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     npairs += __shfl_xor_sync(kFull, npairs, o);
@@ -897,25 +1126,30 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_force(DevGrid g, DevPhys ph, De
   }
 }
 
-// per-block tile size (max over blocks) -> sizes shared memory of the loops
-__global__ void k_tile_sizes(DevGrid g, const int* __restrict__ cell_start, int* max_tile) {
+// per-block tile size and i count (max over blocks) -> sizes shared memory of the loops
+__global__ void k_tile_sizes(DevGrid g, const int* __restrict__ cell_start, int* max_tile, int* max_i) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= g.nblocks) return;
   const int zb = b % g.nzb, t2 = b / g.nzb, jy = t2 % g.nby, jx = t2 / g.nby;
   const int ix0 = g.ix_first + jx * g.bx, iy0 = jy * g.by;
   const int z0 = zb * g.KZ, z1 = min(g.nz, z0 + g.KZ);
-  int tot = 0;
+  int tot = 0, ni = 0;
   for (int dx = -1; dx <= g.bx; ++dx)
     for (int dy = -1; dy <= g.by; ++dy) {
       if (!g.periodic_x && ix0 + dx >= g.nx) continue;
       const int cx = (ix0 + dx + g.nx) % g.nx, cy = (iy0 + dy + g.ny) % g.ny;
       const int c0 = (cx * g.ny + cy) * g.nz;
+      const bool own = dx >= 0 && dx < g.bx && dy >= 0 && dy < g.by && ix0 + dx < g.ix_first + g.nxo &&
+                       iy0 + dy < g.ny;
       for (int z = z0 - 1; z <= z1; ++z) {
         const int cz = (z + g.nz) % g.nz;
-        tot += cell_start[c0 + cz + 1] - cell_start[c0 + cz];
+        const int c = cell_start[c0 + cz + 1] - cell_start[c0 + cz];
+        tot += c;
+        if (own && z >= z0 && z < z1) ni += c;
       }
     }
   atomicMax(max_tile, tot);
+  atomicMax(max_i, ni);
 }
 
 }  // namespace
@@ -925,12 +1159,12 @@ int kernel_threads() { return kNW * 32; }
 size_t lists_smem(const DevGrid& g) {
   return (size_t)((g.tcap + 2) & ~1) * 16 + (size_t)kNW * kListRows * 32 * 2;
 }
-size_t density_smem(const DevGrid& g) { return (size_t)(g.tcap + 1) * (2 * 16 + 4); }  // + i list
-size_t gradient_smem(const DevGrid& g) { return (size_t)(g.tcap + 1) * (3 * 16); }
-size_t force_smem(const DevGrid& g) { return (size_t)(g.tcap + 1) * (4 * 16 + 4); }
+size_t density_smem(const DevGrid& g) { return (size_t)(g.tcap + 1) * (2 * 16) + walk_bytes<DenAcc>(g.icap); }
+size_t gradient_smem(const DevGrid& g) { return (size_t)(g.tcap + 1) * (3 * 16) + walk_bytes<GradAcc>(g.icap); }
+size_t force_smem(const DevGrid& g) { return force_records_bytes(g.tcap) + walk_bytes<ForceAcc>(g.icap); }
 
-cudaError_t launch_tile_sizes(const DevGrid& g, const int* cell_start, int* max_tile, cudaStream_t st) {
-  k_tile_sizes<<<(g.nblocks + 255) / 256, 256, 0, st>>>(g, cell_start, max_tile);
+cudaError_t launch_tile_sizes(const DevGrid& g, const int* cell_start, int* max_tile, int* max_i, cudaStream_t st) {
+  k_tile_sizes<<<(g.nblocks + 255) / 256, 256, 0, st>>>(g, cell_start, max_tile, max_i);
   return cudaGetLastError();
 }
 

@@ -164,6 +164,10 @@ def test_single_rank_slab_path(transport):
     assert np.array_equal(got["count_force"], one["count_force"])
     for k in ("rho", "P", "v_sig"):
         assert_close(k, got[k], one[k], rtol=2e-6)
-    sa = np.abs(one["a"]).max()
-    assert_close("a", got["a"], one["a"], rtol=1e-4, atol_scale=np.full(n, 1e-4 * sa))
+    # accelerations (sums with cancellation): both runs against the oracle where they differ most
+    diff = np.abs(got["a"] - one["a"]).max(1)
+    sample = np.unique(np.concatenate([np.argsort(diff)[-16:], np.arange(0, n, n // 16)]))
+    fo = oracle_hydro(p, dt_ghost=1e-3, fixed_h=True, sample=sample)["force"]
+    for run in (got, one):
+        assert_close("a", run["a"][sample], fo["a"][sample], atol_scale=fo["scale_a"][sample])
     assert abs(dt - one["dt"]) <= 1e-6 * one["dt"]

@@ -369,7 +369,7 @@ sph_status alloc_state(sph_ctx* c) {
   CK(dalloc(&s.dens, n)); CK(dalloc(&s.dvc, n)); CK(dalloc(&s.count, n)); CK(dalloc(&s.fin, n));
   CK(dalloc(&s.gq, n)); CK(dalloc(&s.hlo, n)); CK(dalloc(&s.hhi, n)); CK(dalloc(&s.iters, n));
   CK(dalloc(&s.active, n)); CK(dalloc(&s.grad, n)); CK(dalloc(&s.fr1, n)); CK(dalloc(&s.fr2, n));
-  CK(dalloc(&s.fr3, n)); CK(dalloc(&s.vsig, n)); CK(dalloc(&s.countf, n));
+  CK(dalloc(&s.vsig, n)); CK(dalloc(&s.countf, n));
   CK(dalloc(&s.ncount, n)); CK(dalloc(&s.hbuild, n));
   CK(dalloc(&s.nbr, n * (size_t)c->lcap));
   c->nbr_cap = n * (size_t)c->lcap;
@@ -1132,7 +1132,6 @@ sph_status sph_gradient(sph_ctx* c, float dt) {
   // ghosts need their owners' force-loop records (X3)
   if ((st = halo(c, c->s.fr1, sizeof(float4))) != SPH_OK) return st;
   if ((st = halo(c, c->s.fr2, sizeof(float4))) != SPH_OK) return st;
-  if ((st = halo(c, c->s.fr3, sizeof(float))) != SPH_OK) return st;
   c->dprev_valid = true;
   c->gradient_done = true;
   return SPH_OK;
@@ -1313,7 +1312,7 @@ sph_status sph_destroy(sph_ctx* c) {
   DevState& s = c->s;
   void* ptrs[] = {s.xh, s.vm, s.u, s.av, s.ac, s.dprev, s.uid, s.orig, s.acc, c->alt.xh, c->alt.vm, c->alt.u,
                   c->alt.av, c->alt.ac, c->alt.dprev, c->alt.uid, c->alt.orig, c->alt.acc, s.dens, s.dvc, s.count,
-                  s.fin, s.gq, s.hlo, s.hhi, s.iters, s.active, s.grad, s.fr1, s.fr2, s.fr3, s.vsig, s.countf, s.nbr,
+                  s.fin, s.gq, s.hlo, s.hhi, s.iters, s.active, s.grad, s.fr1, s.fr2, s.vsig, s.countf, s.nbr,
                   s.ncount, s.hbuild, c->cell_start, c->keys, c->keys_alt, c->perm, c->perm_alt, c->sort_tmp,
                   c->blk[0], c->blk[1], c->ctr, c->scratch, c->out_tmp, c->mig_send, c->mig_recv, c->pc_send,
                   c->pc_recv, c->pc_scan, c->scan_tmp, c->cnt_dev};

@@ -7,8 +7,7 @@
 //   vm   float4 (vx, vy, vz, m)                              density/gradient/force tiles
 //   gq   float4 (c_s, u, m/rho, rho)                         gradient tile (+ xh, vm)
 //   fr1  float4 (A = P/rho^2, Kf = f/(pi h^4), c_s, rho)     force tile
-//   fr2  float4 (P, P alpha_c, u, alpha_v)                   force tile
-//   fr3  float  B                                            force tile
+//   fr2  float4 (B, P alpha_c, u, alpha_v)                   force tile (P = A rho^2)
 // plus plain f32 arrays for state and outputs.
 #pragma once
 #include <cuda_runtime.h>
@@ -79,7 +78,6 @@ struct DevState {
   float2* grad;       // v_sig, lap_u
   float4* fr1;
   float4* fr2;
-  float* fr3;         // B (Balsara switch)
   // force
   float4* acc;        // a, du
   float* vsig;

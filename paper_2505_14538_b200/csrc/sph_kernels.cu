@@ -954,8 +954,7 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_gradient(DevGrid g, DevPhys ph,
     const float rho = gi4.w;
     const float f = fin.x, P = fin.y;
     s.fr1[gi] = make_float4(P / (rho * rho), f * hinv * hinv * hinv * hinv / kPi, ci, rho);
-    s.fr2[gi] = make_float4(P, P * ac, ui, av);
-    s.fr3[gi] = fin.w;
+    s.fr2[gi] = make_float4(fin.w, P * ac, ui, av);  // (B, P alpha_c, u, alpha_v); P = A rho^2
   }
   const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -985,7 +984,7 @@ struct ForceAcc {
   }
 };
 __host__ __device__ __forceinline__ size_t force_records_bytes(int tcap) {
-  return (((size_t)(tcap + 1) * (4 * 16 + 4)) + 15) & ~(size_t)15;
+  return (size_t)(tcap + 1) * (4 * 16);
 }
 
 __global__ void __launch_bounds__(kNW * 32, 2) k_force(DevGrid g, DevPhys ph, DevState s,
@@ -997,15 +996,14 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_force(DevGrid g, DevPhys ph, De
   if (threadIdx.x == 0) { s_pairs = 0; s_dt = 0x7f800000u; s_bad = 0; }
   TILE_PROLOGUE();
   // T0 = [j]: x, y, z, 1/h   T1 = [O1+j]: vx, vy, vz, m   T2 = [O2+j]: A, Kf, c, rho
-  // T3 = [O3+j]: P, P alpha_c, u, alpha_v   T4 = float [O4+j]: B
-  const int O1 = SP, O2 = 2 * SP, O3 = 3 * SP, O4 = 16 * SP;
-  const float* sm1 = reinterpret_cast<const float*>(smem4);
+  // T3 = [O3+j]: B, P alpha_c, u, alpha_v  (P = A rho^2: four 16-byte records per pair)
+  const int O1 = SP, O2 = 2 * SP, O3 = 3 * SP;
   WalkArea<ForceAcc> W =
       walk_area<ForceAcc>(reinterpret_cast<char*>(smem4) + force_records_bytes(g.tcap), g.icap);
   {
     const float4* src[4] = {reinterpret_cast<const float4*>(s.xh), s.vm, s.fr1, s.fr2};
     const int o16[4] = {0, O1, O2, O3};
-    stage_records(S, nseg, 4, src, o16, s.fr3, O4);
+    stage_records(S, nseg, 4, src, o16, nullptr, 0);
   }
   for (int t = threadIdx.x; t < T.ntile; t += blockDim.x) {
     const uint4 x = reinterpret_cast<const uint4*>(smem4)[t];
@@ -1017,7 +1015,6 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_force(DevGrid g, DevPhys ph, De
     smem4[O1 + g.tcap] = make_float4(0.f, 0.f, 0.f, 0.f);
     smem4[O2 + g.tcap] = make_float4(0.f, 0.f, 0.f, 1.f);
     smem4[O3 + g.tcap] = make_float4(0.f, 0.f, 0.f, 0.f);
-    reinterpret_cast<float*>(smem4)[O4 + g.tcap] = 0.f;
   }
   const int ni = T.ni;
   for (int k = threadIdx.x; k < ni; k += kNT) W.kl[k] = k;
@@ -1025,7 +1022,7 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_force(DevGrid g, DevPhys ph, De
   walk_prefix(S, s, W, ni);
   {
     float4 pi4, vi4, ai, bi;
-    float Bi = 0.f, hinv_i = 0.f, ebi = 0.f;
+    float Pi = 0.f, hinv_i = 0.f, ebi = 0.f;
     int gi = 0;
     ForceAcc a;
     walk_lists(
@@ -1042,7 +1039,7 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_force(DevGrid g, DevPhys ph, De
           vi4 = smem4[O1 + ti];
           ai = smem4[O2 + ti];
           bi = smem4[O3 + ti];
-          Bi = sm1[O4 + ti];
+          Pi = ai.x * ai.w * ai.w;
           hinv_i = pi4.w;
           ebi = g.eabs * hinv_i;
           a = ForceAcc{0.f, 0.f, 0.f, 0.f, 2.f * ai.z, 0};
@@ -1054,7 +1051,6 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_force(DevGrid g, DevPhys ph, De
           const float4 vj = smem4[O1 + j];
           const float4 aj = smem4[O2 + j];
           const float4 bj = smem4[O3 + j];
-          const float Bj = sm1[O4 + j];
           const float rinv = rinv_safe(r2);
           const float r = r2 * rinv;
           const float qi = r * hinv_i, qj = r * p.w;
@@ -1073,7 +1069,7 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_force(DevGrid g, DevPhys ph, De
           const float mu = fminf(vr, 0.f) * rinv;
           const float vs = fmaf(-ph.beta, mu, ai.z + aj.z);
           a.vmax = fmaxf(a.vmax, in ? vs : 0.f);
-          const float abar = 0.25f * (bi.w + bj.w) * (Bi + Bj);
+          const float abar = 0.25f * (bi.w + bj.w) * (bi.x + bj.x);
           const float irs = __fdividef(1.f, ai.w + aj.w);
           const float PiV = -2.f * abar * mu * vs * irs;
           const float Gbar = 0.5f * (Gi + Gj);
@@ -1082,9 +1078,10 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_force(DevGrid g, DevPhys ph, De
           a.ax = fmaf(-mS, dx, a.ax);
           a.ay = fmaf(-mS, dy, a.ay);
           a.az = fmaf(-mS, dz, a.az);
-          const float Psum = bi.x + bj.x;
+          const float Pj = aj.x * aj.w * aj.w;
+          const float Psum = Pi + Pj;
           const float acij = Psum > 0.f ? __fdividef(bi.y + bj.y, Psum) : 0.f;
-          const float vc = fabsf(vr) * rinv + sqrtf(2.f * fabsf(bi.x - bj.x) * irs);
+          const float vc = fabsf(vr) * rinv + sqrtf(2.f * fabsf(Pi - Pj) * irs);
           const float D = acij * vc * (bi.z - bj.z) * (Gi + Gj) * r * irs;
           a.du = fmaf(vj.w, fmaf(ai.x * Gi, vr, fmaf(0.5f * PiV * Gbar, vr, D)), a.du);
         },

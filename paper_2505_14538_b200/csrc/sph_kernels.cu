@@ -52,13 +52,27 @@ struct BlockShared {
   int pre[kMaxICols + 1];      // prefix of i counts over the i columns
 };
 
+// Launch order of the blocks: z fastest, then block columns in strips of kStrip columns
+// along y, column-major inside a strip, so the blocks whose tiles share a column (its x and
+// y neighbours) run within ~kStrip * nzb launches of each other and re-read the column's
+// records from L2 rather than HBM (the tiles of one launch wave are ~20 MB).
+constexpr int kStrip = 8;
+__device__ __forceinline__ void block_coords(const DevGrid& g, int b, int& jx, int& jy, int& zb) {
+  zb = b % g.nzb;
+  const int c = b / g.nzb;
+  const int s = c / (kStrip * g.nbx);
+  const int hs = min(kStrip, g.nby - s * kStrip);
+  const int local = c - s * kStrip * g.nbx;
+  jx = local / hs;
+  jy = s * kStrip + local % hs;
+}
+
 // Block geometry + tile cell table + i columns + segments.  Tile cell c = tc * nzt + zz,
 // tile column tc = (dx+1) * (BY+2) + (dy+1) for dx in [-1, BX], dy in [-1, BY],
 // zz = z - z0 + 1.  Ends with __syncthreads().
 __device__ void tile_setup(const DevGrid& g, int b, const int* __restrict__ cell_start, BlockShared& S, Tile& T) {
-  const int zb = b % g.nzb;
-  const int t2 = b / g.nzb;
-  const int jy = t2 % g.nby, jx = t2 / g.nby;
+  int jx, jy, zb;
+  block_coords(g, b, jx, jy, zb);
   T.ix0 = g.ix_first + jx * g.bx;
   T.iy0 = jy * g.by;
   T.z0 = zb * g.KZ;
@@ -1127,7 +1141,8 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_force(DevGrid g, DevPhys ph, De
 __global__ void k_tile_sizes(DevGrid g, const int* __restrict__ cell_start, int* max_tile, int* max_i) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= g.nblocks) return;
-  const int zb = b % g.nzb, t2 = b / g.nzb, jy = t2 % g.nby, jx = t2 / g.nby;
+  int jx, jy, zb;
+  block_coords(g, b, jx, jy, zb);
   const int ix0 = g.ix_first + jx * g.bx, iy0 = jy * g.by;
   const int z0 = zb * g.KZ, z1 = min(g.nz, z0 + g.KZ);
   int tot = 0, ni = 0;

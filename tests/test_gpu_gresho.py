@@ -1,6 +1,6 @@
 """Gresho-Chan vortex to t = 0.1 (Fig. 6, Eqs. 27-28):
 the KDK integrator with all three loops and both switches, judged against the analytic
-solution.  At 64^3 the L1 error of v_theta is ~0.05 and of P ~0.04 (128^3: 0.040 / 0.038,
+solution.  At 64^3 the L1 error of v_theta is 0.027 and of P 0.032 (128^3: 0.040 / 0.038,
 profiles/r01/gresho128.json); the bounds below catch a broken loop (a wrong sign or factor
 in the force loop puts L1(v_theta) above 0.2 within a few steps) while leaving room for the
 scheme's own smoothing of the v_theta kink at r = 0.2.  Total momentum and energy are

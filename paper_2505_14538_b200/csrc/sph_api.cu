@@ -30,7 +30,7 @@ namespace {
 
 constexpr int kLcapInit = 96;         // neighbour-list capacity per particle (entries, multiple of 8)
 constexpr size_t kSmemMax = 227 * 1024;
-constexpr size_t kSmemTarget = 106 * 1024;  // two CTAs per SM for the largest (force) tile (+ static smem)
+constexpr size_t kSmemTarget = 107 * 1024;  // two CTAs per SM for the largest (force) tile (+ static smem)
 
 __global__ void k_hmax(int n, const uint4* __restrict__ xh, unsigned int* out) {
   unsigned int m = 0;
@@ -371,6 +371,7 @@ sph_status alloc_state(sph_ctx* c) {
   CK(dalloc(&s.active, n)); CK(dalloc(&s.grad, n)); CK(dalloc(&s.fr1, n)); CK(dalloc(&s.fr2, n));
   CK(dalloc(&s.vsig, n)); CK(dalloc(&s.countf, n));
   CK(dalloc(&s.ncount, n)); CK(dalloc(&s.hbuild, n));
+  CK(cudaMemset(s.ncount, 0, n * sizeof(int32_t)));  // k_lists reads it as a length hint
   CK(dalloc(&s.nbr, n * (size_t)c->lcap));
   c->nbr_cap = n * (size_t)c->lcap;
   CK(dalloc(&c->keys, n)); CK(dalloc(&c->keys_alt, n)); CK(dalloc(&c->perm, n)); CK(dalloc(&c->perm_alt, n));
@@ -817,13 +818,13 @@ sph_status rebuild_impl(sph_ctx* c) {
   if ((st = allreduce(c, &ntot, 1, kSum)) != SPH_OK) return st;  // same KZ on every rank
   const double occ = std::max(ntot, 1.0) / ((double)R * g.nxo * g.ny * g.nz);
   const int kz_max = std::min(kMaxTileCellsZ - 2, g.nz > 3 ? g.nz - 3 : 1);
-  // largest KZ whose force tile (68 B per slot + 32 B per block particle) fits the target,
-  // from the mean occupancy with a 25% margin; then checked against the real maximum below
+  // largest KZ whose force tile (64 B per slot + 32 B per block particle) fits the target,
+  // from the mean occupancy with a 10% margin; then checked against the real maximum below
   int KZ = 1;
   for (int k = 2; k <= kz_max; ++k) {
-    const double slots = 1.25 * occ * (g.bx + 2) * (g.by + 2) * (k + 2);
-    const double icnt = 1.25 * occ * g.bx * g.by * k;
-    if (68.0 * slots + 32.0 * icnt > (double)kSmemTarget) break;
+    const double slots = 1.1 * occ * (g.bx + 2) * (g.by + 2) * (k + 2);
+    const double icnt = 1.1 * occ * g.bx * g.by * k;
+    if (64.0 * slots + 32.0 * icnt > (double)kSmemTarget) break;
     KZ = k;
   }
   if (c->cfg.tile_cells_z > 0) KZ = c->cfg.tile_cells_z;
@@ -843,7 +844,7 @@ sph_status rebuild_impl(sph_ctx* c) {
     g.icap = std::max(32, (int)tmax[1]);
     g.lcap = c->lcap;
     g.skin = c->cfg.cell_skin;
-    const bool fits = force_smem(g) <= kSmemMax && lists_smem(g) <= kSmemMax && g.tcap < 65535;
+    const bool fits = force_smem(g) <= kSmemMax && lists_smem(g) <= kSmemMax && g.tcap < 65520;
     if (fits && (force_smem(g) <= kSmemTarget || KZ == 1)) break;
     if (fits && c->cfg.tile_cells_z > 0) break;
     if (KZ == 1) {
@@ -888,8 +889,9 @@ sph_status build_lists(sph_ctx* c) {
     {
       Timed tm(c, SPH_T_LISTS);
       CK(launch_lists(c->grid, c->phys, c->s, c->cell_start, c->ctr, c->stream));
+      CK(launch_bank(c->gL, c->n_own, c->grid, c->s, c->stream));
     }
-    c->launches++;
+    c->launches += 2;
     sph_status st = sync_ctr(c);
     if (st != SPH_OK) return st;
     double over = c->ctr_h->list_overflow, bad = c->ctr_h->nonfinite == 2 ? 1 : 0;

@@ -15,7 +15,7 @@
 
 namespace sph {
 
-constexpr int kMaxTileCellsZ = 32;          // z cells per block + 2 halo cells
+constexpr int kMaxTileCellsZ = 16;          // z cells per block + 2 halo cells
 constexpr int kMaxTileCells = 16 * kMaxTileCellsZ;  // (BX+2)(BY+2) <= 16 tile columns
 constexpr float kPi = 3.14159265358979323846f;
 
@@ -30,7 +30,7 @@ struct DevGrid {
   int ncells;
   int tcap;           // tile capacity (particles) the launch is sized for; slot tcap = sentinel
   int icap;           // most i particles (owned by the block) of any block
-  int lcap;           // neighbour-list capacity per particle (multiple of 8)
+  int lcap;           // neighbour-list capacity per particle (multiple of 16)
   float skin;         // list radius = (1 + skin) max(H_i, H_j)
   float scale[3];     // L_a / 2^32 as f32 (fixed point -> length)
   double dscale[3];   // L_a * 2^-32 exact (fp64 exact neighbour test)
@@ -82,9 +82,11 @@ struct DevState {
   float4* acc;        // a, du
   float* vsig;
   int32_t* countf;
-  // neighbour lists (tile-relative uint16 slots, padded to 8 with the sentinel slot)
-  uint16_t* nbr;      // [n][lcap]
-  int32_t* ncount;    // padded list length
+  // neighbour lists: tile-relative uint16 slots padded with sentinel slots (tcap .. tcap+7) to
+  // a multiple of 8, in ROWS of 8 whose entry w lies in shared-memory bank group w (slot mod 8;
+  // k_bank, sph_kernels.cu); [n][lcap]
+  uint16_t* nbr;
+  int32_t* ncount;    // padded list length (multiple of 8)
   float* hbuild;      // h when the list was built
 };
 
@@ -116,6 +118,7 @@ size_t lists_smem(const DevGrid& g);
 size_t density_smem(const DevGrid& g);
 size_t gradient_smem(const DevGrid& g);
 size_t force_smem(const DevGrid& g);
+cudaError_t launch_bank(int i0, int n, const DevGrid& g, const DevState& s, cudaStream_t st);
 int kernel_threads();
 
 }  // namespace sph

@@ -7,11 +7,24 @@
 // 3 contiguous ranges of the cell-sorted arrays per column, staged into shared memory with
 // cp.async (LDGSTS) and converted from fixed point to f32 offsets from the block centre.
 //
+// Bank-aware rows.  A loop gathers the records of 8 list entries per lane and step from the
+// shared tile with one 16-byte load per record; the 8 lanes of a quarter-warp (one
+// shared-memory phase) are conflict-free when their 8 slots lie in distinct 16-byte bank
+// groups (slot mod 8).  The walk reads row entry (u + lane) mod 8 at sub-step u, so a row
+// whose entry w lies in bank group w gives distinct groups to the 8 lanes at every sub-step,
+// whatever rows and particles they are on.  k_bank therefore places the t-th entry of group
+// b at row t, column b (t < R = ceil(n / 8)); the rare overflow of a group past R rows fills
+// the free cells left (those gathers may conflict), every other free cell gets the sentinel
+// slot of its group (tcap + group, a far-away zero record).  Lists longer than 8 kCellRows,
+// or with a group of more than kCellRows entries, keep the natural order (correct, more
+// conflicts).
+//
 // Neighbour lists.  k_lists tests, once per cell rebuild (and again only if an h outgrows
 // its list radius), each particle's candidates in its 3 x 3 neighbour columns inside a z
 // window of +-R (cells are z-sorted by the binning key, so a binary search finds the
 // window) and stores, per particle, the tile slots j with r_ij < (1 + skin) max(H_i, H_j)
-// (self included) as uint16, padded to a multiple of 8 with a sentinel slot.  The density passes, the gradient loop and the force
+// (self included) as uint16, padded to a multiple of 8 with sentinel slots, in ROWS of 8 whose
+// entry w lies in shared-memory bank group w (see "Bank-aware rows").  The density passes, the gradient loop and the force
 // loop then run the pair arithmetic over these lists only: every lane works on a real (or
 // skin) neighbour, no candidate is re-tested (the paper's pair tasks test all particle
 // pairs of two cells).  Skin entries, the sentinel and the self pair contribute
@@ -35,6 +48,7 @@ constexpr int kNW = 8;              // warps per CTA
 constexpr float kFar = 1.0e12f;     // sentinel position (tile coordinates)
 constexpr int kMaxICols = 4;        // BX * BY <= 4
 constexpr int kMaxSeg = 3 * 16;     // <= 3 contiguous segments per tile column
+constexpr int kNSent = 8;           // sentinel slots tcap .. tcap+7, one per 16-byte bank group
 
 struct Tile {
   int ix0, iy0, z0, z1, nzt, ntc, nct, ntile, ncol, ni;
@@ -303,7 +317,7 @@ __device__ __forceinline__ void for_list(const uint16_t* __restrict__ list, int 
     return;                                               \
   }                                                       \
   const int nseg = 3 * T.ntc;                             \
-  const int SP = g.tcap + 1; /* slots per record array (last = sentinel) */
+  const int SP = g.tcap + kNSent; /* slots per record array (the last kNSent are sentinels) */
 
 // ========================================================== neighbour lists ==========
 // For every particle i of the block: all tile slots j (self included) with
@@ -321,12 +335,19 @@ __device__ __forceinline__ void for_list(const uint16_t* __restrict__ list, int 
 // per-warp buffer in shared memory and leave for global memory 8 at a time (16-byte stores).
 constexpr int kMaxICells = kMaxICols * (kMaxTileCellsZ - 2);
 constexpr int kListRows = 32;  // ring rows per lane (<= 7 left + 2 single tests + 16 per group)
+constexpr int kCellRows = 16;  // k_bank grid rows per list (longer lists keep the natural order)
+// (the per-lane list buffers are touched only through these volatile asm statements, which
+// keep their order; no memory clobber, so the compiler may move tile loads across them)
 __device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
-  asm volatile("st.shared.u16 [%0], %1;\n" ::"r"(a), "h"((unsigned short)v) : "memory");
+  asm volatile("st.shared.u16 [%0], %1;\n" ::"r"(a), "h"((unsigned short)v));
+}
+__device__ __forceinline__ void sts_u16_if(uint32_t a, uint32_t v, bool p) {
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.shared.u16 [%0], %1; }\n" ::"r"(a),
+               "h"((unsigned short)v), "r"((uint32_t)p));
 }
 __device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
   unsigned short v;
-  asm volatile("ld.shared.u16 %0, [%1];\n" : "=h"(v) : "r"(a) : "memory");
+  asm volatile("ld.shared.u16 %0, [%1];\n" : "=h"(v) : "r"(a));
   return v;
 }
 __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, DevState s,
@@ -494,11 +515,11 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
           drain();
         }
       }
-      // pad to a multiple of 8 with the sentinel slot, flush
+      // pad to a multiple of 8 with sentinel slots (one per bank group), flush
       int nb = (int)(((w - rd) & (kRing - 1u)) >> 6);
       const int cnt = flushed + nb;
       const int cntp = (cnt + 7) & ~7;
-      for (; nb < ((nb + 7) & ~7); ++nb) hit(true, g.tcap);
+      for (; nb < ((nb + 7) & ~7); ++nb) hit(true, g.tcap + (nb & 7));
       drain();
       if (cntp > g.lcap) over = max(over, cntp);
       s.ncount[gi] = min(cntp, g.lcap);
@@ -507,6 +528,83 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
   }
   over = warp_max(over);
   if (lane == 0 && over) atomicMax(&ctr->list_overflow, over);
+}
+
+// k_bank: the bank-aware row layout ("Bank-aware rows" above) of every list of at most
+// 8 kCellRows entries, one lane per list, in one pass over the natural-order list: the t-th
+// real entry of group b goes to cell (t, b) of the lane's grid in shared memory; then the
+// entries of a group past row R = ncount / 8 move to free cells, the other free cells get the
+// group's sentinel, and the R rows are written back.
+__global__ void __launch_bounds__(256) k_bank(int i0, int n, DevGrid g, DevState s) {
+  extern __shared__ unsigned short kb[];  // cell (r, w) of thread t at kb[(8 r + w) * 256 + t]
+  const int i = i0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= i0 + n) return;
+  const int cnt8 = s.ncount[i];
+  if (cnt8 <= 0 || cnt8 > 8 * kCellRows) return;
+  const int R = cnt8 >> 3;
+  uint4* lst = reinterpret_cast<uint4*>(s.nbr + (size_t)i * g.lcap);
+  const uint32_t tcap = (uint32_t)g.tcap;
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(kb) + 2u * threadIdx.x;
+  auto cell = [&](uint32_t r, uint32_t w) { return base + (8u * r + w) * 512u; };
+  unsigned long long run = 0ull;  // entries of each group so far (bytes)
+  uint4 v = __ldg(lst);
+  for (int r = 0; r < R; ++r) {
+    const uint4 nx = r + 1 < R ? __ldg(lst + r + 1) : v;
+    const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t hsl = (wv[k >> 1] >> (16 * (k & 1))) & 0xffffu;
+      const uint32_t b = hsl & 7u;
+      const uint32_t tb = (uint32_t)(run >> (8u * b)) & 0xffu;
+      sts_u16_if(cell(min(tb, (uint32_t)kCellRows - 1u), b), hsl, hsl < tcap);
+      run += (unsigned long long)(hsl < tcap ? 1u : 0u) << (8u * b);
+    }
+    v = nx;
+  }
+  int cntq[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) cntq[q] = (int)((run >> (8 * q)) & 0xffull);
+  bool ovf = false;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) ovf = ovf || cntq[q] > kCellRows;
+  if (ovf) return;  // a group past the grid: the list keeps its natural order
+  int ow = 0, orow = 0;
+  auto colcnt = [&](int q) {
+    int c = cntq[0];
+#pragma unroll
+    for (int x = 1; x < 8; ++x) c = q == x ? cntq[x] : c;
+    return c;
+  };
+  auto place = [&](uint32_t hv) {  // next free cell: rows >= the count of the column
+    for (;;) {
+      const int cw = colcnt(ow);
+      if (orow < cw) orow = cw;
+      if (orow < R) break;
+      ++ow;
+      orow = 0;
+    }
+    sts_u16(cell((uint32_t)orow, (uint32_t)ow), hv);
+    ++orow;
+  };
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+    for (int r = R; r < cntq[q]; ++r) place(lds_u16(cell((uint32_t)r, (uint32_t)q)));
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    int r0 = min(cntq[q], R);
+    if (q < ow) r0 = R;
+    else if (q == ow) r0 = max(r0, orow);
+    const uint32_t sent = tcap + (((uint32_t)q - tcap) & 7u);
+    for (int r = r0; r < R; ++r) sts_u16(cell((uint32_t)r, (uint32_t)q), sent);
+  }
+  for (int r = 0; r < R; ++r) {
+    uint4 o;
+    o.x = lds_u16(cell(r, 0)) | (lds_u16(cell(r, 1)) << 16);
+    o.y = lds_u16(cell(r, 2)) | (lds_u16(cell(r, 3)) << 16);
+    o.z = lds_u16(cell(r, 4)) | (lds_u16(cell(r, 5)) << 16);
+    o.w = lds_u16(cell(r, 6)) | (lds_u16(cell(r, 7)) << 16);
+    lst[r] = o;
+  }
 }
 
 // ================================================ balanced walk over the lists ==========
@@ -571,6 +669,8 @@ __device__ __forceinline__ void walk_lists(int ni, const int* __restrict__ pref,
     const int mid = (lo + hi) >> 1;
     if (pref[mid] <= g0) lo = mid; else hi = mid;
   }
+  const int rot = threadIdx.x & 7;
+  const uint32_t sh = 16u * (uint32_t)(rot & 1);
   int k = lo;
   int p0 = pref[k], p1 = pref[k + 1];
   const uint4* list = reinterpret_cast<const uint4*>(list_of(k)) + (g0 - p0);
@@ -587,7 +687,18 @@ __device__ __forceinline__ void walk_lists(int ni, const int* __restrict__ pref,
       list = reinterpret_cast<const uint4*>(list_of(k));
       begin(k);
     }
-    const uint4 e = __ldg(list);
+    uint4 e = __ldg(list);
+    // rotate the row by rot entries (k_bank: entry w lies in bank group w), so the 8 lanes
+    // of a shared-memory phase gather from 8 distinct bank groups at every sub-step
+    if (rot & 4) { const uint32_t a = e.x, b = e.y; e.x = e.z; e.y = e.w; e.z = a; e.w = b; }
+    if (rot & 2) { const uint32_t a = e.x; e.x = e.y; e.y = e.z; e.z = e.w; e.w = a; }
+    {
+      const uint32_t a = e.x;
+      e.x = __funnelshift_r(e.x, e.y, sh);
+      e.y = __funnelshift_r(e.y, e.z, sh);
+      e.z = __funnelshift_r(e.z, e.w, sh);
+      e.w = __funnelshift_r(e.w, a, sh);
+    }
     pair((int)(e.x & 0xffffu));
     pair((int)(e.x >> 16));
     pair((int)(e.y & 0xffffu));
@@ -681,9 +792,9 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_density(DevGrid g, DevPhys ph, 
     const float3 p = rel_pos(g, T, x);
     smem4[t] = make_float4(p.x, p.y, p.z, __uint_as_float(x.w));
   }
-  if (threadIdx.x == 0) {
-    smem4[g.tcap] = make_float4(kFar, kFar, kFar, 1.f);
-    smem4[O1 + g.tcap] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (threadIdx.x < kNSent) {
+    smem4[g.tcap + threadIdx.x] = make_float4(kFar, kFar, kFar, 1.f);
+    smem4[O1 + g.tcap + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   // the walk's particles: all of the block (pass 0) or the still active ones, compacted in
   // block order (deterministic)
@@ -742,8 +853,11 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_density(DevGrid g, DevPhys ph, 
                                             g.dscale[2]);
             a.nn += (int)ex - neg(d);
           }
-          float w, dw;
-          m4(q, w, dw);
+          // M4 as truncated powers: w = t^3/4 - s^3, w' = -3/4 t^2 + 3 s^2 (t = (2-q)+, s = (1-q)+)
+          const float tq = fmaxf(-d, 0.f), sq = fmaxf(1.f - q, 0.f);
+          const float t2 = tq * tq, s2 = sq * sq;
+          const float w = fmaf(0.25f * tq, t2, -sq * s2);
+          const float dw = fmaf(3.f, s2, -0.75f * t2);
           const float qdw = q * dw;
           a.S0 += w;
           a.S1 += qdw;
@@ -874,10 +988,10 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_gradient(DevGrid g, DevPhys ph,
     const float3 p = rel_pos(g, T, x);
     smem4[t] = make_float4(p.x, p.y, p.z, __uint_as_float(x.w));
   }
-  if (threadIdx.x == 0) {
-    smem4[g.tcap] = make_float4(kFar, kFar, kFar, 1.f);
-    smem4[O1 + g.tcap] = make_float4(0.f, 0.f, 0.f, 0.f);
-    smem4[O2 + g.tcap] = make_float4(0.f, 0.f, 0.f, 1.f);
+  if (threadIdx.x < kNSent) {
+    smem4[g.tcap + threadIdx.x] = make_float4(kFar, kFar, kFar, 1.f);
+    smem4[O1 + g.tcap + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
+    smem4[O2 + g.tcap + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 1.f);
   }
   const int ni = T.ni;
   for (int k = threadIdx.x; k < ni; k += kNT) W.kl[k] = k;
@@ -922,7 +1036,8 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_gradient(DevGrid g, DevPhys ph,
           if (fabsf(d) < qband)
             in = exact_neighbour(s.xh, gi, slot_global(S, T.nct, j), H2, g.dscale[0], g.dscale[1], g.dscale[2]);
           a.nn += in;
-          const float dw = m4_dw(q);
+          const float tq = fmaxf(-d, 0.f), sq = fmaxf(1.f - q, 0.f);
+          const float dw = fmaf(3.f * sq, sq, -0.75f * tq * tq);  // M4 w'(q)
           const float vr = fmaf(vi4.z - q4.z, dz, fmaf(vi4.y - q4.y, dy, (vi4.x - q4.x) * dx));
           const float mu = fminf(vr, 0.f) * rinv;
           const float vs = fmaf(-ph.beta, mu, ci + g4.x);
@@ -967,8 +1082,10 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_gradient(DevGrid g, DevPhys ph,
     s.dprev[gi] = div;
     const float rho = gi4.w;
     const float f = fin.x, P = fin.y;
-    s.fr1[gi] = make_float4(P / (rho * rho), f * hinv * hinv * hinv * hinv / kPi, ci, rho);
-    s.fr2[gi] = make_float4(fin.w, P * ac, ui, av);  // (B, P alpha_c, u, alpha_v); P = A rho^2
+    // force records: (A = P/rho^2, K = -0.75 f/(pi h^4), c, rho) and (B, P alpha_c -- or
+    // -alpha_c when P = 0, for Eq. 20's P_i + P_j = 0 case (R13) --, u, alpha_v); P = A rho^2
+    s.fr1[gi] = make_float4(P / (rho * rho), -0.75f * f * hinv * hinv * hinv * hinv / kPi, ci, rho);
+    s.fr2[gi] = make_float4(fin.w, P > 0.f ? P * ac : -ac, ui, av);
   }
   const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -979,13 +1096,14 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_gradient(DevGrid g, DevPhys ph,
 }
 
 // ================================================================ force loop ==========
-// Gather form of the pairwise sums of Eqs. 7, 17-19 over r_ij < max(H_i, H_j) (R3):
-//   G = f dW/dr / r, A = P/rho^2, Pi_ij = -abar mu v_sig / rhobar (R9), Gbar = (G_i+G_j)/2,
-//   S_ij = A_i G_i + A_j G_j + Pi_ij Gbar,  a_i = -sum_j m_j S_ij r_ij,
-//   du_i = sum_j m_j [A_i G_i v.r + Pi Gbar v.r / 2 + D_ij]  (Eq. 18 + R10 + Eq. 19/R11),
-//   D_ij = alpha_c,ij v_c,ij (u_i - u_j)(G_i + G_j) r / (rho_i + rho_j)  (Eqs. 20, 22; R12, R13).
-// S_ij is evaluated from operands that are symmetric in (i, j), so the pair terms of i and
-// j are exact negatives (momentum and energy conserving up to the summation rounding).
+// Gather form of the pairwise sums of Eqs. 7, 17-19 over r_ij < max(H_i, H_j) (R3), written
+// with g = G r = f dW/dr (the r factors cancel):
+//   A = P/rho^2, Pi_ij = -abar mu v_sig / rhobar (R9), gbar = (g_i + g_j)/2,
+//   T = A_i g_i + A_j g_j + Pi_ij gbar  (= S_ij r),   a_i = -sum_j m_j T r_ij / r,
+//   du_i = sum_j m_j [(A_i g_i + Pi gbar / 2)(v_ij . r_hat) + D_ij]  (Eq. 18 + R10 + Eq. 19/R11),
+//   D_ij = alpha_c,ij v_c,ij (u_i - u_j)(g_i + g_j) / (rho_i + rho_j)  (Eqs. 20, 22; R12, R13).
+// T is evaluated from operands symmetric in (i, j), so the pair terms of i and j are exact
+// negatives (momentum and energy conserving up to the summation rounding).
 // The CFL dt = C_cfl min 2 gamma_k h / v_sig is reduced in the epilogue.
 struct ForceAcc {
   float ax, ay, az, du, vmax;  // vmax > 0: max over its f32 bits as int
@@ -998,7 +1116,13 @@ struct ForceAcc {
   }
 };
 __host__ __device__ __forceinline__ size_t force_records_bytes(int tcap) {
-  return (size_t)(tcap + 1) * (4 * 16);
+  return (size_t)(tcap + kNSent) * (4 * 16);
+}
+
+// -dW/dq / 0.75 of M4: q (4 - 3q) for q < 1, (2 - q)^2 for 1 <= q < 2, 0 beyond
+__device__ __forceinline__ float m4_dwp(float q) {
+  const float t = fmaxf(2.f - q, 0.f);
+  return q < 1.f ? q * fmaf(-3.f, q, 4.f) : t * t;
 }
 
 __global__ void __launch_bounds__(kNW * 32, 2) k_force(DevGrid g, DevPhys ph, DevState s,
@@ -1007,7 +1131,8 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_force(DevGrid g, DevPhys ph, De
   __shared__ unsigned long long s_pairs;
   __shared__ unsigned int s_dt;
   __shared__ int s_bad;
-  if (threadIdx.x == 0) { s_pairs = 0; s_dt = 0x7f800000u; s_bad = 0; }
+  __shared__ unsigned int s_hinv_max;  // largest 1/h of the tile (f32 bits)
+  if (threadIdx.x == 0) { s_pairs = 0; s_dt = 0x7f800000u; s_bad = 0; s_hinv_max = 0u; }
   TILE_PROLOGUE();
   // T0 = [j]: x, y, z, 1/h   T1 = [O1+j]: vx, vy, vz, m   T2 = [O2+j]: A, Kf, c, rho
   // T3 = [O3+j]: B, P alpha_c, u, alpha_v  (P = A rho^2: four 16-byte records per pair)
@@ -1019,24 +1144,37 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_force(DevGrid g, DevPhys ph, De
     const int o16[4] = {0, O1, O2, O3};
     stage_records(S, nseg, 4, src, o16, nullptr, 0);
   }
-  for (int t = threadIdx.x; t < T.ntile; t += blockDim.x) {
-    const uint4 x = reinterpret_cast<const uint4*>(smem4)[t];
-    const float3 p = rel_pos(g, T, x);
-    smem4[t] = make_float4(p.x, p.y, p.z, 1.f / __uint_as_float(x.w));
+  {
+    unsigned int hm = 0u;
+    for (int t = threadIdx.x; t < T.ntile; t += blockDim.x) {
+      const uint4 x = reinterpret_cast<const uint4*>(smem4)[t];
+      const float3 p = rel_pos(g, T, x);
+      const float hinv = 1.f / __uint_as_float(x.w);
+      hm = max(hm, __float_as_uint(hinv));
+      smem4[t] = make_float4(p.x, p.y, p.z, hinv);
+    }
+    hm = (unsigned int)warp_max((int)hm);
+    if ((threadIdx.x & 31) == 0 && hm) atomicMax(&s_hinv_max, hm);
   }
-  if (threadIdx.x == 0) {
-    smem4[g.tcap] = make_float4(kFar, kFar, kFar, 1.f);
-    smem4[O1 + g.tcap] = make_float4(0.f, 0.f, 0.f, 0.f);
-    smem4[O2 + g.tcap] = make_float4(0.f, 0.f, 0.f, 1.f);
-    smem4[O3 + g.tcap] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (threadIdx.x < kNSent) {
+    smem4[g.tcap + threadIdx.x] = make_float4(kFar, kFar, kFar, 1.f);
+    smem4[O1 + g.tcap + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
+    smem4[O2 + g.tcap + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 1.f);
+    smem4[O3 + g.tcap + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   const int ni = T.ni;
   for (int k = threadIdx.x; k < ni; k += kNT) W.kl[k] = k;
   __syncthreads();
   walk_prefix(S, s, W, ni);
   {
+    const float4* __restrict__ T0 = smem4;
+    const float4* __restrict__ T1 = smem4 + O1;
+    const float4* __restrict__ T2 = smem4 + O2;
+    const float4* __restrict__ T3 = smem4 + O3;
+    // |min(q_i, q_j) - 2| below this: decide in fp64 (eabs / min h of the tile)
+    const float band = g.eabs * __uint_as_float(s_hinv_max) + 8e-6f;
     float4 pi4, vi4, ai, bi;
-    float Pi = 0.f, hinv_i = 0.f, ebi = 0.f;
+    float Pi = 0.f;
     int gi = 0;
     ForceAcc a;
     walk_lists(
@@ -1049,55 +1187,57 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_force(DevGrid g, DevPhys ph, De
         [&](int k) {
           int ti;
           i_slot(S, k, ti, gi);
-          pi4 = smem4[ti];
-          vi4 = smem4[O1 + ti];
-          ai = smem4[O2 + ti];
-          bi = smem4[O3 + ti];
+          pi4 = T0[ti];
+          vi4 = T1[ti];
+          ai = T2[ti];
+          bi = T3[ti];
           Pi = ai.x * ai.w * ai.w;
-          hinv_i = pi4.w;
-          ebi = g.eabs * hinv_i;
           a = ForceAcc{0.f, 0.f, 0.f, 0.f, 2.f * ai.z, 0};
         },
         [&](int j) {
-          const float4 p = smem4[j];
+          const float4 p = T0[j];
           const float dx = pi4.x - p.x, dy = pi4.y - p.y, dz = pi4.z - p.z;
           const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-          const float4 vj = smem4[O1 + j];
-          const float4 aj = smem4[O2 + j];
-          const float4 bj = smem4[O3 + j];
+          const float4 vj = T1[j];
+          const float4 aj = T2[j];
+          const float4 bj = T3[j];
           const float rinv = rinv_safe(r2);
           const float r = r2 * rinv;
-          const float qi = r * hinv_i, qj = r * p.w;
+          const float qi = r * pi4.w, qj = r * p.w;
           const float d = fminf(qi, qj) - 2.f;
           int in = neg(d);
-          if (fabsf(d) < fmaxf(ebi, g.eabs * p.w) + 8e-6f) {
+          if (fabsf(d) < band) {
             const int gj = slot_global(S, T.nct, j);
             const double H2 = fmax(h2_exact(__uint_as_float(s.xh[gi].w), ph.gamma_k),
                                    h2_exact(__uint_as_float(s.xh[gj].w), ph.gamma_k));
             in = exact_neighbour(s.xh, gi, gj, H2, g.dscale[0], g.dscale[1], g.dscale[2]);
           }
           a.nn += in;
-          const float Gi = ai.y * m4_dw(qi) * rinv;
-          const float Gj = aj.y * m4_dw(qj) * rinv;
+          const float gI = ai.y * m4_dwp(qi);  // g_i = G_i r = f_i dW/dr(h_i)
+          const float gJ = aj.y * m4_dwp(qj);
           const float vr = fmaf(vi4.z - vj.z, dz, fmaf(vi4.y - vj.y, dy, (vi4.x - vj.x) * dx));
-          const float mu = fminf(vr, 0.f) * rinv;
+          const float vrr = vr * rinv;
+          const float mu = fminf(vrr, 0.f);
           const float vs = fmaf(-ph.beta, mu, ai.z + aj.z);
           a.vmax = fmaxf(a.vmax, in ? vs : 0.f);
-          const float abar = 0.25f * (bi.w + bj.w) * (bi.x + bj.x);
           const float irs = __fdividef(1.f, ai.w + aj.w);
-          const float PiV = -2.f * abar * mu * vs * irs;
-          const float Gbar = 0.5f * (Gi + Gj);
-          const float Sij = fmaf(PiV, Gbar, fmaf(ai.x, Gi, aj.x * Gj));
-          const float mS = vj.w * Sij;
-          a.ax = fmaf(-mS, dx, a.ax);
-          a.ay = fmaf(-mS, dy, a.ay);
-          a.az = fmaf(-mS, dz, a.az);
+          const float gs = gI + gJ;
+          // X = 4 abar mu v_sig (g_i + g_j) / (rho_i + rho_j):  Pi_ij gbar = -X / 4
+          const float X = ((bi.w + bj.w) * (bi.x + bj.x)) * (mu * vs) * (gs * irs);
+          const float AgI = ai.x * gI;
+          const float Tij = fmaf(aj.x, gJ, fmaf(-0.25f, X, AgI));  // S_ij r
+          const float mT = vj.w * Tij * rinv;
+          a.ax = fmaf(-mT, dx, a.ax);
+          a.ay = fmaf(-mT, dy, a.ay);
+          a.az = fmaf(-mT, dz, a.az);
           const float Pj = aj.x * aj.w * aj.w;
+          // alpha_c,ij (Eq. 20): (P_i ac_i + P_j ac_j) / (P_i + P_j), or the mean when
+          // P_i + P_j = 0 (R13; the records then hold -alpha_c)
           const float Psum = Pi + Pj;
-          const float acij = Psum > 0.f ? __fdividef(bi.y + bj.y, Psum) : 0.f;
-          const float vc = fabsf(vr) * rinv + sqrtf(2.f * fabsf(Pi - Pj) * irs);
-          const float D = acij * vc * (bi.z - bj.z) * (Gi + Gj) * r * irs;
-          a.du = fmaf(vj.w, fmaf(ai.x * Gi, vr, fmaf(0.5f * PiV * Gbar, vr, D)), a.du);
+          const float acij = __fdividef(bi.y + bj.y, Psum > 0.f ? Psum : -2.f);
+          const float vc = fabsf(vrr) + sqrtf(2.f * fabsf(Pi - Pj) * irs);
+          const float D = acij * vc * (bi.z - bj.z) * (gs * irs);
+          a.du = fmaf(vj.w, fmaf(fmaf(-0.125f, X, AgI), vrr, D), a.du);
         },
         [&]() { return a; });
   }
@@ -1169,10 +1309,10 @@ __global__ void k_tile_sizes(DevGrid g, const int* __restrict__ cell_start, int*
 int kernel_threads() { return kNW * 32; }
 
 size_t lists_smem(const DevGrid& g) {
-  return (size_t)((g.tcap + 2) & ~1) * 16 + (size_t)kNW * kListRows * 32 * 2;
+  return (size_t)((g.tcap + kNSent + 1) & ~1) * 16 + (size_t)kNW * kListRows * 32 * 2;
 }
-size_t density_smem(const DevGrid& g) { return (size_t)(g.tcap + 1) * (2 * 16) + walk_bytes<DenAcc>(g.icap); }
-size_t gradient_smem(const DevGrid& g) { return (size_t)(g.tcap + 1) * (3 * 16) + walk_bytes<GradAcc>(g.icap); }
+size_t density_smem(const DevGrid& g) { return (size_t)(g.tcap + kNSent) * (2 * 16) + walk_bytes<DenAcc>(g.icap); }
+size_t gradient_smem(const DevGrid& g) { return (size_t)(g.tcap + kNSent) * (3 * 16) + walk_bytes<GradAcc>(g.icap); }
 size_t force_smem(const DevGrid& g) { return force_records_bytes(g.tcap) + walk_bytes<ForceAcc>(g.icap); }
 
 cudaError_t launch_tile_sizes(const DevGrid& g, const int* cell_start, int* max_tile, int* max_i, cudaStream_t st) {
@@ -1192,6 +1332,16 @@ cudaError_t launch_lists(const DevGrid& g, const DevPhys& ph, const DevState& s,
   k_lists<<<g.nblocks, kNW * 32, sm, st>>>(g, ph, s, cell_start, ctr);
   return cudaGetLastError();
 }
+
+cudaError_t launch_bank(int i0, int n, const DevGrid& g, const DevState& s, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const size_t sm = (size_t)8 * kCellRows * 256 * 2;
+  cudaError_t e = set_smem((const void*)k_bank, sm);
+  if (e != cudaSuccess) return e;
+  k_bank<<<(n + 255) / 256, 256, sm, st>>>(i0, n, g, s);
+  return cudaGetLastError();
+}
+
 
 cudaError_t launch_density(const DevGrid& g, const DevPhys& ph, const DevState& s, const int* cell_start, int pass,
                            const uint8_t* blk_in, uint8_t* blk_out, float hfac_stale, DevCounters* ctr,

@@ -93,6 +93,10 @@ typedef struct {
   int32_t transport;      /* sph_transport, used when nranks > 1                            */
   const void* nccl_uid;   /* NCCL: 128-byte id from sph_nccl_unique_id on rank 0, same on all*/
   void* loopback;         /* LOOPBACK: group from sph_loopback_create (shared by the ranks)  */
+  int32_t adaptive_h;     /* one rank, strong h contrast: when the cells sized */
+                          /* from h_max overflow the tiles, size them from an h quantile and   */
+                          /* treat the particles whose support exceeds a cell as "wide"       */
+                          /* (global-index lists); default 1, 0 = fail instead */
 } sph_config;
 
 /* Particle input.  n particles; arrays are host pointers (on_device = 0) or device
@@ -129,6 +133,7 @@ typedef struct {
   int64_t pairs_h_iter;    /* last sph_density: directed pairs over all passes             */
   int64_t coincident;      /* pairs with r_ij = 0, j != i, skipped                 */
   int64_t kernel_launches; /* kernels launched by this context since creation              */
+  int64_t wide_particles;  /* particles handled as wide by the adaptive grid (last rebuild) */
 } sph_counters;
 
 /* Device-time phases (sph_get_timings). */

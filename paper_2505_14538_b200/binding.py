@@ -47,7 +47,7 @@ class Config(ctypes.Structure):
                 ("c_cfl", ctypes.c_float), ("fh_mode", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("stream", ctypes.c_void_p), ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
                 ("tile_cells_z", ctypes.c_int32), ("predict_h", ctypes.c_int32), ("transport", ctypes.c_int32),
-                ("nccl_uid", ctypes.c_void_p), ("loopback", ctypes.c_void_p)]
+                ("nccl_uid", ctypes.c_void_p), ("loopback", ctypes.c_void_p), ("adaptive_h", ctypes.c_int32)]
 
 SPH_TRANSPORT_NCCL, SPH_TRANSPORT_LOOPBACK = 0, 1
 
@@ -73,7 +73,7 @@ class Timings(ctypes.Structure):
 class Counters(ctypes.Structure):
     _fields_ = [("pairs_density", ctypes.c_int64), ("pairs_gradient", ctypes.c_int64),
                 ("pairs_force", ctypes.c_int64), ("pairs_h_iter", ctypes.c_int64), ("coincident", ctypes.c_int64),
-                ("kernel_launches", ctypes.c_int64)]
+                ("kernel_launches", ctypes.c_int64), ("wide_particles", ctypes.c_int64)]
 
 
 EXPORTS = ["sph_abi_version", "sph_config_default", "sph_create", "sph_set_particles", "sph_rebuild_cells",

@@ -10,12 +10,15 @@
 // has P + 2 planes along x (ghost, owned..., ghost) and is periodic in y and z.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <limits>
 #include <new>
 #include <string>
 #include <vector>
@@ -256,6 +259,17 @@ struct sph_ctx {
   bool lists_stale = true;    // neighbour lists must be rebuilt before the next loop
   size_t nbr_cap = 0;         // allocated list entries (cap x lcap)
   int lcap = kLcapInit;
+  // wide particles (adaptive cell side, sph_wide.cu)
+  float h_side = 0.f;          // h the cell side is sized from (0: the global h_max)
+  uint8_t* wide_flag = nullptr;
+  int32_t* widx = nullptr;
+  int32_t* wcount = nullptr;
+  int* n_wide_dev = nullptr;
+  uint32_t* wnbr = nullptr;
+  size_t wnbr_cap = 0;         // allocated wide-list entries
+  int wlcap = 256;
+  void* sel_tmp = nullptr;
+  size_t sel_tmp_bytes = 0;
   bool dprev_valid = false;
   bool dvc_valid = false;     // dvc (div v) is from a density pass in the current particle order
   bool density_done = false, gradient_done = false;
@@ -615,9 +629,39 @@ sph_status read_cs(sph_ctx* c, int cell, int* v) {
 // Choose the grid for the current h, migrate (several ranks), sort, exchange ghost planes, and
 // size the CTA tiles.
 sph_status rebuild_impl(sph_ctx* c);
+sph_status mark_wide(sph_ctx* c);
+sph_status h_quantile(sph_ctx* c, double q, float* out);
+
+// Cell grid for the current h.  One rank with adaptive_h: when cells sized from h_max do not
+// fit the tiles (strong h contrast), size them from decreasing quantiles of h instead; the
+// particles whose support exceeds a cell then become wide (sph_wide.cu).
 sph_status rebuild(sph_ctx* c) {
   Timed tm(c, SPH_T_REBUILD);
-  return rebuild_impl(c);
+  c->h_side = 0.f;
+  sph_status st = rebuild_impl(c);
+  if (st == SPH_ERR_H_EXCEEDS_CELL && !c->slab && c->cfg.adaptive_h) {
+    const std::string first = c->err;
+    float tried = std::numeric_limits<float>::infinity();
+    for (double q : {0.99, 0.95, 0.9, 0.8, 0.65, 0.5, 0.35, 0.2}) {
+      float hq;
+      const sph_status sq = h_quantile(c, q, &hq);
+      if (sq != SPH_OK) return sq;
+      if (!(hq < tried)) continue;
+      tried = hq;
+      c->h_side = hq;
+      st = rebuild_impl(c);
+      if (getenv("SPH_DEBUG"))
+        fprintf(stderr, "[sph] adaptive grid: h quantile %.2f = %.6g -> status %d (%s)\n", q, hq, (int)st,
+                st == SPH_OK ? "ok" : c->err.c_str());
+      if (st != SPH_ERR_H_EXCEEDS_CELL) break;
+    }
+    if (st == SPH_ERR_H_EXCEEDS_CELL) {
+      c->h_side = 0.f;
+      return fail(c, st, first);
+    }
+  }
+  if (st != SPH_OK) return st;
+  return mark_wide(c);
 }
 
 sph_status rebuild_impl(sph_ctx* c) {
@@ -640,7 +684,8 @@ sph_status rebuild_impl(sph_ctx* c) {
   if ((st = allreduce(c, &hm, 1, kMax)) != SPH_OK) return st;
   const float hmax = (float)hm;
   if (!(hmax > 0.f) || !std::isfinite(hmax)) return fail(c, SPH_ERR_INVALID_ARG, "smoothing lengths must be finite and > 0");
-  const double Hs = (double)c->cfg.gamma_k * hmax * (1.0 + c->cfg.cell_skin);
+  const float hcell = c->h_side > 0.f ? std::min(c->h_side, hmax) : hmax;  // adaptive: an h quantile
+  const double Hs = (double)c->cfg.gamma_k * hcell * (1.0 + c->cfg.cell_skin);
   DevGrid& g = c->grid;
   const int R = c->nranks;
   const bool slab = c->slab;
@@ -879,21 +924,104 @@ sph_status rebuild_impl(sph_ctx* c) {
   return SPH_OK;
 }
 
+__global__ void k_h_keys(int n, const uint4* __restrict__ xh, unsigned int* keys) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) keys[i] = xh[i].w;  // positive f32: ordered as unsigned
+}
+
+// q-quantile of the owned particles' h (device radix sort of the f32 bits)
+sph_status h_quantile(sph_ctx* c, double q, float* out) {
+  const int n = c->n_own;
+  if (n <= 0) return fail(c, SPH_ERR_INVALID_ARG, "no particles");
+  k_h_keys<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->s.xh + c->gL, c->keys);
+  c->launches++;
+  CK(cudaGetLastError());
+  size_t tmp = c->sort_tmp_bytes;
+  CK(cub::DeviceRadixSort::SortKeys(c->sort_tmp, tmp, c->keys, c->keys_alt, n, 0, 32, c->stream));
+  const int k = std::min(n - 1, std::max(0, (int)(q * (n - 1))));
+  CK(cudaMemcpyAsync(c->scratch_h + 9, c->keys_alt + k, 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  std::memcpy(out, c->scratch_h + 9, 4);
+  return SPH_OK;
+}
+
+// Flag and list the wide particles of the current grid (none unless the side was sized from
+// an h quantile).
+sph_status mark_wide(sph_ctx* c) {
+  DevState& s = c->s;
+  s.n_wide = 0;
+  s.wide = nullptr;
+  if (c->h_side <= 0.f || c->slab) return SPH_OK;
+  const int n = c->n_own;
+  if (!c->wide_flag) {
+    CK(dalloc(&c->wide_flag, (size_t)c->cap));
+    CK(dalloc(&c->widx, (size_t)c->cap));
+    CK(dalloc(&c->wcount, (size_t)c->cap));
+    CK(dalloc(&c->n_wide_dev, 1));
+  }
+  CK(launch_mark_wide(n, c->grid, c->phys, s, c->wide_flag, c->stream));
+  c->launches++;
+  cub::CountingInputIterator<int> it(0);
+  size_t need = 0;
+  CK(cub::DeviceSelect::Flagged(nullptr, need, it, c->wide_flag, c->widx, c->n_wide_dev, n, c->stream));
+  if (need > c->sel_tmp_bytes) {
+    if (c->sel_tmp) cudaFree(c->sel_tmp);
+    c->sel_tmp = nullptr;
+    CK(cudaMalloc(&c->sel_tmp, need));
+    c->sel_tmp_bytes = need;
+  }
+  CK(cub::DeviceSelect::Flagged(c->sel_tmp, need, it, c->wide_flag, c->widx, c->n_wide_dev, n, c->stream));
+  c->launches++;
+  CK(cudaMemcpyAsync(c->scratch_h + 10, c->n_wide_dev, 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  int nw;
+  std::memcpy(&nw, c->scratch_h + 10, 4);
+  s.n_wide = nw;
+  s.wide = c->wide_flag;
+  s.widx = c->widx;
+  s.wcount = c->wcount;
+  s.wlcap = c->wlcap;
+  const size_t want = (size_t)std::max(nw, 1) * c->wlcap;
+  if (want > c->wnbr_cap) {
+    if (c->wnbr) cudaFree(c->wnbr);
+    c->wnbr = nullptr;
+    CK(dalloc(&c->wnbr, want));
+    c->wnbr_cap = want;
+  }
+  s.wnbr = c->wnbr;
+  return SPH_OK;
+}
+
 // Build the neighbour lists for the current grid and h (growing the capacity if needed).
 sph_status build_lists(sph_ctx* c) {
   for (int attempt = 0; attempt < 4; ++attempt) {
     c->grid.lcap = c->lcap;
     CK(cudaMemsetAsync(&c->ctr->list_overflow, 0, sizeof(int), c->stream));
+    CK(cudaMemsetAsync(&c->ctr->wlist_overflow, 0, sizeof(int), c->stream));
     CK(cudaMemsetAsync(&c->ctr->nonfinite, 0, sizeof(int), c->stream));
     if (lists_smem(c->grid) > kSmemMax) return fail(c, SPH_ERR_H_EXCEEDS_CELL, "neighbour lists exceed shared memory");
     {
       Timed tm(c, SPH_T_LISTS);
       CK(launch_lists(c->grid, c->phys, c->s, c->cell_start, c->ctr, c->stream));
       CK(launch_bank(c->gL, c->n_own, c->grid, c->s, c->stream));
+      CK(launch_wide_lists(c->grid, c->phys, c->s, c->cell_start, c->ctr, c->stream));
     }
-    c->launches += 2;
+    c->launches += 2 + (c->s.n_wide > 0 ? 1 : 0);
     sph_status st = sync_ctr(c);
     if (st != SPH_OK) return st;
+    if (c->ctr_h->wlist_overflow > 0) {  // wide lists (one rank): grow and rebuild
+      c->wlcap = ((int)(c->ctr_h->wlist_overflow * 1.25) + 31) & ~31;
+      c->s.wlcap = c->wlcap;
+      const size_t want = (size_t)std::max(c->s.n_wide, 1) * c->wlcap;
+      if (want > c->wnbr_cap) {
+        if (c->wnbr) cudaFree(c->wnbr);
+        c->wnbr = nullptr;
+        CK(dalloc(&c->wnbr, want));
+        c->wnbr_cap = want;
+      }
+      c->s.wnbr = c->wnbr;
+      continue;
+    }
     double over = c->ctr_h->list_overflow, bad = c->ctr_h->nonfinite == 2 ? 1 : 0;
     double v[2] = {over, bad};
     if ((st = allreduce(c, v, 2, kMax)) != SPH_OK) return st;
@@ -950,6 +1078,7 @@ void sph_config_default(sph_config* cfg) {
   cfg->transport = SPH_TRANSPORT_NCCL;
   cfg->nccl_uid = nullptr;
   cfg->loopback = nullptr;
+  cfg->adaptive_h = 1;
 }
 
 sph_status sph_nccl_unique_id(void* out128) {
@@ -1061,8 +1190,9 @@ sph_status sph_density(sph_ctx* c, sph_density_stats* stats) {
       Timed tm(c, SPH_T_DENSITY);
       CK(launch_density(c->grid, c->phys, c->s, c->cell_start, pass, bin, bout, 1.f + c->cfg.cell_skin, c->ctr,
                         c->stream));
+      CK(launch_wide_density(c->grid, c->phys, c->s, pass, 1.f + c->cfg.cell_skin, c->ctr, c->stream));
     }
-    c->launches++;
+    c->launches += 1 + (c->s.n_wide > 0 ? 1 : 0);
     ++passes_run;
     if ((st = sync_ctr(c)) != SPH_OK) return st;
     // every rank takes the same branch: the flags are reduced over ranks
@@ -1128,8 +1258,9 @@ sph_status sph_gradient(sph_ctx* c, float dt) {
   {
     Timed tm(c, SPH_T_GRADIENT);
     CK(launch_gradient(c->grid, c->phys, c->s, c->cell_start, dt, c->dprev_valid ? 0 : 1, c->ctr, c->stream));
+    CK(launch_wide_gradient(c->grid, c->phys, c->s, dt, c->dprev_valid ? 0 : 1, c->ctr, c->stream));
   }
-  c->launches++;
+  c->launches += 1 + (c->s.n_wide > 0 ? 1 : 0);
   CK(cudaMemcpyAsync(&c->counters.pairs_gradient, &c->ctr->pairs, 8, cudaMemcpyDeviceToHost, c->stream));
   // ghosts need their owners' force-loop records (X3)
   if ((st = halo(c, c->s.fr1, sizeof(float4))) != SPH_OK) return st;
@@ -1149,8 +1280,9 @@ sph_status sph_force(sph_ctx* c, float* dt_next) {
   {
     Timed tm(c, SPH_T_FORCE);
     CK(launch_force(c->grid, c->phys, c->s, c->cell_start, c->ctr, c->stream));
+    CK(launch_wide_force(c->grid, c->phys, c->s, c->ctr, c->stream));
   }
-  c->launches++;
+  c->launches += 1 + (c->s.n_wide > 0 ? 2 : 0);
   if ((st = sync_ctr(c)) != SPH_OK) return st;
   c->counters.pairs_force = (int64_t)c->ctr_h->pairs;
   float dt;
@@ -1262,6 +1394,7 @@ sph_status sph_get_counters(sph_ctx* c, sph_counters* out) {
   CK(cudaStreamSynchronize(c->stream));
   c->counters.coincident = -1;  // not tracked by the GPU loops (R28)
   c->counters.kernel_launches = c->launches;
+  c->counters.wide_particles = c->s.n_wide;
   *out = c->counters;
   return SPH_OK;
 }
@@ -1317,7 +1450,8 @@ sph_status sph_destroy(sph_ctx* c) {
                   s.fin, s.gq, s.hlo, s.hhi, s.iters, s.active, s.grad, s.fr1, s.fr2, s.vsig, s.countf, s.nbr,
                   s.ncount, s.hbuild, c->cell_start, c->keys, c->keys_alt, c->perm, c->perm_alt, c->sort_tmp,
                   c->blk[0], c->blk[1], c->ctr, c->scratch, c->out_tmp, c->mig_send, c->mig_recv, c->pc_send,
-                  c->pc_recv, c->pc_scan, c->scan_tmp, c->cnt_dev};
+                  c->pc_recv, c->pc_scan, c->scan_tmp, c->cnt_dev, c->wide_flag, c->widx, c->wcount,
+                  c->n_wide_dev, c->wnbr, c->sel_tmp};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->ctr_h) cudaFreeHost(c->ctr_h);

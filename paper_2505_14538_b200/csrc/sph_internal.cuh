@@ -88,6 +88,13 @@ struct DevState {
   uint16_t* nbr;
   int32_t* ncount;    // padded list length (multiple of 8)
   float* hbuild;      // h when the list was built
+  // wide particles (adaptive cell side, sph_wide.cu): support past the cell side; nullptr /
+  // 0 when there are none
+  uint8_t* wide;      // [n] flag
+  int32_t* widx;      // [n_wide] their indices, ascending
+  uint32_t* wnbr;     // [n_wide][wlcap] neighbour lists, global indices
+  int32_t* wcount;    // [n_wide] list lengths
+  int n_wide, wlcap;
 };
 
 struct DevCounters {
@@ -100,7 +107,7 @@ struct DevCounters {
   int active_next;
   int list_stale;               // an h outgrew its list radius
   int list_overflow;            // max list length seen above lcap (0 = none)
-  int pad;
+  int wlist_overflow;           // max wide-list length seen above wlcap (0 = none)
 };
 
 // Launchers (sph_kernels.cu).  All enqueue on `st`.
@@ -119,6 +126,17 @@ size_t density_smem(const DevGrid& g);
 size_t gradient_smem(const DevGrid& g);
 size_t force_smem(const DevGrid& g);
 cudaError_t launch_bank(int i0, int n, const DevGrid& g, const DevState& s, cudaStream_t st);
+// wide particles (sph_wide.cu)
+cudaError_t launch_mark_wide(int n, const DevGrid& g, const DevPhys& ph, const DevState& s, uint8_t* flag,
+                             cudaStream_t st);
+cudaError_t launch_wide_lists(const DevGrid& g, const DevPhys& ph, const DevState& s, const int* cell_start,
+                              DevCounters* ctr, cudaStream_t st);
+cudaError_t launch_wide_density(const DevGrid& g, const DevPhys& ph, const DevState& s, int pass, float hfac_stale,
+                                DevCounters* ctr, cudaStream_t st);
+cudaError_t launch_wide_gradient(const DevGrid& g, const DevPhys& ph, const DevState& s, float dt, int first_step,
+                                 DevCounters* ctr, cudaStream_t st);
+cudaError_t launch_wide_force(const DevGrid& g, const DevPhys& ph, const DevState& s, DevCounters* ctr,
+                              cudaStream_t st);
 int kernel_threads();
 
 }  // namespace sph

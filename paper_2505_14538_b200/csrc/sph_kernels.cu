@@ -36,6 +36,7 @@
 #include <stdint.h>
 
 #include "sph_internal.cuh"
+#include "sph_pair.cuh"
 
 namespace sph {
 
@@ -247,48 +248,6 @@ __device__ __forceinline__ int warp_max(int v) {
   return v;
 }
 
-// M4 cubic spline: w(q), dw/dq; exactly zero for q >= 2 (compact support).
-__device__ __forceinline__ void m4(float q, float& w, float& dw) {
-  const float q2 = q * q;
-  const float w_in = fmaf(q2, fmaf(0.75f, q, -1.5f), 1.f);
-  const float dw_in = q * fmaf(2.25f, q, -3.f);
-  const float t = fmaxf(2.f - q, 0.f);
-  const float t2 = t * t;
-  const bool inner = q < 1.f;
-  w = inner ? w_in : 0.25f * t2 * t;
-  dw = inner ? dw_in : -0.75f * t2;
-}
-__device__ __forceinline__ float m4_dw(float q) {
-  const float dw_in = q * fmaf(2.25f, q, -3.f);
-  const float t = fmaxf(2.f - q, 0.f);
-  return q < 1.f ? dw_in : -0.75f * t * t;
-}
-
-// fp64 fixed-point neighbour test, operation for operation the oracle's (oracle.c sep2):
-// r^2 = (dx*dx + dy*dy) + dz*dz < H2 with dx = (double)(int32)(X_i - X_j) * (L * 2^-32).
-// Only reached for pairs within the f32 error band of the support radius (rare).
-__device__ __forceinline__ bool exact_neighbour(const uint4* __restrict__ xh, int gi, int gj, double H2, double sx,
-                                                double sy, double sz) {
-  const uint4 a = xh[gi], b = xh[gj];
-  const double dx = __dmul_rn((double)(int)(a.x - b.x), sx);
-  const double dy = __dmul_rn((double)(int)(a.y - b.y), sy);
-  const double dz = __dmul_rn((double)(int)(a.z - b.z), sz);
-  const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-  return r2 < H2 && r2 > 0.0;
-}
-
-__device__ __forceinline__ double h2_exact(float h, float gamma_k) {
-  const double H = __dmul_rn((double)gamma_k, (double)h);
-  return __dmul_rn(H, H);
-}
-
-// 1 if d < 0 (sign bit), i.e. q < 2 for d = q - 2
-__device__ __forceinline__ int neg(float d) { return (int)(__float_as_uint(d) >> 31); }
-
-// r^-1 with the self pair (r = 0, listed) mapped to a finite value: every pair term of the
-// self pair then carries w'(0) = 0 or v_ij = 0 and vanishes exactly.
-__device__ __forceinline__ float rinv_safe(float r2) { return rsqrtf(fmaxf(r2, 1e-30f)); }
-
 // Iterate a particle's padded neighbour list in groups of 8 (one 16-byte load each).
 template <class PairF>
 __device__ __forceinline__ void for_list(const uint16_t* __restrict__ list, int cnt, PairF&& pair) {
@@ -424,7 +383,7 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
   int over = 0;
   for (int c = warp; c * 32 < ni; c += kNW) {
     const int k = c * 32 + lane;
-    const bool valid = k < ni;
+    bool valid = k < ni;
     const int kk = valid ? k : c * 32;
     int lo = 0, hi = nicell;  // s_cp[lo] <= kk < s_cp[hi]
     while (hi - lo > 1) {
@@ -442,6 +401,10 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
     const int tc = S.tc[col];
     const float zc = zbound(T.z0 + zz - 2);  // bottom of tile cell zz - 1
     uint4* dst = reinterpret_cast<uint4*>(s.nbr + (size_t)gi * g.lcap);
+    if (valid && s.wide && s.wide[gi]) {  // a wide particle's list is built by k_wide_lists
+      s.ncount[gi] = 0;
+      valid = false;
+    }
     uint32_t w = 0u, rd = 0u;  // ring byte offsets: next write, next flush
     int flushed = 0;           // entries already in global memory
     auto hit = [&](bool h, int t) {
@@ -681,9 +644,12 @@ __device__ __forceinline__ void walk_lists(int ni, const int* __restrict__ pref,
   for (int gg = g0; gg < g1; ++gg, ++list) {
     if (gg == p1) {
       finish();
-      ++k;
-      p0 = p1;
-      p1 = pref[k + 1];
+      // next particle with a non-empty list (wide particles have none)
+      do {
+        ++k;
+        p0 = p1;
+        p1 = pref[k + 1];
+      } while (p1 == p0);
       list = reinterpret_cast<const uint4*>(list_of(k));
       begin(k);
     }
@@ -759,17 +725,6 @@ __device__ __forceinline__ void walk_prefix(const BlockShared& S, const DevState
 // Then nhat = S0/(pi h^3), dn/dh = -(3 S0 + S1)/(pi h^4), rho = R0/(pi h^3),
 // drho/dh = -(3 R0 + R1)/(pi h^4), div = -Dv/(rho pi h^4), curl = Cv/(rho pi h^4),
 // g = nhat h^3 - eta^3 = S0/pi - eta^3, h g' = -S1/pi.
-struct DenAcc {
-  float S0, S1, R0, R1, Dv, Cx, Cy, Cz;
-  int nn;
-  __device__ static DenAcc zero() { return DenAcc{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0}; }
-  __device__ void merge_into(DenAcc* d) const {
-    atomicAdd(&d->S0, S0); atomicAdd(&d->S1, S1); atomicAdd(&d->R0, R0); atomicAdd(&d->R1, R1);
-    atomicAdd(&d->Dv, Dv); atomicAdd(&d->Cx, Cx); atomicAdd(&d->Cy, Cy); atomicAdd(&d->Cz, Cz);
-    atomicAdd(&d->nn, nn);
-  }
-};
-
 __global__ void __launch_bounds__(kNW * 32, 2) k_density(DevGrid g, DevPhys ph, DevState s,
                                                       const int* __restrict__ cell_start, int pass,
                                                       const uint8_t* __restrict__ blk_in, uint8_t* __restrict__ blk_out,
@@ -841,98 +796,26 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_density(DevGrid g, DevPhys ph, 
         },
         [&](int j) {
           const float4 p = smem4[j];
-          const float4 q4 = smem4[O1 + j];
-          const float dx = pi4.x - p.x, dy = pi4.y - p.y, dz = pi4.z - p.z;
-          const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-          const float rinv = rinv_safe(r2);
-          const float q = r2 * rinv * hinv;
-          const float d = q - 2.f;
-          a.nn += neg(d);
-          if (fabsf(d) < qband) {
-            const bool ex = exact_neighbour(s.xh, gi, slot_global(S, T.nct, j), H2, g.dscale[0], g.dscale[1],
-                                            g.dscale[2]);
-            a.nn += (int)ex - neg(d);
-          }
-          // M4 as truncated powers: w = t^3/4 - s^3, w' = -3/4 t^2 + 3 s^2 (t = (2-q)+, s = (1-q)+)
-          const float tq = fmaxf(-d, 0.f), sq = fmaxf(1.f - q, 0.f);
-          const float t2 = tq * tq, s2 = sq * sq;
-          const float w = fmaf(0.25f * tq, t2, -sq * s2);
-          const float dw = fmaf(3.f, s2, -0.75f * t2);
-          const float qdw = q * dw;
-          a.S0 += w;
-          a.S1 += qdw;
-          a.R0 = fmaf(q4.w, w, a.R0);
-          a.R1 = fmaf(q4.w, qdw, a.R1);
-          const float F = q4.w * dw * rinv;
-          const float ux = vi4.x - q4.x, uy = vi4.y - q4.y, uz = vi4.z - q4.z;
-          a.Dv = fmaf(F, fmaf(uz, dz, fmaf(uy, dy, ux * dx)), a.Dv);
-          a.Cx = fmaf(F, fmaf(uy, dz, -uz * dy), a.Cx);
-          a.Cy = fmaf(F, fmaf(uz, dx, -ux * dz), a.Cy);
-          a.Cz = fmaf(F, fmaf(ux, dy, -uy * dx), a.Cz);
+          den_pair(a, pi4.x - p.x, pi4.y - p.y, pi4.z - p.z, hinv, qband, vi4, smem4[O1 + j], [&]() {
+            return exact_neighbour(s.xh, gi, slot_global(S, T.nct, j), H2, g.dscale[0], g.dscale[1], g.dscale[2]);
+          });
         },
         [&]() { return a; });
   }
   __syncthreads();
-  const float inv_pi = 1.f / kPi;
   unsigned long long npairs = 0, nfinal = 0;
   for (int k = threadIdx.x; k < ni; k += kNT) {
     const DenAcc a = W.fin[k];
     int ti, gi;
     i_slot(S, W.kl[k], ti, gi);
-    const float h = smem4[ti].w, hinv = 1.f / h;
-    const float mi = smem4[O1 + ti].w;
-    const int nn = a.nn - 1;  // the self pair
-    npairs += (unsigned long long)nn;
-    // ---- epilogue: closure, Newton / finalize
-    const float ih3 = inv_pi * hinv * hinv * hinv;
-    const float nhat = a.S0 * ih3;
-    const float dndh = -(3.f * a.S0 + a.S1) * ih3 * hinv;
-    const float rho = a.R0 * ih3;
-    const float drho = -(3.f * a.R0 + a.R1) * ih3 * hinv;
-    const float gres = a.S0 * inv_pi - ph.eta3;
-    const bool conv = (ph.h_max_iter == 0) || fabsf(gres) <= ph.h_tol * ph.eta3;
-    const int it = pass == 0 ? 0 : s.iters[gi];
-    const bool give_up = !conv && it >= ph.h_max_iter;
-    if (conv || give_up) {
-      const float ih4 = ih3 * hinv / rho;
-      s.dens[gi] = make_float4(rho, drho, nhat, dndh);
-      const float div = -a.Dv * ih4;
-      const float cx = a.Cx * ih4, cy = a.Cy * ih4, cz = a.Cz * ih4;
-      s.dvc[gi] = make_float4(cx, cy, cz, div);
-      s.count[gi] = nn;
-      // finalize: Eq. 8 (n_a = 3), ideal gas, Balsara (R8, R14)
-      const float Omega = 1.f + h / (3.f * rho) * drho;
-      const float f = ph.fh_mode ? Omega : 1.f / Omega;
-      const float u = s.u[gi];
-      const float P = (ph.gamma_eos - 1.f) * rho * u;
-      const float cs = sqrtf(ph.gamma_eos * P / rho);
-      const float adiv = fabsf(div), acurl = sqrtf(cx * cx + cy * cy + cz * cz);
-      const float den = adiv + acurl + 1e-4f * cs * hinv;
-      const float Bal = den > 0.f ? adiv / den : 0.f;
-      s.fin[gi] = make_float4(f, P, cs, Bal);
-      s.gq[gi] = make_float4(cs, u, mi / rho, rho);
-      s.active[gi] = 0;
-      s.iters[gi] = conv ? it : -1;
-      nfinal += (unsigned long long)nn;
-      if (give_up) atomicAdd(&s_unconv, 1);
-    } else {
-      // Newton with bracket + bisection (R7); g is non-decreasing in h
-      float lo = pass == 0 ? 0.f : s.hlo[gi];
-      float hi = pass == 0 ? CUDART_INF_F : s.hhi[gi];
-      if (gres > 0.f) hi = h; else lo = h;
-      float hn = (a.S1 < 0.f) ? h * (1.f + (a.S0 - ph.pi_eta3) / a.S1) : (gres < 0.f ? 2.f * h : 0.5f * h);
-      hn = fminf(fmaxf(hn, 0.5f * h), 2.f * h);
-      if (hn <= lo || hn >= hi) hn = isinf(hi) ? 2.f * h : 0.5f * (lo + hi);
-      s.hlo[gi] = lo;
-      s.hhi[gi] = hi;
-      s.iters[gi] = it + 1;
-      s.active[gi] = 1;
-      reinterpret_cast<unsigned int*>(&s.xh[gi])[3] = __float_as_uint(hn);
-      s_active = 1;
-      const float Hn = ph.gamma_k * hn * (1.f + g.skin);
-      if (Hn > g.side_min) atomicExch(&ctr->h_exceeds, 1);
-      if (hn > hfac_stale * s.hbuild[gi]) atomicExch(&ctr->list_stale, 1);
-    }
+    if (s.wide && s.wide[gi]) continue;  // wide particles: k_wide_density
+    const DenOut o = den_epilogue(g, ph, s, a, gi, smem4[ti].w, smem4[O1 + ti].w, pass, hfac_stale);
+    npairs += (unsigned long long)o.nn;
+    if (o.final_) nfinal += (unsigned long long)o.nn;
+    if (o.give_up) atomicAdd(&s_unconv, 1);
+    if (o.active) s_active = 1;
+    if (o.exceeds) atomicExch(&ctr->h_exceeds, 1);
+    if (o.stale) atomicExch(&ctr->list_stale, 1);
   }
   const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -958,17 +841,6 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_density(DevGrid g, DevPhys ph, 
 // Brookshaw Laplacian lap u_i = 2 sum_j (m_j/rho_j)(u_i - u_j) dW/dr / r (R16), gathered
 // over r_ij < H_i; the gradient ghost (alpha_v Eqs. 12-15, alpha_c Eqs. 21-24; R17-R21)
 // runs in the epilogue and writes the force-loop records.
-struct GradAcc {
-  float vmax, lap;  // vmax > 0: max over its f32 bits as int
-  int nn;
-  __device__ static GradAcc zero() { return GradAcc{0.f, 0.f, 0}; }
-  __device__ void merge_into(GradAcc* d) const {
-    atomicMax(reinterpret_cast<int*>(&d->vmax), __float_as_int(vmax));
-    atomicAdd(&d->lap, lap);
-    atomicAdd(&d->nn, nn);
-  }
-};
-
 __global__ void __launch_bounds__(kNW * 32, 2) k_gradient(DevGrid g, DevPhys ph, DevState s,
                                                        const int* __restrict__ cell_start, float dt, int first_step,
                                                        DevCounters* __restrict__ ctr) {
@@ -1025,24 +897,11 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_gradient(DevGrid g, DevPhys ph,
         },
         [&](int j) {
           const float4 p = smem4[j];
-          const float4 q4 = smem4[O1 + j];
-          const float4 g4 = smem4[O2 + j];
-          const float dx = pi4.x - p.x, dy = pi4.y - p.y, dz = pi4.z - p.z;
-          const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-          const float rinv = rinv_safe(r2);
-          const float q = r2 * rinv * hinv;
-          const float d = q - 2.f;
-          int in = neg(d);
-          if (fabsf(d) < qband)
-            in = exact_neighbour(s.xh, gi, slot_global(S, T.nct, j), H2, g.dscale[0], g.dscale[1], g.dscale[2]);
-          a.nn += in;
-          const float tq = fmaxf(-d, 0.f), sq = fmaxf(1.f - q, 0.f);
-          const float dw = fmaf(3.f * sq, sq, -0.75f * tq * tq);  // M4 w'(q)
-          const float vr = fmaf(vi4.z - q4.z, dz, fmaf(vi4.y - q4.y, dy, (vi4.x - q4.x) * dx));
-          const float mu = fminf(vr, 0.f) * rinv;
-          const float vs = fmaf(-ph.beta, mu, ci + g4.x);
-          a.vmax = fmaxf(a.vmax, in ? vs : 0.f);
-          a.lap = fmaf(g4.z * (ui - g4.y), dw * rinv, a.lap);
+          grad_pair(a, pi4.x - p.x, pi4.y - p.y, pi4.z - p.z, hinv, qband, vi4, ci, ui, ph.beta, smem4[O1 + j],
+                    smem4[O2 + j], [&]() {
+                      return exact_neighbour(s.xh, gi, slot_global(S, T.nct, j), H2, g.dscale[0], g.dscale[1],
+                                             g.dscale[2]);
+                    });
         },
         [&]() { return a; });
   }
@@ -1052,40 +911,9 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_gradient(DevGrid g, DevPhys ph,
     const GradAcc a = W.fin[k];
     int ti, gi;
     i_slot(S, k, ti, gi);
-    const float h = smem4[ti].w, hinv = 1.f / h;
+    if (s.wide && s.wide[gi]) continue;  // wide particles: k_wide_gradient
     const float4 gi4 = smem4[O2 + ti];
-    const float ci = gi4.x, ui = gi4.y;
-    const int nn = a.nn - 1;  // the self pair
-    npairs += (unsigned long long)nn;
-    const float lap_u = 2.f * a.lap * hinv * hinv * hinv * hinv / kPi;
-    const float vsig = a.vmax;
-    // gradient ghost (R17-R21)
-    const float H = ph.gamma_k * h;
-    const float4 dvc = s.dvc[gi];
-    const float4 fin = s.fin[gi];
-    const float div = dvc.w;
-    float av = s.av[gi], ac = s.ac[gi];
-    const float Ddot = first_step ? 0.f : (div - s.dprev[gi]) / dt;
-    const float Sx = H * H * fmaxf(-Ddot, 0.f);
-    const float den = vsig * vsig + Sx;
-    const float aloc = den > 0.f ? ph.alpha_v_max * Sx / den : 0.f;
-    if (av < aloc) av = aloc;
-    else av = aloc + (av - aloc) * expf(-ph.ell * ci * dt / H);
-    const float src = ui > 0.f ? ph.beta_c * H * lap_u / sqrtf(ui) : 0.f;
-    const float dac = src - (ac - ph.alpha_c_min) * vsig / H;
-    ac = ac + dt * dac;
-    const float ceil_ = fmaxf(ph.alpha_c_min, ph.alpha_c_max * (1.f - av / ph.alpha_v_max));
-    ac = fmaxf(fminf(ac, ceil_), ph.alpha_c_min);
-    s.grad[gi] = make_float2(vsig, lap_u);
-    s.av[gi] = av;
-    s.ac[gi] = ac;
-    s.dprev[gi] = div;
-    const float rho = gi4.w;
-    const float f = fin.x, P = fin.y;
-    // force records: (A = P/rho^2, K = -0.75 f/(pi h^4), c, rho) and (B, P alpha_c -- or
-    // -alpha_c when P = 0, for Eq. 20's P_i + P_j = 0 case (R13) --, u, alpha_v); P = A rho^2
-    s.fr1[gi] = make_float4(P / (rho * rho), -0.75f * f * hinv * hinv * hinv * hinv / kPi, ci, rho);
-    s.fr2[gi] = make_float4(fin.w, P > 0.f ? P * ac : -ac, ui, av);
+    npairs += (unsigned long long)grad_epilogue(ph, s, a, gi, smem4[ti].w, gi4.x, gi4.y, gi4.w, dt, first_step);
   }
   const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -1105,24 +933,8 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_gradient(DevGrid g, DevPhys ph,
 // T is evaluated from operands symmetric in (i, j), so the pair terms of i and j are exact
 // negatives (momentum and energy conserving up to the summation rounding).
 // The CFL dt = C_cfl min 2 gamma_k h / v_sig is reduced in the epilogue.
-struct ForceAcc {
-  float ax, ay, az, du, vmax;  // vmax > 0: max over its f32 bits as int
-  int nn;
-  __device__ static ForceAcc zero() { return ForceAcc{0.f, 0.f, 0.f, 0.f, 0.f, 0}; }
-  __device__ void merge_into(ForceAcc* d) const {
-    atomicAdd(&d->ax, ax); atomicAdd(&d->ay, ay); atomicAdd(&d->az, az); atomicAdd(&d->du, du);
-    atomicMax(reinterpret_cast<int*>(&d->vmax), __float_as_int(vmax));
-    atomicAdd(&d->nn, nn);
-  }
-};
 __host__ __device__ __forceinline__ size_t force_records_bytes(int tcap) {
   return (size_t)(tcap + kNSent) * (4 * 16);
-}
-
-// -dW/dq / 0.75 of M4: q (4 - 3q) for q < 1, (2 - q)^2 for 1 <= q < 2, 0 beyond
-__device__ __forceinline__ float m4_dwp(float q) {
-  const float t = fmaxf(2.f - q, 0.f);
-  return q < 1.f ? q * fmaf(-3.f, q, 4.f) : t * t;
 }
 
 __global__ void __launch_bounds__(kNW * 32, 2) k_force(DevGrid g, DevPhys ph, DevState s,
@@ -1173,8 +985,8 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_force(DevGrid g, DevPhys ph, De
     const float4* __restrict__ T3 = smem4 + O3;
     // |min(q_i, q_j) - 2| below this: decide in fp64 (eabs / min h of the tile)
     const float band = g.eabs * __uint_as_float(s_hinv_max) + 8e-6f;
-    float4 pi4, vi4, ai, bi;
-    float Pi = 0.f;
+    float4 pi4;
+    ForceSide I;
     int gi = 0;
     ForceAcc a;
     walk_lists(
@@ -1188,56 +1000,29 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_force(DevGrid g, DevPhys ph, De
           int ti;
           i_slot(S, k, ti, gi);
           pi4 = T0[ti];
-          vi4 = T1[ti];
-          ai = T2[ti];
-          bi = T3[ti];
-          Pi = ai.x * ai.w * ai.w;
-          a = ForceAcc{0.f, 0.f, 0.f, 0.f, 2.f * ai.z, 0};
+          I.hinv = pi4.w;
+          I.v = T1[ti];
+          I.a = T2[ti];
+          I.b = T3[ti];
+          I.P = I.a.x * I.a.w * I.a.w;
+          a = ForceAcc{0.f, 0.f, 0.f, 0.f, 2.f * I.a.z, 0};
         },
         [&](int j) {
           const float4 p = T0[j];
-          const float dx = pi4.x - p.x, dy = pi4.y - p.y, dz = pi4.z - p.z;
-          const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-          const float4 vj = T1[j];
-          const float4 aj = T2[j];
-          const float4 bj = T3[j];
-          const float rinv = rinv_safe(r2);
-          const float r = r2 * rinv;
-          const float qi = r * pi4.w, qj = r * p.w;
-          const float d = fminf(qi, qj) - 2.f;
-          int in = neg(d);
-          if (fabsf(d) < band) {
+          ForceSide J;
+          J.hinv = p.w;
+          J.v = T1[j];
+          J.a = T2[j];
+          J.b = T3[j];
+          J.P = J.a.x * J.a.w * J.a.w;
+          float vs;
+          int in;
+          force_pair(a, pi4.x - p.x, pi4.y - p.y, pi4.z - p.z, I, J, ph.beta, band, [&]() {
             const int gj = slot_global(S, T.nct, j);
             const double H2 = fmax(h2_exact(__uint_as_float(s.xh[gi].w), ph.gamma_k),
                                    h2_exact(__uint_as_float(s.xh[gj].w), ph.gamma_k));
-            in = exact_neighbour(s.xh, gi, gj, H2, g.dscale[0], g.dscale[1], g.dscale[2]);
-          }
-          a.nn += in;
-          const float gI = ai.y * m4_dwp(qi);  // g_i = G_i r = f_i dW/dr(h_i)
-          const float gJ = aj.y * m4_dwp(qj);
-          const float vr = fmaf(vi4.z - vj.z, dz, fmaf(vi4.y - vj.y, dy, (vi4.x - vj.x) * dx));
-          const float vrr = vr * rinv;
-          const float mu = fminf(vrr, 0.f);
-          const float vs = fmaf(-ph.beta, mu, ai.z + aj.z);
-          a.vmax = fmaxf(a.vmax, in ? vs : 0.f);
-          const float irs = __fdividef(1.f, ai.w + aj.w);
-          const float gs = gI + gJ;
-          // X = 4 abar mu v_sig (g_i + g_j) / (rho_i + rho_j):  Pi_ij gbar = -X / 4
-          const float X = ((bi.w + bj.w) * (bi.x + bj.x)) * (mu * vs) * (gs * irs);
-          const float AgI = ai.x * gI;
-          const float Tij = fmaf(aj.x, gJ, fmaf(-0.25f, X, AgI));  // S_ij r
-          const float mT = vj.w * Tij * rinv;
-          a.ax = fmaf(-mT, dx, a.ax);
-          a.ay = fmaf(-mT, dy, a.ay);
-          a.az = fmaf(-mT, dz, a.az);
-          const float Pj = aj.x * aj.w * aj.w;
-          // alpha_c,ij (Eq. 20): (P_i ac_i + P_j ac_j) / (P_i + P_j), or the mean when
-          // P_i + P_j = 0 (R13; the records then hold -alpha_c)
-          const float Psum = Pi + Pj;
-          const float acij = __fdividef(bi.y + bj.y, Psum > 0.f ? Psum : -2.f);
-          const float vc = fabsf(vrr) + sqrtf(2.f * fabsf(Pi - Pj) * irs);
-          const float D = acij * vc * (bi.z - bj.z) * (gs * irs);
-          a.du = fmaf(vj.w, fmaf(fmaf(-0.125f, X, AgI), vrr, D), a.du);
+            return exact_neighbour(s.xh, gi, gj, H2, g.dscale[0], g.dscale[1], g.dscale[2]);
+          }, vs, in);
         },
         [&]() { return a; });
   }
@@ -1248,6 +1033,7 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_force(DevGrid g, DevPhys ph, De
     const ForceAcc a = W.fin[k];
     int ti, gi;
     i_slot(S, k, ti, gi);
+    if (s.wide && s.wide[gi]) continue;  // wide particles: k_wide_force
     const float hi_ = __uint_as_float(s.xh[gi].w);
     const int nn = a.nn - 1;  // the self pair
     s.acc[gi] = make_float4(a.ax, a.ay, a.az, a.du);

@@ -1,0 +1,304 @@
+// sph_wide.cu -- "wide" particles of the adaptive cell grid.
+//
+// A strong smoothing-length contrast (C3 Sedov: H from 0.63 to 5.6 H_0) makes a grid with
+// side >= (1 + skin) gamma_k h_max hold thousands of particles per cell in the dense regions,
+// far beyond what a shared-memory tile can stage.  The single-rank path then sizes the cells
+// from a quantile of h instead (sph_api.cu rebuild()), and the few particles whose list
+// radius (1 + skin) gamma_k h exceeds the side become WIDE:
+//   - k_wide_lists: one warp per wide particle i scans the cells within +-k_a of its cell
+//     (k_a = ceil(list radius / side_a) per axis) and lists, by global index, every j with
+//     r_ij < (1 + skin) gamma_k max(h_i, h_j) -- the same criterion as the tile lists;
+//   - k_wide_density / k_wide_gradient / k_wide_force: one thread per wide particle runs
+//     the shared pair arithmetic (sph_pair.cuh) over its list, gathering the neighbour
+//     records from global memory (L2), with the same epilogues as the tile loops;
+//   - symmetry of the force set r < max(H_i, H_j) (R3): a partner j that did not list i
+//     (a tile particle more than one cell away, or a wide particle whose own search range
+//     stops short of i) gets its side of the pair from i, added with atomics (a, du/dt,
+//     N_force) and atomicMax (v_sig); its CFL dt candidate goes to the global minimum.
+// The tile kernels skip wide particles as i (empty list, no epilogue) and see them as j like
+// any other particle of their tile.
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+#include "sph_internal.cuh"
+#include "sph_pair.cuh"
+
+namespace sph {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ int cell_axis(uint32_t x, int n) { return (int)(((unsigned long long)x * (unsigned)n) >> 32); }
+
+// search half-width in cells along each axis for a list radius R (capped to the whole axis)
+__device__ __forceinline__ int reach(float R, float side, int n) {
+  const int k = (int)ceilf(R / side);
+  return min(k, (n - 1) / 2 + 1);
+}
+
+// cells i and j are within +-k of each other along an axis of n cells (periodic)
+__device__ __forceinline__ bool within(int a, int b, int k, int n) {
+  if (2 * k + 1 >= n) return true;
+  int d = a - b;
+  d = d < 0 ? -d : d;
+  d = min(d, n - d);
+  return d <= k;
+}
+
+__global__ void k_mark_wide(int n, DevGrid g, DevPhys ph, DevState s, uint8_t* flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float R = (1.f + g.skin) * ph.gamma_k * __uint_as_float(s.xh[i].w);
+  flag[i] = R > g.side_min ? 1 : 0;
+}
+
+// One warp per wide particle.  Overflow of wlcap: the count is still returned (max in
+// ctr->list_overflow) and the host rebuilds with a larger capacity.
+__global__ void __launch_bounds__(256) k_wide_lists(DevGrid g, DevPhys ph, DevState s, const int* __restrict__ cell_start,
+                                                    DevCounters* __restrict__ ctr) {
+  const int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (wi >= s.n_wide) return;
+  const int i = s.widx[wi];
+  const uint4 xi = s.xh[i];
+  const float Hfac = (1.f + g.skin) * ph.gamma_k;
+  const float hi = __uint_as_float(xi.w);
+  const float Hi2 = (Hfac * hi) * (Hfac * hi);
+  const int cx = cell_axis(xi.x, g.nx), cy = cell_axis(xi.y, g.ny), cz = cell_axis(xi.z, g.nz);
+  const int kx = reach(Hfac * hi, g.side[0], g.nx), ky = reach(Hfac * hi, g.side[1], g.ny),
+            kz = reach(Hfac * hi, g.side[2], g.nz);
+  const int zlo = (2 * kz + 1 >= g.nz) ? 0 : cz - kz, zn = (2 * kz + 1 >= g.nz) ? g.nz : 2 * kz + 1;
+  uint32_t* lst = s.wnbr + (size_t)wi * s.wlcap;
+  int cnt = 0;
+  const int nxr = (2 * kx + 1 >= g.nx) ? g.nx : 2 * kx + 1, nyr = (2 * ky + 1 >= g.ny) ? g.ny : 2 * ky + 1;
+  const int x0 = (2 * kx + 1 >= g.nx) ? 0 : cx - kx, y0 = (2 * ky + 1 >= g.ny) ? 0 : cy - ky;
+  for (int ax = 0; ax < nxr; ++ax) {
+    const int ccx = ((x0 + ax) % g.nx + g.nx) % g.nx;
+    for (int ay = 0; ay < nyr; ++ay) {
+      const int ccy = ((y0 + ay) % g.ny + g.ny) % g.ny;
+      const int col = (ccx * g.ny + ccy) * g.nz;
+      // the z range as at most two contiguous runs of cells
+      const int za = ((zlo % g.nz) + g.nz) % g.nz;
+      const int run1 = min(zn, g.nz - za);
+      for (int part = 0; part < 2; ++part) {
+        const int c0 = part == 0 ? za : 0, nc = part == 0 ? run1 : zn - run1;
+        if (nc <= 0) continue;
+        const int j0 = cell_start[col + c0], j1 = cell_start[col + c0 + nc];
+        for (int jb = j0; jb < j1; jb += 32) {
+          const int j = jb + lane;
+          bool hit = false;
+          if (j < j1) {
+            const uint4 xj = s.xh[j];
+            const float dx = (float)(int)(xi.x - xj.x) * g.scale[0];
+            const float dy = (float)(int)(xi.y - xj.y) * g.scale[1];
+            const float dz = (float)(int)(xi.z - xj.z) * g.scale[2];
+            const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+            const float hj = __uint_as_float(xj.w);
+            hit = r2 < fmaxf(Hi2, (Hfac * hj) * (Hfac * hj));
+          }
+          const unsigned b = __ballot_sync(kFull, hit);
+          const int pos = cnt + __popc(b & ((1u << lane) - 1u));
+          if (hit && pos < s.wlcap) lst[pos] = (uint32_t)j;
+          cnt += __popc(b);
+        }
+      }
+    }
+  }
+  if (lane == 0) {
+    s.wcount[wi] = min(cnt, s.wlcap);
+    s.hbuild[i] = hi;
+    if (cnt > s.wlcap) atomicMax(&ctr->wlist_overflow, cnt);
+  }
+}
+
+// relative position r_i - r_j of two particles (minimum image on the 2^-32 grid)
+__device__ __forceinline__ float3 rel(const DevGrid& g, const uint4& a, const uint4& b) {
+  return make_float3((float)(int)(a.x - b.x) * g.scale[0], (float)(int)(a.y - b.y) * g.scale[1],
+                     (float)(int)(a.z - b.z) * g.scale[2]);
+}
+
+// |q - 2| below this: decide membership in fp64 (fp32 r from exact integer differences errs
+// by < 1e-6 relative)
+constexpr float kBandW = 2e-5f;
+
+__global__ void __launch_bounds__(128) k_wide_density(DevGrid g, DevPhys ph, DevState s, int pass, float hfac_stale,
+                                                      DevCounters* __restrict__ ctr) {
+  const int wi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (wi >= s.n_wide) return;
+  const int i = s.widx[wi];
+  if (pass > 0 && !s.active[i]) return;
+  const uint4 xi = s.xh[i];
+  const float4 vi = s.vm[i];
+  const float h = __uint_as_float(xi.w), hinv = 1.f / h;
+  const double H2 = h2_exact(h, ph.gamma_k);
+  const uint32_t* lst = s.wnbr + (size_t)wi * s.wlcap;
+  const int n = s.wcount[wi];
+  DenAcc a = DenAcc::zero();
+  for (int k = 0; k < n; ++k) {
+    const int j = (int)__ldg(lst + k);
+    const float3 d = rel(g, xi, s.xh[j]);
+    den_pair(a, d.x, d.y, d.z, hinv, kBandW, vi, s.vm[j], [&]() {
+      return exact_neighbour(s.xh, i, j, H2, g.dscale[0], g.dscale[1], g.dscale[2]);
+    });
+  }
+  const DenOut o = den_epilogue(g, ph, s, a, i, h, vi.w, pass, hfac_stale);
+  atomicAdd(&ctr->pairs_all, (unsigned long long)o.nn);
+  if (o.final_) atomicAdd(&ctr->pairs, (unsigned long long)o.nn);
+  if (o.give_up) atomicAdd(&ctr->unconverged, 1);
+  if (o.active) atomicAdd(&ctr->active_next, 1);
+  if (o.stale) atomicExch(&ctr->list_stale, 1);
+}
+
+__global__ void __launch_bounds__(128) k_wide_gradient(DevGrid g, DevPhys ph, DevState s, float dt, int first_step,
+                                                       DevCounters* __restrict__ ctr) {
+  const int wi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (wi >= s.n_wide) return;
+  const int i = s.widx[wi];
+  const uint4 xi = s.xh[i];
+  const float4 vi = s.vm[i];
+  const float4 gi4 = s.gq[i];
+  const float h = __uint_as_float(xi.w), hinv = 1.f / h;
+  const double H2 = h2_exact(h, ph.gamma_k);
+  const uint32_t* lst = s.wnbr + (size_t)wi * s.wlcap;
+  const int n = s.wcount[wi];
+  GradAcc a{2.f * gi4.x, 0.f, 0};
+  for (int k = 0; k < n; ++k) {
+    const int j = (int)__ldg(lst + k);
+    const float3 d = rel(g, xi, s.xh[j]);
+    grad_pair(a, d.x, d.y, d.z, hinv, kBandW, vi, gi4.x, gi4.y, ph.beta, s.vm[j], s.gq[j], [&]() {
+      return exact_neighbour(s.xh, i, j, H2, g.dscale[0], g.dscale[1], g.dscale[2]);
+    });
+  }
+  const int nn = grad_epilogue(ph, s, a, i, h, gi4.x, gi4.y, gi4.w, dt, first_step);
+  atomicAdd(&ctr->pairs, (unsigned long long)nn);
+}
+
+// acc, v_sig and N_force of the wide particles start from zero: k_wide_force adds them
+__global__ void k_wide_zero(DevState s) {
+  const int wi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (wi >= s.n_wide) return;
+  const int i = s.widx[wi];
+  s.acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  s.vsig[i] = 0.f;
+  s.countf[i] = 0;
+}
+
+__device__ __forceinline__ ForceSide side_of(const DevState& s, int i, float h) {
+  ForceSide f;
+  f.hinv = 1.f / h;
+  f.v = s.vm[i];
+  f.a = s.fr1[i];
+  f.b = s.fr2[i];
+  f.P = f.a.x * f.a.w * f.a.w;
+  return f;
+}
+
+__device__ __forceinline__ void dt_candidate(const DevPhys& ph, DevCounters* ctr, float h, float vsig) {
+  const float dt = ph.c_cfl * 2.f * ph.gamma_k * h / vsig;
+  if (dt > 0.f && dt < CUDART_INF_F) atomicMin(&ctr->dt_bits, __float_as_uint(dt));
+}
+
+__global__ void __launch_bounds__(128) k_wide_force(DevGrid g, DevPhys ph, DevState s, DevCounters* __restrict__ ctr) {
+  const int wi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (wi >= s.n_wide) return;
+  const int i = s.widx[wi];
+  const uint4 xi = s.xh[i];
+  const float h = __uint_as_float(xi.w);
+  const ForceSide I = side_of(s, i, h);
+  const double Hi2 = h2_exact(h, ph.gamma_k);
+  const float Hfac = (1.f + g.skin) * ph.gamma_k;
+  const int cxi = cell_axis(xi.x, g.nx), cyi = cell_axis(xi.y, g.ny), czi = cell_axis(xi.z, g.nz);
+  const uint32_t* lst = s.wnbr + (size_t)wi * s.wlcap;
+  const int n = s.wcount[wi];
+  ForceAcc a{0.f, 0.f, 0.f, 0.f, 2.f * I.a.z, 0};
+  unsigned long long scattered = 0;
+  for (int k = 0; k < n; ++k) {
+    const int j = (int)__ldg(lst + k);
+    const uint4 xj = s.xh[j];
+    const float hj = __uint_as_float(xj.w);
+    const ForceSide J = side_of(s, j, hj);
+    const float3 d = rel(g, xi, xj);
+    auto exact = [&]() {
+      return exact_neighbour(s.xh, i, j, fmax(Hi2, h2_exact(hj, ph.gamma_k)), g.dscale[0], g.dscale[1], g.dscale[2]);
+    };
+    float vs;
+    int in;
+    force_pair(a, d.x, d.y, d.z, I, J, ph.beta, kBandW, exact, vs, in);
+    // did j list i?  tile particles list the cells within +-1 of their own, wide ones the
+    // cells within their list radius at build time (k_wide_lists)
+    const int cxj = cell_axis(xj.x, g.nx), cyj = cell_axis(xj.y, g.ny), czj = cell_axis(xj.z, g.nz);
+    const bool jwide = s.wide[j] != 0;
+    const float Rj = Hfac * s.hbuild[j];
+    const int kx = jwide ? reach(Rj, g.side[0], g.nx) : 1, ky = jwide ? reach(Rj, g.side[1], g.ny) : 1,
+              kz = jwide ? reach(Rj, g.side[2], g.nz) : 1;
+    const bool seen = within(cxi, cxj, kx, g.nx) && within(cyi, cyj, ky, g.ny) && within(czi, czj, kz, g.nz);
+    if (!seen && j != i) {
+      // j's side of the pair (r_ji = -r_ij): the same symmetric terms, its own accumulators
+      ForceAcc b{0.f, 0.f, 0.f, 0.f, 0.f, 0};
+      float vs2;
+      int in2;
+      force_pair(b, -d.x, -d.y, -d.z, J, I, ph.beta, kBandW, exact, vs2, in2);
+      atomicAdd(&s.acc[j].x, b.ax);
+      atomicAdd(&s.acc[j].y, b.ay);
+      atomicAdd(&s.acc[j].z, b.az);
+      atomicAdd(&s.acc[j].w, b.du);
+      if (in2) {
+        atomicMax(reinterpret_cast<int*>(&s.vsig[j]), __float_as_int(vs2));
+        atomicAdd(&s.countf[j], 1);
+        dt_candidate(ph, ctr, hj, vs2);
+        ++scattered;
+      }
+    }
+  }
+  atomicAdd(&s.acc[i].x, a.ax);
+  atomicAdd(&s.acc[i].y, a.ay);
+  atomicAdd(&s.acc[i].z, a.az);
+  atomicAdd(&s.acc[i].w, a.du);
+  atomicMax(reinterpret_cast<int*>(&s.vsig[i]), __float_as_int(a.vmax));
+  atomicAdd(&s.countf[i], a.nn - 1);  // (the self pair)
+  dt_candidate(ph, ctr, h, a.vmax);
+  if (!(isfinite(a.vmax) && isfinite(a.ax) && isfinite(a.ay) && isfinite(a.az) && isfinite(a.du)))
+    atomicExch(&ctr->nonfinite, 1);
+  atomicAdd(&ctr->pairs, (unsigned long long)(a.nn - 1) + scattered);
+}
+
+}  // namespace
+
+cudaError_t launch_mark_wide(int n, const DevGrid& g, const DevPhys& ph, const DevState& s, uint8_t* flag,
+                             cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  k_mark_wide<<<(n + 255) / 256, 256, 0, st>>>(n, g, ph, s, flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wide_lists(const DevGrid& g, const DevPhys& ph, const DevState& s, const int* cell_start,
+                              DevCounters* ctr, cudaStream_t st) {
+  if (s.n_wide <= 0) return cudaSuccess;
+  k_wide_lists<<<(s.n_wide * 32 + 255) / 256, 256, 0, st>>>(g, ph, s, cell_start, ctr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wide_density(const DevGrid& g, const DevPhys& ph, const DevState& s, int pass, float hfac_stale,
+                                DevCounters* ctr, cudaStream_t st) {
+  if (s.n_wide <= 0) return cudaSuccess;
+  k_wide_density<<<(s.n_wide + 127) / 128, 128, 0, st>>>(g, ph, s, pass, hfac_stale, ctr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wide_gradient(const DevGrid& g, const DevPhys& ph, const DevState& s, float dt, int first_step,
+                                 DevCounters* ctr, cudaStream_t st) {
+  if (s.n_wide <= 0) return cudaSuccess;
+  k_wide_gradient<<<(s.n_wide + 127) / 128, 128, 0, st>>>(g, ph, s, dt, first_step, ctr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wide_force(const DevGrid& g, const DevPhys& ph, const DevState& s, DevCounters* ctr,
+                              cudaStream_t st) {
+  if (s.n_wide <= 0) return cudaSuccess;
+  k_wide_zero<<<(s.n_wide + 255) / 256, 256, 0, st>>>(s);
+  k_wide_force<<<(s.n_wide + 127) / 128, 128, 0, st>>>(g, ph, s, ctr);
+  return cudaGetLastError();
+}
+
+}  // namespace sph

@@ -23,6 +23,8 @@ def _cases():
         "sod16": lambda: W.sod(16),
         "gresho24": lambda: W.gresho(24),
         "gresho24j": lambda: W.gresho(24, jitter=0.1),
+        # C3-like h contrast: the adaptive grid with wide particles
+        "sedov24": lambda: W.sedov(24),
     }
 
 
@@ -55,7 +57,7 @@ def test_density_fixed_h(case):
     assert g["stats"]["pairs_density"] == int(d["count"].sum())
 
 
-@pytest.mark.parametrize("case", ["lattice16", "jitter16", "poisson4096", "sod16", "gresho24j"])
+@pytest.mark.parametrize("case", ["lattice16", "jitter16", "poisson4096", "sod16", "gresho24j", "sedov24"])
 def test_full_pass_fixed_h(case):
     """Density -> finalize -> gradient (+ghost) -> force -> dt at the given h."""
     p = _with_switches(_cases()[case](), 5)
@@ -85,7 +87,7 @@ def test_full_pass_fixed_h(case):
 
 
 @pytest.mark.parametrize("case,fac", [("lattice16", 1.5), ("lattice16", 0.7), ("jitter16", 1.3),
-                                      ("poisson4096", 1.0), ("sod16", 1.2)])
+                                      ("poisson4096", 1.0), ("sod16", 1.2), ("sedov24", 1.0)])
 def test_h_iteration_end_to_end(case, fac):
     """Newton h iteration on the GPU vs the oracle's exact root (tol 1e-13): with the GPU at
     h_tol = 1e-6, h and rho agree to 1e-5 and counts are exact; with the paper's 1e-4 every
@@ -134,12 +136,25 @@ def test_isolated_particle_not_converged():
     p["X"][0] = p["X"][0]  # keep lattice; make particle 0 isolated by shrinking its h
     p["h"] = p["h"].copy()
     p["h"][0] = p["h"][0] * 0.05
-    ctx = Context(p, h_max_iter=3)
+    ctx = Context(p, h_max_iter=3, adaptive_h=0)
     st = ctx.density(allow_unconverged=True)
     assert st["status"] == 5 and st["unconverged"] >= 1
     assert ctx.get("iters")[0] == -1
-    with pytest.raises(SphError):
+    with pytest.raises(SphError):  # resumes from the kept h: outgrows the fixed grid
         ctx.density()
+    ctx.close()
+    # with the adaptive grid the particle becomes wide as its h grows and the resumed
+    # iteration reaches the closure
+    ctx = Context(p, h_max_iter=3)
+    assert ctx.density(allow_unconverged=True)["status"] == 5
+    st = None
+    for _ in range(4):
+        st = ctx.density(allow_unconverged=True)
+        if st["status"] == 0:
+            break
+    assert st["status"] == 0
+    eta3 = 1.2348 ** 3
+    assert abs(float(ctx.get("nhat")[0]) * float(ctx.get("h")[0]) ** 3 - eta3) <= 1.2e-4 * eta3
     ctx.close()
 
 
@@ -173,3 +188,37 @@ def test_box_too_small_is_an_error():
     p = W.lattice(4, h_factor=1.0)
     with pytest.raises(SphError):
         Context(p)
+
+
+def test_adaptive_grid_has_wide_particles():
+    """Sedov's h contrast overflows tiles sized from h_max: the grid is sized from an h quantile
+    and the particles whose support exceeds a cell are wide; parity with the
+    oracle is covered by the sedov24 cases above.  Turning the adaptive grid off restores the
+    explicit error."""
+    from paper_2505_14538_b200 import Context, SphError
+
+    p = W.sedov(24)
+    ctx = Context(p)
+    ctx.density()
+    nw = ctx.counters()["wide_particles"]
+    assert 0 < nw < len(p["h"]) // 4
+    ctx.close()
+    with pytest.raises(SphError):
+        Context(p, adaptive_h=0)
+
+
+def test_wide_scatter_conserves_momentum_and_energy():
+    """Force pairs of wide particles with partners that do not list them are scattered to the
+    partner (R3's symmetric set): sum m a and sum m (v.a + du) still vanish to 1e-5 of scale."""
+    p = _with_switches(W.sedov(24), 7)
+    g = gpu_hydro(p, fixed_h=True)
+    assert g["counters"]["wide_particles"] > 0
+    m = p["m"].astype(np.float64)
+    a = g["a"].astype(np.float64)
+    v = p["v"].astype(np.float64)
+    du = g["du"].astype(np.float64)
+    P = (m[:, None] * a).sum(0)
+    assert np.all(np.abs(P) <= 1e-5 * (m[:, None] * np.abs(a)).sum(0))
+    va = (v * a).sum(1)
+    E = (m * (va + du)).sum()
+    assert abs(E) <= 1e-5 * (m * (np.abs(va) + np.abs(du))).sum()

@@ -281,12 +281,14 @@ def run_ours(args, world, rank, local):
     inter = 0
     pd = pg = pf = ph_iter = 0
     iters = []
+    regrids = []
     for st, c in log:
         pd += c["pairs_density"]
         pg += c["pairs_gradient"]
         pf += c["pairs_force"]
         ph_iter += c["pairs_h_iter"]
         iters.append(st["iterations"])
+        regrids.append(st["rebuilds"])
     inter = pd + pg + pf
     K = args.steps
     ms_step = ms / K
@@ -346,7 +348,8 @@ def run_ours(args, world, rank, local):
                        "parallelism": f"x-slabs{world} (NCCL halo exchange)" if world > 1 else "1gpu",
                        "step": "KDK: kick/drift, rebuild, density+h-iteration, gradient, force+dt, kick",
                        "l2": "inputs larger than L2 (n x ~300 B >> 126 MB)",
-                       "interactions_per_step": inter_all / K, "density_passes_mean": float(np.mean(iters))},
+                       "interactions_per_step": inter_all / K, "density_passes_mean": float(np.mean(iters)),
+                       "density_regrids_mean": float(np.mean(regrids))},
             "gpu_launches": int(launches),
             "kernels": kernels,
             "roofline": roof,

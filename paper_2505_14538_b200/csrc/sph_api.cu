@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -261,6 +262,7 @@ struct sph_ctx {
   int lcap = kLcapInit;
   // wide particles (adaptive cell side, sph_wide.cu)
   float h_side = 0.f;          // h the cell side is sized from (0: the global h_max)
+  double adapt_q = 0.0;        // its quantile (0: none)
   uint8_t* wide_flag = nullptr;
   int32_t* widx = nullptr;
   int32_t* wcount = nullptr;
@@ -637,9 +639,33 @@ sph_status h_quantile(sph_ctx* c, double q, float* out);
 // particles whose support exceeds a cell then become wide (sph_wide.cu).
 sph_status rebuild(sph_ctx* c) {
   Timed tm(c, SPH_T_REBUILD);
+  const bool adaptive = !c->slab && c->cfg.adaptive_h;
+  sph_status st;
+  if (adaptive && c->adapt_q > 0.0) {  // the quantile that worked last time, first
+    float hq;
+    const auto t0 = std::chrono::steady_clock::now();
+    if ((st = h_quantile(c, c->adapt_q, &hq)) != SPH_OK) return st;
+    const auto t1 = std::chrono::steady_clock::now();
+    c->h_side = hq;
+    st = rebuild_impl(c);
+    const auto t2 = std::chrono::steady_clock::now();
+    if (st == SPH_OK) {
+      st = mark_wide(c);
+      if (getenv("SPH_DEBUG")) {
+        cudaStreamSynchronize(c->stream);
+        const auto t3 = std::chrono::steady_clock::now();
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        fprintf(stderr, "[sph] rebuild ms: quantile %.3f grid %.3f wide %.3f (n_wide %d)\n", ms(t0, t1), ms(t1, t2),
+                ms(t2, t3), c->s.n_wide);
+      }
+      return st;
+    }
+    if (st != SPH_ERR_H_EXCEEDS_CELL) return st;
+  }
   c->h_side = 0.f;
-  sph_status st = rebuild_impl(c);
-  if (st == SPH_ERR_H_EXCEEDS_CELL && !c->slab && c->cfg.adaptive_h) {
+  c->adapt_q = 0.0;
+  st = rebuild_impl(c);
+  if (st == SPH_ERR_H_EXCEEDS_CELL && adaptive) {
     const std::string first = c->err;
     float tried = std::numeric_limits<float>::infinity();
     for (double q : {0.99, 0.95, 0.9, 0.8, 0.65, 0.5, 0.35, 0.2}) {
@@ -653,10 +679,14 @@ sph_status rebuild(sph_ctx* c) {
       if (getenv("SPH_DEBUG"))
         fprintf(stderr, "[sph] adaptive grid: h quantile %.2f = %.6g -> status %d (%s)\n", q, hq, (int)st,
                 st == SPH_OK ? "ok" : c->err.c_str());
-      if (st != SPH_ERR_H_EXCEEDS_CELL) break;
+      if (st != SPH_ERR_H_EXCEEDS_CELL) {
+        c->adapt_q = q;
+        break;
+      }
     }
     if (st == SPH_ERR_H_EXCEEDS_CELL) {
       c->h_side = 0.f;
+      c->adapt_q = 0.0;
       return fail(c, st, first);
     }
   }
@@ -762,10 +792,13 @@ sph_status rebuild_impl(sph_ctx* c) {
     const long long nnew = nmid + mL + mR;
     if ((st = agree(c, nnew > c->cap, SPH_ERR_OOM, "slab holds more particles than the context capacity")) != SPH_OK)
       return st;
+    const size_t mig_old = c->mig_cap;
     if ((st = grow(c, &c->mig_send, c->mig_cap, (size_t)std::max(nL + nR, mL + mR) * 2 + 16)) != SPH_OK) return st;
-    if (c->mig_recv) cudaFree(c->mig_recv);
-    c->mig_recv = nullptr;
-    CK(dalloc(&c->mig_recv, c->mig_cap));
+    if (!c->mig_recv || c->mig_cap != mig_old) {  // (same capacity as mig_send)
+      if (c->mig_recv) cudaFree(c->mig_recv);
+      c->mig_recv = nullptr;
+      CK(dalloc(&c->mig_recv, c->mig_cap));
+    }
     MigRec* sR = c->mig_send;
     MigRec* sL = c->mig_send + nR;
     if (nR > 0) k_pack_mig<<<nblk(nR, 256), 256, 0, c->stream>>>((int)nR, c->perm_alt + cP1, cur, sR);
@@ -805,12 +838,15 @@ sph_status rebuild_impl(sph_ctx* c) {
       return st;
     c->gL = (int)gL;
     c->gR = (int)gR;
+    const size_t pc_old = c->pc_cap;
     if ((st = grow(c, &c->pc_send, c->pc_cap, (size_t)4 * pcells + 64)) != SPH_OK) return st;
-    if (c->pc_recv) cudaFree(c->pc_recv);
-    if (c->pc_scan) cudaFree(c->pc_scan);
-    c->pc_recv = c->pc_scan = nullptr;
-    CK(dalloc(&c->pc_recv, c->pc_cap));
-    CK(dalloc(&c->pc_scan, c->pc_cap));
+    if (!c->pc_recv || c->pc_cap != pc_old) {  // (same capacity as pc_send)
+      if (c->pc_recv) cudaFree(c->pc_recv);
+      if (c->pc_scan) cudaFree(c->pc_scan);
+      c->pc_recv = c->pc_scan = nullptr;
+      CK(dalloc(&c->pc_recv, c->pc_cap));
+      CK(dalloc(&c->pc_scan, c->pc_cap));
+    }
     k_plane_counts<<<nblk(pcells, 256), 256, 0, c->stream>>>(pcells, c->cell_start, P * pcells, c->pc_send);
     k_plane_counts<<<nblk(pcells, 256), 256, 0, c->stream>>>(pcells, c->cell_start, pcells, c->pc_send + pcells);
     c->launches += 2;
@@ -914,10 +950,13 @@ sph_status rebuild_impl(sph_ctx* c) {
             c->rank, g.nx, g.ny, g.nz, g.nxo, g.ix_first, g.bx, g.by, g.nbx, g.nby, g.KZ, g.nzb, g.nblocks, g.tcap,
             c->n_own, c->gL, c->gR, c->planeL, c->planeR, cs[0], cs[g.ncells], bad, g.x_lo, g.wfix);
   }
+  const size_t blk_old = c->blk_cap;
   if ((st = grow(c, &c->blk[0], c->blk_cap, (size_t)g.nblocks)) != SPH_OK) return st;
-  if (c->blk[1]) cudaFree(c->blk[1]);
-  c->blk[1] = nullptr;
-  CK(dalloc(&c->blk[1], c->blk_cap));
+  if (!c->blk[1] || c->blk_cap != blk_old) {  // (same capacity as blk[0])
+    if (c->blk[1]) cudaFree(c->blk[1]);
+    c->blk[1] = nullptr;
+    CK(dalloc(&c->blk[1], c->blk_cap));
+  }
   c->stale = false;
   c->lists_stale = true;
   c->dvc_valid = false;
@@ -982,11 +1021,11 @@ sph_status mark_wide(sph_ctx* c) {
   s.wcount = c->wcount;
   s.wlcap = c->wlcap;
   const size_t want = (size_t)std::max(nw, 1) * c->wlcap;
-  if (want > c->wnbr_cap) {
+  if (want > c->wnbr_cap) {  // (with headroom: the wide set changes a little every rebuild)
     if (c->wnbr) cudaFree(c->wnbr);
     c->wnbr = nullptr;
-    CK(dalloc(&c->wnbr, want));
-    c->wnbr_cap = want;
+    CK(dalloc(&c->wnbr, want + want / 2));
+    c->wnbr_cap = want + want / 2;
   }
   s.wnbr = c->wnbr;
   return SPH_OK;
@@ -1203,9 +1242,15 @@ sph_status sph_density(sph_ctx* c, sph_density_stats* stats) {
     if (fl[0] == 0) break;
     if (fl[1] > 0) {
       // an h grew past what the cell grid holds: rebin with the new h and restart the passes
+      // (adaptive grid: the particle just becomes wide, no rebinning)
       if (++rebuilds > 8) return fail(c, SPH_ERR_H_EXCEEDS_CELL, "h kept outgrowing the cell grid");
       pairs_all += (long long)c->ctr_h->pairs_all;
-      if ((st = rebuild(c)) != SPH_OK) return st;
+      if (c->h_side > 0.f && !c->slab) {
+        Timed tm(c, SPH_T_REBUILD);
+        if ((st = mark_wide(c)) != SPH_OK) return st;
+      } else if ((st = rebuild(c)) != SPH_OK) {
+        return st;
+      }
       if ((st = build_lists(c)) != SPH_OK) return st;
       if ((st = reset_ctr(c)) != SPH_OK) return st;
       pass = 0;

@@ -62,6 +62,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample", default="G64", choices=sorted(WORKLOADS))
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
+    ap.add_argument("--tile-z", type=int, default=0, help="cells per CTA block along z (0 = auto)")
     return ap.parse_args()
 
 
@@ -226,6 +227,8 @@ def run_ours(args, world, rank, local):
     if world > 1:
         uid = share_uid(nccl_unique_id() if rank == 0 else b"", rank, device=dev)
         multi = dict(rank=rank, nranks=world, n_total=n_total, nccl_uid=uid)
+    if args.tile_z:
+        multi["tile_cells_z"] = args.tile_z
     ctx = Context(p, stream=stream.cuda_stream, device=local, **multi)
     dt = 1e-4
 

@@ -32,6 +32,7 @@ struct DevGrid {
   int icap;           // most i particles (owned by the block) of any block
   int lcap;           // neighbour-list capacity per particle (multiple of 16)
   float skin;         // list radius = (1 + skin) max(H_i, H_j)
+  int force_threads;  // block size of the force kernel: 256, or 512 when one CTA fills an SM
   float scale[3];     // L_a / 2^32 as f32 (fixed point -> length)
   double dscale[3];   // L_a * 2^-32 exact (fp64 exact neighbour test)
   float side[3];      // cell side per axis

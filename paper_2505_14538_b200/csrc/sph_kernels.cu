@@ -580,15 +580,16 @@ __global__ void __launch_bounds__(256) k_bank(int i0, int n, DevGrid g, DevState
 // groups lie inside one thread's range is summed by that thread alone and stored; a particle
 // split across threads gets its partial sums combined with shared-memory atomics (float
 // adds: the split particles' sums may differ in the last bit between runs).
-constexpr int kNT = kNW * 32;
-__device__ __forceinline__ int group_start(int t, int G) { return (int)(((long long)t * G) / kNT); }
+constexpr int kMaxNW = 16;  // loop kernels run 256 or 512 threads (blockDim.x)
+__device__ __forceinline__ int group_start(int t, int G) { return (int)(((long long)t * G) / blockDim.x); }
 
 // In-place exclusive scan of a[0..n) by the whole block; a[n] = total.  Ends with a barrier.
 __device__ void block_exclusive_scan(int* a, int n) {
-  __shared__ int s_w[kNW + 1];
+  __shared__ int s_w[kMaxNW + 1];
+  const int nw = blockDim.x >> 5, nt = blockDim.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int carry = 0;
-  for (int base = 0; base < n; base += kNT) {
+  for (int base = 0; base < n; base += nt) {
     const int k = base + threadIdx.x;
     const int v0 = k < n ? a[k] : 0;
     int v = v0;
@@ -601,16 +602,16 @@ __device__ void block_exclusive_scan(int* a, int n) {
     __syncthreads();
     if (threadIdx.x == 0) {
       int acc = 0;
-      for (int w = 0; w < kNW; ++w) {
+      for (int w = 0; w < nw; ++w) {
         const int t = s_w[w];
         s_w[w] = acc;
         acc += t;
       }
-      s_w[kNW] = acc;
+      s_w[nw] = acc;
     }
     __syncthreads();
     if (k < n) a[k] = carry + s_w[warp] + v - v0;
-    carry += s_w[kNW];
+    carry += s_w[nw];
     __syncthreads();
   }
   if (threadIdx.x == 0) a[n] = carry;
@@ -706,7 +707,7 @@ template <class Acc>
 __device__ __forceinline__ void walk_prefix(const BlockShared& S, const DevState& s, WalkArea<Acc>& W, int ni) {
   const int* kl = W.kl;
   int* pref = W.pref;
-  for (int k = threadIdx.x; k < ni; k += kNT) {
+  for (int k = threadIdx.x; k < ni; k += blockDim.x) {
     int ti, gi;
     i_slot(S, kl[k], ti, gi);
     pref[k] = __ldg(s.ncount + gi) >> 3;
@@ -725,7 +726,7 @@ __device__ __forceinline__ void walk_prefix(const BlockShared& S, const DevState
 // Then nhat = S0/(pi h^3), dn/dh = -(3 S0 + S1)/(pi h^4), rho = R0/(pi h^3),
 // drho/dh = -(3 R0 + R1)/(pi h^4), div = -Dv/(rho pi h^4), curl = Cv/(rho pi h^4),
 // g = nhat h^3 - eta^3 = S0/pi - eta^3, h g' = -S1/pi.
-__global__ void __launch_bounds__(kNW * 32, 2) k_density(DevGrid g, DevPhys ph, DevState s,
+__global__ void __launch_bounds__(256, 3) k_density(DevGrid g, DevPhys ph, DevState s,
                                                       const int* __restrict__ cell_start, int pass,
                                                       const uint8_t* __restrict__ blk_in, uint8_t* __restrict__ blk_out,
                                                       float hfac_stale, DevCounters* __restrict__ ctr) {
@@ -754,17 +755,17 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_density(DevGrid g, DevPhys ph, 
   // the walk's particles: all of the block (pass 0) or the still active ones, compacted in
   // block order (deterministic)
   if (pass == 0) {
-    for (int k = threadIdx.x; k < T.ni; k += kNT) W.kl[k] = k;
+    for (int k = threadIdx.x; k < T.ni; k += blockDim.x) W.kl[k] = k;
     if (threadIdx.x == 0) s_ni = T.ni;
   } else {
-    for (int k = threadIdx.x; k < T.ni; k += kNT) {
+    for (int k = threadIdx.x; k < T.ni; k += blockDim.x) {
       int ti, gi;
       i_slot(S, k, ti, gi);
       W.pref[k] = s.active[gi] ? 1 : 0;
     }
     __syncthreads();
     block_exclusive_scan(W.pref, T.ni);
-    for (int k = threadIdx.x; k < T.ni; k += kNT)
+    for (int k = threadIdx.x; k < T.ni; k += blockDim.x)
       if (W.pref[k + 1] > W.pref[k]) W.kl[W.pref[k]] = k;
     if (threadIdx.x == 0) s_ni = W.pref[T.ni];
   }
@@ -804,7 +805,7 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_density(DevGrid g, DevPhys ph, 
   }
   __syncthreads();
   unsigned long long npairs = 0, nfinal = 0;
-  for (int k = threadIdx.x; k < ni; k += kNT) {
+  for (int k = threadIdx.x; k < ni; k += blockDim.x) {
     const DenAcc a = W.fin[k];
     int ti, gi;
     i_slot(S, W.kl[k], ti, gi);
@@ -841,7 +842,7 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_density(DevGrid g, DevPhys ph, 
 // Brookshaw Laplacian lap u_i = 2 sum_j (m_j/rho_j)(u_i - u_j) dW/dr / r (R16), gathered
 // over r_ij < H_i; the gradient ghost (alpha_v Eqs. 12-15, alpha_c Eqs. 21-24; R17-R21)
 // runs in the epilogue and writes the force-loop records.
-__global__ void __launch_bounds__(kNW * 32, 2) k_gradient(DevGrid g, DevPhys ph, DevState s,
+__global__ void __launch_bounds__(256, 3) k_gradient(DevGrid g, DevPhys ph, DevState s,
                                                        const int* __restrict__ cell_start, float dt, int first_step,
                                                        DevCounters* __restrict__ ctr) {
   __shared__ unsigned long long s_pairs;
@@ -866,7 +867,7 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_gradient(DevGrid g, DevPhys ph,
     smem4[O2 + g.tcap + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 1.f);
   }
   const int ni = T.ni;
-  for (int k = threadIdx.x; k < ni; k += kNT) W.kl[k] = k;
+  for (int k = threadIdx.x; k < ni; k += blockDim.x) W.kl[k] = k;
   __syncthreads();
   walk_prefix(S, s, W, ni);
   {
@@ -907,7 +908,7 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_gradient(DevGrid g, DevPhys ph,
   }
   __syncthreads();
   unsigned long long npairs = 0;
-  for (int k = threadIdx.x; k < ni; k += kNT) {
+  for (int k = threadIdx.x; k < ni; k += blockDim.x) {
     const GradAcc a = W.fin[k];
     int ti, gi;
     i_slot(S, k, ti, gi);
@@ -937,7 +938,7 @@ __host__ __device__ __forceinline__ size_t force_records_bytes(int tcap) {
   return (size_t)(tcap + kNSent) * (4 * 16);
 }
 
-__global__ void __launch_bounds__(kNW * 32, 2) k_force(DevGrid g, DevPhys ph, DevState s,
+__global__ void __launch_bounds__(512, 1) k_force(DevGrid g, DevPhys ph, DevState s,
                                                     const int* __restrict__ cell_start,
                                                     DevCounters* __restrict__ ctr) {
   __shared__ unsigned long long s_pairs;
@@ -975,7 +976,7 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_force(DevGrid g, DevPhys ph, De
     smem4[O3 + g.tcap + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   const int ni = T.ni;
-  for (int k = threadIdx.x; k < ni; k += kNT) W.kl[k] = k;
+  for (int k = threadIdx.x; k < ni; k += blockDim.x) W.kl[k] = k;
   __syncthreads();
   walk_prefix(S, s, W, ni);
   {
@@ -1029,7 +1030,7 @@ __global__ void __launch_bounds__(kNW * 32, 2) k_force(DevGrid g, DevPhys ph, De
   __syncthreads();
   unsigned long long npairs = 0;
   float dtmin = CUDART_INF_F;
-  for (int k = threadIdx.x; k < ni; k += kNT) {
+  for (int k = threadIdx.x; k < ni; k += blockDim.x) {
     const ForceAcc a = W.fin[k];
     int ti, gi;
     i_slot(S, k, ti, gi);
@@ -1153,7 +1154,7 @@ cudaError_t launch_force(const DevGrid& g, const DevPhys& ph, const DevState& s,
   const size_t sm = force_smem(g);
   cudaError_t e = set_smem((const void*)k_force, sm);
   if (e != cudaSuccess) return e;
-  k_force<<<g.nblocks, kNW * 32, sm, st>>>(g, ph, s, cell_start, ctr);
+  k_force<<<g.nblocks, g.force_threads, sm, st>>>(g, ph, s, cell_start, ctr);
   return cudaGetLastError();
 }
 

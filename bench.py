@@ -45,6 +45,7 @@ WORKLOADS = {
     "C4j": ("gresho256_jitter0.1", lambda: W.gresho(256, jitter=0.1)),
     "C2": ("sod2x64", lambda: W.sod(64)),
     "C3": ("sedov128", lambda: W.sedov(128)),
+    "C5s": ("clustered128", lambda: W.clustered(128 ** 3)),
     "C1": ("lattice16", lambda: W.lattice(16)),
     "G128": ("gresho128", lambda: W.gresho(128)),
     "G64": ("gresho64", lambda: W.gresho(64)),

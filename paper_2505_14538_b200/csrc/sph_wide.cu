@@ -8,7 +8,7 @@
 //   - k_wide_lists: one warp per wide particle i scans the cells within +-k_a of its cell
 //     (k_a = ceil(list radius / side_a) per axis) and lists, by global index, every j with
 //     r_ij < (1 + skin) gamma_k max(h_i, h_j) -- the same criterion as the tile lists;
-//   - k_wide_density / k_wide_gradient / k_wide_force: one thread per wide particle runs
+//   - k_wide_density / k_wide_gradient / k_wide_force: one warp per wide particle runs
 //     the shared pair arithmetic (sph_pair.cuh) over its list, gathering the neighbour
 //     records from global memory (L2), with the same epilogues as the tile loops;
 //   - symmetry of the force set r < max(H_i, H_j) (R3): a partner j that did not list i
@@ -122,12 +122,30 @@ __device__ __forceinline__ float3 rel(const DevGrid& g, const uint4& a, const ui
 // by < 1e-6 relative)
 constexpr float kBandW = 2e-5f;
 
-__global__ void __launch_bounds__(128) k_wide_density(DevGrid g, DevPhys ph, DevState s, int pass, float hfac_stale,
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+__device__ __forceinline__ int warp_isum(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_fmax(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+
+// One warp per wide particle: the lanes split the list, the sums are reduced over the warp
+// (lane order, deterministic), lane 0 runs the epilogue.
+__global__ void __launch_bounds__(256) k_wide_density(DevGrid g, DevPhys ph, DevState s, int pass, float hfac_stale,
                                                       DevCounters* __restrict__ ctr) {
-  const int wi = blockIdx.x * blockDim.x + threadIdx.x;
+  const int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (wi >= s.n_wide) return;
   const int i = s.widx[wi];
-  if (pass > 0 && !s.active[i]) return;
+  if (pass > 0 && !s.active[i]) return;  // warp-uniform
   const uint4 xi = s.xh[i];
   const float4 vi = s.vm[i];
   const float h = __uint_as_float(xi.w), hinv = 1.f / h;
@@ -135,13 +153,17 @@ __global__ void __launch_bounds__(128) k_wide_density(DevGrid g, DevPhys ph, Dev
   const uint32_t* lst = s.wnbr + (size_t)wi * s.wlcap;
   const int n = s.wcount[wi];
   DenAcc a = DenAcc::zero();
-  for (int k = 0; k < n; ++k) {
+  for (int k = lane; k < n; k += 32) {
     const int j = (int)__ldg(lst + k);
     const float3 d = rel(g, xi, s.xh[j]);
     den_pair(a, d.x, d.y, d.z, hinv, kBandW, vi, s.vm[j], [&]() {
       return exact_neighbour(s.xh, i, j, H2, g.dscale[0], g.dscale[1], g.dscale[2]);
     });
   }
+  a.S0 = warp_sum(a.S0); a.S1 = warp_sum(a.S1); a.R0 = warp_sum(a.R0); a.R1 = warp_sum(a.R1);
+  a.Dv = warp_sum(a.Dv); a.Cx = warp_sum(a.Cx); a.Cy = warp_sum(a.Cy); a.Cz = warp_sum(a.Cz);
+  a.nn = warp_isum(a.nn);
+  if (lane != 0) return;
   const DenOut o = den_epilogue(g, ph, s, a, i, h, vi.w, pass, hfac_stale);
   atomicAdd(&ctr->pairs_all, (unsigned long long)o.nn);
   if (o.final_) atomicAdd(&ctr->pairs, (unsigned long long)o.nn);
@@ -150,9 +172,9 @@ __global__ void __launch_bounds__(128) k_wide_density(DevGrid g, DevPhys ph, Dev
   if (o.stale) atomicExch(&ctr->list_stale, 1);
 }
 
-__global__ void __launch_bounds__(128) k_wide_gradient(DevGrid g, DevPhys ph, DevState s, float dt, int first_step,
+__global__ void __launch_bounds__(256) k_wide_gradient(DevGrid g, DevPhys ph, DevState s, float dt, int first_step,
                                                        DevCounters* __restrict__ ctr) {
-  const int wi = blockIdx.x * blockDim.x + threadIdx.x;
+  const int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (wi >= s.n_wide) return;
   const int i = s.widx[wi];
   const uint4 xi = s.xh[i];
@@ -163,13 +185,17 @@ __global__ void __launch_bounds__(128) k_wide_gradient(DevGrid g, DevPhys ph, De
   const uint32_t* lst = s.wnbr + (size_t)wi * s.wlcap;
   const int n = s.wcount[wi];
   GradAcc a{2.f * gi4.x, 0.f, 0};
-  for (int k = 0; k < n; ++k) {
+  for (int k = lane; k < n; k += 32) {
     const int j = (int)__ldg(lst + k);
     const float3 d = rel(g, xi, s.xh[j]);
     grad_pair(a, d.x, d.y, d.z, hinv, kBandW, vi, gi4.x, gi4.y, ph.beta, s.vm[j], s.gq[j], [&]() {
       return exact_neighbour(s.xh, i, j, H2, g.dscale[0], g.dscale[1], g.dscale[2]);
     });
   }
+  a.vmax = warp_fmax(a.vmax);
+  a.lap = warp_sum(a.lap);
+  a.nn = warp_isum(a.nn);
+  if (lane != 0) return;
   const int nn = grad_epilogue(ph, s, a, i, h, gi4.x, gi4.y, gi4.w, dt, first_step);
   atomicAdd(&ctr->pairs, (unsigned long long)nn);
 }
@@ -199,8 +225,8 @@ __device__ __forceinline__ void dt_candidate(const DevPhys& ph, DevCounters* ctr
   if (dt > 0.f && dt < CUDART_INF_F) atomicMin(&ctr->dt_bits, __float_as_uint(dt));
 }
 
-__global__ void __launch_bounds__(128) k_wide_force(DevGrid g, DevPhys ph, DevState s, DevCounters* __restrict__ ctr) {
-  const int wi = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(256) k_wide_force(DevGrid g, DevPhys ph, DevState s, DevCounters* __restrict__ ctr) {
+  const int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (wi >= s.n_wide) return;
   const int i = s.widx[wi];
   const uint4 xi = s.xh[i];
@@ -212,8 +238,8 @@ __global__ void __launch_bounds__(128) k_wide_force(DevGrid g, DevPhys ph, DevSt
   const uint32_t* lst = s.wnbr + (size_t)wi * s.wlcap;
   const int n = s.wcount[wi];
   ForceAcc a{0.f, 0.f, 0.f, 0.f, 2.f * I.a.z, 0};
-  unsigned long long scattered = 0;
-  for (int k = 0; k < n; ++k) {
+  int scattered = 0;
+  for (int k = lane; k < n; k += 32) {
     const int j = (int)__ldg(lst + k);
     const uint4 xj = s.xh[j];
     const float hj = __uint_as_float(xj.w);
@@ -251,6 +277,14 @@ __global__ void __launch_bounds__(128) k_wide_force(DevGrid g, DevPhys ph, DevSt
       }
     }
   }
+  a.ax = warp_sum(a.ax);
+  a.ay = warp_sum(a.ay);
+  a.az = warp_sum(a.az);
+  a.du = warp_sum(a.du);
+  a.vmax = warp_fmax(a.vmax);
+  a.nn = warp_isum(a.nn);
+  scattered = warp_isum(scattered);
+  if (lane != 0) return;
   atomicAdd(&s.acc[i].x, a.ax);
   atomicAdd(&s.acc[i].y, a.ay);
   atomicAdd(&s.acc[i].z, a.az);
@@ -260,7 +294,7 @@ __global__ void __launch_bounds__(128) k_wide_force(DevGrid g, DevPhys ph, DevSt
   dt_candidate(ph, ctr, h, a.vmax);
   if (!(isfinite(a.vmax) && isfinite(a.ax) && isfinite(a.ay) && isfinite(a.az) && isfinite(a.du)))
     atomicExch(&ctr->nonfinite, 1);
-  atomicAdd(&ctr->pairs, (unsigned long long)(a.nn - 1) + scattered);
+  atomicAdd(&ctr->pairs, (unsigned long long)(a.nn - 1) + (unsigned long long)scattered);
 }
 
 }  // namespace
@@ -282,14 +316,14 @@ cudaError_t launch_wide_lists(const DevGrid& g, const DevPhys& ph, const DevStat
 cudaError_t launch_wide_density(const DevGrid& g, const DevPhys& ph, const DevState& s, int pass, float hfac_stale,
                                 DevCounters* ctr, cudaStream_t st) {
   if (s.n_wide <= 0) return cudaSuccess;
-  k_wide_density<<<(s.n_wide + 127) / 128, 128, 0, st>>>(g, ph, s, pass, hfac_stale, ctr);
+  k_wide_density<<<(s.n_wide * 32 + 255) / 256, 256, 0, st>>>(g, ph, s, pass, hfac_stale, ctr);
   return cudaGetLastError();
 }
 
 cudaError_t launch_wide_gradient(const DevGrid& g, const DevPhys& ph, const DevState& s, float dt, int first_step,
                                  DevCounters* ctr, cudaStream_t st) {
   if (s.n_wide <= 0) return cudaSuccess;
-  k_wide_gradient<<<(s.n_wide + 127) / 128, 128, 0, st>>>(g, ph, s, dt, first_step, ctr);
+  k_wide_gradient<<<(s.n_wide * 32 + 255) / 256, 256, 0, st>>>(g, ph, s, dt, first_step, ctr);
   return cudaGetLastError();
 }
 
@@ -297,7 +331,7 @@ cudaError_t launch_wide_force(const DevGrid& g, const DevPhys& ph, const DevStat
                               cudaStream_t st) {
   if (s.n_wide <= 0) return cudaSuccess;
   k_wide_zero<<<(s.n_wide + 255) / 256, 256, 0, st>>>(s);
-  k_wide_force<<<(s.n_wide + 127) / 128, 128, 0, st>>>(g, ph, s, ctr);
+  k_wide_force<<<(s.n_wide * 32 + 255) / 256, 256, 0, st>>>(g, ph, s, ctr);
   return cudaGetLastError();
 }
 

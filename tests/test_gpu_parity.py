@@ -25,6 +25,8 @@ def _cases():
         "gresho24j": lambda: W.gresho(24, jitter=0.1),
         # C3-like h contrast: the adaptive grid with wide particles
         "sedov24": lambda: W.sedov(24),
+        # C5-like clustered box: uniform initial h, ~10x h contrast once converged
+        "clustered8k": lambda: W.clustered(8192, seed=77),
     }
 
 
@@ -87,7 +89,8 @@ def test_full_pass_fixed_h(case):
 
 
 @pytest.mark.parametrize("case,fac", [("lattice16", 1.5), ("lattice16", 0.7), ("jitter16", 1.3),
-                                      ("poisson4096", 1.0), ("sod16", 1.2), ("sedov24", 1.0)])
+                                      ("poisson4096", 1.0), ("sod16", 1.2), ("sedov24", 1.0),
+                                      ("clustered8k", 1.0)])
 def test_h_iteration_end_to_end(case, fac):
     """Newton h iteration on the GPU vs the oracle's exact root (tol 1e-13): with the GPU at
     h_tol = 1e-6, h and rho agree to 1e-5 and counts are exact; with the paper's 1e-4 every

@@ -186,7 +186,7 @@ def gresho(n=256, jitter=0.0, seed=3, h_factor=1.0):
                  h_factor * H_STAR_LATTICE * dx, (1.0, 1.0, 1.0))
 
 
-def clustered(N=128 ** 3, seed=12345, f_halo=0.6, core=0.05):
+def clustered(N=128 ** 3, seed=12345, f_halo=0.6, core=0.05, knn_h=True):
     """C5: cosmological-like clustered box, equal masses, u = 1.
 
     40 % uniform background + 60 % in NFW halos (c = 10, cored at core*r_s), halo sizes
@@ -225,11 +225,22 @@ def clustered(N=128 ** 3, seed=12345, f_halo=0.6, core=0.05):
         xs.append(centre[None, :] + dirs * rr[:, None])
         sig = 0.05 * (s / 64.0) ** (1.0 / 3.0)
         vs.append(rng.normal(0.0, sig, size=(s, 3)))
-    x = np.concatenate(xs)
+    x = np.concatenate(xs) % 1.0
     v = np.concatenate(vs)
-    dx = N ** (-1.0 / 3.0)
-    h = np.full(N, H_STAR_LATTICE * dx)
+    h = _h_from_knn(x, k=64) if knn_h else np.full(N, H_STAR_LATTICE * N ** (-1.0 / 3.0))
     return _pack(f"clustered{N}", _fixed_point(x, (1, 1, 1)), v, 1.0 / N, 1.0, h, (1.0, 1.0, 1.0))
+
+
+def _h_from_knn(x, k=64):
+    """Initial h from the local number density of the k nearest neighbours (periodic unit box):
+    n = k / (4/3 pi d_k^3), h = eta n^(-1/3) (the closure's target, R1).  A starting guess only:
+    the h iteration converges to the unique root from any start (R26)."""
+    from scipy.spatial import cKDTree
+
+    tree = cKDTree(x, boxsize=1.0)
+    d, _ = tree.query(x, k=[k], workers=-1)
+    n_loc = k / (4.0 / 3.0 * math.pi * d[:, 0] ** 3)
+    return ETA * n_loc ** (-1.0 / 3.0)
 
 
 def by_name(name: str, **kw):

@@ -354,7 +354,8 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
   if (threadIdx.x == 0) {
     int acc = 0;
     for (int e = 0; e < nicell; ++e) {
-      const int zz = e / ncolI + 1, k = e - (zz - 1) * ncolI;
+      // column-major: a warp's 32 particles share a column (coherent candidate windows)
+      const int k = e / (T.nzt - 2), zz = e - k * (T.nzt - 2) + 1;
       const int c = S.tc[k] * T.nzt + zz;
       s_cp[e] = acc;
       s_ct[e] = S.off[c];
@@ -390,7 +391,7 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
       const int mid = (lo + hi) >> 1;
       if (s_cp[mid] <= kk) lo = mid; else hi = mid;
     }
-    const int zz = lo / ncolI + 1, col = lo - (zz - 1) * ncolI;
+    const int col = lo / (T.nzt - 2), zz = lo - col * (T.nzt - 2) + 1;
     const int ti = s_ct[lo] + (kk - s_cp[lo]);
     const int gi = s_cg[lo] + (kk - s_cp[lo]);
     const float* pi = P + (ti >> 1) * 8 + (ti & 1);

@@ -237,34 +237,10 @@ __device__ __forceinline__ float3 rel_pos(const DevGrid& g, const Tile& T, uint4
                      (float)(int)(x.z - T.ref[2]) * g.scale[2]);
 }
 
-__device__ __forceinline__ int warp_min(int v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(kFull, v, o));
-  return v;
-}
 __device__ __forceinline__ int warp_max(int v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(kFull, v, o));
   return v;
-}
-
-// Iterate a particle's padded neighbour list in groups of 8 (one 16-byte load each).
-template <class PairF>
-__device__ __forceinline__ void for_list(const uint16_t* __restrict__ list, int cnt, PairF&& pair) {
-  const int mx = warp_max(cnt);
-  for (int k0 = 0; k0 < mx; k0 += 8) {
-    if (k0 < cnt) {
-      const uint4 e = __ldg(reinterpret_cast<const uint4*>(list + k0));
-      pair((int)(e.x & 0xffffu));
-      pair((int)(e.x >> 16));
-      pair((int)(e.y & 0xffffu));
-      pair((int)(e.y >> 16));
-      pair((int)(e.z & 0xffffu));
-      pair((int)(e.z >> 16));
-      pair((int)(e.w & 0xffffu));
-      pair((int)(e.w >> 16));
-    }
-  }
 }
 
 #define TILE_PROLOGUE()                                   \

@@ -203,7 +203,7 @@ def run_reference(args, world, rank):
     name, _ = WORKLOADS[args.workload]
     line = {"impl": "reference", "metric": "SPH pair interactions/sec (density+gradient+force)",
             "value": base["value"], "unit": "interactions/s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOADS[args.cpu_sample][0], "bench_workload": name,
                        "note": "fp64 oracle on host cores; bounded sample of the workload family"},
@@ -345,7 +345,7 @@ def run_ours(args, world, rank, local):
         line = {
             "metric": "SPH pair interactions/sec (density+gradient+force) and time per hydro step",
             "value": value, "unit": "interactions/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
-            "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling if world > 1 else "weak",
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
             "config": {"workload": name, "particles": n_total,

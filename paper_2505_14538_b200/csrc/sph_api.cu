@@ -286,6 +286,8 @@ struct sph_ctx {
   void* sort_tmp = nullptr;
   size_t sort_tmp_bytes = 0;
   uint8_t* blk[2] = {nullptr, nullptr};
+  char* desc_buf = nullptr;   // tile descriptors, nblocks x tile_desc_bytes()
+  size_t desc_cap = 0;
   size_t blk_cap = 0;
   DevCounters* ctr = nullptr;     // device
   DevCounters* ctr_h = nullptr;   // pinned host mirror
@@ -952,6 +954,11 @@ sph_status rebuild_impl(sph_ctx* c) {
             c->rank, g.nx, g.ny, g.nz, g.nxo, g.ix_first, g.bx, g.by, g.nbx, g.nby, g.KZ, g.nzb, g.nblocks, g.tcap,
             c->n_own, c->gL, c->gR, c->planeL, c->planeR, cs[0], cs[g.ncells], bad, g.x_lo, g.wfix);
   }
+  // per-block tile descriptors for the loop kernels (k_tile_desc)
+  if ((st = grow(c, &c->desc_buf, c->desc_cap, (size_t)g.nblocks * tile_desc_bytes())) != SPH_OK) return st;
+  g.desc = c->desc_buf;
+  CK(launch_tile_desc(g, c->cell_start, c->stream));
+  c->launches++;
   const size_t blk_old = c->blk_cap;
   if ((st = grow(c, &c->blk[0], c->blk_cap, (size_t)g.nblocks)) != SPH_OK) return st;
   if (!c->blk[1] || c->blk_cap != blk_old) {  // (same capacity as blk[0])
@@ -1498,7 +1505,7 @@ sph_status sph_destroy(sph_ctx* c) {
                   s.ncount, s.hbuild, c->cell_start, c->keys, c->keys_alt, c->perm, c->perm_alt, c->sort_tmp,
                   c->blk[0], c->blk[1], c->ctr, c->scratch, c->out_tmp, c->mig_send, c->mig_recv, c->pc_send,
                   c->pc_recv, c->pc_scan, c->scan_tmp, c->cnt_dev, c->wide_flag, c->widx, c->wcount,
-                  c->n_wide_dev, c->wnbr, c->sel_tmp};
+                  c->n_wide_dev, c->wnbr, c->sel_tmp, c->desc_buf};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->ctr_h) cudaFreeHost(c->ctr_h);

@@ -33,6 +33,7 @@ struct DevGrid {
   int lcap;           // neighbour-list capacity per particle (multiple of 16)
   float skin;         // list radius = (1 + skin) max(H_i, H_j)
   int force_threads;  // block size of the force kernel: 256, or 512 when one CTA fills an SM
+  const void* desc;   // [nblocks] tile descriptors (sph_kernels.cu TileDesc, k_tile_desc)
   float scale[3];     // L_a / 2^32 as f32 (fixed point -> length)
   double dscale[3];   // L_a * 2^-32 exact (fp64 exact neighbour test)
   float side[3];      // cell side per axis
@@ -139,5 +140,7 @@ cudaError_t launch_wide_gradient(const DevGrid& g, const DevPhys& ph, const DevS
 cudaError_t launch_wide_force(const DevGrid& g, const DevPhys& ph, const DevState& s, DevCounters* ctr,
                               cudaStream_t st);
 int kernel_threads();
+size_t tile_desc_bytes();
+cudaError_t launch_tile_desc(const DevGrid& g, const int* cell_start, cudaStream_t st);
 
 }  // namespace sph

@@ -67,6 +67,17 @@ struct BlockShared {
   int pre[kMaxICols + 1];      // prefix of i counts over the i columns
 };
 
+// A block's tile descriptor, computed once per rebuild (k_tile_desc: the tile geometry, the
+// contiguous segments to stage, the i columns) and loaded by the loop kernels with one
+// coalesced read instead of redoing tile_setup's cell scans and serial steps every launch.
+struct TileDesc {
+  Tile T;                      // 13 ints
+  int ib[kMaxICols], g0[kMaxICols], tc[kMaxICols], pre[kMaxICols + 1];
+  int pad[2];                  // (128-byte header)
+  int4 seg[kMaxSeg];           // (tile start, global start, length) per segment
+};
+static_assert(sizeof(TileDesc) % 16 == 0, "TileDesc size");
+
 // Launch order of the blocks: z fastest, then block columns in strips of kStrip columns
 // along y, column-major inside a strip, so the blocks whose tiles share a column (its x and
 // y neighbours) run within ~kStrip * nzb launches of each other and re-read the column's
@@ -185,7 +196,8 @@ __device__ void tile_setup(const DevGrid& g, int b, const int* __restrict__ cell
 }
 
 // block-local i index -> (tile slot, global index)
-__device__ __forceinline__ void i_slot(const BlockShared& S, int li, int& ti, int& gi) {
+template <class SS>
+__device__ __forceinline__ void i_slot(const SS& S, int li, int& ti, int& gi) {
   int k = 0;
 #pragma unroll
   for (int r = 1; r < kMaxICols; ++r) k += (li >= S.pre[r]) ? 1 : 0;
@@ -203,6 +215,15 @@ __device__ __forceinline__ int slot_global(const BlockShared& S, int nct, int t)
   return S.gst[lo] + (t - S.off[lo]);
 }
 
+// tile slot -> global particle index from the staged segments (rare path)
+__device__ __forceinline__ int slot_global(const TileDesc& D, int nseg, int t) {
+  for (int k = 0; k < nseg; ++k) {
+    const int4 sg = D.seg[k];
+    if (t >= sg.x && t < sg.x + sg.z) return sg.y + (t - sg.x);
+  }
+  return 0;  // (unreachable for a slot of the tile)
+}
+
 __device__ __forceinline__ void cp_async16(const void* smem_dst, const void* gmem_src) {
   const unsigned int d = (unsigned int)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src));
@@ -216,7 +237,8 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // Stage nrec16 16-byte per-particle records (at smem4[o16[r] + slot]) and optionally one
 // 4-byte record (at float offset o4) of every tile slot with cp.async: no register round
 // trip, every copy of the CTA in flight at once.
-__device__ __forceinline__ void stage_records(const BlockShared& S, int nseg, int nrec16, const float4* const* src16,
+template <class SS>
+__device__ __forceinline__ void stage_records(const SS& S, int nseg, int nrec16, const float4* const* src16,
                                               const int* o16, const float* src4, int o4) {
   float* sm1 = reinterpret_cast<float*>(smem4);
   // one warp per segment (segments are ~1-3 cells long): no block-wide pass over all of them
@@ -252,6 +274,23 @@ __device__ __forceinline__ int warp_max(int v) {
     return;                                               \
   }                                                       \
   const int nseg = 3 * T.ntc;                             \
+  const int SP = g.tcap + kNSent; /* slots per record array (the last kNSent are sentinels) */
+
+// Loop kernels: the block's descriptor from k_tile_desc (S.seg, S.ib, ... and T), one barrier.
+#define DESC_PROLOGUE()                                                          \
+  __shared__ TileDesc S;                                                         \
+  {                                                                              \
+    const int* src_ = reinterpret_cast<const int*>(g.desc) + (size_t)blockIdx.x * (sizeof(TileDesc) / 4); \
+    int* dst_ = reinterpret_cast<int*>(&S);                                      \
+    for (int q_ = threadIdx.x; q_ < (int)(sizeof(TileDesc) / 4); q_ += blockDim.x) dst_[q_] = __ldg(src_ + q_); \
+  }                                                                              \
+  __syncthreads();                                                               \
+  const Tile T = S.T;                                                            \
+  if (T.ntile > g.tcap) {                                                        \
+    if (threadIdx.x == 0) atomicExch(&ctr->nonfinite, 2);                        \
+    return;                                                                      \
+  }                                                                              \
+  const int nseg = 3 * T.ntc;                                                    \
   const int SP = g.tcap + kNSent; /* slots per record array (the last kNSent are sentinels) */
 
 // ========================================================== neighbour lists ==========
@@ -680,8 +719,8 @@ __device__ __forceinline__ WalkArea<Acc> walk_area(char* base, int icap) {
 
 // Fill pref[] with the list groups of the walk's particles (kl[0..ni)), scan it, and clear
 // the accumulators.
-template <class Acc>
-__device__ __forceinline__ void walk_prefix(const BlockShared& S, const DevState& s, WalkArea<Acc>& W, int ni) {
+template <class Acc, class SS>
+__device__ __forceinline__ void walk_prefix(const SS& S, const DevState& s, WalkArea<Acc>& W, int ni) {
   const int* kl = W.kl;
   int* pref = W.pref;
   for (int k = threadIdx.x; k < ni; k += blockDim.x) {
@@ -712,7 +751,7 @@ __global__ void __launch_bounds__(256, 3) k_density(DevGrid g, DevPhys ph, DevSt
   __shared__ unsigned long long s_pairs, s_final;
   __shared__ int s_unconv, s_active;
   if (threadIdx.x == 0) { s_ni = 0; s_pairs = 0; s_final = 0; s_unconv = 0; s_active = 0; }
-  TILE_PROLOGUE();
+  DESC_PROLOGUE();
   const int O1 = SP;  // T0 = smem4[j]: x, y, z, h   T1 = smem4[O1 + j]: vx, vy, vz, m
   WalkArea<DenAcc> W = walk_area<DenAcc>(reinterpret_cast<char*>(smem4 + 2 * SP), g.icap);
   {
@@ -775,7 +814,7 @@ __global__ void __launch_bounds__(256, 3) k_density(DevGrid g, DevPhys ph, DevSt
         [&](int j) {
           const float4 p = smem4[j];
           den_pair(a, pi4.x - p.x, pi4.y - p.y, pi4.z - p.z, hinv, qband, vi4, smem4[O1 + j], [&]() {
-            return exact_neighbour(s.xh, gi, slot_global(S, T.nct, j), H2, g.dscale[0], g.dscale[1], g.dscale[2]);
+            return exact_neighbour(s.xh, gi, slot_global(S, nseg, j), H2, g.dscale[0], g.dscale[1], g.dscale[2]);
           });
         },
         [&]() { return a; });
@@ -824,7 +863,7 @@ __global__ void __launch_bounds__(256, 3) k_gradient(DevGrid g, DevPhys ph, DevS
                                                        DevCounters* __restrict__ ctr) {
   __shared__ unsigned long long s_pairs;
   if (threadIdx.x == 0) s_pairs = 0;
-  TILE_PROLOGUE();
+  DESC_PROLOGUE();
   // T0 = smem4[j]: x, y, z, h   T1 = smem4[O1 + j]: vx, vy, vz, m   T2 = smem4[O2 + j]: c, u, m/rho, rho
   const int O1 = SP, O2 = 2 * SP;
   WalkArea<GradAcc> W = walk_area<GradAcc>(reinterpret_cast<char*>(smem4 + 3 * SP), g.icap);
@@ -877,7 +916,7 @@ __global__ void __launch_bounds__(256, 3) k_gradient(DevGrid g, DevPhys ph, DevS
           const float4 p = smem4[j];
           grad_pair(a, pi4.x - p.x, pi4.y - p.y, pi4.z - p.z, hinv, qband, vi4, ci, ui, ph.beta, smem4[O1 + j],
                     smem4[O2 + j], [&]() {
-                      return exact_neighbour(s.xh, gi, slot_global(S, T.nct, j), H2, g.dscale[0], g.dscale[1],
+                      return exact_neighbour(s.xh, gi, slot_global(S, nseg, j), H2, g.dscale[0], g.dscale[1],
                                              g.dscale[2]);
                     });
         },
@@ -923,7 +962,7 @@ __global__ void __launch_bounds__(512, 1) k_force(DevGrid g, DevPhys ph, DevStat
   __shared__ int s_bad;
   __shared__ unsigned int s_hinv_max;  // largest 1/h of the tile (f32 bits)
   if (threadIdx.x == 0) { s_pairs = 0; s_dt = 0x7f800000u; s_bad = 0; s_hinv_max = 0u; }
-  TILE_PROLOGUE();
+  DESC_PROLOGUE();
   // T0 = [j]: x, y, z, 1/h   T1 = [O1+j]: vx, vy, vz, m   T2 = [O2+j]: A, Kf, c, rho
   // T3 = [O3+j]: B, P alpha_c, u, alpha_v  (P = A rho^2: four 16-byte records per pair)
   const int O1 = SP, O2 = 2 * SP, O3 = 3 * SP;
@@ -996,7 +1035,7 @@ __global__ void __launch_bounds__(512, 1) k_force(DevGrid g, DevPhys ph, DevStat
           float vs;
           int in;
           force_pair(a, pi4.x - p.x, pi4.y - p.y, pi4.z - p.z, I, J, ph.beta, band, [&]() {
-            const int gj = slot_global(S, T.nct, j);
+            const int gj = slot_global(S, nseg, j);
             const double H2 = fmax(h2_exact(__uint_as_float(s.xh[gi].w), ph.gamma_k),
                                    h2_exact(__uint_as_float(s.xh[gj].w), ph.gamma_k));
             return exact_neighbour(s.xh, gi, gj, H2, g.dscale[0], g.dscale[1], g.dscale[2]);
@@ -1041,6 +1080,22 @@ __global__ void __launch_bounds__(512, 1) k_force(DevGrid g, DevPhys ph, DevStat
   }
 }
 
+// One CTA per block: tile_setup, then the descriptor out (k_tile_desc, once per rebuild).
+__global__ void __launch_bounds__(64) k_tile_desc(DevGrid g, const int* __restrict__ cell_start) {
+  __shared__ BlockShared S;
+  Tile T;
+  tile_setup(g, blockIdx.x, cell_start, S, T);
+  TileDesc* D = reinterpret_cast<TileDesc*>(const_cast<void*>(g.desc)) + blockIdx.x;
+  if (threadIdx.x == 0) D->T = T;
+  if (threadIdx.x < kMaxICols) {
+    D->ib[threadIdx.x] = S.ib[threadIdx.x];
+    D->g0[threadIdx.x] = S.g0[threadIdx.x];
+    D->tc[threadIdx.x] = S.tc[threadIdx.x];
+  }
+  if (threadIdx.x <= kMaxICols) D->pre[threadIdx.x] = S.pre[threadIdx.x];
+  if (threadIdx.x < kMaxSeg) D->seg[threadIdx.x] = S.seg[threadIdx.x];
+}
+
 // per-block tile size and i count (max over blocks) -> sizes shared memory of the loops
 __global__ void k_tile_sizes(DevGrid g, const int* __restrict__ cell_start, int* max_tile, int* max_i) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1071,6 +1126,12 @@ __global__ void k_tile_sizes(DevGrid g, const int* __restrict__ cell_start, int*
 }  // namespace
 
 int kernel_threads() { return kNW * 32; }
+size_t tile_desc_bytes() { return sizeof(TileDesc); }
+
+cudaError_t launch_tile_desc(const DevGrid& g, const int* cell_start, cudaStream_t st) {
+  k_tile_desc<<<g.nblocks, 64, 0, st>>>(g, cell_start);
+  return cudaGetLastError();
+}
 
 size_t lists_smem(const DevGrid& g) {
   return (size_t)((g.tcap + kNSent + 1) & ~1) * 16 + (size_t)kNW * kListRows * 32 * 2;

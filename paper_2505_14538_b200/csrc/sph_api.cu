@@ -957,6 +957,7 @@ sph_status rebuild_impl(sph_ctx* c) {
   // per-block tile descriptors for the loop kernels (k_tile_desc)
   if ((st = grow(c, &c->desc_buf, c->desc_cap, (size_t)g.nblocks * tile_desc_bytes())) != SPH_OK) return st;
   g.desc = c->desc_buf;
+  g.desc_cells = c->desc_buf + (size_t)g.nblocks * tile_desc_header_bytes();
   CK(launch_tile_desc(g, c->cell_start, c->stream));
   c->launches++;
   const size_t blk_old = c->blk_cap;

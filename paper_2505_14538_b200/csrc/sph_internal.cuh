@@ -34,6 +34,7 @@ struct DevGrid {
   float skin;         // list radius = (1 + skin) max(H_i, H_j)
   int force_threads;  // block size of the force kernel: 256, or 512 when one CTA fills an SM
   const void* desc;   // [nblocks] tile descriptors (sph_kernels.cu TileDesc, k_tile_desc)
+  const void* desc_cells;  // [nblocks][kMaxTileCells + 1] per tile cell (tile offset, global start)
   float scale[3];     // L_a / 2^32 as f32 (fixed point -> length)
   double dscale[3];   // L_a * 2^-32 exact (fp64 exact neighbour test)
   float side[3];      // cell side per axis
@@ -140,7 +141,8 @@ cudaError_t launch_wide_gradient(const DevGrid& g, const DevPhys& ph, const DevS
 cudaError_t launch_wide_force(const DevGrid& g, const DevPhys& ph, const DevState& s, DevCounters* ctr,
                               cudaStream_t st);
 int kernel_threads();
-size_t tile_desc_bytes();
+size_t tile_desc_bytes();  // descriptor + per-cell table, per block
+size_t tile_desc_header_bytes();  // the descriptor alone
 cudaError_t launch_tile_desc(const DevGrid& g, const int* cell_start, cudaStream_t st);
 
 }  // namespace sph

@@ -332,7 +332,35 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
   __shared__ int s_cg[kMaxICells];      // global start of each i cell
   __shared__ unsigned int s_hmax;       // largest h of the tile (f32 bits)
   if (threadIdx.x == 0) s_hmax = 0u;
-  TILE_PROLOGUE();
+  // the block's tile from its descriptor (k_tile_desc) instead of tile_setup
+  __shared__ BlockShared S;
+  __shared__ Tile Tsh;
+  {
+    const TileDesc* D = reinterpret_cast<const TileDesc*>(g.desc) + blockIdx.x;
+    if (threadIdx.x == 0) Tsh = D->T;
+    if (threadIdx.x < kMaxICols) {
+      S.ib[threadIdx.x] = D->ib[threadIdx.x];
+      S.g0[threadIdx.x] = D->g0[threadIdx.x];
+      S.tc[threadIdx.x] = D->tc[threadIdx.x];
+    }
+    if (threadIdx.x <= kMaxICols) S.pre[threadIdx.x] = D->pre[threadIdx.x];
+    for (int q = threadIdx.x; q < kMaxSeg; q += blockDim.x) S.seg[q] = D->seg[q];
+    const int nct = D->T.nct;
+    const int2* C = reinterpret_cast<const int2*>(g.desc_cells) + (size_t)blockIdx.x * (kMaxTileCells + 1);
+    for (int c = threadIdx.x; c <= nct; c += blockDim.x) {
+      const int2 v = __ldg(C + c);
+      S.off[c] = v.x;
+      if (c < nct) S.gst[c] = v.y;
+    }
+  }
+  __syncthreads();
+  const Tile T = Tsh;
+  if (T.ntile > g.tcap) {
+    if (threadIdx.x == 0) atomicExch(&ctr->nonfinite, 2);
+    return;
+  }
+  const int nseg = 3 * T.ntc;
+  const int SP = g.tcap + kNSent;
   {
     const float4* src[1] = {reinterpret_cast<const float4*>(s.xh)};
     const int o16[1] = {0};
@@ -1094,6 +1122,9 @@ __global__ void __launch_bounds__(64) k_tile_desc(DevGrid g, const int* __restri
   }
   if (threadIdx.x <= kMaxICols) D->pre[threadIdx.x] = S.pre[threadIdx.x];
   if (threadIdx.x < kMaxSeg) D->seg[threadIdx.x] = S.seg[threadIdx.x];
+  // per tile cell (tile offset, global start) for k_lists' window searches
+  int2* C = reinterpret_cast<int2*>(const_cast<void*>(g.desc_cells)) + (size_t)blockIdx.x * (kMaxTileCells + 1);
+  for (int c = threadIdx.x; c <= T.nct; c += blockDim.x) C[c] = make_int2(S.off[c], c < T.nct ? S.gst[c] : 0);
 }
 
 // per-block tile size and i count (max over blocks) -> sizes shared memory of the loops
@@ -1126,7 +1157,8 @@ __global__ void k_tile_sizes(DevGrid g, const int* __restrict__ cell_start, int*
 }  // namespace
 
 int kernel_threads() { return kNW * 32; }
-size_t tile_desc_bytes() { return sizeof(TileDesc); }
+size_t tile_desc_bytes() { return sizeof(TileDesc) + (size_t)(kMaxTileCells + 1) * sizeof(int2); }
+size_t tile_desc_header_bytes() { return sizeof(TileDesc); }
 
 cudaError_t launch_tile_desc(const DevGrid& g, const int* cell_start, cudaStream_t st) {
   k_tile_desc<<<g.nblocks, 64, 0, st>>>(g, cell_start);

@@ -288,6 +288,8 @@ struct sph_ctx {
   uint8_t* blk[2] = {nullptr, nullptr};
   char* desc_buf = nullptr;   // tile descriptors, nblocks x tile_desc_bytes()
   size_t desc_cap = 0;
+  int* pref_buf = nullptr;    // per-block list-group prefixes (k_lists)
+  size_t pref_cap = 0;
   size_t blk_cap = 0;
   DevCounters* ctr = nullptr;     // device
   DevCounters* ctr_h = nullptr;   // pinned host mirror
@@ -958,6 +960,8 @@ sph_status rebuild_impl(sph_ctx* c) {
   if ((st = grow(c, &c->desc_buf, c->desc_cap, (size_t)g.nblocks * tile_desc_bytes())) != SPH_OK) return st;
   g.desc = c->desc_buf;
   g.desc_cells = c->desc_buf + (size_t)g.nblocks * tile_desc_header_bytes();
+  if ((st = grow(c, &c->pref_buf, c->pref_cap, (size_t)g.nblocks * (g.icap + 1))) != SPH_OK) return st;
+  g.desc_pref = c->pref_buf;
   CK(launch_tile_desc(g, c->cell_start, c->stream));
   c->launches++;
   const size_t blk_old = c->blk_cap;
@@ -1506,7 +1510,7 @@ sph_status sph_destroy(sph_ctx* c) {
                   s.ncount, s.hbuild, c->cell_start, c->keys, c->keys_alt, c->perm, c->perm_alt, c->sort_tmp,
                   c->blk[0], c->blk[1], c->ctr, c->scratch, c->out_tmp, c->mig_send, c->mig_recv, c->pc_send,
                   c->pc_recv, c->pc_scan, c->scan_tmp, c->cnt_dev, c->wide_flag, c->widx, c->wcount,
-                  c->n_wide_dev, c->wnbr, c->sel_tmp, c->desc_buf};
+                  c->n_wide_dev, c->wnbr, c->sel_tmp, c->desc_buf, c->pref_buf};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->ctr_h) cudaFreeHost(c->ctr_h);

@@ -35,6 +35,7 @@ struct DevGrid {
   int force_threads;  // block size of the force kernel: 256, or 512 when one CTA fills an SM
   const void* desc;   // [nblocks] tile descriptors (sph_kernels.cu TileDesc, k_tile_desc)
   const void* desc_cells;  // [nblocks][kMaxTileCells + 1] per tile cell (tile offset, global start)
+  int* desc_pref;     // [nblocks][icap + 1] list-group prefix of the block's particles (k_lists)
   float scale[3];     // L_a / 2^32 as f32 (fixed point -> length)
   double dscale[3];   // L_a * 2^-32 exact (fp64 exact neighbour test)
   float side[3];      // cell side per axis

@@ -307,6 +307,7 @@ __device__ __forceinline__ int warp_max(int v) {
 // z_2p+1, H2_2p, H2_2p+1), so one lane tests two consecutive candidates with two LDS.128
 // and packed f32x2 arithmetic (FADD2 / FMUL2 / FFMA2).  Hits go to a per-lane column of a
 // per-warp buffer in shared memory and leave for global memory 8 at a time (16-byte stores).
+__device__ void block_exclusive_scan(int* a, int n);
 constexpr int kMaxICells = kMaxICols * (kMaxTileCellsZ - 2);
 constexpr int kListRows = 32;  // ring rows per lane (<= 7 left + 2 single tests + 16 per group)
 constexpr int kCellRows = 16;  // k_bank grid rows per list (longer lists keep the natural order)
@@ -422,6 +423,7 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
   // kListRows x 32-lane uint16 ring per warp after the pair array (row stride 64 bytes):
   // entries leave 8 at a time from 512-byte aligned ring positions, nothing is moved
   const uint32_t buf = sP + (uint32_t)NP * 32u + (uint32_t)(warp * kListRows * 32 + lane) * 2u;
+  int* grp = reinterpret_cast<int*>(reinterpret_cast<char*>(P) + (size_t)NP * 32 + (size_t)kNW * kListRows * 32 * 2);
   constexpr uint32_t kRing = kListRows * 64u;
   const int ni = s_cp[nicell];
   int over = 0;
@@ -449,6 +451,7 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
       s.ncount[gi] = 0;
       valid = false;
     }
+    int mygrp = 0;             // list groups of this lane's particle (0: none / wide)
     uint32_t w = 0u, rd = 0u;  // ring byte offsets: next write, next flush
     int flushed = 0;           // entries already in global memory
     auto hit = [&](bool h, int t) {
@@ -530,11 +533,19 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
       drain();
       if (cntp > g.lcap) over = max(over, cntp);
       s.ncount[gi] = min(cntp, g.lcap);
+      mygrp = min(cntp, g.lcap) >> 3;
       s.hbuild[gi] = sqrtf(Hi2) / Hfac;
     }
+    if (k < ni) grp[k] = mygrp;
   }
   over = warp_max(over);
   if (lane == 0 && over) atomicMax(&ctr->list_overflow, over);
+  // the block's list-group prefix, in the loops' block-local particle order (column-major,
+  // as here), for the loop kernels' walks (walk_prefix_pre)
+  __syncthreads();
+  block_exclusive_scan(grp, ni);
+  int* out = g.desc_pref + (size_t)blockIdx.x * (g.icap + 1);
+  for (int k = threadIdx.x; k <= ni; k += blockDim.x) out[k] = grp[k];
 }
 
 // k_bank: the bank-aware row layout ("Bank-aware rows" above) of every list of at most
@@ -747,6 +758,15 @@ __device__ __forceinline__ WalkArea<Acc> walk_area(char* base, int icap) {
 
 // Fill pref[] with the list groups of the walk's particles (kl[0..ni)), scan it, and clear
 // the accumulators.
+// The same for a walk over all the block's particles (kl[k] = k): the prefix k_lists stored.
+template <class Acc>
+__device__ __forceinline__ void walk_prefix_pre(const DevGrid& g, WalkArea<Acc>& W, int ni) {
+  const int* src = g.desc_pref + (size_t)blockIdx.x * (g.icap + 1);
+  for (int k = threadIdx.x; k <= ni; k += blockDim.x) W.pref[k] = __ldg(src + k);
+  for (int k = threadIdx.x; k < ni; k += blockDim.x) W.fin[k] = Acc::zero();
+  __syncthreads();
+}
+
 template <class Acc, class SS>
 __device__ __forceinline__ void walk_prefix(const SS& S, const DevState& s, WalkArea<Acc>& W, int ni) {
   const int* kl = W.kl;
@@ -815,7 +835,8 @@ __global__ void __launch_bounds__(256, 3) k_density(DevGrid g, DevPhys ph, DevSt
   }
   __syncthreads();
   const int ni = s_ni;
-  walk_prefix(S, s, W, ni);
+  if (pass == 0) walk_prefix_pre(g, W, ni);
+  else walk_prefix(S, s, W, ni);
   {
     float4 pi4, vi4;
     float hinv = 0.f, qband = 0.f;
@@ -912,8 +933,7 @@ __global__ void __launch_bounds__(256, 3) k_gradient(DevGrid g, DevPhys ph, DevS
   }
   const int ni = T.ni;
   for (int k = threadIdx.x; k < ni; k += blockDim.x) W.kl[k] = k;
-  __syncthreads();
-  walk_prefix(S, s, W, ni);
+  walk_prefix_pre(g, W, ni);
   {
     float4 pi4, vi4;
     float hinv = 0.f, qband = 0.f, ci = 0.f, ui = 0.f;
@@ -1021,8 +1041,7 @@ __global__ void __launch_bounds__(512, 1) k_force(DevGrid g, DevPhys ph, DevStat
   }
   const int ni = T.ni;
   for (int k = threadIdx.x; k < ni; k += blockDim.x) W.kl[k] = k;
-  __syncthreads();
-  walk_prefix(S, s, W, ni);
+  walk_prefix_pre(g, W, ni);
   {
     const float4* __restrict__ T0 = smem4;
     const float4* __restrict__ T1 = smem4 + O1;
@@ -1166,7 +1185,7 @@ cudaError_t launch_tile_desc(const DevGrid& g, const int* cell_start, cudaStream
 }
 
 size_t lists_smem(const DevGrid& g) {
-  return (size_t)((g.tcap + kNSent + 1) & ~1) * 16 + (size_t)kNW * kListRows * 32 * 2;
+  return (size_t)((g.tcap + kNSent + 1) & ~1) * 16 + (size_t)kNW * kListRows * 32 * 2 + (size_t)(g.icap + 1) * 4;
 }
 size_t density_smem(const DevGrid& g) { return (size_t)(g.tcap + kNSent) * (2 * 16) + walk_bytes<DenAcc>(g.icap); }
 size_t gradient_smem(const DevGrid& g) { return (size_t)(g.tcap + kNSent) * (3 * 16) + walk_bytes<GradAcc>(g.icap); }

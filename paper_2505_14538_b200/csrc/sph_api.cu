@@ -929,9 +929,11 @@ sph_status rebuild_impl(sph_ctx* c) {
     g.icap = std::max(32, (int)tmax[1]);
     g.lcap = c->lcap;
     g.skin = c->cfg.cell_skin;
-    const bool fits = force_smem(g) <= kSmemMax && lists_smem(g) <= kSmemMax && g.tcap < 65520;
     // force: 256 threads when two CTAs fit an SM, else one CTA of 512
-    g.force_threads = force_smem(g) <= kSmemTarget ? 256 : 512;
+    g.force_threads = 256;
+    if (force_smem(g) > kSmemTarget) g.force_threads = 512;
+    const bool fits = force_smem(g) <= kSmemMax && lists_smem(g) <= kSmemMax && density_smem(g) <= kSmemMax &&
+                      gradient_smem(g) <= kSmemMax && g.tcap < 65520;
     if (fits && (force_smem(g) <= kSmemTarget || KZ == 1)) break;
     if (fits && c->cfg.tile_cells_z > 0) break;
     if (KZ == 1) {

@@ -677,7 +677,7 @@ __device__ void block_exclusive_scan(int* a, int n) {
 // (i state, accumulators); pair(j) accumulates one entry; take() returns the accumulators.
 // fin[] must hold Acc::zero() for every particle.
 template <class Acc, class ListOf, class Begin, class Pair, class Take>
-__device__ __forceinline__ void walk_lists(int ni, const int* __restrict__ pref, Acc* fin, int /*sentinel*/,
+__device__ __forceinline__ void walk_lists(int ni, const int* __restrict__ pref, Acc* fin, Acc* head, Acc* tail,
                                            ListOf&& list_of, Begin&& begin, Pair&& pair, Take&& take) {
   const int G = pref[ni];
   if (G == 0) return;
@@ -694,8 +694,13 @@ __device__ __forceinline__ void walk_lists(int ni, const int* __restrict__ pref,
   int p0 = pref[k], p1 = pref[k + 1];
   const uint4* list = reinterpret_cast<const uint4*>(list_of(k)) + (g0 - p0);
   begin(k);
+  // a particle whose rows lie in this thread's range is stored whole; a split one goes to
+  // this thread's head record (the particle its range starts in) or tail record (the one it
+  // ends in), summed by the epilogue (gather_acc) in thread order -- no atomics
   auto finish = [&]() {
-    if (g0 <= p0 && p1 <= g1) fin[k] = take(); else take().merge_into(&fin[k]);
+    if (g0 <= p0 && p1 <= g1) fin[k] = take();
+    else if (k == lo) head[threadIdx.x] = take();
+    else tail[threadIdx.x] = take();
   };
   for (int gg = g0; gg < g1; ++gg, ++list) {
     if (gg == p1) {
@@ -738,12 +743,14 @@ template <class Acc>
 struct WalkArea {
   int* pref;  // [icap + 1]
   int* kl;    // [icap]  walk index -> block-local i index
-  Acc* fin;   // [icap]
+  Acc* fin;   // [icap]  whole particles
+  Acc* head;  // [threads] split particle a thread's range starts in
+  Acc* tail;  // [threads] split particle a thread's range ends in
 };
 template <class Acc>
-__host__ __device__ __forceinline__ size_t walk_bytes(int icap) {
+__host__ __device__ __forceinline__ size_t walk_bytes(int icap, int threads = kNW * 32) {
   return (((size_t)(icap + 1) * 4 + 15) & ~(size_t)15) + (((size_t)icap * 4 + 15) & ~(size_t)15) +
-         (size_t)icap * sizeof(Acc);
+         (((size_t)icap * sizeof(Acc) + 15) & ~(size_t)15) + (size_t)2 * threads * sizeof(Acc);
 }
 template <class Acc>
 __device__ __forceinline__ WalkArea<Acc> walk_area(char* base, int icap) {
@@ -753,7 +760,29 @@ __device__ __forceinline__ WalkArea<Acc> walk_area(char* base, int icap) {
   w.kl = reinterpret_cast<int*>(base);
   base += ((size_t)icap * 4 + 15) & ~(size_t)15;
   w.fin = reinterpret_cast<Acc*>(base);
+  base += ((size_t)icap * sizeof(Acc) + 15) & ~(size_t)15;
+  w.head = reinterpret_cast<Acc*>(base);
+  w.tail = w.head + blockDim.x;
   return w;
+}
+
+// Accumulators of walk particle k: its whole record, or the sum, in thread order, of the
+// head / tail records of the threads its rows were split over (walk_lists).
+template <class Acc>
+__device__ __forceinline__ Acc gather_acc(const WalkArea<Acc>& W, int ni, int k) {
+  const long long G = W.pref[ni];
+  const int a = W.pref[k], b = W.pref[k + 1];
+  if (b <= a) return Acc::zero();
+  const long long nt = blockDim.x;
+  const int ta = (int)((nt * (a + 1) - 1) / G), tb = (int)((nt * b - 1) / G);
+  if (ta == tb) return W.fin[k];
+  Acc s = Acc::zero();
+  for (int t2 = ta; t2 <= tb; ++t2) {
+    const int s0 = (int)(((long long)t2 * G) / nt), s1 = (int)(((long long)(t2 + 1) * G) / nt);
+    if (s0 >= s1) continue;  // (a thread without rows)
+    s.add(s0 >= a ? W.head[t2] : W.tail[t2]);
+  }
+  return s;
 }
 
 // Fill pref[] with the list groups of the walk's particles (kl[0..ni)), scan it, and clear
@@ -844,7 +873,7 @@ __global__ void __launch_bounds__(256, 3) k_density(DevGrid g, DevPhys ph, DevSt
     int gi = 0;
     DenAcc a;
     walk_lists(
-        ni, W.pref, W.fin, g.tcap,
+        ni, W.pref, W.fin, W.head, W.tail,
         [&](int k) {
           int ti, gk;
           i_slot(S, W.kl[k], ti, gk);
@@ -871,7 +900,7 @@ __global__ void __launch_bounds__(256, 3) k_density(DevGrid g, DevPhys ph, DevSt
   __syncthreads();
   unsigned long long npairs = 0, nfinal = 0;
   for (int k = threadIdx.x; k < ni; k += blockDim.x) {
-    const DenAcc a = W.fin[k];
+    const DenAcc a = gather_acc(W, ni, k);
     int ti, gi;
     i_slot(S, W.kl[k], ti, gi);
     if (s.wide && s.wide[gi]) continue;  // wide particles: k_wide_density
@@ -941,7 +970,7 @@ __global__ void __launch_bounds__(256, 3) k_gradient(DevGrid g, DevPhys ph, DevS
     int gi = 0;
     GradAcc a;
     walk_lists(
-        ni, W.pref, W.fin, g.tcap,
+        ni, W.pref, W.fin, W.head, W.tail,
         [&](int k) {
           int ti, gk;
           i_slot(S, W.kl[k], ti, gk);
@@ -973,7 +1002,7 @@ __global__ void __launch_bounds__(256, 3) k_gradient(DevGrid g, DevPhys ph, DevS
   __syncthreads();
   unsigned long long npairs = 0;
   for (int k = threadIdx.x; k < ni; k += blockDim.x) {
-    const GradAcc a = W.fin[k];
+    const GradAcc a = gather_acc(W, ni, k);
     int ti, gi;
     i_slot(S, k, ti, gi);
     if (s.wide && s.wide[gi]) continue;  // wide particles: k_wide_gradient
@@ -1054,7 +1083,7 @@ __global__ void __launch_bounds__(512, 1) k_force(DevGrid g, DevPhys ph, DevStat
     int gi = 0;
     ForceAcc a;
     walk_lists(
-        ni, W.pref, W.fin, g.tcap,
+        ni, W.pref, W.fin, W.head, W.tail,
         [&](int k) {
           int ti, gk;
           i_slot(S, W.kl[k], ti, gk);
@@ -1094,7 +1123,7 @@ __global__ void __launch_bounds__(512, 1) k_force(DevGrid g, DevPhys ph, DevStat
   unsigned long long npairs = 0;
   float dtmin = CUDART_INF_F;
   for (int k = threadIdx.x; k < ni; k += blockDim.x) {
-    const ForceAcc a = W.fin[k];
+    const ForceAcc a = gather_acc(W, ni, k);
     int ti, gi;
     i_slot(S, k, ti, gi);
     if (s.wide && s.wide[gi]) continue;  // wide particles: k_wide_force
@@ -1189,7 +1218,9 @@ size_t lists_smem(const DevGrid& g) {
 }
 size_t density_smem(const DevGrid& g) { return (size_t)(g.tcap + kNSent) * (2 * 16) + walk_bytes<DenAcc>(g.icap); }
 size_t gradient_smem(const DevGrid& g) { return (size_t)(g.tcap + kNSent) * (3 * 16) + walk_bytes<GradAcc>(g.icap); }
-size_t force_smem(const DevGrid& g) { return force_records_bytes(g.tcap) + walk_bytes<ForceAcc>(g.icap); }
+size_t force_smem(const DevGrid& g) {
+  return force_records_bytes(g.tcap) + walk_bytes<ForceAcc>(g.icap, g.force_threads > 0 ? g.force_threads : kNW * 32);
+}
 
 cudaError_t launch_tile_sizes(const DevGrid& g, const int* cell_start, int* max_tile, int* max_i, cudaStream_t st) {
   k_tile_sizes<<<(g.nblocks + 255) / 256, 256, 0, st>>>(g, cell_start, max_tile, max_i);

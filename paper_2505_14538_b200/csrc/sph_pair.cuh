@@ -54,10 +54,8 @@ struct DenAcc {
   float S0, S1, R0, R1, Dv, Cx, Cy, Cz;
   int nn;
   __device__ static DenAcc zero() { return DenAcc{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0}; }
-  __device__ void merge_into(DenAcc* d) const {
-    atomicAdd(&d->S0, S0); atomicAdd(&d->S1, S1); atomicAdd(&d->R0, R0); atomicAdd(&d->R1, R1);
-    atomicAdd(&d->Dv, Dv); atomicAdd(&d->Cx, Cx); atomicAdd(&d->Cy, Cy); atomicAdd(&d->Cz, Cz);
-    atomicAdd(&d->nn, nn);
+  __device__ void add(const DenAcc& o) {
+    S0 += o.S0; S1 += o.S1; R0 += o.R0; R1 += o.R1; Dv += o.Dv; Cx += o.Cx; Cy += o.Cy; Cz += o.Cz; nn += o.nn;
   }
 };
 
@@ -166,11 +164,7 @@ struct GradAcc {
   float vmax, lap;  // vmax > 0: max over its f32 bits as int
   int nn;
   __device__ static GradAcc zero() { return GradAcc{0.f, 0.f, 0}; }
-  __device__ void merge_into(GradAcc* d) const {
-    atomicMax(reinterpret_cast<int*>(&d->vmax), __float_as_int(vmax));
-    atomicAdd(&d->lap, lap);
-    atomicAdd(&d->nn, nn);
-  }
+  __device__ void add(const GradAcc& o) { vmax = fmaxf(vmax, o.vmax); lap += o.lap; nn += o.nn; }
 };
 
 // vj = (v_j, m_j), gj = (c_j, u_j, m_j/rho_j, rho_j)
@@ -242,10 +236,8 @@ struct ForceAcc {
   float ax, ay, az, du, vmax;  // vmax > 0: max over its f32 bits as int
   int nn;
   __device__ static ForceAcc zero() { return ForceAcc{0.f, 0.f, 0.f, 0.f, 0.f, 0}; }
-  __device__ void merge_into(ForceAcc* d) const {
-    atomicAdd(&d->ax, ax); atomicAdd(&d->ay, ay); atomicAdd(&d->az, az); atomicAdd(&d->du, du);
-    atomicMax(reinterpret_cast<int*>(&d->vmax), __float_as_int(vmax));
-    atomicAdd(&d->nn, nn);
+  __device__ void add(const ForceAcc& o) {
+    ax += o.ax; ay += o.ay; az += o.az; du += o.du; vmax = fmaxf(vmax, o.vmax); nn += o.nn;
   }
 };
 

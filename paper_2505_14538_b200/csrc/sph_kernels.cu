@@ -31,6 +31,7 @@
 // exactly zero (compact support, w'(0) = 0); membership (neighbour counts, v_sig) is decided
 // in f32 with a rigorous band and re-decided in fp64 inside it, so counts equal the
 // definition exactly.
+#include <algorithm>
 #include <cuda_runtime.h>
 #include <math_constants.h>
 #include <stdint.h>
@@ -311,6 +312,7 @@ __device__ void block_exclusive_scan(int* a, int n);
 constexpr int kMaxICells = kMaxICols * (kMaxTileCellsZ - 2);
 constexpr int kListRows = 32;  // ring rows per lane (<= 7 left + 2 single tests + 16 per group)
 constexpr int kCellRows = 16;  // k_bank grid rows per list (longer lists keep the natural order)
+constexpr int kZSub = 16;      // z sub-buckets per cell in k_lists' window table
 // (the per-lane list buffers are touched only through these volatile asm statements, which
 // keep their order; no memory clobber, so the compiler may move tile loads across them)
 __device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
@@ -332,6 +334,9 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
   __shared__ int s_ct[kMaxICells];      // tile start of each i cell
   __shared__ int s_cg[kMaxICells];      // global start of each i cell
   __shared__ unsigned int s_hmax;       // largest h of the tile (f32 bits)
+  // z window table: s_zw[16 c + k] = first slot of tile cell c in z sub-bucket >= k (16 per
+  // cell, the top 4 z bits inside the cell -- the sort key's, so exact), s_zw[16 nct] = end
+  __shared__ unsigned short s_zw[kMaxTileCells * kZSub + 1];
   if (threadIdx.x == 0) s_hmax = 0u;
   // the block's tile from its descriptor (k_tile_desc) instead of tile_setup
   __shared__ BlockShared S;
@@ -371,6 +376,10 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
   float* P = reinterpret_cast<float*>(smem4);
   const float Hfac = (1.f + g.skin) * ph.gamma_k;
   unsigned int hm = 0u;
+  // each slot's z sub-bucket (bytes; the region of the list ring, not yet in use)
+  unsigned char* zsb = reinterpret_cast<unsigned char*>(P) + (size_t)NP * 32;
+  const int zb4 = min(g.zbits, 4);
+  const uint32_t zmask = (1u << (4 - zb4)) - 1u;  // (coarse sort keys: fewer sub-buckets)
   for (int pp = threadIdx.x; pp < NP; pp += blockDim.x) {
     float4 q[2];
 #pragma unroll
@@ -383,6 +392,7 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
         const float Hs = Hfac * __uint_as_float(x.w);
         hm = max(hm, x.w);
         q[u] = make_float4(r.x, r.y, r.z, Hs * Hs);
+        zsb[t] = (unsigned char)((((uint32_t)((unsigned long long)x.z * (unsigned)g.nz)) >> 28) & ~zmask);
       }
     }
     // (the raw records of this pair are read before the pair's 32 bytes are rewritten)
@@ -391,6 +401,23 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
   }
   hm = warp_max((int)hm);
   if ((threadIdx.x & 31) == 0) atomicMax(&s_hmax, hm);
+  __syncthreads();
+  {  // the z window table, one warp per tile cell
+    const int lane = threadIdx.x & 31;
+    for (int c = threadIdx.x >> 5; c < T.nct; c += kNW) {
+      const int s0 = S.off[c], s1 = S.off[c + 1];
+      unsigned short* row = s_zw + c * kZSub;
+      if (s0 == s1 && lane < kZSub) row[lane] = (unsigned short)s0;
+      for (int u = s0 + lane; u < s1; u += 32) {
+        const int b = zsb[u];
+        const int bp = u > s0 ? (int)zsb[u - 1] : -1;
+        for (int k = bp + 1; k <= b; ++k) row[k] = (unsigned short)u;
+        if (u == s1 - 1)
+          for (int k = b + 1; k < kZSub; ++k) row[k] = (unsigned short)s1;
+      }
+    }
+    if (threadIdx.x == 0) s_zw[T.nct * kZSub] = (unsigned short)S.off[T.nct];
+  }
   int ncolI = 0;
 #pragma unroll
   for (int r = 0; r < kMaxICols; ++r) ncolI += (r == 0 || S.tc[r] != 0) ? 1 : 0;
@@ -414,7 +441,7 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
   const float zpad = Hfac * __uint_as_float(s_hmax) + g.zbucket + g.eabs;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t sP = (uint32_t)__cvta_generic_to_shared(P);
-  const float inv_side = 1.f / g.side[2];
+  const float sub_scale = (float)kZSub / g.side[2];
   auto zbound = [&](int cz) {  // tile-relative z of the lower boundary of grid cell cz (may wrap)
     const int c = cz < 0 ? cz + g.nz : cz;
     const uint32_t b = (uint32_t)((((unsigned long long)c) << 32) / (unsigned long long)g.nz);
@@ -481,28 +508,20 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
         flushed += 8;
       }
     };
-    auto zat = [&](int t) { return P[(t >> 1) * 8 + 4 + (t & 1)]; };
-    // slot guess for height u above the bottom of tile cell c0 (3 cells c0 .. c0 + 2)
-    auto guess = [&](int c0, float u, int lo, int hi) {
-      const float f = fminf(fmaxf(u * inv_side, 0.f), 2.999f);
-      const int k = (int)f;
-      const int s0 = S.off[c0 + k], s1 = S.off[c0 + k + 1];
-      return min(max(s0 + (int)((f - (float)k) * (float)(s1 - s0)), lo), hi);
-    };
+    // window ends in sub-buckets above the bottom of the column's first window cell (a
+    // margin of 1/100 sub-bucket covers the rounding of the tile coordinates)
+    const float ulo = (zi - zpad - zc) * sub_scale - 0.01f, uhi = (zi + zpad - zc) * sub_scale + 0.01f;
+    const int klo = (int)(min(max(floorf(ulo), 0.f), (float)(3 * kZSub))) & ~(int)zmask;
+    const int khi = (((int)(min(max(ceilf(uhi), 0.f), (float)(3 * kZSub))) - 1) | (int)zmask) + 1;
     if (valid) {
 #pragma unroll 1
       for (int d = 0; d < 9; ++d) {
         const int tcol = tc + (d / 3 - 1) * (g.by + 2) + (d % 3 - 1);
         const int cb = tcol * T.nzt + zz;
-        const int a0 = S.off[cb - 1], e0 = S.off[cb + 2];
-        // first slot with z >= zi - zpad and first slot with z > zi + zpad: a guess from the
-        // cell boundaries (slots spread ~evenly over a cell), then a short walk
-        int a = guess(cb - 1, zi - zpad - zc, a0, e0);
-        while (a < e0 && zat(a) < zi - zpad) ++a;
-        while (a > a0 && zat(a - 1) >= zi - zpad) --a;
-        int e = guess(cb - 1, zi + zpad - zc, a, e0);
-        while (e < e0 && zat(e) <= zi + zpad) ++e;
-        while (e > a && zat(e - 1) > zi + zpad) --e;
+        // every slot of the 3 window cells with |z - zi| <= zpad lies in [a, e): the table
+        // rows are the cells' sub-bucket starts, consecutive down the tile column
+        int a = s_zw[(cb - 1) * kZSub + klo];
+        int e = s_zw[(cb - 1) * kZSub + khi];
         if (a >= e) continue;
         if (a & 1) test_one(a++);
         if ((e - a) & 1) test_one(--e);
@@ -633,8 +652,9 @@ __global__ void __launch_bounds__(256) k_bank(int i0, int n, DevGrid g, DevState
 // [t G / 256, (t+1) G / 256) in particle order, in one flat loop (every thread runs the same
 // number of iterations up to one; only the particle switch diverges).  A particle whose
 // groups lie inside one thread's range is summed by that thread alone and stored; a particle
-// split across threads gets its partial sums combined with shared-memory atomics (float
-// adds: the split particles' sums may differ in the last bit between runs).
+// split across threads leaves one partial record per thread it touches (the thread's head
+// record if the thread's range starts inside it, else its tail record), summed by the
+// epilogue in thread order (gather_acc): no atomics, and the sums are the same every run.
 constexpr int kMaxNW = 16;  // loop kernels run 256 or 512 threads (blockDim.x)
 __device__ __forceinline__ int group_start(int t, int G) { return (int)(((long long)t * G) / blockDim.x); }
 
@@ -1214,7 +1234,9 @@ cudaError_t launch_tile_desc(const DevGrid& g, const int* cell_start, cudaStream
 }
 
 size_t lists_smem(const DevGrid& g) {
-  return (size_t)((g.tcap + kNSent + 1) & ~1) * 16 + (size_t)kNW * kListRows * 32 * 2 + (size_t)(g.icap + 1) * 4;
+  // pair array, then the list rings + group counts (first holding one z sub-bucket byte per slot)
+  const size_t ring = (size_t)kNW * kListRows * 32 * 2 + (size_t)(g.icap + 1) * 4;
+  return (size_t)((g.tcap + kNSent + 1) & ~1) * 16 + std::max(ring, (size_t)g.tcap + 16);
 }
 size_t density_smem(const DevGrid& g) { return (size_t)(g.tcap + kNSent) * (2 * 16) + walk_bytes<DenAcc>(g.icap); }
 size_t gradient_smem(const DevGrid& g) { return (size_t)(g.tcap + kNSent) * (3 * 16) + walk_bytes<GradAcc>(g.icap); }

@@ -914,6 +914,7 @@ sph_status rebuild_impl(sph_ctx* c) {
   }
   if (c->cfg.tile_cells_z > 0) KZ = c->cfg.tile_cells_z;
   KZ = std::max(1, std::min(KZ, kz_max));
+  g.lists_warps = 8;  // (the largest k_lists CTA for the fit test)
   for (;;) {
     g.KZ = KZ;
     g.nzb = (g.nz + KZ - 1) / KZ;
@@ -943,6 +944,9 @@ sph_status rebuild_impl(sph_ctx* c) {
     }
     KZ = std::max(1, KZ - 1);
   }
+  // k_lists: about one warp per 32 particles of a mean block (+10 %); the warps of a larger CTA
+  // would only wait at its final barrier (the tile, not the warp count, limits CTAs per SM)
+  g.lists_warps = std::max(2, std::min(8, (int)std::ceil(1.1 * n / std::max(g.nblocks, 1) / 32.0)));
   // rounding error of a tile coordinate: offsets reach (B/2 + 1) cells from the block centre
   const float max_off = std::max(std::max((0.5f * g.bx + 1.0f) * g.side[0], (0.5f * g.by + 1.0f) * g.side[1]),
                                  (0.5f * g.KZ + 1.0f) * g.side[2]);

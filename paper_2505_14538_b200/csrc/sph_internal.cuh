@@ -33,6 +33,7 @@ struct DevGrid {
   int lcap;           // neighbour-list capacity per particle (multiple of 16)
   float skin;         // list radius = (1 + skin) max(H_i, H_j)
   int force_threads;  // block size of the force kernel: 256, or 512 when one CTA fills an SM
+  int lists_warps;    // warps per k_lists CTA: ~ the mean block particle count / 32 (a warp per 32)
   const void* desc;   // [nblocks] tile descriptors (sph_kernels.cu TileDesc, k_tile_desc)
   const void* desc_cells;  // [nblocks][kMaxTileCells + 1] per tile cell (tile offset, global start)
   int* desc_pref;     // [nblocks][icap + 1] list-group prefix of the block's particles (k_lists)

@@ -313,6 +313,16 @@ constexpr int kMaxICells = kMaxICols * (kMaxTileCellsZ - 2);
 constexpr int kListRows = 32;  // ring rows per lane (<= 7 left + 2 single tests + 16 per group)
 constexpr int kCellRows = 16;  // k_bank grid rows per list (longer lists keep the natural order)
 constexpr int kZSub = 16;      // z sub-buckets per cell in k_lists' window table
+// k_lists' dynamic shared memory after the pair array: the per-warp list rings and the group
+// counts (holding one z sub-bucket byte per slot before the walk), then the z window table
+__host__ __device__ __forceinline__ size_t lists_ring_bytes(const DevGrid& g, int nw) {
+  const size_t ring = (size_t)nw * kListRows * 32 * 2 + (size_t)(g.icap + 1) * 4;
+  const size_t zsb = (size_t)g.tcap + 16;
+  return ((ring > zsb ? ring : zsb) + 15) & ~(size_t)15;
+}
+__host__ __device__ __forceinline__ size_t lists_zw_bytes(const DevGrid& g) {
+  return ((size_t)(g.bx + 2) * (g.by + 2) * (g.KZ + 2) * kZSub + 1) * 2;
+}
 // (the per-lane list buffers are touched only through these volatile asm statements, which
 // keep their order; no memory clobber, so the compiler may move tile loads across them)
 __device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
@@ -334,10 +344,8 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
   __shared__ int s_ct[kMaxICells];      // tile start of each i cell
   __shared__ int s_cg[kMaxICells];      // global start of each i cell
   __shared__ unsigned int s_hmax;       // largest h of the tile (f32 bits)
-  // z window table: s_zw[16 c + k] = first slot of tile cell c in z sub-bucket >= k (16 per
-  // cell, the top 4 z bits inside the cell -- the sort key's, so exact), s_zw[16 nct] = end
-  __shared__ unsigned short s_zw[kMaxTileCells * kZSub + 1];
   if (threadIdx.x == 0) s_hmax = 0u;
+  const int nw = blockDim.x >> 5;  // warps (host-chosen from the mean block particle count)
   // the block's tile from its descriptor (k_tile_desc) instead of tile_setup
   __shared__ BlockShared S;
   __shared__ Tile Tsh;
@@ -374,6 +382,10 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
   }
   const int NP = (SP + 1) >> 1;  // slot pairs
   float* P = reinterpret_cast<float*>(smem4);
+  // z window table: s_zw[16 c + k] = first slot of tile cell c in z sub-bucket >= k (16 per
+  // cell, the top 4 z bits inside the cell -- the sort key's, so exact), s_zw[16 nct] = end
+  unsigned short* s_zw = reinterpret_cast<unsigned short*>(reinterpret_cast<char*>(P) + (size_t)NP * 32 +
+                                                           lists_ring_bytes(g, nw));
   const float Hfac = (1.f + g.skin) * ph.gamma_k;
   unsigned int hm = 0u;
   // each slot's z sub-bucket (bytes; the region of the list ring, not yet in use)
@@ -404,7 +416,7 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
   __syncthreads();
   {  // the z window table, one warp per tile cell
     const int lane = threadIdx.x & 31;
-    for (int c = threadIdx.x >> 5; c < T.nct; c += kNW) {
+    for (int c = threadIdx.x >> 5; c < T.nct; c += nw) {
       const int s0 = S.off[c], s1 = S.off[c + 1];
       unsigned short* row = s_zw + c * kZSub;
       if (s0 == s1 && lane < kZSub) row[lane] = (unsigned short)s0;
@@ -450,11 +462,11 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
   // kListRows x 32-lane uint16 ring per warp after the pair array (row stride 64 bytes):
   // entries leave 8 at a time from 512-byte aligned ring positions, nothing is moved
   const uint32_t buf = sP + (uint32_t)NP * 32u + (uint32_t)(warp * kListRows * 32 + lane) * 2u;
-  int* grp = reinterpret_cast<int*>(reinterpret_cast<char*>(P) + (size_t)NP * 32 + (size_t)kNW * kListRows * 32 * 2);
+  int* grp = reinterpret_cast<int*>(reinterpret_cast<char*>(P) + (size_t)NP * 32 + (size_t)nw * kListRows * 32 * 2);
   constexpr uint32_t kRing = kListRows * 64u;
   const int ni = s_cp[nicell];
   int over = 0;
-  for (int c = warp; c * 32 < ni; c += kNW) {
+  for (int c = warp; c * 32 < ni; c += nw) {
     const int k = c * 32 + lane;
     bool valid = k < ni;
     const int kk = valid ? k : c * 32;
@@ -1234,9 +1246,8 @@ cudaError_t launch_tile_desc(const DevGrid& g, const int* cell_start, cudaStream
 }
 
 size_t lists_smem(const DevGrid& g) {
-  // pair array, then the list rings + group counts (first holding one z sub-bucket byte per slot)
-  const size_t ring = (size_t)kNW * kListRows * 32 * 2 + (size_t)(g.icap + 1) * 4;
-  return (size_t)((g.tcap + kNSent + 1) & ~1) * 16 + std::max(ring, (size_t)g.tcap + 16);
+  const int nw = g.lists_warps > 0 ? g.lists_warps : kNW;
+  return (size_t)((g.tcap + kNSent + 1) & ~1) * 16 + lists_ring_bytes(g, nw) + lists_zw_bytes(g);
 }
 size_t density_smem(const DevGrid& g) { return (size_t)(g.tcap + kNSent) * (2 * 16) + walk_bytes<DenAcc>(g.icap); }
 size_t gradient_smem(const DevGrid& g) { return (size_t)(g.tcap + kNSent) * (3 * 16) + walk_bytes<GradAcc>(g.icap); }
@@ -1258,7 +1269,7 @@ cudaError_t launch_lists(const DevGrid& g, const DevPhys& ph, const DevState& s,
   const size_t sm = lists_smem(g);
   cudaError_t e = set_smem((const void*)k_lists, sm);
   if (e != cudaSuccess) return e;
-  k_lists<<<g.nblocks, kNW * 32, sm, st>>>(g, ph, s, cell_start, ctr);
+  k_lists<<<g.nblocks, (g.lists_warps > 0 ? g.lists_warps : kNW) * 32, sm, st>>>(g, ph, s, cell_start, ctr);
   return cudaGetLastError();
 }
 

@@ -707,7 +707,6 @@ __device__ void block_exclusive_scan(int* a, int n) {
 
 // Walk this thread's groups.  list_of(k) is particle k's list; begin(k) sets up particle k
 // (i state, accumulators); pair(j) accumulates one entry; take() returns the accumulators.
-// fin[] must hold Acc::zero() for every particle.
 template <class Acc, class ListOf, class Begin, class Pair, class Take>
 __device__ __forceinline__ void walk_lists(int ni, const int* __restrict__ pref, Acc* fin, Acc* head, Acc* tail,
                                            ListOf&& list_of, Begin&& begin, Pair&& pair, Take&& take) {
@@ -826,11 +825,10 @@ __device__ __forceinline__ Acc gather_acc(const WalkArea<Acc>& W, int ni, int k)
 // the accumulators.
 // The same for a walk over all the block's particles (kl[k] = k): the prefix k_lists stored.
 template <class Acc>
+// Issued with cp.async before the tile staging, whose wait + barrier completes it.
 __device__ __forceinline__ void walk_prefix_pre(const DevGrid& g, WalkArea<Acc>& W, int ni) {
   const int* src = g.desc_pref + (size_t)blockIdx.x * (g.icap + 1);
-  for (int k = threadIdx.x; k <= ni; k += blockDim.x) W.pref[k] = __ldg(src + k);
-  for (int k = threadIdx.x; k < ni; k += blockDim.x) W.fin[k] = Acc::zero();
-  __syncthreads();
+  for (int k = threadIdx.x; k <= ni; k += blockDim.x) cp_async4(W.pref + k, src + k);
 }
 
 template <class Acc, class SS>
@@ -841,7 +839,6 @@ __device__ __forceinline__ void walk_prefix(const SS& S, const DevState& s, Walk
     int ti, gi;
     i_slot(S, kl[k], ti, gi);
     pref[k] = __ldg(s.ncount + gi) >> 3;
-    W.fin[k] = Acc::zero();
   }
   __syncthreads();
   block_exclusive_scan(pref, ni);
@@ -868,6 +865,7 @@ __global__ void __launch_bounds__(256, 3) k_density(DevGrid g, DevPhys ph, DevSt
   DESC_PROLOGUE();
   const int O1 = SP;  // T0 = smem4[j]: x, y, z, h   T1 = smem4[O1 + j]: vx, vy, vz, m
   WalkArea<DenAcc> W = walk_area<DenAcc>(reinterpret_cast<char*>(smem4 + 2 * SP), g.icap);
+  if (pass == 0) walk_prefix_pre(g, W, T.ni);
   {
     const float4* src[2] = {reinterpret_cast<const float4*>(s.xh), s.vm};
     const int o16[2] = {0, O1};
@@ -901,8 +899,7 @@ __global__ void __launch_bounds__(256, 3) k_density(DevGrid g, DevPhys ph, DevSt
   }
   __syncthreads();
   const int ni = s_ni;
-  if (pass == 0) walk_prefix_pre(g, W, ni);
-  else walk_prefix(S, s, W, ni);
+  if (pass > 0) walk_prefix(S, s, W, ni);
   {
     float4 pi4, vi4;
     float hinv = 0.f, qband = 0.f;
@@ -982,6 +979,7 @@ __global__ void __launch_bounds__(256, 3) k_gradient(DevGrid g, DevPhys ph, DevS
   // T0 = smem4[j]: x, y, z, h   T1 = smem4[O1 + j]: vx, vy, vz, m   T2 = smem4[O2 + j]: c, u, m/rho, rho
   const int O1 = SP, O2 = 2 * SP;
   WalkArea<GradAcc> W = walk_area<GradAcc>(reinterpret_cast<char*>(smem4 + 3 * SP), g.icap);
+  walk_prefix_pre(g, W, T.ni);
   {
     const float4* src[3] = {reinterpret_cast<const float4*>(s.xh), s.vm, s.gq};
     const int o16[3] = {0, O1, O2};
@@ -999,7 +997,7 @@ __global__ void __launch_bounds__(256, 3) k_gradient(DevGrid g, DevPhys ph, DevS
   }
   const int ni = T.ni;
   for (int k = threadIdx.x; k < ni; k += blockDim.x) W.kl[k] = k;
-  walk_prefix_pre(g, W, ni);
+  __syncthreads();
   {
     float4 pi4, vi4;
     float hinv = 0.f, qband = 0.f, ci = 0.f, ui = 0.f;
@@ -1082,6 +1080,7 @@ __global__ void __launch_bounds__(512, 1) k_force(DevGrid g, DevPhys ph, DevStat
   const int O1 = SP, O2 = 2 * SP, O3 = 3 * SP;
   WalkArea<ForceAcc> W =
       walk_area<ForceAcc>(reinterpret_cast<char*>(smem4) + force_records_bytes(g.tcap), g.icap);
+  walk_prefix_pre(g, W, T.ni);
   {
     const float4* src[4] = {reinterpret_cast<const float4*>(s.xh), s.vm, s.fr1, s.fr2};
     const int o16[4] = {0, O1, O2, O3};
@@ -1107,7 +1106,7 @@ __global__ void __launch_bounds__(512, 1) k_force(DevGrid g, DevPhys ph, DevStat
   }
   const int ni = T.ni;
   for (int k = threadIdx.x; k < ni; k += blockDim.x) W.kl[k] = k;
-  walk_prefix_pre(g, W, ni);
+  __syncthreads();
   {
     const float4* __restrict__ T0 = smem4;
     const float4* __restrict__ T1 = smem4 + O1;

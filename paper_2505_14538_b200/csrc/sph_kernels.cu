@@ -705,11 +705,18 @@ __device__ void block_exclusive_scan(int* a, int n) {
   __syncthreads();
 }
 
+// A pair2 of two calls of a one-entry pair (the loops without packed pair arithmetic).
+template <class P>
+__device__ __forceinline__ auto pair2_of(P p) {
+  return [=](int j0, int j1) { p(j0); p(j1); };
+}
+
 // Walk this thread's groups.  list_of(k) is particle k's list; begin(k) sets up particle k
-// (i state, accumulators); pair(j) accumulates one entry; take() returns the accumulators.
-template <class Acc, class ListOf, class Begin, class Pair, class Take>
+// (i state, accumulators); pair2(j0, j1) accumulates two entries; take() returns the
+// accumulators.
+template <class Acc, class ListOf, class Begin, class Pair2, class Take>
 __device__ __forceinline__ void walk_lists(int ni, const int* __restrict__ pref, Acc* fin, Acc* head, Acc* tail,
-                                           ListOf&& list_of, Begin&& begin, Pair&& pair, Take&& take) {
+                                           ListOf&& list_of, Begin&& begin, Pair2&& pair2, Take&& take) {
   const int G = pref[ni];
   if (G == 0) return;
   const int g0 = group_start(threadIdx.x, G), g1 = group_start(threadIdx.x + 1, G);
@@ -762,14 +769,10 @@ __device__ __forceinline__ void walk_lists(int ni, const int* __restrict__ pref,
       e.z = __funnelshift_r(e.z, e.w, sh);
       e.w = __funnelshift_r(e.w, a, sh);
     }
-    pair((int)(e.x & 0xffffu));
-    pair((int)(e.x >> 16));
-    pair((int)(e.y & 0xffffu));
-    pair((int)(e.y >> 16));
-    pair((int)(e.z & 0xffffu));
-    pair((int)(e.z >> 16));
-    pair((int)(e.w & 0xffffu));
-    pair((int)(e.w >> 16));
+    pair2((int)(e.x & 0xffffu), (int)(e.x >> 16));
+    pair2((int)(e.y & 0xffffu), (int)(e.y >> 16));
+    pair2((int)(e.z & 0xffffu), (int)(e.z >> 16));
+    pair2((int)(e.w & 0xffffu), (int)(e.w >> 16));
   }
   finish();
 }
@@ -923,12 +926,12 @@ __global__ void __launch_bounds__(256, 3) k_density(DevGrid g, DevPhys ph, DevSt
           H2 = h2_exact(pi4.w, ph.gamma_k);
           a = DenAcc{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0};
         },
-        [&](int j) {
+        pair2_of([&](int j) {
           const float4 p = smem4[j];
           den_pair(a, pi4.x - p.x, pi4.y - p.y, pi4.z - p.z, hinv, qband, vi4, smem4[O1 + j], [&]() {
             return exact_neighbour(s.xh, gi, slot_global(S, nseg, j), H2, g.dscale[0], g.dscale[1], g.dscale[2]);
           });
-        },
+        }),
         [&]() { return a; });
   }
   __syncthreads();
@@ -1024,14 +1027,14 @@ __global__ void __launch_bounds__(256, 3) k_gradient(DevGrid g, DevPhys ph, DevS
           ui = gi4.y;
           a = GradAcc{2.f * ci, 0.f, 0};
         },
-        [&](int j) {
+        pair2_of([&](int j) {
           const float4 p = smem4[j];
           grad_pair(a, pi4.x - p.x, pi4.y - p.y, pi4.z - p.z, hinv, qband, vi4, ci, ui, ph.beta, smem4[O1 + j],
                     smem4[O2 + j], [&]() {
                       return exact_neighbour(s.xh, gi, slot_global(S, nseg, j), H2, g.dscale[0], g.dscale[1],
                                              g.dscale[2]);
                     });
-        },
+        }),
         [&]() { return a; });
   }
   __syncthreads();
@@ -1136,7 +1139,7 @@ __global__ void __launch_bounds__(512, 1) k_force(DevGrid g, DevPhys ph, DevStat
           I.P = I.a.x * I.a.w * I.a.w;
           a = ForceAcc{0.f, 0.f, 0.f, 0.f, 2.f * I.a.z, 0};
         },
-        [&](int j) {
+        pair2_of([&](int j) {
           const float4 p = T0[j];
           ForceSide J;
           J.hinv = p.w;
@@ -1152,7 +1155,7 @@ __global__ void __launch_bounds__(512, 1) k_force(DevGrid g, DevPhys ph, DevStat
                                    h2_exact(__uint_as_float(s.xh[gj].w), ph.gamma_k));
             return exact_neighbour(s.xh, gi, gj, H2, g.dscale[0], g.dscale[1], g.dscale[2]);
           }, vs, in);
-        },
+        }),
         [&]() { return a; });
   }
   __syncthreads();

@@ -286,6 +286,10 @@ struct sph_ctx {
   void* sort_tmp = nullptr;
   size_t sort_tmp_bytes = 0;
   uint8_t* blk[2] = {nullptr, nullptr};
+  uint8_t* act_flag = nullptr;  // [nblocks] block has i particles
+  int* blk_list = nullptr;      // [nact] active block ids
+  size_t act_cap = 0;
+  size_t list_cap = 0;
   char* desc_buf = nullptr;   // tile descriptors, nblocks x tile_desc_bytes()
   size_t desc_cap = 0;
   int* pref_buf = nullptr;    // per-block list-group prefixes (k_lists)
@@ -944,34 +948,59 @@ sph_status rebuild_impl(sph_ctx* c) {
     }
     KZ = std::max(1, KZ - 1);
   }
+  // the blocks with i particles, in block order: one loop CTA each (a clustered box on a fine
+  // grid has mostly empty blocks)
+  if ((st = grow(c, &c->act_flag, c->act_cap, (size_t)g.nblocks)) != SPH_OK) return st;
+  if ((st = grow(c, &c->blk_list, c->list_cap, (size_t)g.nblocks)) != SPH_OK) return st;
+  CK(launch_block_active(g, c->cell_start, c->act_flag, c->stream));
+  c->launches++;
+  {
+    cub::CountingInputIterator<int> it(0);
+    size_t need = 0;
+    int* nact_dev = reinterpret_cast<int*>(c->scratch + 12);
+    CK(cub::DeviceSelect::Flagged(nullptr, need, it, c->act_flag, c->blk_list, nact_dev, g.nblocks, c->stream));
+    if (need > c->sel_tmp_bytes) {
+      if (c->sel_tmp) cudaFree(c->sel_tmp);
+      c->sel_tmp = nullptr;
+      CK(cudaMalloc(&c->sel_tmp, need));
+      c->sel_tmp_bytes = need;
+    }
+    CK(cub::DeviceSelect::Flagged(c->sel_tmp, need, it, c->act_flag, c->blk_list, nact_dev, g.nblocks, c->stream));
+    c->launches++;
+    CK(cudaMemcpyAsync(c->scratch_h + 12, c->scratch + 12, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    g.nact = (int)c->scratch_h[12];
+    g.blk_list = c->blk_list;
+  }
   // k_lists: about one warp per 32 particles of a mean block (+10 %); the warps of a larger CTA
   // would only wait at its final barrier (the tile, not the warp count, limits CTAs per SM)
-  g.lists_warps = std::max(2, std::min(8, (int)std::ceil(1.1 * n / std::max(g.nblocks, 1) / 32.0)));
+  g.lists_warps = std::max(2, std::min(8, (int)std::ceil(1.1 * n / std::max(g.nact, 1) / 32.0)));
   // rounding error of a tile coordinate: offsets reach (B/2 + 1) cells from the block centre
   const float max_off = std::max(std::max((0.5f * g.bx + 1.0f) * g.side[0], (0.5f * g.by + 1.0f) * g.side[1]),
                                  (0.5f * g.KZ + 1.0f) * g.side[2]);
   g.eabs = 4.0f * ulp_of(max_off) * 2.0f;  // 8 x (ulp/2): two coordinates per difference, with margin
   if (getenv("SPH_DEBUG")) {
-    std::vector<int> cs(g.ncells + 1);
+    std::vector<int> cs(std::min(g.ncells, 1 << 24) + 1);  // (the monotonicity check on small grids only)
     cudaMemcpyAsync(cs.data(), c->cell_start, cs.size() * 4, cudaMemcpyDeviceToHost, c->stream);
     cudaStreamSynchronize(c->stream);
     int bad = 0;
-    for (int k = 0; k < g.ncells; ++k) bad += cs[k + 1] < cs[k];
+    for (size_t k = 0; k + 1 < cs.size(); ++k) bad += cs[k + 1] < cs[k];
     fprintf(stderr, "[sph rank %d] nx %d ny %d nz %d nxo %d ix_first %d bx %d by %d nbx %d nby %d KZ %d nzb %d nblocks %d "
-            "tcap %d n_own %d gL %d gR %d planeL %d planeR %d cs0 %d csN %d nonmono %d x_lo %u wfix %llu\n",
-            c->rank, g.nx, g.ny, g.nz, g.nxo, g.ix_first, g.bx, g.by, g.nbx, g.nby, g.KZ, g.nzb, g.nblocks, g.tcap,
-            c->n_own, c->gL, c->gR, c->planeL, c->planeR, cs[0], cs[g.ncells], bad, g.x_lo, g.wfix);
+            "nact %d tcap %d n_own %d gL %d gR %d planeL %d planeR %d cs0 %d csN %d nonmono %d x_lo %u wfix %llu\n",
+            c->rank, g.nx, g.ny, g.nz, g.nxo, g.ix_first, g.bx, g.by, g.nbx, g.nby, g.KZ, g.nzb, g.nblocks, g.nact, g.tcap,
+            c->n_own, c->gL, c->gR, c->planeL, c->planeR, cs[0], cs[cs.size() - 1], bad, g.x_lo, g.wfix);
   }
   // per-block tile descriptors for the loop kernels (k_tile_desc)
-  if ((st = grow(c, &c->desc_buf, c->desc_cap, (size_t)g.nblocks * tile_desc_bytes())) != SPH_OK) return st;
+  const size_t na = (size_t)std::max(g.nact, 1);
+  if ((st = grow(c, &c->desc_buf, c->desc_cap, na * tile_desc_bytes())) != SPH_OK) return st;
   g.desc = c->desc_buf;
-  g.desc_cells = c->desc_buf + (size_t)g.nblocks * tile_desc_header_bytes();
-  if ((st = grow(c, &c->pref_buf, c->pref_cap, (size_t)g.nblocks * (g.icap + 1))) != SPH_OK) return st;
+  g.desc_cells = c->desc_buf + na * tile_desc_header_bytes();
+  if ((st = grow(c, &c->pref_buf, c->pref_cap, na * (g.icap + 1))) != SPH_OK) return st;
   g.desc_pref = c->pref_buf;
   CK(launch_tile_desc(g, c->cell_start, c->stream));
   c->launches++;
   const size_t blk_old = c->blk_cap;
-  if ((st = grow(c, &c->blk[0], c->blk_cap, (size_t)g.nblocks)) != SPH_OK) return st;
+  if ((st = grow(c, &c->blk[0], c->blk_cap, na)) != SPH_OK) return st;
   if (!c->blk[1] || c->blk_cap != blk_old) {  // (same capacity as blk[0])
     if (c->blk[1]) cudaFree(c->blk[1]);
     c->blk[1] = nullptr;
@@ -1242,7 +1271,7 @@ sph_status sph_density(sph_ctx* c, sph_density_stats* stats) {
   for (;;) {
     uint8_t* bin = c->blk[pass & 1];
     uint8_t* bout = c->blk[(pass + 1) & 1];
-    CK(cudaMemsetAsync(bout, 0, (size_t)c->grid.nblocks, c->stream));
+    CK(cudaMemsetAsync(bout, 0, (size_t)std::max(c->grid.nact, 1), c->stream));
     CK(cudaMemsetAsync(&c->ctr->active_next, 0, 3 * sizeof(int), c->stream));  // active_next, list_stale, overflow
     CK(cudaMemsetAsync(&c->ctr->h_exceeds, 0, sizeof(int), c->stream));
     {
@@ -1516,7 +1545,8 @@ sph_status sph_destroy(sph_ctx* c) {
                   s.ncount, s.hbuild, c->cell_start, c->keys, c->keys_alt, c->perm, c->perm_alt, c->sort_tmp,
                   c->blk[0], c->blk[1], c->ctr, c->scratch, c->out_tmp, c->mig_send, c->mig_recv, c->pc_send,
                   c->pc_recv, c->pc_scan, c->scan_tmp, c->cnt_dev, c->wide_flag, c->widx, c->wcount,
-                  c->n_wide_dev, c->wnbr, c->sel_tmp, c->desc_buf, c->pref_buf};
+                  c->n_wide_dev, c->wnbr, c->sel_tmp, c->desc_buf, c->pref_buf,
+                  c->act_flag, c->blk_list};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->ctr_h) cudaFreeHost(c->ctr_h);

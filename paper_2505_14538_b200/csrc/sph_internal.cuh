@@ -27,6 +27,8 @@ struct DevGrid {
   int nbx, nby;       // blocks along x, y
   int nzb, KZ;        // z blocks per column, cells per block
   int nblocks;        // nbx * nby * nzb
+  int nact;           // blocks with i particles: the loop kernels' CTAs (a = blockIdx.x)
+  const int* blk_list;  // [nact] active index a -> block id (per-block arrays are indexed by a)
   int ncells;
   int tcap;           // tile capacity (particles) the launch is sized for; slot tcap = sentinel
   int icap;           // most i particles (owned by the block) of any block
@@ -146,5 +148,6 @@ int kernel_threads();
 size_t tile_desc_bytes();  // descriptor + per-cell table, per block
 size_t tile_desc_header_bytes();  // the descriptor alone
 cudaError_t launch_tile_desc(const DevGrid& g, const int* cell_start, cudaStream_t st);
+cudaError_t launch_block_active(const DevGrid& g, const int* cell_start, uint8_t* flag, cudaStream_t st);
 
 }  // namespace sph

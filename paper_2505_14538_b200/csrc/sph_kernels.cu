@@ -1199,7 +1199,7 @@ __global__ void __launch_bounds__(512, 1) k_force(DevGrid g, DevPhys ph, DevStat
 __global__ void __launch_bounds__(64) k_tile_desc(DevGrid g, const int* __restrict__ cell_start) {
   __shared__ BlockShared S;
   Tile T;
-  tile_setup(g, blockIdx.x, cell_start, S, T);
+  tile_setup(g, g.blk_list[blockIdx.x], cell_start, S, T);
   TileDesc* D = reinterpret_cast<TileDesc*>(const_cast<void*>(g.desc)) + blockIdx.x;
   if (threadIdx.x == 0) D->T = T;
   if (threadIdx.x < kMaxICols) {
@@ -1214,10 +1214,8 @@ __global__ void __launch_bounds__(64) k_tile_desc(DevGrid g, const int* __restri
   for (int c = threadIdx.x; c <= T.nct; c += blockDim.x) C[c] = make_int2(S.off[c], c < T.nct ? S.gst[c] : 0);
 }
 
-// per-block tile size and i count (max over blocks) -> sizes shared memory of the loops
-__global__ void k_tile_sizes(DevGrid g, const int* __restrict__ cell_start, int* max_tile, int* max_i) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= g.nblocks) return;
+// tile size and i count of block b
+__device__ void block_counts(const DevGrid& g, const int* __restrict__ cell_start, int b, int& tot_out, int& ni_out) {
   int jx, jy, zb;
   block_coords(g, b, jx, jy, zb);
   const int ix0 = g.ix_first + jx * g.bx, iy0 = jy * g.by;
@@ -1237,8 +1235,27 @@ __global__ void k_tile_sizes(DevGrid g, const int* __restrict__ cell_start, int*
         if (own && z >= z0 && z < z1) ni += c;
       }
     }
-  atomicMax(max_tile, tot);
-  atomicMax(max_i, ni);
+  tot_out = tot;
+  ni_out = ni;
+}
+
+// per-block tile size and i count (max over blocks) -> sizes shared memory of the loops
+__global__ void k_tile_sizes(DevGrid g, const int* __restrict__ cell_start, int* max_tile, int* max_i) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= g.nblocks) return;
+  int tot, ni;
+  block_counts(g, cell_start, b, tot, ni);
+  if (tot) atomicMax(max_tile, tot);
+  if (ni) atomicMax(max_i, ni);
+}
+
+// blocks with i particles (the others launch no loop CTA)
+__global__ void k_block_active(DevGrid g, const int* __restrict__ cell_start, uint8_t* flag) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= g.nblocks) return;
+  int tot, ni;
+  block_counts(g, cell_start, b, tot, ni);
+  flag[b] = ni > 0 ? 1 : 0;
 }
 
 }  // namespace
@@ -1248,7 +1265,13 @@ size_t tile_desc_bytes() { return sizeof(TileDesc) + (size_t)(kMaxTileCells + 1)
 size_t tile_desc_header_bytes() { return sizeof(TileDesc); }
 
 cudaError_t launch_tile_desc(const DevGrid& g, const int* cell_start, cudaStream_t st) {
-  k_tile_desc<<<g.nblocks, 64, 0, st>>>(g, cell_start);
+  if (g.nact == 0) return cudaSuccess;
+  k_tile_desc<<<g.nact, 64, 0, st>>>(g, cell_start);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_block_active(const DevGrid& g, const int* cell_start, uint8_t* flag, cudaStream_t st) {
+  k_block_active<<<(g.nblocks + 255) / 256, 256, 0, st>>>(g, cell_start, flag);
   return cudaGetLastError();
 }
 
@@ -1276,7 +1299,8 @@ cudaError_t launch_lists(const DevGrid& g, const DevPhys& ph, const DevState& s,
   const size_t sm = lists_smem(g);
   cudaError_t e = set_smem((const void*)k_lists, sm);
   if (e != cudaSuccess) return e;
-  k_lists<<<g.nblocks, (g.lists_warps > 0 ? g.lists_warps : kNW) * 32, sm, st>>>(g, ph, s, cell_start, ctr);
+  if (g.nact == 0) return cudaSuccess;
+  k_lists<<<g.nact, (g.lists_warps > 0 ? g.lists_warps : kNW) * 32, sm, st>>>(g, ph, s, cell_start, ctr);
   return cudaGetLastError();
 }
 
@@ -1296,7 +1320,8 @@ cudaError_t launch_density(const DevGrid& g, const DevPhys& ph, const DevState& 
   const size_t sm = density_smem(g);
   cudaError_t e = set_smem((const void*)k_density, sm);
   if (e != cudaSuccess) return e;
-  k_density<<<g.nblocks, kNW * 32, sm, st>>>(g, ph, s, cell_start, pass, blk_in, blk_out, hfac_stale, ctr);
+  if (g.nact == 0) return cudaSuccess;
+  k_density<<<g.nact, kNW * 32, sm, st>>>(g, ph, s, cell_start, pass, blk_in, blk_out, hfac_stale, ctr);
   return cudaGetLastError();
 }
 
@@ -1305,7 +1330,8 @@ cudaError_t launch_gradient(const DevGrid& g, const DevPhys& ph, const DevState&
   const size_t sm = gradient_smem(g);
   cudaError_t e = set_smem((const void*)k_gradient, sm);
   if (e != cudaSuccess) return e;
-  k_gradient<<<g.nblocks, kNW * 32, sm, st>>>(g, ph, s, cell_start, dt, first_step, ctr);
+  if (g.nact == 0) return cudaSuccess;
+  k_gradient<<<g.nact, kNW * 32, sm, st>>>(g, ph, s, cell_start, dt, first_step, ctr);
   return cudaGetLastError();
 }
 
@@ -1314,7 +1340,8 @@ cudaError_t launch_force(const DevGrid& g, const DevPhys& ph, const DevState& s,
   const size_t sm = force_smem(g);
   cudaError_t e = set_smem((const void*)k_force, sm);
   if (e != cudaSuccess) return e;
-  k_force<<<g.nblocks, g.force_threads, sm, st>>>(g, ph, s, cell_start, ctr);
+  if (g.nact == 0) return cudaSuccess;
+  k_force<<<g.nact, g.force_threads, sm, st>>>(g, ph, s, cell_start, ctr);
   return cudaGetLastError();
 }
 

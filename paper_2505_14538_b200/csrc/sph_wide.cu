@@ -70,41 +70,49 @@ __global__ void __launch_bounds__(256) k_wide_lists(DevGrid g, DevPhys ph, DevSt
             kz = reach(Hfac * hi, g.side[2], g.nz);
   const int zlo = (2 * kz + 1 >= g.nz) ? 0 : cz - kz, zn = (2 * kz + 1 >= g.nz) ? g.nz : 2 * kz + 1;
   uint32_t* lst = s.wnbr + (size_t)wi * s.wlcap;
-  int cnt = 0;
   const int nxr = (2 * kx + 1 >= g.nx) ? g.nx : 2 * kx + 1, nyr = (2 * ky + 1 >= g.ny) ? g.ny : 2 * ky + 1;
   const int x0 = (2 * kx + 1 >= g.nx) ? 0 : cx - kx, y0 = (2 * ky + 1 >= g.ny) ? 0 : cy - ky;
-  for (int ax = 0; ax < nxr; ++ax) {
-    const int ccx = ((x0 + ax) % g.nx + g.nx) % g.nx;
-    for (int ay = 0; ay < nyr; ++ay) {
-      const int ccy = ((y0 + ay) % g.ny + g.ny) % g.ny;
+  const int za = ((zlo % g.nz) + g.nz) % g.nz;
+  const int run1 = min(zn, g.nz - za);
+  // lane-parallel over the (2kx+1)(2ky+1) grid columns (most are short or empty on a fine
+  // grid): a counting pass, a warp scan of the counts, then the same scan writing each lane's
+  // hits at its offset -- the list is in (lane, column, slot) order, the same every run
+  auto scan = [&](uint32_t* out, int cap) {
+    int c = 0;
+    for (int q = lane; q < nxr * nyr; q += 32) {
+      const int ax = q / nyr, ay = q - ax * nyr;
+      const int ccx = ((x0 + ax) % g.nx + g.nx) % g.nx, ccy = ((y0 + ay) % g.ny + g.ny) % g.ny;
       const int col = (ccx * g.ny + ccy) * g.nz;
-      // the z range as at most two contiguous runs of cells
-      const int za = ((zlo % g.nz) + g.nz) % g.nz;
-      const int run1 = min(zn, g.nz - za);
-      for (int part = 0; part < 2; ++part) {
+      for (int part = 0; part < 2; ++part) {  // the z range as at most two contiguous runs
         const int c0 = part == 0 ? za : 0, nc = part == 0 ? run1 : zn - run1;
         if (nc <= 0) continue;
-        const int j0 = cell_start[col + c0], j1 = cell_start[col + c0 + nc];
-        for (int jb = j0; jb < j1; jb += 32) {
-          const int j = jb + lane;
-          bool hit = false;
-          if (j < j1) {
-            const uint4 xj = s.xh[j];
-            const float dx = (float)(int)(xi.x - xj.x) * g.scale[0];
-            const float dy = (float)(int)(xi.y - xj.y) * g.scale[1];
-            const float dz = (float)(int)(xi.z - xj.z) * g.scale[2];
-            const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-            const float hj = __uint_as_float(xj.w);
-            hit = r2 < fmaxf(Hi2, (Hfac * hj) * (Hfac * hj));
+        const int j0 = __ldg(cell_start + col + c0), j1 = __ldg(cell_start + col + c0 + nc);
+        for (int j = j0; j < j1; ++j) {
+          const uint4 xj = s.xh[j];
+          const float dx = (float)(int)(xi.x - xj.x) * g.scale[0];
+          const float dy = (float)(int)(xi.y - xj.y) * g.scale[1];
+          const float dz = (float)(int)(xi.z - xj.z) * g.scale[2];
+          const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+          const float hj = __uint_as_float(xj.w);
+          if (r2 < fmaxf(Hi2, (Hfac * hj) * (Hfac * hj))) {
+            if (out && c < cap) out[c] = (uint32_t)j;
+            ++c;
           }
-          const unsigned b = __ballot_sync(kFull, hit);
-          const int pos = cnt + __popc(b & ((1u << lane) - 1u));
-          if (hit && pos < s.wlcap) lst[pos] = (uint32_t)j;
-          cnt += __popc(b);
         }
       }
     }
+    return c;
+  };
+  const int mine = scan(nullptr, 0);
+  int incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += v;
   }
+  const int cnt = __shfl_sync(kFull, incl, 31);
+  const int off = incl - mine;
+  if (mine > 0 && off < s.wlcap) scan(lst + off, s.wlcap - off);
   if (lane == 0) {
     s.wcount[wi] = min(cnt, s.wlcap);
     s.hbuild[i] = hi;

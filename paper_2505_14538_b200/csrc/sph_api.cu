@@ -288,6 +288,8 @@ struct sph_ctx {
   uint8_t* blk[2] = {nullptr, nullptr};
   uint8_t* act_flag = nullptr;  // [nblocks] block has i particles
   int* blk_list = nullptr;      // [nact] active block ids
+  int* run_list = nullptr;      // [nrun] active indices of the blocks with a non-wide i particle
+  size_t run_cap = 0;
   size_t act_cap = 0;
   size_t list_cap = 0;
   char* desc_buf = nullptr;   // tile descriptors, nblocks x tile_desc_bytes()
@@ -703,6 +705,15 @@ sph_status rebuild(sph_ctx* c) {
 }
 
 sph_status rebuild_impl(sph_ctx* c) {
+  // SPH_DEBUG: elapsed ms at the stages of the rebuild (synchronising)
+  const bool dbg = getenv("SPH_DEBUG") != nullptr;
+  const auto tr0 = std::chrono::steady_clock::now();
+  auto stage = [&](const char* what) {
+    if (!dbg) return;
+    cudaStreamSynchronize(c->stream);
+    fprintf(stderr, "[sph]   rebuild %s at %.3f ms\n", what,
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tr0).count());
+  };
   sph_status st;
   // the owned particles sit at [base, base + n); the old ghosts are dropped (re-received below)
   const int base = c->gL;
@@ -897,6 +908,7 @@ sph_status rebuild_impl(sph_ctx* c) {
     CK(cudaGetLastError());
     swap_persist(c);
   }
+  stage("binned");
   // CTA blocks: BX x BY grid columns x KZ cells (BX, BY = 2 when the grid allows: the tile of
   // (BX+2)(BY+2) columns is then ~2x smaller per owned particle than with single columns)
   g.bx = (g.periodic_x ? g.nx >= 6 : g.nxo >= 2) ? 2 : 1;
@@ -919,6 +931,11 @@ sph_status rebuild_impl(sph_ctx* c) {
   if (c->cfg.tile_cells_z > 0) KZ = c->cfg.tile_cells_z;
   KZ = std::max(1, std::min(KZ, kz_max));
   g.lists_warps = 8;  // (the largest k_lists CTA for the fit test)
+  // the largest KZ <= the estimate whose tiles fit (tile sizes grow with KZ): the estimate
+  // first, then a bisection over [1, KZ) when it does not fit (several probes on a grid
+  // whose densest tiles are far above the mean, e.g. clustered boxes)
+  int kz_lo = 0, kz_hi = KZ + 1;  // fits at kz_lo (0: none known), not at kz_hi
+  bool probing = false;
   for (;;) {
     g.KZ = KZ;
     g.nzb = (g.nz + KZ - 1) / KZ;
@@ -939,15 +956,24 @@ sph_status rebuild_impl(sph_ctx* c) {
     if (force_smem(g) > kSmemTarget) g.force_threads = 512;
     const bool fits = force_smem(g) <= kSmemMax && lists_smem(g) <= kSmemMax && density_smem(g) <= kSmemMax &&
                       gradient_smem(g) <= kSmemMax && g.tcap < 65520;
-    if (fits && (force_smem(g) <= kSmemTarget || KZ == 1)) break;
+    const bool ok = fits && (force_smem(g) <= kSmemTarget || KZ == 1);
     if (fits && c->cfg.tile_cells_z > 0) break;
-    if (KZ == 1) {
+    if (!probing && ok) break;  // the estimate fits
+    if (ok) kz_lo = KZ; else kz_hi = KZ;
+    if (!ok && KZ == 1) {
       char b[256];
       snprintf(b, sizeof b, "largest cell tile (%d particles) exceeds shared memory; h contrast too high for one grid", g.tcap);
       return fail(c, SPH_ERR_H_EXCEEDS_CELL, b);
     }
-    KZ = std::max(1, KZ - 1);
+    probing = true;
+    if (kz_hi - kz_lo <= 1) {
+      if (KZ == kz_lo) break;  // (the state of the last probe is the answer)
+      KZ = kz_lo;              // re-probe the answer so g holds its sizes
+      continue;
+    }
+    KZ = kz_lo == 0 ? std::max(1, kz_hi / 2) : (kz_lo + kz_hi) / 2;
   }
+  stage("KZ chosen");
   // the blocks with i particles, in block order: one loop CTA each (a clustered box on a fine
   // grid has mostly empty blocks)
   if ((st = grow(c, &c->act_flag, c->act_cap, (size_t)g.nblocks)) != SPH_OK) return st;
@@ -990,6 +1016,7 @@ sph_status rebuild_impl(sph_ctx* c) {
             c->rank, g.nx, g.ny, g.nz, g.nxo, g.ix_first, g.bx, g.by, g.nbx, g.nby, g.KZ, g.nzb, g.nblocks, g.nact, g.tcap,
             c->n_own, c->gL, c->gR, c->planeL, c->planeR, cs[0], cs[cs.size() - 1], bad, g.x_lo, g.wfix);
   }
+  stage("active blocks");
   // per-block tile descriptors for the loop kernels (k_tile_desc)
   const size_t na = (size_t)std::max(g.nact, 1);
   if ((st = grow(c, &c->desc_buf, c->desc_cap, na * tile_desc_bytes())) != SPH_OK) return st;
@@ -1006,6 +1033,9 @@ sph_status rebuild_impl(sph_ctx* c) {
     c->blk[1] = nullptr;
     CK(dalloc(&c->blk[1], c->blk_cap));
   }
+  stage("descriptors");
+  g.nrun = g.nact;  // (mark_wide narrows it to the blocks with tile particles)
+  g.run_list = nullptr;
   c->stale = false;
   c->lists_stale = true;
   c->dvc_valid = false;
@@ -1039,6 +1069,8 @@ sph_status mark_wide(sph_ctx* c) {
   DevState& s = c->s;
   s.n_wide = 0;
   s.wide = nullptr;
+  c->grid.nrun = c->grid.nact;
+  c->grid.run_list = nullptr;
   if (c->h_side <= 0.f || c->slab) return SPH_OK;
   const int n = c->n_own;
   if (!c->wide_flag) {
@@ -1066,6 +1098,29 @@ sph_status mark_wide(sph_ctx* c) {
   std::memcpy(&nw, c->scratch_h + 10, 4);
   s.n_wide = nw;
   s.wide = c->wide_flag;
+  if (nw > 0 && c->grid.nact > 0) {
+    // the loop kernels run only the blocks with a non-wide i particle
+    DevGrid& g = c->grid;
+    const sph_status st = grow(c, &c->run_list, c->run_cap, (size_t)g.nact);
+    if (st != SPH_OK) return st;
+    CK(launch_block_run(g, s, c->act_flag, c->stream));
+    c->launches++;
+    size_t need2 = 0;
+    int* nrun_dev = reinterpret_cast<int*>(c->scratch + 13);
+    CK(cub::DeviceSelect::Flagged(nullptr, need2, it, c->act_flag, c->run_list, nrun_dev, g.nact, c->stream));
+    if (need2 > c->sel_tmp_bytes) {
+      if (c->sel_tmp) cudaFree(c->sel_tmp);
+      c->sel_tmp = nullptr;
+      CK(cudaMalloc(&c->sel_tmp, need2));
+      c->sel_tmp_bytes = need2;
+    }
+    CK(cub::DeviceSelect::Flagged(c->sel_tmp, need2, it, c->act_flag, c->run_list, nrun_dev, g.nact, c->stream));
+    c->launches++;
+    CK(cudaMemcpyAsync(c->scratch_h + 13, c->scratch + 13, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    g.nrun = (int)c->scratch_h[13];
+    g.run_list = c->run_list;
+  }
   s.widx = c->widx;
   s.wcount = c->wcount;
   s.wlcap = c->wlcap;
@@ -1546,7 +1601,7 @@ sph_status sph_destroy(sph_ctx* c) {
                   c->blk[0], c->blk[1], c->ctr, c->scratch, c->out_tmp, c->mig_send, c->mig_recv, c->pc_send,
                   c->pc_recv, c->pc_scan, c->scan_tmp, c->cnt_dev, c->wide_flag, c->widx, c->wcount,
                   c->n_wide_dev, c->wnbr, c->sel_tmp, c->desc_buf, c->pref_buf,
-                  c->act_flag, c->blk_list};
+                  c->act_flag, c->blk_list, c->run_list};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->ctr_h) cudaFreeHost(c->ctr_h);

@@ -29,6 +29,8 @@ struct DevGrid {
   int nblocks;        // nbx * nby * nzb
   int nact;           // blocks with i particles: the loop kernels' CTAs (a = blockIdx.x)
   const int* blk_list;  // [nact] active index a -> block id (per-block arrays are indexed by a)
+  int nrun;           // blocks the loop kernels run: those with a non-wide i particle
+  const int* run_list;  // [nrun] -> active index a (null: all nact, a = blockIdx.x)
   int ncells;
   int tcap;           // tile capacity (particles) the launch is sized for; slot tcap = sentinel
   int icap;           // most i particles (owned by the block) of any block
@@ -149,5 +151,6 @@ size_t tile_desc_bytes();  // descriptor + per-cell table, per block
 size_t tile_desc_header_bytes();  // the descriptor alone
 cudaError_t launch_tile_desc(const DevGrid& g, const int* cell_start, cudaStream_t st);
 cudaError_t launch_block_active(const DevGrid& g, const int* cell_start, uint8_t* flag, cudaStream_t st);
+cudaError_t launch_block_run(const DevGrid& g, const DevState& s, uint8_t* flag, cudaStream_t st);
 
 }  // namespace sph

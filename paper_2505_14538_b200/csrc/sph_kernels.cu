@@ -266,22 +266,15 @@ __device__ __forceinline__ int warp_max(int v) {
   return v;
 }
 
-#define TILE_PROLOGUE()                                   \
-  __shared__ BlockShared S;                               \
-  Tile T;                                                 \
-  tile_setup(g, blockIdx.x, cell_start, S, T);            \
-  if (T.ntile > g.tcap) {                                 \
-    if (threadIdx.x == 0) atomicExch(&ctr->nonfinite, 2); \
-    return;                                               \
-  }                                                       \
-  const int nseg = 3 * T.ntc;                             \
-  const int SP = g.tcap + kNSent; /* slots per record array (the last kNSent are sentinels) */
-
 // Loop kernels: the block's descriptor from k_tile_desc (S.seg, S.ib, ... and T), one barrier.
+// The active-block index of this CTA (the index of the per-block arrays).
+__device__ __forceinline__ int blk_a(const DevGrid& g) { return g.run_list ? g.run_list[blockIdx.x] : (int)blockIdx.x; }
+
 #define DESC_PROLOGUE()                                                          \
   __shared__ TileDesc S;                                                         \
+  const int ba = blk_a(g); /* active-block index: descriptor, prefix, density flags */ \
   {                                                                              \
-    const int* src_ = reinterpret_cast<const int*>(g.desc) + (size_t)blockIdx.x * (sizeof(TileDesc) / 4); \
+    const int* src_ = reinterpret_cast<const int*>(g.desc) + (size_t)ba * (sizeof(TileDesc) / 4); \
     int* dst_ = reinterpret_cast<int*>(&S);                                      \
     for (int q_ = threadIdx.x; q_ < (int)(sizeof(TileDesc) / 4); q_ += blockDim.x) dst_[q_] = __ldg(src_ + q_); \
   }                                                                              \
@@ -348,9 +341,10 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
   const int nw = blockDim.x >> 5;  // warps (host-chosen from the mean block particle count)
   // the block's tile from its descriptor (k_tile_desc) instead of tile_setup
   __shared__ BlockShared S;
+  const int ba = blk_a(g);
   __shared__ Tile Tsh;
   {
-    const TileDesc* D = reinterpret_cast<const TileDesc*>(g.desc) + blockIdx.x;
+    const TileDesc* D = reinterpret_cast<const TileDesc*>(g.desc) + ba;
     if (threadIdx.x == 0) Tsh = D->T;
     if (threadIdx.x < kMaxICols) {
       S.ib[threadIdx.x] = D->ib[threadIdx.x];
@@ -360,7 +354,7 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
     if (threadIdx.x <= kMaxICols) S.pre[threadIdx.x] = D->pre[threadIdx.x];
     for (int q = threadIdx.x; q < kMaxSeg; q += blockDim.x) S.seg[q] = D->seg[q];
     const int nct = D->T.nct;
-    const int2* C = reinterpret_cast<const int2*>(g.desc_cells) + (size_t)blockIdx.x * (kMaxTileCells + 1);
+    const int2* C = reinterpret_cast<const int2*>(g.desc_cells) + (size_t)ba * (kMaxTileCells + 1);
     for (int c = threadIdx.x; c <= nct; c += blockDim.x) {
       const int2 v = __ldg(C + c);
       S.off[c] = v.x;
@@ -575,7 +569,7 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
   // as here), for the loop kernels' walks (walk_prefix_pre)
   __syncthreads();
   block_exclusive_scan(grp, ni);
-  int* out = g.desc_pref + (size_t)blockIdx.x * (g.icap + 1);
+  int* out = g.desc_pref + (size_t)ba * (g.icap + 1);
   for (int k = threadIdx.x; k <= ni; k += blockDim.x) out[k] = grp[k];
 }
 
@@ -830,7 +824,7 @@ __device__ __forceinline__ Acc gather_acc(const WalkArea<Acc>& W, int ni, int k)
 template <class Acc>
 // Issued with cp.async before the tile staging, whose wait + barrier completes it.
 __device__ __forceinline__ void walk_prefix_pre(const DevGrid& g, WalkArea<Acc>& W, int ni) {
-  const int* src = g.desc_pref + (size_t)blockIdx.x * (g.icap + 1);
+  const int* src = g.desc_pref + (size_t)blk_a(g) * (g.icap + 1);
   for (int k = threadIdx.x; k <= ni; k += blockDim.x) cp_async4(W.pref + k, src + k);
 }
 
@@ -860,7 +854,7 @@ __global__ void __launch_bounds__(256, 3) k_density(DevGrid g, DevPhys ph, DevSt
                                                       const int* __restrict__ cell_start, int pass,
                                                       const uint8_t* __restrict__ blk_in, uint8_t* __restrict__ blk_out,
                                                       float hfac_stale, DevCounters* __restrict__ ctr) {
-  if (pass > 0 && !blk_in[blockIdx.x]) return;
+  if (pass > 0 && !blk_in[blk_a(g)]) return;
   __shared__ int s_ni;
   __shared__ unsigned long long s_pairs, s_final;
   __shared__ int s_unconv, s_active;
@@ -964,7 +958,7 @@ __global__ void __launch_bounds__(256, 3) k_density(DevGrid g, DevPhys ph, DevSt
     if (s_pairs) atomicAdd(&ctr->pairs_all, s_pairs);  // all pairs of this pass (h iteration work)
     if (s_final) atomicAdd(&ctr->pairs, s_final);
     if (s_unconv) atomicAdd(&ctr->unconverged, s_unconv);
-    if (s_active) { blk_out[blockIdx.x] = 1; atomicAdd(&ctr->active_next, 1); }
+    if (s_active) { blk_out[ba] = 1; atomicAdd(&ctr->active_next, 1); }
   }
 }
 
@@ -1249,6 +1243,20 @@ __global__ void k_tile_sizes(DevGrid g, const int* __restrict__ cell_start, int*
   if (ni) atomicMax(max_i, ni);
 }
 
+// active blocks with a non-wide i particle (the loop kernels run only these)
+__global__ void k_block_run(DevGrid g, DevState s, uint8_t* flag) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= g.nact) return;
+  const TileDesc* D = reinterpret_cast<const TileDesc*>(g.desc) + a;
+  int run = 0;
+  for (int r = 0; r < kMaxICols && !run; ++r) {
+    const int c = D->pre[r + 1] - D->pre[r], g0 = D->g0[r];
+    for (int k = 0; k < c; ++k)
+      if (!s.wide[g0 + k]) { run = 1; break; }
+  }
+  flag[a] = (uint8_t)run;
+}
+
 // blocks with i particles (the others launch no loop CTA)
 __global__ void k_block_active(DevGrid g, const int* __restrict__ cell_start, uint8_t* flag) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1267,6 +1275,12 @@ size_t tile_desc_header_bytes() { return sizeof(TileDesc); }
 cudaError_t launch_tile_desc(const DevGrid& g, const int* cell_start, cudaStream_t st) {
   if (g.nact == 0) return cudaSuccess;
   k_tile_desc<<<g.nact, 64, 0, st>>>(g, cell_start);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_block_run(const DevGrid& g, const DevState& s, uint8_t* flag, cudaStream_t st) {
+  if (g.nact == 0) return cudaSuccess;
+  k_block_run<<<(g.nact + 255) / 256, 256, 0, st>>>(g, s, flag);
   return cudaGetLastError();
 }
 
@@ -1299,8 +1313,8 @@ cudaError_t launch_lists(const DevGrid& g, const DevPhys& ph, const DevState& s,
   const size_t sm = lists_smem(g);
   cudaError_t e = set_smem((const void*)k_lists, sm);
   if (e != cudaSuccess) return e;
-  if (g.nact == 0) return cudaSuccess;
-  k_lists<<<g.nact, (g.lists_warps > 0 ? g.lists_warps : kNW) * 32, sm, st>>>(g, ph, s, cell_start, ctr);
+  if (g.nrun == 0) return cudaSuccess;
+  k_lists<<<g.nrun, (g.lists_warps > 0 ? g.lists_warps : kNW) * 32, sm, st>>>(g, ph, s, cell_start, ctr);
   return cudaGetLastError();
 }
 
@@ -1320,8 +1334,8 @@ cudaError_t launch_density(const DevGrid& g, const DevPhys& ph, const DevState& 
   const size_t sm = density_smem(g);
   cudaError_t e = set_smem((const void*)k_density, sm);
   if (e != cudaSuccess) return e;
-  if (g.nact == 0) return cudaSuccess;
-  k_density<<<g.nact, kNW * 32, sm, st>>>(g, ph, s, cell_start, pass, blk_in, blk_out, hfac_stale, ctr);
+  if (g.nrun == 0) return cudaSuccess;
+  k_density<<<g.nrun, kNW * 32, sm, st>>>(g, ph, s, cell_start, pass, blk_in, blk_out, hfac_stale, ctr);
   return cudaGetLastError();
 }
 
@@ -1330,8 +1344,8 @@ cudaError_t launch_gradient(const DevGrid& g, const DevPhys& ph, const DevState&
   const size_t sm = gradient_smem(g);
   cudaError_t e = set_smem((const void*)k_gradient, sm);
   if (e != cudaSuccess) return e;
-  if (g.nact == 0) return cudaSuccess;
-  k_gradient<<<g.nact, kNW * 32, sm, st>>>(g, ph, s, cell_start, dt, first_step, ctr);
+  if (g.nrun == 0) return cudaSuccess;
+  k_gradient<<<g.nrun, kNW * 32, sm, st>>>(g, ph, s, cell_start, dt, first_step, ctr);
   return cudaGetLastError();
 }
 
@@ -1340,8 +1354,8 @@ cudaError_t launch_force(const DevGrid& g, const DevPhys& ph, const DevState& s,
   const size_t sm = force_smem(g);
   cudaError_t e = set_smem((const void*)k_force, sm);
   if (e != cudaSuccess) return e;
-  if (g.nact == 0) return cudaSuccess;
-  k_force<<<g.nact, g.force_threads, sm, st>>>(g, ph, s, cell_start, ctr);
+  if (g.nrun == 0) return cudaSuccess;
+  k_force<<<g.nrun, g.force_threads, sm, st>>>(g, ph, s, cell_start, ctr);
   return cudaGetLastError();
 }
 

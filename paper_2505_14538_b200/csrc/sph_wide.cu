@@ -51,6 +51,7 @@ __global__ void k_mark_wide(int n, DevGrid g, DevPhys ph, DevState s, uint8_t* f
   if (i >= n) return;
   const float R = (1.f + g.skin) * ph.gamma_k * __uint_as_float(s.xh[i].w);
   flag[i] = R > g.side_min ? 1 : 0;
+  if (R > g.side_min) s.ncount[i] = 0;  // (no tile list: its block may not even run)
 }
 
 // One warp per wide particle.  Overflow of wlcap: the count is still returned (max in

@@ -570,6 +570,13 @@ sph_status grow(sph_ctx* c, T** p, size_t& cap, size_t need) {
   return SPH_OK;
 }
 
+// grow() with 25 % headroom, for buffers sized by counts that drift from rebuild to rebuild
+// (active blocks): a realloc (and the device sync of cudaFree) only every so often
+template <class T>
+sph_status grow_h(sph_ctx* c, T** p, size_t& cap, size_t need) {
+  return need <= cap ? SPH_OK : grow(c, p, cap, need + need / 4);
+}
+
 // Ghost halo exchange of one per-particle array (elem bytes each): the first owned plane goes
 // to the left neighbour (its right ghosts), the last owned plane to the right neighbour (its
 // left ghosts).  Ghost sets are fixed between rebuilds, so no sizes are exchanged.
@@ -976,8 +983,8 @@ sph_status rebuild_impl(sph_ctx* c) {
   stage("KZ chosen");
   // the blocks with i particles, in block order: one loop CTA each (a clustered box on a fine
   // grid has mostly empty blocks)
-  if ((st = grow(c, &c->act_flag, c->act_cap, (size_t)g.nblocks)) != SPH_OK) return st;
-  if ((st = grow(c, &c->blk_list, c->list_cap, (size_t)g.nblocks)) != SPH_OK) return st;
+  if ((st = grow_h(c, &c->act_flag, c->act_cap, (size_t)g.nblocks)) != SPH_OK) return st;
+  if ((st = grow_h(c, &c->blk_list, c->list_cap, (size_t)g.nblocks)) != SPH_OK) return st;
   CK(launch_block_active(g, c->cell_start, c->act_flag, c->stream));
   c->launches++;
   {
@@ -1019,15 +1026,15 @@ sph_status rebuild_impl(sph_ctx* c) {
   stage("active blocks");
   // per-block tile descriptors for the loop kernels (k_tile_desc)
   const size_t na = (size_t)std::max(g.nact, 1);
-  if ((st = grow(c, &c->desc_buf, c->desc_cap, na * tile_desc_bytes())) != SPH_OK) return st;
+  if ((st = grow_h(c, &c->desc_buf, c->desc_cap, na * tile_desc_bytes())) != SPH_OK) return st;
   g.desc = c->desc_buf;
   g.desc_cells = c->desc_buf + na * tile_desc_header_bytes();
-  if ((st = grow(c, &c->pref_buf, c->pref_cap, na * (g.icap + 1))) != SPH_OK) return st;
+  if ((st = grow_h(c, &c->pref_buf, c->pref_cap, na * (g.icap + 1))) != SPH_OK) return st;
   g.desc_pref = c->pref_buf;
   CK(launch_tile_desc(g, c->cell_start, c->stream));
   c->launches++;
   const size_t blk_old = c->blk_cap;
-  if ((st = grow(c, &c->blk[0], c->blk_cap, na)) != SPH_OK) return st;
+  if ((st = grow_h(c, &c->blk[0], c->blk_cap, na)) != SPH_OK) return st;
   if (!c->blk[1] || c->blk_cap != blk_old) {  // (same capacity as blk[0])
     if (c->blk[1]) cudaFree(c->blk[1]);
     c->blk[1] = nullptr;
@@ -1101,7 +1108,7 @@ sph_status mark_wide(sph_ctx* c) {
   if (nw > 0 && c->grid.nact > 0) {
     // the loop kernels run only the blocks with a non-wide i particle
     DevGrid& g = c->grid;
-    const sph_status st = grow(c, &c->run_list, c->run_cap, (size_t)g.nact);
+    const sph_status st = grow_h(c, &c->run_list, c->run_cap, (size_t)g.nact);
     if (st != SPH_OK) return st;
     CK(launch_block_run(g, s, c->act_flag, c->stream));
     c->launches++;

@@ -27,6 +27,8 @@ def _cases():
         "sedov24": lambda: W.sedov(24),
         # C5-like clustered box: uniform initial h, ~10x h contrast once converged
         "clustered8k": lambda: W.clustered(8192, seed=77),
+        # particles in 6 % of the box: most blocks empty (compacted block list)
+        "blob4096": lambda: W.blob(4096),
     }
 
 
@@ -59,7 +61,7 @@ def test_density_fixed_h(case):
     assert g["stats"]["pairs_density"] == int(d["count"].sum())
 
 
-@pytest.mark.parametrize("case", ["lattice16", "jitter16", "poisson4096", "sod16", "gresho24j", "sedov24"])
+@pytest.mark.parametrize("case", ["lattice16", "jitter16", "poisson4096", "sod16", "gresho24j", "sedov24", "blob4096"])
 def test_full_pass_fixed_h(case):
     """Density -> finalize -> gradient (+ghost) -> force -> dt at the given h."""
     p = _with_switches(_cases()[case](), 5)
@@ -90,7 +92,7 @@ def test_full_pass_fixed_h(case):
 
 @pytest.mark.parametrize("case,fac", [("lattice16", 1.5), ("lattice16", 0.7), ("jitter16", 1.3),
                                       ("poisson4096", 1.0), ("sod16", 1.2), ("sedov24", 1.0),
-                                      ("clustered8k", 1.0)])
+                                      ("clustered8k", 1.0), ("blob4096", 1.0)])
 def test_h_iteration_end_to_end(case, fac):
     """Newton h iteration on the GPU vs the oracle's exact root (tol 1e-13): with the GPU at
     h_tol = 1e-6, h and rho agree to 1e-5 and counts are exact; with the paper's 1e-4 every

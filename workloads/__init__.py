@@ -18,6 +18,7 @@ from .generators import (  # noqa: F401
     lattice,
     jittered_lattice,
     poisson,
+    blob,
     sod,
     sedov,
     gresho,

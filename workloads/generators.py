@@ -98,6 +98,18 @@ def poisson(N=4096, seed=2, vel_sigma=0.05, u=1.5, u_sigma=0.2, h_factor=1.0):
                  h_factor * H_STAR_LATTICE * dx, (1.0, 1.0, 1.0))
 
 
+def blob(N=4096, side=0.4, seed=31, vel_sigma=0.05, u=1.5, u_sigma=0.2, h_factor=1.0):
+    """Uniform-random positions in a cube of `side` at the origin of the unit box, the rest
+    empty: most cell blocks of the grid hold no particle (the loop kernels' block compaction)."""
+    rng = np.random.default_rng(seed)
+    x = rng.uniform(0.0, side, size=(N, 3)) + 0.05
+    v = rng.normal(0.0, vel_sigma, size=(N, 3))
+    uu = u * np.exp(u_sigma * rng.standard_normal(N))
+    dx = side * N ** (-1.0 / 3.0)
+    return _pack(f"blob{N}", _fixed_point(x, (1, 1, 1)), v, 1.0 / N, uu,
+                 h_factor * H_STAR_LATTICE * dx, (1.0, 1.0, 1.0))
+
+
 def sod(n=64, h_factor=1.0):
     """C2: 3-D Sod shock tube, two n^3 lattices with equal spacing 1/n in [0,2)x[0,1)^2.
 

@@ -28,6 +28,8 @@ for k in sys.argv[2:] or ["k_density", "k_gradient", "k_force"]:
     s, te = h.index("Source"), h.index("Predicated-On Thread Instructions Executed")
     fl = 0.0
     for row in data:
+        if len(row) != len(h):  # (the next launch's table: count the first launch only)
+            break
         t = row[s].strip()
         op = (t.split()[1] if t.startswith("@") else t.split()[0]) if t else ""
         n = float(row[te] or 0)

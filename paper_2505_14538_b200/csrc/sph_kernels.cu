@@ -903,16 +903,15 @@ __global__ void __launch_bounds__(256, 3) k_density(DevGrid g, DevPhys ph, DevSt
     double H2 = 0.0;
     int gi = 0;
     DenAcc a;
+    int ti_c = 0;  // tile slot of the walk's current particle (list_of -> begin)
     walk_lists(
         ni, W.pref, W.fin, W.head, W.tail,
-        [&](int k) {
-          int ti, gk;
-          i_slot(S, W.kl[k], ti, gk);
-          return s.nbr + (size_t)gk * g.lcap;
+        [&](int k) {  // (list_of runs right before begin: the slot lookup is shared)
+          i_slot(S, W.kl[k], ti_c, gi);
+          return s.nbr + (size_t)gi * g.lcap;
         },
-        [&](int k) {
-          int ti;
-          i_slot(S, W.kl[k], ti, gi);
+        [&](int) {
+          const int ti = ti_c;
           pi4 = smem4[ti];
           vi4 = smem4[O1 + ti];
           hinv = 1.f / pi4.w;
@@ -1001,16 +1000,15 @@ __global__ void __launch_bounds__(256, 3) k_gradient(DevGrid g, DevPhys ph, DevS
     double H2 = 0.0;
     int gi = 0;
     GradAcc a;
+    int ti_c = 0;  // tile slot of the walk's current particle (list_of -> begin)
     walk_lists(
         ni, W.pref, W.fin, W.head, W.tail,
-        [&](int k) {
-          int ti, gk;
-          i_slot(S, W.kl[k], ti, gk);
-          return s.nbr + (size_t)gk * g.lcap;
+        [&](int k) {  // (list_of runs right before begin: the slot lookup is shared)
+          i_slot(S, W.kl[k], ti_c, gi);
+          return s.nbr + (size_t)gi * g.lcap;
         },
-        [&](int k) {
-          int ti;
-          i_slot(S, k, ti, gi);
+        [&](int) {
+          const int ti = ti_c;
           pi4 = smem4[ti];
           vi4 = smem4[O1 + ti];
           const float4 gi4 = smem4[O2 + ti];
@@ -1115,16 +1113,15 @@ __global__ void __launch_bounds__(512, 1) k_force(DevGrid g, DevPhys ph, DevStat
     ForceSide I;
     int gi = 0;
     ForceAcc a;
+    int ti_c = 0;  // tile slot of the walk's current particle (list_of -> begin)
     walk_lists(
         ni, W.pref, W.fin, W.head, W.tail,
-        [&](int k) {
-          int ti, gk;
-          i_slot(S, W.kl[k], ti, gk);
-          return s.nbr + (size_t)gk * g.lcap;
+        [&](int k) {  // (list_of runs right before begin: the slot lookup is shared)
+          i_slot(S, W.kl[k], ti_c, gi);
+          return s.nbr + (size_t)gi * g.lcap;
         },
-        [&](int k) {
-          int ti;
-          i_slot(S, k, ti, gi);
+        [&](int) {
+          const int ti = ti_c;
           pi4 = T0[ti];
           I.hinv = pi4.w;
           I.v = T1[ti];

@@ -234,6 +234,19 @@ __device__ __forceinline__ void cp_async4(const void* smem_dst, const void* gmem
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(gmem_src));
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+// 16-byte shared-memory load at a 32-bit shared address: the loops gather their neighbour
+// records this way from record-array bases held in registers (smem_base's opaque move keeps
+// the compiler from rebuilding the shared window address before every gather)
+__device__ __forceinline__ float4 lds4(uint32_t a) {
+  float4 v;
+  asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t smem_base(int rec) {
+  uint32_t a;
+  asm volatile("mov.u32 %0, %1;" : "=r"(a) : "r"((uint32_t)__cvta_generic_to_shared(smem4) + (uint32_t)rec * 16u));
+  return a;
+}
 
 // Stage nrec16 16-byte per-particle records (at smem4[o16[r] + slot]) and optionally one
 // 4-byte record (at float offset o4) of every tile slot with cp.async: no register round
@@ -903,6 +916,7 @@ __global__ void __launch_bounds__(256, 3) k_density(DevGrid g, DevPhys ph, DevSt
     double H2 = 0.0;
     int gi = 0;
     DenAcc a;
+    const uint32_t sb0 = smem_base(0), sb1 = smem_base(O1);
     int ti_c = 0;  // tile slot of the walk's current particle (list_of -> begin)
     walk_lists(
         ni, W.pref, W.fin, W.head, W.tail,
@@ -920,8 +934,9 @@ __global__ void __launch_bounds__(256, 3) k_density(DevGrid g, DevPhys ph, DevSt
           a = DenAcc{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0};
         },
         pair2_of([&](int j) {
-          const float4 p = smem4[j];
-          den_pair(a, pi4.x - p.x, pi4.y - p.y, pi4.z - p.z, hinv, qband, vi4, smem4[O1 + j], [&]() {
+          const uint32_t o = (uint32_t)j << 4;
+          const float4 p = lds4(sb0 + o);
+          den_pair(a, pi4.x - p.x, pi4.y - p.y, pi4.z - p.z, hinv, qband, vi4, lds4(sb1 + o), [&]() {
             return exact_neighbour(s.xh, gi, slot_global(S, nseg, j), H2, g.dscale[0], g.dscale[1], g.dscale[2]);
           });
         }),
@@ -1000,6 +1015,7 @@ __global__ void __launch_bounds__(256, 3) k_gradient(DevGrid g, DevPhys ph, DevS
     double H2 = 0.0;
     int gi = 0;
     GradAcc a;
+    const uint32_t sb0 = smem_base(0), sb1 = smem_base(O1), sb2 = smem_base(O2);
     int ti_c = 0;  // tile slot of the walk's current particle (list_of -> begin)
     walk_lists(
         ni, W.pref, W.fin, W.head, W.tail,
@@ -1020,9 +1036,10 @@ __global__ void __launch_bounds__(256, 3) k_gradient(DevGrid g, DevPhys ph, DevS
           a = GradAcc{2.f * ci, 0.f, 0};
         },
         pair2_of([&](int j) {
-          const float4 p = smem4[j];
-          grad_pair(a, pi4.x - p.x, pi4.y - p.y, pi4.z - p.z, hinv, qband, vi4, ci, ui, ph.beta, smem4[O1 + j],
-                    smem4[O2 + j], [&]() {
+          const uint32_t o = (uint32_t)j << 4;
+          const float4 p = lds4(sb0 + o);
+          grad_pair(a, pi4.x - p.x, pi4.y - p.y, pi4.z - p.z, hinv, qband, vi4, ci, ui, ph.beta, lds4(sb1 + o),
+                    lds4(sb2 + o), [&]() {
                       return exact_neighbour(s.xh, gi, slot_global(S, nseg, j), H2, g.dscale[0], g.dscale[1],
                                              g.dscale[2]);
                     });
@@ -1113,6 +1130,7 @@ __global__ void __launch_bounds__(512, 1) k_force(DevGrid g, DevPhys ph, DevStat
     ForceSide I;
     int gi = 0;
     ForceAcc a;
+    const uint32_t sb0 = smem_base(0), sb1 = smem_base(O1), sb2 = smem_base(O2), sb3 = smem_base(O3);
     int ti_c = 0;  // tile slot of the walk's current particle (list_of -> begin)
     walk_lists(
         ni, W.pref, W.fin, W.head, W.tail,
@@ -1131,12 +1149,13 @@ __global__ void __launch_bounds__(512, 1) k_force(DevGrid g, DevPhys ph, DevStat
           a = ForceAcc{0.f, 0.f, 0.f, 0.f, 2.f * I.a.z, 0};
         },
         pair2_of([&](int j) {
-          const float4 p = T0[j];
+          const uint32_t o = (uint32_t)j << 4;
+          const float4 p = lds4(sb0 + o);
           ForceSide J;
           J.hinv = p.w;
-          J.v = T1[j];
-          J.a = T2[j];
-          J.b = T3[j];
+          J.v = lds4(sb1 + o);
+          J.a = lds4(sb2 + o);
+          J.b = lds4(sb3 + o);
           J.P = J.a.x * J.a.w * J.a.w;
           float vs;
           int in;

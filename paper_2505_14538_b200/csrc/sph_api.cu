@@ -290,6 +290,10 @@ struct sph_ctx {
   int* blk_list = nullptr;      // [nact] active block ids
   int* run_list = nullptr;      // [nrun] active indices of the blocks with a non-wide i particle
   size_t run_cap = 0;
+  uint32_t* cperm = nullptr;    // wide search grid: particles in coarse-cell order
+  size_t cperm_cap = 0;
+  int* ccs = nullptr;           // its coarse cell starts
+  size_t ccs_cap = 0;
   size_t act_cap = 0;
   size_t list_cap = 0;
   char* desc_buf = nullptr;   // tile descriptors, nblocks x tile_desc_bytes()
@@ -1105,6 +1109,37 @@ sph_status mark_wide(sph_ctx* c) {
   std::memcpy(&nw, c->scratch_h + 10, 4);
   s.n_wide = nw;
   s.wide = c->wide_flag;
+  if (nw > 0) {
+    // the wide particles' search grid (sph_wide.cu): coarse cells of F^3 grid cells, F such
+    // that a particle at the 99th percentile of h reaches about two coarse cells
+    DevGrid& g = c->grid;
+    float hq;
+    sph_status sq;
+    if ((sq = h_quantile(c, 0.99, &hq)) != SPH_OK) return sq;
+    const float R = (1.f + c->cfg.cell_skin) * c->cfg.gamma_k * hq;
+    const float side = std::min(g.side[0], std::min(g.side[1], g.side[2]));
+    const int F = std::max(1, std::min(64, (int)std::ceil(R / (2.f * side))));
+    s.cF = F;
+    s.cnx = (g.nx + F - 1) / F;
+    s.cny = (g.ny + F - 1) / F;
+    s.cnz = (g.nz + F - 1) / F;
+    const long long ncc = (long long)s.cnx * s.cny * s.cnz;
+    if ((sq = grow_h(c, &c->cperm, c->cperm_cap, (size_t)std::max(n, 1))) != SPH_OK) return sq;
+    if ((sq = grow_h(c, &c->ccs, c->ccs_cap, (size_t)ncc + 1)) != SPH_OK) return sq;
+    CK(launch_coarse_keys(n, 0, g, s, c->keys, c->perm, c->stream));
+    c->launches++;
+    int bits = 1;
+    while ((1LL << bits) <= ncc) ++bits;
+    size_t tmp = c->sort_tmp_bytes;
+    CK(cub::DeviceRadixSort::SortPairs(c->sort_tmp, tmp, c->keys, c->keys_alt, c->perm, c->cperm, n, 0, bits,
+                                       c->stream));
+    c->launches++;
+    k_cell_start<<<nblk(n + 1, 256), 256, 0, c->stream>>>(n, (int)ncc, 0, c->keys_alt, c->ccs);
+    c->launches++;
+    CK(cudaGetLastError());
+    s.cperm = c->cperm;
+    s.ccs = c->ccs;
+  }
   if (nw > 0 && c->grid.nact > 0) {
     // the loop kernels run only the blocks with a non-wide i particle
     DevGrid& g = c->grid;
@@ -1608,7 +1643,7 @@ sph_status sph_destroy(sph_ctx* c) {
                   c->blk[0], c->blk[1], c->ctr, c->scratch, c->out_tmp, c->mig_send, c->mig_recv, c->pc_send,
                   c->pc_recv, c->pc_scan, c->scan_tmp, c->cnt_dev, c->wide_flag, c->widx, c->wcount,
                   c->n_wide_dev, c->wnbr, c->sel_tmp, c->desc_buf, c->pref_buf,
-                  c->act_flag, c->blk_list, c->run_list};
+                  c->act_flag, c->blk_list, c->run_list, c->cperm, c->ccs};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->ctr_h) cudaFreeHost(c->ctr_h);

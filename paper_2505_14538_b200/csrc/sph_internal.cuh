@@ -104,6 +104,11 @@ struct DevState {
   uint32_t* wnbr;     // [n_wide][wlcap] neighbour lists, global indices
   int32_t* wcount;    // [n_wide] list lengths
   int n_wide, wlcap;
+  // the wide particles' search grid: coarse cells of cF^3 grid cells (cnx x cny x cnz, the
+  // last along an axis possibly thinner), particles sorted by coarse cell (cperm), ranges ccs
+  const uint32_t* cperm;  // [n_own] particle indices in coarse-cell order
+  const int* ccs;         // [cnx cny cnz + 1] coarse cell starts in cperm
+  int cF, cnx, cny, cnz;
 };
 
 struct DevCounters {
@@ -138,6 +143,8 @@ cudaError_t launch_bank(int i0, int n, const DevGrid& g, const DevState& s, cuda
 // wide particles (sph_wide.cu)
 cudaError_t launch_mark_wide(int n, const DevGrid& g, const DevPhys& ph, const DevState& s, uint8_t* flag,
                              cudaStream_t st);
+cudaError_t launch_coarse_keys(int n, int i0, const DevGrid& g, const DevState& s, unsigned int* keys,
+                               unsigned int* vals, cudaStream_t st);
 cudaError_t launch_wide_lists(const DevGrid& g, const DevPhys& ph, const DevState& s, const int* cell_start,
                               DevCounters* ctr, cudaStream_t st);
 cudaError_t launch_wide_density(const DevGrid& g, const DevPhys& ph, const DevState& s, int pass, float hfac_stale,

@@ -46,6 +46,41 @@ __device__ __forceinline__ bool within(int a, int b, int k, int n) {
   return d <= k;
 }
 
+// The wide particles search a coarse grid: coarse cell (cx / F, cy / F, cz / F) of grid cell
+// (cx, cy, cz), F = s.cF (the last coarse cell along an axis may be thinner).  A particle with
+// list radius R lists candidates from every coarse cell that meets the grid-cell box
+// +-reach(R) around its own cell -- a superset of its sphere -- and the force kernel decides
+// "did the wide j list i" with the same predicate (coarse_meets).
+__device__ __forceinline__ bool coarse_meets(int ci, int a, int k, int n, int F) {
+  if (2 * k + 1 >= n) return true;  // (the whole axis)
+  const int f0 = ci * F, w = min(F, n - f0);
+  const int d0 = ((f0 - a) % n + n) % n;  // start of the coarse cell, from a (mod n)
+  return d0 <= 2 * k || d0 + w > n;
+}
+// coarse cells meeting the grid-cell range [a, a + 2k] (mod n): c0 (the one holding a) and
+// the cnt that follow it cyclically
+__device__ __forceinline__ void coarse_range(int a, int k, int n, int F, int cn, int& c0, int& cnt) {
+  const int am = ((a % n) + n) % n;
+  c0 = (2 * k + 1 >= n) ? 0 : am / F;
+  cnt = 0;
+  int ci = c0;
+  while (cnt < cn && coarse_meets(ci, a, k, n, F)) {
+    ++cnt;
+    ci = ci + 1 == cn ? 0 : ci + 1;
+  }
+}
+
+__global__ void k_coarse_keys(int n, DevGrid g, DevState s, unsigned int* keys, unsigned int* vals) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint4 x = s.xh[i];
+  const int F = s.cF;
+  const unsigned int ccx = (unsigned)(cell_axis(x.x, g.nx) / F), ccy = (unsigned)(cell_axis(x.y, g.ny) / F),
+                     ccz = (unsigned)(cell_axis(x.z, g.nz) / F);
+  keys[i] = (ccx * (unsigned)s.cny + ccy) * (unsigned)s.cnz + ccz;
+  vals[i] = (unsigned)i;
+}
+
 __global__ void k_mark_wide(int n, DevGrid g, DevPhys ph, DevState s, uint8_t* flag) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -69,51 +104,45 @@ __global__ void __launch_bounds__(256) k_wide_lists(DevGrid g, DevPhys ph, DevSt
   const int cx = cell_axis(xi.x, g.nx), cy = cell_axis(xi.y, g.ny), cz = cell_axis(xi.z, g.nz);
   const int kx = reach(Hfac * hi, g.side[0], g.nx), ky = reach(Hfac * hi, g.side[1], g.ny),
             kz = reach(Hfac * hi, g.side[2], g.nz);
-  const int zlo = (2 * kz + 1 >= g.nz) ? 0 : cz - kz, zn = (2 * kz + 1 >= g.nz) ? g.nz : 2 * kz + 1;
+  const int F = s.cF;
+  int x0, nxc, y0, nyc, z0, nzc;  // coarse cells meeting the grid-cell box, per axis
+  coarse_range(cx - kx, kx, g.nx, F, s.cnx, x0, nxc);
+  coarse_range(cy - ky, ky, g.ny, F, s.cny, y0, nyc);
+  coarse_range(cz - kz, kz, g.nz, F, s.cnz, z0, nzc);
+  const int run1 = min(nzc, s.cnz - z0);  // the z range as at most two contiguous runs
   uint32_t* lst = s.wnbr + (size_t)wi * s.wlcap;
-  const int nxr = (2 * kx + 1 >= g.nx) ? g.nx : 2 * kx + 1, nyr = (2 * ky + 1 >= g.ny) ? g.ny : 2 * ky + 1;
-  const int x0 = (2 * kx + 1 >= g.nx) ? 0 : cx - kx, y0 = (2 * ky + 1 >= g.ny) ? 0 : cy - ky;
-  const int za = ((zlo % g.nz) + g.nz) % g.nz;
-  const int run1 = min(zn, g.nz - za);
-  // lane-parallel over the (2kx+1)(2ky+1) grid columns (most are short or empty on a fine
-  // grid): a counting pass, a warp scan of the counts, then the same scan writing each lane's
-  // hits at its offset -- the list is in (lane, column, slot) order, the same every run
-  auto scan = [&](uint32_t* out, int cap) {
-    int c = 0;
-    for (int q = lane; q < nxr * nyr; q += 32) {
-      const int ax = q / nyr, ay = q - ax * nyr;
-      const int ccx = ((x0 + ax) % g.nx + g.nx) % g.nx, ccy = ((y0 + ay) % g.ny + g.ny) % g.ny;
-      const int col = (ccx * g.ny + ccy) * g.nz;
-      for (int part = 0; part < 2; ++part) {  // the z range as at most two contiguous runs
-        const int c0 = part == 0 ? za : 0, nc = part == 0 ? run1 : zn - run1;
-        if (nc <= 0) continue;
-        const int j0 = __ldg(cell_start + col + c0), j1 = __ldg(cell_start + col + c0 + nc);
-        for (int j = j0; j < j1; ++j) {
+  // the warp walks the (few) coarse columns in order, its lanes over each column's z run of
+  // candidates, hits compacted with a ballot: the list is in (column, slot) order
+  int cnt = 0;
+  for (int q = 0; q < nxc * nyc; ++q) {
+    const int ax = q / nyc, ay = q - ax * nyc;
+    const int ccx = (x0 + ax) % s.cnx, ccy = (y0 + ay) % s.cny;
+    const int col = (ccx * s.cny + ccy) * s.cnz;
+    for (int part = 0; part < 2; ++part) {
+      const int c0 = part == 0 ? z0 : 0, nc = part == 0 ? run1 : nzc - run1;
+      if (nc <= 0) continue;
+      const int t0 = __ldg(s.ccs + col + c0), t1 = __ldg(s.ccs + col + c0 + nc);
+      for (int tb = t0; tb < t1; tb += 32) {
+        const int tt = tb + lane;
+        bool hit = false;
+        int j = 0;
+        if (tt < t1) {
+          j = (int)__ldg(s.cperm + tt);
           const uint4 xj = s.xh[j];
           const float dx = (float)(int)(xi.x - xj.x) * g.scale[0];
           const float dy = (float)(int)(xi.y - xj.y) * g.scale[1];
           const float dz = (float)(int)(xi.z - xj.z) * g.scale[2];
           const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
           const float hj = __uint_as_float(xj.w);
-          if (r2 < fmaxf(Hi2, (Hfac * hj) * (Hfac * hj))) {
-            if (out && c < cap) out[c] = (uint32_t)j;
-            ++c;
-          }
+          hit = r2 < fmaxf(Hi2, (Hfac * hj) * (Hfac * hj));
         }
+        const unsigned b = __ballot_sync(kFull, hit);
+        const int pos = cnt + __popc(b & ((1u << lane) - 1u));
+        if (hit && pos < s.wlcap) lst[pos] = (uint32_t)j;
+        cnt += __popc(b);
       }
     }
-    return c;
-  };
-  const int mine = scan(nullptr, 0);
-  int incl = mine;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int v = __shfl_up_sync(kFull, incl, o);
-    if (lane >= o) incl += v;
   }
-  const int cnt = __shfl_sync(kFull, incl, 31);
-  const int off = incl - mine;
-  if (mine > 0 && off < s.wlcap) scan(lst + off, s.wlcap - off);
   if (lane == 0) {
     s.wcount[wi] = min(cnt, s.wlcap);
     s.hbuild[i] = hi;
@@ -265,9 +294,15 @@ __global__ void __launch_bounds__(256) k_wide_force(DevGrid g, DevPhys ph, DevSt
     const int cxj = cell_axis(xj.x, g.nx), cyj = cell_axis(xj.y, g.ny), czj = cell_axis(xj.z, g.nz);
     const bool jwide = s.wide[j] != 0;
     const float Rj = Hfac * s.hbuild[j];
-    const int kx = jwide ? reach(Rj, g.side[0], g.nx) : 1, ky = jwide ? reach(Rj, g.side[1], g.ny) : 1,
-              kz = jwide ? reach(Rj, g.side[2], g.nz) : 1;
-    const bool seen = within(cxi, cxj, kx, g.nx) && within(cyi, cyj, ky, g.ny) && within(czi, czj, kz, g.nz);
+    bool seen;
+    if (jwide) {  // j's search: the coarse cells meeting its grid-cell box (k_wide_lists)
+      const int kx = reach(Rj, g.side[0], g.nx), ky = reach(Rj, g.side[1], g.ny), kz = reach(Rj, g.side[2], g.nz);
+      const int F = s.cF;
+      seen = coarse_meets(cxi / F, cxj - kx, kx, g.nx, F) && coarse_meets(cyi / F, cyj - ky, ky, g.ny, F) &&
+             coarse_meets(czi / F, czj - kz, kz, g.nz, F);
+    } else {
+      seen = within(cxi, cxj, 1, g.nx) && within(cyi, cyj, 1, g.ny) && within(czi, czj, 1, g.nz);
+    }
     if (!seen && j != i) {
       // j's side of the pair (r_ji = -r_ij): the same symmetric terms, its own accumulators
       ForceAcc b{0.f, 0.f, 0.f, 0.f, 0.f, 0};
@@ -312,6 +347,14 @@ cudaError_t launch_mark_wide(int n, const DevGrid& g, const DevPhys& ph, const D
                              cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   k_mark_wide<<<(n + 255) / 256, 256, 0, st>>>(n, g, ph, s, flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_coarse_keys(int n, int i0, const DevGrid& g, const DevState& s, unsigned int* keys,
+                               unsigned int* vals, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  (void)i0;
+  k_coarse_keys<<<(n + 255) / 256, 256, 0, st>>>(n, g, s, keys, vals);
   return cudaGetLastError();
 }
 

@@ -290,6 +290,7 @@ struct sph_ctx {
   int* blk_list = nullptr;      // [nact] active block ids
   int* run_list = nullptr;      // [nrun] active indices of the blocks with a non-wide i particle
   size_t run_cap = 0;
+  int kz_hint = 0;              // KZ chosen at the last rebuild (first probe of the next)
   uint32_t* cperm = nullptr;    // wide search grid: particles in coarse-cell order
   size_t cperm_cap = 0;
   int* ccs = nullptr;           // its coarse cell starts
@@ -939,6 +940,7 @@ sph_status rebuild_impl(sph_ctx* c) {
     if (64.0 * slots + 32.0 * icnt > (double)kSmemTarget) break;
     KZ = k;
   }
+  if (c->kz_hint > 0 && c->kz_hint < KZ) KZ = c->kz_hint;  // (tiles rarely shrink between rebuilds)
   if (c->cfg.tile_cells_z > 0) KZ = c->cfg.tile_cells_z;
   KZ = std::max(1, std::min(KZ, kz_max));
   g.lists_warps = 8;  // (the largest k_lists CTA for the fit test)
@@ -984,6 +986,7 @@ sph_status rebuild_impl(sph_ctx* c) {
     }
     KZ = kz_lo == 0 ? std::max(1, kz_hi / 2) : (kz_lo + kz_hi) / 2;
   }
+  c->kz_hint = g.KZ;
   stage("KZ chosen");
   // the blocks with i particles, in block order: one loop CTA each (a clustered box on a fine
   // grid has mostly empty blocks)

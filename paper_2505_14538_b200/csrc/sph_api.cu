@@ -954,7 +954,10 @@ sph_status rebuild_impl(sph_ctx* c) {
     g.nzb = (g.nz + KZ - 1) / KZ;
     g.nblocks = g.nbx * g.nby * g.nzb;
     CK(cudaMemsetAsync(c->scratch + 6, 0, 8, c->stream));
-    CK(launch_tile_sizes(g, c->cell_start, (int*)(c->scratch + 6), (int*)(c->scratch + 7), c->stream));
+    // (the probe also flags the blocks with i particles: the last probe is at the chosen KZ)
+    if ((st = grow_h(c, &c->act_flag, c->act_cap, (size_t)g.nblocks)) != SPH_OK) return st;
+    CK(launch_tile_sizes(g, c->cell_start, (int*)(c->scratch + 6), (int*)(c->scratch + 7), c->act_flag,
+                         c->stream));
     c->launches++;
     CK(cudaMemcpyAsync(c->scratch_h + 6, c->scratch + 6, 8, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -990,10 +993,7 @@ sph_status rebuild_impl(sph_ctx* c) {
   stage("KZ chosen");
   // the blocks with i particles, in block order: one loop CTA each (a clustered box on a fine
   // grid has mostly empty blocks)
-  if ((st = grow_h(c, &c->act_flag, c->act_cap, (size_t)g.nblocks)) != SPH_OK) return st;
   if ((st = grow_h(c, &c->blk_list, c->list_cap, (size_t)g.nblocks)) != SPH_OK) return st;
-  CK(launch_block_active(g, c->cell_start, c->act_flag, c->stream));
-  c->launches++;
   {
     cub::CountingInputIterator<int> it(0);
     size_t need = 0;

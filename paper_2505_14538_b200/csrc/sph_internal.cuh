@@ -134,7 +134,8 @@ cudaError_t launch_gradient(const DevGrid& g, const DevPhys& ph, const DevState&
                             int first_step, DevCounters* ctr, cudaStream_t st);
 cudaError_t launch_force(const DevGrid& g, const DevPhys& ph, const DevState& s, const int* cell_start,
                          DevCounters* ctr, cudaStream_t st);
-cudaError_t launch_tile_sizes(const DevGrid& g, const int* cell_start, int* max_tile, int* max_i, cudaStream_t st);
+cudaError_t launch_tile_sizes(const DevGrid& g, const int* cell_start, int* max_tile, int* max_i, uint8_t* flag,
+                              cudaStream_t st);
 size_t lists_smem(const DevGrid& g);
 size_t density_smem(const DevGrid& g);
 size_t gradient_smem(const DevGrid& g);
@@ -157,7 +158,6 @@ int kernel_threads();
 size_t tile_desc_bytes();  // descriptor + per-cell table, per block
 size_t tile_desc_header_bytes();  // the descriptor alone
 cudaError_t launch_tile_desc(const DevGrid& g, const int* cell_start, cudaStream_t st);
-cudaError_t launch_block_active(const DevGrid& g, const int* cell_start, uint8_t* flag, cudaStream_t st);
 cudaError_t launch_block_run(const DevGrid& g, const DevState& s, uint8_t* flag, cudaStream_t st);
 
 }  // namespace sph

@@ -1250,11 +1250,14 @@ __device__ void block_counts(const DevGrid& g, const int* __restrict__ cell_star
 }
 
 // per-block tile size and i count (max over blocks) -> sizes shared memory of the loops
-__global__ void k_tile_sizes(DevGrid g, const int* __restrict__ cell_start, int* max_tile, int* max_i) {
+// (and, with `flag`, which blocks have i particles: the active-block flags of this grid)
+__global__ void k_tile_sizes(DevGrid g, const int* __restrict__ cell_start, int* max_tile, int* max_i,
+                             uint8_t* flag) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= g.nblocks) return;
   int tot, ni;
   block_counts(g, cell_start, b, tot, ni);
+  if (flag) flag[b] = ni > 0 ? 1 : 0;
   if (tot) atomicMax(max_tile, tot);
   if (ni) atomicMax(max_i, ni);
 }
@@ -1273,14 +1276,6 @@ __global__ void k_block_run(DevGrid g, DevState s, uint8_t* flag) {
   flag[a] = (uint8_t)run;
 }
 
-// blocks with i particles (the others launch no loop CTA)
-__global__ void k_block_active(DevGrid g, const int* __restrict__ cell_start, uint8_t* flag) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= g.nblocks) return;
-  int tot, ni;
-  block_counts(g, cell_start, b, tot, ni);
-  flag[b] = ni > 0 ? 1 : 0;
-}
 
 }  // namespace
 
@@ -1300,11 +1295,6 @@ cudaError_t launch_block_run(const DevGrid& g, const DevState& s, uint8_t* flag,
   return cudaGetLastError();
 }
 
-cudaError_t launch_block_active(const DevGrid& g, const int* cell_start, uint8_t* flag, cudaStream_t st) {
-  k_block_active<<<(g.nblocks + 255) / 256, 256, 0, st>>>(g, cell_start, flag);
-  return cudaGetLastError();
-}
-
 size_t lists_smem(const DevGrid& g) {
   const int nw = g.lists_warps > 0 ? g.lists_warps : kNW;
   return (size_t)((g.tcap + kNSent + 1) & ~1) * 16 + lists_ring_bytes(g, nw) + lists_zw_bytes(g);
@@ -1315,8 +1305,9 @@ size_t force_smem(const DevGrid& g) {
   return force_records_bytes(g.tcap) + walk_bytes<ForceAcc>(g.icap, g.force_threads > 0 ? g.force_threads : kNW * 32);
 }
 
-cudaError_t launch_tile_sizes(const DevGrid& g, const int* cell_start, int* max_tile, int* max_i, cudaStream_t st) {
-  k_tile_sizes<<<(g.nblocks + 255) / 256, 256, 0, st>>>(g, cell_start, max_tile, max_i);
+cudaError_t launch_tile_sizes(const DevGrid& g, const int* cell_start, int* max_tile, int* max_i, uint8_t* flag,
+                              cudaStream_t st) {
+  k_tile_sizes<<<(g.nblocks + 255) / 256, 256, 0, st>>>(g, cell_start, max_tile, max_i, flag);
   return cudaGetLastError();
 }
 

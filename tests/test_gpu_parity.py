@@ -29,6 +29,8 @@ def _cases():
         "clustered8k": lambda: W.clustered(8192, seed=77),
         # particles in 6 % of the box: most blocks empty (compacted block list)
         "blob4096": lambda: W.blob(4096),
+        # a ragged count: no multiple of the warp, the 8-entry list rows or the block shape
+        "poisson999": lambda: W.poisson(999, seed=29, vel_sigma=0.1, u_sigma=0.3),
     }
 
 
@@ -61,7 +63,8 @@ def test_density_fixed_h(case):
     assert g["stats"]["pairs_density"] == int(d["count"].sum())
 
 
-@pytest.mark.parametrize("case", ["lattice16", "jitter16", "poisson4096", "sod16", "gresho24j", "sedov24", "blob4096"])
+@pytest.mark.parametrize("case", ["lattice16", "jitter16", "poisson4096", "sod16", "gresho24j", "sedov24", "blob4096",
+                                  "poisson999"])
 def test_full_pass_fixed_h(case):
     """Density -> finalize -> gradient (+ghost) -> force -> dt at the given h."""
     p = _with_switches(_cases()[case](), 5)
@@ -193,6 +196,18 @@ def test_box_too_small_is_an_error():
     p = W.lattice(4, h_factor=1.0)
     with pytest.raises(SphError):
         Context(p)
+
+
+def test_empty_input_is_an_error():
+    """A single-rank context without particles is a usage error (SPH_ERR_INVALID_ARG), not a
+    silent no-op; one particle alone cannot close the h iteration (NOT_CONVERGED, above)."""
+    from paper_2505_14538_b200 import Context, SphError
+
+    p = W.poisson(64, seed=3)
+    q = {k: (v[:0] if isinstance(v, np.ndarray) and v.shape[:1] == (64,) else v) for k, v in p.items()}
+    with pytest.raises(SphError) as e:
+        Context(q)
+    assert e.value.status == 1
 
 
 def test_adaptive_grid_has_wide_particles():

@@ -64,6 +64,7 @@ def parse():
     ap.add_argument("--cpu-sample", default="G64", choices=sorted(WORKLOADS))
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--tile-z", type=int, default=0, help="cells per CTA block along z (0 = auto)")
+    ap.add_argument("--skin", type=float, default=None, help="cell_skin (default: the library's)")
     return ap.parse_args()
 
 
@@ -235,6 +236,8 @@ def run_ours(args, world, rank, local):
         multi = dict(rank=rank, nranks=world, n_total=n_total, nccl_uid=uid)
     if args.tile_z:
         multi["tile_cells_z"] = args.tile_z
+    if args.skin is not None:
+        multi["cell_skin"] = args.skin
     ctx = Context(p, stream=stream.cuda_stream, device=local, **multi)
     dt = 1e-4
 

@@ -307,13 +307,16 @@ __device__ __forceinline__ int blk_a(const DevGrid& g) { return g.run_list ? g.r
 // (1 + skin) of its value here (checked by the density epilogue).
 // One lane per particle i, each walking its OWN candidates: in each of the 3 x 3 tile
 // columns around i's column, only the slots with |z_j - z_i| <= R (R = the largest list
-// radius in the tile), found by binary search -- each cell's particles are sorted by z up
-// to one bucket of zbucket (the z bits of the sort key), so the window is exact up to that
-// bucket, which is added to R.  This tests ~2R/(3 side) of the 27-cell candidates.
+// radius in the tile, plus the sort bucket and rounding slack), rounded out to 1/16-cell
+// sub-buckets: each cell's particles are sorted by the top z bits of the sort key, so a
+// per-block table of each sub-bucket's first slot (s_zw) gives both window ends with two
+// loads.  This tests ~2R/(3 side) of the 27-cell candidates.
 // The tile is staged pair-interleaved, P[8p .. 8p+7] = (x_2p, x_2p+1, y_2p, y_2p+1, z_2p,
 // z_2p+1, H2_2p, H2_2p+1), so one lane tests two consecutive candidates with two LDS.128
 // and packed f32x2 arithmetic (FADD2 / FMUL2 / FFMA2).  Hits go to a per-lane column of a
-// per-warp buffer in shared memory and leave for global memory 8 at a time (16-byte stores).
+// per-warp buffer in shared memory and leave for global memory 8 at a time (16-byte stores);
+// k_bank then lays each list out in bank-aware rows.  The CTA has about one warp per 32 of
+// the mean block's particles (DevGrid::lists_warps).
 __device__ void block_exclusive_scan(int* a, int n);
 constexpr int kMaxICells = kMaxICols * (kMaxTileCellsZ - 2);
 constexpr int kListRows = 32;  // ring rows per lane (<= 7 left + 2 single tests + 16 per group)

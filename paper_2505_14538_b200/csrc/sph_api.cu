@@ -8,10 +8,10 @@
 // [r nx/R, (r+1) nx/R) along x; the planes on either side are ghost planes received from the
 // neighbours (cell side >= (1+skin) max H, so one plane is the whole halo).  The local grid
 // has P + 2 planes along x (ghost, owned..., ghost) and is periodic in y and z.
+#include <thrust/iterator/counting_iterator.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
-#include <cub/iterator/counting_input_iterator.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -995,7 +995,7 @@ sph_status rebuild_impl(sph_ctx* c) {
   // grid has mostly empty blocks)
   if ((st = grow_h(c, &c->blk_list, c->list_cap, (size_t)g.nblocks)) != SPH_OK) return st;
   {
-    cub::CountingInputIterator<int> it(0);
+    thrust::counting_iterator<int> it(0);
     size_t need = 0;
     int* nact_dev = reinterpret_cast<int*>(c->scratch + 12);
     CK(cub::DeviceSelect::Flagged(nullptr, need, it, c->act_flag, c->blk_list, nact_dev, g.nblocks, c->stream));
@@ -1095,7 +1095,7 @@ sph_status mark_wide(sph_ctx* c) {
   }
   CK(launch_mark_wide(n, c->grid, c->phys, s, c->wide_flag, c->stream));
   c->launches++;
-  cub::CountingInputIterator<int> it(0);
+  thrust::counting_iterator<int> it(0);
   size_t need = 0;
   CK(cub::DeviceSelect::Flagged(nullptr, need, it, c->wide_flag, c->widx, c->n_wide_dev, n, c->stream));
   if (need > c->sel_tmp_bytes) {

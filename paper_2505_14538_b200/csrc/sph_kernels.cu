@@ -206,16 +206,6 @@ __device__ __forceinline__ void i_slot(const SS& S, int li, int& ti, int& gi) {
   gi = S.g0[k] + (li - S.pre[k]);
 }
 
-// tile slot -> global particle index (binary search over the cell table; rare path)
-__device__ __forceinline__ int slot_global(const BlockShared& S, int nct, int t) {
-  int lo = 0, hi = nct;
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (S.off[mid] <= t) lo = mid; else hi = mid;
-  }
-  return S.gst[lo] + (t - S.off[lo]);
-}
-
 // tile slot -> global particle index from the staged segments (rare path)
 __device__ __forceinline__ int slot_global(const TileDesc& D, int nseg, int t) {
   for (int k = 0; k < nseg; ++k) {

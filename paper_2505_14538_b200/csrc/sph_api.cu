@@ -940,7 +940,10 @@ sph_status rebuild_impl(sph_ctx* c) {
     if (64.0 * slots + 32.0 * icnt > (double)kSmemTarget) break;
     KZ = k;
   }
-  if (c->kz_hint > 0 && c->kz_hint < KZ) KZ = c->kz_hint;  // (tiles rarely shrink between rebuilds)
+  // the last rebuild's KZ is only a first probe: one above it (tiles may have shrunk since), then
+  // the hint itself if that does not fit, then a bisection below
+  const int hint = (c->kz_hint > 0 && c->kz_hint < KZ) ? c->kz_hint : 0;
+  if (hint) KZ = hint + 1;
   if (c->cfg.tile_cells_z > 0) KZ = c->cfg.tile_cells_z;
   KZ = std::max(1, std::min(KZ, kz_max));
   g.lists_warps = 8;  // (the largest k_lists CTA for the fit test)
@@ -987,7 +990,7 @@ sph_status rebuild_impl(sph_ctx* c) {
       KZ = kz_lo;              // re-probe the answer so g holds its sizes
       continue;
     }
-    KZ = kz_lo == 0 ? std::max(1, kz_hi / 2) : (kz_lo + kz_hi) / 2;
+    KZ = kz_lo == 0 ? (hint && hint < kz_hi ? hint : std::max(1, kz_hi / 2)) : (kz_lo + kz_hi) / 2;
   }
   c->kz_hint = g.KZ;
   stage("KZ chosen");
@@ -1053,6 +1056,8 @@ sph_status rebuild_impl(sph_ctx* c) {
   c->stale = false;
   c->lists_stale = true;
   c->dvc_valid = false;
+  // the particles were re-sorted: every per-particle result of the loops is in the old order
+  c->density_done = c->gradient_done = false;
   return SPH_OK;
 }
 
@@ -1445,7 +1450,8 @@ sph_status sph_density(sph_ctx* c, sph_density_stats* stats) {
 
 sph_status sph_gradient(sph_ctx* c, float dt) {
   GUARD(c);
-  if (!c->density_done) return fail(c, SPH_ERR_STATE, "sph_gradient needs a completed sph_density");
+  if (!c->density_done || c->stale || c->lists_stale)
+    return fail(c, SPH_ERR_STATE, "sph_gradient needs a completed sph_density on the current cells");
   if (!(dt > 0.f) || !std::isfinite(dt)) return fail(c, SPH_ERR_INVALID_ARG, "sph_gradient: dt must be > 0 (S:246)");
   sph_status st;
   if ((st = reset_ctr(c)) != SPH_OK) return st;
@@ -1466,7 +1472,8 @@ sph_status sph_gradient(sph_ctx* c, float dt) {
 
 sph_status sph_force(sph_ctx* c, float* dt_next) {
   GUARD(c);
-  if (!c->gradient_done) return fail(c, SPH_ERR_STATE, "sph_force needs a completed sph_gradient");
+  if (!c->gradient_done || c->stale || c->lists_stale)
+    return fail(c, SPH_ERR_STATE, "sph_force needs a completed sph_gradient on the current cells");
   sph_status st;
   if ((st = reset_ctr(c)) != SPH_OK) return st;
   unsigned int inf_bits = 0x7f800000u;

@@ -404,6 +404,7 @@ sph_status alloc_state(sph_ctx* c) {
   CK(dalloc(&s.ncount, n)); CK(dalloc(&s.hbuild, n));
   CK(cudaMemset(s.ncount, 0, n * sizeof(int32_t)));  // k_lists reads it as a length hint
   CK(dalloc(&s.nbr, n * (size_t)c->lcap));
+  CK(dalloc(&s.nbr_raw, n * (size_t)c->lcap));
   c->nbr_cap = n * (size_t)c->lcap;
   CK(dalloc(&c->keys, n)); CK(dalloc(&c->keys_alt, n)); CK(dalloc(&c->perm, n)); CK(dalloc(&c->perm_alt, n));
   CK(dalloc(&c->ctr, 1));
@@ -974,7 +975,7 @@ sph_status rebuild_impl(sph_ctx* c) {
     g.force_threads = 256;
     if (force_smem(g) > kSmemTarget) g.force_threads = 512;
     const bool fits = force_smem(g) <= kSmemMax && lists_smem(g) <= kSmemMax && density_smem(g) <= kSmemMax &&
-                      gradient_smem(g) <= kSmemMax && g.tcap < 65520;
+                      gradient_smem(g) <= kSmemMax && g.tcap < 32760;  // (list entries: 15-bit slots)
     const bool ok = fits && (force_smem(g) <= kSmemTarget || KZ == 1);
     if (fits && c->cfg.tile_cells_z > 0) break;
     if (!probing && ok) break;  // the estimate fits
@@ -1039,8 +1040,9 @@ sph_status rebuild_impl(sph_ctx* c) {
   if ((st = grow_h(c, &c->desc_buf, c->desc_cap, na * tile_desc_bytes())) != SPH_OK) return st;
   g.desc = c->desc_buf;
   g.desc_cells = c->desc_buf + na * tile_desc_header_bytes();
-  if ((st = grow_h(c, &c->pref_buf, c->pref_cap, na * (g.icap + 1))) != SPH_OK) return st;
+  if ((st = grow_h(c, &c->pref_buf, c->pref_cap, 2 * na * (g.icap + 1))) != SPH_OK) return st;
   g.desc_pref = c->pref_buf;
+  g.desc_prefF = c->pref_buf + na * (g.icap + 1);
   CK(launch_tile_desc(g, c->cell_start, c->stream));
   c->launches++;
   const size_t blk_old = c->blk_cap;
@@ -1229,8 +1231,10 @@ sph_status build_lists(sph_ctx* c) {
     size_t want = (size_t)c->cap * c->lcap;
     if (want > c->nbr_cap) {
       cudaFree(c->s.nbr);
-      c->s.nbr = nullptr;
+      cudaFree(c->s.nbr_raw);
+      c->s.nbr = c->s.nbr_raw = nullptr;
       CK(dalloc(&c->s.nbr, want));
+      CK(dalloc(&c->s.nbr_raw, want));
       c->nbr_cap = want;
     }
   }
@@ -1480,10 +1484,13 @@ sph_status sph_force(sph_ctx* c, float* dt_next) {
   CK(cudaMemcpyAsync(&c->ctr->dt_bits, &inf_bits, 4, cudaMemcpyHostToDevice, c->stream));
   {
     Timed tm(c, SPH_T_FORCE);
+    // the pair-once loop adds both sides of every pair into acc (ghost slots included)
+    CK(cudaMemsetAsync(c->s.acc, 0, sizeof(float4) * (size_t)(c->gL + c->n_own + c->gR), c->stream));
     CK(launch_force(c->grid, c->phys, c->s, c->cell_start, c->ctr, c->stream));
     CK(launch_wide_force(c->grid, c->phys, c->s, c->ctr, c->stream));
+    CK(launch_force_fin(c->gL, c->n_own, c->phys, c->s, c->ctr, c->stream));
   }
-  c->launches += 1 + (c->s.n_wide > 0 ? 2 : 0);
+  c->launches += 2 + (c->s.n_wide > 0 ? 2 : 0);
   if ((st = sync_ctr(c)) != SPH_OK) return st;
   c->counters.pairs_force = (int64_t)c->ctr_h->pairs;
   float dt;
@@ -1648,7 +1655,7 @@ sph_status sph_destroy(sph_ctx* c) {
   DevState& s = c->s;
   void* ptrs[] = {s.xh, s.vm, s.u, s.av, s.ac, s.dprev, s.uid, s.orig, s.acc, c->alt.xh, c->alt.vm, c->alt.u,
                   c->alt.av, c->alt.ac, c->alt.dprev, c->alt.uid, c->alt.orig, c->alt.acc, s.dens, s.dvc, s.count,
-                  s.fin, s.gq, s.hlo, s.hhi, s.iters, s.active, s.grad, s.fr1, s.fr2, s.vsig, s.countf, s.nbr,
+                  s.fin, s.gq, s.hlo, s.hhi, s.iters, s.active, s.grad, s.fr1, s.fr2, s.vsig, s.countf, s.nbr, s.nbr_raw,
                   s.ncount, s.hbuild, c->cell_start, c->keys, c->keys_alt, c->perm, c->perm_alt, c->sort_tmp,
                   c->blk[0], c->blk[1], c->ctr, c->scratch, c->out_tmp, c->mig_send, c->mig_recv, c->pc_send,
                   c->pc_recv, c->pc_scan, c->scan_tmp, c->cnt_dev, c->wide_flag, c->widx, c->wcount,

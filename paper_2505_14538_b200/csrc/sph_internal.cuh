@@ -41,6 +41,7 @@ struct DevGrid {
   const void* desc;   // [nblocks] tile descriptors (sph_kernels.cu TileDesc, k_tile_desc)
   const void* desc_cells;  // [nblocks][kMaxTileCells + 1] per tile cell (tile offset, global start)
   int* desc_pref;     // [nblocks][icap + 1] list-group prefix of the block's particles (k_lists)
+  int* desc_prefF;    // [nblocks][icap + 1] the same over the force part of each list (k_lists)
   float scale[3];     // L_a / 2^32 as f32 (fixed point -> length)
   double dscale[3];   // L_a * 2^-32 exact (fp64 exact neighbour test)
   float side[3];      // cell side per axis
@@ -91,11 +92,15 @@ struct DevState {
   float4* acc;        // a, du
   float* vsig;
   int32_t* countf;
-  // neighbour lists: tile-relative uint16 slots padded with sentinel slots (tcap .. tcap+7) to
-  // a multiple of 8, in ROWS of 8 whose entry w lies in shared-memory bank group w (slot mod 8;
-  // k_bank, sph_kernels.cu); [n][lcap]
+  // neighbour lists: tile-relative uint16 slots in two parts, each padded with sentinel slots
+  // (tcap .. tcap+7) to a multiple of 8 and laid out in ROWS of 8 whose entry w lies in
+  // shared-memory bank group w (slot mod 8; k_bank, sph_kernels.cu); [n][lcap]:
+  //   rows [0, nF8)          the FORCE part: the pairs this particle evaluates once for both sides
+  //                          (partner in the "upper" half of the cell stencil, or a ghost)
+  //   rows [nF8, nF8 + nL8)  the rest (self included): density and gradient walk both parts
   uint16_t* nbr;
-  int32_t* ncount;    // padded list length (multiple of 8)
+  uint16_t* nbr_raw;  // k_lists' output before k_bank: natural order, bit 15 = force part
+  int32_t* ncount;    // nF | nL << 16: real entries of the two parts (k_lists)
   float* hbuild;      // h when the list was built
   // wide particles (adaptive cell side, sph_wide.cu): support past the cell side; nullptr /
   // 0 when there are none
@@ -134,6 +139,7 @@ cudaError_t launch_gradient(const DevGrid& g, const DevPhys& ph, const DevState&
                             int first_step, DevCounters* ctr, cudaStream_t st);
 cudaError_t launch_force(const DevGrid& g, const DevPhys& ph, const DevState& s, const int* cell_start,
                          DevCounters* ctr, cudaStream_t st);
+cudaError_t launch_force_fin(int i0, int n, const DevPhys& ph, const DevState& s, DevCounters* ctr, cudaStream_t st);
 cudaError_t launch_tile_sizes(const DevGrid& g, const int* cell_start, int* max_tile, int* max_i, uint8_t* flag,
                               cudaStream_t st);
 size_t lists_smem(const DevGrid& g);

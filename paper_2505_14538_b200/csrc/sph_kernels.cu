@@ -238,23 +238,50 @@ __device__ __forceinline__ uint32_t smem_base(int rec) {
   return a;
 }
 
-// Stage nrec16 16-byte per-particle records (at smem4[o16[r] + slot]) and optionally one
-// 4-byte record (at float offset o4) of every tile slot with cp.async: no register round
-// trip, every copy of the CTA in flight at once.
+// The tile staging's mbarrier (one per CTA, used once: phase 0).  Thread 0 initialises it
+// before the kernel's first barrier (stage_mbar_init), stage_records waits on it.
+__shared__ __align__(8) unsigned long long s_stage_mbar;
+__device__ __forceinline__ uint32_t stage_mbar() { return (uint32_t)__cvta_generic_to_shared(&s_stage_mbar); }
+__device__ __forceinline__ void stage_mbar_init() {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n"
+               "fence.mbarrier_init.release.cluster;" ::"r"(stage_mbar())
+               : "memory");
+}
+
+// Stage nrec16 16-byte per-particle records (at smem4[o16[r] + slot]) of every tile slot:
+// each of the tile's contiguous segments (<= 3 per tile column, TileDesc::seg) is one 1-D
+// bulk copy per record array (cp.async.bulk on the TMA engine, no per-lane loop), counted in
+// bytes on the CTA's mbarrier (armed by thread 0 before the copies, __syncthreads of the
+// prologue); lane 0 of every warp issues a share of them (the copies of one lane issue one
+// after another).  Every thread then waits on the mbarrier (and on its own earlier cp.async
+// copies), and the block synchronises.
 template <class SS>
 __device__ __forceinline__ void stage_records(const SS& S, int nseg, int nrec16, const float4* const* src16,
-                                              const int* o16, const float* src4, int o4) {
-  float* sm1 = reinterpret_cast<float*>(smem4);
-  // one warp per segment (segments are ~1-3 cells long): no block-wide pass over all of them
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int k = warp; k < nseg; k += nw) {
-    const int4 sg = S.seg[k];
-    for (int t = lane; t < sg.z; t += 32) {
-      for (int r = 0; r < nrec16; ++r) cp_async16(&smem4[o16[r] + sg.x + t], src16[r] + sg.y + t);
-      if (src4) cp_async4(&sm1[o4 + sg.x + t], src4 + sg.y + t);
+                                              const int* o16, int ntile) {
+  const uint32_t mbar = stage_mbar();
+  if (threadIdx.x == 0)
+    asm volatile("{ .reg .b64 st; mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1; }" ::"r"(mbar),
+                 "r"((uint32_t)(nrec16 * 16 * ntile))
+                 : "memory");
+  __syncthreads();
+  {
+    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5, warp = threadIdx.x >> 5;
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem4);
+    // copy c = (segment, record) of the CTA's nseg * nrec16: lane (c / nw) % 32 of warp c % nw
+    for (int c = warp + nw * lane; c < nseg * nrec16; c += 32 * nw) {
+      const int k = c % nseg, r = c / nseg;
+      const int4 sg = S.seg[k];
+      if (sg.z <= 0) continue;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              sbase + 16u * (uint32_t)(o16[r] + sg.x)),
+          "l"(src16[r] + sg.y), "r"(16u * (uint32_t)sg.z), "r"(mbar)
+          : "memory");
     }
   }
   cp_async_wait_all();
+  asm volatile("{ .reg .pred p; W%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0; @!p bra W%=; }" ::"r"(mbar)
+               : "memory");
   __syncthreads();
 }
 
@@ -280,6 +307,7 @@ __device__ __forceinline__ int blk_a(const DevGrid& g) { return g.run_list ? g.r
     const int* src_ = reinterpret_cast<const int*>(g.desc) + (size_t)ba * (sizeof(TileDesc) / 4); \
     int* dst_ = reinterpret_cast<int*>(&S);                                      \
     for (int q_ = threadIdx.x; q_ < (int)(sizeof(TileDesc) / 4); q_ += blockDim.x) dst_[q_] = __ldg(src_ + q_); \
+    if (threadIdx.x == 0) stage_mbar_init();                                     \
   }                                                                              \
   __syncthreads();                                                               \
   const Tile T = S.T;                                                            \
@@ -315,12 +343,12 @@ constexpr int kZSub = 16;      // z sub-buckets per cell in k_lists' window tabl
 // k_lists' dynamic shared memory after the pair array: the per-warp list rings and the group
 // counts (holding one z sub-bucket byte per slot before the walk), then the z window table
 __host__ __device__ __forceinline__ size_t lists_ring_bytes(const DevGrid& g, int nw) {
-  const size_t ring = (size_t)nw * kListRows * 32 * 2 + (size_t)(g.icap + 1) * 4;
+  const size_t ring = (size_t)nw * kListRows * 32 * 2 + (size_t)(g.icap + 1) * 8;
   const size_t zsb = (size_t)g.tcap + 16;
   return ((ring > zsb ? ring : zsb) + 15) & ~(size_t)15;
 }
 __host__ __device__ __forceinline__ size_t lists_zw_bytes(const DevGrid& g) {
-  return ((size_t)(g.bx + 2) * (g.by + 2) * (g.KZ + 2) * kZSub + 1) * 2;
+  return ((((size_t)(g.bx + 2) * (g.by + 2) * (g.KZ + 2) * kZSub + 1) * 2 + 15) & ~(size_t)15);
 }
 // (the per-lane list buffers are touched only through these volatile asm statements, which
 // keep their order; no memory clobber, so the compiler may move tile loads across them)
@@ -336,6 +364,10 @@ __device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
   asm volatile("ld.shared.u16 %0, [%1];\n" : "=h"(v) : "r"(a));
   return v;
 }
+// kTag: tag each entry as it leaves the ring (wide particles or ghost planes present); else the
+// list is sorted by slot and its force part is simply its tail (position >= the count of
+// entries up to the particle's own slot).
+template <bool kWide, bool kTag>
 __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, DevState s,
                                                        const int* __restrict__ cell_start,
                                                        DevCounters* __restrict__ ctr) {
@@ -366,6 +398,7 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
       S.off[c] = v.x;
       if (c < nct) S.gst[c] = v.y;
     }
+    if (threadIdx.x == 0) stage_mbar_init();
   }
   __syncthreads();
   const Tile T = Tsh;
@@ -375,17 +408,27 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
   }
   const int nseg = 3 * T.ntc;
   const int SP = g.tcap + kNSent;
-  {
-    const float4* src[1] = {reinterpret_cast<const float4*>(s.xh)};
-    const int o16[1] = {0};
-    stage_records(S, nseg, 1, src, o16, nullptr, 0);
-  }
   const int NP = (SP + 1) >> 1;  // slot pairs
   float* P = reinterpret_cast<float*>(smem4);
   // z window table: s_zw[16 c + k] = first slot of tile cell c in z sub-bucket >= k (16 per
   // cell, the top 4 z bits inside the cell -- the sort key's, so exact), s_zw[16 nct] = end
   unsigned short* s_zw = reinterpret_cast<unsigned short*>(reinterpret_cast<char*>(P) + (size_t)NP * 32 +
                                                            lists_ring_bytes(g, nw));
+  // wide particles (adaptive grid): one flag byte per slot after the window table (a wide
+  // partner's pair is never in the force part: k_wide_force applies it to both sides)
+  unsigned char* wfl = reinterpret_cast<unsigned char*>(s_zw) + lists_zw_bytes(g);
+  if (kWide) {
+    const int lane_ = threadIdx.x & 31;
+    for (int k = threadIdx.x >> 5; k < nseg; k += nw) {
+      const int4 sg = S.seg[k];
+      for (int t = lane_; t < sg.z; t += 32) wfl[sg.x + t] = s.wide[sg.y + t];
+    }
+  }
+  {
+    const float4* src[1] = {reinterpret_cast<const float4*>(s.xh)};
+    const int o16[1] = {0};
+    stage_records(S, nseg, 1, src, o16, T.ntile);
+  }
   const float Hfac = (1.f + g.skin) * ph.gamma_k;
   unsigned int hm = 0u;
   // each slot's z sub-bucket (bytes; the region of the list ring, not yet in use)
@@ -463,9 +506,19 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
   // entries leave 8 at a time from 512-byte aligned ring positions, nothing is moved
   const uint32_t buf = sP + (uint32_t)NP * 32u + (uint32_t)(warp * kListRows * 32 + lane) * 2u;
   int* grp = reinterpret_cast<int*>(reinterpret_cast<char*>(P) + (size_t)NP * 32 + (size_t)nw * kListRows * 32 * 2);
+  int* grpF = grp + (g.icap + 1);  // force-part groups
   constexpr uint32_t kRing = kListRows * 64u;
   const int ni = s_cp[nicell];
   int over = 0;
+  // slots of the slab's ghost planes (several ranks): the tile's x-columns outside the owned
+  // planes, [0, gLo) and [gHi, ...)
+  int gLo = 0, gHi = 0x7fffffff;
+  if (!g.periodic_x) {
+    const int colx = (g.by + 2) * T.nzt;  // tile cells per tile x-column
+    if (T.ix0 == g.ix_first) gLo = S.off[colx];
+    const int xr = g.ix_first + g.nxo - T.ix0 + 1;  // first tile x-column past the owned planes
+    if (xr <= g.bx + 1) gHi = S.off[xr * colx];
+  }
   for (int c = warp; c * 32 < ni; c += nw) {
     const int k = c * 32 + lane;
     bool valid = k < ni;
@@ -485,14 +538,29 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
     const float Hi2 = pi[6];
     const int tc = S.tc[col];
     const float zc = zbound(T.z0 + zz - 2);  // bottom of tile cell zz - 1
-    uint4* dst = reinterpret_cast<uint4*>(s.nbr + (size_t)gi * g.lcap);
-    if (valid && s.wide && s.wide[gi]) {  // a wide particle's list is built by k_wide_lists
+    uint4* dst = reinterpret_cast<uint4*>(s.nbr_raw + (size_t)gi * g.lcap);
+    if (valid && kWide && s.wide[gi]) {  // a wide particle's list is built by k_wide_lists
       s.ncount[gi] = 0;
       valid = false;
     }
-    int mygrp = 0;             // list groups of this lane's particle (0: none / wide)
+    int mygrp = 0, mygrpF = 0;  // list groups of this lane's particle, all / force part (0: none / wide)
     uint32_t w = 0u, rd = 0u;  // ring byte offsets: next write, next flush
     int flushed = 0;           // entries already in global memory
+    uint32_t nF2 = 0u;         // force-part entries flushed (two 16-bit halves)
+    // Force part (bit 15, set as the entries leave the ring): each unordered pair is evaluated
+    // once, by the particle whose partner has the later tile slot.  Tile columns run in the
+    // order of their (x, y) cell offsets and each column in z order, so "later slot" is "the
+    // partner's cell lies in the upper half of the 3x3x3 stencil (minimum-image cell offset
+    // lexicographically positive), or the same cell and a later global index": the same
+    // decision seen from either particle's block, whatever the periodic wraps.  A ghost partner
+    // (slot outside [gLo, gHi)) is always in it: the other rank evaluates its own side.
+    const uint32_t uti = (uint32_t)ti;
+    auto ftag = [&](uint32_t t) -> uint32_t {
+      if (!kTag) return t;
+      bool f = t < (uint32_t)g.tcap && (t > uti || t < (uint32_t)gLo || t >= (uint32_t)gHi);
+      if (kWide) f = f && !wfl[t];
+      return f ? 0x8000u | t : t;
+    };
     auto hit = [&](bool h, int t) {
       if (h) {
         sts_u16(buf + w, (uint32_t)t);
@@ -510,11 +578,14 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
         if (flushed + 8 <= g.lcap) {
           const uint32_t r = buf + rd;
           uint4 v;
-          v.x = lds_u16(r + 0 * 64) | (lds_u16(r + 1 * 64) << 16);
-          v.y = lds_u16(r + 2 * 64) | (lds_u16(r + 3 * 64) << 16);
-          v.z = lds_u16(r + 4 * 64) | (lds_u16(r + 5 * 64) << 16);
-          v.w = lds_u16(r + 6 * 64) | (lds_u16(r + 7 * 64) << 16);
+          v.x = ftag(lds_u16(r + 0 * 64)) | (ftag(lds_u16(r + 1 * 64)) << 16);
+          v.y = ftag(lds_u16(r + 2 * 64)) | (ftag(lds_u16(r + 3 * 64)) << 16);
+          v.z = ftag(lds_u16(r + 4 * 64)) | (ftag(lds_u16(r + 5 * 64)) << 16);
+          v.w = ftag(lds_u16(r + 6 * 64)) | (ftag(lds_u16(r + 7 * 64)) << 16);
           dst[flushed >> 3] = v;
+          if (kTag)
+            nF2 += ((v.x >> 15) & 0x10001u) + ((v.y >> 15) & 0x10001u) + ((v.z >> 15) & 0x10001u) +
+                   ((v.w >> 15) & 0x10001u);
         }
         rd = (rd + 8u * 64u) & (kRing - 1u);
         flushed += 8;
@@ -525,20 +596,14 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
     const float ulo = (zi - zpad - zc) * sub_scale - 0.01f, uhi = (zi + zpad - zc) * sub_scale + 0.01f;
     const int klo = (int)(min(max(floorf(ulo), 0.f), (float)(3 * kZSub))) & ~(int)zmask;
     const int khi = (((int)(min(max(ceilf(uhi), 0.f), (float)(3 * kZSub))) - 1) | (int)zmask) + 1;
-    if (valid) {
-#pragma unroll 1
-      for (int d = 0; d < 9; ++d) {
-        const int tcol = tc + (d / 3 - 1) * (g.by + 2) + (d % 3 - 1);
-        const int cb = tcol * T.nzt + zz;
-        // every slot of the 3 window cells with |z - zi| <= zpad lies in [a, e): the table
-        // rows are the cells' sub-bucket starts, consecutive down the tile column
-        int a = s_zw[(cb - 1) * kZSub + klo];
-        int e = s_zw[(cb - 1) * kZSub + khi];
-        if (a >= e) continue;
-        if (a & 1) test_one(a++);
-        if ((e - a) & 1) test_one(--e);
-        drain();
-        for (int p0 = a >> 1; p0 < (e >> 1); p0 += 8) {
+    int c1 = 0;  // (!kTag) entries with a slot <= ti: the part outside the force loop
+    // one window [a, e) of a tile column, in slot order
+    auto scan = [&](int a, int e) {
+      if (a >= e) return;
+      if (a & 1) test_one(a++);
+      if ((e - a) & 1) test_one(--e);
+      drain();
+      for (int p0 = a >> 1; p0 < (e >> 1); p0 += 8) {
           const int pn = min(e >> 1, p0 + 8);
 #pragma unroll 4
           for (int pp = p0; pp < pn; ++pp) {
@@ -555,19 +620,47 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
           }
           drain();
         }
+    };
+    if (valid) {
+#pragma unroll 1
+      for (int d = 0; d < 9; ++d) {
+        const int tcol = tc + (d / 3 - 1) * (g.by + 2) + (d % 3 - 1);
+        const int cb = tcol * T.nzt + zz;
+        // every slot of the 3 window cells with |z - zi| <= zpad lies in [a, e): the table
+        // rows are the cells' sub-bucket starts, consecutive down the tile column
+        const int a = s_zw[(cb - 1) * kZSub + klo];
+        const int e = s_zw[(cb - 1) * kZSub + khi];
+        // the columns come in slot order, so the hits do: in the own column (d = 4) the
+        // window is cut after the particle's own slot and the count there taken
+        if (!kTag && d == 4) {
+          scan(a, min(e, ti + 1));
+          c1 = flushed + (int)(((w - rd) & (kRing - 1u)) >> 6);
+          scan(max(a, ti + 1), e);
+        } else {
+          scan(a, e);
+        }
       }
-      // pad to a multiple of 8 with sentinel slots (one per bank group), flush
+      // pad to a multiple of 8 with sentinel slots (one per bank group, not in the force part), flush
       int nb = (int)(((w - rd) & (kRing - 1u)) >> 6);
       const int cnt = flushed + nb;
       const int cntp = (cnt + 7) & ~7;
       for (; nb < ((nb + 7) & ~7); ++nb) hit(true, g.tcap + (nb & 7));
       drain();
-      if (cntp > g.lcap) over = max(over, cntp);
-      s.ncount[gi] = min(cntp, g.lcap);
-      mygrp = min(cntp, g.lcap) >> 3;
+      const int nF = kTag ? (int)((nF2 & 0xffffu) + (nF2 >> 16)) : cnt - c1, nL = cnt - nF;
+      const int gF = (nF + 7) >> 3, gL = (nL + 7) >> 3;  // k_bank pads each part to rows of 8
+      const int need = max(cntp, 8 * (gF + gL));
+      if (need > g.lcap) over = max(over, need);
+      const bool fits = need <= g.lcap;
+      // bit 31: untagged, the first nL raw entries are the non-force part
+      s.ncount[gi] = fits ? (nF | (nL << 16) | (kTag ? 0 : (int)0x80000000u)) : 0;
+      mygrp = fits ? gF + gL : 0;
+      mygrpF = fits ? gF : 0;
       s.hbuild[gi] = sqrtf(Hi2) / Hfac;
     }
-    if (k < ni) grp[k] = mygrp;
+    if (k < ni) {
+      grp[k] = mygrp;
+      grpF[k] = mygrpF;
+    }
   }
   over = warp_max(over);
   if (lane == 0 && over) atomicMax(&ctr->list_overflow, over);
@@ -575,84 +668,151 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
   // as here), for the loop kernels' walks (walk_prefix_pre)
   __syncthreads();
   block_exclusive_scan(grp, ni);
+  block_exclusive_scan(grpF, ni);
   int* out = g.desc_pref + (size_t)ba * (g.icap + 1);
-  for (int k = threadIdx.x; k <= ni; k += blockDim.x) out[k] = grp[k];
+  int* outF = g.desc_prefF + (size_t)ba * (g.icap + 1);
+  for (int k = threadIdx.x; k <= ni; k += blockDim.x) {
+    out[k] = grp[k];
+    outF[k] = grpF[k];
+  }
 }
 
-// k_bank: the bank-aware row layout ("Bank-aware rows" above) of every list of at most
-// 8 kCellRows entries, one lane per list, in one pass over the natural-order list: the t-th
-// real entry of group b goes to cell (t, b) of the lane's grid in shared memory; then the
-// entries of a group past row R = ncount / 8 move to free cells, the other free cells get the
-// group's sentinel, and the R rows are written back.
-__global__ void __launch_bounds__(256) k_bank(int i0, int n, DevGrid g, DevState s) {
-  extern __shared__ unsigned short kb[];  // cell (r, w) of thread t at kb[(8 r + w) * 256 + t]
+// k_bank: k_lists' natural-order list (nbr_raw) -> the two-part bank-aware layout of nbr
+// (sph_internal.cuh): rows [0, RF) the force part, rows [RF, RF + RL) the rest, each part in
+// bank-aware rows ("Bank-aware rows" above).  The parts come either as the raw list's tail /
+// head (ncount bit 31: the list is in slot order) or by tag (bit 15 of an entry: force part).
+// One lane per list, one pass over the raw list: the t-th real entry of group b of part p
+// goes straight to cell (row0_p + t, b) of the lane's grid in shared memory while
+// t < R_p = ceil(n_p / 8), past that into the part's overflow queue.  The rows are then
+// written out cell by cell: a grid entry where the column has one, else the part's next
+// queued entry, else the column's sentinel (tcap + its bank group).  Counts are 4-bit fields
+// (8 groups per 32-bit word per part).  A list of more than kCellRows rows, a group of more
+// than 15 entries or more than kBankQ overflowing entries in a part takes the natural-order
+// path (still split in the two parts).
+constexpr int kBankThreads = 256;
+constexpr int kBankQ = 8;  // overflow queue entries per lane and part
+__global__ void __launch_bounds__(kBankThreads) k_bank(int i0, int n, DevGrid g, DevState s) {
+  // cell (r, w) of thread t at kb[(8 r + w) T + t]; queue entry q of part p at kb[(8 kCellRows + p kBankQ + q) T + t]
+  extern __shared__ unsigned short kb[];
   const int i = i0 + blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= i0 + n) return;
-  const int cnt8 = s.ncount[i];
-  if (cnt8 <= 0 || cnt8 > 8 * kCellRows) return;
-  const int R = cnt8 >> 3;
+  const int packed = s.ncount[i];
+  const int nF = packed & 0xffff, nL = (packed >> 16) & 0x7fff;
+  const bool bypos = packed < 0;  // untagged: raw entries [0, nL) are the non-force part
+  if (nF + nL == 0) return;
+  const int RF = (nF + 7) >> 3, RL = (nL + 7) >> 3, Rraw = (nF + nL + 7) >> 3;
+  const uint4* raw = reinterpret_cast<const uint4*>(s.nbr_raw + (size_t)i * g.lcap);
   uint4* lst = reinterpret_cast<uint4*>(s.nbr + (size_t)i * g.lcap);
   const uint32_t tcap = (uint32_t)g.tcap;
+  constexpr uint32_t kStride = 2u * kBankThreads;
   const uint32_t base = (uint32_t)__cvta_generic_to_shared(kb) + 2u * threadIdx.x;
-  auto cell = [&](uint32_t r, uint32_t w) { return base + (8u * r + w) * 512u; };
-  unsigned long long run = 0ull;  // entries of each group so far (bytes)
-  uint4 v = __ldg(lst);
-  for (int r = 0; r < R; ++r) {
-    const uint4 nx = r + 1 < R ? __ldg(lst + r + 1) : v;
-    const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+  const uint32_t qbF = base + 8u * kCellRows * kStride, qbL = qbF + kBankQ * kStride;
+  auto cell = [&](uint32_t r, uint32_t w) { return base + (8u * r + w) * kStride; };
+  bool grid_ok = RF + RL <= kCellRows;
+  uint32_t cF = 0u, cL = 0u;  // 4-bit entry counts of the 8 groups, per part
+  int qF = 0, qL = 0;         // queued entries per part
+  if (grid_ok && bypos) {
+    // raw entries [lo, hi) of one part into its grid rows [row0, row0 + R)
+    auto place_range = [&](int lo, int hi, uint32_t& c, int& qn, uint32_t R, uint32_t row0, uint32_t qb) {
+      for (int r = lo >> 3; r < ((hi + 7) >> 3); ++r) {
+        const uint4 v = __ldg(raw + r);
+        const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const uint32_t hsl = (wv[k >> 1] >> (16 * (k & 1))) & 0xffffu;
-      const uint32_t b = hsl & 7u;
-      const uint32_t tb = (uint32_t)(run >> (8u * b)) & 0xffu;
-      sts_u16_if(cell(min(tb, (uint32_t)kCellRows - 1u), b), hsl, hsl < tcap);
-      run += (unsigned long long)(hsl < tcap ? 1u : 0u) << (8u * b);
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t sl = (wv[k >> 1] >> (16 * (k & 1))) & 0xffffu, b = sl & 7u;
+          const int idx = 8 * r + k;
+          const bool real = idx >= lo && idx < hi;  // (padding sentinels lie past hi)
+          const uint32_t tb = (c >> (4u * b)) & 15u;
+          sts_u16_if(cell(row0 + tb, b), sl, real && tb < R);
+          sts_u16_if(qb + (uint32_t)min(qn, kBankQ - 1) * kStride, sl, real && tb >= R);
+          qn += (real && tb >= R) ? 1 : 0;
+          c += (real ? 1u : 0u) << (4u * b);
+        }
+      }
+    };
+    place_range(0, nL, cL, qL, (uint32_t)RL, (uint32_t)RF, qbL);
+    place_range(nL, nL + nF, cF, qF, (uint32_t)RF, 0u, qbF);
+  } else if (grid_ok) {
+    const uint32_t rf = (uint32_t)RF, rl = (uint32_t)RL;
+    for (int r = 0; r < Rraw; ++r) {
+      const uint4 v = __ldg(raw + r);
+      const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t e = (wv[k >> 1] >> (16 * (k & 1))) & 0xffffu;
+        const uint32_t sl = e & 0x7fffu, b = e & 7u;
+        const bool lpart = e < 0x8000u, real = sl < tcap;
+        const uint32_t c = lpart ? cL : cF;
+        const uint32_t tb = (c >> (4u * b)) & 15u;
+        const uint32_t R = lpart ? rl : rf;
+        const bool ovf = real && tb >= R;
+        sts_u16_if(cell((lpart ? rf : 0u) + tb, b), sl, real && tb < R);
+        const int qn = lpart ? qL : qF;
+        sts_u16_if((lpart ? qbL : qbF) + (uint32_t)min(qn, kBankQ - 1) * kStride, sl, ovf);
+        if (lpart) qL += ovf ? 1 : 0; else qF += ovf ? 1 : 0;
+        const uint32_t inc = (real ? 1u : 0u) << (4u * b);
+        if (lpart) cL += inc; else cF += inc;
+      }
     }
-    v = nx;
   }
-  int cntq[8];
+  if (grid_ok) {
+    // (a group past 15 entries carries into the next field: the sums no longer match)
+    uint32_t sF = 0u, sL = 0u;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) cntq[q] = (int)((run >> (8 * q)) & 0xffull);
-  bool ovf = false;
+    for (int q = 0; q < 8; ++q) { sF += (cF >> (4 * q)) & 15u; sL += (cL >> (4 * q)) & 15u; }
+    grid_ok = qF <= kBankQ && qL <= kBankQ && sF == (uint32_t)nF && sL == (uint32_t)nL;
+  }
+  if (grid_ok) {
+#pragma unroll 1
+    for (int p = 0; p < 2; ++p) {
+      const int R = p ? RL : RF, row0 = p ? RF : 0, qn = p ? qL : qF;
+      const uint32_t c = p ? cL : cF, qb = p ? qbL : qbF;
+      int cw[8];
 #pragma unroll
-  for (int q = 0; q < 8; ++q) ovf = ovf || cntq[q] > kCellRows;
-  if (ovf) return;  // a group past the grid: the list keeps its natural order
-  int ow = 0, orow = 0;
-  auto colcnt = [&](int q) {
-    int c = cntq[0];
+      for (int w = 0; w < 8; ++w) cw[w] = (int)((c >> (4 * w)) & 15u);
+      int q = 0;
+      for (int r = 0; r < R; ++r) {
+        uint32_t o[8];
 #pragma unroll
-    for (int x = 1; x < 8; ++x) c = q == x ? cntq[x] : c;
-    return c;
-  };
-  auto place = [&](uint32_t hv) {  // next free cell: rows >= the count of the column
-    for (;;) {
-      const int cw = colcnt(ow);
-      if (orow < cw) orow = cw;
-      if (orow < R) break;
-      ++ow;
-      orow = 0;
+        for (int w = 0; w < 8; ++w) {
+          uint32_t hv = tcap + (((uint32_t)w - tcap) & 7u);  // the column's sentinel
+          if (r < cw[w]) hv = lds_u16(cell((uint32_t)(row0 + r), (uint32_t)w));
+          else if (q < qn) hv = lds_u16(qb + (uint32_t)(q++) * kStride);
+          o[w] = hv;
+        }
+        lst[row0 + r] = make_uint4(o[0] | (o[1] << 16), o[2] | (o[3] << 16), o[4] | (o[5] << 16), o[6] | (o[7] << 16));
+      }
     }
-    sts_u16(cell((uint32_t)orow, (uint32_t)ow), hv);
-    ++orow;
-  };
-#pragma unroll
-  for (int q = 0; q < 8; ++q)
-    for (int r = R; r < cntq[q]; ++r) place(lds_u16(cell((uint32_t)r, (uint32_t)q)));
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    int r0 = min(cntq[q], R);
-    if (q < ow) r0 = R;
-    else if (q == ow) r0 = max(r0, orow);
-    const uint32_t sent = tcap + (((uint32_t)q - tcap) & 7u);
-    for (int r = r0; r < R; ++r) sts_u16(cell((uint32_t)r, (uint32_t)q), sent);
+    return;
   }
-  for (int r = 0; r < R; ++r) {
-    uint4 o;
-    o.x = lds_u16(cell(r, 0)) | (lds_u16(cell(r, 1)) << 16);
-    o.y = lds_u16(cell(r, 2)) | (lds_u16(cell(r, 3)) << 16);
-    o.z = lds_u16(cell(r, 4)) | (lds_u16(cell(r, 5)) << 16);
-    o.w = lds_u16(cell(r, 6)) | (lds_u16(cell(r, 7)) << 16);
-    lst[r] = o;
+  // natural order, split in the two parts (each padded with sentinels to a row of 8)
+#pragma unroll 1
+  for (uint32_t p = 0; p < 2; ++p) {
+    int orow = p ? RF : 0, m = 0;
+    uint4 buf = make_uint4(0u, 0u, 0u, 0u);
+    auto put = [&](uint32_t sl) {
+      const int k = m & 7;
+      const uint32_t lo = (k & 1) ? 0xffffu : 0u, hi = (k & 1) ? (sl << 16) : sl;
+      const int wd = k >> 1;
+      if (wd == 0) buf.x = (buf.x & lo) | hi;
+      else if (wd == 1) buf.y = (buf.y & lo) | hi;
+      else if (wd == 2) buf.z = (buf.z & lo) | hi;
+      else buf.w = (buf.w & lo) | hi;
+      if (k == 7) lst[orow++] = buf;
+      ++m;
+    };
+    for (int r = 0; r < Rraw; ++r) {
+      const uint4 v = __ldg(raw + r);
+      const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t e = (wv[k >> 1] >> (16 * (k & 1))) & 0xffffu;
+        const uint32_t sl = e & 0x7fffu;
+        const bool lpart = bypos ? 8 * r + k < nL : e < 0x8000u;
+        if (sl < tcap && lpart == (p == 1u)) put(sl);
+      }
+    }
+    while (m & 7) put(tcap + (uint32_t)(m & 7));
   }
 }
 
@@ -665,8 +825,9 @@ __global__ void __launch_bounds__(256) k_bank(int i0, int n, DevGrid g, DevState
 // number of iterations up to one; only the particle switch diverges).  A particle whose
 // groups lie inside one thread's range is summed by that thread alone and stored; a particle
 // split across threads leaves one partial record per thread it touches (the thread's head
-// record if the thread's range starts inside it, else its tail record), summed by the
-// epilogue in thread order (gather_acc): no atomics, and the sums are the same every run.
+// record if the thread's range starts inside it, else -- the one thread whose range ends
+// inside it -- the particle's own record), summed by the epilogue in thread order
+// (gather_acc): no atomics, and the sums are the same every run.
 constexpr int kMaxNW = 16;  // loop kernels run 256 or 512 threads (blockDim.x)
 __device__ __forceinline__ int group_start(int t, int G) { return (int)(((long long)t * G) / blockDim.x); }
 
@@ -714,9 +875,11 @@ __device__ __forceinline__ auto pair2_of(P p) {
 // Walk this thread's groups.  list_of(k) is particle k's list; begin(k) sets up particle k
 // (i state, accumulators); pair2(j0, j1) accumulates two entries; take() returns the
 // accumulators.
-template <class Acc, class ListOf, class Begin, class Pair2, class Take>
-__device__ __forceinline__ void walk_lists(int ni, const int* __restrict__ pref, Acc* fin, Acc* head, Acc* tail,
-                                           ListOf&& list_of, Begin&& begin, Pair2&& pair2, Take&& take) {
+// finish(k, part): particle k's rows in this thread's range are done; part = 0 when they are
+// all of its rows, 1 when this thread's range starts inside it (its head), 2 otherwise (tail).
+template <class ListOf, class Begin, class Pair2, class Finish>
+__device__ __forceinline__ void walk_rows(int ni, const int* __restrict__ pref, ListOf&& list_of, Begin&& begin,
+                                          Pair2&& pair2, Finish&& finish_k) {
   const int G = pref[ni];
   if (G == 0) return;
   const int g0 = group_start(threadIdx.x, G), g1 = group_start(threadIdx.x + 1, G);
@@ -735,11 +898,7 @@ __device__ __forceinline__ void walk_lists(int ni, const int* __restrict__ pref,
   // a particle whose rows lie in this thread's range is stored whole; a split one goes to
   // this thread's head record (the particle its range starts in) or tail record (the one it
   // ends in), summed by the epilogue (gather_acc) in thread order -- no atomics
-  auto finish = [&]() {
-    if (g0 <= p0 && p1 <= g1) fin[k] = take();
-    else if (k == lo) head[threadIdx.x] = take();
-    else tail[threadIdx.x] = take();
-  };
+  auto finish = [&]() { finish_k(k, (g0 <= p0 && p1 <= g1) ? 0 : (k == lo ? 1 : 2)); };
   // each row is loaded one iteration ahead (its global-load latency was ~8 % of the loop
   // kernels' warp stalls when the row was used right after its load)
   uint4 enext = __ldg(list);
@@ -777,19 +936,27 @@ __device__ __forceinline__ void walk_lists(int ni, const int* __restrict__ pref,
   finish();
 }
 
+template <class Acc, class ListOf, class Begin, class Pair2, class Take>
+__device__ __forceinline__ void walk_lists(int ni, const int* __restrict__ pref, Acc* fin, Acc* head,
+                                           ListOf&& list_of, Begin&& begin, Pair2&& pair2, Take&& take) {
+  walk_rows(ni, pref, list_of, begin, pair2, [&](int k, int part) {
+    if (part == 1) head[threadIdx.x] = take();
+    else fin[k] = take();  // (whole, or the split particle's part in the thread ending inside it)
+  });
+}
+
 // Walk-area layout after a kernel's tile records (byte offset `base`, 16-aligned).
 template <class Acc>
 struct WalkArea {
   int* pref;  // [icap + 1]
   int* kl;    // [icap]  walk index -> block-local i index
-  Acc* fin;   // [icap]  whole particles
+  Acc* fin;   // [icap]  whole particles (split ones: the part of the thread whose range ends inside)
   Acc* head;  // [threads] split particle a thread's range starts in
-  Acc* tail;  // [threads] split particle a thread's range ends in
 };
 template <class Acc>
 __host__ __device__ __forceinline__ size_t walk_bytes(int icap, int threads = kNW * 32) {
   return (((size_t)(icap + 1) * 4 + 15) & ~(size_t)15) + (((size_t)icap * 4 + 15) & ~(size_t)15) +
-         (((size_t)icap * sizeof(Acc) + 15) & ~(size_t)15) + (size_t)2 * threads * sizeof(Acc);
+         (((size_t)icap * sizeof(Acc) + 15) & ~(size_t)15) + (size_t)threads * sizeof(Acc);
 }
 template <class Acc>
 __device__ __forceinline__ WalkArea<Acc> walk_area(char* base, int icap) {
@@ -801,12 +968,11 @@ __device__ __forceinline__ WalkArea<Acc> walk_area(char* base, int icap) {
   w.fin = reinterpret_cast<Acc*>(base);
   base += ((size_t)icap * sizeof(Acc) + 15) & ~(size_t)15;
   w.head = reinterpret_cast<Acc*>(base);
-  w.tail = w.head + blockDim.x;
   return w;
 }
 
 // Accumulators of walk particle k: its whole record, or the sum, in thread order, of the
-// head / tail records of the threads its rows were split over (walk_lists).
+// records of the threads its rows were split over (walk_lists).
 template <class Acc>
 __device__ __forceinline__ Acc gather_acc(const WalkArea<Acc>& W, int ni, int k) {
   const long long G = W.pref[ni];
@@ -819,7 +985,7 @@ __device__ __forceinline__ Acc gather_acc(const WalkArea<Acc>& W, int ni, int k)
   for (int t2 = ta; t2 <= tb; ++t2) {
     const int s0 = (int)(((long long)t2 * G) / nt), s1 = (int)(((long long)(t2 + 1) * G) / nt);
     if (s0 >= s1) continue;  // (a thread without rows)
-    s.add(s0 >= a ? W.head[t2] : W.tail[t2]);
+    s.add(s0 >= a ? W.head[t2] : W.fin[k]);
   }
   return s;
 }
@@ -829,8 +995,8 @@ __device__ __forceinline__ Acc gather_acc(const WalkArea<Acc>& W, int ni, int k)
 // The same for a walk over all the block's particles (kl[k] = k): the prefix k_lists stored.
 template <class Acc>
 // Issued with cp.async before the tile staging, whose wait + barrier completes it.
-__device__ __forceinline__ void walk_prefix_pre(const DevGrid& g, WalkArea<Acc>& W, int ni) {
-  const int* src = g.desc_pref + (size_t)blk_a(g) * (g.icap + 1);
+__device__ __forceinline__ void walk_prefix_pre(const DevGrid& g, WalkArea<Acc>& W, int ni, bool force_part = false) {
+  const int* src = (force_part ? g.desc_prefF : g.desc_pref) + (size_t)blk_a(g) * (g.icap + 1);
   for (int k = threadIdx.x; k <= ni; k += blockDim.x) cp_async4(W.pref + k, src + k);
 }
 
@@ -841,7 +1007,8 @@ __device__ __forceinline__ void walk_prefix(const SS& S, const DevState& s, Walk
   for (int k = threadIdx.x; k < ni; k += blockDim.x) {
     int ti, gi;
     i_slot(S, kl[k], ti, gi);
-    pref[k] = __ldg(s.ncount + gi) >> 3;
+    const int c = __ldg(s.ncount + gi);
+    pref[k] = (((c & 0xffff) + 7) >> 3) + ((((c >> 16) & 0x7fff) + 7) >> 3);
   }
   __syncthreads();
   block_exclusive_scan(pref, ni);
@@ -872,7 +1039,7 @@ __global__ void __launch_bounds__(256, 3) k_density(DevGrid g, DevPhys ph, DevSt
   {
     const float4* src[2] = {reinterpret_cast<const float4*>(s.xh), s.vm};
     const int o16[2] = {0, O1};
-    stage_records(S, nseg, 2, src, o16, nullptr, 0);
+    stage_records(S, nseg, 2, src, o16, T.ntile);
   }
   for (int t = threadIdx.x; t < T.ntile; t += blockDim.x) {
     const uint4 x = reinterpret_cast<const uint4*>(smem4)[t];
@@ -912,7 +1079,7 @@ __global__ void __launch_bounds__(256, 3) k_density(DevGrid g, DevPhys ph, DevSt
     const uint32_t sb0 = smem_base(0), sb1 = smem_base(O1);
     int ti_c = 0;  // tile slot of the walk's current particle (list_of -> begin)
     walk_lists(
-        ni, W.pref, W.fin, W.head, W.tail,
+        ni, W.pref, W.fin, W.head,
         [&](int k) {  // (list_of runs right before begin: the slot lookup is shared)
           i_slot(S, W.kl[k], ti_c, gi);
           return s.nbr + (size_t)gi * g.lcap;
@@ -978,25 +1145,35 @@ __global__ void __launch_bounds__(256, 3) k_gradient(DevGrid g, DevPhys ph, DevS
                                                        const int* __restrict__ cell_start, float dt, int first_step,
                                                        DevCounters* __restrict__ ctr) {
   __shared__ unsigned long long s_pairs;
-  if (threadIdx.x == 0) s_pairs = 0;
+  __shared__ unsigned int s_hinv_max;  // largest 1/h of the tile (f32 bits)
+  if (threadIdx.x == 0) { s_pairs = 0; s_hinv_max = 0u; }
   DESC_PROLOGUE();
-  // T0 = smem4[j]: x, y, z, h   T1 = smem4[O1 + j]: vx, vy, vz, m   T2 = smem4[O2 + j]: c, u, m/rho, rho
+  // T0 = smem4[j]: x, y, z, h   T1 = smem4[O1 + j]: vx, vy, vz, 1/h (m_j is not used here)
+  // T2 = smem4[O2 + j]: c, u, m/rho, rho
   const int O1 = SP, O2 = 2 * SP;
   WalkArea<GradAcc> W = walk_area<GradAcc>(reinterpret_cast<char*>(smem4 + 3 * SP), g.icap);
   walk_prefix_pre(g, W, T.ni);
   {
     const float4* src[3] = {reinterpret_cast<const float4*>(s.xh), s.vm, s.gq};
     const int o16[3] = {0, O1, O2};
-    stage_records(S, nseg, 3, src, o16, nullptr, 0);
+    stage_records(S, nseg, 3, src, o16, T.ntile);
   }
-  for (int t = threadIdx.x; t < T.ntile; t += blockDim.x) {
-    const uint4 x = reinterpret_cast<const uint4*>(smem4)[t];
-    const float3 p = rel_pos(g, T, x);
-    smem4[t] = make_float4(p.x, p.y, p.z, __uint_as_float(x.w));
+  {
+    unsigned int hm = 0u;
+    for (int t = threadIdx.x; t < T.ntile; t += blockDim.x) {
+      const uint4 x = reinterpret_cast<const uint4*>(smem4)[t];
+      const float3 p = rel_pos(g, T, x);
+      smem4[t] = make_float4(p.x, p.y, p.z, __uint_as_float(x.w));
+      const float hinv = 1.f / __uint_as_float(x.w);
+      reinterpret_cast<float*>(smem4 + O1 + t)[3] = hinv;
+      hm = max(hm, __float_as_uint(hinv));
+    }
+    hm = (unsigned int)warp_max((int)hm);
+    if ((threadIdx.x & 31) == 0 && hm) atomicMax(&s_hinv_max, hm);
   }
   if (threadIdx.x < kNSent) {
     smem4[g.tcap + threadIdx.x] = make_float4(kFar, kFar, kFar, 1.f);
-    smem4[O1 + g.tcap + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
+    smem4[O1 + g.tcap + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 1.f);
     smem4[O2 + g.tcap + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 1.f);
   }
   const int ni = T.ni;
@@ -1005,13 +1182,15 @@ __global__ void __launch_bounds__(256, 3) k_gradient(DevGrid g, DevPhys ph, DevS
   {
     float4 pi4, vi4;
     float hinv = 0.f, qband = 0.f, ci = 0.f, ui = 0.f;
+    // |min(q_i, q_j) - 2| below this: decide the symmetric set in fp64 (eabs / min h of the tile)
+    const float sband = g.eabs * __uint_as_float(s_hinv_max) + 8e-6f;
     double H2 = 0.0;
     int gi = 0;
     GradAcc a;
     const uint32_t sb0 = smem_base(0), sb1 = smem_base(O1), sb2 = smem_base(O2);
     int ti_c = 0;  // tile slot of the walk's current particle (list_of -> begin)
     walk_lists(
-        ni, W.pref, W.fin, W.head, W.tail,
+        ni, W.pref, W.fin, W.head,
         [&](int k) {  // (list_of runs right before begin: the slot lookup is shared)
           i_slot(S, W.kl[k], ti_c, gi);
           return s.nbr + (size_t)gi * g.lcap;
@@ -1021,21 +1200,28 @@ __global__ void __launch_bounds__(256, 3) k_gradient(DevGrid g, DevPhys ph, DevS
           pi4 = smem4[ti];
           vi4 = smem4[O1 + ti];
           const float4 gi4 = smem4[O2 + ti];
-          hinv = 1.f / pi4.w;
+          hinv = vi4.w;
           qband = g.eabs * hinv + 8e-6f;
           H2 = h2_exact(pi4.w, ph.gamma_k);
           ci = gi4.x;
           ui = gi4.y;
-          a = GradAcc{2.f * ci, 0.f, 0};
+          a = GradAcc{2.f * ci, 0.f, 0, 2.f * ci};
         },
         pair2_of([&](int j) {
           const uint32_t o = (uint32_t)j << 4;
           const float4 p = lds4(sb0 + o);
-          grad_pair(a, pi4.x - p.x, pi4.y - p.y, pi4.z - p.z, hinv, qband, vi4, ci, ui, ph.beta, lds4(sb1 + o),
-                    lds4(sb2 + o), [&]() {
-                      return exact_neighbour(s.xh, gi, slot_global(S, nseg, j), H2, g.dscale[0], g.dscale[1],
-                                             g.dscale[2]);
-                    });
+          const float4 vj = lds4(sb1 + o);
+          grad_pair_sym(
+              a, pi4.x - p.x, pi4.y - p.y, pi4.z - p.z, hinv, vj.w, qband, sband, vi4, ci, ui, ph.beta, vj,
+              lds4(sb2 + o),
+              [&]() {
+                return exact_neighbour(s.xh, gi, slot_global(S, nseg, j), H2, g.dscale[0], g.dscale[1], g.dscale[2]);
+              },
+              [&]() {
+                const int gj = slot_global(S, nseg, j);
+                return exact_neighbour(s.xh, gi, gj, fmax(H2, h2_exact(__uint_as_float(s.xh[gj].w), ph.gamma_k)),
+                                       g.dscale[0], g.dscale[1], g.dscale[2]);
+              });
         }),
         [&]() { return a; });
   }
@@ -1045,9 +1231,13 @@ __global__ void __launch_bounds__(256, 3) k_gradient(DevGrid g, DevPhys ph, DevS
     const GradAcc a = gather_acc(W, ni, k);
     int ti, gi;
     i_slot(S, k, ti, gi);
-    if (s.wide && s.wide[gi]) continue;  // wide particles: k_wide_gradient
+    if (s.wide && s.wide[gi]) continue;  // wide particles: k_wide_gradient, k_wide_force
     const float4 gi4 = smem4[O2 + ti];
     npairs += (unsigned long long)grad_epilogue(ph, s, a, gi, smem4[ti].w, gi4.x, gi4.y, gi4.w, dt, first_step);
+    // the force loop's v_sig and N_force (symmetric set; a wide partner that did not list this
+    // particle adds its pair in k_wide_force)
+    s.vsig[gi] = a.vmaxs;
+    s.countf[gi] = (a.nn >> 16) - 1;  // (the self pair)
   }
   const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -1058,50 +1248,57 @@ __global__ void __launch_bounds__(256, 3) k_gradient(DevGrid g, DevPhys ph, DevS
 }
 
 // ================================================================ force loop ==========
-// Gather form of the pairwise sums of Eqs. 7, 17-19 over r_ij < max(H_i, H_j) (R3), written
-// with g = G r = f dW/dr (the r factors cancel):
-//   A = P/rho^2, Pi_ij = -abar mu v_sig / rhobar (R9), gbar = (g_i + g_j)/2,
-//   T = A_i g_i + A_j g_j + Pi_ij gbar  (= S_ij r),   a_i = -sum_j m_j T r_ij / r,
-//   du_i = sum_j m_j [(A_i g_i + Pi gbar / 2)(v_ij . r_hat) + D_ij]  (Eq. 18 + R10 + Eq. 19/R11),
-//   D_ij = alpha_c,ij v_c,ij (u_i - u_j)(g_i + g_j) / (rho_i + rho_j)  (Eqs. 20, 22; R12, R13).
-// T is evaluated from operands symmetric in (i, j), so the pair terms of i and j are exact
-// negatives (momentum and energy conserving up to the summation rounding).
-// The CFL dt = C_cfl min 2 gamma_k h / v_sig is reduced in the epilogue.
+// Pair-once form of the pairwise sums of Eqs. 7, 17-19 over r_ij < max(H_i, H_j) (R3): each
+// unordered pair is evaluated ONCE, by the particle whose list holds it in its force part
+// (k_lists: partner in the upper half of the cell stencil), and applied to both particles with
+// opposite signs (force_pair2): the i side accumulates in registers and is added to acc[i]
+// when the thread's rows of i end, the j side is added to acc[j] with one vector reduction
+// (red.global.add.v4.f32) per pair that has a term.  acc is zeroed before the launch; the CFL
+// dt and the finiteness check run over the finished sums in k_force_fin.  v_sig and N_force
+// of the symmetric set were taken by the gradient loop.
 __host__ __device__ __forceinline__ size_t force_records_bytes(int tcap) {
-  return (size_t)(tcap + kNSent) * (4 * 16);
+  const size_t sp = (size_t)tcap + kNSent;
+  return sp * (4 * 16) + ((sp + 3) & ~(size_t)3) * 4;  // four records + the slot's global index
+}
+
+__device__ __forceinline__ void red_add4(float4* p, const float4& v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ int lds1(uint32_t a) {
+  int v;
+  asm("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
 }
 
 __global__ void __launch_bounds__(512, 1) k_force(DevGrid g, DevPhys ph, DevState s,
                                                     const int* __restrict__ cell_start,
                                                     DevCounters* __restrict__ ctr) {
-  __shared__ unsigned long long s_pairs;
-  __shared__ unsigned int s_dt;
-  __shared__ int s_bad;
-  __shared__ unsigned int s_hinv_max;  // largest 1/h of the tile (f32 bits)
-  if (threadIdx.x == 0) { s_pairs = 0; s_dt = 0x7f800000u; s_bad = 0; s_hinv_max = 0u; }
   DESC_PROLOGUE();
   // T0 = [j]: x, y, z, 1/h   T1 = [O1+j]: vx, vy, vz, m   T2 = [O2+j]: A, Kf, c, rho
-  // T3 = [O3+j]: B, P alpha_c, u, alpha_v  (P = A rho^2: four 16-byte records per pair)
+  // T3 = [O3+j]: B, P alpha_c, u, alpha_v  (P = A rho^2)   GI[j]: global index of slot j
   const int O1 = SP, O2 = 2 * SP, O3 = 3 * SP;
-  WalkArea<ForceAcc> W =
-      walk_area<ForceAcc>(reinterpret_cast<char*>(smem4) + force_records_bytes(g.tcap), g.icap);
-  walk_prefix_pre(g, W, T.ni);
+  int* GI = reinterpret_cast<int*>(smem4 + 4 * SP);
+  int* pref = GI + ((SP + 3) & ~3);  // [icap + 1] force-part group prefix (k_lists)
+  {
+    const int* src = g.desc_prefF + (size_t)ba * (g.icap + 1);
+    for (int k = threadIdx.x; k <= T.ni; k += blockDim.x) cp_async4(pref + k, src + k);
+    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int k = threadIdx.x >> 5; k < nseg; k += nw) {
+      const int4 sg = S.seg[k];
+      for (int t = lane; t < sg.z; t += 32) GI[sg.x + t] = sg.y + t;
+    }
+    if (threadIdx.x < kNSent) GI[g.tcap + threadIdx.x] = 0;  // (sentinels: never a term)
+  }
   {
     const float4* src[4] = {reinterpret_cast<const float4*>(s.xh), s.vm, s.fr1, s.fr2};
     const int o16[4] = {0, O1, O2, O3};
-    stage_records(S, nseg, 4, src, o16, nullptr, 0);
+    stage_records(S, nseg, 4, src, o16, T.ntile);
   }
-  {
-    unsigned int hm = 0u;
-    for (int t = threadIdx.x; t < T.ntile; t += blockDim.x) {
-      const uint4 x = reinterpret_cast<const uint4*>(smem4)[t];
-      const float3 p = rel_pos(g, T, x);
-      const float hinv = 1.f / __uint_as_float(x.w);
-      hm = max(hm, __float_as_uint(hinv));
-      smem4[t] = make_float4(p.x, p.y, p.z, hinv);
-    }
-    hm = (unsigned int)warp_max((int)hm);
-    if ((threadIdx.x & 31) == 0 && hm) atomicMax(&s_hinv_max, hm);
+  for (int t = threadIdx.x; t < T.ntile; t += blockDim.x) {
+    const uint4 x = reinterpret_cast<const uint4*>(smem4)[t];
+    const float3 p = rel_pos(g, T, x);
+    smem4[t] = make_float4(p.x, p.y, p.z, 1.f / __uint_as_float(x.w));
   }
   if (threadIdx.x < kNSent) {
     smem4[g.tcap + threadIdx.x] = make_float4(kFar, kFar, kFar, 1.f);
@@ -1109,86 +1306,81 @@ __global__ void __launch_bounds__(512, 1) k_force(DevGrid g, DevPhys ph, DevStat
     smem4[O2 + g.tcap + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 1.f);
     smem4[O3 + g.tcap + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  const int ni = T.ni;
-  for (int k = threadIdx.x; k < ni; k += blockDim.x) W.kl[k] = k;
   __syncthreads();
-  {
-    const float4* __restrict__ T0 = smem4;
-    const float4* __restrict__ T1 = smem4 + O1;
-    const float4* __restrict__ T2 = smem4 + O2;
-    const float4* __restrict__ T3 = smem4 + O3;
-    // |min(q_i, q_j) - 2| below this: decide in fp64 (eabs / min h of the tile)
-    const float band = g.eabs * __uint_as_float(s_hinv_max) + 8e-6f;
-    float4 pi4;
-    ForceSide I;
-    int gi = 0;
-    ForceAcc a;
-    const uint32_t sb0 = smem_base(0), sb1 = smem_base(O1), sb2 = smem_base(O2), sb3 = smem_base(O3);
-    int ti_c = 0;  // tile slot of the walk's current particle (list_of -> begin)
-    walk_lists(
-        ni, W.pref, W.fin, W.head, W.tail,
-        [&](int k) {  // (list_of runs right before begin: the slot lookup is shared)
-          i_slot(S, W.kl[k], ti_c, gi);
-          return s.nbr + (size_t)gi * g.lcap;
-        },
-        [&](int) {
-          const int ti = ti_c;
-          pi4 = T0[ti];
-          I.hinv = pi4.w;
-          I.v = T1[ti];
-          I.a = T2[ti];
-          I.b = T3[ti];
-          I.P = I.a.x * I.a.w * I.a.w;
-          a = ForceAcc{0.f, 0.f, 0.f, 0.f, 2.f * I.a.z, 0};
-        },
-        pair2_of([&](int j) {
-          const uint32_t o = (uint32_t)j << 4;
-          const float4 p = lds4(sb0 + o);
-          ForceSide J;
-          J.hinv = p.w;
-          J.v = lds4(sb1 + o);
-          J.a = lds4(sb2 + o);
-          J.b = lds4(sb3 + o);
-          J.P = J.a.x * J.a.w * J.a.w;
-          float vs;
-          int in;
-          force_pair(a, pi4.x - p.x, pi4.y - p.y, pi4.z - p.z, I, J, ph.beta, band, [&]() {
-            const int gj = slot_global(S, nseg, j);
-            const double H2 = fmax(h2_exact(__uint_as_float(s.xh[gi].w), ph.gamma_k),
-                                   h2_exact(__uint_as_float(s.xh[gj].w), ph.gamma_k));
-            return exact_neighbour(s.xh, gi, gj, H2, g.dscale[0], g.dscale[1], g.dscale[2]);
-          }, vs, in);
-        }),
-        [&]() { return a; });
-  }
-  __syncthreads();
-  unsigned long long npairs = 0;
+  const float4* __restrict__ T0 = smem4;
+  const float4* __restrict__ T1 = smem4 + O1;
+  const float4* __restrict__ T2 = smem4 + O2;
+  const float4* __restrict__ T3 = smem4 + O3;
+  float4 pi4;
+  ForceSide I;
+  int gi = 0;
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+  const uint32_t sb0 = smem_base(0), sb1 = smem_base(O1), sb2 = smem_base(O2), sb3 = smem_base(O3);
+  const uint32_t sbg = smem_base(4 * SP);
+  int ti_c = 0;  // tile slot of the walk's current particle (list_of -> begin)
+  walk_rows(
+      T.ni, pref,
+      [&](int k) {  // (list_of runs right before begin: the slot lookup is shared)
+        i_slot(S, k, ti_c, gi);
+        return s.nbr + (size_t)gi * g.lcap;
+      },
+      [&](int) {
+        const int ti = ti_c;
+        pi4 = T0[ti];
+        I.hinv = pi4.w;
+        I.v = T1[ti];
+        I.a = T2[ti];
+        I.b = T3[ti];
+        I.P = I.a.x * I.a.w * I.a.w;
+        a = make_float4(0.f, 0.f, 0.f, 0.f);
+      },
+      pair2_of([&](int j) {
+        const uint32_t o = (uint32_t)j << 4;
+        const float4 p = lds4(sb0 + o);
+        ForceSide J;
+        J.hinv = p.w;
+        J.v = lds4(sb1 + o);
+        J.a = lds4(sb2 + o);
+        J.b = lds4(sb3 + o);
+        J.P = J.a.x * J.a.w * J.a.w;
+        float4 jo;
+        if (force_pair2(a, jo, pi4.x - p.x, pi4.y - p.y, pi4.z - p.z, I, J, ph.beta))
+          red_add4(s.acc + lds1(sbg + ((uint32_t)j << 2)), jo);
+      }),
+      [&](int, int) { red_add4(s.acc + gi, a); });
+}
+
+// After k_force (and the wide particles' k_wide_force): the CFL dt = C_cfl min 2 gamma_k h / v_sig
+// (S:261), the finiteness check of a, du/dt and v_sig, and sum N_force.
+__global__ void __launch_bounds__(256) k_force_fin(int i0, int n, DevPhys ph, DevState s,
+                                                   DevCounters* __restrict__ ctr) {
+  const int i = i0 + blockIdx.x * blockDim.x + threadIdx.x;
   float dtmin = CUDART_INF_F;
-  for (int k = threadIdx.x; k < ni; k += blockDim.x) {
-    const ForceAcc a = gather_acc(W, ni, k);
-    int ti, gi;
-    i_slot(S, k, ti, gi);
-    if (s.wide && s.wide[gi]) continue;  // wide particles: k_wide_force
-    const float hi_ = __uint_as_float(s.xh[gi].w);
-    const int nn = a.nn - 1;  // the self pair
-    s.acc[gi] = make_float4(a.ax, a.ay, a.az, a.du);
-    s.vsig[gi] = a.vmax;
-    s.countf[gi] = nn;
-    npairs += (unsigned long long)nn;
-    const float dti = ph.c_cfl * 2.f * ph.gamma_k * hi_ / a.vmax;
-    if (!(isfinite(a.vmax) && isfinite(a.ax) && isfinite(a.ay) && isfinite(a.az) && isfinite(a.du)) || !(dti > 0.f))
-      s_bad = 1;
-    dtmin = fminf(dtmin, dti);
+  unsigned long long npairs = 0;
+  bool bad = false;
+  if (i < i0 + n) {
+    const float h = __uint_as_float(s.xh[i].w);
+    const float vs = s.vsig[i];
+    const float4 a = s.acc[i];
+    const float dti = ph.c_cfl * 2.f * ph.gamma_k * h / vs;
+    bad = !(isfinite(vs) && isfinite(a.x) && isfinite(a.y) && isfinite(a.z) && isfinite(a.w)) || !(dti > 0.f);
+    dtmin = dti > 0.f ? dti : CUDART_INF_F;
+    npairs = (unsigned long long)max(s.countf[i], 0);
   }
-  const int lane = threadIdx.x & 31;
+  __shared__ unsigned long long s_pairs;
+  __shared__ unsigned int s_dt;
+  __shared__ int s_bad;
+  if (threadIdx.x == 0) { s_pairs = 0; s_dt = 0x7f800000u; s_bad = 0; }
+  __syncthreads();
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     npairs += __shfl_xor_sync(kFull, npairs, o);
     dtmin = fminf(dtmin, __shfl_xor_sync(kFull, dtmin, o));
   }
-  if (lane == 0) {
+  if (bad) s_bad = 1;
+  if ((threadIdx.x & 31) == 0) {
     if (npairs) atomicAdd(&s_pairs, npairs);
-    if (dtmin < CUDART_INF_F && dtmin > 0.f) atomicMin(&s_dt, __float_as_uint(dtmin));
+    if (dtmin < CUDART_INF_F) atomicMin(&s_dt, __float_as_uint(dtmin));
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1290,13 +1482,12 @@ cudaError_t launch_block_run(const DevGrid& g, const DevState& s, uint8_t* flag,
 
 size_t lists_smem(const DevGrid& g) {
   const int nw = g.lists_warps > 0 ? g.lists_warps : kNW;
-  return (size_t)((g.tcap + kNSent + 1) & ~1) * 16 + lists_ring_bytes(g, nw) + lists_zw_bytes(g);
+  return (size_t)((g.tcap + kNSent + 1) & ~1) * 16 + lists_ring_bytes(g, nw) + lists_zw_bytes(g) +
+         (((size_t)g.tcap + kNSent + 15) & ~(size_t)15);
 }
 size_t density_smem(const DevGrid& g) { return (size_t)(g.tcap + kNSent) * (2 * 16) + walk_bytes<DenAcc>(g.icap); }
 size_t gradient_smem(const DevGrid& g) { return (size_t)(g.tcap + kNSent) * (3 * 16) + walk_bytes<GradAcc>(g.icap); }
-size_t force_smem(const DevGrid& g) {
-  return force_records_bytes(g.tcap) + walk_bytes<ForceAcc>(g.icap, g.force_threads > 0 ? g.force_threads : kNW * 32);
-}
+size_t force_smem(const DevGrid& g) { return force_records_bytes(g.tcap) + (size_t)(g.icap + 1) * 4; }
 
 cudaError_t launch_tile_sizes(const DevGrid& g, const int* cell_start, int* max_tile, int* max_i, uint8_t* flag,
                               cudaStream_t st) {
@@ -1311,19 +1502,25 @@ static cudaError_t set_smem(const void* fn, size_t bytes) {
 cudaError_t launch_lists(const DevGrid& g, const DevPhys& ph, const DevState& s, const int* cell_start,
                          DevCounters* ctr, cudaStream_t st) {
   const size_t sm = lists_smem(g);
-  cudaError_t e = set_smem((const void*)k_lists, sm);
+  const bool wide = s.wide != nullptr && s.n_wide > 0, tag = wide || !g.periodic_x;
+  const void* fn = wide ? (const void*)k_lists<true, true>
+                        : (tag ? (const void*)k_lists<false, true> : (const void*)k_lists<false, false>);
+  cudaError_t e = set_smem(fn, sm);
   if (e != cudaSuccess) return e;
   if (g.nrun == 0) return cudaSuccess;
-  k_lists<<<g.nrun, (g.lists_warps > 0 ? g.lists_warps : kNW) * 32, sm, st>>>(g, ph, s, cell_start, ctr);
+  const int thr = (g.lists_warps > 0 ? g.lists_warps : kNW) * 32;
+  if (wide) k_lists<true, true><<<g.nrun, thr, sm, st>>>(g, ph, s, cell_start, ctr);
+  else if (tag) k_lists<false, true><<<g.nrun, thr, sm, st>>>(g, ph, s, cell_start, ctr);
+  else k_lists<false, false><<<g.nrun, thr, sm, st>>>(g, ph, s, cell_start, ctr);
   return cudaGetLastError();
 }
 
 cudaError_t launch_bank(int i0, int n, const DevGrid& g, const DevState& s, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  const size_t sm = (size_t)8 * kCellRows * 256 * 2;
+  const size_t sm = (size_t)(8 * kCellRows + 2 * kBankQ) * kBankThreads * 2;
   cudaError_t e = set_smem((const void*)k_bank, sm);
   if (e != cudaSuccess) return e;
-  k_bank<<<(n + 255) / 256, 256, sm, st>>>(i0, n, g, s);
+  k_bank<<<(n + kBankThreads - 1) / kBankThreads, kBankThreads, sm, st>>>(i0, n, g, s);
   return cudaGetLastError();
 }
 
@@ -1356,6 +1553,12 @@ cudaError_t launch_force(const DevGrid& g, const DevPhys& ph, const DevState& s,
   if (e != cudaSuccess) return e;
   if (g.nrun == 0) return cudaSuccess;
   k_force<<<g.nrun, g.force_threads, sm, st>>>(g, ph, s, cell_start, ctr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_force_fin(int i0, int n, const DevPhys& ph, const DevState& s, DevCounters* ctr, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  k_force_fin<<<(n + 255) / 256, 256, 0, st>>>(i0, n, ph, s, ctr);
   return cudaGetLastError();
 }
 

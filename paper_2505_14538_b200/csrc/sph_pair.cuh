@@ -160,11 +160,18 @@ __device__ __forceinline__ DenOut den_epilogue(const DevGrid& g, const DevPhys& 
 // ------------------------------------------------------------- gradient (Eqs. 10-16) ----
 // v_sig,i = max(2 c_i, max_j (c_i + c_j - beta mu_ij)) (Eqs. 10-11, R15) and the Brookshaw
 // Laplacian lap u_i = 2 sum_j (m_j/rho_j)(u_i - u_j) dW/dr / r (R16), over r_ij < H_i.
+// vmaxs and the high half of nn: the force loop's signal velocity and neighbour count over the
+// symmetric set r_ij < max(H_i, H_j) (R3, R15), taken by the tile gradient loop (same v and
+// c_s as the force loop; the pair-once force loop then carries no per-pair maximum or count).
+// nn = gather count | symmetric count << 16 (16 bytes per accumulator record).
 struct GradAcc {
   float vmax, lap;  // vmax > 0: max over its f32 bits as int
   int nn;
-  __device__ static GradAcc zero() { return GradAcc{0.f, 0.f, 0}; }
-  __device__ void add(const GradAcc& o) { vmax = fmaxf(vmax, o.vmax); lap += o.lap; nn += o.nn; }
+  float vmaxs;
+  __device__ static GradAcc zero() { return GradAcc{0.f, 0.f, 0, 0.f}; }
+  __device__ void add(const GradAcc& o) {
+    vmax = fmaxf(vmax, o.vmax); lap += o.lap; nn += o.nn; vmaxs = fmaxf(vmaxs, o.vmaxs);
+  }
 };
 
 // vj = (v_j, m_j), gj = (c_j, u_j, m_j/rho_j, rho_j)
@@ -185,6 +192,33 @@ __device__ __forceinline__ void grad_pair(GradAcc& a, float dx, float dy, float 
   const float mu = fminf(vr, 0.f) * rinv;
   const float vs = fmaf(-beta, mu, ci + gj.x);
   a.vmax = fmaxf(a.vmax, in ? vs : 0.f);
+  a.lap = fmaf(gj.z * (ui - gj.y), dw * rinv, a.lap);
+}
+
+// The tile loop's pair: grad_pair plus membership of the symmetric force set,
+// min(q_i, q_j) < 2 (qj = r / h_j; fp64 inside the band `sband`).
+template <class Exact, class ExactS>
+__device__ __forceinline__ void grad_pair_sym(GradAcc& a, float dx, float dy, float dz, float hinv, float hinvj,
+                                              float qband, float sband, const float4& vi, float ci, float ui, float beta,
+                                              const float4& vj, const float4& gj, Exact&& exact, ExactS&& exact_s) {
+  const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+  const float rinv = rinv_safe(r2);
+  const float r = r2 * rinv;
+  const float q = r * hinv;
+  const float d = q - 2.f;
+  int in = neg(d);
+  if (fabsf(d) < qband) in = exact();
+  const float ds = fminf(q, r * hinvj) - 2.f;
+  int ins = neg(ds);
+  if (fabsf(ds) < sband) ins = exact_s();
+  a.nn += in + (ins << 16);
+  const float tq = fmaxf(-d, 0.f), sq = fmaxf(1.f - q, 0.f);
+  const float dw = fmaf(3.f * sq, sq, -0.75f * tq * tq);  // M4 w'(q)
+  const float vr = fmaf(vi.z - vj.z, dz, fmaf(vi.y - vj.y, dy, (vi.x - vj.x) * dx));
+  const float mu = fminf(vr, 0.f) * rinv;
+  const float vs = fmaf(-beta, mu, ci + gj.x);
+  a.vmax = fmaxf(a.vmax, in ? vs : 0.f);
+  a.vmaxs = fmaxf(a.vmaxs, ins ? vs : 0.f);
   a.lap = fmaf(gj.z * (ui - gj.y), dw * rinv, a.lap);
 }
 
@@ -220,7 +254,7 @@ __device__ __forceinline__ int grad_epilogue(const DevPhys& ph, const DevState& 
   const float f = fin.x, P = fin.y;
   s.fr1[gi] = make_float4(P / (rho * rho), -0.75f * f * hinv * hinv * hinv * hinv / kPi, ci, rho);
   s.fr2[gi] = make_float4(fin.w, P > 0.f ? P * ac : -ac, ui, av);
-  return a.nn - 1;
+  return (a.nn & 0xffff) - 1;
 }
 
 // ------------------------------------------------------------ force (Eqs. 7, 17-24) ----
@@ -284,12 +318,56 @@ __device__ __forceinline__ void force_pair(ForceAcc& acc, float dx, float dy, fl
   // alpha_c,ij (Eq. 20): (P_i ac_i + P_j ac_j) / (P_i + P_j), or the mean when
   // P_i + P_j = 0 (R13; the records then hold -alpha_c)
   const float Psum = I.P + J.P;
-  const float acij = __fdividef(I.b.y + J.b.y, Psum > 0.f ? Psum : -2.f);
+  const float acij = Psum > 0.f ? __fdividef(fmaxf(I.b.y, 0.f) + fmaxf(J.b.y, 0.f), Psum) : -0.5f * (I.b.y + J.b.y);
   const float vc = fabsf(vrr) + sqrtf(2.f * fabsf(I.P - J.P) * irs);
   const float D = acij * vc * (I.b.z - J.b.z) * (gs * irs);
   acc.du = fmaf(J.v.w, fmaf(fmaf(-0.125f, X, AgI), vrr, D), acc.du);
   vs_out = vs;
   in_out = in;
+}
+
+// Both sides of the unordered pair (i, j) (pair-once force loop), r_ij = (dx, dy, dz) = r_i - r_j:
+// the same terms as force_pair, i's added to acc (a_i, du_i), j's returned in jo (a_j, du_j):
+//   a_i -= m_j T r_ij / r,  a_j += m_i T r_ij / r  (Eq. 17: antisymmetric, momentum exact),
+//   du_i += m_j [(A_i g_i + Pi gbar / 2)(v_ij . r_hat) + D_ij],
+//   du_j += m_i [(A_j g_j + Pi gbar / 2)(v_ij . r_hat) - D_ij]  (v_ji . r_ji = v_ij . r_ij, D_ji = -D_ij).
+// Membership needs no test: g_i = g_j = 0 beyond both supports, so every term vanishes.
+// Returns whether the pair has any term (g_i + g_j != 0).
+__device__ __forceinline__ bool force_pair2(float4& acc, float4& jo, float dx, float dy, float dz, const ForceSide& I,
+                                            const ForceSide& J, float beta) {
+  const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+  const float rinv = rinv_safe(r2);
+  const float r = r2 * rinv;
+  const float gI = I.a.y * m4_dwp(r * I.hinv);  // g_i = G_i r = f_i dW/dr(h_i)
+  const float gJ = J.a.y * m4_dwp(r * J.hinv);
+  const float vr = fmaf(I.v.z - J.v.z, dz, fmaf(I.v.y - J.v.y, dy, (I.v.x - J.v.x) * dx));
+  const float vrr = vr * rinv;
+  const float mu = fminf(vrr, 0.f);
+  const float vs = fmaf(-beta, mu, I.a.z + J.a.z);
+  const float irs = __fdividef(1.f, I.a.w + J.a.w);
+  const float gs = gI + gJ;
+  const float gsr = gs * irs;
+  // X = 4 abar mu v_sig (g_i + g_j) / (rho_i + rho_j):  Pi_ij gbar = -X / 4
+  const float X = ((I.b.w + J.b.w) * (I.b.x + J.b.x)) * (mu * vs) * gsr;
+  const float AgI = I.a.x * gI, AgJ = J.a.x * gJ;
+  const float Tr = fmaf(-0.25f, X, AgI + AgJ) * rinv;  // S_ij = T / r
+  const float mTi = J.v.w * Tr, mTj = I.v.w * Tr;
+  acc.x = fmaf(-mTi, dx, acc.x);
+  acc.y = fmaf(-mTi, dy, acc.y);
+  acc.z = fmaf(-mTi, dz, acc.z);
+  jo.x = mTj * dx;
+  jo.y = mTj * dy;
+  jo.z = mTj * dz;
+  // alpha_c,ij (Eq. 20): (P_i ac_i + P_j ac_j) / (P_i + P_j), or the mean when P_i + P_j = 0
+  // (R13; the records hold -alpha_c when P = 0, which contributes nothing to the weighted sum)
+  const float Psum = I.P + J.P;
+  const float acij = Psum > 0.f ? __fdividef(fmaxf(I.b.y, 0.f) + fmaxf(J.b.y, 0.f), Psum) : -0.5f * (I.b.y + J.b.y);
+  const float vc = fabsf(vrr) + sqrtf(2.f * fabsf(I.P - J.P) * irs);
+  const float D = acij * vc * (I.b.z - J.b.z) * gsr;
+  const float hX = -0.125f * X;
+  acc.w = fmaf(J.v.w, fmaf(hX + AgI, vrr, D), acc.w);
+  jo.w = I.v.w * fmaf(hX + AgJ, vrr, -D);
+  return gs != 0.f;
 }
 
 }  // namespace sph

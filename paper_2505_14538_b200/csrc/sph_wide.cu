@@ -303,7 +303,9 @@ __global__ void __launch_bounds__(256) k_wide_force(DevGrid g, DevPhys ph, DevSt
     } else {
       seen = within(cxi, cxj, 1, g.nx) && within(cyi, cyj, 1, g.ny) && within(czi, czj, 1, g.nz);
     }
-    if (!seen && j != i) {
+    // j's side of the pair: a tile particle never evaluates a pair with a wide partner (k_lists
+    // keeps those out of its force part), a wide one only if its own list holds i
+    if (j != i && (!jwide || !seen)) {
       // j's side of the pair (r_ji = -r_ij): the same symmetric terms, its own accumulators
       ForceAcc b{0.f, 0.f, 0.f, 0.f, 0.f, 0};
       float vs2;
@@ -313,7 +315,8 @@ __global__ void __launch_bounds__(256) k_wide_force(DevGrid g, DevPhys ph, DevSt
       atomicAdd(&s.acc[j].y, b.ay);
       atomicAdd(&s.acc[j].z, b.az);
       atomicAdd(&s.acc[j].w, b.du);
-      if (in2) {
+      // v_sig and N_force of a partner that listed i already hold the pair (gradient loop)
+      if (in2 && !seen) {
         atomicMax(reinterpret_cast<int*>(&s.vsig[j]), __float_as_int(vs2));
         atomicAdd(&s.countf[j], 1);
         dt_candidate(ph, ctr, hj, vs2);
@@ -338,7 +341,7 @@ __global__ void __launch_bounds__(256) k_wide_force(DevGrid g, DevPhys ph, DevSt
   dt_candidate(ph, ctr, h, a.vmax);
   if (!(isfinite(a.vmax) && isfinite(a.ax) && isfinite(a.ay) && isfinite(a.az) && isfinite(a.du)))
     atomicExch(&ctr->nonfinite, 1);
-  atomicAdd(&ctr->pairs, (unsigned long long)(a.nn - 1) + (unsigned long long)scattered);
+  (void)scattered;  // (N_force is summed over all particles by k_force_fin)
 }
 
 }  // namespace

@@ -1023,6 +1023,13 @@ sph_status rebuild_impl(sph_ctx* c) {
   const float max_off = std::max(std::max((0.5f * g.bx + 1.0f) * g.side[0], (0.5f * g.by + 1.0f) * g.side[1]),
                                  (0.5f * g.KZ + 1.0f) * g.side[2]);
   g.eabs = 4.0f * ulp_of(max_off) * 2.0f;  // 8 x (ulp/2): two coordinates per difference, with margin
+  {
+    // k_lists tests candidates in fp16 (unit roundoff 2^-11) on coordinates of magnitude <= C
+    // cells: each coordinate difference errs by <= 2^-11 (2 C + |d|), |d| <= ~1.5 cells near
+    // the list radius, the squares and sums by a few more ulps; the margin covers all of it
+    const float C = max_off / g.side_min;
+    g.lpad = std::ldexp(1.0f, -11) * (1.7321f * (2.0f * C + 3.0f) + 4.0f);
+  }
   if (getenv("SPH_DEBUG")) {
     std::vector<int> cs(std::min(g.ncells, 1 << 24) + 1);  // (the monotonicity check on small grids only)
     cudaMemcpyAsync(cs.data(), c->cell_start, cs.size() * 4, cudaMemcpyDeviceToHost, c->stream);

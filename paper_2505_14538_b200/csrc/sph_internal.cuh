@@ -47,6 +47,7 @@ struct DevGrid {
   float side[3];      // cell side per axis
   float side_min;
   float eabs;         // 8 x max rounding error of a tile coordinate (length units)
+  float lpad;         // k_lists' fp16 candidate test: list radius margin (units of side_min)
   int zbits;          // particles of a cell sorted by the top zbits of their z inside the cell
   float zbucket;      // side_z 2^-zbits: z order inside a cell holds up to this
   // Slab decomposition along x.  The rank owns x in [x_lo, x_lo + wfix) on the 2^-32 grid,

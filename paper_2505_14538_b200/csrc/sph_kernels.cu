@@ -32,6 +32,7 @@
 // in f32 with a rigorous band and re-decided in fp64 inside it, so counts equal the
 // definition exactly.
 #include <algorithm>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <math_constants.h>
 #include <stdint.h>
@@ -255,9 +256,9 @@ __device__ __forceinline__ void stage_mbar_init() {
 // prologue); lane 0 of every warp issues a share of them (the copies of one lane issue one
 // after another).  Every thread then waits on the mbarrier (and on its own earlier cp.async
 // copies), and the block synchronises.
-template <class SS>
-__device__ __forceinline__ void stage_records(const SS& S, int nseg, int nrec16, const float4* const* src16,
-                                              const int* o16, int ntile) {
+template <int nrec16, class SS>
+__device__ __forceinline__ void stage_records(const SS& S, int nseg, const float4* const* src16, const int* o16,
+                                              int ntile) {
   const uint32_t mbar = stage_mbar();
   if (threadIdx.x == 0)
     asm volatile("{ .reg .b64 st; mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1; }" ::"r"(mbar),
@@ -272,10 +273,16 @@ __device__ __forceinline__ void stage_records(const SS& S, int nseg, int nrec16,
       const int k = c % nseg, r = c / nseg;
       const int4 sg = S.seg[k];
       if (sg.z <= 0) continue;
+      // (record r by selects: a dynamic index into src16 / o16 would put them in local memory)
+      const float4* src = src16[0];
+      int o = o16[0];
+#pragma unroll
+      for (int q = 1; q < nrec16; ++q)
+        if (r == q) { src = src16[q]; o = o16[q]; }
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-              sbase + 16u * (uint32_t)(o16[r] + sg.x)),
-          "l"(src16[r] + sg.y), "r"(16u * (uint32_t)sg.z), "r"(mbar)
+              sbase + 16u * (uint32_t)(o + sg.x)),
+          "l"(src + sg.y), "r"(16u * (uint32_t)sg.z), "r"(mbar)
           : "memory");
     }
   }
@@ -342,10 +349,16 @@ constexpr int kCellRows = 16;  // k_bank grid rows per list (longer lists keep t
 constexpr int kZSub = 16;      // z sub-buckets per cell in k_lists' window table
 // k_lists' dynamic shared memory after the pair array: the per-warp list rings and the group
 // counts (holding one z sub-bucket byte per slot before the walk), then the z window table
-__host__ __device__ __forceinline__ size_t lists_ring_bytes(const DevGrid& g, int nw) {
+// k_lists' dynamic shared memory: region A (the staged raw records; after the conversion to
+// the fp16 candidate records, the per-warp list rings and the group counts), the candidate
+// records P16, the slots' z sub-bucket bytes, the z window table, the wide flags
+__host__ __device__ __forceinline__ size_t lists_a_bytes(const DevGrid& g, int nw) {
+  const size_t raw = (size_t)((g.tcap + kNSent + 1) & ~1) * 16;
   const size_t ring = (size_t)nw * kListRows * 32 * 2 + (size_t)(g.icap + 1) * 8;
-  const size_t zsb = (size_t)g.tcap + 16;
-  return ((ring > zsb ? ring : zsb) + 15) & ~(size_t)15;
+  return ((raw > ring ? raw : ring) + 15) & ~(size_t)15;
+}
+__host__ __device__ __forceinline__ size_t lists_slot_bytes(const DevGrid& g) {
+  return ((size_t)g.tcap + kNSent + 15) & ~(size_t)15;
 }
 __host__ __device__ __forceinline__ size_t lists_zw_bytes(const DevGrid& g) {
   return ((((size_t)(g.bx + 2) * (g.by + 2) * (g.KZ + 2) * kZSub + 1) * 2 + 15) & ~(size_t)15);
@@ -412,11 +425,15 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
   float* P = reinterpret_cast<float*>(smem4);
   // z window table: s_zw[16 c + k] = first slot of tile cell c in z sub-bucket >= k (16 per
   // cell, the top 4 z bits inside the cell -- the sort key's, so exact), s_zw[16 nct] = end
-  unsigned short* s_zw = reinterpret_cast<unsigned short*>(reinterpret_cast<char*>(P) + (size_t)NP * 32 +
-                                                           lists_ring_bytes(g, nw));
+  // (layout: lists_a_bytes)
+  const size_t abytes = lists_a_bytes(g, nw);
+  char* ring0 = reinterpret_cast<char*>(P);  // (after the conversion below)
+  uint4* P16 = reinterpret_cast<uint4*>(reinterpret_cast<char*>(P) + abytes);
+  unsigned char* zsb = reinterpret_cast<unsigned char*>(P16 + NP);
+  unsigned short* s_zw = reinterpret_cast<unsigned short*>(zsb + lists_slot_bytes(g));
   // wide particles (adaptive grid): one flag byte per slot after the window table (a wide
   // partner's pair is never in the force part: k_wide_force applies it to both sides)
-  unsigned char* wfl = reinterpret_cast<unsigned char*>(s_zw) + lists_zw_bytes(g);
+  unsigned char* wfl = reinterpret_cast<unsigned char*>(s_zw) + lists_zw_bytes(g);  // (lists_slot_bytes)
   if (kWide) {
     const int lane_ = threadIdx.x & 31;
     for (int k = threadIdx.x >> 5; k < nseg; k += nw) {
@@ -427,32 +444,40 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
   {
     const float4* src[1] = {reinterpret_cast<const float4*>(s.xh)};
     const int o16[1] = {0};
-    stage_records(S, nseg, 1, src, o16, T.ntile);
+    stage_records<1>(S, nseg, src, o16, T.ntile);
   }
   const float Hfac = (1.f + g.skin) * ph.gamma_k;
   unsigned int hm = 0u;
   // each slot's z sub-bucket (bytes; the region of the list ring, not yet in use)
-  unsigned char* zsb = reinterpret_cast<unsigned char*>(P) + (size_t)NP * 32;
   const int zb4 = min(g.zbits, 4);
   const uint32_t zmask = (1u << (4 - zb4)) - 1u;  // (coarse sort keys: fewer sub-buckets)
+  // Candidate records in fp16, pair-interleaved: P16[p] = (x, y, z, H^2) of slots 2p, 2p+1 as
+  // half2, coordinates in units of the smallest cell side from the block centre.  The test
+  // r^2 < max(H_i^2, H_j^2) in half precision only has to keep every pair of the f32 list
+  // criterion: each list radius carries g.lpad cells for the fp16 rounding of the coordinates
+  // and of the squares (host: from the largest tile offset), and H^2 is rounded up.  The extra
+  // entries are skin entries (exactly zero in every loop).
+  const float cs = 1.f / g.side_min;
   for (int pp = threadIdx.x; pp < NP; pp += blockDim.x) {
     float4 q[2];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int t = 2 * pp + u;
-      q[u] = make_float4(kFar, kFar, kFar, 0.f);
+      q[u] = make_float4(3.0e4f, 3.0e4f, 3.0e4f, 0.f);
       if (t < T.ntile) {
         const uint4 x = reinterpret_cast<const uint4*>(smem4)[t];
         const float3 r = rel_pos(g, T, x);
-        const float Hs = Hfac * __uint_as_float(x.w);
+        const float Hs = Hfac * __uint_as_float(x.w) * cs + g.lpad;
         hm = max(hm, x.w);
-        q[u] = make_float4(r.x, r.y, r.z, Hs * Hs);
+        q[u] = make_float4(r.x * cs, r.y * cs, r.z * cs, Hs * Hs);
         zsb[t] = (unsigned char)((((uint32_t)((unsigned long long)x.z * (unsigned)g.nz)) >> 28) & ~zmask);
       }
     }
-    // (the raw records of this pair are read before the pair's 32 bytes are rewritten)
-    reinterpret_cast<float4*>(P)[2 * pp] = make_float4(q[0].x, q[1].x, q[0].y, q[1].y);
-    reinterpret_cast<float4*>(P)[2 * pp + 1] = make_float4(q[0].z, q[1].z, q[0].w, q[1].w);
+    const __half2 hx = __floats2half2_rn(q[0].x, q[1].x), hy = __floats2half2_rn(q[0].y, q[1].y),
+                  hz = __floats2half2_rn(q[0].z, q[1].z);
+    const __half2 hh = __halves2half2(__float2half_ru(q[0].w), __float2half_ru(q[1].w));
+    P16[pp] = make_uint4(*reinterpret_cast<const uint32_t*>(&hx), *reinterpret_cast<const uint32_t*>(&hy),
+                         *reinterpret_cast<const uint32_t*>(&hz), *reinterpret_cast<const uint32_t*>(&hh));
   }
   hm = warp_max((int)hm);
   if ((threadIdx.x & 31) == 0) atomicMax(&s_hmax, hm);
@@ -493,7 +518,7 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
   __syncthreads();
   // window half-width: the largest list radius of any pair in the tile, plus the z-order
   // bucket and the coordinate rounding bound
-  const float zpad = Hfac * __uint_as_float(s_hmax) + g.zbucket + g.eabs;
+  const float zpad = Hfac * __uint_as_float(s_hmax) + g.zbucket + g.eabs + 2.f * g.lpad * g.side_min;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t sP = (uint32_t)__cvta_generic_to_shared(P);
   const float sub_scale = (float)kZSub / g.side[2];
@@ -504,8 +529,8 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
   };
   // kListRows x 32-lane uint16 ring per warp after the pair array (row stride 64 bytes):
   // entries leave 8 at a time from 512-byte aligned ring positions, nothing is moved
-  const uint32_t buf = sP + (uint32_t)NP * 32u + (uint32_t)(warp * kListRows * 32 + lane) * 2u;
-  int* grp = reinterpret_cast<int*>(reinterpret_cast<char*>(P) + (size_t)NP * 32 + (size_t)nw * kListRows * 32 * 2);
+  const uint32_t buf = sP + (uint32_t)(warp * kListRows * 32 + lane) * 2u;
+  int* grp = reinterpret_cast<int*>(ring0 + (size_t)nw * kListRows * 32 * 2);
   int* grpF = grp + (g.icap + 1);  // force-part groups
   constexpr uint32_t kRing = kListRows * 64u;
   const int ni = s_cp[nicell];
@@ -531,11 +556,10 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
     const int col = lo / (T.nzt - 2), zz = lo - col * (T.nzt - 2) + 1;
     const int ti = s_ct[lo] + (kk - s_cp[lo]);
     const int gi = s_cg[lo] + (kk - s_cp[lo]);
-    const float* pi = P + (ti >> 1) * 8 + (ti & 1);
-    const float2 nX = make_float2(-pi[0], -pi[0]), nY = make_float2(-pi[2], -pi[2]);
-    const float zi = pi[4];
-    const float2 nZ = make_float2(-zi, -zi);
-    const float Hi2 = pi[6];
+    const __half* pi = reinterpret_cast<const __half*>(P16 + (ti >> 1)) + (ti & 1);
+    const __half2 nX = __half2half2(__hneg(pi[0])), nY = __half2half2(__hneg(pi[2])),
+                  nZ = __half2half2(__hneg(pi[4])), Hi2 = __half2half2(pi[6]);
+    const float zi = __half2float(pi[4]) * g.side_min;  // (length units, for the z windows)
     const int tc = S.tc[col];
     const float zc = zbound(T.z0 + zz - 2);  // bottom of tile cell zz - 1
     uint4* dst = reinterpret_cast<uint4*>(s.nbr_raw + (size_t)gi * g.lcap);
@@ -568,10 +592,15 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
       }
     };
     auto test_one = [&](int t) {  // a single candidate (window ends)
-      const float* q = P + (t >> 1) * 8 + (t & 1);
-      const float dx = q[0] + nX.x, dy = q[2] + nY.x, dz = q[4] + nZ.x;
-      const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-      hit(r2 < Hi2 || r2 < q[6], t);
+      const uint4 A = P16[t >> 1];
+      __half2 dx = __hadd2(*reinterpret_cast<const __half2*>(&A.x), nX);
+      __half2 dy = __hadd2(*reinterpret_cast<const __half2*>(&A.y), nY);
+      __half2 dz = __hadd2(*reinterpret_cast<const __half2*>(&A.z), nZ);
+      __half2 r2 = __hmul2(dx, dx);
+      r2 = __hfma2(dy, dy, r2);
+      r2 = __hfma2(dz, dz, r2);
+      const unsigned mk = __hlt2_mask(r2, __hmax2(Hi2, *reinterpret_cast<const __half2*>(&A.w)));
+      hit(((mk >> (16 * (t & 1))) & 1u) != 0u, t);
     };
     auto drain = [&]() {  // buffered entries -> global memory, 8 at a time
       while (((w - rd) & (kRing - 1u)) >= 8u * 64u) {
@@ -607,16 +636,16 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
           const int pn = min(e >> 1, p0 + 8);
 #pragma unroll 4
           for (int pp = p0; pp < pn; ++pp) {
-            const float4 A = reinterpret_cast<const float4*>(P)[2 * pp];
-            const float4 B = reinterpret_cast<const float4*>(P)[2 * pp + 1];
-            const float2 dx = __fadd2_rn(make_float2(A.x, A.y), nX);
-            const float2 dy = __fadd2_rn(make_float2(A.z, A.w), nY);
-            const float2 dz = __fadd2_rn(make_float2(B.x, B.y), nZ);
-            float2 r2 = __fmul2_rn(dx, dx);
-            r2 = __ffma2_rn(dy, dy, r2);
-            r2 = __ffma2_rn(dz, dz, r2);
-            hit(r2.x < fmaxf(Hi2, B.z), 2 * pp);
-            hit(r2.y < fmaxf(Hi2, B.w), 2 * pp + 1);
+            const uint4 A = P16[pp];  // (one 16-byte load, packed half2 arithmetic: two candidates)
+            const __half2 dx = __hadd2(*reinterpret_cast<const __half2*>(&A.x), nX);
+            const __half2 dy = __hadd2(*reinterpret_cast<const __half2*>(&A.y), nY);
+            const __half2 dz = __hadd2(*reinterpret_cast<const __half2*>(&A.z), nZ);
+            __half2 r2 = __hmul2(dx, dx);
+            r2 = __hfma2(dy, dy, r2);
+            r2 = __hfma2(dz, dz, r2);
+            const unsigned mk = __hlt2_mask(r2, __hmax2(Hi2, *reinterpret_cast<const __half2*>(&A.w)));
+            hit((mk & 1u) != 0u, 2 * pp);
+            hit((mk >> 16) != 0u, 2 * pp + 1);
           }
           drain();
         }
@@ -655,7 +684,7 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
       s.ncount[gi] = fits ? (nF | (nL << 16) | (kTag ? 0 : (int)0x80000000u)) : 0;
       mygrp = fits ? gF + gL : 0;
       mygrpF = fits ? gF : 0;
-      s.hbuild[gi] = sqrtf(Hi2) / Hfac;
+      s.hbuild[gi] = __uint_as_float(__ldg(&s.xh[gi].w));
     }
     if (k < ni) {
       grp[k] = mygrp;
@@ -1039,7 +1068,7 @@ __global__ void __launch_bounds__(256, 3) k_density(DevGrid g, DevPhys ph, DevSt
   {
     const float4* src[2] = {reinterpret_cast<const float4*>(s.xh), s.vm};
     const int o16[2] = {0, O1};
-    stage_records(S, nseg, 2, src, o16, T.ntile);
+    stage_records<2>(S, nseg, src, o16, T.ntile);
   }
   for (int t = threadIdx.x; t < T.ntile; t += blockDim.x) {
     const uint4 x = reinterpret_cast<const uint4*>(smem4)[t];
@@ -1156,7 +1185,7 @@ __global__ void __launch_bounds__(256, 3) k_gradient(DevGrid g, DevPhys ph, DevS
   {
     const float4* src[3] = {reinterpret_cast<const float4*>(s.xh), s.vm, s.gq};
     const int o16[3] = {0, O1, O2};
-    stage_records(S, nseg, 3, src, o16, T.ntile);
+    stage_records<3>(S, nseg, src, o16, T.ntile);
   }
   {
     unsigned int hm = 0u;
@@ -1265,6 +1294,12 @@ __device__ __forceinline__ void red_add4(float4* p, const float4& v) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                : "memory");
 }
+// the same under a predicate (no branch around it in the pair loop)
+__device__ __forceinline__ void red_add4_if(float4* p, const float4& v, bool on) {
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %5, 0; @q red.global.add.v4.f32 [%0], {%1, %2, %3, %4}; }" ::"l"(p),
+               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"((uint32_t)on)
+               : "memory");
+}
 __device__ __forceinline__ int lds1(uint32_t a) {
   int v;
   asm("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
@@ -1293,7 +1328,7 @@ __global__ void __launch_bounds__(512, 1) k_force(DevGrid g, DevPhys ph, DevStat
   {
     const float4* src[4] = {reinterpret_cast<const float4*>(s.xh), s.vm, s.fr1, s.fr2};
     const int o16[4] = {0, O1, O2, O3};
-    stage_records(S, nseg, 4, src, o16, T.ntile);
+    stage_records<4>(S, nseg, src, o16, T.ntile);
   }
   for (int t = threadIdx.x; t < T.ntile; t += blockDim.x) {
     const uint4 x = reinterpret_cast<const uint4*>(smem4)[t];
@@ -1344,8 +1379,8 @@ __global__ void __launch_bounds__(512, 1) k_force(DevGrid g, DevPhys ph, DevStat
         J.b = lds4(sb3 + o);
         J.P = J.a.x * J.a.w * J.a.w;
         float4 jo;
-        if (force_pair2(a, jo, pi4.x - p.x, pi4.y - p.y, pi4.z - p.z, I, J, ph.beta))
-          red_add4(s.acc + lds1(sbg + ((uint32_t)j << 2)), jo);
+        const bool term = force_pair2(a, jo, pi4.x - p.x, pi4.y - p.y, pi4.z - p.z, I, J, ph.beta);
+        red_add4_if(s.acc + lds1(sbg + ((uint32_t)j << 2)), jo, term);
       }),
       [&](int, int) { red_add4(s.acc + gi, a); });
 }
@@ -1482,8 +1517,8 @@ cudaError_t launch_block_run(const DevGrid& g, const DevState& s, uint8_t* flag,
 
 size_t lists_smem(const DevGrid& g) {
   const int nw = g.lists_warps > 0 ? g.lists_warps : kNW;
-  return (size_t)((g.tcap + kNSent + 1) & ~1) * 16 + lists_ring_bytes(g, nw) + lists_zw_bytes(g) +
-         (((size_t)g.tcap + kNSent + 15) & ~(size_t)15);
+  return lists_a_bytes(g, nw) + (size_t)((g.tcap + kNSent + 1) >> 1) * 16 + lists_slot_bytes(g) +
+         lists_zw_bytes(g) + lists_slot_bytes(g);
 }
 size_t density_smem(const DevGrid& g) { return (size_t)(g.tcap + kNSent) * (2 * 16) + walk_bytes<DenAcc>(g.icap); }
 size_t gradient_smem(const DevGrid& g) { return (size_t)(g.tcap + kNSent) * (3 * 16) + walk_bytes<GradAcc>(g.icap); }

@@ -96,12 +96,14 @@ struct DevState {
   // neighbour lists: tile-relative uint16 slots in two parts, each padded with sentinel slots
   // (tcap .. tcap+7) to a multiple of 8 and laid out in ROWS of 8 whose entry w lies in
   // shared-memory bank group w (slot mod 8; k_bank, sph_kernels.cu); [n][lcap]:
-  //   rows [0, nF8)          the FORCE part: the pairs this particle evaluates once for both sides
+  //   rows [0, nL8)          the rest (self included): density and gradient walk both parts
+  //   rows [nL8, nL8 + nF8)  the FORCE part: the pairs this particle evaluates once for both sides
   //                          (partner in the "upper" half of the cell stencil, or a ghost)
-  //   rows [nF8, nF8 + nL8)  the rest (self included): density and gradient walk both parts
+  // Lists without ghost planes or wide particles leave k_lists in this layout in slot order
+  // (no bank-aware rows: ncount bit 31); the others go through k_bank.
   uint16_t* nbr;
-  uint16_t* nbr_raw;  // k_lists' output before k_bank: natural order, bit 15 = force part
-  int32_t* ncount;    // nF | nL << 16: real entries of the two parts (k_lists)
+  uint16_t* nbr_raw;  // k_lists' tagged output before k_bank: natural order, bit 15 = force part
+  int32_t* ncount;    // nF | nL << 16 | final << 31: real entries of the two parts (k_lists)
   float* hbuild;      // h when the list was built
   // wide particles (adaptive cell side, sph_wide.cu): support past the cell side; nullptr /
   // 0 when there are none

@@ -562,7 +562,8 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
     const float zi = __half2float(pi[4]) * g.side_min;  // (length units, for the z windows)
     const int tc = S.tc[col];
     const float zc = zbound(T.z0 + zz - 2);  // bottom of tile cell zz - 1
-    uint4* dst = reinterpret_cast<uint4*>(s.nbr_raw + (size_t)gi * g.lcap);
+    // (kTag: k_bank lays the tagged list out; else the list leaves in its final layout)
+    uint4* dst = reinterpret_cast<uint4*>((kTag ? s.nbr_raw : s.nbr) + (size_t)gi * g.lcap);
     if (valid && kWide && s.wide[gi]) {  // a wide particle's list is built by k_wide_lists
       s.ncount[gi] = 0;
       valid = false;
@@ -663,7 +664,9 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
         // window is cut after the particle's own slot and the count there taken
         if (!kTag && d == 4) {
           scan(a, min(e, ti + 1));
+          // the rest of the list is the force part: close the row with sentinels
           c1 = flushed + (int)(((w - rd) & (kRing - 1u)) >> 6);
+          for (int k = c1; k & 7; ++k) hit(true, g.tcap + (k & 7));
           scan(max(a, ti + 1), e);
         } else {
           scan(a, e);
@@ -675,12 +678,13 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
       const int cntp = (cnt + 7) & ~7;
       for (; nb < ((nb + 7) & ~7); ++nb) hit(true, g.tcap + (nb & 7));
       drain();
-      const int nF = kTag ? (int)((nF2 & 0xffffu) + (nF2 >> 16)) : cnt - c1, nL = cnt - nF;
+      const int nF = kTag ? (int)((nF2 & 0xffffu) + (nF2 >> 16)) : cnt - ((c1 + 7) & ~7);
+      const int nL = kTag ? cnt - nF : c1;
       const int gF = (nF + 7) >> 3, gL = (nL + 7) >> 3;  // k_bank pads each part to rows of 8
       const int need = max(cntp, 8 * (gF + gL));
       if (need > g.lcap) over = max(over, need);
       const bool fits = need <= g.lcap;
-      // bit 31: untagged, the first nL raw entries are the non-force part
+      // bit 31: the list is already in its final layout (no k_bank pass)
       s.ncount[gi] = fits ? (nF | (nL << 16) | (kTag ? 0 : (int)0x80000000u)) : 0;
       mygrp = fits ? gF + gL : 0;
       mygrpF = fits ? gF : 0;
@@ -706,18 +710,18 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
   }
 }
 
-// k_bank: k_lists' natural-order list (nbr_raw) -> the two-part bank-aware layout of nbr
-// (sph_internal.cuh): rows [0, RF) the force part, rows [RF, RF + RL) the rest, each part in
-// bank-aware rows ("Bank-aware rows" above).  The parts come either as the raw list's tail /
-// head (ncount bit 31: the list is in slot order) or by tag (bit 15 of an entry: force part).
-// One lane per list, one pass over the raw list: the t-th real entry of group b of part p
-// goes straight to cell (row0_p + t, b) of the lane's grid in shared memory while
-// t < R_p = ceil(n_p / 8), past that into the part's overflow queue.  The rows are then
-// written out cell by cell: a grid entry where the column has one, else the part's next
-// queued entry, else the column's sentinel (tcap + its bank group).  Counts are 4-bit fields
-// (8 groups per 32-bit word per part).  A list of more than kCellRows rows, a group of more
-// than 15 entries or more than kBankQ overflowing entries in a part takes the natural-order
-// path (still split in the two parts).
+// k_bank: a TAGGED list of k_lists (ghost planes or wide particles present: the force part
+// is not a tail of the slot order) -> the two-part layout of nbr (sph_internal.cuh): rows
+// [0, RL) the non-force part, rows [RL, RL + RF) the force part, each part in bank-aware rows
+// ("Bank-aware rows" above).  One lane per list, one pass over the raw list: the t-th real
+// entry of group b of part p goes straight to cell (row0_p + t, b) of the lane's grid in
+// shared memory while t < R_p = ceil(n_p / 8), past that into the part's overflow queue.  The
+// rows are then written out cell by cell: a grid entry where the column has one, else the
+// part's next queued entry, else the column's sentinel (tcap + its bank group).  Counts are
+// 4-bit fields (8 groups per 32-bit word per part).  A list of more than kCellRows rows, a
+// group of more than 15 entries or more than kBankQ overflowing entries in a part takes the
+// natural-order path (still split in the two parts).  Untagged lists (ncount bit 31) left
+// k_lists in their final layout and are skipped.
 constexpr int kBankThreads = 256;
 constexpr int kBankQ = 8;  // overflow queue entries per lane and part
 __global__ void __launch_bounds__(kBankThreads) k_bank(int i0, int n, DevGrid g, DevState s) {
@@ -726,9 +730,8 @@ __global__ void __launch_bounds__(kBankThreads) k_bank(int i0, int n, DevGrid g,
   const int i = i0 + blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= i0 + n) return;
   const int packed = s.ncount[i];
+  if (packed <= 0) return;  // (final already, or no list)
   const int nF = packed & 0xffff, nL = (packed >> 16) & 0x7fff;
-  const bool bypos = packed < 0;  // untagged: raw entries [0, nL) are the non-force part
-  if (nF + nL == 0) return;
   const int RF = (nF + 7) >> 3, RL = (nL + 7) >> 3, Rraw = (nF + nL + 7) >> 3;
   const uint4* raw = reinterpret_cast<const uint4*>(s.nbr_raw + (size_t)i * g.lcap);
   uint4* lst = reinterpret_cast<uint4*>(s.nbr + (size_t)i * g.lcap);
@@ -740,28 +743,7 @@ __global__ void __launch_bounds__(kBankThreads) k_bank(int i0, int n, DevGrid g,
   bool grid_ok = RF + RL <= kCellRows;
   uint32_t cF = 0u, cL = 0u;  // 4-bit entry counts of the 8 groups, per part
   int qF = 0, qL = 0;         // queued entries per part
-  if (grid_ok && bypos) {
-    // raw entries [lo, hi) of one part into its grid rows [row0, row0 + R)
-    auto place_range = [&](int lo, int hi, uint32_t& c, int& qn, uint32_t R, uint32_t row0, uint32_t qb) {
-      for (int r = lo >> 3; r < ((hi + 7) >> 3); ++r) {
-        const uint4 v = __ldg(raw + r);
-        const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t sl = (wv[k >> 1] >> (16 * (k & 1))) & 0xffffu, b = sl & 7u;
-          const int idx = 8 * r + k;
-          const bool real = idx >= lo && idx < hi;  // (padding sentinels lie past hi)
-          const uint32_t tb = (c >> (4u * b)) & 15u;
-          sts_u16_if(cell(row0 + tb, b), sl, real && tb < R);
-          sts_u16_if(qb + (uint32_t)min(qn, kBankQ - 1) * kStride, sl, real && tb >= R);
-          qn += (real && tb >= R) ? 1 : 0;
-          c += (real ? 1u : 0u) << (4u * b);
-        }
-      }
-    };
-    place_range(0, nL, cL, qL, (uint32_t)RL, (uint32_t)RF, qbL);
-    place_range(nL, nL + nF, cF, qF, (uint32_t)RF, 0u, qbF);
-  } else if (grid_ok) {
+  if (grid_ok) {
     const uint32_t rf = (uint32_t)RF, rl = (uint32_t)RL;
     for (int r = 0; r < Rraw; ++r) {
       const uint4 v = __ldg(raw + r);
@@ -775,7 +757,7 @@ __global__ void __launch_bounds__(kBankThreads) k_bank(int i0, int n, DevGrid g,
         const uint32_t tb = (c >> (4u * b)) & 15u;
         const uint32_t R = lpart ? rl : rf;
         const bool ovf = real && tb >= R;
-        sts_u16_if(cell((lpart ? rf : 0u) + tb, b), sl, real && tb < R);
+        sts_u16_if(cell((lpart ? 0u : rl) + tb, b), sl, real && tb < R);
         const int qn = lpart ? qL : qF;
         sts_u16_if((lpart ? qbL : qbF) + (uint32_t)min(qn, kBankQ - 1) * kStride, sl, ovf);
         if (lpart) qL += ovf ? 1 : 0; else qF += ovf ? 1 : 0;
@@ -783,8 +765,6 @@ __global__ void __launch_bounds__(kBankThreads) k_bank(int i0, int n, DevGrid g,
         if (lpart) cL += inc; else cF += inc;
       }
     }
-  }
-  if (grid_ok) {
     // (a group past 15 entries carries into the next field: the sums no longer match)
     uint32_t sF = 0u, sL = 0u;
 #pragma unroll
@@ -793,9 +773,9 @@ __global__ void __launch_bounds__(kBankThreads) k_bank(int i0, int n, DevGrid g,
   }
   if (grid_ok) {
 #pragma unroll 1
-    for (int p = 0; p < 2; ++p) {
-      const int R = p ? RL : RF, row0 = p ? RF : 0, qn = p ? qL : qF;
-      const uint32_t c = p ? cL : cF, qb = p ? qbL : qbF;
+    for (int p = 0; p < 2; ++p) {  // p = 0: the non-force part (rows from 0), 1: the force part
+      const int R = p ? RF : RL, row0 = p ? RL : 0, qn = p ? qF : qL;
+      const uint32_t c = p ? cF : cL, qb = p ? qbF : qbL;
       int cw[8];
 #pragma unroll
       for (int w = 0; w < 8; ++w) cw[w] = (int)((c >> (4 * w)) & 15u);
@@ -817,7 +797,7 @@ __global__ void __launch_bounds__(kBankThreads) k_bank(int i0, int n, DevGrid g,
   // natural order, split in the two parts (each padded with sentinels to a row of 8)
 #pragma unroll 1
   for (uint32_t p = 0; p < 2; ++p) {
-    int orow = p ? RF : 0, m = 0;
+    int orow = p ? RL : 0, m = 0;
     uint4 buf = make_uint4(0u, 0u, 0u, 0u);
     auto put = [&](uint32_t sl) {
       const int k = m & 7;
@@ -837,8 +817,7 @@ __global__ void __launch_bounds__(kBankThreads) k_bank(int i0, int n, DevGrid g,
       for (int k = 0; k < 8; ++k) {
         const uint32_t e = (wv[k >> 1] >> (16 * (k & 1))) & 0xffffu;
         const uint32_t sl = e & 0x7fffu;
-        const bool lpart = bypos ? 8 * r + k < nL : e < 0x8000u;
-        if (sl < tcap && lpart == (p == 1u)) put(sl);
+        if (sl < tcap && (e >= 0x8000u) == (p == 1u)) put(sl);
       }
     }
     while (m & 7) put(tcap + (uint32_t)(m & 7));
@@ -1315,9 +1294,14 @@ __global__ void __launch_bounds__(512, 1) k_force(DevGrid g, DevPhys ph, DevStat
   const int O1 = SP, O2 = 2 * SP, O3 = 3 * SP;
   int* GI = reinterpret_cast<int*>(smem4 + 4 * SP);
   int* pref = GI + ((SP + 3) & ~3);  // [icap + 1] force-part group prefix (k_lists)
+  int* prefA = pref + (g.icap + 1);  // [icap + 1] whole-list group prefix
   {
     const int* src = g.desc_prefF + (size_t)ba * (g.icap + 1);
-    for (int k = threadIdx.x; k <= T.ni; k += blockDim.x) cp_async4(pref + k, src + k);
+    const int* srcA = g.desc_pref + (size_t)ba * (g.icap + 1);
+    for (int k = threadIdx.x; k <= T.ni; k += blockDim.x) {
+      cp_async4(pref + k, src + k);
+      cp_async4(prefA + k, srcA + k);
+    }
     const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     for (int k = threadIdx.x >> 5; k < nseg; k += nw) {
       const int4 sg = S.seg[k];
@@ -1357,7 +1341,9 @@ __global__ void __launch_bounds__(512, 1) k_force(DevGrid g, DevPhys ph, DevStat
       T.ni, pref,
       [&](int k) {  // (list_of runs right before begin: the slot lookup is shared)
         i_slot(S, k, ti_c, gi);
-        return s.nbr + (size_t)gi * g.lcap;
+        // the force part follows the RL rows of the rest of the list
+        const int RL = (prefA[k + 1] - prefA[k]) - (pref[k + 1] - pref[k]);
+        return s.nbr + (size_t)gi * g.lcap + 8 * RL;
       },
       [&](int) {
         const int ti = ti_c;
@@ -1522,7 +1508,7 @@ size_t lists_smem(const DevGrid& g) {
 }
 size_t density_smem(const DevGrid& g) { return (size_t)(g.tcap + kNSent) * (2 * 16) + walk_bytes<DenAcc>(g.icap); }
 size_t gradient_smem(const DevGrid& g) { return (size_t)(g.tcap + kNSent) * (3 * 16) + walk_bytes<GradAcc>(g.icap); }
-size_t force_smem(const DevGrid& g) { return force_records_bytes(g.tcap) + (size_t)(g.icap + 1) * 4; }
+size_t force_smem(const DevGrid& g) { return force_records_bytes(g.tcap) + (size_t)(g.icap + 1) * 8; }
 
 cudaError_t launch_tile_sizes(const DevGrid& g, const int* cell_start, int* max_tile, int* max_i, uint8_t* flag,
                               cudaStream_t st) {
@@ -1551,7 +1537,8 @@ cudaError_t launch_lists(const DevGrid& g, const DevPhys& ph, const DevState& s,
 }
 
 cudaError_t launch_bank(int i0, int n, const DevGrid& g, const DevState& s, cudaStream_t st) {
-  if (n <= 0) return cudaSuccess;
+  // (k_lists tags lists, and leaves them to k_bank, only with ghost planes or wide particles)
+  if (n <= 0 || (g.periodic_x && !(s.wide != nullptr && s.n_wide > 0))) return cudaSuccess;
   const size_t sm = (size_t)(8 * kCellRows + 2 * kBankQ) * kBankThreads * 2;
   cudaError_t e = set_smem((const void*)k_bank, sm);
   if (e != cudaSuccess) return e;

@@ -36,24 +36,17 @@ def oracle_hydro(p, dt_ghost=1e-3, fixed_h=False, h_tol=1e-13, mode="cells", sam
     return o.hydro(st, dt_ghost=dt_ghost, first_step=True, fixed_h=fixed_h, sample=sample)
 
 
-def band_mask(p, h, R_factor=2.0, rel=1e-6):
-    """Particles with any pair inside |r_ij - H_i| < rel * h_i (north star exclusion band),
-    computed with the oracle's neighbour enumeration."""
-    st = oracle.State.from_particles(p)
-    g = oracle.Geometry(st.X, st.box, use_cells=True, min_side=R_factor * float(np.max(h)) * 1.01)
-    x = st.X.astype(np.int64)
-    L = st.box
-    bad = np.zeros(len(h), dtype=bool)
-    for i in range(len(h)):
-        H = R_factor * float(h[i])
-        nb = g.neighbours(i, H * (1 + rel))
-        if nb.size == 0:
-            continue
-        d = ((x[nb] - x[i] + 2 ** 31) % 2 ** 32 - 2 ** 31) * (L[None, :] / 2 ** 32)
-        r = np.sqrt((d ** 2).sum(1))
-        if np.any(np.abs(r - H) < rel * h[i]):
-            bad[i] = True
-    return bad
+def oracle_counts_at(p, h, dt_ghost=1e-3, **prm):
+    """The oracle's density and force neighbour counts at the given (GPU-converged) h.
+
+    The GPU's h iteration stops at its h_tol (1e-6 of eta^3 in the tests), ~h_tol/3 relative
+    from the oracle's exact root; a pair inside that band of the support edge may flip (the
+    north star excludes pairs within 1e-6 h of it).  At equal h the counts are bit-exact with
+    no exclusion: the GPU re-decides edge pairs in fp64 with the oracle's operation sequence."""
+    q = dict(p)
+    q["h"] = np.asarray(h, dtype=np.float32)
+    o = oracle_hydro(q, dt_ghost=dt_ghost, fixed_h=True, **prm)
+    return o["density"]["count"], o["force"]["count"].astype(np.int32)
 
 
 def assert_close(name, got, ref, rtol=RTOL, atol_scale=None, mask=None):

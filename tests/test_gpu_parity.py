@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import workloads as W
-from parity_util import RTOL, assert_close, gpu_hydro, oracle_hydro
+from parity_util import RTOL, assert_close, gpu_hydro, oracle_counts_at, oracle_hydro
 
 pytestmark = pytest.mark.gpu
 
@@ -109,7 +109,9 @@ def test_h_iteration_end_to_end(case, fac):
     assert_close("h", g["h"], d["h"], rtol=1e-5)
     assert_close("rho", g["rho"], d["rho"], rtol=2e-5)
     assert_close("P", g["P"], o["finalize"]["P"], rtol=2e-5)
-    assert np.array_equal(g["count"], d["count"])
+    cnt, cntf = oracle_counts_at(p, g["h"])  # (bit-exact at the GPU's h)
+    assert np.array_equal(g["count"], cnt)
+    assert np.array_equal(g["count_force"], cntf)
     assert_close("a", g["a"], o["force"]["a"], atol_scale=o["force"]["scale_a"])
     g4 = gpu_hydro(p, h_tol=1e-4)
     eta3 = 1.2348 ** 3

@@ -326,7 +326,7 @@ def run_ours(args, world, rank, local):
     # roofline: the loop kernel (§8 rows a2/a5/a7) with the largest share of the step
     dom = max(("density", "gradient", "force"), key=lambda k: kernels.get(k, {}).get("ms_per_step", 0.0))
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "r01", "ncu_summary.json")
+    prof = os.path.join(ROOT, "profiles", "r02", "ncu_summary.json")
     if os.path.exists(prof):
         try:
             traffic = json.load(open(prof)).get("dram_bytes_per_launch", {}).get(dom)

@@ -39,6 +39,28 @@ import workloads as W  # noqa: E402
 FLOPS_DENSITY, FLOPS_GRADIENT, FLOPS_FORCE_UNORDERED = 54.0, 30.0, 95.0
 # FP32 peak derived from unit counts and clock: 148 SM x 128 lanes x 2 x 1.965 GHz.
 FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+# Algorithmic HBM bytes per particle of one launch (the records a loop
+# must read once + the results it writes): density 32 + 36, gradient 48 + 8, force 64 + 20.
+BYTES_PER_PARTICLE = {"density": 68.0, "gradient": 56.0, "force": 84.0}
+
+
+def hbm_peak():
+    """Measured copy bandwidth (MEASURED_PEAKS.json, driver-written), else the profiling guide's
+    fallback (6.65 TB/s)."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "MEASURED_PEAKS.json"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
 
 WORKLOADS = {
     "C4": ("gresho256", lambda: W.gresho(256)),
@@ -65,6 +87,8 @@ def parse():
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--tile-z", type=int, default=0, help="cells per CTA block along z (0 = auto)")
     ap.add_argument("--skin", type=float, default=None, help="cell_skin (default: the library's)")
+    ap.add_argument("--cpu-baseline-all", default=None, metavar="OUT.json",
+                    help="time the oracle on every config family (+ single-thread C1-C3) and exit")
     return ap.parse_args()
 
 
@@ -190,9 +214,47 @@ def oracle_rate(sample_key, steps=1, threads=None):
         times.append(time.perf_counter() - t0)
         inter = int(r["density"]["count"].sum()) * 2 + int(r["force"]["count"].sum())
     t = float(np.mean(times))
+    npart = p["X"].shape[0]
     return {"value": inter / t, "unit": "interactions/s", "cores": oracle.max_threads(), "kind": "oracle",
+            "particle_passes_per_s_per_core": npart / t / oracle.max_threads(),
             "sample": f"{name}: one full hydro pass (density+h, gradient, force) with the fp64 cell-list "
-                      f"oracle, {p['X'].shape[0]} particles, {inter} interactions, {t:.2f} s/pass"}, t, inter, times
+                      f"oracle, {npart} particles, {inter} interactions, {t:.2f} s/pass"}, t, inter, times
+
+
+# bounded single-thread samples of the C1-C3 families (PAPER.md:506 quotes ~120k particle
+# steps/s per core for SWIFT's CPU loops): the oracle on one core
+SINGLE_THREAD_SAMPLES = {"C1": ("lattice16", lambda: W.lattice(16)), "C2": ("sod2x32", lambda: W.sod(32)),
+                         "C3": ("sedov48", lambda: W.sedov(48))}
+
+
+def oracle_single_thread(keys=("C1",)):
+    import oracle
+
+    nmax = oracle.max_threads()
+    out = {}
+    try:
+        for k in keys:
+            name, gen = SINGLE_THREAD_SAMPLES[k]
+            WORKLOADS["_st"] = (name, gen)
+            r = oracle_rate("_st", threads=1)[0]
+            out[k] = {"value": r["value"], "unit": r["unit"], "cores": 1,
+                      "particle_passes_per_s": r["particle_passes_per_s_per_core"], "sample": r["sample"]}
+    finally:
+        WORKLOADS.pop("_st", None)
+        oracle.set_threads(nmax)
+    return out
+
+
+def cpu_baseline_all(out_path):
+    """--cpu-baseline-all: the oracle on every config family (bounded samples, all host cores)
+    and single-threaded on C1-C3, with the CPU model; written to out_path."""
+    res = {"cpu_model": cpu_model(), "configs": {}, "single_thread": oracle_single_thread(("C1", "C2", "C3"))}
+    for key in ("C1", "C2", "G64", "C3", "C5s"):
+        r = oracle_rate(key)[0]
+        res["configs"][key] = r
+        print(key, json.dumps(r), flush=True)
+    json.dump(res, open(out_path, "w"), indent=1)
+    print(json.dumps(res["single_thread"]), flush=True)
 
 
 METRIC = "SPH pair interactions/sec (density+gradient+force) and time per hydro step"
@@ -334,7 +396,16 @@ def run_ours(args, world, rank, local):
             traffic = None
     roof = {"bound": "alu", "kernel": dom, "achieved": kernels[dom]["tflops"], "peak": FP32_PEAK_TFLOPS,
             "unit": "TFLOP/s", "frac": kernels[dom]["tflops"] / FP32_PEAK_TFLOPS, "traffic": traffic,
-            "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (DESIGN.md §7)"}
+            "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (DESIGN.md §7); "
+                           "FFMA2 microbenchmark 74.2 TFLOP/s (profiles/r01/ubench2.jsonl)"}
+    # the same kernel against the HBM roofline: algorithmic bytes (d.2) and the ncu DRAM bytes
+    # of one launch over the live average launch time
+    pk, pk_src = hbm_peak()
+    t_launch = kernels[dom]["ms_per_launch"] * 1e-3
+    alg_bytes = BYTES_PER_PARTICLE[dom] * n_total / max(world, 1)
+    roof["hbm"] = {"algorithmic_bytes": alg_bytes, "algorithmic_gbs": alg_bytes / t_launch / 1e9,
+                   "dram_gbs": (traffic / t_launch / 1e9) if traffic else None, "peak_gbs": pk,
+                   "frac": (traffic / t_launch / 1e9 / pk) if traffic else None, "peak_source": pk_src}
 
     e2e = None
     if not args.no_e2e:
@@ -349,6 +420,9 @@ def run_ours(args, world, rank, local):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = oracle_rate(args.cpu_sample)[0]
+        cpu["cpu_model"] = cpu_model()
+        cpu["single_thread"] = oracle_single_thread(("C1",))
+        cpu["all_configs"] = "profiles/r02/cpu_baseline.json (bench.py --cpu-baseline-all)"
     if rank == 0:
         line = {
             "metric": METRIC,
@@ -432,6 +506,9 @@ def run_e2e(ctx, p, torch, dev, stream, K, world):
 
 def main():
     args = parse()
+    if args.cpu_baseline_all:
+        cpu_baseline_all(args.cpu_baseline_all)
+        return
     world, rank, local = dist_init(args)
     if args.impl == "reference":
         run_reference(args, world, rank)

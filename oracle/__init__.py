@@ -73,10 +73,12 @@ def lib():
         L.orc_neighbours.restype = ctypes.c_int64
         L.orc_neighbours.argtypes = [_P, ctypes.c_int64, ctypes.c_double, _I64, ctypes.c_int64]
         L.orc_density.restype = ctypes.c_int
-        L.orc_density.argtypes = [_P, ctypes.POINTER(Params), _I64, ctypes.c_int64, _D, _D, _D, _D, _I64, _I32, _I64]
+        L.orc_density.argtypes = [_P, ctypes.POINTER(Params), _I64, ctypes.c_int64, _D, _D, _D, _D, _I64, _I32, _I64,
+                                  _D, _D]
         L.orc_finalize.argtypes = [ctypes.POINTER(Params), _I64, ctypes.c_int64, _D, _D, _D, _D]
         L.orc_gradient.restype = ctypes.c_int
-        L.orc_gradient.argtypes = [_P, ctypes.POINTER(Params), _I64, ctypes.c_int64, _D, _D, _D, _D, _D, _D, _U8, _D]
+        L.orc_gradient.argtypes = [_P, ctypes.POINTER(Params), _I64, ctypes.c_int64, _D, _D, _D, _D, _D, _D, _U8, _D,
+                                   _D, _D]
         L.orc_gradient_ghost.argtypes = [ctypes.POINTER(Params), _I64, ctypes.c_int64, ctypes.c_double, ctypes.c_int,
                                          _D, _D, _D, _D, _D, _D]
         L.orc_force.restype = ctypes.c_int
@@ -207,12 +209,15 @@ class Oracle:
         count = np.full(n, -1, dtype=np.int64)
         iters = np.full(n, -2, dtype=np.int32)
         coinc = ctypes.c_int64(0)
+        sdv = np.full(n, np.nan)
+        sdt = np.full(n, np.nan)
         status = lib().orc_density(g.h, ctypes.byref(prm), _ptr(ii, _I64), ii.size, _ptr(h, _D),
                                    _ptr(np.ascontiguousarray(st.v), _D), _ptr(st.m, _D), _ptr(dens, _D),
-                                   _ptr(count, _I64), _ptr(iters, _I32), ctypes.byref(coinc))
+                                   _ptr(count, _I64), _ptr(iters, _I32), ctypes.byref(coinc), _ptr(sdv, _D),
+                                   _ptr(sdt, _D))
         return dict(status=status, h=h, rho=dens[:, 0], drho_dh=dens[:, 1], nhat=dens[:, 2], dn_dh=dens[:, 3],
                     div=dens[:, 4], curl=dens[:, 5:8], count=count, iters=iters, coincident=coinc.value,
-                    _dens=dens, idx=ii)
+                    scale_dv=sdv, scale_dv_tail=sdt, _dens=dens, idx=ii)
 
     def finalize(self, st: State, d, idx=None):
         n = st.X.shape[0]
@@ -227,12 +232,16 @@ class Oracle:
         ii = _idx(n, idx)
         g = geom or self.geometry(st)
         grad = np.full((n, 2), np.nan)
+        slap = np.full(n, np.nan)
+        stl = np.full(n, np.nan)
         vm = None if valid is None else np.ascontiguousarray(valid, dtype=np.uint8)
         status = lib().orc_gradient(g.h, ctypes.byref(self.params), _ptr(ii, _I64), ii.size, _ptr(h, _D),
                                     _ptr(np.ascontiguousarray(st.v), _D), _ptr(st.m, _D), _ptr(st.u, _D),
                                     _ptr(np.ascontiguousarray(rho), _D), _ptr(np.ascontiguousarray(c), _D),
-                                    None if vm is None else _ptr(vm, _U8), _ptr(grad, _D))
-        return dict(status=status, v_sig=grad[:, 0], lap_u=grad[:, 1], _grad=grad)
+                                    None if vm is None else _ptr(vm, _U8), _ptr(grad, _D), _ptr(slap, _D),
+                                    _ptr(stl, _D))
+        return dict(status=status, v_sig=grad[:, 0], lap_u=grad[:, 1], scale_lap=slap, scale_lap_tail=stl,
+                    _grad=grad)
 
     def gradient_ghost(self, st: State, h, c, div, grad, dt, first_step, idx=None):
         n = st.X.shape[0]
@@ -248,7 +257,7 @@ class Oracle:
         ii = _idx(n, idx)
         g = geom or self.geometry(st)
         pp = np.ascontiguousarray(np.stack([f, P, c, B, rho, st.u, alpha_v, alpha_c], axis=1))
-        out = np.full((n, 10), np.nan)
+        out = np.full((n, 11), np.nan)
         vm = None if valid is None else np.ascontiguousarray(valid, dtype=np.uint8)
         hm = float(np.nanmax(h if valid is None else np.where(valid, h, np.nan)))
         status = lib().orc_force(g.h, ctypes.byref(self.params), _ptr(ii, _I64), ii.size, _ptr(h, _D),
@@ -256,7 +265,7 @@ class Oracle:
                                  None if vm is None else _ptr(vm, _U8), hm, _ptr(out, _D))
         return dict(status=status, a=out[:, 0:3], du=out[:, 3], v_sig=out[:, 4], scale_a=out[:, 5],
                     scale_u=out[:, 6], count=out[:, 7], scale_cond=out[:, 8],
-                    scale_tail=out[:, 9])
+                    scale_tail=out[:, 9], scale_v=out[:, 10])
 
     def dt(self, h, v_sig, idx=None):
         ii = _idx(h.shape[0], idx)
@@ -286,7 +295,8 @@ class Oracle:
             m0 = np.zeros(n, dtype=np.uint8)
             m0[np.asarray(sample)] = 1
             m1 = g.closure(m0, R)
-            m2 = g.closure(m1, R)
+            # (a 1-hop set covering most of the box: computing everything is the cheaper superset)
+            m2 = g.closure(m1, R) if m1.sum() < n // 2 else np.ones(n, dtype=bool)
             s0, s1, s2 = np.flatnonzero(m0), np.flatnonzero(m1), np.flatnonzero(m2)
             valid = m2
         d = self.density(st, idx=s2, geom=g, fixed_h=fixed_h)

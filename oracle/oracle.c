@@ -214,6 +214,8 @@ static int64_t orc_cap(const orc_geom* g) {
  * out[0..8] = rho, drho_dh, nhat, dn_dh, div, curl_x, curl_y, curl_z, (unused)   */
 typedef struct {
   double rho, drho_dh, nhat, dn_dh, div, curl[3];
+  double sdv; /* (1/rho) sum_{j!=i} m_j |dW/dr| |v_ij|: bounds every term of div and curl (a tolerance scale) */
+  double sdt; /* the same with |dW/dr| -> q |d2W/dr dq|: sensitivity to the rounding of q (support edge) */
   int64_t count, coincident;
 } dens_sums;
 
@@ -240,11 +242,18 @@ static int density_at(const orc_geom* g, const orc_params* p, int64_t i, double 
     double gw[3] = {dWdr * d[0] / r, dWdr * d[1] / r, dWdr * d[2] / r}; /* grad_i W_ij (R4) */
     double vij[3] = {v[3 * i] - v[3 * j], v[3 * i + 1] - v[3 * j + 1], v[3 * i + 2] - v[3 * j + 2]};
     divs += m[j] * (vij[0] * gw[0] + vij[1] * gw[1] + vij[2] * gw[2]);
+    s->sdv += m[j] * fabs(dWdr) * sqrt(vij[0] * vij[0] + vij[1] * vij[1] + vij[2] * vij[2]);
+    /* a relative error e of q moves dW/dr by e q |w''(q)|/(pi h^4): w' ~ (2 - q)^2 makes a pair near
+     * the support edge carry a large relative error in any finite precision */
+    s->sdt += m[j] * (r / h) * fabs(orc_ddw(r / h)) / (PI * h * h * h * h) *
+              sqrt(vij[0] * vij[0] + vij[1] * vij[1] + vij[2] * vij[2]);
     cs[0] += m[j] * (vij[1] * gw[2] - vij[2] * gw[1]);
     cs[1] += m[j] * (vij[2] * gw[0] - vij[0] * gw[2]);
     cs[2] += m[j] * (vij[0] * gw[1] - vij[1] * gw[0]);
   }
   s->div = -divs / s->rho;
+  s->sdv /= s->rho;
+  s->sdt /= s->rho;
   for (int a = 0; a < 3; ++a) s->curl[a] = cs[a] / s->rho;
   return ORC_OK;
 }
@@ -257,11 +266,14 @@ static int density_at(const orc_geom* g, const orc_params* p, int64_t i, double 
  *   h_max_iter Newton updates without convergence -> ORC_ERR_NOT_CONVERGED.
  *   h_max_iter == 0 -> density at the given h, no iteration ("fixed-h" mode).
  * For each i in idx[0..nidx): in h[i] (initial guess) -> out h[i]; out dens[i*8..]:
- *   rho, drho_dh, nhat, dn_dh, div, curl_x, curl_y, curl_z; count[i]; iters[i].
+ *   rho, drho_dh, nhat, dn_dh, div, curl_x, curl_y, curl_z; count[i]; iters[i]; and, if
+ *   scale_dv is not NULL, scale_dv[i] = (1/rho) sum_{j!=i} m_j |dW/dr| |v_ij| (the tolerance
+ *   scale of div and curl: no term of either sum exceeds it in magnitude), and scale_dv_tail[i] the
+ *   same sum with |dW/dr| replaced by q |d2W/dr dq| (the terms' sensitivity to the rounding of q).
  * Returns ORC_OK, or ORC_ERR_NOT_CONVERGED (state still written, flagged iters = -1). */
 int orc_density(const orc_geom* g, const orc_params* p, const int64_t* idx, int64_t nidx, double* h,
                 const double* v, const double* m, double* dens, int64_t* count, int32_t* iters,
-                int64_t* coincident_total) {
+                int64_t* coincident_total, double* scale_dv, double* scale_dv_tail) {
   int status = ORC_OK;
   int64_t coinc = 0;
   const double eta3 = p->eta * p->eta * p->eta;
@@ -295,6 +307,8 @@ int orc_density(const orc_geom* g, const orc_params* p, const int64_t* idx, int6
       o[0] = s.rho; o[1] = s.drho_dh; o[2] = s.nhat; o[3] = s.dn_dh; o[4] = s.div;
       o[5] = s.curl[0]; o[6] = s.curl[1]; o[7] = s.curl[2];
       count[i] = s.count;
+      if (scale_dv) scale_dv[i] = s.sdv;
+      if (scale_dv_tail) scale_dv_tail[i] = s.sdt;
       iters[i] = ok ? it : -1;
       coinc += s.coincident;
       if (!ok) {
@@ -338,10 +352,12 @@ void orc_finalize(const orc_params* p, const int64_t* idx, int64_t nidx, const d
  *   v_sig,i = max(2 c_i, max_j (c_i + c_j - beta mu_ij))    Eq. 10 (R15)
  *   lap u_i = 2 sum_j (m_j/rho_j)(u_i - u_j) dW/dr(r_ij, h_i)/|r_ij|   Brookshaw (R16)
  * `valid` marks particles whose density-stage outputs exist (sampled runs).
- * out grad[i*2..] = v_sig, lap_u */
+ * out grad[i*2..] = v_sig, lap_u; scale_lap[i] (if not NULL) = 2 sum_j (m_j/rho_j)|u_i - u_j||dW/dr|/r,
+ * the sum of the magnitudes of lap u's terms (a tolerance scale); scale_lap_tail[i] the same with
+ * |dW/dr| replaced by q |d2W/dr dq| (sensitivity to the rounding of q near the support edge) */
 int orc_gradient(const orc_geom* g, const orc_params* p, const int64_t* idx, int64_t nidx, const double* h,
                  const double* v, const double* m, const double* u, const double* rho, const double* c,
-                 const uint8_t* valid, double* grad) {
+                 const uint8_t* valid, double* grad, double* scale_lap, double* scale_lap_tail) {
   int status = ORC_OK;
 #pragma omp parallel
   {
@@ -352,7 +368,7 @@ int orc_gradient(const orc_geom* g, const orc_params* p, const int64_t* idx, int
       int64_t i = idx[t];
       double H = p->gamma_k * h[i], d[3];
       int64_t nn = orc_neighbours(g, i, H, buf, cap);
-      double vsig = 2.0 * c[i], lap = 0.0;
+      double vsig = 2.0 * c[i], lap = 0.0, slap = 0.0, stail = 0.0;
       for (int64_t k = 0; k < nn; ++k) {
         int64_t j = buf[k];
         if (j == i) continue;
@@ -372,9 +388,14 @@ int orc_gradient(const orc_geom* g, const orc_params* p, const int64_t* idx, int
         double W, dWdr, dWdh;
         orc_kernel(r, h[i], &W, &dWdr, &dWdh);
         lap += m[j] / rho[j] * (u[i] - u[j]) * dWdr / r;
+        slap += m[j] / rho[j] * fabs(u[i] - u[j]) * fabs(dWdr) / r;
+        stail += m[j] / rho[j] * fabs(u[i] - u[j]) * (r / h[i]) * fabs(orc_ddw(r / h[i])) /
+                 (PI * h[i] * h[i] * h[i] * h[i] * r);
       }
       grad[2 * i] = vsig;
       grad[2 * i + 1] = 2.0 * lap;
+      if (scale_lap) scale_lap[i] = 2.0 * slap;
+      if (scale_lap_tail) scale_lap_tail[i] = 2.0 * stail;
     }
     free(buf);
   }
@@ -436,8 +457,8 @@ void orc_gradient_ghost(const orc_params* p, const int64_t* idx, int64_t nidx, d
  *   v_sig,i = max(2 c_i, max_j v_sig,ij)                           (R15)
  * Also returns per-particle tolerance scales  sa_i = sum_j m_j |S_ij| |r_ij|  and
  * su_i = sum_j m_j (|A_i G_i v.r| + |Pi Gbar v.r|/2 + |D_ij|), and the pair count.
- * pp[i*8..] = f, P, c, B, rho, u, alpha_v, alpha_c.  out force[i*8..] = ax, ay, az, du,
- * v_sig, sa, su, count. */
+ * pp[i*8..] = f, P, c, B, rho, u, alpha_v, alpha_c.  out force[i*11..] = ax, ay, az, du,
+ * v_sig, sa, su, count, sc, st, sv (the last three: sensitivity scales, below). */
 int orc_force(const orc_geom* g, const orc_params* p, const int64_t* idx, int64_t nidx, const double* h,
               const double* v, const double* m, const double* pp, const uint8_t* valid, double h_max,
               double* force) {
@@ -455,7 +476,7 @@ int orc_force(const orc_geom* g, const orc_params* p, const int64_t* idx, int64_
       const double* qi = pp + 8 * i;
       double fi = qi[0], Pi_ = qi[1], ci = qi[2], Bi = qi[3], rhoi = qi[4], ui = qi[5], avi = qi[6], aci = qi[7];
       double Ai = Pi_ / (rhoi * rhoi);
-      double a[3] = {0, 0, 0}, du = 0.0, vsig = 2.0 * ci, sa = 0.0, su = 0.0, sc = 0.0, st = 0.0, d[3];
+      double a[3] = {0, 0, 0}, du = 0.0, vsig = 2.0 * ci, sa = 0.0, su = 0.0, sc = 0.0, st = 0.0, sv = 0.0, d[3];
       int64_t cnt = 0;
       for (int64_t k = 0; k < nn; ++k) {
         int64_t j = buf[k];
@@ -495,10 +516,27 @@ int orc_force(const orc_geom* g, const orc_params* p, const int64_t* idx, int64_
         if (vs > vsig) vsig = vs;
         sa += m[j] * fabs(S) * r;
         su += m[j] * (fabs(t1) + fabs(t2) + fabs(D));
-        /* sensitivity of D to the pressure difference inside v_c: sqrt(2|P_i-P_j|/rho) has an
-         * unbounded derivative at P_i = P_j, so an input error e (P_i+P_j) moves v_c by
-         * sqrt(2 e (P_i+P_j)/(rho_i+rho_j)); sc = sum_j m_j |D_ij/v_c| sqrt((P_i+P_j)/(rho_i+rho_j)) */
-        sc += m[j] * fabs(acij * (ui - uj) * (Gi + Gj) * r / (rhoi + rhoj)) * sqrt((Pi_ + Pj) / (rhoi + rhoj));
+        /* sensitivity to the rounding of v_ij . r_ij: the du terms with |v_ij . r_ij| replaced by
+         * |v_ij| |r_ij| (a rigid rotation has v_ij . r_ij = 0 up to the input rounding of v, so its
+         * terms are rounding-level and any finite precision resolves them only to ~eps |v||r|) */
+        {
+          double vn = sqrt((v[3 * i] - v[3 * j]) * (v[3 * i] - v[3 * j]) +
+                           (v[3 * i + 1] - v[3 * j + 1]) * (v[3 * i + 1] - v[3 * j + 1]) +
+                           (v[3 * i + 2] - v[3 * j + 2]) * (v[3 * i + 2] - v[3 * j + 2]));
+          sv += m[j] * (fabs(Ai * Gi) + fabs(0.5 * PiV * Gbar)) * vn * r;
+        }
+        /* sensitivity of D to the pressure difference inside v_c (Eq. 22): sqrt(2|P_i-P_j|/rho)
+         * has an unbounded derivative at P_i = P_j.  An error of the pressures of relative size
+         * EPS_P = 1e-6 (f32 densities and the h-iteration tolerance) moves |P_i - P_j| by at most
+         * EPS_P (P_i + P_j), hence v_c by at most
+         *   dv = sqrt(2 (|P_i-P_j| + EPS_P (P_i+P_j))/rho_s) - sqrt(2 |P_i-P_j|/rho_s)
+         * (~ sqrt(2 EPS_P (P_i+P_j)/rho_s) when P_i = P_j, EPS_P (P_i+P_j)/(rho_s v_p) once
+         * |P_i - P_j| >> EPS_P (P_i + P_j)).  sc = sum_j m_j |D_ij/v_c| dv: an absolute du bound. */
+        {
+          const double EPS_P = 1e-6, rs = rhoi + rhoj, dP = fabs(Pi_ - Pj);
+          const double dv = sqrt(2.0 * (dP + EPS_P * (Pi_ + Pj)) / rs) - sqrt(2.0 * dP / rs);
+          sc += m[j] * fabs(acij * (ui - uj) * (Gi + Gj) * r / rs) * dv;
+        }
         /* sensitivity to the kernel derivative near the support edge: w'(q) ~ (2-q)^2 has a
          * large relative error when q -> 2 in any finite precision.  A relative error e of q
          * moves w' by e q |w''(q)|; st = the du terms with |w'| replaced by q |w''(q)|, so the
@@ -512,9 +550,9 @@ int orc_force(const orc_geom* g, const orc_params* p, const int64_t* idx, int64_
         }
         cnt++;
       }
-      double* o = force + 10 * i;
+      double* o = force + 11 * i;
       o[0] = a[0]; o[1] = a[1]; o[2] = a[2]; o[3] = du; o[4] = vsig; o[5] = sa; o[6] = su; o[7] = (double)cnt;
-      o[8] = sc; o[9] = st;
+      o[8] = sc; o[9] = st; o[10] = sv;
     }
     free(buf);
   }

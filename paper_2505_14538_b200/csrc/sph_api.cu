@@ -13,6 +13,7 @@
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 #include <cuda_runtime.h>
+#include <nvtx3/nvtx3.hpp>
 
 #include <algorithm>
 #include <chrono>
@@ -81,6 +82,29 @@ __global__ void k_cell_start(int n, int ncells, int zbits, const unsigned int* _
   int lo = (p == 0) ? 0 : min((int)(keys[p - 1] >> zbits) + 1, ncells + 1);
   int hi = (p == n) ? ncells : min((int)(keys[p] >> zbits), ncells);
   for (int c = lo; c <= hi; ++c) cell_start[c] = p;
+}
+
+// Coincident particles (a pair with r_ij = 0, j != i, contributes nothing and is counted).
+// Exactly equal fixed-point positions give equal sort keys (cell + z sub-bucket), so a particle's
+// coincident partners lie in its run of equal keys: flag every particle that has one and count the
+// directed pairs.  p indexes the sorted owned particles (keys[p] belongs to xh[p]).
+__global__ void k_dup(int n, const unsigned int* __restrict__ keys, const uint4* __restrict__ xh, uint8_t* dup,
+                      unsigned int* npairs) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const unsigned int k = keys[p];
+  const uint4 a = xh[p];
+  unsigned int m = 0;
+  for (int q = p - 1; q >= 0 && keys[q] == k; --q) {
+    const uint4 b = xh[q];
+    m += (b.x == a.x && b.y == a.y && b.z == a.z) ? 1u : 0u;
+  }
+  for (int q = p + 1; q < n && keys[q] == k; ++q) {
+    const uint4 b = xh[q];
+    m += (b.x == a.x && b.y == a.y && b.z == a.z) ? 1u : 0u;
+  }
+  dup[p] = m ? 1 : 0;
+  if (m) atomicAdd(npairs, m);
 }
 
 struct Persist {
@@ -291,6 +315,7 @@ struct sph_ctx {
   int* run_list = nullptr;      // [nrun] active indices of the blocks with a non-wide i particle
   size_t run_cap = 0;
   int kz_hint = 0;              // KZ chosen at the last rebuild (first probe of the next)
+  long long n_coinc = 0;        // directed coincident pairs of the owned particles (k_dup)
   uint32_t* cperm = nullptr;    // wide search grid: particles in coarse-cell order
   size_t cperm_cap = 0;
   int* ccs = nullptr;           // its coarse cell starts
@@ -342,11 +367,16 @@ cudaEvent_t ev_get(sph_ctx* c) {
 }
 
 // Scope of one timed phase on the context stream (no-op unless timing is on).
+// (every timed phase is also an NVTX range, named after the phase: visible in nsys / ncu
+// --nvtx timelines, free when no tool is attached)
+const char* const kPhaseName[SPH_T_COUNT] = {"sph:rebuild", "sph:lists", "sph:density", "sph:gradient",
+                                             "sph:force", "sph:kick_drift", "sph:exchange", "sph:other"};
 struct Timed {
   sph_ctx* c;
   int kind;
   cudaEvent_t a = nullptr;
-  Timed(sph_ctx* ctx, int k) : c(ctx), kind(k) {
+  nvtx3::scoped_range range;
+  Timed(sph_ctx* ctx, int k) : c(ctx), kind(k), range(kPhaseName[k]) {
     if (c->timing) {
       a = ev_get(c);
       cudaEventRecord(a, c->stream);
@@ -400,7 +430,8 @@ sph_status alloc_state(sph_ctx* c) {
   CK(dalloc(&s.dens, n)); CK(dalloc(&s.dvc, n)); CK(dalloc(&s.count, n)); CK(dalloc(&s.fin, n));
   CK(dalloc(&s.gq, n)); CK(dalloc(&s.hlo, n)); CK(dalloc(&s.hhi, n)); CK(dalloc(&s.iters, n));
   CK(dalloc(&s.active, n)); CK(dalloc(&s.grad, n)); CK(dalloc(&s.fr1, n)); CK(dalloc(&s.fr2, n));
-  CK(dalloc(&s.vsig, n)); CK(dalloc(&s.countf, n));
+  CK(dalloc(&s.vsig, n)); CK(dalloc(&s.countf, n)); CK(dalloc(&s.dup, n));
+  CK(cudaMemset(s.dup, 0, n));
   CK(dalloc(&s.ncount, n)); CK(dalloc(&s.hbuild, n));
   CK(cudaMemset(s.ncount, 0, n * sizeof(int32_t)));  // k_lists reads it as a length hint
   CK(dalloc(&s.nbr, n * (size_t)c->lcap));
@@ -605,6 +636,14 @@ sph_status allreduce(sph_ctx* c, double* v, int n, ReduceOp op) {
   return SPH_OK;
 }
 
+// global reduction of uint32 values in device memory, enqueued on the context stream (no host
+// synchronisation over NCCL; no-op on one rank).  The next read-back sees the global values.
+sph_status allreduce_dev(sph_ctx* c, void* d, int n, ReduceOp op) {
+  if (!c->slab) return SPH_OK;
+  CKC(c->comm->allreduce_dev_u32(static_cast<uint32_t*>(d), n, op, c->stream));
+  return SPH_OK;
+}
+
 // Collective error agreement: every rank takes the same branch (a rank that fails alone
 // would leave its neighbours waiting in the next exchange).
 sph_status agree(sph_ctx* c, bool bad, sph_status code, const char* msg) {
@@ -738,13 +777,12 @@ sph_status rebuild_impl(sph_ctx* c) {
     c->launches++;
   }
   CK(cudaGetLastError());
+  // global h_max (positive f32 bits order as uint32): device-side reduction, one read-back
+  if ((st = allreduce_dev(c, c->scratch, 1, kMax)) != SPH_OK) return st;
   CK(cudaMemcpyAsync(c->scratch_h, c->scratch, 4, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  float hmax_l;
-  std::memcpy(&hmax_l, c->scratch_h, 4);
-  double hm = hmax_l;
-  if ((st = allreduce(c, &hm, 1, kMax)) != SPH_OK) return st;
-  const float hmax = (float)hm;
+  float hmax;
+  std::memcpy(&hmax, c->scratch_h, 4);
   if (!(hmax > 0.f) || !std::isfinite(hmax)) return fail(c, SPH_ERR_INVALID_ARG, "smoothing lengths must be finite and > 0");
   const float hcell = c->h_side > 0.f ? std::min(c->h_side, hmax) : hmax;  // adaptive: an h quantile
   const double Hs = (double)c->cfg.gamma_k * hcell * (1.0 + c->cfg.cell_skin);
@@ -922,6 +960,15 @@ sph_status rebuild_impl(sph_ctx* c) {
     swap_persist(c);
   }
   stage("binned");
+  // coincident particles: flags for k_lists and the directed pair count (read with the
+  // tile sizes below)
+  CK(cudaMemsetAsync(c->scratch + 14, 0, 4, c->stream));
+  if (n > 0) {
+    k_dup<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->keys_alt, c->s.xh + c->gL, c->s.dup + c->gL, c->scratch + 14);
+    c->launches++;
+  }
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(c->scratch_h + 14, c->scratch + 14, 4, cudaMemcpyDeviceToHost, c->stream));
   // CTA blocks: BX x BY grid columns x KZ cells (BX, BY = 2 when the grid allows: the tile of
   // (BX+2)(BY+2) columns is then ~2x smaller per owned particle than with single columns)
   g.bx = (g.periodic_x ? g.nx >= 6 : g.nxo >= 2) ? 2 : 1;
@@ -963,16 +1010,16 @@ sph_status rebuild_impl(sph_ctx* c) {
     CK(launch_tile_sizes(g, c->cell_start, (int*)(c->scratch + 6), (int*)(c->scratch + 7), c->act_flag,
                          c->stream));
     c->launches++;
+    if ((st = allreduce_dev(c, c->scratch + 6, 2, kMax)) != SPH_OK) return st;  // same capacities on every rank
     CK(cudaMemcpyAsync(c->scratch_h + 6, c->scratch + 6, 8, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     double tmax[2] = {(double)c->scratch_h[6], (double)c->scratch_h[7]};
-    if ((st = allreduce(c, tmax, 2, kMax)) != SPH_OK) return st;  // same capacities on every rank
     g.tcap = std::max(32, (int)tmax[0]);
     g.icap = std::max(32, (int)tmax[1]);
     g.lcap = c->lcap;
     g.skin = c->cfg.cell_skin;
     // force: 256 threads when two CTAs fit an SM, else one CTA of 512
-    g.force_threads = 256;
+    g.force_threads = 384;
     if (force_smem(g) > kSmemTarget) g.force_threads = 512;
     const bool fits = force_smem(g) <= kSmemMax && lists_smem(g) <= kSmemMax && density_smem(g) <= kSmemMax &&
                       gradient_smem(g) <= kSmemMax && g.tcap < 32760;  // (list entries: 15-bit slots)
@@ -994,6 +1041,8 @@ sph_status rebuild_impl(sph_ctx* c) {
     KZ = kz_lo == 0 ? (hint && hint < kz_hi ? hint : std::max(1, kz_hi / 2)) : (kz_lo + kz_hi) / 2;
   }
   c->kz_hint = g.KZ;
+  c->n_coinc = (long long)c->scratch_h[14];  // (the tile-size probes synchronised the stream)
+  g.coinc = c->n_coinc > 0 ? 1 : 0;
   stage("KZ chosen");
   // the blocks with i particles, in block order: one loop CTA each (a clustered box on a fine
   // grid has mostly empty blocks)
@@ -1398,11 +1447,12 @@ sph_status sph_density(sph_ctx* c, sph_density_stats* stats) {
     }
     c->launches += 1 + (c->s.n_wide > 0 ? 1 : 0);
     ++passes_run;
+    // every rank takes the same branch: the pass's flags (h_exceeds .. wlist_overflow, seven
+    // uint32 in DevCounters) are reduced over ranks on the device, then read back once
+    if ((st = allreduce_dev(c, &c->ctr->h_exceeds, 7, kMax)) != SPH_OK) return st;
     if ((st = sync_ctr(c)) != SPH_OK) return st;
-    // every rank takes the same branch: the flags are reduced over ranks
     double fl[4] = {(double)c->ctr_h->active_next, (double)c->ctr_h->h_exceeds, (double)c->ctr_h->list_stale,
                     c->ctr_h->nonfinite == 2 ? 1.0 : 0.0};
-    if ((st = allreduce(c, fl, 4, kMax)) != SPH_OK) return st;
     if (fl[3] > 0) return fail(c, SPH_ERR_CUDA, "internal: tile larger than its capacity");
     if (fl[0] == 0) break;
     if (fl[1] > 0) {
@@ -1498,18 +1548,18 @@ sph_status sph_force(sph_ctx* c, float* dt_next) {
     CK(launch_force_fin(c->gL, c->n_own, c->phys, c->s, c->ctr, c->stream));
   }
   c->launches += 2 + (c->s.n_wide > 0 ? 2 : 0);
+  // CFL dt: global minimum (X4; positive f32 bits order as uint32) and the error flag, reduced
+  // on the device, one read-back
+  if ((st = allreduce_dev(c, &c->ctr->dt_bits, 1, kMin)) != SPH_OK) return st;
+  if ((st = allreduce_dev(c, &c->ctr->nonfinite, 1, kMax)) != SPH_OK) return st;
   if ((st = sync_ctr(c)) != SPH_OK) return st;
   c->counters.pairs_force = (int64_t)c->ctr_h->pairs;
   float dt;
   std::memcpy(&dt, &c->ctr_h->dt_bits, 4);
-  double red[2] = {std::isfinite(dt) ? (double)dt : 1e300, (double)c->ctr_h->nonfinite};
-  double mx = red[1];
-  if ((st = allreduce(c, red, 1, kMin)) != SPH_OK) return st;   // CFL dt: global minimum (X4)
-  if ((st = allreduce(c, &mx, 1, kMax)) != SPH_OK) return st;
-  dt = (float)red[0];
+  const int mx = c->ctr_h->nonfinite;
   if (dt_next) *dt_next = dt;
   if (mx == 2) return fail(c, SPH_ERR_CUDA, "internal: tile larger than its capacity");
-  if (mx > 0 || !std::isfinite(dt) || red[0] >= 1e300) return fail(c, SPH_ERR_NUMERIC, "non-finite acceleration, v_sig or dt (S:262)");
+  if (mx > 0 || !std::isfinite(dt)) return fail(c, SPH_ERR_NUMERIC, "non-finite acceleration, v_sig or dt (S:262)");
   return SPH_OK;
 }
 
@@ -1607,7 +1657,7 @@ sph_status sph_get_counters(sph_ctx* c, sph_counters* out) {
   GUARD(c);
   if (!out) return SPH_ERR_INVALID_ARG;
   CK(cudaStreamSynchronize(c->stream));
-  c->counters.coincident = -1;  // not tracked by the GPU loops (R28)
+  c->counters.coincident = c->n_coinc;  // directed pairs, skipped by the loops (k_dup)
   c->counters.kernel_launches = c->launches;
   c->counters.wide_particles = c->s.n_wide;
   *out = c->counters;

@@ -100,6 +100,11 @@ class NcclComm : public Comm {
     if (cudaStreamSynchronize(st) != cudaSuccess) return "allreduce: sync failed";
     return "";
   }
+  std::string allreduce_dev_u32(uint32_t* d, int n, ReduceOp op, cudaStream_t st) override {
+    ncclRedOp_t o = op == kSum ? ncclSum : (op == kMax ? ncclMax : ncclMin);
+    ncclResult_t e = g_nccl.AllReduce(d, d, n, ncclUint32, o, comm_, st);
+    return e == ncclSuccess ? "" : std::string("ncclAllReduce: ") + g_nccl.GetErrorString(e);
+  }
 
  private:
   int rank_, n_;
@@ -229,6 +234,21 @@ class LoopComm : public Comm {
       g_->cv.wait(lk, [&] { return g_->ar_gen != gen; });
     }
     for (int k = 0; k < n; ++k) v[k] = g_->ar_res[k];
+    return "";
+  }
+  // (one process: through the host, exactly as allreduce)
+  std::string allreduce_dev_u32(uint32_t* d, int n, ReduceOp op, cudaStream_t st) override {
+    if (n > 64) return "allreduce: too many values";
+    uint32_t h[64];
+    double v[64];
+    if (cudaMemcpyAsync(h, d, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+      return "allreduce: D2H failed";
+    if (cudaStreamSynchronize(st) != cudaSuccess) return "allreduce: sync failed";
+    for (int k = 0; k < n; ++k) v[k] = (double)h[k];
+    std::string e = allreduce(v, n, op, st);
+    if (!e.empty()) return e;
+    for (int k = 0; k < n; ++k) h[k] = (uint32_t)v[k];
+    if (cudaMemcpy(d, h, n * sizeof(uint32_t), cudaMemcpyHostToDevice) != cudaSuccess) return "allreduce: H2D failed";
     return "";
   }
 

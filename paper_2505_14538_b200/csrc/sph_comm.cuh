@@ -33,6 +33,9 @@ class Comm {
   virtual std::string exchange(const Xfer* sends, int ns, const Xfer* recvs, int nr, cudaStream_t st) = 0;
   // In-place allreduce of host scalars; synchronises `st`.
   virtual std::string allreduce(double* v, int n, ReduceOp op, cudaStream_t st) = 0;
+  // In-place allreduce of n uint32 values in DEVICE memory, enqueued on `st` (NCCL: no host
+  // synchronisation; the caller's next read-back of the values is the only one).
+  virtual std::string allreduce_dev_u32(uint32_t* d, int n, ReduceOp op, cudaStream_t st) = 0;
 };
 
 Comm* make_nccl_comm(const void* unique_id, int rank, int nranks, std::string& err);

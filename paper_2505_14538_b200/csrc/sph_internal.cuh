@@ -36,12 +36,14 @@ struct DevGrid {
   int icap;           // most i particles (owned by the block) of any block
   int lcap;           // neighbour-list capacity per particle (multiple of 16)
   float skin;         // list radius = (1 + skin) max(H_i, H_j)
-  int force_threads;  // block size of the force kernel: 256, or 512 when one CTA fills an SM
+  int force_threads;  // block size of the force kernel: 384 (two CTAs per SM), or 512 when one CTA fills an SM
   int lists_warps;    // warps per k_lists CTA: ~ the mean block particle count / 32 (a warp per 32)
   const void* desc;   // [nblocks] tile descriptors (sph_kernels.cu TileDesc, k_tile_desc)
   const void* desc_cells;  // [nblocks][kMaxTileCells + 1] per tile cell (tile offset, global start)
   int* desc_pref;     // [nblocks][icap + 1] list-group prefix of the block's particles (k_lists)
   int* desc_prefF;    // [nblocks][icap + 1] the same over the force part of each list (k_lists)
+  int coinc;          // some particles share their exact position with another (k_dup): the lists drop
+                      // those pairs
   float scale[3];     // L_a / 2^32 as f32 (fixed point -> length)
   double dscale[3];   // L_a * 2^-32 exact (fp64 exact neighbour test)
   float side[3];      // cell side per axis
@@ -108,6 +110,7 @@ struct DevState {
   // wide particles (adaptive cell side, sph_wide.cu): support past the cell side; nullptr /
   // 0 when there are none
   uint8_t* wide;      // [n] flag
+  uint8_t* dup;       // [n] 1: another particle has exactly this position (k_dup, sph_api.cu)
   int32_t* widx;      // [n_wide] their indices, ascending
   uint32_t* wnbr;     // [n_wide][wlcap] neighbour lists, global indices
   int32_t* wcount;    // [n_wide] list lengths

@@ -434,11 +434,13 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
   // wide particles (adaptive grid): one flag byte per slot after the window table (a wide
   // partner's pair is never in the force part: k_wide_force applies it to both sides)
   unsigned char* wfl = reinterpret_cast<unsigned char*>(s_zw) + lists_zw_bytes(g);  // (lists_slot_bytes)
-  if (kWide) {
+  // (bit 0: wide, bit 1: a coincident partner exists, k_dup)
+  if (kWide || g.coinc) {
     const int lane_ = threadIdx.x & 31;
     for (int k = threadIdx.x >> 5; k < nseg; k += nw) {
       const int4 sg = S.seg[k];
-      for (int t = lane_; t < sg.z; t += 32) wfl[sg.x + t] = s.wide[sg.y + t];
+      for (int t = lane_; t < sg.z; t += 32)
+        wfl[sg.x + t] = (kWide ? s.wide[sg.y + t] : 0) | (g.coinc ? (s.dup[sg.y + t] << 1) : 0);
     }
   }
   {
@@ -583,7 +585,7 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
     auto ftag = [&](uint32_t t) -> uint32_t {
       if (!kTag) return t;
       bool f = t < (uint32_t)g.tcap && (t > uti || t < (uint32_t)gLo || t >= (uint32_t)gHi);
-      if (kWide) f = f && !wfl[t];
+      if (kWide) f = f && !(wfl[t] & 1);
       return f ? 0x8000u | t : t;
     };
     auto hit = [&](bool h, int t) {
@@ -688,6 +690,23 @@ __global__ void __launch_bounds__(kNW * 32, 4) k_lists(DevGrid g, DevPhys ph, De
       s.ncount[gi] = fits ? (nF | (nL << 16) | (kTag ? 0 : (int)0x80000000u)) : 0;
       mygrp = fits ? gF + gL : 0;
       mygrpF = fits ? gF : 0;
+      // a partner at exactly i's position (j != i) is dropped: its entry becomes the
+      // sentinel of its column (after the list is written, so the hot drain stays lean; only on
+      // grids where k_dup found such particles, only for the particles it flagged)
+      if (g.coinc && fits && s.dup[gi]) {
+        uint16_t* L = (kTag ? s.nbr_raw : s.nbr) + (size_t)gi * g.lcap;
+        for (int q = 0; q < cntp; ++q) {
+          const uint32_t t = L[q] & 0x7fffu;
+          if (t >= (uint32_t)g.tcap || t == uti || !(wfl[t] & 2)) continue;
+          int gj = 0;
+          for (int sq = 0; sq < nseg; ++sq) {
+            const int4 sg = S.seg[sq];
+            if ((int)t >= sg.x && (int)t < sg.x + sg.z) gj = sg.y + ((int)t - sg.x);
+          }
+          const uint4 xa = s.xh[gi], xb = s.xh[gj];
+          if (xa.x == xb.x && xa.y == xb.y && xa.z == xb.z) L[q] = (uint16_t)((L[q] & 0x8000u) | (g.tcap + (q & 7)));
+        }
+      }
       s.hbuild[gi] = __uint_as_float(__ldg(&s.xh[gi].w));
     }
     if (k < ni) {
@@ -1285,7 +1304,10 @@ __device__ __forceinline__ int lds1(uint32_t a) {
   return v;
 }
 
-__global__ void __launch_bounds__(512, 1) k_force(DevGrid g, DevPhys ph, DevState s,
+// (NT threads, MINB CTAs per SM: 384 x 2 when two tiles fit an SM -- 24 warps to hide the
+// gather latency, registers <= 85 --, else 512 x 1)
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_force(DevGrid g, DevPhys ph, DevState s,
                                                     const int* __restrict__ cell_start,
                                                     DevCounters* __restrict__ ctr) {
   DESC_PROLOGUE();
@@ -1571,10 +1593,12 @@ cudaError_t launch_gradient(const DevGrid& g, const DevPhys& ph, const DevState&
 cudaError_t launch_force(const DevGrid& g, const DevPhys& ph, const DevState& s, const int* cell_start,
                          DevCounters* ctr, cudaStream_t st) {
   const size_t sm = force_smem(g);
-  cudaError_t e = set_smem((const void*)k_force, sm);
+  const void* fn = g.force_threads == 512 ? (const void*)k_force<512, 1> : (const void*)k_force<384, 2>;
+  cudaError_t e = set_smem(fn, sm);
   if (e != cudaSuccess) return e;
   if (g.nrun == 0) return cudaSuccess;
-  k_force<<<g.nrun, g.force_threads, sm, st>>>(g, ph, s, cell_start, ctr);
+  if (g.force_threads == 512) k_force<512, 1><<<g.nrun, 512, sm, st>>>(g, ph, s, cell_start, ctr);
+  else k_force<384, 2><<<g.nrun, 384, sm, st>>>(g, ph, s, cell_start, ctr);
   return cudaGetLastError();
 }
 

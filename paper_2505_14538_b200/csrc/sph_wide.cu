@@ -135,6 +135,8 @@ __global__ void __launch_bounds__(256) k_wide_lists(DevGrid g, DevPhys ph, DevSt
           const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
           const float hj = __uint_as_float(xj.w);
           hit = r2 < fmaxf(Hi2, (Hfac * hj) * (Hfac * hj));
+          // a partner at exactly i's position (j != i) is skipped
+          if (j != i && xj.x == xi.x && xj.y == xi.y && xj.z == xi.z) hit = false;
         }
         const unsigned b = __ballot_sync(kFull, hit);
         const int pos = cnt + __popc(b & ((1u << lane) - 1u));

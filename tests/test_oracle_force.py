@@ -264,3 +264,26 @@ def test_gresho_initial_conditions():
     speed = np.hypot(g["v"][:, 0], g["v"][:, 1])
     assert np.allclose(speed, W.gresho_analytic(r)[0], atol=1e-6)
     assert np.allclose(g["u"], 1.5 * W.gresho_analytic(r)[1], rtol=1e-6)
+
+
+def test_tolerance_scales_bound_their_sums(orc):
+    """The per-particle tolerance scales the parity tests use are sums of term magnitudes, so
+    each bounds its sum: |div|, |curl_a| <= scale_dv, |lap u| <= scale_lap, |a_a| <= scale_a,
+    |du| <= scale_u; all vanish on the lattice at rest (where the sums are exactly 0).  The
+    conduction bound scale_cond is 0 when alpha_c = 0 and grows like sqrt(eps) at P_i = P_j."""
+    p = _rand_set(seed=12, n=600)
+    st, r = _forces(orc, p)
+    d, gr, fo = r["density"], r["gradient"], r["force"]
+    assert np.all(np.abs(d["div"]) <= d["scale_dv"] * (1 + 1e-12))
+    assert np.all(np.abs(d["curl"]) <= d["scale_dv"][:, None] * (1 + 1e-12))
+    assert np.all(np.abs(gr["lap_u"]) <= gr["scale_lap"] * (1 + 1e-12))
+    assert np.all(np.abs(fo["a"]) <= fo["scale_a"][:, None] * (1 + 1e-12))
+    assert np.all(np.abs(fo["du"]) <= fo["scale_u"] * (1 + 1e-12))
+    assert np.all(fo["scale_cond"] > 0)
+    q = dict(p)
+    q["alpha_c"] = np.zeros_like(p["alpha_c"])
+    r0 = orc.Oracle(orc.Params(alpha_c_max=0.0), mode="brute").hydro(_state(orc, q), dt_ghost=1e-3, first_step=True)
+    assert np.all(r0["force"]["scale_cond"] == 0)
+    lat = W.lattice(8, h_factor=1.0)
+    rl = orc.Oracle(orc.Params(h_max_iter=0), mode="brute").hydro(_state(orc, lat), dt_ghost=1e-3, first_step=True)
+    assert np.all(rl["density"]["scale_dv"] == 0) and np.all(rl["gradient"]["scale_lap"] == 0)

@@ -25,5 +25,7 @@ from .generators import (  # noqa: F401
     gresho_analytic,
     clustered,
     by_name,
+    with_duplicates,
+    with_cold,
     positions_f64,
 )

@@ -255,6 +255,38 @@ def _h_from_knn(x, k=64):
     return ETA * n_loc ** (-1.0 / 3.0)
 
 
+def with_duplicates(p, frac=0.05, seed=5, vel_sigma=0.1, u_sigma=0.2):
+    """Edge case S:203: append copies of a seeded `frac` of the particles at EXACTLY the same
+    fixed-point position (coincident pairs, r_ij = 0 with j != i), with their own seeded
+    velocities and internal energies and the original's mass and h."""
+    rng = np.random.default_rng(seed)
+    n = p["X"].shape[0]
+    src = np.sort(rng.choice(n, max(1, int(frac * n)), replace=False))
+    k = src.size
+    q = dict(p)
+    q["name"] = p["name"] + "_dup"
+    q["X"] = np.ascontiguousarray(np.concatenate([p["X"], p["X"][src]]), dtype=np.uint32)
+    q["v"] = np.ascontiguousarray(np.concatenate([p["v"], p["v"][src] + rng.normal(0.0, vel_sigma, (k, 3))]),
+                                  dtype=np.float32)
+    u2 = p["u"][src] * np.exp(rng.normal(0.0, u_sigma, k))
+    q["u"] = np.ascontiguousarray(np.concatenate([p["u"], u2]), dtype=np.float32)
+    for f in ("m", "h", "alpha_v", "alpha_c"):
+        q[f] = np.ascontiguousarray(np.concatenate([p[f], p[f][src]]), dtype=np.float32)
+    return q
+
+
+def with_cold(p, frac=0.1, seed=6):
+    """Edge case: internal energy u = 0 (so P = c_s = 0) for a seeded `frac` of the particles,
+    next to particles with P > 0 (Eq. 20's pressure-weighted alpha_c,ij with one side at P = 0)."""
+    rng = np.random.default_rng(seed)
+    q = dict(p)
+    q["name"] = p["name"] + "_cold"
+    u = p["u"].copy()
+    u[rng.random(u.size) < frac] = 0.0
+    q["u"] = u
+    return q
+
+
 def by_name(name: str, **kw):
     """Named workloads used by tests and bench.py."""
     table = {

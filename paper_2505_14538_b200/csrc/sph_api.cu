@@ -88,23 +88,27 @@ __global__ void k_cell_start(int n, int ncells, int zbits, const unsigned int* _
 // Exactly equal fixed-point positions give equal sort keys (cell + z sub-bucket), so a particle's
 // coincident partners lie in its run of equal keys: flag every particle that has one and count the
 // directed pairs.  p indexes the sorted owned particles (keys[p] belongs to xh[p]).
+// (dup must be zero before the launch; each unordered pair is found once, by its first particle,
+// which flags both and counts it twice)
 __global__ void k_dup(int n, const unsigned int* __restrict__ keys, const uint4* __restrict__ xh, uint8_t* dup,
                       unsigned int* npairs) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const unsigned int k = keys[p];
+  if (p + 1 >= n || keys[p + 1] != k) return;  // (most particles: the next key differs)
   const uint4 a = xh[p];
   unsigned int m = 0;
-  for (int q = p - 1; q >= 0 && keys[q] == k; --q) {
-    const uint4 b = xh[q];
-    m += (b.x == a.x && b.y == a.y && b.z == a.z) ? 1u : 0u;
-  }
   for (int q = p + 1; q < n && keys[q] == k; ++q) {
     const uint4 b = xh[q];
-    m += (b.x == a.x && b.y == a.y && b.z == a.z) ? 1u : 0u;
+    if (b.x == a.x && b.y == a.y && b.z == a.z) {
+      dup[q] = 1;
+      ++m;
+    }
   }
-  dup[p] = m ? 1 : 0;
-  if (m) atomicAdd(npairs, m);
+  if (m) {
+    dup[p] = 1;
+    atomicAdd(npairs, 2u * m);
+  }
 }
 
 struct Persist {
@@ -964,6 +968,7 @@ sph_status rebuild_impl(sph_ctx* c) {
   // tile sizes below)
   CK(cudaMemsetAsync(c->scratch + 14, 0, 4, c->stream));
   if (n > 0) {
+    CK(cudaMemsetAsync(c->s.dup + c->gL, 0, (size_t)n, c->stream));
     k_dup<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->keys_alt, c->s.xh + c->gL, c->s.dup + c->gL, c->scratch + 14);
     c->launches++;
   }

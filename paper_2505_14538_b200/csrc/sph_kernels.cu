@@ -1050,6 +1050,7 @@ __device__ __forceinline__ void walk_prefix(const SS& S, const DevState& s, Walk
 // Then nhat = S0/(pi h^3), dn/dh = -(3 S0 + S1)/(pi h^4), rho = R0/(pi h^3),
 // drho/dh = -(3 R0 + R1)/(pi h^4), div = -Dv/(rho pi h^4), curl = Cv/(rho pi h^4),
 // g = nhat h^3 - eta^3 = S0/pi - eta^3, h g' = -S1/pi.
+constexpr int kDensInner = 6;  // Newton iterations per density pass inside the CTA
 __global__ void __launch_bounds__(256, 3) k_density(DevGrid g, DevPhys ph, DevState s,
                                                       const int* __restrict__ cell_start, int pass,
                                                       const uint8_t* __restrict__ blk_in, uint8_t* __restrict__ blk_out,
@@ -1095,54 +1096,82 @@ __global__ void __launch_bounds__(256, 3) k_density(DevGrid g, DevPhys ph, DevSt
     if (threadIdx.x == 0) s_ni = W.pref[T.ni];
   }
   __syncthreads();
-  const int ni = s_ni;
+  int ni = s_ni;
   if (pass > 0) walk_prefix(S, s, W, ni);
-  {
-    float4 pi4, vi4;
-    float hinv = 0.f, qband = 0.f;
-    double H2 = 0.0;
-    int gi = 0;
-    DenAcc a;
-    const uint32_t sb0 = smem_base(0), sb1 = smem_base(O1);
-    int ti_c = 0;  // tile slot of the walk's current particle (list_of -> begin)
-    walk_lists(
-        ni, W.pref, W.fin, W.head,
-        [&](int k) {  // (list_of runs right before begin: the slot lookup is shared)
-          i_slot(S, W.kl[k], ti_c, gi);
-          return s.nbr + (size_t)gi * g.lcap;
-        },
-        [&](int) {
-          const int ti = ti_c;
-          pi4 = smem4[ti];
-          vi4 = smem4[O1 + ti];
-          hinv = 1.f / pi4.w;
-          qband = g.eabs * hinv + 8e-6f;  // |q - 2| below this: decide in fp64
-          H2 = h2_exact(pi4.w, ph.gamma_k);
-          a = DenAcc{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0};
-        },
-        pair2_of([&](int j) {
-          const uint32_t o = (uint32_t)j << 4;
-          const float4 p = lds4(sb0 + o);
-          den_pair(a, pi4.x - p.x, pi4.y - p.y, pi4.z - p.z, hinv, qband, vi4, lds4(sb1 + o), [&]() {
-            return exact_neighbour(s.xh, gi, slot_global(S, nseg, j), H2, g.dscale[0], g.dscale[1], g.dscale[2]);
-          });
-        }),
-        [&]() { return a; });
-  }
-  __syncthreads();
+  // Newton iterations inside the CTA (h iteration, R7): a particle's density sums depend
+  // only on the positions and its own h (gather, W(r_ij, h_i)), so while its new h stays within
+  // its list radius and the cell, the next iteration walks its list again over the tile still in
+  // shared memory.  Only the particles that outgrow their list or cell (or reach kDensInner
+  // iterations here) are left active for another pass of the host loop (sph_density).
   unsigned long long npairs = 0, nfinal = 0;
-  for (int k = threadIdx.x; k < ni; k += blockDim.x) {
-    const DenAcc a = gather_acc(W, ni, k);
-    int ti, gi;
-    i_slot(S, W.kl[k], ti, gi);
-    if (s.wide && s.wide[gi]) continue;  // wide particles: k_wide_density
-    const DenOut o = den_epilogue(g, ph, s, a, gi, smem4[ti].w, smem4[O1 + ti].w, pass, hfac_stale);
-    npairs += (unsigned long long)o.nn;
-    if (o.final_) nfinal += (unsigned long long)o.nn;
-    if (o.give_up) atomicAdd(&s_unconv, 1);
-    if (o.active) s_active = 1;
-    if (o.exceeds) atomicExch(&ctr->h_exceeds, 1);
-    if (o.stale) atomicExch(&ctr->list_stale, 1);
+  for (int it = 0;; ++it) {
+    {
+      float4 pi4, vi4;
+      float hinv = 0.f, qband = 0.f;
+      double H2 = 0.0;
+      int gi = 0;
+      DenAcc a;
+      const uint32_t sb0 = smem_base(0), sb1 = smem_base(O1);
+      int ti_c = 0;  // tile slot of the walk's current particle (list_of -> begin)
+      walk_lists(
+          ni, W.pref, W.fin, W.head,
+          [&](int k) {  // (list_of runs right before begin: the slot lookup is shared)
+            i_slot(S, W.kl[k], ti_c, gi);
+            return s.nbr + (size_t)gi * g.lcap;
+          },
+          [&](int) {
+            const int ti = ti_c;
+            pi4 = smem4[ti];
+            vi4 = smem4[O1 + ti];
+            hinv = 1.f / pi4.w;
+            qband = g.eabs * hinv + 8e-6f;  // |q - 2| below this: decide in fp64
+            H2 = h2_exact(pi4.w, ph.gamma_k);
+            a = DenAcc{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0};
+          },
+          pair2_of([&](int j) {
+            const uint32_t o = (uint32_t)j << 4;
+            const float4 p = lds4(sb0 + o);
+            den_pair(a, pi4.x - p.x, pi4.y - p.y, pi4.z - p.z, hinv, qband, vi4, lds4(sb1 + o), [&]() {
+              return exact_neighbour(s.xh, gi, slot_global(S, nseg, j), H2, g.dscale[0], g.dscale[1], g.dscale[2]);
+            });
+          }),
+          [&]() { return a; });
+    }
+    __syncthreads();
+    const bool more = it + 1 < kDensInner;
+    for (int k = threadIdx.x; k < ni; k += blockDim.x) {
+      const DenAcc a = gather_acc(W, ni, k);
+      int ti, gi;
+      const int kl = W.kl[k];
+      i_slot(S, kl, ti, gi);
+      bool cont = false;
+      if (!(s.wide && s.wide[gi])) {  // wide particles: k_wide_density
+        const DenOut o = den_epilogue(g, ph, s, a, gi, smem4[ti].w, smem4[O1 + ti].w, pass + it, hfac_stale);
+        npairs += (unsigned long long)o.nn;
+        if (o.final_) nfinal += (unsigned long long)o.nn;
+        if (o.give_up) atomicAdd(&s_unconv, 1);
+        if (o.exceeds) atomicExch(&ctr->h_exceeds, 1);
+        if (o.stale) atomicExch(&ctr->list_stale, 1);
+        cont = o.active && !o.exceeds && !o.stale && more;
+        if (o.active && !cont) s_active = 1;
+        if (cont) smem4[ti].w = o.hn;
+      }
+      W.pref[k] = cont ? 1 : 0;
+    }
+    __syncthreads();
+    // the particles that keep iterating, compacted in block order (deterministic), through the
+    // walk's record area (consumed by the epilogue above)
+    block_exclusive_scan(W.pref, ni);
+    const int nnext = W.pref[ni];
+    if (nnext == 0) break;
+    int* tmp = reinterpret_cast<int*>(W.fin);
+    for (int k = threadIdx.x; k < ni; k += blockDim.x)
+      if (W.pref[k + 1] > W.pref[k]) tmp[W.pref[k]] = W.kl[k];
+    __syncthreads();
+    for (int k = threadIdx.x; k < nnext; k += blockDim.x) W.kl[k] = tmp[k];
+    __syncthreads();
+    ni = nnext;
+    walk_prefix(S, s, W, ni);
   }
   const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -1288,15 +1317,15 @@ __host__ __device__ __forceinline__ size_t force_records_bytes(int tcap) {
   return sp * (4 * 16) + ((sp + 3) & ~(size_t)3) * 4;  // four records + the slot's global index
 }
 
+// (no "memory" clobber: the reductions target global memory the kernel never reads, so the
+// shared-memory gathers of the next pair may be scheduled across them)
 __device__ __forceinline__ void red_add4(float4* p, const float4& v) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
-               : "memory");
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w));
 }
 // the same under a predicate (no branch around it in the pair loop)
 __device__ __forceinline__ void red_add4_if(float4* p, const float4& v, bool on) {
   asm volatile("{ .reg .pred q; setp.ne.u32 q, %5, 0; @q red.global.add.v4.f32 [%0], {%1, %2, %3, %4}; }" ::"l"(p),
-               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"((uint32_t)on)
-               : "memory");
+               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"((uint32_t)on));
 }
 __device__ __forceinline__ int lds1(uint32_t a) {
   int v;

@@ -98,10 +98,11 @@ struct DenOut {
   bool active;   // another pass needed
   bool exceeds;  // the new support outgrows the cell side
   bool stale;    // the new h outgrows the list radius
+  float hn;      // the new h (active)
 };
 __device__ __forceinline__ DenOut den_epilogue(const DevGrid& g, const DevPhys& ph, const DevState& s, const DenAcc& a,
                                                int gi, float h, float mi, int pass, float hfac_stale) {
-  DenOut o{a.nn - 1, false, false, false, false, false};  // (the self pair)
+  DenOut o{a.nn - 1, false, false, false, false, false, h};  // (the self pair)
   const float inv_pi = 1.f / kPi;
   const float hinv = 1.f / h;
   const float ih3 = inv_pi * hinv * hinv * hinv;
@@ -149,6 +150,7 @@ __device__ __forceinline__ DenOut den_epilogue(const DevGrid& g, const DevPhys& 
     s.active[gi] = 1;
     reinterpret_cast<unsigned int*>(&s.xh[gi])[3] = __float_as_uint(hn);
     o.active = true;
+    o.hn = hn;
     // a particle already wide may grow past the cell: its list search widens instead
     const bool wide = s.wide && s.wide[gi];
     o.exceeds = !wide && ph.gamma_k * hn * (1.f + g.skin) > g.side_min;

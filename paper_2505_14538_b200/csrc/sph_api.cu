@@ -318,6 +318,16 @@ struct sph_ctx {
   int* blk_list = nullptr;      // [nact] active block ids
   int* run_list = nullptr;      // [nrun] active indices of the blocks with a non-wide i particle
   size_t run_cap = 0;
+  // slab path: the halo exchanges after the density (X2) and gradient (X3) loops run on a
+  // communication stream while the next loop's interior blocks (tiles without ghost particles)
+  // run on the context stream; its boundary blocks wait for the exchange
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t ev_main = nullptr, ev_x2 = nullptr, ev_x3 = nullptr;
+  bool x2_pending = false, x3_pending = false;
+  uint8_t* side_flag = nullptr;  // [2 nact]: interior, boundary flags
+  int* side_list = nullptr;      // [2 nact]: interior active indices at 0, boundary ones at nact
+  size_t side_cap = 0, side_flag_cap = 0;
+  int n_int = 0, n_bnd = 0;
   int kz_hint = 0;              // KZ chosen at the last rebuild (first probe of the next)
   long long n_coinc = 0;        // directed coincident pairs of the owned particles (k_dup)
   uint32_t* cperm = nullptr;    // wide search grid: particles in coarse-cell order
@@ -630,6 +640,38 @@ sph_status halo(sph_ctx* c, void* base, size_t elem) {
   Xfer r[2] = {{left_of(c), b, (size_t)c->gL * elem},
                {right_of(c), b + (size_t)(c->gL + c->n_own) * elem, (size_t)c->gR * elem}};
   CKC(c->comm->exchange(s, 2, r, 2, c->stream));
+  return SPH_OK;
+}
+
+// The same exchange enqueued on stream st (untimed: it overlaps the interior blocks' loop).
+sph_status halo_on(sph_ctx* c, void* base, size_t elem, cudaStream_t st) {
+  char* b = static_cast<char*>(base);
+  Xfer s[2] = {{right_of(c), b + (size_t)(c->gL + c->n_own - c->planeR) * elem, (size_t)c->planeR * elem},
+               {left_of(c), b + (size_t)c->gL * elem, (size_t)c->planeL * elem}};
+  Xfer r[2] = {{left_of(c), b, (size_t)c->gL * elem},
+               {right_of(c), b + (size_t)(c->gL + c->n_own) * elem, (size_t)c->gR * elem}};
+  CKC(c->comm->exchange(s, 2, r, 2, st));
+  return SPH_OK;
+}
+
+// Start an asynchronous halo exchange of `n` arrays on the communication stream after the work
+// enqueued so far on the context stream; `ev` marks its completion.
+sph_status halo_async(sph_ctx* c, void* const* bases, const size_t* elems, int n, cudaEvent_t ev) {
+  CK(cudaEventRecord(c->ev_main, c->stream));
+  CK(cudaStreamWaitEvent(c->cstream, c->ev_main, 0));
+  for (int k = 0; k < n; ++k) {
+    const sph_status st = halo_on(c, bases[k], elems[k], c->cstream);
+    if (st != SPH_OK) return st;
+  }
+  CK(cudaEventRecord(ev, c->cstream));
+  return SPH_OK;
+}
+
+// The context stream waits for every pending asynchronous exchange.
+sph_status join_comm(sph_ctx* c) {
+  if (c->x2_pending) CK(cudaStreamWaitEvent(c->stream, c->ev_x2, 0));
+  if (c->x3_pending) CK(cudaStreamWaitEvent(c->stream, c->ev_x3, 0));
+  c->x2_pending = c->x3_pending = false;
   return SPH_OK;
 }
 
@@ -1116,6 +1158,31 @@ sph_status rebuild_impl(sph_ctx* c) {
   stage("descriptors");
   g.nrun = g.nact;  // (mark_wide narrows it to the blocks with tile particles)
   g.run_list = nullptr;
+  if (slab) {
+    // interior / boundary active blocks (the halo exchanges overlap the interior ones)
+    if ((st = grow_h(c, &c->side_flag, c->side_flag_cap, 2 * na)) != SPH_OK) return st;
+    if ((st = grow_h(c, &c->side_list, c->side_cap, 2 * na)) != SPH_OK) return st;
+    CK(launch_block_side(g, c->side_flag, c->side_flag + na, c->stream));
+    c->launches++;
+    thrust::counting_iterator<int> it(0);
+    size_t need = 0;
+    int* n_dev = reinterpret_cast<int*>(c->scratch + 8);
+    CK(cub::DeviceSelect::Flagged(nullptr, need, it, c->side_flag, c->side_list, n_dev, g.nact, c->stream));
+    if (need > c->sel_tmp_bytes) {
+      if (c->sel_tmp) cudaFree(c->sel_tmp);
+      c->sel_tmp = nullptr;
+      CK(cudaMalloc(&c->sel_tmp, need));
+      c->sel_tmp_bytes = need;
+    }
+    CK(cub::DeviceSelect::Flagged(c->sel_tmp, need, it, c->side_flag, c->side_list, n_dev, g.nact, c->stream));
+    CK(cub::DeviceSelect::Flagged(c->sel_tmp, need, it, c->side_flag + na, c->side_list + na, n_dev + 1, g.nact,
+                                  c->stream));
+    c->launches += 2;
+    CK(cudaMemcpyAsync(c->scratch_h + 8, c->scratch + 8, 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->n_int = g.nact > 0 ? (int)c->scratch_h[8] : 0;
+    c->n_bnd = g.nact > 0 ? (int)c->scratch_h[9] : 0;
+  }
   c->stale = false;
   c->lists_stale = true;
   c->dvc_valid = false;
@@ -1388,6 +1455,11 @@ sph_status sph_create(const sph_config* cfg, const sph_particles_in* in, sph_ctx
     c->own_stream = true;
   }
   if (c->slab) {
+    if (cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_main, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_x2, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_x3, cudaEventDisableTiming) != cudaSuccess)
+      return bail(SPH_ERR_CUDA);
     std::string e;
     c->comm = cfg->transport == SPH_TRANSPORT_LOOPBACK ? make_loopback_comm(cfg->loopback, c->rank, e)
                                                        : make_nccl_comm(cfg->nccl_uid, c->rank, c->nranks, e);
@@ -1417,16 +1489,19 @@ sph_status sph_create(const sph_config* cfg, const sph_particles_in* in, sph_ctx
 
 sph_status sph_set_particles(sph_ctx* c, const sph_particles_in* in) {
   GUARD(c);
+  if (join_comm(c) != SPH_OK) return SPH_ERR_CUDA;  // (pending halo exchanges)
   return ingest(c, in);
 }
 
 sph_status sph_rebuild_cells(sph_ctx* c) {
   GUARD(c);
+  if (join_comm(c) != SPH_OK) return SPH_ERR_CUDA;  // (pending halo exchanges)
   return rebuild(c);
 }
 
 sph_status sph_density(sph_ctx* c, sph_density_stats* stats) {
   GUARD(c);
+  if (join_comm(c) != SPH_OK) return SPH_ERR_CUDA;  // (pending halo exchanges)
   sph_status st;
   if (c->stale && (st = rebuild(c)) != SPH_OK) return st;
   if (c->ghost_v_stale && (st = halo(c, c->s.vm, sizeof(float4))) != SPH_OK) return st;
@@ -1487,8 +1562,12 @@ sph_status sph_density(sph_ctx* c, sph_density_stats* stats) {
   pairs_all += (long long)c->ctr_h->pairs_all;
   unconverged = c->ctr_h->unconverged;
   // ghosts need the final h and the gradient-loop record of their owners (X2)
-  if ((st = halo(c, c->s.xh, sizeof(uint4))) != SPH_OK) return st;
-  if ((st = halo(c, c->s.gq, sizeof(float4))) != SPH_OK) return st;
+  if (c->slab) {
+    void* const b[2] = {c->s.xh, c->s.gq};
+    const size_t e[2] = {sizeof(uint4), sizeof(float4)};
+    if ((st = halo_async(c, b, e, 2, c->ev_x2)) != SPH_OK) return st;
+    c->x2_pending = true;
+  }
   double un = unconverged;
   if ((st = allreduce(c, &un, 1, kMax)) != SPH_OK) return st;
   c->counters.pairs_density = (int64_t)final_pairs;
@@ -1521,16 +1600,37 @@ sph_status sph_gradient(sph_ctx* c, float dt) {
   if (!(dt > 0.f) || !std::isfinite(dt)) return fail(c, SPH_ERR_INVALID_ARG, "sph_gradient: dt must be > 0 (S:246)");
   sph_status st;
   if ((st = reset_ctr(c)) != SPH_OK) return st;
+  const int first = c->dprev_valid ? 0 : 1;
   {
     Timed tm(c, SPH_T_GRADIENT);
-    CK(launch_gradient(c->grid, c->phys, c->s, c->cell_start, dt, c->dprev_valid ? 0 : 1, c->ctr, c->stream));
-    CK(launch_wide_gradient(c->grid, c->phys, c->s, dt, c->dprev_valid ? 0 : 1, c->ctr, c->stream));
+    if (c->slab && c->x2_pending && !c->grid.run_list) {
+      // interior blocks while the X2 halo (ghost h and gradient records) is in flight, then the
+      // boundary blocks
+      DevGrid gi = c->grid, gb = c->grid;
+      gi.run_list = c->side_list;
+      gi.nrun = c->n_int;
+      gb.run_list = c->side_list + std::max(c->grid.nact, 1);
+      gb.nrun = c->n_bnd;
+      CK(launch_gradient(gi, c->phys, c->s, c->cell_start, dt, first, c->ctr, c->stream));
+      if ((st = join_comm(c)) != SPH_OK) return st;
+      CK(launch_gradient(gb, c->phys, c->s, c->cell_start, dt, first, c->ctr, c->stream));
+      c->launches += 1;
+    } else {
+      if ((st = join_comm(c)) != SPH_OK) return st;
+      CK(launch_gradient(c->grid, c->phys, c->s, c->cell_start, dt, first, c->ctr, c->stream));
+    }
+    CK(launch_wide_gradient(c->grid, c->phys, c->s, dt, first, c->ctr, c->stream));
   }
   c->launches += 1 + (c->s.n_wide > 0 ? 1 : 0);
   CK(cudaMemcpyAsync(&c->counters.pairs_gradient, &c->ctr->pairs, 8, cudaMemcpyDeviceToHost, c->stream));
-  // ghosts need their owners' force-loop records (X3)
-  if ((st = halo(c, c->s.fr1, sizeof(float4))) != SPH_OK) return st;
-  if ((st = halo(c, c->s.fr2, sizeof(float4))) != SPH_OK) return st;
+  // ghosts need their owners' force-loop records (X3): on the communication stream, overlapping
+  // the force loop's interior blocks
+  if (c->slab) {
+    void* const b[2] = {c->s.fr1, c->s.fr2};
+    const size_t e[2] = {sizeof(float4), sizeof(float4)};
+    if ((st = halo_async(c, b, e, 2, c->ev_x3)) != SPH_OK) return st;
+    c->x3_pending = true;
+  }
   c->dprev_valid = true;
   c->gradient_done = true;
   return SPH_OK;
@@ -1548,7 +1648,21 @@ sph_status sph_force(sph_ctx* c, float* dt_next) {
     Timed tm(c, SPH_T_FORCE);
     // the pair-once loop adds both sides of every pair into acc (ghost slots included)
     CK(cudaMemsetAsync(c->s.acc, 0, sizeof(float4) * (size_t)(c->gL + c->n_own + c->gR), c->stream));
-    CK(launch_force(c->grid, c->phys, c->s, c->cell_start, c->ctr, c->stream));
+    if (c->slab && c->x3_pending && !c->grid.run_list) {
+      // interior blocks while the X3 halo (ghost force records) is in flight, then the boundary
+      DevGrid gi = c->grid, gb = c->grid;
+      gi.run_list = c->side_list;
+      gi.nrun = c->n_int;
+      gb.run_list = c->side_list + std::max(c->grid.nact, 1);
+      gb.nrun = c->n_bnd;
+      CK(launch_force(gi, c->phys, c->s, c->cell_start, c->ctr, c->stream));
+      if ((st = join_comm(c)) != SPH_OK) return st;
+      CK(launch_force(gb, c->phys, c->s, c->cell_start, c->ctr, c->stream));
+      c->launches += 1;
+    } else {
+      if ((st = join_comm(c)) != SPH_OK) return st;
+      CK(launch_force(c->grid, c->phys, c->s, c->cell_start, c->ctr, c->stream));
+    }
     CK(launch_wide_force(c->grid, c->phys, c->s, c->ctr, c->stream));
     CK(launch_force_fin(c->gL, c->n_own, c->phys, c->s, c->ctr, c->stream));
   }
@@ -1570,6 +1684,7 @@ sph_status sph_force(sph_ctx* c, float* dt_next) {
 
 sph_status sph_kick_drift(sph_ctx* c, float dt_kick, float dt_drift) {
   GUARD(c);
+  if (join_comm(c) != SPH_OK) return SPH_ERR_CUDA;  // (pending halo exchanges)
   if (!std::isfinite(dt_kick) || !std::isfinite(dt_drift)) return fail(c, SPH_ERR_INVALID_ARG, "non-finite dt");
   const double f[3] = {std::ldexp(1.0, 32) / c->cfg.box[0], std::ldexp(1.0, 32) / c->cfg.box[1],
                        std::ldexp(1.0, 32) / c->cfg.box[2]};
@@ -1590,6 +1705,7 @@ sph_status sph_kick_drift(sph_ctx* c, float dt_kick, float dt_drift) {
 
 sph_status sph_get(sph_ctx* c, int field, void* dst, int on_device) {
   GUARD(c);
+  if (join_comm(c) != SPH_OK) return SPH_ERR_CUDA;  // (pending halo exchanges)
   if (!dst) return fail(c, SPH_ERR_INVALID_ARG, "dst is NULL");
   const DevState& s = c->s;
   const void* src = nullptr;
@@ -1671,6 +1787,7 @@ sph_status sph_get_counters(sph_ctx* c, sph_counters* out) {
 
 sph_status sph_synchronize(sph_ctx* c) {
   GUARD(c);
+  if (join_comm(c) != SPH_OK) return SPH_ERR_CUDA;
   CK(cudaStreamSynchronize(c->stream));
   return SPH_OK;
 }
@@ -1714,6 +1831,7 @@ sph_status sph_destroy(sph_ctx* c) {
   if (!c) return SPH_OK;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->cstream) cudaStreamSynchronize(c->cstream);
   DevState& s = c->s;
   void* ptrs[] = {s.xh, s.vm, s.u, s.av, s.ac, s.dprev, s.uid, s.orig, s.acc, c->alt.xh, c->alt.vm, c->alt.u,
                   c->alt.av, c->alt.ac, c->alt.dprev, c->alt.uid, c->alt.orig, c->alt.acc, s.dens, s.dvc, s.count,
@@ -1722,7 +1840,7 @@ sph_status sph_destroy(sph_ctx* c) {
                   c->blk[0], c->blk[1], c->ctr, c->scratch, c->out_tmp, c->mig_send, c->mig_recv, c->pc_send,
                   c->pc_recv, c->pc_scan, c->scan_tmp, c->cnt_dev, c->wide_flag, c->widx, c->wcount,
                   c->n_wide_dev, c->wnbr, c->sel_tmp, c->desc_buf, c->pref_buf,
-                  c->act_flag, c->blk_list, c->run_list, c->cperm, c->ccs};
+                  c->act_flag, c->blk_list, c->run_list, c->cperm, c->ccs, s.dup, c->side_flag, c->side_list};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->ctr_h) cudaFreeHost(c->ctr_h);
@@ -1734,6 +1852,9 @@ sph_status sph_destroy(sph_ctx* c) {
   }
   for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
   delete c->comm;
+  for (cudaEvent_t e : {c->ev_main, c->ev_x2, c->ev_x3})
+    if (e) cudaEventDestroy(e);
+  if (c->cstream) cudaStreamDestroy(c->cstream);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return SPH_OK;

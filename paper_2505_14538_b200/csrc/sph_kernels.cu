@@ -1536,6 +1536,26 @@ __global__ void k_block_run(DevGrid g, DevState s, uint8_t* flag) {
 
 }  // namespace
 
+// Slab decomposition: which active blocks have a tile inside the owned planes (interior: no
+// ghost particle in the tile, so the loop can run before the halo arrives) and which touch a
+// ghost plane (boundary).  Tile x-planes are [ix0 - 1, ix0 + bx]; the ghost planes are 0 and nx - 1.
+__global__ void k_block_side(DevGrid g, uint8_t* interior, uint8_t* boundary) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= g.nact) return;
+  int jx, jy, zb;
+  block_coords(g, g.blk_list[a], jx, jy, zb);
+  const int ix0 = g.ix_first + jx * g.bx;
+  const bool in = g.periodic_x || (ix0 - 1 > 0 && ix0 + g.bx < g.nx - 1);
+  interior[a] = in ? 1 : 0;
+  boundary[a] = in ? 0 : 1;
+}
+
+cudaError_t launch_block_side(const DevGrid& g, uint8_t* interior, uint8_t* boundary, cudaStream_t st) {
+  if (g.nact == 0) return cudaSuccess;
+  k_block_side<<<(g.nact + 255) / 256, 256, 0, st>>>(g, interior, boundary);
+  return cudaGetLastError();
+}
+
 int kernel_threads() { return kNW * 32; }
 size_t tile_desc_bytes() { return sizeof(TileDesc) + (size_t)(kMaxTileCells + 1) * sizeof(int2); }
 size_t tile_desc_header_bytes() { return sizeof(TileDesc); }

@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define SPH_ABI_VERSION 1
+#define SPH_ABI_VERSION 2
 
 typedef enum {
   SPH_OK = 0,
@@ -97,6 +97,9 @@ typedef struct {
                           /* from h_max overflow the tiles, size them from an h quantile and   */
                           /* treat the particles whose support exceeds a cell as "wide"       */
                           /* (global-index lists); default 1, 0 = fail instead */
+  int32_t decomp[3];      /* ranks per axis of the domain decomposition;*/
+                          /* {0,0,0} (default) = x-slabs {nranks, 1, 1}, the one implemented:   */
+                          /* any other product of nranks is SPH_ERR_INVALID_ARG                */
 } sph_config;
 
 /* Particle input.  n particles; arrays are host pointers (on_device = 0) or device
@@ -121,7 +124,8 @@ typedef struct {
   int32_t iterations;      /* density passes run (1 = converged on the first pass)         */
   int32_t unconverged;     /* particles not converged after the last pass                  */
   int32_t rebuilds;        /* cell-grid rebuilds forced by growing h                       */
-  int32_t reserved;
+  float max_rel_resid;     /* max over the particles of |nhat h^3 - eta^3| / eta^3 at their  */
+                           /* final h (the closure residual; <= h_tol when converged)  */
   int64_t pairs_density;   /* sum_i N_i at the final h (directed pairs, j != i)            */
   int64_t pairs_h_iter;    /* directed pairs evaluated over all density passes             */
 } sph_density_stats;

@@ -47,7 +47,8 @@ class Config(ctypes.Structure):
                 ("c_cfl", ctypes.c_float), ("fh_mode", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("stream", ctypes.c_void_p), ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
                 ("tile_cells_z", ctypes.c_int32), ("predict_h", ctypes.c_int32), ("transport", ctypes.c_int32),
-                ("nccl_uid", ctypes.c_void_p), ("loopback", ctypes.c_void_p), ("adaptive_h", ctypes.c_int32)]
+                ("nccl_uid", ctypes.c_void_p), ("loopback", ctypes.c_void_p), ("adaptive_h", ctypes.c_int32),
+                ("decomp", ctypes.c_int32 * 3)]
 
 SPH_TRANSPORT_NCCL, SPH_TRANSPORT_LOOPBACK = 0, 1
 
@@ -60,7 +61,8 @@ class ParticlesIn(ctypes.Structure):
 
 class DensityStats(ctypes.Structure):
     _fields_ = [("iterations", ctypes.c_int32), ("unconverged", ctypes.c_int32), ("rebuilds", ctypes.c_int32),
-                ("reserved", ctypes.c_int32), ("pairs_density", ctypes.c_int64), ("pairs_h_iter", ctypes.c_int64)]
+                ("max_rel_resid", ctypes.c_float), ("pairs_density", ctypes.c_int64),
+                ("pairs_h_iter", ctypes.c_int64)]
 
 
 PHASES = ["rebuild", "lists", "density", "gradient", "force", "kick_drift", "exchange"]

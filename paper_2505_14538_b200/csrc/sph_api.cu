@@ -498,6 +498,10 @@ sph_status validate_cfg(sph_ctx* c, const sph_config* cfg) {
       return fail(c, SPH_ERR_INVALID_ARG, "loopback transport needs a group (sph_loopback_create)");
     if (cfg->n_total <= 0) return fail(c, SPH_ERR_INVALID_ARG, "multi-rank contexts need n_total");
   }
+  const bool slabs = (cfg->decomp[0] == 0 && cfg->decomp[1] == 0 && cfg->decomp[2] == 0) ||
+                     (cfg->decomp[0] == cfg->nranks && cfg->decomp[1] == 1 && cfg->decomp[2] == 1);
+  if (!slabs)
+    return fail(c, SPH_ERR_INVALID_ARG, "decomp: only x-slabs {nranks, 1, 1} are implemented (DESIGN.md §9)");
   return SPH_OK;
 }
 
@@ -1052,13 +1056,32 @@ sph_status rebuild_impl(sph_ctx* c) {
     g.nzb = (g.nz + KZ - 1) / KZ;
     g.nblocks = g.nbx * g.nby * g.nzb;
     CK(cudaMemsetAsync(c->scratch + 6, 0, 8, c->stream));
-    // (the probe also flags the blocks with i particles: the last probe is at the chosen KZ)
+    // the blocks with i particles (flagged from the occupied cells, compacted in block order: one
+    // loop CTA each), then the largest tile and i count over those blocks only (a clustered box
+    // on a fine grid has mostly empty blocks); the last probe is at the chosen KZ
     if ((st = grow_h(c, &c->act_flag, c->act_cap, (size_t)g.nblocks)) != SPH_OK) return st;
-    CK(launch_tile_sizes(g, c->cell_start, (int*)(c->scratch + 6), (int*)(c->scratch + 7), c->act_flag,
-                         c->stream));
-    c->launches++;
+    if ((st = grow_h(c, &c->blk_list, c->list_cap, (size_t)g.nblocks)) != SPH_OK) return st;
+    CK(cudaMemsetAsync(c->act_flag, 0, (size_t)g.nblocks, c->stream));
+    CK(launch_block_flags(n, c->keys_alt, g, c->act_flag, c->stream));
+    {
+      thrust::counting_iterator<int> it(0);
+      size_t need = 0;
+      int* nact_dev = reinterpret_cast<int*>(c->scratch + 12);
+      CK(cub::DeviceSelect::Flagged(nullptr, need, it, c->act_flag, c->blk_list, nact_dev, g.nblocks, c->stream));
+      if (need > c->sel_tmp_bytes) {
+        if (c->sel_tmp) cudaFree(c->sel_tmp);
+        c->sel_tmp = nullptr;
+        CK(cudaMalloc(&c->sel_tmp, need));
+        c->sel_tmp_bytes = need;
+      }
+      CK(cub::DeviceSelect::Flagged(c->sel_tmp, need, it, c->act_flag, c->blk_list, nact_dev, g.nblocks, c->stream));
+      CK(launch_tile_sizes_list(g, c->cell_start, c->blk_list, nact_dev, (int*)(c->scratch + 6),
+                                (int*)(c->scratch + 7), c->stream));
+    }
+    c->launches += 3;
     if ((st = allreduce_dev(c, c->scratch + 6, 2, kMax)) != SPH_OK) return st;  // same capacities on every rank
     CK(cudaMemcpyAsync(c->scratch_h + 6, c->scratch + 6, 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(c->scratch_h + 12, c->scratch + 12, 4, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     double tmax[2] = {(double)c->scratch_h[6], (double)c->scratch_h[7]};
     g.tcap = std::max(32, (int)tmax[0]);
@@ -1088,30 +1111,16 @@ sph_status rebuild_impl(sph_ctx* c) {
     KZ = kz_lo == 0 ? (hint && hint < kz_hi ? hint : std::max(1, kz_hi / 2)) : (kz_lo + kz_hi) / 2;
   }
   c->kz_hint = g.KZ;
+  {
+    const char* e = getenv("SPH_DENS_INNER");  // (tuning: Newton iterations per pass inside the CTA)
+    g.dens_inner = e ? std::max(1, atoi(e)) : 6;
+  }
   c->n_coinc = (long long)c->scratch_h[14];  // (the tile-size probes synchronised the stream)
   g.coinc = c->n_coinc > 0 ? 1 : 0;
   stage("KZ chosen");
-  // the blocks with i particles, in block order: one loop CTA each (a clustered box on a fine
-  // grid has mostly empty blocks)
-  if ((st = grow_h(c, &c->blk_list, c->list_cap, (size_t)g.nblocks)) != SPH_OK) return st;
-  {
-    thrust::counting_iterator<int> it(0);
-    size_t need = 0;
-    int* nact_dev = reinterpret_cast<int*>(c->scratch + 12);
-    CK(cub::DeviceSelect::Flagged(nullptr, need, it, c->act_flag, c->blk_list, nact_dev, g.nblocks, c->stream));
-    if (need > c->sel_tmp_bytes) {
-      if (c->sel_tmp) cudaFree(c->sel_tmp);
-      c->sel_tmp = nullptr;
-      CK(cudaMalloc(&c->sel_tmp, need));
-      c->sel_tmp_bytes = need;
-    }
-    CK(cub::DeviceSelect::Flagged(c->sel_tmp, need, it, c->act_flag, c->blk_list, nact_dev, g.nblocks, c->stream));
-    c->launches++;
-    CK(cudaMemcpyAsync(c->scratch_h + 12, c->scratch + 12, 4, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    g.nact = (int)c->scratch_h[12];
-    g.blk_list = c->blk_list;
-  }
+  // the blocks with i particles of the last probe (its KZ), in block order
+  g.nact = n > 0 ? (int)c->scratch_h[12] : 0;
+  g.blk_list = c->blk_list;
   // k_lists: about one warp per 32 particles of a mean block (+10 %); the warps of a larger CTA
   // would only wait at its final barrier (the tile, not the warp count, limits CTAs per SM)
   g.lists_warps = std::max(2, std::min(8, (int)std::ceil(1.1 * n / std::max(g.nact, 1) / 32.0)));
@@ -1404,6 +1413,7 @@ void sph_config_default(sph_config* cfg) {
   cfg->nccl_uid = nullptr;
   cfg->loopback = nullptr;
   cfg->adaptive_h = 1;
+  cfg->decomp[0] = cfg->decomp[1] = cfg->decomp[2] = 0;
 }
 
 sph_status sph_nccl_unique_id(void* out128) {
@@ -1527,9 +1537,9 @@ sph_status sph_density(sph_ctx* c, sph_density_stats* stats) {
     }
     c->launches += 1 + (c->s.n_wide > 0 ? 1 : 0);
     ++passes_run;
-    // every rank takes the same branch: the pass's flags (h_exceeds .. wlist_overflow, seven
+    // every rank takes the same branch: the pass's flags (h_exceeds .. max_resid_bits, eight
     // uint32 in DevCounters) are reduced over ranks on the device, then read back once
-    if ((st = allreduce_dev(c, &c->ctr->h_exceeds, 7, kMax)) != SPH_OK) return st;
+    if ((st = allreduce_dev(c, &c->ctr->h_exceeds, 8, kMax)) != SPH_OK) return st;
     if ((st = sync_ctr(c)) != SPH_OK) return st;
     double fl[4] = {(double)c->ctr_h->active_next, (double)c->ctr_h->h_exceeds, (double)c->ctr_h->list_stale,
                     c->ctr_h->nonfinite == 2 ? 1.0 : 0.0};
@@ -1579,7 +1589,9 @@ sph_status sph_density(sph_ctx* c, sph_density_stats* stats) {
     stats->iterations = passes_run;
     stats->unconverged = unconverged;
     stats->rebuilds = rebuilds;
-    stats->reserved = 0;
+    float mr;
+    std::memcpy(&mr, &c->ctr_h->max_resid_bits, 4);
+    stats->max_rel_resid = mr;
     stats->pairs_density = (int64_t)final_pairs;
     stats->pairs_h_iter = pairs_all;
   }

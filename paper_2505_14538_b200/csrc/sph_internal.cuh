@@ -42,6 +42,7 @@ struct DevGrid {
   const void* desc_cells;  // [nblocks][kMaxTileCells + 1] per tile cell (tile offset, global start)
   int* desc_pref;     // [nblocks][icap + 1] list-group prefix of the block's particles (k_lists)
   int* desc_prefF;    // [nblocks][icap + 1] the same over the force part of each list (k_lists)
+  int dens_inner;     // Newton iterations per density pass inside the CTA (k_density; >= 1)
   int coinc;          // some particles share their exact position with another (k_dup): the lists drop
                       // those pairs
   float scale[3];     // L_a / 2^32 as f32 (fixed point -> length)
@@ -133,6 +134,7 @@ struct DevCounters {
   int list_stale;               // an h outgrew its list radius
   int list_overflow;            // max list length seen above lcap (0 = none)
   int wlist_overflow;           // max wide-list length seen above wlcap (0 = none)
+  unsigned int max_resid_bits;  // density: max |nhat h^3 - eta^3| / eta^3 of the finished particles (f32 bits)
 };
 
 // Launchers (sph_kernels.cu).  All enqueue on `st`.
@@ -172,5 +174,8 @@ size_t tile_desc_header_bytes();  // the descriptor alone
 cudaError_t launch_tile_desc(const DevGrid& g, const int* cell_start, cudaStream_t st);
 cudaError_t launch_block_run(const DevGrid& g, const DevState& s, uint8_t* flag, cudaStream_t st);
 cudaError_t launch_block_side(const DevGrid& g, uint8_t* interior, uint8_t* boundary, cudaStream_t st);
+cudaError_t launch_block_flags(int n, const unsigned int* keys, const DevGrid& g, uint8_t* flag, cudaStream_t st);
+cudaError_t launch_tile_sizes_list(const DevGrid& g, const int* cell_start, const int* list, const int* nlist,
+                                   int* max_tile, int* max_i, cudaStream_t st);
 
 }  // namespace sph

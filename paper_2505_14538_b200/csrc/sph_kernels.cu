@@ -1050,7 +1050,6 @@ __device__ __forceinline__ void walk_prefix(const SS& S, const DevState& s, Walk
 // Then nhat = S0/(pi h^3), dn/dh = -(3 S0 + S1)/(pi h^4), rho = R0/(pi h^3),
 // drho/dh = -(3 R0 + R1)/(pi h^4), div = -Dv/(rho pi h^4), curl = Cv/(rho pi h^4),
 // g = nhat h^3 - eta^3 = S0/pi - eta^3, h g' = -S1/pi.
-constexpr int kDensInner = 6;  // Newton iterations per density pass inside the CTA
 __global__ void __launch_bounds__(256, 3) k_density(DevGrid g, DevPhys ph, DevState s,
                                                       const int* __restrict__ cell_start, int pass,
                                                       const uint8_t* __restrict__ blk_in, uint8_t* __restrict__ blk_out,
@@ -1059,7 +1058,8 @@ __global__ void __launch_bounds__(256, 3) k_density(DevGrid g, DevPhys ph, DevSt
   __shared__ int s_ni;
   __shared__ unsigned long long s_pairs, s_final;
   __shared__ int s_unconv, s_active;
-  if (threadIdx.x == 0) { s_ni = 0; s_pairs = 0; s_final = 0; s_unconv = 0; s_active = 0; }
+  __shared__ unsigned int s_rmax;
+  if (threadIdx.x == 0) { s_ni = 0; s_pairs = 0; s_final = 0; s_unconv = 0; s_active = 0; s_rmax = 0u; }
   DESC_PROLOGUE();
   const int O1 = SP;  // T0 = smem4[j]: x, y, z, h   T1 = smem4[O1 + j]: vx, vy, vz, m
   WalkArea<DenAcc> W = walk_area<DenAcc>(reinterpret_cast<char*>(smem4 + 2 * SP), g.icap);
@@ -1101,9 +1101,10 @@ __global__ void __launch_bounds__(256, 3) k_density(DevGrid g, DevPhys ph, DevSt
   // Newton iterations inside the CTA (h iteration, R7): a particle's density sums depend
   // only on the positions and its own h (gather, W(r_ij, h_i)), so while its new h stays within
   // its list radius and the cell, the next iteration walks its list again over the tile still in
-  // shared memory.  Only the particles that outgrow their list or cell (or reach kDensInner
+  // shared memory.  Only the particles that outgrow their list or cell (or reach DevGrid::dens_inner
   // iterations here) are left active for another pass of the host loop (sph_density).
   unsigned long long npairs = 0, nfinal = 0;
+  float rmax = 0.f;  // largest closure residual of the particles finished here
   for (int it = 0;; ++it) {
     {
       float4 pi4, vi4;
@@ -1138,8 +1139,11 @@ __global__ void __launch_bounds__(256, 3) k_density(DevGrid g, DevPhys ph, DevSt
           [&]() { return a; });
     }
     __syncthreads();
-    const bool more = it + 1 < kDensInner;
-    for (int k = threadIdx.x; k < ni; k += blockDim.x) {
+    // (the continue flags stay in a register mask until every thread's epilogue has read the walk
+    // area -- gather_acc reads W.pref -- then go to W.pref for the compaction)
+    const bool more = it + 1 < g.dens_inner && ni <= 32 * (int)blockDim.x;
+    uint32_t cmask = 0u;
+    for (int k = threadIdx.x, q = 0; k < ni; k += blockDim.x, ++q) {
       const DenAcc a = gather_acc(W, ni, k);
       int ti, gi;
       const int kl = W.kl[k];
@@ -1149,6 +1153,7 @@ __global__ void __launch_bounds__(256, 3) k_density(DevGrid g, DevPhys ph, DevSt
         const DenOut o = den_epilogue(g, ph, s, a, gi, smem4[ti].w, smem4[O1 + ti].w, pass + it, hfac_stale);
         npairs += (unsigned long long)o.nn;
         if (o.final_) nfinal += (unsigned long long)o.nn;
+        if (o.final_) rmax = fmaxf(rmax, o.resid);
         if (o.give_up) atomicAdd(&s_unconv, 1);
         if (o.exceeds) atomicExch(&ctr->h_exceeds, 1);
         if (o.stale) atomicExch(&ctr->list_stale, 1);
@@ -1156,8 +1161,10 @@ __global__ void __launch_bounds__(256, 3) k_density(DevGrid g, DevPhys ph, DevSt
         if (o.active && !cont) s_active = 1;
         if (cont) smem4[ti].w = o.hn;
       }
-      W.pref[k] = cont ? 1 : 0;
+      if (cont) cmask |= 1u << q;
     }
+    __syncthreads();
+    for (int k = threadIdx.x, q = 0; k < ni; k += blockDim.x, ++q) W.pref[k] = (int)((cmask >> q) & 1u);
     __syncthreads();
     // the particles that keep iterating, compacted in block order (deterministic), through the
     // walk's record area (consumed by the epilogue above)
@@ -1179,12 +1186,15 @@ __global__ void __launch_bounds__(256, 3) k_density(DevGrid g, DevPhys ph, DevSt
     npairs += __shfl_xor_sync(kFull, npairs, o);
     nfinal += __shfl_xor_sync(kFull, nfinal, o);
   }
+  rmax = __int_as_float(warp_max(__float_as_int(rmax)));  // (non-negative: int order)
   if (lane == 0) {
     if (npairs) atomicAdd(&s_pairs, npairs);
     if (nfinal) atomicAdd(&s_final, nfinal);
+    if (rmax > 0.f) atomicMax(&s_rmax, __float_as_uint(rmax));
   }
   __syncthreads();
   if (threadIdx.x == 0) {
+    if (s_rmax) atomicMax(&ctr->max_resid_bits, s_rmax);
     if (s_pairs) atomicAdd(&ctr->pairs_all, s_pairs);  // all pairs of this pass (h iteration work)
     if (s_final) atomicAdd(&ctr->pairs, s_final);
     if (s_unconv) atomicAdd(&ctr->unconverged, s_unconv);
@@ -1519,6 +1529,49 @@ __global__ void k_tile_sizes(DevGrid g, const int* __restrict__ cell_start, int*
   if (ni) atomicMax(max_i, ni);
 }
 
+// Block id of grid column (jx, jy), z block zb: the inverse of block_coords.
+__device__ __forceinline__ int block_of(const DevGrid& g, int jx, int jy, int zb) {
+  const int sgm = jy / kStrip;
+  const int hs = min(kStrip, g.nby - sgm * kStrip);
+  const int c = sgm * kStrip * g.nbx + jx * hs + (jy - sgm * kStrip);
+  return c * g.nzb + zb;
+}
+
+// Flag the blocks holding an owned particle (cell ids from the sorted keys, cell << zbits): the
+// active blocks without a pass over every block of the grid (a clustered box's fine grid has
+// ~70x more blocks than occupied ones).  flag must be zero before the launch.
+__global__ void k_block_flags(int n, const unsigned int* __restrict__ keys, DevGrid g, uint8_t* flag) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const unsigned int cell = keys[p] >> g.zbits;
+  if (p > 0 && (keys[p - 1] >> g.zbits) == cell) return;  // (one thread per occupied cell)
+  if ((int)cell >= g.ncells) return;
+  const int cz = (int)(cell % (unsigned)g.nz);
+  const int cxy = (int)(cell / (unsigned)g.nz);
+  const int cy = cxy % g.ny, cx = cxy / g.ny;
+  if (cx < g.ix_first || cx >= g.ix_first + g.nxo) return;
+  flag[block_of(g, (cx - g.ix_first) / g.bx, cy / g.by, cz / g.KZ)] = 1;
+}
+
+// tile size and i count (max over the listed blocks), grid-stride over the device-side count
+__global__ void k_tile_sizes_list(DevGrid g, const int* __restrict__ cell_start, const int* __restrict__ list,
+                                  const int* __restrict__ nlist, int* max_tile, int* max_i) {
+  const int n = *nlist;
+  int mt = 0, mi = 0;
+  for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < n; a += gridDim.x * blockDim.x) {
+    int tot, ni;
+    block_counts(g, cell_start, list[a], tot, ni);
+    mt = max(mt, tot);
+    mi = max(mi, ni);
+  }
+  mt = warp_max(mt);
+  mi = warp_max(mi);
+  if ((threadIdx.x & 31) == 0) {
+    if (mt) atomicMax(max_tile, mt);
+    if (mi) atomicMax(max_i, mi);
+  }
+}
+
 // active blocks with a non-wide i particle (the loop kernels run only these)
 __global__ void k_block_run(DevGrid g, DevState s, uint8_t* flag) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1548,6 +1601,18 @@ __global__ void k_block_side(DevGrid g, uint8_t* interior, uint8_t* boundary) {
   const bool in = g.periodic_x || (ix0 - 1 > 0 && ix0 + g.bx < g.nx - 1);
   interior[a] = in ? 1 : 0;
   boundary[a] = in ? 0 : 1;
+}
+
+cudaError_t launch_block_flags(int n, const unsigned int* keys, const DevGrid& g, uint8_t* flag, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  k_block_flags<<<(n + 255) / 256, 256, 0, st>>>(n, keys, g, flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tile_sizes_list(const DevGrid& g, const int* cell_start, const int* list, const int* nlist,
+                                   int* max_tile, int* max_i, cudaStream_t st) {
+  k_tile_sizes_list<<<148 * 4, 256, 0, st>>>(g, cell_start, list, nlist, max_tile, max_i);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_block_side(const DevGrid& g, uint8_t* interior, uint8_t* boundary, cudaStream_t st) {

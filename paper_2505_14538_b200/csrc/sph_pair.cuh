@@ -99,10 +99,11 @@ struct DenOut {
   bool exceeds;  // the new support outgrows the cell side
   bool stale;    // the new h outgrows the list radius
   float hn;      // the new h (active)
+  float resid;   // final: |nhat h^3 - eta^3| / eta^3 (the closure residual)
 };
 __device__ __forceinline__ DenOut den_epilogue(const DevGrid& g, const DevPhys& ph, const DevState& s, const DenAcc& a,
                                                int gi, float h, float mi, int pass, float hfac_stale) {
-  DenOut o{a.nn - 1, false, false, false, false, false, h};  // (the self pair)
+  DenOut o{a.nn - 1, false, false, false, false, false, h, 0.f};  // (the self pair)
   const float inv_pi = 1.f / kPi;
   const float hinv = 1.f / h;
   const float ih3 = inv_pi * hinv * hinv * hinv;
@@ -136,6 +137,7 @@ __device__ __forceinline__ DenOut den_epilogue(const DevGrid& g, const DevPhys& 
     s.iters[gi] = conv ? it : -1;
     o.final_ = true;
     o.give_up = give_up;
+    o.resid = fabsf(gres) / ph.eta3;
   } else {
     // Newton with bracket + bisection (R7); g is non-decreasing in h
     float lo = pass == 0 ? 0.f : s.hlo[gi];

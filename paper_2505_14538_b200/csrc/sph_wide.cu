@@ -207,6 +207,7 @@ __global__ void __launch_bounds__(256) k_wide_density(DevGrid g, DevPhys ph, Dev
   const DenOut o = den_epilogue(g, ph, s, a, i, h, vi.w, pass, hfac_stale);
   atomicAdd(&ctr->pairs_all, (unsigned long long)o.nn);
   if (o.final_) atomicAdd(&ctr->pairs, (unsigned long long)o.nn);
+  if (o.final_ && o.resid > 0.f) atomicMax(&ctr->max_resid_bits, __float_as_uint(o.resid));
   if (o.give_up) atomicAdd(&ctr->unconverged, 1);
   if (o.active) atomicAdd(&ctr->active_next, 1);
   if (o.stale) atomicExch(&ctr->list_stale, 1);

@@ -42,7 +42,7 @@ def test_library_exports_every_declared_symbol(sphlib):
     L = sphlib.lib()
     for n in declared_functions():
         assert hasattr(L, n)
-    assert L.sph_abi_version() == 1
+    assert L.sph_abi_version() == 2
 
 
 def test_struct_layout_matches_header(sphlib, tmp_path):
@@ -53,9 +53,10 @@ def test_struct_layout_matches_header(sphlib, tmp_path):
 #include <stddef.h>
 #include "sph.h"
 int main(void) {
-  printf("%zu %zu %zu %zu %zu %zu %zu\n", sizeof(sph_config), offsetof(sph_config, stream),
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(sph_config), offsetof(sph_config, stream),
          offsetof(sph_config, tile_cells_z), sizeof(sph_particles_in), offsetof(sph_particles_in, id),
-         sizeof(sph_density_stats), sizeof(sph_counters));
+         sizeof(sph_density_stats), sizeof(sph_counters), offsetof(sph_config, decomp),
+         offsetof(sph_density_stats, max_rel_resid));
   return 0;
 }''')
     exe = tmp_path / "probe"
@@ -64,7 +65,7 @@ int main(void) {
     b = sphlib
     exp = [ctypes.sizeof(b.Config), b.Config.stream.offset, b.Config.tile_cells_z.offset,
            ctypes.sizeof(b.ParticlesIn), b.ParticlesIn.id.offset, ctypes.sizeof(b.DensityStats),
-           ctypes.sizeof(b.Counters)]
+           ctypes.sizeof(b.Counters), b.Config.decomp.offset, b.DensityStats.max_rel_resid.offset]
     assert got == exp
 
 

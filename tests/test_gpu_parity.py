@@ -131,6 +131,9 @@ def test_h_iteration_end_to_end(case, fac):
     eta3 = 1.2348 ** 3
     clos = np.abs(g4["nhat"].astype(np.float64) * g4["h"].astype(np.float64) ** 3 - eta3) / eta3
     assert clos.max() <= 1.2e-4
+    # the library's own report of the largest closure residual (sph_density_stats.max_rel_resid)
+    assert 0.0 < g4["stats"]["max_rel_resid"] <= 1e-4
+    assert abs(g4["stats"]["max_rel_resid"] - clos.max()) <= 2e-6
     # |g| <= 1e-4 eta^3 and h g' = 3 eta^3 Omega at the root -> |dh|/h <= 1e-4/(3 Omega)
     Omega = 1.0 + d["h"] / (3.0 * d["rho"]) * d["drho_dh"]
     assert np.all(np.abs(g4["h"] - d["h"]) <= 1.2e-4 / (3.0 * Omega) * d["h"])
@@ -212,6 +215,19 @@ def test_box_too_small_is_an_error():
     p = W.lattice(4, h_factor=1.0)
     with pytest.raises(SphError):
         Context(p)
+
+
+def test_decomposition_other_than_slabs_is_an_error():
+    """sph_config.decomp: {0,0,0} or {nranks,1,1} are x-slabs; bricks are not
+    implemented and are refused explicitly (SPH_ERR_INVALID_ARG)."""
+    from paper_2505_14538_b200 import Context, SphError
+
+    p = W.lattice(8, h_factor=1.0)
+    ctx = Context(p, decomp=(1, 1, 1))
+    ctx.close()
+    with pytest.raises(SphError) as e:
+        Context(p, decomp=(1, 2, 1))
+    assert e.value.status == 1
 
 
 def test_empty_input_is_an_error():

@@ -330,6 +330,7 @@ struct sph_ctx {
   int n_int = 0, n_bnd = 0;
   int kz_hint = 0;              // KZ chosen at the last rebuild (first probe of the next)
   long long n_coinc = 0;        // directed coincident pairs of the owned particles (k_dup)
+  float wide_margin = 0.2f;     // adaptive grid: DevGrid::wide_margin (env SPH_WIDE_MARGIN overrides)
   uint32_t* cperm = nullptr;    // wide search grid: particles in coarse-cell order
   size_t cperm_cap = 0;
   int* ccs = nullptr;           // its coarse cell starts
@@ -1237,23 +1238,32 @@ sph_status mark_wide(sph_ctx* c) {
     CK(dalloc(&c->wcount, (size_t)c->cap));
     CK(dalloc(&c->n_wide_dev, 1));
   }
-  CK(launch_mark_wide(n, c->grid, c->phys, s, c->wide_flag, c->stream));
-  c->launches++;
-  thrust::counting_iterator<int> it(0);
-  size_t need = 0;
-  CK(cub::DeviceSelect::Flagged(nullptr, need, it, c->wide_flag, c->widx, c->n_wide_dev, n, c->stream));
-  if (need > c->sel_tmp_bytes) {
-    if (c->sel_tmp) cudaFree(c->sel_tmp);
-    c->sel_tmp = nullptr;
-    CK(cudaMalloc(&c->sel_tmp, need));
-    c->sel_tmp_bytes = need;
+  // wide: support past the cell side, or within wide_margin of it (the margin is dropped when it
+  // would add more than 10 % to the wide set, e.g. a uniform region whose h sits at the threshold)
+  int nw = 0;
+  for (float margin : {c->wide_margin, 0.f}) {
+    c->grid.wide_margin = margin;
+    CK(cudaMemsetAsync(c->scratch + 15, 0, 4, c->stream));
+    CK(launch_mark_wide(n, c->grid, c->phys, s, c->wide_flag, c->scratch + 15, c->stream));
+    c->launches++;
+    thrust::counting_iterator<int> it(0);
+    size_t need = 0;
+    CK(cub::DeviceSelect::Flagged(nullptr, need, it, c->wide_flag, c->widx, c->n_wide_dev, n, c->stream));
+    if (need > c->sel_tmp_bytes) {
+      if (c->sel_tmp) cudaFree(c->sel_tmp);
+      c->sel_tmp = nullptr;
+      CK(cudaMalloc(&c->sel_tmp, need));
+      c->sel_tmp_bytes = need;
+    }
+    CK(cub::DeviceSelect::Flagged(c->sel_tmp, need, it, c->wide_flag, c->widx, c->n_wide_dev, n, c->stream));
+    c->launches++;
+    CK(cudaMemcpyAsync(c->scratch_h + 10, c->n_wide_dev, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(c->scratch_h + 15, c->scratch + 15, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    std::memcpy(&nw, c->scratch_h + 10, 4);
+    const int n0 = (int)c->scratch_h[15];
+    if (margin == 0.f || nw <= n0 + n0 / 10 + 1024) break;
   }
-  CK(cub::DeviceSelect::Flagged(c->sel_tmp, need, it, c->wide_flag, c->widx, c->n_wide_dev, n, c->stream));
-  c->launches++;
-  CK(cudaMemcpyAsync(c->scratch_h + 10, c->n_wide_dev, 4, cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-  int nw;
-  std::memcpy(&nw, c->scratch_h + 10, 4);
   s.n_wide = nw;
   s.wide = c->wide_flag;
   if (nw > 0) {
@@ -1295,6 +1305,7 @@ sph_status mark_wide(sph_ctx* c) {
     CK(launch_block_run(g, s, c->act_flag, c->stream));
     c->launches++;
     size_t need2 = 0;
+    thrust::counting_iterator<int> it(0);
     int* nrun_dev = reinterpret_cast<int*>(c->scratch + 13);
     CK(cub::DeviceSelect::Flagged(nullptr, need2, it, c->act_flag, c->run_list, nrun_dev, g.nact, c->stream));
     if (need2 > c->sel_tmp_bytes) {
@@ -1480,6 +1491,7 @@ sph_status sph_create(const sph_config* cfg, const sph_particles_in* in, sph_ctx
     }
   }
   fill_phys(c);
+  if (const char* m = getenv("SPH_WIDE_MARGIN")) c->wide_margin = (float)std::max(0.0, atof(m));
   if ((st = alloc_state(c)) != SPH_OK) return bail(st);
   if ((st = ingest(c, in)) != SPH_OK) return bail(st);
   if ((st = rebuild(c)) != SPH_OK) {

@@ -43,6 +43,7 @@ struct DevGrid {
   int* desc_pref;     // [nblocks][icap + 1] list-group prefix of the block's particles (k_lists)
   int* desc_prefF;    // [nblocks][icap + 1] the same over the force part of each list (k_lists)
   int dens_inner;     // Newton iterations per density pass inside the CTA (k_density; >= 1)
+  float wide_margin;  // adaptive grid: wide when (1 + skin)(1 + wide_margin) gamma_k h > the cell side
   int coinc;          // some particles share their exact position with another (k_dup): the lists drop
                       // those pairs
   float scale[3];     // L_a / 2^32 as f32 (fixed point -> length)
@@ -157,7 +158,7 @@ size_t force_smem(const DevGrid& g);
 cudaError_t launch_bank(int i0, int n, const DevGrid& g, const DevState& s, cudaStream_t st);
 // wide particles (sph_wide.cu)
 cudaError_t launch_mark_wide(int n, const DevGrid& g, const DevPhys& ph, const DevState& s, uint8_t* flag,
-                             cudaStream_t st);
+                             unsigned int* n0, cudaStream_t st);
 cudaError_t launch_coarse_keys(int n, int i0, const DevGrid& g, const DevState& s, unsigned int* keys,
                                unsigned int* vals, cudaStream_t st);
 cudaError_t launch_wide_lists(const DevGrid& g, const DevPhys& ph, const DevState& s, const int* cell_start,

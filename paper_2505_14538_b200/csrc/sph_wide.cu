@@ -81,12 +81,21 @@ __global__ void k_coarse_keys(int n, DevGrid g, DevState s, unsigned int* keys, 
   vals[i] = (unsigned)i;
 }
 
-__global__ void k_mark_wide(int n, DevGrid g, DevPhys ph, DevState s, uint8_t* flag) {
+// (a particle within wide_margin of the cell side is wide already: its h may still grow in the h
+// iteration, and outgrowing the cell mid-iteration costs a regrid of the lists; n0 counts the
+// particles wide without the margin, so the host can refuse a margin that flips a whole population)
+__global__ void k_mark_wide(int n, DevGrid g, DevPhys ph, DevState s, uint8_t* flag, unsigned int* n0) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const float R = (1.f + g.skin) * ph.gamma_k * __uint_as_float(s.xh[i].w);
-  flag[i] = R > g.side_min ? 1 : 0;
-  if (R > g.side_min) s.ncount[i] = 0;  // (no tile list: its block may not even run)
+  bool w0 = false;
+  if (i < n) {
+    const float R = (1.f + g.skin) * ph.gamma_k * __uint_as_float(s.xh[i].w);
+    const bool w = R * (1.f + g.wide_margin) > g.side_min;
+    w0 = R > g.side_min;
+    flag[i] = w ? 1 : 0;
+    if (w) s.ncount[i] = 0;  // (no tile list: its block may not even run)
+  }
+  const unsigned b = __ballot_sync(kFull, w0);
+  if ((threadIdx.x & 31) == 0 && b) atomicAdd(n0, (unsigned)__popc(b));
 }
 
 // One warp per wide particle.  Overflow of wlcap: the count is still returned (max in
@@ -350,9 +359,9 @@ __global__ void __launch_bounds__(256) k_wide_force(DevGrid g, DevPhys ph, DevSt
 }  // namespace
 
 cudaError_t launch_mark_wide(int n, const DevGrid& g, const DevPhys& ph, const DevState& s, uint8_t* flag,
-                             cudaStream_t st) {
+                             unsigned int* n0, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  k_mark_wide<<<(n + 255) / 256, 256, 0, st>>>(n, g, ph, s, flag);
+  k_mark_wide<<<(n + 255) / 256, 256, 0, st>>>(n, g, ph, s, flag, n0);
   return cudaGetLastError();
 }
 

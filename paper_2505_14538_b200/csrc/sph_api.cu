@@ -1090,7 +1090,7 @@ sph_status rebuild_impl(sph_ctx* c) {
     g.lcap = c->lcap;
     g.skin = c->cfg.cell_skin;
     // force: 256 threads when two CTAs fit an SM, else one CTA of 512
-    g.force_threads = 384;
+    g.force_threads = 448;
     if (force_smem(g) > kSmemTarget) g.force_threads = 512;
     const bool fits = force_smem(g) <= kSmemMax && lists_smem(g) <= kSmemMax && density_smem(g) <= kSmemMax &&
                       gradient_smem(g) <= kSmemMax && g.tcap < 32760;  // (list entries: 15-bit slots)

@@ -36,7 +36,7 @@ struct DevGrid {
   int icap;           // most i particles (owned by the block) of any block
   int lcap;           // neighbour-list capacity per particle (multiple of 16)
   float skin;         // list radius = (1 + skin) max(H_i, H_j)
-  int force_threads;  // block size of the force kernel: 384 (two CTAs per SM), or 512 when one CTA fills an SM
+  int force_threads;  // block size of the force kernel: 448 (two CTAs per SM), or 512 when one CTA fills an SM
   int lists_warps;    // warps per k_lists CTA: ~ the mean block particle count / 32 (a warp per 32)
   const void* desc;   // [nblocks] tile descriptors (sph_kernels.cu TileDesc, k_tile_desc)
   const void* desc_cells;  // [nblocks][kMaxTileCells + 1] per tile cell (tile offset, global start)

@@ -1343,8 +1343,9 @@ __device__ __forceinline__ int lds1(uint32_t a) {
   return v;
 }
 
-// (NT threads, MINB CTAs per SM: 384 x 2 when two tiles fit an SM -- 24 warps to hide the
-// gather latency, registers <= 85 --, else 512 x 1)
+// (NT threads, MINB CTAs per SM: 448 x 2 when two tiles fit an SM -- 28 warps to hide the
+// gather latency, registers <= 73; C4 force: 256 x 2 7.29, 384 x 2 7.32, 448 x 2 7.07, 512 x 2 7.27 ms
+// (spills) --, else 512 x 1)
 template <int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_force(DevGrid g, DevPhys ph, DevState s,
                                                     const int* __restrict__ cell_start,
@@ -1707,12 +1708,12 @@ cudaError_t launch_gradient(const DevGrid& g, const DevPhys& ph, const DevState&
 cudaError_t launch_force(const DevGrid& g, const DevPhys& ph, const DevState& s, const int* cell_start,
                          DevCounters* ctr, cudaStream_t st) {
   const size_t sm = force_smem(g);
-  const void* fn = g.force_threads == 512 ? (const void*)k_force<512, 1> : (const void*)k_force<384, 2>;
+  const void* fn = g.force_threads == 512 ? (const void*)k_force<512, 1> : (const void*)k_force<448, 2>;
   cudaError_t e = set_smem(fn, sm);
   if (e != cudaSuccess) return e;
   if (g.nrun == 0) return cudaSuccess;
   if (g.force_threads == 512) k_force<512, 1><<<g.nrun, 512, sm, st>>>(g, ph, s, cell_start, ctr);
-  else k_force<384, 2><<<g.nrun, 384, sm, st>>>(g, ph, s, cell_start, ctr);
+  else k_force<448, 2><<<g.nrun, 448, sm, st>>>(g, ph, s, cell_start, ctr);
   return cudaGetLastError();
 }
 

@@ -275,6 +275,17 @@ __device__ __forceinline__ void dt_candidate(const DevPhys& ph, DevCounters* ctr
   if (dt > 0.f && dt < CUDART_INF_F) atomicMin(&ctr->dt_bits, __float_as_uint(dt));
 }
 
+__device__ __forceinline__ void red_add4_w(float4* p, const float4& v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w));
+}
+
+// One warp per wide particle i over its list.  Every pair of the symmetric force set is
+// evaluated ONCE (force_pair2: both sides, Eqs. 17-18) by exactly one particle and applied to
+// both: a tile partner never evaluates a pair with a wide one (k_lists keeps those out of its
+// force part), so i does; a wide partner that listed i too does it only if it has the lower index;
+// one that did not list i leaves it to i.  i's side is reduced over the warp (lane order), j's
+// goes to acc[j] with one vector reduction.  v_sig and N_force: i's over its list; a partner
+// that did not list i gets its share of the pair here (atomics), with its CFL candidate.
 __global__ void __launch_bounds__(256) k_wide_force(DevGrid g, DevPhys ph, DevState s, DevCounters* __restrict__ ctr) {
   const int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (wi >= s.n_wide) return;
@@ -287,20 +298,28 @@ __global__ void __launch_bounds__(256) k_wide_force(DevGrid g, DevPhys ph, DevSt
   const int cxi = cell_axis(xi.x, g.nx), cyi = cell_axis(xi.y, g.ny), czi = cell_axis(xi.z, g.nz);
   const uint32_t* lst = s.wnbr + (size_t)wi * s.wlcap;
   const int n = s.wcount[wi];
-  ForceAcc a{0.f, 0.f, 0.f, 0.f, 2.f * I.a.z, 0};
-  int scattered = 0;
+  float4 ai = make_float4(0.f, 0.f, 0.f, 0.f);
+  float vmax = 2.f * I.a.z;  // (R15)
+  int nn = 0;
   for (int k = lane; k < n; k += 32) {
     const int j = (int)__ldg(lst + k);
     const uint4 xj = s.xh[j];
     const float hj = __uint_as_float(xj.w);
     const ForceSide J = side_of(s, j, hj);
     const float3 d = rel(g, xi, xj);
-    auto exact = [&]() {
-      return exact_neighbour(s.xh, i, j, fmax(Hi2, h2_exact(hj, ph.gamma_k)), g.dscale[0], g.dscale[1], g.dscale[2]);
-    };
-    float vs;
-    int in;
-    force_pair(a, d.x, d.y, d.z, I, J, ph.beta, kBandW, exact, vs, in);
+    // membership of the symmetric set, r < max(H_i, H_j) (R3; fp64 inside the band), and the
+    // pair's signal velocity (Eqs. 10-11)
+    const float r2 = fmaf(d.z, d.z, fmaf(d.y, d.y, d.x * d.x));
+    const float rinv = rinv_safe(r2);
+    const float r = r2 * rinv;
+    const float dd = fminf(r * I.hinv, r * J.hinv) - 2.f;
+    int in = neg(dd);
+    if (fabsf(dd) < kBandW)
+      in = exact_neighbour(s.xh, i, j, fmax(Hi2, h2_exact(hj, ph.gamma_k)), g.dscale[0], g.dscale[1], g.dscale[2]);
+    const float vrr = fmaf(I.v.z - J.v.z, d.z, fmaf(I.v.y - J.v.y, d.y, (I.v.x - J.v.x) * d.x)) * rinv;
+    const float vs = fmaf(-ph.beta, fminf(vrr, 0.f), I.a.z + J.a.z);
+    nn += in;
+    vmax = fmaxf(vmax, in ? vs : 0.f);
     // did j list i?  tile particles list the cells within +-1 of their own, wide ones the
     // cells within their list radius at build time (k_wide_lists)
     const int cxj = cell_axis(xj.x, g.nx), cyj = cell_axis(xj.y, g.ny), czj = cell_axis(xj.z, g.nz);
@@ -315,45 +334,31 @@ __global__ void __launch_bounds__(256) k_wide_force(DevGrid g, DevPhys ph, DevSt
     } else {
       seen = within(cxi, cxj, 1, g.nx) && within(cyi, cyj, 1, g.ny) && within(czi, czj, 1, g.nz);
     }
-    // j's side of the pair: a tile particle never evaluates a pair with a wide partner (k_lists
-    // keeps those out of its force part), a wide one only if its own list holds i
-    if (j != i && (!jwide || !seen)) {
-      // j's side of the pair (r_ji = -r_ij): the same symmetric terms, its own accumulators
-      ForceAcc b{0.f, 0.f, 0.f, 0.f, 0.f, 0};
-      float vs2;
-      int in2;
-      force_pair(b, -d.x, -d.y, -d.z, J, I, ph.beta, kBandW, exact, vs2, in2);
-      atomicAdd(&s.acc[j].x, b.ax);
-      atomicAdd(&s.acc[j].y, b.ay);
-      atomicAdd(&s.acc[j].z, b.az);
-      atomicAdd(&s.acc[j].w, b.du);
-      // v_sig and N_force of a partner that listed i already hold the pair (gradient loop)
-      if (in2 && !seen) {
-        atomicMax(reinterpret_cast<int*>(&s.vsig[j]), __float_as_int(vs2));
-        atomicAdd(&s.countf[j], 1);
-        dt_candidate(ph, ctr, hj, vs2);
-        ++scattered;
-      }
+    if (j != i && (!jwide || !seen || i < j)) {
+      float4 jo;
+      force_pair2(ai, jo, d.x, d.y, d.z, I, J, ph.beta);
+      red_add4_w(s.acc + j, jo);
+    }
+    // v_sig and N_force of a partner that listed i already hold the pair (gradient loop)
+    if (j != i && in && !seen) {
+      atomicMax(reinterpret_cast<int*>(&s.vsig[j]), __float_as_int(vs));
+      atomicAdd(&s.countf[j], 1);
+      dt_candidate(ph, ctr, hj, vs);
     }
   }
-  a.ax = warp_sum(a.ax);
-  a.ay = warp_sum(a.ay);
-  a.az = warp_sum(a.az);
-  a.du = warp_sum(a.du);
-  a.vmax = warp_fmax(a.vmax);
-  a.nn = warp_isum(a.nn);
-  scattered = warp_isum(scattered);
+  ai.x = warp_sum(ai.x);
+  ai.y = warp_sum(ai.y);
+  ai.z = warp_sum(ai.z);
+  ai.w = warp_sum(ai.w);
+  vmax = warp_fmax(vmax);
+  nn = warp_isum(nn);
   if (lane != 0) return;
-  atomicAdd(&s.acc[i].x, a.ax);
-  atomicAdd(&s.acc[i].y, a.ay);
-  atomicAdd(&s.acc[i].z, a.az);
-  atomicAdd(&s.acc[i].w, a.du);
-  atomicMax(reinterpret_cast<int*>(&s.vsig[i]), __float_as_int(a.vmax));
-  atomicAdd(&s.countf[i], a.nn - 1);  // (the self pair)
-  dt_candidate(ph, ctr, h, a.vmax);
-  if (!(isfinite(a.vmax) && isfinite(a.ax) && isfinite(a.ay) && isfinite(a.az) && isfinite(a.du)))
+  red_add4_w(s.acc + i, ai);
+  atomicMax(reinterpret_cast<int*>(&s.vsig[i]), __float_as_int(vmax));
+  atomicAdd(&s.countf[i], nn - 1);  // (the self pair)
+  dt_candidate(ph, ctr, h, vmax);
+  if (!(isfinite(vmax) && isfinite(ai.x) && isfinite(ai.y) && isfinite(ai.z) && isfinite(ai.w)))
     atomicExch(&ctr->nonfinite, 1);
-  (void)scattered;  // (N_force is summed over all particles by k_force_fin)
 }
 
 }  // namespace

@@ -26,7 +26,7 @@ def stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or stale():
         tmp = LIB + ".tmp"
-        cmd = [NVCC] + FLAGS + ["-o", tmp] + SOURCES
+        cmd = [NVCC] + FLAGS + os.environ.get("SPH_NVCC_EXTRA", "").split() + ["-o", tmp] + SOURCES
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         out = subprocess.run(cmd, capture_output=True, text=True)

@@ -331,6 +331,7 @@ struct sph_ctx {
   int kz_hint = 0;              // KZ chosen at the last rebuild (first probe of the next)
   long long n_coinc = 0;        // directed coincident pairs of the owned particles (k_dup)
   float wide_margin = 0.2f;     // adaptive grid: DevGrid::wide_margin (env SPH_WIDE_MARGIN overrides)
+  int sparse_wide = 32;         // adaptive grid: blocks with fewer tile particles go wide (env SPH_SPARSE_WIDE; 0 = off)
   uint32_t* cperm = nullptr;    // wide search grid: particles in coarse-cell order
   size_t cperm_cap = 0;
   int* ccs = nullptr;           // its coarse cell starts
@@ -1264,6 +1265,24 @@ sph_status mark_wide(sph_ctx* c) {
     const int n0 = (int)c->scratch_h[15];
     if (margin == 0.f || nw <= n0 + n0 / 10 + 1024) break;
   }
+  // sparse blocks' tile particles are handled as wide too (k_sparse_wide)
+  if (c->sparse_wide > 0 && nw > 0) {
+    CK(launch_sparse_wide(c->grid, c->wide_flag, s.ncount, c->sparse_wide, c->stream));
+    thrust::counting_iterator<int> it(0);
+    size_t need = 0;
+    CK(cub::DeviceSelect::Flagged(nullptr, need, it, c->wide_flag, c->widx, c->n_wide_dev, n, c->stream));
+    if (need > c->sel_tmp_bytes) {
+      if (c->sel_tmp) cudaFree(c->sel_tmp);
+      c->sel_tmp = nullptr;
+      CK(cudaMalloc(&c->sel_tmp, need));
+      c->sel_tmp_bytes = need;
+    }
+    CK(cub::DeviceSelect::Flagged(c->sel_tmp, need, it, c->wide_flag, c->widx, c->n_wide_dev, n, c->stream));
+    c->launches += 2;
+    CK(cudaMemcpyAsync(c->scratch_h + 10, c->n_wide_dev, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    std::memcpy(&nw, c->scratch_h + 10, 4);
+  }
   s.n_wide = nw;
   s.wide = c->wide_flag;
   if (nw > 0) {
@@ -1492,6 +1511,7 @@ sph_status sph_create(const sph_config* cfg, const sph_particles_in* in, sph_ctx
   }
   fill_phys(c);
   if (const char* m = getenv("SPH_WIDE_MARGIN")) c->wide_margin = (float)std::max(0.0, atof(m));
+  if (const char* m = getenv("SPH_SPARSE_WIDE")) c->sparse_wide = std::max(0, atoi(m));
   if ((st = alloc_state(c)) != SPH_OK) return bail(st);
   if ((st = ingest(c, in)) != SPH_OK) return bail(st);
   if ((st = rebuild(c)) != SPH_OK) {

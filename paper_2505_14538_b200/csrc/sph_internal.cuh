@@ -174,6 +174,7 @@ size_t tile_desc_bytes();  // descriptor + per-cell table, per block
 size_t tile_desc_header_bytes();  // the descriptor alone
 cudaError_t launch_tile_desc(const DevGrid& g, const int* cell_start, cudaStream_t st);
 cudaError_t launch_block_run(const DevGrid& g, const DevState& s, uint8_t* flag, cudaStream_t st);
+cudaError_t launch_sparse_wide(const DevGrid& g, uint8_t* wide, int32_t* ncount, int kmin, cudaStream_t st);
 cudaError_t launch_block_side(const DevGrid& g, uint8_t* interior, uint8_t* boundary, cudaStream_t st);
 cudaError_t launch_block_flags(int n, const unsigned int* keys, const DevGrid& g, uint8_t* flag, cudaStream_t st);
 cudaError_t launch_tile_sizes_list(const DevGrid& g, const int* cell_start, const int* list, const int* nlist,

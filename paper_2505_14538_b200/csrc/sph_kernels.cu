@@ -980,6 +980,14 @@ struct WalkArea {
   Acc* fin;   // [icap]  whole particles (split ones: the part of the thread whose range ends inside)
   Acc* head;  // [threads] split particle a thread's range starts in
 };
+#ifndef SPH_DENS_T
+#define SPH_DENS_T 256
+#endif
+#ifndef SPH_GRAD_T
+#define SPH_GRAD_T 256
+#endif
+constexpr int kDensT = SPH_DENS_T;  // k_density threads per CTA (3 CTAs per SM)
+constexpr int kGradT = SPH_GRAD_T;  // k_gradient threads per CTA (3 CTAs per SM)
 template <class Acc>
 __host__ __device__ __forceinline__ size_t walk_bytes(int icap, int threads = kNW * 32) {
   return (((size_t)(icap + 1) * 4 + 15) & ~(size_t)15) + (((size_t)icap * 4 + 15) & ~(size_t)15) +
@@ -1050,7 +1058,7 @@ __device__ __forceinline__ void walk_prefix(const SS& S, const DevState& s, Walk
 // Then nhat = S0/(pi h^3), dn/dh = -(3 S0 + S1)/(pi h^4), rho = R0/(pi h^3),
 // drho/dh = -(3 R0 + R1)/(pi h^4), div = -Dv/(rho pi h^4), curl = Cv/(rho pi h^4),
 // g = nhat h^3 - eta^3 = S0/pi - eta^3, h g' = -S1/pi.
-__global__ void __launch_bounds__(256, 3) k_density(DevGrid g, DevPhys ph, DevState s,
+__global__ void __launch_bounds__(kDensT, 3) k_density(DevGrid g, DevPhys ph, DevState s,
                                                       const int* __restrict__ cell_start, int pass,
                                                       const uint8_t* __restrict__ blk_in, uint8_t* __restrict__ blk_out,
                                                       float hfac_stale, DevCounters* __restrict__ ctr) {
@@ -1207,7 +1215,7 @@ __global__ void __launch_bounds__(256, 3) k_density(DevGrid g, DevPhys ph, DevSt
 // Brookshaw Laplacian lap u_i = 2 sum_j (m_j/rho_j)(u_i - u_j) dW/dr / r (R16), gathered
 // over r_ij < H_i; the gradient ghost (alpha_v Eqs. 12-15, alpha_c Eqs. 21-24; R17-R21)
 // runs in the epilogue and writes the force-loop records.
-__global__ void __launch_bounds__(256, 3) k_gradient(DevGrid g, DevPhys ph, DevState s,
+__global__ void __launch_bounds__(kGradT, 3) k_gradient(DevGrid g, DevPhys ph, DevState s,
                                                        const int* __restrict__ cell_start, float dt, int first_step,
                                                        DevCounters* __restrict__ ctr) {
   __shared__ unsigned long long s_pairs;
@@ -1573,6 +1581,30 @@ __global__ void k_tile_sizes_list(DevGrid g, const int* __restrict__ cell_start,
   }
 }
 
+// Sparse blocks (adaptive grid): a block with fewer than kmin tile (non-wide) i particles pays a
+// whole tile staging for them; its particles are handled as wide instead (global-index lists, one
+// warp each), cheaper per particle on a clustered box's mostly empty fine grid.
+__global__ void k_sparse_wide(DevGrid g, uint8_t* wide, int32_t* ncount, int kmin) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= g.nact) return;
+  const TileDesc* D = reinterpret_cast<const TileDesc*>(g.desc) + a;
+  int cnt = 0;
+  for (int r = 0; r < kMaxICols; ++r) {
+    const int c = D->pre[r + 1] - D->pre[r], g0 = D->g0[r];
+    for (int k = 0; k < c; ++k)
+      if (!wide[g0 + k] && ++cnt >= kmin) return;
+  }
+  if (cnt == 0) return;
+  for (int r = 0; r < kMaxICols; ++r) {
+    const int c = D->pre[r + 1] - D->pre[r], g0 = D->g0[r];
+    for (int k = 0; k < c; ++k)
+      if (!wide[g0 + k]) {
+        wide[g0 + k] = 1;
+        ncount[g0 + k] = 0;  // (no tile list)
+      }
+  }
+}
+
 // active blocks with a non-wide i particle (the loop kernels run only these)
 __global__ void k_block_run(DevGrid g, DevState s, uint8_t* flag) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1632,6 +1664,12 @@ cudaError_t launch_tile_desc(const DevGrid& g, const int* cell_start, cudaStream
   return cudaGetLastError();
 }
 
+cudaError_t launch_sparse_wide(const DevGrid& g, uint8_t* wide, int32_t* ncount, int kmin, cudaStream_t st) {
+  if (g.nact == 0 || kmin <= 0) return cudaSuccess;
+  k_sparse_wide<<<(g.nact + 255) / 256, 256, 0, st>>>(g, wide, ncount, kmin);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_block_run(const DevGrid& g, const DevState& s, uint8_t* flag, cudaStream_t st) {
   if (g.nact == 0) return cudaSuccess;
   k_block_run<<<(g.nact + 255) / 256, 256, 0, st>>>(g, s, flag);
@@ -1643,8 +1681,12 @@ size_t lists_smem(const DevGrid& g) {
   return lists_a_bytes(g, nw) + (size_t)((g.tcap + kNSent + 1) >> 1) * 16 + lists_slot_bytes(g) +
          lists_zw_bytes(g) + lists_slot_bytes(g);
 }
-size_t density_smem(const DevGrid& g) { return (size_t)(g.tcap + kNSent) * (2 * 16) + walk_bytes<DenAcc>(g.icap); }
-size_t gradient_smem(const DevGrid& g) { return (size_t)(g.tcap + kNSent) * (3 * 16) + walk_bytes<GradAcc>(g.icap); }
+size_t density_smem(const DevGrid& g) {
+  return (size_t)(g.tcap + kNSent) * (2 * 16) + walk_bytes<DenAcc>(g.icap, kDensT);
+}
+size_t gradient_smem(const DevGrid& g) {
+  return (size_t)(g.tcap + kNSent) * (3 * 16) + walk_bytes<GradAcc>(g.icap, kGradT);
+}
 size_t force_smem(const DevGrid& g) { return force_records_bytes(g.tcap) + (size_t)(g.icap + 1) * 8; }
 
 cudaError_t launch_tile_sizes(const DevGrid& g, const int* cell_start, int* max_tile, int* max_i, uint8_t* flag,
@@ -1691,7 +1733,7 @@ cudaError_t launch_density(const DevGrid& g, const DevPhys& ph, const DevState& 
   cudaError_t e = set_smem((const void*)k_density, sm);
   if (e != cudaSuccess) return e;
   if (g.nrun == 0) return cudaSuccess;
-  k_density<<<g.nrun, kNW * 32, sm, st>>>(g, ph, s, cell_start, pass, blk_in, blk_out, hfac_stale, ctr);
+  k_density<<<g.nrun, kDensT, sm, st>>>(g, ph, s, cell_start, pass, blk_in, blk_out, hfac_stale, ctr);
   return cudaGetLastError();
 }
 
@@ -1701,7 +1743,7 @@ cudaError_t launch_gradient(const DevGrid& g, const DevPhys& ph, const DevState&
   cudaError_t e = set_smem((const void*)k_gradient, sm);
   if (e != cudaSuccess) return e;
   if (g.nrun == 0) return cudaSuccess;
-  k_gradient<<<g.nrun, kNW * 32, sm, st>>>(g, ph, s, cell_start, dt, first_step, ctr);
+  k_gradient<<<g.nrun, kGradT, sm, st>>>(g, ph, s, cell_start, dt, first_step, ctr);
   return cudaGetLastError();
 }
 

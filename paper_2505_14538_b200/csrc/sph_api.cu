@@ -445,6 +445,7 @@ sph_status alloc_state(sph_ctx* c) {
   CK(dalloc(&a.dprev, n)); CK(dalloc(&a.uid, n)); CK(dalloc(&a.orig, n)); CK(dalloc(&a.acc, n));
   CK(dalloc(&s.dens, n)); CK(dalloc(&s.dvc, n)); CK(dalloc(&s.count, n)); CK(dalloc(&s.fin, n));
   CK(dalloc(&s.gq, n)); CK(dalloc(&s.hlo, n)); CK(dalloc(&s.hhi, n)); CK(dalloc(&s.iters, n));
+  CK(dalloc(&s.vc, n)); CK(dalloc(&s.um, n));
   CK(dalloc(&s.active, n)); CK(dalloc(&s.grad, n)); CK(dalloc(&s.fr1, n)); CK(dalloc(&s.fr2, n));
   CK(dalloc(&s.vsig, n)); CK(dalloc(&s.countf, n)); CK(dalloc(&s.dup, n));
   CK(cudaMemset(s.dup, 0, n));
@@ -1605,9 +1606,9 @@ sph_status sph_density(sph_ctx* c, sph_density_stats* stats) {
   unconverged = c->ctr_h->unconverged;
   // ghosts need the final h and the gradient-loop record of their owners (X2)
   if (c->slab) {
-    void* const b[2] = {c->s.xh, c->s.gq};
-    const size_t e[2] = {sizeof(uint4), sizeof(float4)};
-    if ((st = halo_async(c, b, e, 2, c->ev_x2)) != SPH_OK) return st;
+    void* const b[4] = {c->s.xh, c->s.gq, c->s.vc, c->s.um};
+    const size_t e[4] = {sizeof(uint4), sizeof(float4), sizeof(float4), sizeof(float2)};
+    if ((st = halo_async(c, b, e, 4, c->ev_x2)) != SPH_OK) return st;
     c->x2_pending = true;
   }
   double un = unconverged;
@@ -1884,7 +1885,8 @@ sph_status sph_destroy(sph_ctx* c) {
                   c->blk[0], c->blk[1], c->ctr, c->scratch, c->out_tmp, c->mig_send, c->mig_recv, c->pc_send,
                   c->pc_recv, c->pc_scan, c->scan_tmp, c->cnt_dev, c->wide_flag, c->widx, c->wcount,
                   c->n_wide_dev, c->wnbr, c->sel_tmp, c->desc_buf, c->pref_buf,
-                  c->act_flag, c->blk_list, c->run_list, c->cperm, c->ccs, s.dup, c->side_flag, c->side_list};
+                  c->act_flag, c->blk_list, c->run_list, c->cperm, c->ccs, s.dup, c->side_flag, c->side_list,
+                  s.vc, s.um};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->ctr_h) cudaFreeHost(c->ctr_h);

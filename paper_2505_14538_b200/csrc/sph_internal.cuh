@@ -85,6 +85,8 @@ struct DevState {
   int32_t* count;
   float4* fin;        // f, P, c, B
   float4* gq;         // c, u, m/rho, rho
+  float4* vc;         // v, c      (the gradient tile's j records: 16 + 16 + 8 bytes per pair)
+  float2* um;         // u, m/rho
   float* hlo;
   float* hhi;
   int32_t* iters;

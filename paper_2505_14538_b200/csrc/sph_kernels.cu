@@ -220,6 +220,10 @@ __device__ __forceinline__ void cp_async16(const void* smem_dst, const void* gme
   const unsigned int d = (unsigned int)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src));
 }
+__device__ __forceinline__ void cp_async8(const void* smem_dst, const void* gmem_src) {
+  const unsigned int d = (unsigned int)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gmem_src));
+}
 __device__ __forceinline__ void cp_async4(const void* smem_dst, const void* gmem_src) {
   const unsigned int d = (unsigned int)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(gmem_src));
@@ -231,6 +235,11 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 __device__ __forceinline__ float4 lds4(uint32_t a) {
   float4 v;
   asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float2 lds2(uint32_t a) {
+  float2 v;
+  asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
   return v;
 }
 __device__ __forceinline__ uint32_t smem_base(int rec) {
@@ -1215,6 +1224,10 @@ __global__ void __launch_bounds__(kDensT, 3) k_density(DevGrid g, DevPhys ph, De
 // Brookshaw Laplacian lap u_i = 2 sum_j (m_j/rho_j)(u_i - u_j) dW/dr / r (R16), gathered
 // over r_ij < H_i; the gradient ghost (alpha_v Eqs. 12-15, alpha_c Eqs. 21-24; R17-R21)
 // runs in the epilogue and writes the force-loop records.
+// the gradient tile's (u, m/rho) array, 16-byte aligned
+__host__ __device__ __forceinline__ size_t gradient_t2_bytes(const DevGrid& g) {
+  return (((size_t)(g.tcap + kNSent) * 8) + 15) & ~(size_t)15;
+}
 __global__ void __launch_bounds__(kGradT, 3) k_gradient(DevGrid g, DevPhys ph, DevState s,
                                                        const int* __restrict__ cell_start, float dt, int first_step,
                                                        DevCounters* __restrict__ ctr) {
@@ -1222,24 +1235,30 @@ __global__ void __launch_bounds__(kGradT, 3) k_gradient(DevGrid g, DevPhys ph, D
   __shared__ unsigned int s_hinv_max;  // largest 1/h of the tile (f32 bits)
   if (threadIdx.x == 0) { s_pairs = 0; s_hinv_max = 0u; }
   DESC_PROLOGUE();
-  // T0 = smem4[j]: x, y, z, h   T1 = smem4[O1 + j]: vx, vy, vz, 1/h (m_j is not used here)
-  // T2 = smem4[O2 + j]: c, u, m/rho, rho
-  const int O1 = SP, O2 = 2 * SP;
-  WalkArea<GradAcc> W = walk_area<GradAcc>(reinterpret_cast<char*>(smem4 + 3 * SP), g.icap);
+  // T0 = smem4[j]: x, y, z, 1/h   T1 = smem4[O1 + j]: vx, vy, vz, c (the density loop's vc record)
+  // T2 = float2 [j]: u, m/rho (um): a pair gathers 16 + 16 + 8 bytes
+  const int O1 = SP;
+  float2* T2 = reinterpret_cast<float2*>(smem4 + 2 * SP);
+  WalkArea<GradAcc> W = walk_area<GradAcc>(reinterpret_cast<char*>(T2) + gradient_t2_bytes(g), g.icap);
   walk_prefix_pre(g, W, T.ni);
   {
-    const float4* src[3] = {reinterpret_cast<const float4*>(s.xh), s.vm, s.gq};
-    const int o16[3] = {0, O1, O2};
-    stage_records<3>(S, nseg, src, o16, T.ntile);
+    // (the 8-byte records with cp.async, completed by the staging's wait + barrier)
+    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int k = threadIdx.x >> 5; k < nseg; k += nw) {
+      const int4 sg = S.seg[k];
+      for (int t = lane; t < sg.z; t += 32) cp_async8(T2 + sg.x + t, s.um + sg.y + t);
+    }
+    const float4* src[2] = {reinterpret_cast<const float4*>(s.xh), s.vc};
+    const int o16[2] = {0, O1};
+    stage_records<2>(S, nseg, src, o16, T.ntile);
   }
   {
     unsigned int hm = 0u;
     for (int t = threadIdx.x; t < T.ntile; t += blockDim.x) {
       const uint4 x = reinterpret_cast<const uint4*>(smem4)[t];
       const float3 p = rel_pos(g, T, x);
-      smem4[t] = make_float4(p.x, p.y, p.z, __uint_as_float(x.w));
       const float hinv = 1.f / __uint_as_float(x.w);
-      reinterpret_cast<float*>(smem4 + O1 + t)[3] = hinv;
+      smem4[t] = make_float4(p.x, p.y, p.z, hinv);
       hm = max(hm, __float_as_uint(hinv));
     }
     hm = (unsigned int)warp_max((int)hm);
@@ -1247,8 +1266,8 @@ __global__ void __launch_bounds__(kGradT, 3) k_gradient(DevGrid g, DevPhys ph, D
   }
   if (threadIdx.x < kNSent) {
     smem4[g.tcap + threadIdx.x] = make_float4(kFar, kFar, kFar, 1.f);
-    smem4[O1 + g.tcap + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 1.f);
-    smem4[O2 + g.tcap + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 1.f);
+    smem4[O1 + g.tcap + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
+    T2[g.tcap + threadIdx.x] = make_float2(0.f, 0.f);
   }
   const int ni = T.ni;
   for (int k = threadIdx.x; k < ni; k += blockDim.x) W.kl[k] = k;
@@ -1261,7 +1280,7 @@ __global__ void __launch_bounds__(kGradT, 3) k_gradient(DevGrid g, DevPhys ph, D
     double H2 = 0.0;
     int gi = 0;
     GradAcc a;
-    const uint32_t sb0 = smem_base(0), sb1 = smem_base(O1), sb2 = smem_base(O2);
+    const uint32_t sb0 = smem_base(0), sb1 = smem_base(O1), sb2 = smem_base(2 * SP);
     int ti_c = 0;  // tile slot of the walk's current particle (list_of -> begin)
     walk_lists(
         ni, W.pref, W.fin, W.head,
@@ -1273,21 +1292,21 @@ __global__ void __launch_bounds__(kGradT, 3) k_gradient(DevGrid g, DevPhys ph, D
           const int ti = ti_c;
           pi4 = smem4[ti];
           vi4 = smem4[O1 + ti];
-          const float4 gi4 = smem4[O2 + ti];
-          hinv = vi4.w;
+          hinv = pi4.w;
           qband = g.eabs * hinv + 8e-6f;
-          H2 = h2_exact(pi4.w, ph.gamma_k);
-          ci = gi4.x;
-          ui = gi4.y;
+          H2 = h2_exact(__uint_as_float(__ldg(&s.xh[gi].w)), ph.gamma_k);  // (the exact h: fp64 edge test)
+          ci = vi4.w;
+          ui = T2[ti].x;
           a = GradAcc{2.f * ci, 0.f, 0, 2.f * ci};
         },
         pair2_of([&](int j) {
           const uint32_t o = (uint32_t)j << 4;
           const float4 p = lds4(sb0 + o);
           const float4 vj = lds4(sb1 + o);
+          const float2 uj = lds2(sb2 + ((uint32_t)j << 3));
           grad_pair_sym(
-              a, pi4.x - p.x, pi4.y - p.y, pi4.z - p.z, hinv, vj.w, qband, sband, vi4, ci, ui, ph.beta, vj,
-              lds4(sb2 + o),
+              a, pi4.x - p.x, pi4.y - p.y, pi4.z - p.z, hinv, p.w, qband, sband, vi4, ci, ui, ph.beta, vj,
+              make_float4(vj.w, uj.x, uj.y, 0.f),
               [&]() {
                 return exact_neighbour(s.xh, gi, slot_global(S, nseg, j), H2, g.dscale[0], g.dscale[1], g.dscale[2]);
               },
@@ -1306,8 +1325,8 @@ __global__ void __launch_bounds__(kGradT, 3) k_gradient(DevGrid g, DevPhys ph, D
     int ti, gi;
     i_slot(S, k, ti, gi);
     if (s.wide && s.wide[gi]) continue;  // wide particles: k_wide_gradient, k_wide_force
-    const float4 gi4 = smem4[O2 + ti];
-    npairs += (unsigned long long)grad_epilogue(ph, s, a, gi, smem4[ti].w, gi4.x, gi4.y, gi4.w, dt, first_step);
+    npairs += (unsigned long long)grad_epilogue(ph, s, a, gi, __uint_as_float(s.xh[gi].w), smem4[O1 + ti].w,
+                                                T2[ti].x, s.gq[gi].w, dt, first_step);
     // the force loop's v_sig and N_force (symmetric set; a wide partner that did not list this
     // particle adds its pair in k_wide_force)
     s.vsig[gi] = a.vmaxs;
@@ -1685,7 +1704,7 @@ size_t density_smem(const DevGrid& g) {
   return (size_t)(g.tcap + kNSent) * (2 * 16) + walk_bytes<DenAcc>(g.icap, kDensT);
 }
 size_t gradient_smem(const DevGrid& g) {
-  return (size_t)(g.tcap + kNSent) * (3 * 16) + walk_bytes<GradAcc>(g.icap, kGradT);
+  return (size_t)(g.tcap + kNSent) * (2 * 16) + gradient_t2_bytes(g) + walk_bytes<GradAcc>(g.icap, kGradT);
 }
 size_t force_smem(const DevGrid& g) { return force_records_bytes(g.tcap) + (size_t)(g.icap + 1) * 8; }
 

@@ -133,6 +133,9 @@ __device__ __forceinline__ DenOut den_epilogue(const DevGrid& g, const DevPhys& 
     const float Bal = den > 0.f ? adiv / den : 0.f;
     s.fin[gi] = make_float4(f, P, cs, Bal);
     s.gq[gi] = make_float4(cs, u, mi / rho, rho);
+    const float4 vmi = s.vm[gi];
+    s.vc[gi] = make_float4(vmi.x, vmi.y, vmi.z, cs);
+    s.um[gi] = make_float2(u, mi / rho);
     s.active[gi] = 0;
     s.iters[gi] = conv ? it : -1;
     o.final_ = true;

@@ -122,7 +122,8 @@ typedef struct {
 
 typedef struct {
   int32_t iterations;      /* density passes run (1 = converged on the first pass)         */
-  int32_t unconverged;     /* particles not converged after the last pass                  */
+  int32_t unconverged;     /* particles not converged after the last pass (several ranks:   */
+                           /* the largest count of any rank)                                */
   int32_t rebuilds;        /* cell-grid rebuilds forced by growing h                       */
   float max_rel_resid;     /* max over the particles of |nhat h^3 - eta^3| / eta^3 at their  */
                            /* final h (the closure residual; <= h_tol when converged)  */

@@ -1570,9 +1570,11 @@ sph_status sph_density(sph_ctx* c, sph_density_stats* stats) {
     }
     c->launches += 1 + (c->s.n_wide > 0 ? 1 : 0);
     ++passes_run;
-    // every rank takes the same branch: the pass's flags (h_exceeds .. max_resid_bits, eight
-    // uint32 in DevCounters) are reduced over ranks on the device, then read back once
-    if ((st = allreduce_dev(c, &c->ctr->h_exceeds, 8, kMax)) != SPH_OK) return st;
+    // every rank takes the same branch: the pass's flags (unconverged .. max_resid_bits, nine
+    // uint32 in DevCounters) are reduced over ranks on the device (MAX), then read back once; the
+    // unconverged count is then the largest over ranks (no host allreduce after the pass loop, so
+    // the X2 exchange below overlaps the gradient loop's interior blocks)
+    if ((st = allreduce_dev(c, &c->ctr->unconverged, 9, kMax)) != SPH_OK) return st;
     if ((st = sync_ctr(c)) != SPH_OK) return st;
     double fl[4] = {(double)c->ctr_h->active_next, (double)c->ctr_h->h_exceeds, (double)c->ctr_h->list_stale,
                     c->ctr_h->nonfinite == 2 ? 1.0 : 0.0};
@@ -1611,8 +1613,7 @@ sph_status sph_density(sph_ctx* c, sph_density_stats* stats) {
     if ((st = halo_async(c, b, e, 4, c->ev_x2)) != SPH_OK) return st;
     c->x2_pending = true;
   }
-  double un = unconverged;
-  if ((st = allreduce(c, &un, 1, kMax)) != SPH_OK) return st;
+  const double un = unconverged;  // (already the maximum over ranks)
   c->counters.pairs_density = (int64_t)final_pairs;
   c->counters.pairs_h_iter = pairs_all;
   c->density_done = true;

@@ -330,6 +330,7 @@ struct sph_ctx {
   int n_int = 0, n_bnd = 0;
   int kz_hint = 0;              // KZ chosen at the last rebuild (first probe of the next)
   long long n_coinc = 0;        // directed coincident pairs of the owned particles (k_dup)
+  unsigned long long* pairs_grad_h = nullptr;  // pinned: the last gradient loop's directed pairs
   float wide_margin = 0.2f;     // adaptive grid: DevGrid::wide_margin (env SPH_WIDE_MARGIN overrides)
   int sparse_wide = 32;         // adaptive grid: blocks with fewer tile particles go wide (env SPH_SPARSE_WIDE; 0 = off)
   uint32_t* cperm = nullptr;    // wide search grid: particles in coarse-cell order
@@ -457,6 +458,8 @@ sph_status alloc_state(sph_ctx* c) {
   CK(dalloc(&c->keys, n)); CK(dalloc(&c->keys_alt, n)); CK(dalloc(&c->perm, n)); CK(dalloc(&c->perm_alt, n));
   CK(dalloc(&c->ctr, 1));
   CK(cudaMallocHost((void**)&c->ctr_h, sizeof(DevCounters)));
+  CK(cudaMallocHost((void**)&c->pairs_grad_h, sizeof(unsigned long long)));
+  *c->pairs_grad_h = 0;
   CK(dalloc(&c->scratch, 16));
   CK(cudaMallocHost((void**)&c->scratch_h, 16 * sizeof(unsigned int)));
   CK(dalloc(&c->cnt_dev, 8));
@@ -1668,7 +1671,9 @@ sph_status sph_gradient(sph_ctx* c, float dt) {
     CK(launch_wide_gradient(c->grid, c->phys, c->s, dt, first, c->ctr, c->stream));
   }
   c->launches += 1 + (c->s.n_wide > 0 ? 1 : 0);
-  CK(cudaMemcpyAsync(&c->counters.pairs_gradient, &c->ctr->pairs, 8, cudaMemcpyDeviceToHost, c->stream));
+  // (into pinned memory: a pageable destination would block the host until the loop ends;
+  // sph_get_counters synchronises and reads it)
+  CK(cudaMemcpyAsync(c->pairs_grad_h, &c->ctr->pairs, 8, cudaMemcpyDeviceToHost, c->stream));
   // ghosts need their owners' force-loop records (X3): on the communication stream, overlapping
   // the force loop's interior blocks
   if (c->slab) {
@@ -1824,6 +1829,7 @@ sph_status sph_get_counters(sph_ctx* c, sph_counters* out) {
   GUARD(c);
   if (!out) return SPH_ERR_INVALID_ARG;
   CK(cudaStreamSynchronize(c->stream));
+  c->counters.pairs_gradient = (int64_t)*c->pairs_grad_h;
   c->counters.coincident = c->n_coinc;  // directed pairs, skipped by the loops (k_dup)
   c->counters.kernel_launches = c->launches;
   c->counters.wide_particles = c->s.n_wide;
@@ -1891,6 +1897,7 @@ sph_status sph_destroy(sph_ctx* c) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->ctr_h) cudaFreeHost(c->ctr_h);
+  if (c->pairs_grad_h) cudaFreeHost(c->pairs_grad_h);
   if (c->scratch_h) cudaFreeHost(c->scratch_h);
   if (c->cnt_h) cudaFreeHost(c->cnt_h);
   for (const auto& t : c->tev) {

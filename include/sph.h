@@ -93,10 +93,12 @@ typedef struct {
   int32_t transport;      /* sph_transport, used when nranks > 1                            */
   const void* nccl_uid;   /* NCCL: 128-byte id from sph_nccl_unique_id on rank 0, same on all*/
   void* loopback;         /* LOOPBACK: group from sph_loopback_create (shared by the ranks)  */
-  int32_t adaptive_h;     /* one rank, strong h contrast: when the cells sized */
-                          /* from h_max overflow the tiles, size them from an h quantile and   */
-                          /* treat the particles whose support exceeds a cell as "wide"       */
-                          /* (global-index lists); default 1, 0 = fail instead */
+  int32_t adaptive_h;     /* strong h contrast: when the cells sized from      */
+                          /* h_max overflow the tiles, size them from an h quantile and treat  */
+                          /* the particles whose support exceeds a cell as "wide" (global-index*/
+                          /* lists); default 1, 0 = fail instead.  Slab path:   */
+                          /* the largest of the ranks' quantiles, and up to 16 ghost cell planes*/
+                          /* per side (more: SPH_ERR_H_EXCEEDS_CELL)                           */
   int32_t decomp[3];      /* ranks per axis of the domain decomposition;*/
                           /* {0,0,0} (default) = x-slabs {nranks, 1, 1}, the one implemented:   */
                           /* any other product of nranks is SPH_ERR_INVALID_ARG                */

@@ -35,6 +35,7 @@ namespace {
 
 constexpr int kLcapInit = 96;         // neighbour-list capacity per particle (entries, multiple of 8)
 constexpr size_t kSmemMax = 227 * 1024;
+constexpr int kMaxGhostPlanes = 16;     // slab path: ghost planes per side (wide particles)
 constexpr size_t kSmemTarget = 107 * 1024;  // two CTAs per SM for the largest (force) tile (+ static smem)
 
 __global__ void k_hmax(int n, const uint4* __restrict__ xh, unsigned int* out) {
@@ -42,6 +43,24 @@ __global__ void k_hmax(int n, const uint4* __restrict__ xh, unsigned int* out) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) m = max(m, xh[i].w);
   for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0) atomicMax(out, m);  // positive f32 order as u32
+}
+
+// ghost planes the owned particle needs (ghost_planes_needed) for a list radius Hfac h; a
+// particle that left the slab counts at its nearest owned plane
+__global__ void k_ghost_need(int n, const uint4* __restrict__ xh, DevGrid g, float Hfac, unsigned int* out) {
+  unsigned int m = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint4 x = xh[i];
+    long long d = (long long)(unsigned int)(x.x - g.x_lo);
+    if ((unsigned long long)d >= g.wfix + ((1ull << 32) - g.wfix) / 2) d -= (1ll << 32);
+    const long long q = d * (long long)g.nxo, w = (long long)g.wfix;
+    long long pl = q >= 0 ? q / w : -((-q + w - 1) / w);
+    pl = pl < 0 ? 0 : (pl >= g.nxo ? g.nxo - 1 : pl);
+    const int k = (int)ceilf(Hfac * __uint_as_float(x.w) / g.side_min);
+    m = max(m, (unsigned int)ghost_planes_needed(k, (int)pl, g.nxo));
+  }
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
 }
 
 // cell key of each particle in the local grid (DevGrid slab fields); a particle outside the
@@ -195,14 +214,14 @@ __global__ void k_plane_counts(int plane_cells, const int* __restrict__ cs, int 
 
 // final cell_start of the [ghost | owned | ghost] layout: owned planes shifted by gL, ghost
 // planes from the exclusive scans of the received per-cell counts
-__global__ void k_final_cs(int ncells, int plane_cells, int P, int gL, int n_own, const int* __restrict__ scanL,
+__global__ void k_final_cs(int ncells, int plane_cells, int G, int P, int gL, int n_own, const int* __restrict__ scanL,
                            const int* __restrict__ scanR, int n_loc, int* cs) {
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c > ncells) return;
   if (c == ncells) { cs[c] = n_loc; return; }
-  int plane = c / plane_cells, k = c - plane * plane_cells;
-  if (plane == 0) cs[c] = scanL[k];
-  else if (plane == P + 1) cs[c] = gL + n_own + scanR[k];
+  const int plane = c / plane_cells;
+  if (plane < G) cs[c] = scanL[c];                                          // left ghost planes
+  else if (plane >= G + P) cs[c] = gL + n_own + scanR[c - (G + P) * plane_cells];  // right ghost planes
   else cs[c] = cs[c] + gL;
 }
 
@@ -282,7 +301,8 @@ struct sph_ctx {
   bool slab = false;          // slab path (a transport was given; always when nranks > 1)
   Comm* comm = nullptr;
   bool ghost_v_stale = false;   // owners' v changed since the ghosts were received
-  int planeL = 0, planeR = 0;   // owned particles in the first / last owned plane (ghost sources)
+  int planeL = 0, planeR = 0;   // owned particles in the first / last G owned planes (ghost sources)
+  int gplanes = 1;              // G: ghost planes on each side of the slab
   bool poisoned = false;
   bool stale = true;          // grid must be rebuilt before the next loop
   bool lists_stale = true;    // neighbour lists must be rebuilt before the next loop
@@ -750,14 +770,15 @@ sph_status read_cs(sph_ctx* c, int cell, int* v) {
 // size the CTA tiles.
 sph_status rebuild_impl(sph_ctx* c);
 sph_status mark_wide(sph_ctx* c);
-sph_status h_quantile(sph_ctx* c, double q, float* out);
+sph_status h_quantile(sph_ctx* c, double q, float* out, bool global = true);
 
-// Cell grid for the current h.  One rank with adaptive_h: when cells sized from h_max do not
-// fit the tiles (strong h contrast), size them from decreasing quantiles of h instead; the
-// particles whose support exceeds a cell then become wide (sph_wide.cu).
+// Cell grid for the current h.  adaptive_h: when cells sized from h_max do not fit the tiles
+// (strong h contrast), size them from decreasing quantiles of h instead (on the slab path the
+// largest of the ranks' quantiles, so every rank takes the same grid); the particles whose
+// support exceeds a cell then become wide (sph_wide.cu).
 sph_status rebuild(sph_ctx* c) {
   Timed tm(c, SPH_T_REBUILD);
-  const bool adaptive = !c->slab && c->cfg.adaptive_h;
+  const bool adaptive = c->cfg.adaptive_h;
   sph_status st;
   if (adaptive && c->adapt_q > 0.0) {  // the quantile that worked last time, first
     float hq;
@@ -844,6 +865,7 @@ sph_status rebuild_impl(sph_ctx* c) {
   const double Hs = (double)c->cfg.gamma_k * hcell * (1.0 + c->cfg.cell_skin);
   DevGrid& g = c->grid;
   const int R = c->nranks;
+  int G = c->gplanes;  // ghost planes per side (slab path; more with wide particles, below)
   const bool slab = c->slab;
   // slab of this rank on the 2^-32 grid (fixed by position, independent of h)
   const double two32 = std::ldexp(1.0, 32);
@@ -857,8 +879,8 @@ sph_status rebuild_impl(sph_ctx* c) {
     // planes along x per slab (same on every rank), cells along y, z
     const double len = a == 0 ? c->cfg.box[0] * ((double)wmin / two32) : c->cfg.box[a];
     double k = std::floor(len / Hs);
-    // R nxo >= 3: the ghost planes are distinct from each other and from the owned ones
-    const double kmin = (a == 0 && slab) ? (double)((3 + R - 1) / R) : 3;
+    // (x planes of a slab: checked against the ghost planes below)
+    const double kmin = (a == 0 && slab) ? 1 : 3;
     if (k < kmin) {
       char b[256];
       snprintf(b, sizeof b, "support radius %.6g leaves fewer than %g cells along axis %d (length %.6g over %d ranks)",
@@ -867,26 +889,11 @@ sph_status rebuild_impl(sph_ctx* c) {
     }
     nc[a] = (int)std::min(k, 1024.0);
   }
-  auto ncells_of = [&]() { return (long long)(nc[0] + (slab ? 2 : 0)) * nc[1] * nc[2]; };
+  auto ncells_of = [&]() { return (long long)(nc[0] + (slab ? 2 * kMaxGhostPlanes : 0)) * nc[1] * nc[2]; };
   while (ncells_of() > (1LL << 30)) { for (int a = 0; a < 3; ++a) nc[a] = std::max(3, nc[a] / 2); }
   g.nxo = nc[0];
-  if (slab) {
-    g.nx = nc[0] + 2;
-    g.periodic_x = 0;
-    g.ix_first = 1;
-  } else {
-    g.nx = nc[0];
-    g.periodic_x = 1;
-    g.ix_first = 0;
-  }
   g.ny = nc[1];
   g.nz = nc[2];
-  g.ncells = g.nx * g.ny * g.nz;
-  {
-    int cbits = 1;
-    while ((1LL << cbits) <= g.ncells) ++cbits;
-    g.zbits = std::max(0, std::min(12, 32 - cbits));
-  }
   for (int a = 0; a < 3; ++a) {
     g.side[a] = (float)(c->cfg.box[a] / nc[a]);
     g.scale[a] = (float)(c->cfg.box[a] * std::ldexp(1.0, -32));
@@ -898,6 +905,53 @@ sph_status rebuild_impl(sph_ctx* c) {
     side_x_min = (float)(c->cfg.box[0] * ((double)wmin / two32) / nc[0]);           // thinnest planes of any slab
   }
   g.side_min = std::min(side_x_min, std::min(g.side[1], g.side[2]));
+  if (slab && c->h_side > 0.f) {
+    // wide particles on the slab path: G ghost planes per side such that every particle whose
+    // list radius (+25 % for its growth in the h iteration; k_wide_density asks for a rebuild
+    // past it) crosses a slab face lies within G planes of it, and its own search stays inside
+    // the local planes (ghost_planes_needed; the largest over the ranks)
+    CK(cudaMemsetAsync(c->scratch + 5, 0, 4, c->stream));
+    if (n > 0) {
+      k_ghost_need<<<std::min(nblk(n, 256), 1184), 256, 0, c->stream>>>(
+          n, c->s.xh + base, g, (1.f + c->cfg.cell_skin) * c->cfg.gamma_k * 1.25f, c->scratch + 5);
+      c->launches++;
+    }
+    CK(cudaGetLastError());
+    if ((st = allreduce_dev(c, c->scratch + 5, 1, kMax)) != SPH_OK) return st;
+    CK(cudaMemcpyAsync(c->scratch_h + 5, c->scratch + 5, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    G = std::max(G, (int)c->scratch_h[5]);
+    if (G > kMaxGhostPlanes) {
+      char b[256];
+      snprintf(b, sizeof b, "wide particles reach %d cell planes past their slab (at most %d ghost planes)", G,
+               kMaxGhostPlanes);
+      return fail(c, SPH_ERR_H_EXCEEDS_CELL, b);
+    }
+  }
+  if (slab) {
+    // the G ghost planes on each side are distinct from each other and, for R = 1, from the
+    // owned planes they image: nxo >= 2G + 1 (R = 1), 2G (R = 2), G (R >= 3)
+    const int kmin = R == 1 ? 2 * G + 1 : R == 2 ? 2 * G : G;
+    if (g.nxo < kmin) {
+      char b[256];
+      snprintf(b, sizeof b, "support radius %.6g leaves fewer than %d cells along axis 0 (length %.6g over %d ranks, "
+               "%d ghost planes)", Hs, kmin, c->cfg.box[0], R, G);
+      return fail(c, SPH_ERR_H_EXCEEDS_CELL, b);
+    }
+    g.nx = g.nxo + 2 * G;
+    g.periodic_x = 0;
+    g.ix_first = G;
+  } else {
+    g.nx = g.nxo;
+    g.periodic_x = 1;
+    g.ix_first = 0;
+  }
+  g.ncells = g.nx * g.ny * g.nz;
+  {
+    int cbits = 1;
+    while ((1LL << cbits) <= g.ncells) ++cbits;
+    g.zbits = std::max(0, std::min(12, 32 - cbits));
+  }
   g.zbucket = (float)(c->cfg.box[2] / nc[2] * std::ldexp(1.0, -g.zbits));
   if ((st = grow(c, &c->cell_start, c->cell_cap, (size_t)g.ncells + 1)) != SPH_OK) return st;
   const int pcells = g.ny * g.nz;
@@ -906,12 +960,13 @@ sph_status rebuild_impl(sph_ctx* c) {
   const Persist cur = offset(persist_of(c->s), base);
   if (slab) {
     // ---- migration (X6): particles now in a ghost plane belong to the neighbour
-    if ((st = agree(c, outside > 0, SPH_ERR_INVALID_ARG, "a particle moved more than one cell plane out of its slab")) != SPH_OK)
+    if ((st = agree(c, outside > 0, SPH_ERR_INVALID_ARG, "a particle moved more than G cell planes out of its slab")) !=
+        SPH_OK)
       return st;
     const int P = g.nxo;
     int c1, cP1;
-    if ((st = read_cs(c, pcells, &c1)) != SPH_OK) return st;             // first owned plane
-    if ((st = read_cs(c, (P + 1) * pcells, &cP1)) != SPH_OK) return st;  // right ghost plane
+    if ((st = read_cs(c, G * pcells, &c1)) != SPH_OK) return st;          // first owned plane
+    if ((st = read_cs(c, (G + P) * pcells, &cP1)) != SPH_OK) return st;  // first right ghost plane
     const long long nL = c1, nR = n - cP1, nmid = cP1 - c1;
     long long mL = 0, mR = 0;
     if ((st = exchange_sizes(c, nR, nL, mL, mR)) != SPH_OK) return st;
@@ -951,12 +1006,14 @@ sph_status rebuild_impl(sph_ctx* c) {
     if ((st = sort_cells(c, 0, n, &outside)) != SPH_OK) return st;
     if ((st = agree(c, outside > 0, SPH_ERR_INVALID_ARG, "migrated particle outside its slab")) != SPH_OK) return st;
     // ---- ghost planes (X1): sizes and per-cell counts first
+    // (the owned planes are [G, G + P); the ghost sources are the first and the last G of them)
+    const int gpc = G * pcells;
     int cP;
-    if ((st = read_cs(c, P * pcells, &cP)) != SPH_OK) return st;  // start of the last owned plane
+    if ((st = read_cs(c, P * pcells, &cP)) != SPH_OK) return st;  // start of the last G owned planes
     int c2;
-    if ((st = read_cs(c, 2 * pcells, &c2)) != SPH_OK) return st;  // end of the first owned plane
-    c->planeL = c2;        // first owned plane: [0, c2) of the sorted owned set
-    c->planeR = n - cP;    // last owned plane: [cP, n)
+    if ((st = read_cs(c, 2 * gpc, &c2)) != SPH_OK) return st;  // end of the first G owned planes
+    c->planeL = c2;        // first G owned planes: [0, c2) of the sorted owned set
+    c->planeR = n - cP;    // last G owned planes: [cP, n)
     long long gL = 0, gR = 0;
     if ((st = exchange_sizes(c, c->planeR, c->planeL, gL, gR)) != SPH_OK) return st;
     if ((st = agree(c, gL + n + gR > c->cap, SPH_ERR_OOM, "owned + ghost particles exceed the context capacity")) !=
@@ -964,8 +1021,14 @@ sph_status rebuild_impl(sph_ctx* c) {
       return st;
     c->gL = (int)gL;
     c->gR = (int)gR;
+    g.gL = c->gL;
+    g.n_own = n;
+    g.x_loL = (unsigned int)slab_lo((c->rank + R - 1) % R);
+    g.wfixL = slab_lo((c->rank + R - 1) % R + 1) - slab_lo((c->rank + R - 1) % R);
+    g.x_loR = (unsigned int)slab_lo((c->rank + 1) % R);
+    g.wfixR = slab_lo((c->rank + 1) % R + 1) - slab_lo((c->rank + 1) % R);
     const size_t pc_old = c->pc_cap;
-    if ((st = grow(c, &c->pc_send, c->pc_cap, (size_t)4 * pcells + 64)) != SPH_OK) return st;
+    if ((st = grow(c, &c->pc_send, c->pc_cap, (size_t)4 * gpc + 64)) != SPH_OK) return st;
     if (!c->pc_recv || c->pc_cap != pc_old) {  // (same capacity as pc_send)
       if (c->pc_recv) cudaFree(c->pc_recv);
       if (c->pc_scan) cudaFree(c->pc_scan);
@@ -973,33 +1036,33 @@ sph_status rebuild_impl(sph_ctx* c) {
       CK(dalloc(&c->pc_recv, c->pc_cap));
       CK(dalloc(&c->pc_scan, c->pc_cap));
     }
-    k_plane_counts<<<nblk(pcells, 256), 256, 0, c->stream>>>(pcells, c->cell_start, P * pcells, c->pc_send);
-    k_plane_counts<<<nblk(pcells, 256), 256, 0, c->stream>>>(pcells, c->cell_start, pcells, c->pc_send + pcells);
+    k_plane_counts<<<nblk(gpc, 256), 256, 0, c->stream>>>(gpc, c->cell_start, P * pcells, c->pc_send);
+    k_plane_counts<<<nblk(gpc, 256), 256, 0, c->stream>>>(gpc, c->cell_start, gpc, c->pc_send + gpc);
     c->launches += 2;
     CK(cudaGetLastError());
     {
-      Xfer s2[2] = {{right_of(c), c->pc_send, (size_t)pcells * 4}, {left_of(c), c->pc_send + pcells, (size_t)pcells * 4}};
-      Xfer r2[2] = {{left_of(c), c->pc_recv, (size_t)pcells * 4}, {right_of(c), c->pc_recv + pcells, (size_t)pcells * 4}};
+      Xfer s2[2] = {{right_of(c), c->pc_send, (size_t)gpc * 4}, {left_of(c), c->pc_send + gpc, (size_t)gpc * 4}};
+      Xfer r2[2] = {{left_of(c), c->pc_recv, (size_t)gpc * 4}, {right_of(c), c->pc_recv + gpc, (size_t)gpc * 4}};
       CKC(c->comm->exchange(s2, 2, r2, 2, c->stream));
     }
     size_t need = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, need, c->pc_recv, c->pc_scan, pcells, c->stream);
+    cub::DeviceScan::ExclusiveSum(nullptr, need, c->pc_recv, c->pc_scan, gpc, c->stream);
     if (need > c->scan_tmp_bytes) {
       if (c->scan_tmp) cudaFree(c->scan_tmp);
       c->scan_tmp = nullptr;
       CK(cudaMalloc(&c->scan_tmp, need));
       c->scan_tmp_bytes = need;
     }
-    CK(cub::DeviceScan::ExclusiveSum(c->scan_tmp, need, c->pc_recv, c->pc_scan, pcells, c->stream));
-    CK(cub::DeviceScan::ExclusiveSum(c->scan_tmp, need, c->pc_recv + pcells, c->pc_scan + pcells, pcells, c->stream));
+    CK(cub::DeviceScan::ExclusiveSum(c->scan_tmp, need, c->pc_recv, c->pc_scan, gpc, c->stream));
+    CK(cub::DeviceScan::ExclusiveSum(c->scan_tmp, need, c->pc_recv + gpc, c->pc_scan + gpc, gpc, c->stream));
     c->launches += 2;
     // owned particles into their final place, then the ghost payload straight into the ghost slots
     if (n > 0) {
       k_permute<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->perm_alt, persist_of(c->s), offset(c->alt, c->gL));
       c->launches++;
     }
-    k_final_cs<<<nblk(g.ncells + 1, 256), 256, 0, c->stream>>>(g.ncells, pcells, P, c->gL, n, c->pc_scan,
-                                                               c->pc_scan + pcells, c->gL + n + c->gR, c->cell_start);
+    k_final_cs<<<nblk(g.ncells + 1, 256), 256, 0, c->stream>>>(g.ncells, pcells, G, P, c->gL, n, c->pc_scan,
+                                                               c->pc_scan + gpc, c->gL + n + c->gR, c->cell_start);
     c->launches++;
     CK(cudaGetLastError());
     swap_persist(c);
@@ -1008,6 +1071,8 @@ sph_status rebuild_impl(sph_ctx* c) {
     c->ghost_v_stale = false;
   } else {
     if (outside) return fail(c, SPH_ERR_INVALID_ARG, "internal: particle outside the periodic grid");
+    g.gL = 0;
+    g.n_own = n;
     if (n > 0) {
       k_permute<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->perm_alt, cur, c->alt);
       c->launches++;
@@ -1211,91 +1276,122 @@ __global__ void k_h_keys(int n, const uint4* __restrict__ xh, unsigned int* keys
   if (i < n) keys[i] = xh[i].w;  // positive f32: ordered as unsigned
 }
 
-// q-quantile of the owned particles' h (device radix sort of the f32 bits)
-sph_status h_quantile(sph_ctx* c, double q, float* out) {
+// q-quantile of the owned particles' h (device radix sort of the f32 bits).  global (slab
+// path): the largest of the ranks' quantiles (a collective: every rank calls it)
+sph_status h_quantile(sph_ctx* c, double q, float* out, bool global) {
   const int n = c->n_own;
-  if (n <= 0) return fail(c, SPH_ERR_INVALID_ARG, "no particles");
-  k_h_keys<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->s.xh + c->gL, c->keys);
-  c->launches++;
-  CK(cudaGetLastError());
-  size_t tmp = c->sort_tmp_bytes;
-  CK(cub::DeviceRadixSort::SortKeys(c->sort_tmp, tmp, c->keys, c->keys_alt, n, 0, 32, c->stream));
-  const int k = std::min(n - 1, std::max(0, (int)(q * (n - 1))));
-  CK(cudaMemcpyAsync(c->scratch_h + 9, c->keys_alt + k, 4, cudaMemcpyDeviceToHost, c->stream));
+  global = global && c->slab;
+  if (n <= 0 && !global) return fail(c, SPH_ERR_INVALID_ARG, "no particles");
+  CK(cudaMemsetAsync(c->scratch + 9, 0, 4, c->stream));
+  if (n > 0) {
+    k_h_keys<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->s.xh + c->gL, c->keys);
+    c->launches++;
+    CK(cudaGetLastError());
+    size_t tmp = c->sort_tmp_bytes;
+    CK(cub::DeviceRadixSort::SortKeys(c->sort_tmp, tmp, c->keys, c->keys_alt, n, 0, 32, c->stream));
+    const int k = std::min(n - 1, std::max(0, (int)(q * (n - 1))));
+    CK(cudaMemcpyAsync(c->scratch + 9, c->keys_alt + k, 4, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  sph_status st;
+  if (global && (st = allreduce_dev(c, c->scratch + 9, 1, kMax)) != SPH_OK) return st;
+  CK(cudaMemcpyAsync(c->scratch_h + 9, c->scratch + 9, 4, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   std::memcpy(out, c->scratch_h + 9, 4);
+  if (!(*out > 0.f)) return fail(c, SPH_ERR_INVALID_ARG, "no particles");
   return SPH_OK;
 }
+
+// a wide ghost (index outside the owned range [lo, hi))
+struct GhostFlag {
+  const uint8_t* w;
+  int lo, hi;
+  __host__ __device__ bool operator()(int i) const { return w[i] != 0 && (i < lo || i >= hi); }
+};
 
 // Flag and list the wide particles of the current grid (none unless the side was sized from
 // an h quantile).
 sph_status mark_wide(sph_ctx* c) {
   DevState& s = c->s;
-  s.n_wide = 0;
+  s.n_wide = s.n_wide_own = 0;
   s.wide = nullptr;
   c->grid.nrun = c->grid.nact;
   c->grid.run_list = nullptr;
-  if (c->h_side <= 0.f || c->slab) return SPH_OK;
+  if (c->h_side <= 0.f) return SPH_OK;
   const int n = c->n_own;
+  // slab path: the ghosts are flagged too (a ghost whose support reaches an owned particle beyond
+  // the neighbouring cells evaluates that pair here, k_wide_force)
+  const int n_loc = c->gL + n + c->gR;
   if (!c->wide_flag) {
     CK(dalloc(&c->wide_flag, (size_t)c->cap));
     CK(dalloc(&c->widx, (size_t)c->cap));
     CK(dalloc(&c->wcount, (size_t)c->cap));
-    CK(dalloc(&c->n_wide_dev, 1));
+    CK(dalloc(&c->n_wide_dev, 2));
   }
-  // wide: support past the cell side, or within wide_margin of it (the margin is dropped when it
-  // would add more than 10 % to the wide set, e.g. a uniform region whose h sits at the threshold)
-  int nw = 0;
-  for (float margin : {c->wide_margin, 0.f}) {
-    c->grid.wide_margin = margin;
-    CK(cudaMemsetAsync(c->scratch + 15, 0, 4, c->stream));
-    CK(launch_mark_wide(n, c->grid, c->phys, s, c->wide_flag, c->scratch + 15, c->stream));
-    c->launches++;
-    thrust::counting_iterator<int> it(0);
-    size_t need = 0;
-    CK(cub::DeviceSelect::Flagged(nullptr, need, it, c->wide_flag, c->widx, c->n_wide_dev, n, c->stream));
+  // widx: the owned wide particles (ascending), then the ghost ones
+  int nw = 0, nw_own = 0;
+  auto select = [&]() -> sph_status {
+    thrust::counting_iterator<int> it(c->gL);
+    thrust::counting_iterator<int> it0(0);
+    const GhostFlag gf{c->wide_flag, c->gL, c->gL + n};
+    size_t need = 0, need2 = 0;
+    CK(cub::DeviceSelect::Flagged(nullptr, need, it, c->wide_flag + c->gL, c->widx, c->n_wide_dev, n, c->stream));
+    if (n_loc > n)
+      CK(cub::DeviceSelect::If(nullptr, need2, it0, c->widx, c->n_wide_dev + 1, n_loc, gf, c->stream));
+    need = std::max(need, need2);
     if (need > c->sel_tmp_bytes) {
       if (c->sel_tmp) cudaFree(c->sel_tmp);
       c->sel_tmp = nullptr;
       CK(cudaMalloc(&c->sel_tmp, need));
       c->sel_tmp_bytes = need;
     }
-    CK(cub::DeviceSelect::Flagged(c->sel_tmp, need, it, c->wide_flag, c->widx, c->n_wide_dev, n, c->stream));
+    CK(cub::DeviceSelect::Flagged(c->sel_tmp, need, it, c->wide_flag + c->gL, c->widx, c->n_wide_dev, n, c->stream));
     c->launches++;
     CK(cudaMemcpyAsync(c->scratch_h + 10, c->n_wide_dev, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    std::memcpy(&nw_own, c->scratch_h + 10, 4);
+    nw = nw_own;
+    if (n_loc > n) {
+      CK(cub::DeviceSelect::If(c->sel_tmp, need, it0, c->widx + nw_own, c->n_wide_dev + 1, n_loc, gf, c->stream));
+      c->launches++;
+      CK(cudaMemcpyAsync(c->scratch_h + 10, c->n_wide_dev + 1, 4, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      int ng;
+      std::memcpy(&ng, c->scratch_h + 10, 4);
+      nw += ng;
+    }
+    return SPH_OK;
+  };
+  // wide: support past the cell side, or within wide_margin of it (the margin is dropped when it
+  // would add more than 10 % to the wide set, e.g. a uniform region whose h sits at the threshold)
+  sph_status sq;
+  for (float margin : {c->wide_margin, 0.f}) {
+    c->grid.wide_margin = margin;
+    CK(cudaMemsetAsync(c->scratch + 15, 0, 4, c->stream));
+    CK(launch_mark_wide(n_loc, c->grid, c->phys, s, c->wide_flag, c->scratch + 15, c->stream));
+    c->launches++;
+    if ((sq = select()) != SPH_OK) return sq;
     CK(cudaMemcpyAsync(c->scratch_h + 15, c->scratch + 15, 4, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    std::memcpy(&nw, c->scratch_h + 10, 4);
     const int n0 = (int)c->scratch_h[15];
     if (margin == 0.f || nw <= n0 + n0 / 10 + 1024) break;
   }
   // sparse blocks' tile particles are handled as wide too (k_sparse_wide)
   if (c->sparse_wide > 0 && nw > 0) {
     CK(launch_sparse_wide(c->grid, c->wide_flag, s.ncount, c->sparse_wide, c->stream));
-    thrust::counting_iterator<int> it(0);
-    size_t need = 0;
-    CK(cub::DeviceSelect::Flagged(nullptr, need, it, c->wide_flag, c->widx, c->n_wide_dev, n, c->stream));
-    if (need > c->sel_tmp_bytes) {
-      if (c->sel_tmp) cudaFree(c->sel_tmp);
-      c->sel_tmp = nullptr;
-      CK(cudaMalloc(&c->sel_tmp, need));
-      c->sel_tmp_bytes = need;
-    }
-    CK(cub::DeviceSelect::Flagged(c->sel_tmp, need, it, c->wide_flag, c->widx, c->n_wide_dev, n, c->stream));
-    c->launches += 2;
-    CK(cudaMemcpyAsync(c->scratch_h + 10, c->n_wide_dev, 4, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    std::memcpy(&nw, c->scratch_h + 10, 4);
+    c->launches++;
+    if ((sq = select()) != SPH_OK) return sq;
   }
   s.n_wide = nw;
+  s.n_wide_own = nw_own;
   s.wide = c->wide_flag;
   if (nw > 0) {
     // the wide particles' search grid (sph_wide.cu): coarse cells of F^3 grid cells, F such
-    // that a particle at the 99th percentile of h reaches about two coarse cells
+    // that a particle at the 99th percentile of h reaches about two coarse cells (this rank's
+    // quantile: not a collective, the ranks' wide sets differ); all local particles, ghosts too
     DevGrid& g = c->grid;
-    float hq;
-    sph_status sq;
-    if ((sq = h_quantile(c, 0.99, &hq)) != SPH_OK) return sq;
+    float hq = 0.f;
+    if (n > 0 && (sq = h_quantile(c, 0.99, &hq, false)) != SPH_OK) return sq;
+    if (!(hq > 0.f)) hq = c->h_side;
     const float R = (1.f + c->cfg.cell_skin) * c->cfg.gamma_k * hq;
     const float side = std::min(g.side[0], std::min(g.side[1], g.side[2]));
     const int F = std::max(1, std::min(64, (int)std::ceil(R / (2.f * side))));
@@ -1304,17 +1400,17 @@ sph_status mark_wide(sph_ctx* c) {
     s.cny = (g.ny + F - 1) / F;
     s.cnz = (g.nz + F - 1) / F;
     const long long ncc = (long long)s.cnx * s.cny * s.cnz;
-    if ((sq = grow_h(c, &c->cperm, c->cperm_cap, (size_t)std::max(n, 1))) != SPH_OK) return sq;
+    if ((sq = grow_h(c, &c->cperm, c->cperm_cap, (size_t)std::max(n_loc, 1))) != SPH_OK) return sq;
     if ((sq = grow_h(c, &c->ccs, c->ccs_cap, (size_t)ncc + 1)) != SPH_OK) return sq;
-    CK(launch_coarse_keys(n, 0, g, s, c->keys, c->perm, c->stream));
+    CK(launch_coarse_keys(n_loc, 0, g, s, c->keys, c->perm, c->stream));
     c->launches++;
     int bits = 1;
     while ((1LL << bits) <= ncc) ++bits;
     size_t tmp = c->sort_tmp_bytes;
-    CK(cub::DeviceRadixSort::SortPairs(c->sort_tmp, tmp, c->keys, c->keys_alt, c->perm, c->cperm, n, 0, bits,
+    CK(cub::DeviceRadixSort::SortPairs(c->sort_tmp, tmp, c->keys, c->keys_alt, c->perm, c->cperm, n_loc, 0, bits,
                                        c->stream));
     c->launches++;
-    k_cell_start<<<nblk(n + 1, 256), 256, 0, c->stream>>>(n, (int)ncc, 0, c->keys_alt, c->ccs);
+    k_cell_start<<<nblk(n_loc + 1, 256), 256, 0, c->stream>>>(n_loc, (int)ncc, 0, c->keys_alt, c->ccs);
     c->launches++;
     CK(cudaGetLastError());
     s.cperm = c->cperm;
@@ -1375,8 +1471,9 @@ sph_status build_lists(sph_ctx* c) {
     c->launches += 2 + (c->s.n_wide > 0 ? 1 : 0);
     sph_status st = sync_ctr(c);
     if (st != SPH_OK) return st;
-    if (c->ctr_h->wlist_overflow > 0) {  // wide lists (one rank): grow and rebuild
-      c->wlcap = ((int)(c->ctr_h->wlist_overflow * 1.25) + 31) & ~31;
+    const int wover = c->ctr_h->wlist_overflow;
+    if (wover > 0) {  // wide lists: grow this rank's capacity (the retry below is collective)
+      c->wlcap = ((int)(wover * 1.25) + 31) & ~31;
       c->s.wlcap = c->wlcap;
       const size_t want = (size_t)std::max(c->s.n_wide, 1) * c->wlcap;
       if (want > c->wnbr_cap) {
@@ -1386,16 +1483,16 @@ sph_status build_lists(sph_ctx* c) {
         c->wnbr_cap = want;
       }
       c->s.wnbr = c->wnbr;
-      continue;
     }
     double over = c->ctr_h->list_overflow, bad = c->ctr_h->nonfinite == 2 ? 1 : 0;
-    double v[2] = {over, bad};
-    if ((st = allreduce(c, v, 2, kMax)) != SPH_OK) return st;
+    double v[3] = {over, bad, (double)wover};
+    if ((st = allreduce(c, v, 3, kMax)) != SPH_OK) return st;
     if (v[1] > 0) return fail(c, SPH_ERR_CUDA, "internal: tile larger than its capacity");
-    if (v[0] == 0) {
+    if (v[0] == 0 && v[2] == 0) {
       c->lists_stale = false;
       return SPH_OK;
     }
+    if (v[0] == 0) continue;  // (a wide list overflowed on some rank)
     int need = ((int)(v[0] * 1.25) + 7) & ~7;
     if (need > 8192) return fail(c, SPH_ERR_H_EXCEEDS_CELL, "neighbour list longer than 8192 entries");
     c->lcap = need;
@@ -1486,9 +1583,14 @@ sph_status sph_create(const sph_config* cfg, const sph_particles_in* in, sph_ctx
   if (!c->slab) {
     c->cap = c->n_in;
   } else {
+    // SPH_GHOST_PLANES: more than one ghost plane per side (a test hook for the G-plane layout)
+    if (const char* e = getenv("SPH_GHOST_PLANES")) c->gplanes = std::max(1, std::min(kMaxGhostPlanes, atoi(e)));
     const double per = (double)cfg->n_total / c->nranks;
     const double plane = std::pow((double)cfg->n_total, 2.0 / 3.0);
-    c->cap = (int)std::min<double>(0x3fffffff, 1.5 * std::max<double>(per, c->n_in) + 6.0 * plane + 65536);
+    // ghosts: ~3 particle layers per cell plane; adaptive_h may need up to kMaxGhostPlanes per side
+    const double gmax = cfg->adaptive_h ? kMaxGhostPlanes : c->gplanes;
+    c->cap = (int)std::min<double>(0x3fffffff, 1.5 * std::max<double>(per, c->n_in) +
+                                                   (4.0 + 3.0 * 2.0 * gmax) * plane + 65536);
   }
   auto bail = [&](sph_status s) { sph_destroy(c); return s; };
   if (cudaSetDevice(c->device) != cudaSuccess) return bail(SPH_ERR_CUDA);

@@ -57,12 +57,29 @@ struct DevGrid {
   // Slab decomposition along x.  The rank owns x in [x_lo, x_lo + wfix) on the 2^-32 grid,
   // cut into nxo planes; local plane of x = ix_first + floor((x - x_lo) nxo / wfix).
   // One rank: x_lo = 0, wfix = 2^32, ix_first = 0, nxo = nx, periodic.  Several ranks:
-  // local planes = [ghost, nxo owned, ghost] (nx = nxo + 2), not periodic along x.
-  unsigned long long wfix;
-  unsigned int x_lo;
+  // local planes = [G ghost, nxo owned, G ghost] (nx = nxo + 2G, ix_first = G), not periodic
+  // along x.  The left / right neighbours' slabs (x_loL, wfixL / x_loR, wfixR) place the
+  // ghosts, local indices [0, gL) and [gL + n_own, ...), on their owners' planes.
+  unsigned long long wfix, wfixL, wfixR;
+  unsigned int x_lo, x_loL, x_loR;
   int periodic_x;
   int ix_first, nxo;
+  int gL, n_own;
 };
+
+// Slab path, wide particles: ghost planes per side needed by an owned particle whose search
+// reaches k planes (list radius / side, rounded up) from owned plane pl of nxo.  Its search
+// [pl - k, pl + k] must stay inside the local planes (G >= k - distance to the nearer face),
+// and when it crosses a face the neighbour must hold it as a ghost (G > its distance to that
+// face, in whole planes), so that every pair with an owned particle has its evaluator on the
+// owner's rank.
+__host__ __device__ inline int ghost_planes_needed(int k, int pl, int nxo) {
+  const int dl = pl, dr = nxo - 1 - pl;
+  int need = k - (dl < dr ? dl : dr);
+  if (k > dl && dl + 1 > need) need = dl + 1;
+  if (k > dr && dr + 1 > need) need = dr + 1;
+  return need > 1 ? need : 1;
+}
 
 struct DevPhys {
   float gamma_k, eta3, h_tol, pi_eta3;
@@ -119,6 +136,7 @@ struct DevState {
   uint32_t* wnbr;     // [n_wide][wlcap] neighbour lists, global indices
   int32_t* wcount;    // [n_wide] list lengths
   int n_wide, wlcap;
+  int n_wide_own;     // widx[0, n_wide_own): the owned ones (then the slab path's ghosts)
   // the wide particles' search grid: coarse cells of cF^3 grid cells (cnx x cny x cnz, the
   // last along an axis possibly thinner), particles sorted by coarse cell (cperm), ranges ccs
   const uint32_t* cperm;  // [n_own] particle indices in coarse-cell order

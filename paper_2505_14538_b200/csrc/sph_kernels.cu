@@ -1643,14 +1643,15 @@ __global__ void k_block_run(DevGrid g, DevState s, uint8_t* flag) {
 
 // Slab decomposition: which active blocks have a tile inside the owned planes (interior: no
 // ghost particle in the tile, so the loop can run before the halo arrives) and which touch a
-// ghost plane (boundary).  Tile x-planes are [ix0 - 1, ix0 + bx]; the ghost planes are 0 and nx - 1.
+// ghost plane (boundary).  Tile x-planes are [ix0 - 1, ix0 + bx]; the owned planes are
+// [ix_first, ix_first + nxo).
 __global__ void k_block_side(DevGrid g, uint8_t* interior, uint8_t* boundary) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= g.nact) return;
   int jx, jy, zb;
   block_coords(g, g.blk_list[a], jx, jy, zb);
   const int ix0 = g.ix_first + jx * g.bx;
-  const bool in = g.periodic_x || (ix0 - 1 > 0 && ix0 + g.bx < g.nx - 1);
+  const bool in = g.periodic_x || (ix0 - 1 >= g.ix_first && ix0 + g.bx < g.ix_first + g.nxo);
   interior[a] = in ? 1 : 0;
   boundary[a] = in ? 0 : 1;
 }

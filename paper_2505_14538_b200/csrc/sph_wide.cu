@@ -31,17 +31,35 @@ constexpr unsigned kFull = 0xffffffffu;
 
 __device__ __forceinline__ int cell_axis(uint32_t x, int n) { return (int)(((unsigned long long)x * (unsigned)n) >> 32); }
 
+// local x-plane of particle i: the plane its rank's binning put it in.  One rank: the periodic
+// grid.  Slab path: owned particles on this slab's planes [G, G + nxo) (k_keys); the ghosts
+// on their OWNER's planes (its last G planes -> [0, G), its first G -> [G + nxo, nx)), so the
+// plane agrees with the ghost cell the particle was received into
+__device__ __forceinline__ int plane_of(const DevGrid& g, int i, uint32_t x) {
+  if (g.periodic_x) return cell_axis(x, g.nx);
+  uint32_t lo = g.x_lo;
+  unsigned long long w = g.wfix;
+  int base = g.ix_first;
+  if (i < g.gL) { lo = g.x_loL; w = g.wfixL; base = g.ix_first - g.nxo; }
+  else if (i >= g.gL + g.n_own) { lo = g.x_loR; w = g.wfixR; base = g.ix_first + g.nxo; }
+  const unsigned long long d = (unsigned long long)(uint32_t)(x - lo);
+  const int p = (int)min((d * (unsigned long long)g.nxo) / w, (unsigned long long)(g.nxo - 1));
+  return min(max(base + p, 0), g.nx - 1);
+}
+
 // search half-width in cells along each axis for a list radius R (capped to the whole axis)
 __device__ __forceinline__ int reach(float R, float side, int n) {
   const int k = (int)ceilf(R / side);
   return min(k, (n - 1) / 2 + 1);
 }
 
-// cells i and j are within +-k of each other along an axis of n cells (periodic)
-__device__ __forceinline__ bool within(int a, int b, int k, int n) {
-  if (2 * k + 1 >= n) return true;
+// cells i and j are within +-k of each other along an axis of n cells (periodic, or not: the
+// slab path's local x planes)
+__device__ __forceinline__ bool within(int a, int b, int k, int n, bool per = true) {
   int d = a - b;
   d = d < 0 ? -d : d;
+  if (!per) return d <= k;
+  if (2 * k + 1 >= n) return true;
   d = min(d, n - d);
   return d <= k;
 }
@@ -51,15 +69,22 @@ __device__ __forceinline__ bool within(int a, int b, int k, int n) {
 // list radius R lists candidates from every coarse cell that meets the grid-cell box
 // +-reach(R) around its own cell -- a superset of its sphere -- and the force kernel decides
 // "did the wide j list i" with the same predicate (coarse_meets).
-__device__ __forceinline__ bool coarse_meets(int ci, int a, int k, int n, int F) {
-  if (2 * k + 1 >= n) return true;  // (the whole axis)
+__device__ __forceinline__ bool coarse_meets(int ci, int a, int k, int n, int F, bool per = true) {
   const int f0 = ci * F, w = min(F, n - f0);
+  if (!per) return f0 <= a + 2 * k && f0 + w - 1 >= a;  // (non-periodic: the range clipped to the axis)
+  if (2 * k + 1 >= n) return true;  // (the whole axis)
   const int d0 = ((f0 - a) % n + n) % n;  // start of the coarse cell, from a (mod n)
   return d0 <= 2 * k || d0 + w > n;
 }
 // coarse cells meeting the grid-cell range [a, a + 2k] (mod n): c0 (the one holding a) and
 // the cnt that follow it cyclically
-__device__ __forceinline__ void coarse_range(int a, int k, int n, int F, int cn, int& c0, int& cnt) {
+__device__ __forceinline__ void coarse_range(int a, int k, int n, int F, int cn, int& c0, int& cnt, bool per = true) {
+  if (!per) {  // [a, a + 2k] clipped to [0, n)
+    const int lo = max(a, 0), hi = min(a + 2 * k, n - 1);
+    c0 = lo / F;
+    cnt = hi >= lo ? hi / F - c0 + 1 : 0;
+    return;
+  }
   const int am = ((a % n) + n) % n;
   c0 = (2 * k + 1 >= n) ? 0 : am / F;
   cnt = 0;
@@ -75,7 +100,7 @@ __global__ void k_coarse_keys(int n, DevGrid g, DevState s, unsigned int* keys, 
   if (i >= n) return;
   const uint4 x = s.xh[i];
   const int F = s.cF;
-  const unsigned int ccx = (unsigned)(cell_axis(x.x, g.nx) / F), ccy = (unsigned)(cell_axis(x.y, g.ny) / F),
+  const unsigned int ccx = (unsigned)(plane_of(g, i, x.x) / F), ccy = (unsigned)(cell_axis(x.y, g.ny) / F),
                      ccz = (unsigned)(cell_axis(x.z, g.nz) / F);
   keys[i] = (ccx * (unsigned)s.cny + ccy) * (unsigned)s.cnz + ccz;
   vals[i] = (unsigned)i;
@@ -110,12 +135,13 @@ __global__ void __launch_bounds__(256) k_wide_lists(DevGrid g, DevPhys ph, DevSt
   const float Hfac = (1.f + g.skin) * ph.gamma_k;
   const float hi = __uint_as_float(xi.w);
   const float Hi2 = (Hfac * hi) * (Hfac * hi);
-  const int cx = cell_axis(xi.x, g.nx), cy = cell_axis(xi.y, g.ny), cz = cell_axis(xi.z, g.nz);
-  const int kx = reach(Hfac * hi, g.side[0], g.nx), ky = reach(Hfac * hi, g.side[1], g.ny),
-            kz = reach(Hfac * hi, g.side[2], g.nz);
+  const bool px = g.periodic_x;
+  const int cx = plane_of(g, i, xi.x), cy = cell_axis(xi.y, g.ny), cz = cell_axis(xi.z, g.nz);
+  const int kx = px ? reach(Hfac * hi, g.side[0], g.nx) : (int)ceilf(Hfac * hi / g.side[0]),
+            ky = reach(Hfac * hi, g.side[1], g.ny), kz = reach(Hfac * hi, g.side[2], g.nz);
   const int F = s.cF;
   int x0, nxc, y0, nyc, z0, nzc;  // coarse cells meeting the grid-cell box, per axis
-  coarse_range(cx - kx, kx, g.nx, F, s.cnx, x0, nxc);
+  coarse_range(cx - kx, kx, g.nx, F, s.cnx, x0, nxc, px);
   coarse_range(cy - ky, ky, g.ny, F, s.cny, y0, nyc);
   coarse_range(cz - kz, kz, g.nz, F, s.cnz, z0, nzc);
   const int run1 = min(nzc, s.cnz - z0);  // the z range as at most two contiguous runs
@@ -192,7 +218,7 @@ __device__ __forceinline__ float warp_fmax(float v) {
 __global__ void __launch_bounds__(256) k_wide_density(DevGrid g, DevPhys ph, DevState s, int pass, float hfac_stale,
                                                       DevCounters* __restrict__ ctr) {
   const int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (wi >= s.n_wide) return;
+  if (wi >= s.n_wide_own) return;  // (ghosts: their owner iterates them)
   const int i = s.widx[wi];
   if (pass > 0 && !s.active[i]) return;  // warp-uniform
   const uint4 xi = s.xh[i];
@@ -220,12 +246,18 @@ __global__ void __launch_bounds__(256) k_wide_density(DevGrid g, DevPhys ph, Dev
   if (o.give_up) atomicAdd(&ctr->unconverged, 1);
   if (o.active) atomicAdd(&ctr->active_next, 1);
   if (o.stale) atomicExch(&ctr->list_stale, 1);
+  // slab path: the new list radius must still fit the G ghost planes (ghost_planes_needed);
+  // past them the grid is rebuilt with a larger G
+  if (!g.periodic_x && o.active &&
+      ghost_planes_needed((int)ceilf((1.f + g.skin) * ph.gamma_k * o.hn / g.side_min),
+                          plane_of(g, i, xi.x) - g.ix_first, g.nxo) > g.ix_first)
+    atomicExch(&ctr->h_exceeds, 1);
 }
 
 __global__ void __launch_bounds__(256) k_wide_gradient(DevGrid g, DevPhys ph, DevState s, float dt, int first_step,
                                                        DevCounters* __restrict__ ctr) {
   const int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (wi >= s.n_wide) return;
+  if (wi >= s.n_wide_own) return;  // (ghosts: the X3 exchange brings their records)
   const int i = s.widx[wi];
   const uint4 xi = s.xh[i];
   const float4 vi = s.vm[i];
@@ -295,7 +327,10 @@ __global__ void __launch_bounds__(256) k_wide_force(DevGrid g, DevPhys ph, DevSt
   const ForceSide I = side_of(s, i, h);
   const double Hi2 = h2_exact(h, ph.gamma_k);
   const float Hfac = (1.f + g.skin) * ph.gamma_k;
-  const int cxi = cell_axis(xi.x, g.nx), cyi = cell_axis(xi.y, g.ny), czi = cell_axis(xi.z, g.nz);
+  const bool px = g.periodic_x;
+  const int cxi = plane_of(g, i, xi.x), cyi = cell_axis(xi.y, g.ny), czi = cell_axis(xi.z, g.nz);
+  // a ghost i (slab path) evaluates its pairs for the owned partners only; its own side is its owner's
+  const bool iown = wi < s.n_wide_own;
   const uint32_t* lst = s.wnbr + (size_t)wi * s.wlcap;
   const int n = s.wcount[wi];
   float4 ai = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -322,25 +357,27 @@ __global__ void __launch_bounds__(256) k_wide_force(DevGrid g, DevPhys ph, DevSt
     vmax = fmaxf(vmax, in ? vs : 0.f);
     // did j list i?  tile particles list the cells within +-1 of their own, wide ones the
     // cells within their list radius at build time (k_wide_lists)
-    const int cxj = cell_axis(xj.x, g.nx), cyj = cell_axis(xj.y, g.ny), czj = cell_axis(xj.z, g.nz);
+    const int cxj = plane_of(g, j, xj.x), cyj = cell_axis(xj.y, g.ny), czj = cell_axis(xj.z, g.nz);
     const bool jwide = s.wide[j] != 0;
     const float Rj = Hfac * s.hbuild[j];
     bool seen;
     if (jwide) {  // j's search: the coarse cells meeting its grid-cell box (k_wide_lists)
-      const int kx = reach(Rj, g.side[0], g.nx), ky = reach(Rj, g.side[1], g.ny), kz = reach(Rj, g.side[2], g.nz);
+      const int kx = px ? reach(Rj, g.side[0], g.nx) : (int)ceilf(Rj / g.side[0]), ky = reach(Rj, g.side[1], g.ny),
+                kz = reach(Rj, g.side[2], g.nz);
       const int F = s.cF;
-      seen = coarse_meets(cxi / F, cxj - kx, kx, g.nx, F) && coarse_meets(cyi / F, cyj - ky, ky, g.ny, F) &&
+      seen = coarse_meets(cxi / F, cxj - kx, kx, g.nx, F, px) && coarse_meets(cyi / F, cyj - ky, ky, g.ny, F) &&
              coarse_meets(czi / F, czj - kz, kz, g.nz, F);
     } else {
-      seen = within(cxi, cxj, 1, g.nx) && within(cyi, cyj, 1, g.ny) && within(czi, czj, 1, g.nz);
+      seen = within(cxi, cxj, 1, g.nx, px) && within(cyi, cyj, 1, g.ny) && within(czi, czj, 1, g.nz);
     }
+    const bool jown = px || (j >= g.gL && j < g.gL + g.n_own);
     if (j != i && (!jwide || !seen || i < j)) {
       float4 jo;
       force_pair2(ai, jo, d.x, d.y, d.z, I, J, ph.beta);
       red_add4_w(s.acc + j, jo);
     }
     // v_sig and N_force of a partner that listed i already hold the pair (gradient loop)
-    if (j != i && in && !seen) {
+    if (j != i && in && !seen && jown) {
       atomicMax(reinterpret_cast<int*>(&s.vsig[j]), __float_as_int(vs));
       atomicAdd(&s.countf[j], 1);
       dt_candidate(ph, ctr, hj, vs);
@@ -352,7 +389,7 @@ __global__ void __launch_bounds__(256) k_wide_force(DevGrid g, DevPhys ph, DevSt
   ai.w = warp_sum(ai.w);
   vmax = warp_fmax(vmax);
   nn = warp_isum(nn);
-  if (lane != 0) return;
+  if (lane != 0 || !iown) return;
   red_add4_w(s.acc + i, ai);
   atomicMax(reinterpret_cast<int*>(&s.vsig[i]), __float_as_int(vmax));
   atomicAdd(&s.countf[i], nn - 1);  // (the self pair)

@@ -15,8 +15,8 @@ import pytest
 
 import workloads as W
 from multirank_util import run_ranks
-from parity_util import (RTOL, assert_close, assert_counts_in_band, du_tolerance, gpu_hydro, oracle_count_band,
-                         oracle_hydro)
+from parity_util import (RTOL, assert_close, assert_counts_in_band, du_tolerance, dv_tolerance, gpu_hydro,
+                         lap_tolerance, oracle_count_band, oracle_hydro, oracle_sampled)
 
 pytestmark = pytest.mark.gpu
 
@@ -88,6 +88,78 @@ def test_multirank_matches_single_gpu(case, R):
     fo = o["force"]
     for run in (g, one):
         assert_close("a", run["a"][sample], fo["a"][sample], atol_scale=fo["scale_a"][sample])
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_multirank_more_ghost_planes(G, monkeypatch):
+    """The [G ghost | owned | G ghost] plane layout (the one wide particles need)
+    holds the same neighbours as G = 1: results identical to the single-context run."""
+    monkeypatch.setenv("SPH_GHOST_PLANES", str(G))
+    p = _switches(W.jittered_lattice(40, seed=64, vel_sigma=0.2, u_sigma=0.4), 4)
+    one = gpu_hydro(p, dt_ghost=1e-3, fixed_h=True)
+    g, parts = run_ranks(p, 3, _hydro(1e-3), h_max_iter=0)
+    assert np.array_equal(g["count"], one["count"])
+    assert np.array_equal(g["count_force"], one["count_force"])
+    for k in ("rho", "P", "v_sig_grad", "v_sig"):
+        assert_close(k, g[k], one[k], rtol=2e-5)
+    assert sum(q["counters"]["pairs_force"] for q in parts) == int(one["count_force"].sum())
+    # accelerations (sums with cancellation): both runs against the oracle where they differ most
+    diff = np.abs(g["a"] - one["a"]).max(1)
+    sample = np.unique(np.argsort(diff)[-48:])
+    fo = oracle_hydro(p, dt_ghost=1e-3, fixed_h=True, sample=sample)["force"]
+    for run in (g, one):
+        assert_close("a", run["a"][sample], fo["a"][sample], atol_scale=fo["scale_a"][sample])
+
+
+@pytest.mark.parametrize("R", [2, 3, 4])
+def test_multirank_adaptive_sedov(R):
+    """C3-like Sedov blast on the slab path: the adaptive grid with wide particles on every rank
+    (DESIGN.md §9, §11).  The blast centre's wide particles reach several cell planes into the
+    neighbouring slabs (G ghost planes per side).
+      (a) fixed h: the same neighbour sets as the single-context run (counts exact, floats to
+          f32 summation order);
+      (b) the h iteration: a sample (random, the largest h, the particles nearest the slab faces)
+          against the oracle's own root, at the single-GPU parity bars."""
+    p = _switches(W.sedov(64), 8)
+    n = p["X"].shape[0]
+    one = gpu_hydro(p, dt_ghost=1e-3, fixed_h=True)
+    g, parts = run_ranks(p, R, _hydro(1e-3), h_max_iter=0)
+    wide = [q["counters"]["wide_particles"] for q in parts]
+    assert min(wide) > 0 and one["counters"]["wide_particles"] > 0
+    assert np.array_equal(g["count"], one["count"])
+    assert np.array_equal(g["count_force"], one["count_force"])
+    for k in ("rho", "P", "c", "f", "v_sig_grad", "v_sig"):
+        assert_close(k, g[k], one[k], rtol=2e-5)
+    assert sum(q["counters"]["pairs_force"] for q in parts) == int(one["count_force"].sum())
+    assert {q["dt"] for q in parts} == {parts[0]["dt"]}
+    # (b)
+    g, parts = run_ranks(p, R, _hydro(1e-3), h_tol=1e-6)
+    assert all(q["stats"]["unconverged"] == 0 for q in parts)
+    x = p["X"][:, 0].astype(np.float64) / 2.0 ** 32
+    face = np.min(np.abs(((x[:, None] - np.arange(R)[None, :] / R) + 0.5) % 1.0 - 0.5), axis=1)
+    rng = np.random.default_rng(R)
+    s = np.unique(np.concatenate([rng.choice(n, 400, replace=False), np.argsort(g["h"])[-48:],
+                                  np.argsort(face)[:96]]))
+    cs = 2.0 * float(np.percentile(p["h"], 75))
+    o = oracle_sampled(p, s, dt_ghost=1e-3, cell_side=cs)
+    d, fin, gr, fo = o["density"], o["finalize"], o["gradient"], o["force"]
+    s2 = o["sets"][2]
+    hroot = p["h"].astype(np.float64).copy()
+    hroot[s2] = d["h"][s2]
+    dlo, dhi, flo, fhi = oracle_count_band(p, hroot, dt_ghost=1e-3, sample=s, hop_radius=o["hop_radius"],
+                                           cell_side=cs)
+    assert_counts_in_band("count", g["count"], dlo, dhi, idx=s)
+    assert_counts_in_band("count_force", g["count_force"], flo, fhi, idx=s)
+    assert_close("h", g["h"][s], d["h"][s], rtol=1e-5)
+    assert_close("rho", g["rho"][s], d["rho"][s], rtol=RTOL)
+    assert_close("P", g["P"][s], fin["P"][s], rtol=RTOL)
+    assert_close("div", g["div"][s], d["div"][s], atol_scale=dv_tolerance(d)[s])
+    assert_close("v_sig_grad", g["v_sig_grad"][s], gr["v_sig"][s], rtol=RTOL)
+    assert_close("lap_u", g["lap_u"][s], gr["lap_u"][s], atol_scale=lap_tolerance(gr)[s])
+    assert_close("v_sig", g["v_sig"][s], fo["v_sig"][s], rtol=RTOL)
+    assert_close("a", g["a"][s], fo["a"][s], atol_scale=fo["scale_a"][s])
+    sc_u, at_u = du_tolerance(fo)
+    assert_close("du", g["du"][s], fo["du"][s], atol_scale=sc_u[s], atol=at_u[s])
 
 
 def _kdk(steps, log):

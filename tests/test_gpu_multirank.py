@@ -177,7 +177,7 @@ def _kdk(steps, log):
             ctx.kick_drift(0.5 * dt, 0.0)
             dt = dt_new
             log.append(ctx.n)
-        return {"n0": n0, "id0": id0, "dt": dt}
+        return {"n0": n0, "id0": id0, "dt": dt, "counters": ctx.counters()}
 
     return prog
 
@@ -248,3 +248,31 @@ def test_single_rank_slab_path(transport):
     for run in (got, one):
         assert_close("a", run["a"][sample], fo["a"][sample], atol_scale=fo["scale_a"][sample])
     assert abs(dt - one["dt"]) <= 1e-6 * one["dt"]
+
+
+def test_multirank_kdk_sedov_wide():
+    """KDK steps of the C3-like Sedov blast on three ranks: migration, rebuilds with G ghost
+    planes and wide particles on every rank.  Momentum: cross-rank pairs are evaluated on both
+    ranks (each keeps its own side) from tile coordinates, so the two sides agree to f32
+    rounding, not bitwise (DESIGN.md §9): |Delta P| <= 1e-6 sum m |v| per step (north star);
+    the trajectories track the single-context run to f32 rounding growth."""
+    from paper_2505_14538_b200 import Context
+
+    p = _switches(W.sedov(48), 11)
+    m = p["m"].astype(np.float64)
+    steps = 3
+    g, parts = run_ranks(p, 3, _kdk(steps, []), h_tol=1e-5)
+    assert min(q["counters"]["wide_particles"] for q in parts) > 0
+    ctx = Context(p, h_tol=1e-5)
+    ref = _kdk(steps, [])(ctx)
+    X1, rho1, v1 = ctx.get("X"), ctx.get("rho"), ctx.get("v")
+    ctx.close()
+    v0 = p["v"].astype(np.float64)
+    pscale = float((m * (np.linalg.norm(v0, axis=1) + np.linalg.norm(g["v"].astype(np.float64), axis=1))).sum())
+    dP = np.abs((m[:, None] * (g["v"].astype(np.float64) - v0)).sum(0)).max()
+    assert dP <= 1e-6 * pscale * steps, (dP, pscale)
+    dX = (g["X"].astype(np.int64) - X1.astype(np.int64) + 2 ** 31) % 2 ** 32 - 2 ** 31
+    assert np.abs(dX).max() < 2 ** 32 * 1e-6, "positions drifted apart"
+    assert_close("rho", g["rho"], rho1, rtol=1e-4)
+    assert_close("v", g["v"], v1, rtol=1e-4, atol_scale=np.full(len(rho1), 1e-2))
+    assert abs(parts[0]["dt"] - ref["dt"]) <= 1e-4 * ref["dt"]

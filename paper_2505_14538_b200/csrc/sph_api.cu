@@ -1346,7 +1346,9 @@ sph_status mark_wide(sph_ctx* c) {
     }
     CK(cub::DeviceSelect::Flagged(c->sel_tmp, need, it, c->wide_flag + c->gL, c->widx, c->n_wide_dev, n, c->stream));
     c->launches++;
+    // (with the population counter n0 in the same read-back)
     CK(cudaMemcpyAsync(c->scratch_h + 10, c->n_wide_dev, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(c->scratch_h + 15, c->scratch + 15, 4, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     std::memcpy(&nw_own, c->scratch_h + 10, 4);
     nw = nw_own;
@@ -1370,8 +1372,6 @@ sph_status mark_wide(sph_ctx* c) {
     CK(launch_mark_wide(n_loc, c->grid, c->phys, s, c->wide_flag, c->scratch + 15, c->stream));
     c->launches++;
     if ((sq = select()) != SPH_OK) return sq;
-    CK(cudaMemcpyAsync(c->scratch_h + 15, c->scratch + 15, 4, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
     const int n0 = (int)c->scratch_h[15];
     if (margin == 0.f || nw <= n0 + n0 / 10 + 1024) break;
   }

@@ -35,8 +35,11 @@ __device__ __forceinline__ int cell_axis(uint32_t x, int n) { return (int)(((uns
 // grid.  Slab path: owned particles on this slab's planes [G, G + nxo) (k_keys); the ghosts
 // on their OWNER's planes (its last G planes -> [0, G), its first G -> [G + nxo, nx)), so the
 // plane agrees with the ghost cell the particle was received into
+// (PX: the grid is periodic along x, one rank; the kernels are instantiated for both cases so
+// the single-rank build keeps its registers)
+template <bool PX>
 __device__ __forceinline__ int plane_of(const DevGrid& g, int i, uint32_t x) {
-  if (g.periodic_x) return cell_axis(x, g.nx);
+  if (PX) return cell_axis(x, g.nx);
   uint32_t lo = g.x_lo;
   unsigned long long w = g.wfix;
   int base = g.ix_first;
@@ -95,12 +98,13 @@ __device__ __forceinline__ void coarse_range(int a, int k, int n, int F, int cn,
   }
 }
 
+template <bool PX>
 __global__ void k_coarse_keys(int n, DevGrid g, DevState s, unsigned int* keys, unsigned int* vals) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint4 x = s.xh[i];
   const int F = s.cF;
-  const unsigned int ccx = (unsigned)(plane_of(g, i, x.x) / F), ccy = (unsigned)(cell_axis(x.y, g.ny) / F),
+  const unsigned int ccx = (unsigned)(plane_of<PX>(g, i, x.x) / F), ccy = (unsigned)(cell_axis(x.y, g.ny) / F),
                      ccz = (unsigned)(cell_axis(x.z, g.nz) / F);
   keys[i] = (ccx * (unsigned)s.cny + ccy) * (unsigned)s.cnz + ccz;
   vals[i] = (unsigned)i;
@@ -125,6 +129,7 @@ __global__ void k_mark_wide(int n, DevGrid g, DevPhys ph, DevState s, uint8_t* f
 
 // One warp per wide particle.  Overflow of wlcap: the count is still returned (max in
 // ctr->list_overflow) and the host rebuilds with a larger capacity.
+template <bool PX>
 __global__ void __launch_bounds__(256) k_wide_lists(DevGrid g, DevPhys ph, DevState s, const int* __restrict__ cell_start,
                                                     DevCounters* __restrict__ ctr) {
   const int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -135,8 +140,8 @@ __global__ void __launch_bounds__(256) k_wide_lists(DevGrid g, DevPhys ph, DevSt
   const float Hfac = (1.f + g.skin) * ph.gamma_k;
   const float hi = __uint_as_float(xi.w);
   const float Hi2 = (Hfac * hi) * (Hfac * hi);
-  const bool px = g.periodic_x;
-  const int cx = plane_of(g, i, xi.x), cy = cell_axis(xi.y, g.ny), cz = cell_axis(xi.z, g.nz);
+  constexpr bool px = PX;
+  const int cx = plane_of<PX>(g, i, xi.x), cy = cell_axis(xi.y, g.ny), cz = cell_axis(xi.z, g.nz);
   const int kx = px ? reach(Hfac * hi, g.side[0], g.nx) : (int)ceilf(Hfac * hi / g.side[0]),
             ky = reach(Hfac * hi, g.side[1], g.ny), kz = reach(Hfac * hi, g.side[2], g.nz);
   const int F = s.cF;
@@ -250,7 +255,7 @@ __global__ void __launch_bounds__(256) k_wide_density(DevGrid g, DevPhys ph, Dev
   // past them the grid is rebuilt with a larger G
   if (!g.periodic_x && o.active &&
       ghost_planes_needed((int)ceilf((1.f + g.skin) * ph.gamma_k * o.hn / g.side_min),
-                          plane_of(g, i, xi.x) - g.ix_first, g.nxo) > g.ix_first)
+                          plane_of<false>(g, i, xi.x) - g.ix_first, g.nxo) > g.ix_first)
     atomicExch(&ctr->h_exceeds, 1);
 }
 
@@ -318,6 +323,7 @@ __device__ __forceinline__ void red_add4_w(float4* p, const float4& v) {
 // one that did not list i leaves it to i.  i's side is reduced over the warp (lane order), j's
 // goes to acc[j] with one vector reduction.  v_sig and N_force: i's over its list; a partner
 // that did not list i gets its share of the pair here (atomics), with its CFL candidate.
+template <bool PX>
 __global__ void __launch_bounds__(256) k_wide_force(DevGrid g, DevPhys ph, DevState s, DevCounters* __restrict__ ctr) {
   const int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (wi >= s.n_wide) return;
@@ -327,10 +333,10 @@ __global__ void __launch_bounds__(256) k_wide_force(DevGrid g, DevPhys ph, DevSt
   const ForceSide I = side_of(s, i, h);
   const double Hi2 = h2_exact(h, ph.gamma_k);
   const float Hfac = (1.f + g.skin) * ph.gamma_k;
-  const bool px = g.periodic_x;
-  const int cxi = plane_of(g, i, xi.x), cyi = cell_axis(xi.y, g.ny), czi = cell_axis(xi.z, g.nz);
+  constexpr bool px = PX;
+  const int cxi = plane_of<PX>(g, i, xi.x), cyi = cell_axis(xi.y, g.ny), czi = cell_axis(xi.z, g.nz);
   // a ghost i (slab path) evaluates its pairs for the owned partners only; its own side is its owner's
-  const bool iown = wi < s.n_wide_own;
+  const bool iown = PX || wi < s.n_wide_own;
   const uint32_t* lst = s.wnbr + (size_t)wi * s.wlcap;
   const int n = s.wcount[wi];
   float4 ai = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -357,7 +363,7 @@ __global__ void __launch_bounds__(256) k_wide_force(DevGrid g, DevPhys ph, DevSt
     vmax = fmaxf(vmax, in ? vs : 0.f);
     // did j list i?  tile particles list the cells within +-1 of their own, wide ones the
     // cells within their list radius at build time (k_wide_lists)
-    const int cxj = plane_of(g, j, xj.x), cyj = cell_axis(xj.y, g.ny), czj = cell_axis(xj.z, g.nz);
+    const int cxj = plane_of<PX>(g, j, xj.x), cyj = cell_axis(xj.y, g.ny), czj = cell_axis(xj.z, g.nz);
     const bool jwide = s.wide[j] != 0;
     const float Rj = Hfac * s.hbuild[j];
     bool seen;
@@ -411,14 +417,16 @@ cudaError_t launch_coarse_keys(int n, int i0, const DevGrid& g, const DevState& 
                                unsigned int* vals, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   (void)i0;
-  k_coarse_keys<<<(n + 255) / 256, 256, 0, st>>>(n, g, s, keys, vals);
+  if (g.periodic_x) k_coarse_keys<true><<<(n + 255) / 256, 256, 0, st>>>(n, g, s, keys, vals);
+  else k_coarse_keys<false><<<(n + 255) / 256, 256, 0, st>>>(n, g, s, keys, vals);
   return cudaGetLastError();
 }
 
 cudaError_t launch_wide_lists(const DevGrid& g, const DevPhys& ph, const DevState& s, const int* cell_start,
                               DevCounters* ctr, cudaStream_t st) {
   if (s.n_wide <= 0) return cudaSuccess;
-  k_wide_lists<<<(s.n_wide * 32 + 255) / 256, 256, 0, st>>>(g, ph, s, cell_start, ctr);
+  if (g.periodic_x) k_wide_lists<true><<<(s.n_wide * 32 + 255) / 256, 256, 0, st>>>(g, ph, s, cell_start, ctr);
+  else k_wide_lists<false><<<(s.n_wide * 32 + 255) / 256, 256, 0, st>>>(g, ph, s, cell_start, ctr);
   return cudaGetLastError();
 }
 
@@ -440,7 +448,8 @@ cudaError_t launch_wide_force(const DevGrid& g, const DevPhys& ph, const DevStat
                               cudaStream_t st) {
   if (s.n_wide <= 0) return cudaSuccess;
   k_wide_zero<<<(s.n_wide + 255) / 256, 256, 0, st>>>(s);
-  k_wide_force<<<(s.n_wide * 32 + 255) / 256, 256, 0, st>>>(g, ph, s, ctr);
+  if (g.periodic_x) k_wide_force<true><<<(s.n_wide * 32 + 255) / 256, 256, 0, st>>>(g, ph, s, ctr);
+  else k_wide_force<false><<<(s.n_wide * 32 + 255) / 256, 256, 0, st>>>(g, ph, s, ctr);
   return cudaGetLastError();
 }
 

@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsph.so")
+# (SPH_LIB names another in-tree build of the same library: A/B timing of kernel variants)
+LIB_PATH = os.environ.get("SPH_LIB") or os.path.join(_HERE, "libsph.so")
 
 SPH_OK, SPH_ERR_INVALID_ARG, SPH_ERR_CUDA, SPH_ERR_NCCL, SPH_ERR_OOM = 0, 1, 2, 3, 4
 SPH_ERR_NOT_CONVERGED, SPH_ERR_H_EXCEEDS_CELL, SPH_ERR_NUMERIC, SPH_ERR_STATE = 5, 6, 7, 8
@@ -48,7 +49,7 @@ class Config(ctypes.Structure):
                 ("stream", ctypes.c_void_p), ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
                 ("tile_cells_z", ctypes.c_int32), ("predict_h", ctypes.c_int32), ("transport", ctypes.c_int32),
                 ("nccl_uid", ctypes.c_void_p), ("loopback", ctypes.c_void_p), ("adaptive_h", ctypes.c_int32),
-                ("decomp", ctypes.c_int32 * 3)]
+                ("decomp", ctypes.c_int32 * 3), ("halo_put", ctypes.c_int32)]
 
 SPH_TRANSPORT_NCCL, SPH_TRANSPORT_LOOPBACK = 0, 1
 

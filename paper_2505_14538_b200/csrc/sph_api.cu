@@ -343,6 +343,11 @@ struct sph_ctx {
   // run on the context stream; its boundary blocks wait for the exchange
   cudaStream_t cstream = nullptr;
   cudaEvent_t ev_main = nullptr, ev_x2 = nullptr, ev_x3 = nullptr;
+  // halo put (sph_config.halo_put): the neighbours' fr1 / fr2 buffers mapped into this process
+  // ([0] left, [1] right), so the gradient epilogue stores X3's ghost records there itself
+  bool halo_put = false;
+  float4* peer_fr1[2] = {nullptr, nullptr};
+  float4* peer_fr2[2] = {nullptr, nullptr};
   bool x2_pending = false, x3_pending = false;
   uint8_t* side_flag = nullptr;  // [2 nact]: interior, boundary flags
   int* side_list = nullptr;      // [2 nact]: interior active indices at 0, boundary ones at nact
@@ -1021,6 +1026,21 @@ sph_status rebuild_impl(sph_ctx* c) {
       return st;
     c->gL = (int)gL;
     c->gR = (int)gR;
+    if (c->halo_put) {
+      // halo put targets: the first G owned planes go to the left neighbour's right ghosts (at
+      // its gL + n_own, which it sends us), the last G to the right neighbour's left ghosts (at 0)
+      long long dstL = 0, unused = 0;
+      if ((st = exchange_sizes(c, (long long)c->gL + n, 0, dstL, unused)) != SPH_OK) return st;
+      DevState& ds = c->s;
+      ds.put_fr1[0] = c->peer_fr1[0] + dstL;
+      ds.put_fr2[0] = c->peer_fr2[0] + dstL;
+      ds.put_lo[0] = c->gL;
+      ds.put_hi[0] = c->gL + c->planeL;
+      ds.put_fr1[1] = c->peer_fr1[1];
+      ds.put_fr2[1] = c->peer_fr2[1];
+      ds.put_lo[1] = c->gL + n - c->planeR;
+      ds.put_hi[1] = c->gL + n;
+    }
     g.gL = c->gL;
     g.n_own = n;
     g.x_loL = (unsigned int)slab_lo((c->rank + R - 1) % R);
@@ -1545,6 +1565,7 @@ void sph_config_default(sph_config* cfg) {
   cfg->loopback = nullptr;
   cfg->adaptive_h = 1;
   cfg->decomp[0] = cfg->decomp[1] = cfg->decomp[2] = 0;
+  cfg->halo_put = -1;
 }
 
 sph_status sph_nccl_unique_id(void* out128) {
@@ -1619,6 +1640,24 @@ sph_status sph_create(const sph_config* cfg, const sph_particles_in* in, sph_ctx
   if (const char* m = getenv("SPH_WIDE_MARGIN")) c->wide_margin = (float)std::max(0.0, atof(m));
   if (const char* m = getenv("SPH_SPARSE_WIDE")) c->sparse_wide = std::max(0, atoi(m));
   if ((st = alloc_state(c)) != SPH_OK) return bail(st);
+  if (c->slab) {
+    c->halo_put = cfg->halo_put == 1 ||
+                  (cfg->halo_put < 0 && (cfg->transport == SPH_TRANSPORT_LOOPBACK || c->nranks == 1));
+    if (c->halo_put) {
+      void* p[4];
+      std::string e = c->comm->map_peer(c->s.fr1, left_of(c), right_of(c), &p[0], &p[1], c->stream);
+      if (e.empty()) e = c->comm->map_peer(c->s.fr2, left_of(c), right_of(c), &p[2], &p[3], c->stream);
+      if (!e.empty()) {
+        fail(c, SPH_ERR_NCCL, "halo put: " + e);
+        fprintf(stderr, "sph_create: %s\n", c->err.c_str());
+        return bail(SPH_ERR_NCCL);
+      }
+      for (int d = 0; d < 2; ++d) {
+        c->peer_fr1[d] = static_cast<float4*>(p[d]);
+        c->peer_fr2[d] = static_cast<float4*>(p[2 + d]);
+      }
+    }
+  }
   if ((st = ingest(c, in)) != SPH_OK) return bail(st);
   if ((st = rebuild(c)) != SPH_OK) {
     fprintf(stderr, "sph_create: %s\n", c->err.c_str());
@@ -1779,9 +1818,21 @@ sph_status sph_gradient(sph_ctx* c, float dt) {
   // ghosts need their owners' force-loop records (X3): on the communication stream, overlapping
   // the force loop's interior blocks
   if (c->slab) {
-    void* const b[2] = {c->s.fr1, c->s.fr2};
-    const size_t e[2] = {sizeof(float4), sizeof(float4)};
-    if ((st = halo_async(c, b, e, 2, c->ev_x3)) != SPH_OK) return st;
+    if (c->halo_put) {
+      // the gradient epilogues stored the ghost records in the neighbours' buffers already: a
+      // zero-payload token (8 bytes each way) orders the neighbours' boundary force blocks after
+      // this rank's gradient kernels, and theirs before ours
+      CK(cudaEventRecord(c->ev_main, c->stream));
+      CK(cudaStreamWaitEvent(c->cstream, c->ev_main, 0));
+      Xfer ts[2] = {{right_of(c), c->cnt_dev + 4, 8}, {left_of(c), c->cnt_dev + 5, 8}};
+      Xfer tr[2] = {{left_of(c), c->cnt_dev + 6, 8}, {right_of(c), c->cnt_dev + 7, 8}};
+      CKC(c->comm->exchange(ts, 2, tr, 2, c->cstream));
+      CK(cudaEventRecord(c->ev_x3, c->cstream));
+    } else {
+      void* const b[2] = {c->s.fr1, c->s.fr2};
+      const size_t e[2] = {sizeof(float4), sizeof(float4)};
+      if ((st = halo_async(c, b, e, 2, c->ev_x3)) != SPH_OK) return st;
+    }
     c->x3_pending = true;
   }
   c->dprev_valid = true;

@@ -65,6 +65,7 @@ class NcclComm : public Comm {
  public:
   NcclComm(int rank, int n) : rank_(rank), n_(n) {}
   ~NcclComm() override {
+    for (auto& kv : opened_) cudaIpcCloseMemHandle(kv.second);
     if (scratch_) cudaFree(scratch_);
     if (comm_) g_nccl.CommDestroy(comm_);
   }
@@ -105,11 +106,52 @@ class NcclComm : public Comm {
     ncclResult_t e = g_nccl.AllReduce(d, d, n, ncclUint32, o, comm_, st);
     return e == ncclSuccess ? "" : std::string("ncclAllReduce: ") + g_nccl.GetErrorString(e);
   }
+  // IPC handles through the scratch buffer (sent to both neighbours, theirs received), then
+  // opened once per (peer, handle) with lazy peer access (NVLink P2P on an NVSwitch node).
+  std::string map_peer(void* mine, int left, int right, void** left_out, void** right_out,
+                       cudaStream_t st) override {
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, mine) != cudaSuccess) return "cudaIpcGetMemHandle failed";
+    char* sc = reinterpret_cast<char*>(scratch_);  // 512 bytes: [mine | from left | from right]
+    if (cudaMemcpyAsync(sc, &h, 64, cudaMemcpyHostToDevice, st) != cudaSuccess) return "map_peer: H2D failed";
+    Xfer s[2] = {{right, sc, 64}, {left, sc, 64}};
+    Xfer r[2] = {{left, sc + 64, 64}, {right, sc + 128, 64}};
+    std::string e = exchange(s, 2, r, 2, st);
+    if (!e.empty()) return e;
+    cudaIpcMemHandle_t hl, hr;
+    if (cudaMemcpyAsync(&hl, sc + 64, 64, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaMemcpyAsync(&hr, sc + 128, 64, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      return "map_peer: D2H failed";
+    e = open_peer(left, hl, mine, left_out);
+    if (e.empty()) e = open_peer(right, hr, mine, right_out);
+    return e;
+  }
 
  private:
+  std::string open_peer(int peer, const cudaIpcMemHandle_t& h, void* mine, void** out) {
+    if (peer == rank_) {
+      *out = mine;
+      return "";
+    }
+    const std::string key(reinterpret_cast<const char*>(&h), sizeof(h));
+    auto it = opened_.find(key);
+    if (it != opened_.end()) {
+      *out = it->second;
+      return "";
+    }
+    void* p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+      return "cudaIpcOpenMemHandle failed (peer rank " + std::to_string(peer) + ")";
+    opened_[key] = p;
+    *out = p;
+    return "";
+  }
   int rank_, n_;
   ncclComm_t comm_ = nullptr;
   double* scratch_ = nullptr;
+  std::map<std::string, void*> opened_;  // IPC mappings (closed in the destructor)
 };
 
 }  // namespace
@@ -154,6 +196,7 @@ struct LoopGroup {
   long ar_gen = 0;
   int ar_count = 0;
   std::vector<double> ar_acc, ar_res;
+  std::map<std::pair<int, long>, void*> peers;  // (rank, map_peer sequence) -> published buffer
   explicit LoopGroup(int k) : n(k) {}
 };
 
@@ -236,6 +279,20 @@ class LoopComm : public Comm {
     for (int k = 0; k < n; ++k) v[k] = g_->ar_res[k];
     return "";
   }
+  // (one process, one device: a buffer of another context is directly addressable; each rank
+  // publishes its buffer under its map_peer sequence number and takes its neighbours')
+  std::string map_peer(void* mine, int left, int right, void** left_out, void** right_out,
+                       cudaStream_t) override {
+    const long seq = map_seq_++;
+    std::unique_lock<std::mutex> lk(g_->mu);
+    g_->peers[std::make_pair(rank_, seq)] = mine;
+    g_->cv.notify_all();
+    const auto kl = std::make_pair(left, seq), kr = std::make_pair(right, seq);
+    g_->cv.wait(lk, [&] { return g_->peers.count(kl) && g_->peers.count(kr); });
+    *left_out = g_->peers[kl];
+    *right_out = g_->peers[kr];
+    return "";
+  }
   // (one process: through the host, exactly as allreduce)
   std::string allreduce_dev_u32(uint32_t* d, int n, ReduceOp op, cudaStream_t st) override {
     if (n > 64) return "allreduce: too many values";
@@ -256,6 +313,7 @@ class LoopComm : public Comm {
   LoopGroup* g_;
   int rank_;
   long seq_ = 0;
+  long map_seq_ = 0;
 };
 
 }  // namespace

@@ -36,6 +36,14 @@ class Comm {
   // In-place allreduce of n uint32 values in DEVICE memory, enqueued on `st` (NCCL: no host
   // synchronisation; the caller's next read-back of the values is the only one).
   virtual std::string allreduce_dev_u32(uint32_t* d, int n, ReduceOp op, cudaStream_t st) = 0;
+  // Peer memory (halo put): every rank passes the same buffer of its own (`mine`,
+  // the base of a cudaMalloc allocation) and gets the corresponding buffers of the ranks `left`
+  // and `right` as addresses its kernels can store to (NCCL: CUDA IPC handles exchanged with
+  // the neighbours, opened with peer access over NVLink; loopback: the other contexts'
+  // pointers; a rank that is its own neighbour gets `mine`).  Collective; the mappings live as
+  // long as the Comm.
+  virtual std::string map_peer(void* mine, int left, int right, void** left_out, void** right_out,
+                               cudaStream_t st) = 0;
 };
 
 Comm* make_nccl_comm(const void* unique_id, int rank, int nranks, std::string& err);

@@ -7,7 +7,7 @@
 //   vm   float4 (vx, vy, vz, m)                              density/gradient/force tiles
 //   gq   float4 (c_s, u, m/rho, rho)                         gradient tile (+ xh, vm)
 //   fr1  float4 (A = P/rho^2, Kf = f/(pi h^4), c_s, rho)     force tile
-//   fr2  float4 (B, P alpha_c, u, alpha_v)                   force tile (P = A rho^2)
+//   fr2  float4 (B, (P + kPeps) alpha_c, u, alpha_v)         force tile (P = A rho^2)
 // plus plain f32 arrays for state and outputs.
 #pragma once
 #include <cuda_runtime.h>
@@ -112,6 +112,12 @@ struct DevState {
   float2* grad;       // v_sig, lap_u
   float4* fr1;
   float4* fr2;
+  // halo put (X3 over peer memory): the gradient epilogue also stores the fr1 /
+  // fr2 records of the owned particles gi in [put_lo[d], put_hi[d]) at put_fr1[d][gi - put_lo[d]]
+  // / put_fr2[d][...]: the ghost slots of the left (d = 0) / right (d = 1) neighbour; null = off
+  float4* put_fr1[2];
+  float4* put_fr2[2];
+  int put_lo[2], put_hi[2];
   // force
   float4* acc;        // a, du
   float* vsig;

@@ -997,6 +997,10 @@ struct WalkArea {
 #endif
 constexpr int kDensT = SPH_DENS_T;  // k_density threads per CTA (3 CTAs per SM)
 constexpr int kGradT = SPH_GRAD_T;  // k_gradient threads per CTA (3 CTAs per SM)
+#ifndef SPH_FORCE_T
+#define SPH_FORCE_T 448
+#endif
+constexpr int kForceT = SPH_FORCE_T;  // k_force threads per CTA when two CTAs fit an SM
 template <class Acc>
 __host__ __device__ __forceinline__ size_t walk_bytes(int icap, int threads = kNW * 32) {
   return (((size_t)(icap + 1) * 4 + 15) & ~(size_t)15) + (((size_t)icap * 4 + 15) & ~(size_t)15) +
@@ -1379,7 +1383,7 @@ __global__ void __launch_bounds__(NT, MINB) k_force(DevGrid g, DevPhys ph, DevSt
                                                     DevCounters* __restrict__ ctr) {
   DESC_PROLOGUE();
   // T0 = [j]: x, y, z, 1/h   T1 = [O1+j]: vx, vy, vz, m   T2 = [O2+j]: A, Kf, c, rho
-  // T3 = [O3+j]: B, P alpha_c, u, alpha_v  (P = A rho^2)   GI[j]: global index of slot j
+  // T3 = [O3+j]: B, (P + kPeps) alpha_c, u, alpha_v  (P = A rho^2)   GI[j]: global index of slot j
   const int O1 = SP, O2 = 2 * SP, O3 = 3 * SP;
   int* GI = reinterpret_cast<int*>(smem4 + 4 * SP);
   int* pref = GI + ((SP + 3) & ~3);  // [icap + 1] force-part group prefix (k_lists)
@@ -1444,6 +1448,9 @@ __global__ void __launch_bounds__(NT, MINB) k_force(DevGrid g, DevPhys ph, DevSt
         I.P = I.a.x * I.a.w * I.a.w;
         a = make_float4(0.f, 0.f, 0.f, 0.f);
       },
+      // (one entry at a time: a packed f32x2 version over two entries, force_pair2 with
+      // FFMA2 / FMUL2, ran 17 % fewer loop instructions but needs 128 registers -- 256 x 2
+      // threads per SM: 7.60 ms against 7.06 on C4; the loop is latency-bound, not issue-bound)
       pair2_of([&](int j) {
         const uint32_t o = (uint32_t)j << 4;
         const float4 p = lds4(sb0 + o);
@@ -1770,12 +1777,12 @@ cudaError_t launch_gradient(const DevGrid& g, const DevPhys& ph, const DevState&
 cudaError_t launch_force(const DevGrid& g, const DevPhys& ph, const DevState& s, const int* cell_start,
                          DevCounters* ctr, cudaStream_t st) {
   const size_t sm = force_smem(g);
-  const void* fn = g.force_threads == 512 ? (const void*)k_force<512, 1> : (const void*)k_force<448, 2>;
+  const void* fn = g.force_threads == 512 ? (const void*)k_force<512, 1> : (const void*)k_force<kForceT, 2>;
   cudaError_t e = set_smem(fn, sm);
   if (e != cudaSuccess) return e;
   if (g.nrun == 0) return cudaSuccess;
   if (g.force_threads == 512) k_force<512, 1><<<g.nrun, 512, sm, st>>>(g, ph, s, cell_start, ctr);
-  else k_force<448, 2><<<g.nrun, 448, sm, st>>>(g, ph, s, cell_start, ctr);
+  else k_force<kForceT, 2><<<g.nrun, kForceT, sm, st>>>(g, ph, s, cell_start, ctr);
   return cudaGetLastError();
 }
 

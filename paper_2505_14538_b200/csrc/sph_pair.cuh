@@ -37,11 +37,15 @@ __device__ __forceinline__ double h2_exact(float h, float gamma_k) {
   return __dmul_rn(H, H);
 }
 
-// -dW/dq / 0.75 of M4: q (4 - 3q) for q < 1, (2 - q)^2 for 1 <= q < 2, 0 beyond
+// -dW/dq / 0.75 of M4: q (4 - 3q) for q < 1, (2 - q)^2 for 1 <= q < 2, 0 beyond, as the
+// truncated powers t^2 - 4 s^2 (t = (2 - q)+, s = (1 - q)+): no branch or predicate
 __device__ __forceinline__ float m4_dwp(float q) {
-  const float t = fmaxf(2.f - q, 0.f);
-  return q < 1.f ? q * fmaf(-3.f, q, 4.f) : t * t;
+  const float t = fmaxf(2.f - q, 0.f), s = fmaxf(1.f - q, 0.f);
+  return fmaf(t, t, -4.f * (s * s));
 }
+
+// alpha_c weight floor of the force records (force_pair2, Eq. 20 / R13)
+constexpr float kPeps = 1e-30f;
 
 // ---------------------------------------------------------------- density (Eqs. 2-6) ----
 // Accumulators per particle i (q = r/h_i, w = M4; the self pair is in the list: w(0) = 1):
@@ -231,8 +235,8 @@ __device__ __forceinline__ void grad_pair_sym(GradAcc& a, float dx, float dy, fl
 
 // Gradient ghost of particle gi (R17-R21): alpha_v (Eqs. 12-15), alpha_c (Eqs. 21-24), and
 // the force-loop records fr1 = (A = P/rho^2, K = -0.75 f/(pi h^4), c, rho) and fr2 = (B,
-// P alpha_c -- or -alpha_c when P = 0, for Eq. 20's P_i + P_j = 0 case (R13) --, u,
-// alpha_v).  Returns N_i (self excluded).
+// (P + kPeps) alpha_c -- Eq. 20's weight, with its P_i + P_j = 0 case (R13), see force_pair2 --,
+// u, alpha_v).  Returns N_i (self excluded).
 __device__ __forceinline__ int grad_epilogue(const DevPhys& ph, const DevState& s, const GradAcc& a, int gi, float h,
                                              float ci, float ui, float rho, float dt, int first_step) {
   const float hinv = 1.f / h;
@@ -259,91 +263,55 @@ __device__ __forceinline__ int grad_epilogue(const DevPhys& ph, const DevState& 
   s.ac[gi] = ac;
   s.dprev[gi] = div;
   const float f = fin.x, P = fin.y;
-  s.fr1[gi] = make_float4(P / (rho * rho), -0.75f * f * hinv * hinv * hinv * hinv / kPi, ci, rho);
-  s.fr2[gi] = make_float4(fin.w, P > 0.f ? P * ac : -ac, ui, av);
+  const float4 r1 = make_float4(P / (rho * rho), -0.75f * f * hinv * hinv * hinv * hinv / kPi, ci, rho);
+  const float4 r2 = make_float4(fin.w, (P + kPeps) * ac, ui, av);
+  s.fr1[gi] = r1;
+  s.fr2[gi] = r2;
+  // halo put: a boundary-plane particle's records also go straight to the neighbours' ghost
+  // slots (peer stores; the X3 exchange then carries only an ordering token)
+#pragma unroll
+  for (int d = 0; d < 2; ++d)
+    if (s.put_fr1[d] && gi >= s.put_lo[d] && gi < s.put_hi[d]) {
+      s.put_fr1[d][gi - s.put_lo[d]] = r1;
+      s.put_fr2[d][gi - s.put_lo[d]] = r2;
+    }
   return (a.nn & 0xffff) - 1;
 }
 
 // ------------------------------------------------------------ force (Eqs. 7, 17-24) ----
-// Gather form of the pairwise sums over r_ij < max(H_i, H_j) (R3), written with
-// g = G r = f dW/dr (the r factors cancel):
+// Pairwise sums over r_ij < max(H_i, H_j) (R3), written with g = G r = f dW/dr (the r
+// factors cancel):
 //   A = P/rho^2, Pi_ij = -abar mu v_sig / rhobar (R9), gbar = (g_i + g_j)/2,
 //   T = A_i g_i + A_j g_j + Pi_ij gbar  (= S_ij r),   a_i = -sum_j m_j T r_ij / r,
 //   du_i = sum_j m_j [(A_i g_i + Pi gbar / 2)(v_ij . r_hat) + D_ij]  (Eq. 18 + R10 + Eq. 19/R11),
 //   D_ij = alpha_c,ij v_c,ij (u_i - u_j)(g_i + g_j) / (rho_i + rho_j)  (Eqs. 20, 22; R12, R13).
 // T is evaluated from operands symmetric in (i, j), so the pair terms of i and j are exact
 // negatives (momentum and energy conserving up to the summation rounding).
-struct ForceAcc {
-  float ax, ay, az, du, vmax;  // vmax > 0: max over its f32 bits as int
-  int nn;
-  __device__ static ForceAcc zero() { return ForceAcc{0.f, 0.f, 0.f, 0.f, 0.f, 0}; }
-  __device__ void add(const ForceAcc& o) {
-    ax += o.ax; ay += o.ay; az += o.az; du += o.du; vmax = fmaxf(vmax, o.vmax); nn += o.nn;
-  }
-};
 
 // Operands of one side of a force pair: 1/h, v, m, the fr1 / fr2 records, P = A rho^2.
 struct ForceSide {
   float hinv;
   float4 v;  // (v, m)
   float4 a;  // fr1: A, K, c, rho
-  float4 b;  // fr2: B, P alpha_c (-alpha_c if P = 0), u, alpha_v
+  float4 b;  // fr2: B, (P + kPeps) alpha_c, u, alpha_v
   float P;
 };
 
-// Pair terms of i (its side of the pair) for r_ij = (dx, dy, dz); returns the pair's signal
-// velocity v_sig,ij through vs and membership (r < max(H_i, H_j), fp64 inside the band).
-template <class Exact>
-__device__ __forceinline__ void force_pair(ForceAcc& acc, float dx, float dy, float dz, const ForceSide& I,
-                                           const ForceSide& J, float beta, float band, Exact&& exact, float& vs_out,
-                                           int& in_out) {
-  const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-  const float rinv = rinv_safe(r2);
-  const float r = r2 * rinv;
-  const float qi = r * I.hinv, qj = r * J.hinv;
-  const float d = fminf(qi, qj) - 2.f;
-  int in = neg(d);
-  if (fabsf(d) < band) in = exact();
-  acc.nn += in;
-  const float gI = I.a.y * m4_dwp(qi);  // g_i = G_i r = f_i dW/dr(h_i)
-  const float gJ = J.a.y * m4_dwp(qj);
-  const float vr = fmaf(I.v.z - J.v.z, dz, fmaf(I.v.y - J.v.y, dy, (I.v.x - J.v.x) * dx));
-  const float vrr = vr * rinv;
-  const float mu = fminf(vrr, 0.f);
-  const float vs = fmaf(-beta, mu, I.a.z + J.a.z);
-  acc.vmax = fmaxf(acc.vmax, in ? vs : 0.f);
-  const float irs = __fdividef(1.f, I.a.w + J.a.w);
-  const float gs = gI + gJ;
-  // X = 4 abar mu v_sig (g_i + g_j) / (rho_i + rho_j):  Pi_ij gbar = -X / 4
-  const float X = ((I.b.w + J.b.w) * (I.b.x + J.b.x)) * (mu * vs) * (gs * irs);
-  const float AgI = I.a.x * gI;
-  const float Tij = fmaf(J.a.x, gJ, fmaf(-0.25f, X, AgI));  // S_ij r
-  const float mT = J.v.w * Tij * rinv;
-  acc.ax = fmaf(-mT, dx, acc.ax);
-  acc.ay = fmaf(-mT, dy, acc.ay);
-  acc.az = fmaf(-mT, dz, acc.az);
-  // alpha_c,ij (Eq. 20): (P_i ac_i + P_j ac_j) / (P_i + P_j), or the mean when
-  // P_i + P_j = 0 (R13; the records then hold -alpha_c)
-  const float Psum = I.P + J.P;
-  const float acij = Psum > 0.f ? __fdividef(fmaxf(I.b.y, 0.f) + fmaxf(J.b.y, 0.f), Psum) : -0.5f * (I.b.y + J.b.y);
-  const float vc = fabsf(vrr) + sqrtf(2.f * fabsf(I.P - J.P) * irs);
-  const float D = acij * vc * (I.b.z - J.b.z) * (gs * irs);
-  acc.du = fmaf(J.v.w, fmaf(fmaf(-0.125f, X, AgI), vrr, D), acc.du);
-  vs_out = vs;
-  in_out = in;
-}
-
 // Both sides of the unordered pair (i, j) (pair-once force loop), r_ij = (dx, dy, dz) = r_i - r_j:
-// the same terms as force_pair, i's added to acc (a_i, du_i), j's returned in jo (a_j, du_j):
+// i's terms added to acc (a_i, du_i), j's returned in jo (a_j, du_j):
 //   a_i -= m_j T r_ij / r,  a_j += m_i T r_ij / r  (Eq. 17: antisymmetric, momentum exact),
 //   du_i += m_j [(A_i g_i + Pi gbar / 2)(v_ij . r_hat) + D_ij],
 //   du_j += m_i [(A_j g_j + Pi gbar / 2)(v_ij . r_hat) - D_ij]  (v_ji . r_ji = v_ij . r_ij, D_ji = -D_ij).
 // Membership needs no test: g_i = g_j = 0 beyond both supports, so every term vanishes.
+// alpha_c,ij (Eq. 20) = (P_i ac_i + P_j ac_j) / (P_i + P_j), the mean when P_i + P_j = 0 (R13),
+// is ((P_i + e) ac_i + (P_j + e) ac_j) / (P_i + P_j + 2e) with e = kPeps (grad_epilogue stores
+// (P + e) ac): the mean when both P vanish, the weighted mean to a relative 1e-30 / P otherwise.
 // Returns whether the pair has any term (g_i + g_j != 0).
 __device__ __forceinline__ bool force_pair2(float4& acc, float4& jo, float dx, float dy, float dz, const ForceSide& I,
                                             const ForceSide& J, float beta) {
-  const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-  const float rinv = rinv_safe(r2);
+  // (r^2 + 1e-30: rinv_safe's floor folded into the first FMA; no pair has 0 < r^2 < 1e-20)
+  const float r2 = fmaf(dz, dz, fmaf(dy, dy, fmaf(dx, dx, 1e-30f)));
+  const float rinv = rsqrtf(r2);
   const float r = r2 * rinv;
   const float gI = I.a.y * m4_dwp(r * I.hinv);  // g_i = G_i r = f_i dW/dr(h_i)
   const float gJ = J.a.y * m4_dwp(r * J.hinv);
@@ -365,10 +333,7 @@ __device__ __forceinline__ bool force_pair2(float4& acc, float4& jo, float dx, f
   jo.x = mTj * dx;
   jo.y = mTj * dy;
   jo.z = mTj * dz;
-  // alpha_c,ij (Eq. 20): (P_i ac_i + P_j ac_j) / (P_i + P_j), or the mean when P_i + P_j = 0
-  // (R13; the records hold -alpha_c when P = 0, which contributes nothing to the weighted sum)
-  const float Psum = I.P + J.P;
-  const float acij = Psum > 0.f ? __fdividef(fmaxf(I.b.y, 0.f) + fmaxf(J.b.y, 0.f), Psum) : -0.5f * (I.b.y + J.b.y);
+  const float acij = __fdividef(I.b.y + J.b.y, I.P + J.P + 2.f * kPeps);
   const float vc = fabsf(vrr) + sqrtf(2.f * fabsf(I.P - J.P) * irs);
   const float D = acij * vc * (I.b.z - J.b.z) * gsr;
   const float hX = -0.125f * X;

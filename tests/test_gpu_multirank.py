@@ -90,6 +90,25 @@ def test_multirank_matches_single_gpu(case, R):
         assert_close("a", run["a"][sample], fo["a"][sample], atol_scale=fo["scale_a"][sample])
 
 
+@pytest.mark.parametrize("R", [1, 2, 3])
+def test_halo_put_matches_send_recv(R):
+    """X3 by peer stores from the gradient epilogue (halo_put = 1, NEXT#4) against X3 by
+    send/recv of the ghost planes after the loop (halo_put = 0): the force loop sees the same
+    ghost records, so counts agree exactly and a, du/dt to the summation order."""
+    p = _switches(W.jittered_lattice(30, seed=66, vel_sigma=0.2, u_sigma=0.4), 5)
+    res = {}
+    for put in (0, 1):
+        res[put], _ = run_ranks(p, R, _hydro(1e-3), h_max_iter=0, halo_put=put)
+    a, b = res[0], res[1]
+    assert np.array_equal(a["count"], b["count"])
+    assert np.array_equal(a["count_force"], b["count_force"])
+    for k in ("rho", "P", "v_sig_grad", "v_sig", "alpha_v"):
+        assert np.array_equal(a[k], b[k]), k
+    for k in ("a", "du"):
+        scale = np.abs(a[k]).max()
+        assert np.abs(a[k] - b[k]).max() <= 1e-5 * scale, k
+
+
 @pytest.mark.parametrize("G", [2, 3])
 def test_multirank_more_ghost_planes(G, monkeypatch):
     """The [G ghost | owned | G ghost] plane layout (the one wide particles need)

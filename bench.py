@@ -87,6 +87,9 @@ def parse():
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--tile-z", type=int, default=0, help="cells per CTA block along z (0 = auto)")
     ap.add_argument("--skin", type=float, default=None, help="cell_skin (default: the library's)")
+    ap.add_argument("--halo-put", type=int, default=-1, choices=[-1, 0, 1],
+                    help="X2/X3 halos by peer stores from the loop epilogues (1), NCCL send/recv (0), "
+                         "or the library default (-1: send/recv over several NCCL ranks)")
     ap.add_argument("--cpu-baseline-all", default=None, metavar="OUT.json",
                     help="time the oracle on every config family (+ single-thread C1-C3) and exit")
     return ap.parse_args()
@@ -306,6 +309,8 @@ def run_ours(args, world, rank, local):
         multi["tile_cells_z"] = args.tile_z
     if args.skin is not None:
         multi["cell_skin"] = args.skin
+    if world > 1 and args.halo_put >= 0:
+        multi["halo_put"] = args.halo_put
     ctx = Context(p, stream=stream.cuda_stream, device=local, **multi)
     dt = 1e-4
 

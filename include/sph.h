@@ -102,15 +102,15 @@ typedef struct {
   int32_t decomp[3];      /* ranks per axis of the domain decomposition;*/
                           /* {0,0,0} (default) = x-slabs {nranks, 1, 1}, the one implemented:   */
                           /* any other product of nranks is SPH_ERR_INVALID_ARG                */
-  int32_t halo_put;       /* X3 (force records of the ghost planes): 1 = the */
-                          /* gradient loop's epilogue stores each boundary-plane particle's fr1 / */
-                          /* fr2 records straight into the neighbours' ghost slots over peer     */
-                          /* memory (NVLink P2P stores through CUDA IPC mappings; loopback: the  */
-                          /* other contexts' buffers), and only a zero-payload token is sent to  */
-                          /* order the neighbours' force loops after them; 0 = NCCL send/recv of */
-                          /* the planes after the loop; -1 (default) = 1 for loopback and one    */
+  int32_t halo_put;       /* X2 / X3 halos: 1 = the density and gradient  */
+                          /* loops' epilogues store each boundary-plane particle's records      */
+                          /* straight into the neighbours' ghost slots over peer memory (NVLink */
+                          /* P2P stores through CUDA IPC mappings; loopback: the other contexts'*/
+                          /* buffers) and each exchange sends only a zero-payload token that    */
+                          /* orders the neighbours' next loop after them; 0 = NCCL send/recv of */
+                          /* the planes after the loop; -1 (default) = 1 for loopback and one   */
                           /* rank, 0 for NCCL over several ranks (not yet run on multi-GPU      */
-                          /* hardware).  DESIGN.md §9.                                           */
+                          /* hardware).  DESIGN.md §9.                                          */
 } sph_config;
 
 /* Particle input.  n particles; arrays are host pointers (on_device = 0) or device

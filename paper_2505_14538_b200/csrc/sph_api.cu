@@ -190,6 +190,15 @@ __global__ void k_pack_mig(int n, const unsigned int* __restrict__ perm, Persist
   out[p] = r;
 }
 
+// Halo put (X2): the ghosts' final h, stored into hin by the neighbours' density epilogues,
+// into the ghost positions' h (after the token; ghost slots [0, gL) and [gL + n_own, + gR)).
+__global__ void k_ghost_h(int gL, int n_own, int gR, const float* __restrict__ hin, uint4* xh) {
+  int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= gL + gR) return;
+  if (p >= gL) p += n_own;
+  reinterpret_cast<unsigned int*>(&xh[p])[3] = __float_as_uint(hin[p]);
+}
+
 __global__ void k_unpack_mig(int n, const MigRec* __restrict__ in, Persist dst) {
   int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
@@ -348,6 +357,11 @@ struct sph_ctx {
   bool halo_put = false;
   float4* peer_fr1[2] = {nullptr, nullptr};
   float4* peer_fr2[2] = {nullptr, nullptr};
+  float4* peer_gq[2] = {nullptr, nullptr};
+  float4* peer_vc[2] = {nullptr, nullptr};
+  float2* peer_um[2] = {nullptr, nullptr};
+  float* peer_h[2] = {nullptr, nullptr};
+  float* hin = nullptr;  // [cap] ghost h stored by the neighbours' density epilogues (X2 put)
   bool x2_pending = false, x3_pending = false;
   uint8_t* side_flag = nullptr;  // [2 nact]: interior, boundary flags
   int* side_list = nullptr;      // [2 nact]: interior active indices at 0, boundary ones at nact
@@ -702,6 +716,19 @@ sph_status halo_async(sph_ctx* c, void* const* bases, const size_t* elems, int n
   return SPH_OK;
 }
 
+// Halo put: a zero-payload exchange (8 bytes each way with both neighbours) on the
+// communication stream after the work enqueued so far on the context stream.  Stream order
+// makes it leave after the kernels whose epilogues stored into the neighbours' buffers, and
+// arrive after theirs: the ordering NCCL send/recv of the data would have given.
+sph_status halo_token(sph_ctx* c) {
+  CK(cudaEventRecord(c->ev_main, c->stream));
+  CK(cudaStreamWaitEvent(c->cstream, c->ev_main, 0));
+  Xfer ts[2] = {{right_of(c), c->cnt_dev + 4, 8}, {left_of(c), c->cnt_dev + 5, 8}};
+  Xfer tr[2] = {{left_of(c), c->cnt_dev + 6, 8}, {right_of(c), c->cnt_dev + 7, 8}};
+  CKC(c->comm->exchange(ts, 2, tr, 2, c->cstream));
+  return SPH_OK;
+}
+
 // The context stream waits for every pending asynchronous exchange.
 sph_status join_comm(sph_ctx* c) {
   if (c->x2_pending) CK(cudaStreamWaitEvent(c->stream, c->ev_x2, 0));
@@ -1036,8 +1063,16 @@ sph_status rebuild_impl(sph_ctx* c) {
       ds.put_fr2[0] = c->peer_fr2[0] + dstL;
       ds.put_lo[0] = c->gL;
       ds.put_hi[0] = c->gL + c->planeL;
+      ds.put_gq[0] = c->peer_gq[0] + dstL;
+      ds.put_vc[0] = c->peer_vc[0] + dstL;
+      ds.put_um[0] = c->peer_um[0] + dstL;
+      ds.put_h[0] = c->peer_h[0] + dstL;
       ds.put_fr1[1] = c->peer_fr1[1];
       ds.put_fr2[1] = c->peer_fr2[1];
+      ds.put_gq[1] = c->peer_gq[1];
+      ds.put_vc[1] = c->peer_vc[1];
+      ds.put_um[1] = c->peer_um[1];
+      ds.put_h[1] = c->peer_h[1];
       ds.put_lo[1] = c->gL + n - c->planeR;
       ds.put_hi[1] = c->gL + n;
     }
@@ -1644,17 +1679,24 @@ sph_status sph_create(const sph_config* cfg, const sph_particles_in* in, sph_ctx
     c->halo_put = cfg->halo_put == 1 ||
                   (cfg->halo_put < 0 && (cfg->transport == SPH_TRANSPORT_LOOPBACK || c->nranks == 1));
     if (c->halo_put) {
-      void* p[4];
-      std::string e = c->comm->map_peer(c->s.fr1, left_of(c), right_of(c), &p[0], &p[1], c->stream);
-      if (e.empty()) e = c->comm->map_peer(c->s.fr2, left_of(c), right_of(c), &p[2], &p[3], c->stream);
+      if (dalloc(&c->hin, (size_t)c->cap) != cudaSuccess) return bail(SPH_ERR_OOM);
+      void* const mine[6] = {c->s.fr1, c->s.fr2, c->s.gq, c->s.vc, c->s.um, c->hin};
+      void* p[6][2];
+      std::string e;
+      for (int k = 0; k < 6 && e.empty(); ++k)
+        e = c->comm->map_peer(mine[k], left_of(c), right_of(c), &p[k][0], &p[k][1], c->stream);
       if (!e.empty()) {
         fail(c, SPH_ERR_NCCL, "halo put: " + e);
         fprintf(stderr, "sph_create: %s\n", c->err.c_str());
         return bail(SPH_ERR_NCCL);
       }
       for (int d = 0; d < 2; ++d) {
-        c->peer_fr1[d] = static_cast<float4*>(p[d]);
-        c->peer_fr2[d] = static_cast<float4*>(p[2 + d]);
+        c->peer_fr1[d] = static_cast<float4*>(p[0][d]);
+        c->peer_fr2[d] = static_cast<float4*>(p[1][d]);
+        c->peer_gq[d] = static_cast<float4*>(p[2][d]);
+        c->peer_vc[d] = static_cast<float4*>(p[3][d]);
+        c->peer_um[d] = static_cast<float2*>(p[4][d]);
+        c->peer_h[d] = static_cast<float*>(p[5][d]);
       }
     }
   }
@@ -1752,9 +1794,21 @@ sph_status sph_density(sph_ctx* c, sph_density_stats* stats) {
   unconverged = c->ctr_h->unconverged;
   // ghosts need the final h and the gradient-loop record of their owners (X2)
   if (c->slab) {
-    void* const b[4] = {c->s.xh, c->s.gq, c->s.vc, c->s.um};
-    const size_t e[4] = {sizeof(uint4), sizeof(float4), sizeof(float4), sizeof(float2)};
-    if ((st = halo_async(c, b, e, 4, c->ev_x2)) != SPH_OK) return st;
+    if (c->halo_put) {
+      // the density epilogues stored gq / vc / um in the neighbours' ghost slots and h in their
+      // hin: the token orders that before this rank takes its ghost h from hin (and before the
+      // neighbours' gradient boundary blocks)
+      if ((st = halo_token(c)) != SPH_OK) return st;
+      if (c->gL + c->gR > 0) {
+        k_ghost_h<<<nblk(c->gL + c->gR, 256), 256, 0, c->cstream>>>(c->gL, c->n_own, c->gR, c->hin, c->s.xh);
+        CK(cudaGetLastError());
+      }
+      CK(cudaEventRecord(c->ev_x2, c->cstream));
+    } else {
+      void* const b[4] = {c->s.xh, c->s.gq, c->s.vc, c->s.um};
+      const size_t e[4] = {sizeof(uint4), sizeof(float4), sizeof(float4), sizeof(float2)};
+      if ((st = halo_async(c, b, e, 4, c->ev_x2)) != SPH_OK) return st;
+    }
     c->x2_pending = true;
   }
   const double un = unconverged;  // (already the maximum over ranks)
@@ -1819,14 +1873,9 @@ sph_status sph_gradient(sph_ctx* c, float dt) {
   // the force loop's interior blocks
   if (c->slab) {
     if (c->halo_put) {
-      // the gradient epilogues stored the ghost records in the neighbours' buffers already: a
-      // zero-payload token (8 bytes each way) orders the neighbours' boundary force blocks after
-      // this rank's gradient kernels, and theirs before ours
-      CK(cudaEventRecord(c->ev_main, c->stream));
-      CK(cudaStreamWaitEvent(c->cstream, c->ev_main, 0));
-      Xfer ts[2] = {{right_of(c), c->cnt_dev + 4, 8}, {left_of(c), c->cnt_dev + 5, 8}};
-      Xfer tr[2] = {{left_of(c), c->cnt_dev + 6, 8}, {right_of(c), c->cnt_dev + 7, 8}};
-      CKC(c->comm->exchange(ts, 2, tr, 2, c->cstream));
+      // the gradient epilogues stored the ghost records in the neighbours' buffers already: the
+      // token orders the neighbours' boundary force blocks after them, and theirs before ours
+      if ((st = halo_token(c)) != SPH_OK) return st;
       CK(cudaEventRecord(c->ev_x3, c->cstream));
     } else {
       void* const b[2] = {c->s.fr1, c->s.fr2};
@@ -2046,7 +2095,7 @@ sph_status sph_destroy(sph_ctx* c) {
                   c->pc_recv, c->pc_scan, c->scan_tmp, c->cnt_dev, c->wide_flag, c->widx, c->wcount,
                   c->n_wide_dev, c->wnbr, c->sel_tmp, c->desc_buf, c->pref_buf,
                   c->act_flag, c->blk_list, c->run_list, c->cperm, c->ccs, s.dup, c->side_flag, c->side_list,
-                  s.vc, s.um};
+                  s.vc, s.um, c->hin};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->ctr_h) cudaFreeHost(c->ctr_h);

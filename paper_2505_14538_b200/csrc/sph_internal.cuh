@@ -118,6 +118,13 @@ struct DevState {
   float4* put_fr1[2];
   float4* put_fr2[2];
   int put_lo[2], put_hi[2];
+  // and X2 from the density epilogue (finished particles): gq, vc, um into the neighbours'
+  // ghost slots, h into their `hin` (their density loop still reads its ghost h; a copy kernel
+  // moves it into xh after the token)
+  float4* put_gq[2];
+  float4* put_vc[2];
+  float2* put_um[2];
+  float* put_h[2];
   // force
   float4* acc;        // a, du
   float* vsig;

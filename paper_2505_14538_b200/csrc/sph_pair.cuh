@@ -140,6 +140,17 @@ __device__ __forceinline__ DenOut den_epilogue(const DevGrid& g, const DevPhys& 
     const float4 vmi = s.vm[gi];
     s.vc[gi] = make_float4(vmi.x, vmi.y, vmi.z, cs);
     s.um[gi] = make_float2(u, mi / rho);
+    // halo put (X2): a boundary-plane particle's gradient records and h go straight to the
+    // neighbours (peer stores; the exchange then carries only an ordering token)
+#pragma unroll
+    for (int d = 0; d < 2; ++d)
+      if (s.put_gq[d] && gi >= s.put_lo[d] && gi < s.put_hi[d]) {
+        const int t = gi - s.put_lo[d];
+        s.put_gq[d][t] = make_float4(cs, u, mi / rho, rho);
+        s.put_vc[d][t] = make_float4(vmi.x, vmi.y, vmi.z, cs);
+        s.put_um[d][t] = make_float2(u, mi / rho);
+        s.put_h[d][t] = h;
+      }
     s.active[gi] = 0;
     s.iters[gi] = conv ? it : -1;
     o.final_ = true;

@@ -15,7 +15,7 @@ hdr, units = r[0], r[1]
 tscale = {"nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3, "second": 1.0, "s": 1.0}
 dur = {}
 for row in r[2:]:
-    name = row[hdr.index("Kernel Name")].split("(")[0].split("::")[-1]
+    name = row[hdr.index("Kernel Name")].split("(")[0].split("::")[-1].split("<")[0]
     i = hdr.index("gpu__time_duration.sum")
     dur.setdefault(name, float(row[i].replace(",", "")) * tscale.get(units[i], 1e-9))
 for k in sys.argv[2:] or ["k_density", "k_gradient", "k_force"]:

@@ -14,7 +14,7 @@ scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 tscale = {"nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3, "second": 1.0, "s": 1.0}
 res = {"report": rep, "dram_bytes_per_launch": {}, "duration_s": {}}
 for row in r[2:]:
-    name = row[hdr.index("Kernel Name")].split("(")[0].split("::")[-1].replace("k_", "")
+    name = row[hdr.index("Kernel Name")].split("(")[0].split("::")[-1].split("<")[0].replace("k_", "")
     def val(k, tab):
         i = hdr.index(k)
         return float(row[i].replace(",", "")) * tab.get(units[i], 1.0)

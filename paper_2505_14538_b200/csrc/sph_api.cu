@@ -372,6 +372,7 @@ struct sph_ctx {
   unsigned long long* pairs_grad_h = nullptr;  // pinned: the last gradient loop's directed pairs
   float wide_margin = 0.2f;     // adaptive grid: DevGrid::wide_margin (env SPH_WIDE_MARGIN overrides)
   int sparse_wide = 32;         // adaptive grid: blocks with fewer tile particles go wide (env SPH_SPARSE_WIDE; 0 = off)
+  double coarse_q = 0.99;       // wide search grid: the h quantile its coarse cells are sized from (env SPH_COARSE_Q)
   uint32_t* cperm = nullptr;    // wide search grid: particles in coarse-cell order
   size_t cperm_cap = 0;
   int* ccs = nullptr;           // its coarse cell starts
@@ -1445,7 +1446,7 @@ sph_status mark_wide(sph_ctx* c) {
     // quantile: not a collective, the ranks' wide sets differ); all local particles, ghosts too
     DevGrid& g = c->grid;
     float hq = 0.f;
-    if (n > 0 && (sq = h_quantile(c, 0.99, &hq, false)) != SPH_OK) return sq;
+    if (n > 0 && (sq = h_quantile(c, c->coarse_q, &hq, false)) != SPH_OK) return sq;
     if (!(hq > 0.f)) hq = c->h_side;
     const float R = (1.f + c->cfg.cell_skin) * c->cfg.gamma_k * hq;
     const float side = std::min(g.side[0], std::min(g.side[1], g.side[2]));
@@ -1674,6 +1675,7 @@ sph_status sph_create(const sph_config* cfg, const sph_particles_in* in, sph_ctx
   fill_phys(c);
   if (const char* m = getenv("SPH_WIDE_MARGIN")) c->wide_margin = (float)std::max(0.0, atof(m));
   if (const char* m = getenv("SPH_SPARSE_WIDE")) c->sparse_wide = std::max(0, atoi(m));
+  if (const char* m = getenv("SPH_COARSE_Q")) c->coarse_q = std::min(1.0, std::max(0.01, atof(m)));
   if ((st = alloc_state(c)) != SPH_OK) return bail(st);
   if (c->slab) {
     c->halo_put = cfg->halo_put == 1 ||

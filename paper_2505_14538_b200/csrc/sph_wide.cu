@@ -14,7 +14,7 @@
 //   - symmetry of the force set r < max(H_i, H_j) (R3): a partner j that did not list i
 //     (a tile particle more than one cell away, or a wide particle whose own search range
 //     stops short of i) gets its side of the pair from i, added with atomics (a, du/dt,
-//     N_force) and atomicMax (v_sig); its CFL dt candidate goes to the global minimum.
+//     N_force) and atomicMax (v_sig); the CFL dt follows from the final v_sig (k_force_fin).
 // The tile kernels skip wide particles as i (empty list, no epilogue) and see them as j like
 // any other particle of their tile.
 #include <cuda_runtime.h>
@@ -307,11 +307,6 @@ __device__ __forceinline__ ForceSide side_of(const DevState& s, int i, float h) 
   return f;
 }
 
-__device__ __forceinline__ void dt_candidate(const DevPhys& ph, DevCounters* ctr, float h, float vsig) {
-  const float dt = ph.c_cfl * 2.f * ph.gamma_k * h / vsig;
-  if (dt > 0.f && dt < CUDART_INF_F) atomicMin(&ctr->dt_bits, __float_as_uint(dt));
-}
-
 __device__ __forceinline__ void red_add4_w(float4* p, const float4& v) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w));
 }
@@ -322,7 +317,7 @@ __device__ __forceinline__ void red_add4_w(float4* p, const float4& v) {
 // force part), so i does; a wide partner that listed i too does it only if it has the lower index;
 // one that did not list i leaves it to i.  i's side is reduced over the warp (lane order), j's
 // goes to acc[j] with one vector reduction.  v_sig and N_force: i's over its list; a partner
-// that did not list i gets its share of the pair here (atomics), with its CFL candidate.
+// that did not list i gets its share of the pair here (atomics).
 template <bool PX>
 __global__ void __launch_bounds__(256) k_wide_force(DevGrid g, DevPhys ph, DevState s, DevCounters* __restrict__ ctr) {
   const int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
@@ -382,11 +377,11 @@ __global__ void __launch_bounds__(256) k_wide_force(DevGrid g, DevPhys ph, DevSt
       force_pair2(ai, jo, d.x, d.y, d.z, I, J, ph.beta);
       red_add4_w(s.acc + j, jo);
     }
-    // v_sig and N_force of a partner that listed i already hold the pair (gradient loop)
+    // v_sig and N_force of a partner that listed i already hold the pair (gradient loop); the
+    // CFL dt is taken from the final v_sig of every particle afterwards (k_force_fin)
     if (j != i && in && !seen && jown) {
       atomicMax(reinterpret_cast<int*>(&s.vsig[j]), __float_as_int(vs));
       atomicAdd(&s.countf[j], 1);
-      dt_candidate(ph, ctr, hj, vs);
     }
   }
   ai.x = warp_sum(ai.x);
@@ -399,7 +394,6 @@ __global__ void __launch_bounds__(256) k_wide_force(DevGrid g, DevPhys ph, DevSt
   red_add4_w(s.acc + i, ai);
   atomicMax(reinterpret_cast<int*>(&s.vsig[i]), __float_as_int(vmax));
   atomicAdd(&s.countf[i], nn - 1);  // (the self pair)
-  dt_candidate(ph, ctr, h, vmax);
   if (!(isfinite(vmax) && isfinite(ai.x) && isfinite(ai.y) && isfinite(ai.z) && isfinite(ai.w)))
     atomicExch(&ctr->nonfinite, 1);
 }

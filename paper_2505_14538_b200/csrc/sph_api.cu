@@ -373,10 +373,13 @@ struct sph_ctx {
   float wide_margin = 0.2f;     // adaptive grid: DevGrid::wide_margin (env SPH_WIDE_MARGIN overrides)
   int sparse_wide = 32;         // adaptive grid: blocks with fewer tile particles go wide (env SPH_SPARSE_WIDE; 0 = off)
   double coarse_q = 0.99;       // wide search grid: the h quantile its coarse cells are sized from (env SPH_COARSE_Q)
-  uint32_t* cperm = nullptr;    // wide search grid: particles in coarse-cell order
-  size_t cperm_cap = 0;
-  int* ccs = nullptr;           // its coarse cell starts
-  size_t ccs_cap = 0;
+  // distinct wide search grids (env SPH_COARSE_LEVELS, 1..kCoarseLevels); C5s ms per step with 1 / 2 / 3:
+  // 29.5 / 29.0 / 29.2 (the wide list build is bound by its gather latency, not by the candidates)
+  int coarse_levels = 2;
+  uint32_t* cperm[kCoarseLevels] = {};  // wide search grids: particles in coarse-cell order
+  size_t cperm_cap[kCoarseLevels] = {};
+  int* ccs[kCoarseLevels] = {};         // their coarse cell starts
+  size_t ccs_cap[kCoarseLevels] = {};
   size_t act_cap = 0;
   size_t list_cap = 0;
   char* desc_buf = nullptr;   // tile descriptors, nblocks x tile_desc_bytes()
@@ -1450,27 +1453,43 @@ sph_status mark_wide(sph_ctx* c) {
     if (!(hq > 0.f)) hq = c->h_side;
     const float R = (1.f + c->cfg.cell_skin) * c->cfg.gamma_k * hq;
     const float side = std::min(g.side[0], std::min(g.side[1], g.side[2]));
-    const int F = std::max(1, std::min(64, (int)std::ceil(R / (2.f * side))));
-    s.cF = F;
-    s.cnx = (g.nx + F - 1) / F;
-    s.cny = (g.ny + F - 1) / F;
-    s.cnz = (g.nz + F - 1) / F;
-    const long long ncc = (long long)s.cnx * s.cny * s.cnz;
-    if ((sq = grow_h(c, &c->cperm, c->cperm_cap, (size_t)std::max(n_loc, 1))) != SPH_OK) return sq;
-    if ((sq = grow_h(c, &c->ccs, c->ccs_cap, (size_t)ncc + 1)) != SPH_OK) return sq;
-    CK(launch_coarse_keys(n_loc, 0, g, s, c->keys, c->perm, c->stream));
-    c->launches++;
-    int bits = 1;
-    while ((1LL << bits) <= ncc) ++bits;
-    size_t tmp = c->sort_tmp_bytes;
-    CK(cub::DeviceRadixSort::SortPairs(c->sort_tmp, tmp, c->keys, c->keys_alt, c->perm, c->cperm, n_loc, 0, bits,
-                                       c->stream));
-    c->launches++;
-    k_cell_start<<<nblk(n_loc + 1, 256), 256, 0, c->stream>>>(n_loc, (int)ncc, 0, c->keys_alt, c->ccs);
-    c->launches++;
-    CK(cudaGetLastError());
-    s.cperm = c->cperm;
-    s.ccs = c->ccs;
+    const int Ftop = std::max(1, std::min(64, (int)std::ceil(R / (2.f * side))));
+    // levels F/9, F/3, F (finest first; coarse_level takes the finest at least half a particle's
+    // reach; with coarse_levels < kCoarseLevels the finest ones repeat the next), each capped to
+    // 2^26 coarse cells
+    for (int l = 0; l < kCoarseLevels; ++l) {
+      int F = Ftop;
+      for (int q = l; q < kCoarseLevels - 1; ++q) F = q + c->coarse_levels >= kCoarseLevels ? std::max(1, F / 3) : F;
+      while ((long long)((g.nx + F - 1) / F) * ((g.ny + F - 1) / F) * ((g.nz + F - 1) / F) > (1LL << 26)) ++F;
+      if (l > 0) F = std::max(F, s.cF[l - 1]);
+      s.cF[l] = F;
+      s.cnx[l] = (g.nx + F - 1) / F;
+      s.cny[l] = (g.ny + F - 1) / F;
+      s.cnz[l] = (g.nz + F - 1) / F;
+    }
+    for (int l = 0; l < kCoarseLevels; ++l) {
+      if (l > 0 && s.cF[l] == s.cF[l - 1]) {  // (a repeated level shares the finer one's arrays)
+        s.cperm[l] = s.cperm[l - 1];
+        s.ccs[l] = s.ccs[l - 1];
+        continue;
+      }
+      const long long ncc = (long long)s.cnx[l] * s.cny[l] * s.cnz[l];
+      if ((sq = grow_h(c, &c->cperm[l], c->cperm_cap[l], (size_t)std::max(n_loc, 1))) != SPH_OK) return sq;
+      if ((sq = grow_h(c, &c->ccs[l], c->ccs_cap[l], (size_t)ncc + 1)) != SPH_OK) return sq;
+      CK(launch_coarse_keys(n_loc, l, g, s, c->keys, c->perm, c->stream));
+      c->launches++;
+      int bits = 1;
+      while ((1LL << bits) <= ncc) ++bits;
+      size_t tmp = c->sort_tmp_bytes;
+      CK(cub::DeviceRadixSort::SortPairs(c->sort_tmp, tmp, c->keys, c->keys_alt, c->perm, c->cperm[l], n_loc, 0,
+                                         bits, c->stream));
+      c->launches++;
+      k_cell_start<<<nblk(n_loc + 1, 256), 256, 0, c->stream>>>(n_loc, (int)ncc, 0, c->keys_alt, c->ccs[l]);
+      c->launches++;
+      CK(cudaGetLastError());
+      s.cperm[l] = c->cperm[l];
+      s.ccs[l] = c->ccs[l];
+    }
   }
   if (nw > 0 && c->grid.nact > 0) {
     // the loop kernels run only the blocks with a non-wide i particle
@@ -1676,6 +1695,7 @@ sph_status sph_create(const sph_config* cfg, const sph_particles_in* in, sph_ctx
   if (const char* m = getenv("SPH_WIDE_MARGIN")) c->wide_margin = (float)std::max(0.0, atof(m));
   if (const char* m = getenv("SPH_SPARSE_WIDE")) c->sparse_wide = std::max(0, atoi(m));
   if (const char* m = getenv("SPH_COARSE_Q")) c->coarse_q = std::min(1.0, std::max(0.01, atof(m)));
+  if (const char* m = getenv("SPH_COARSE_LEVELS")) c->coarse_levels = std::min(kCoarseLevels, std::max(1, atoi(m)));
   if ((st = alloc_state(c)) != SPH_OK) return bail(st);
   if (c->slab) {
     c->halo_put = cfg->halo_put == 1 ||
@@ -2096,7 +2116,8 @@ sph_status sph_destroy(sph_ctx* c) {
                   c->blk[0], c->blk[1], c->ctr, c->scratch, c->out_tmp, c->mig_send, c->mig_recv, c->pc_send,
                   c->pc_recv, c->pc_scan, c->scan_tmp, c->cnt_dev, c->wide_flag, c->widx, c->wcount,
                   c->n_wide_dev, c->wnbr, c->sel_tmp, c->desc_buf, c->pref_buf,
-                  c->act_flag, c->blk_list, c->run_list, c->cperm, c->ccs, s.dup, c->side_flag, c->side_list,
+                  c->act_flag, c->blk_list, c->run_list, c->cperm[0], c->cperm[1], c->cperm[2], c->ccs[0],
+                  c->ccs[1], c->ccs[2], s.dup, c->side_flag, c->side_list,
                   s.vc, s.um, c->hin};
   for (void* p : ptrs)
     if (p) cudaFree(p);

@@ -87,6 +87,8 @@ struct DevPhys {
   float gamma_eos, beta, alpha_v_max, ell, alpha_c_min, alpha_c_max, beta_c, c_cfl;
 };
 
+constexpr int kCoarseLevels = 3;  // wide search grids (cell factors F, F/3, F/9 of the p99 one)
+
 struct DevState {
   uint4* xh;
   float4* vm;
@@ -150,11 +152,13 @@ struct DevState {
   int32_t* wcount;    // [n_wide] list lengths
   int n_wide, wlcap;
   int n_wide_own;     // widx[0, n_wide_own): the owned ones (then the slab path's ghosts)
-  // the wide particles' search grid: coarse cells of cF^3 grid cells (cnx x cny x cnz, the
-  // last along an axis possibly thinner), particles sorted by coarse cell (cperm), ranges ccs
-  const uint32_t* cperm;  // [n_own] particle indices in coarse-cell order
-  const int* ccs;         // [cnx cny cnz + 1] coarse cell starts in cperm
-  int cF, cnx, cny, cnz;
+  // the wide particles' search grids: kCoarseLevels coarse grids, level l of cells of cF[l]^3
+  // grid cells (cnx x cny x cnz, the last along an axis possibly thinner), particles sorted by
+  // coarse cell (cperm), ranges ccs; a wide particle searches the finest level whose cells are
+  // at least half its reach (coarse_level, sph_wide.cu), so its box meets <= 3 cells per axis
+  const uint32_t* cperm[kCoarseLevels];  // [n local] particle indices in coarse-cell order
+  const int* ccs[kCoarseLevels];         // [cnx cny cnz + 1] coarse cell starts in cperm
+  int cF[kCoarseLevels], cnx[kCoarseLevels], cny[kCoarseLevels], cnz[kCoarseLevels];
 };
 
 struct DevCounters {
@@ -192,7 +196,7 @@ cudaError_t launch_bank(int i0, int n, const DevGrid& g, const DevState& s, cuda
 // wide particles (sph_wide.cu)
 cudaError_t launch_mark_wide(int n, const DevGrid& g, const DevPhys& ph, const DevState& s, uint8_t* flag,
                              unsigned int* n0, cudaStream_t st);
-cudaError_t launch_coarse_keys(int n, int i0, const DevGrid& g, const DevState& s, unsigned int* keys,
+cudaError_t launch_coarse_keys(int n, int level, const DevGrid& g, const DevState& s, unsigned int* keys,
                                unsigned int* vals, cudaStream_t st);
 cudaError_t launch_wide_lists(const DevGrid& g, const DevPhys& ph, const DevState& s, const int* cell_start,
                               DevCounters* ctr, cudaStream_t st);

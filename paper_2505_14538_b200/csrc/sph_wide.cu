@@ -98,15 +98,25 @@ __device__ __forceinline__ void coarse_range(int a, int k, int n, int F, int cn,
   }
 }
 
+// coarse level of a wide particle whose search reaches kx, ky, kz grid cells: the finest
+// whose cells are at least half the reach (its box then meets at most 3 coarse cells per axis)
+__device__ __forceinline__ int coarse_level(const DevState& s, int kx, int ky, int kz) {
+  const int k = max(kx, max(ky, kz));
+  int l = 0;
+#pragma unroll
+  for (int q = 0; q < kCoarseLevels - 1; ++q) l += (2 * s.cF[l] < k) ? 1 : 0;
+  return l;
+}
+
 template <bool PX>
-__global__ void k_coarse_keys(int n, DevGrid g, DevState s, unsigned int* keys, unsigned int* vals) {
+__global__ void k_coarse_keys(int n, int l, DevGrid g, DevState s, unsigned int* keys, unsigned int* vals) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint4 x = s.xh[i];
-  const int F = s.cF;
+  const int F = s.cF[l];
   const unsigned int ccx = (unsigned)(plane_of<PX>(g, i, x.x) / F), ccy = (unsigned)(cell_axis(x.y, g.ny) / F),
                      ccz = (unsigned)(cell_axis(x.z, g.nz) / F);
-  keys[i] = (ccx * (unsigned)s.cny + ccy) * (unsigned)s.cnz + ccz;
+  keys[i] = (ccx * (unsigned)s.cny[l] + ccy) * (unsigned)s.cnz[l] + ccz;
   vals[i] = (unsigned)i;
 }
 
@@ -144,45 +154,73 @@ __global__ void __launch_bounds__(256) k_wide_lists(DevGrid g, DevPhys ph, DevSt
   const int cx = plane_of<PX>(g, i, xi.x), cy = cell_axis(xi.y, g.ny), cz = cell_axis(xi.z, g.nz);
   const int kx = px ? reach(Hfac * hi, g.side[0], g.nx) : (int)ceilf(Hfac * hi / g.side[0]),
             ky = reach(Hfac * hi, g.side[1], g.ny), kz = reach(Hfac * hi, g.side[2], g.nz);
-  const int F = s.cF;
+  const int lev = coarse_level(s, kx, ky, kz);
+  const int F = s.cF[lev], cnx = s.cnx[lev], cny = s.cny[lev], cnz = s.cnz[lev];
+  const int* __restrict__ ccs = s.ccs[lev];
+  const uint32_t* __restrict__ cperm = s.cperm[lev];
   int x0, nxc, y0, nyc, z0, nzc;  // coarse cells meeting the grid-cell box, per axis
-  coarse_range(cx - kx, kx, g.nx, F, s.cnx, x0, nxc, px);
-  coarse_range(cy - ky, ky, g.ny, F, s.cny, y0, nyc);
-  coarse_range(cz - kz, kz, g.nz, F, s.cnz, z0, nzc);
-  const int run1 = min(nzc, s.cnz - z0);  // the z range as at most two contiguous runs
+  coarse_range(cx - kx, kx, g.nx, F, cnx, x0, nxc, px);
+  coarse_range(cy - ky, ky, g.ny, F, cny, y0, nyc);
+  coarse_range(cz - kz, kz, g.nz, F, cnz, z0, nzc);
+  const int run1 = min(nzc, cnz - z0);  // the z range as at most two contiguous runs
   uint32_t* lst = s.wnbr + (size_t)wi * s.wlcap;
-  // the warp walks the (few) coarse columns in order, its lanes over each column's z run of
-  // candidates, hits compacted with a ballot: the list is in (column, slot) order
+  // the candidate ranges -- (coarse column, z run) pairs, in order -- 32 at a time: lane r loads
+  // range r's ends, a warp scan flattens them, and the lanes walk the flattened candidates (so a
+  // short range costs no round trip of its own), hits compacted with a ballot: the list is in
+  // (column, z run, slot) order
   int cnt = 0;
-  for (int q = 0; q < nxc * nyc; ++q) {
-    const int ax = q / nyc, ay = q - ax * nyc;
-    const int ccx = (x0 + ax) % s.cnx, ccy = (y0 + ay) % s.cny;
-    const int col = (ccx * s.cny + ccy) * s.cnz;
-    for (int part = 0; part < 2; ++part) {
-      const int c0 = part == 0 ? z0 : 0, nc = part == 0 ? run1 : nzc - run1;
-      if (nc <= 0) continue;
-      const int t0 = __ldg(s.ccs + col + c0), t1 = __ldg(s.ccs + col + c0 + nc);
-      for (int tb = t0; tb < t1; tb += 32) {
-        const int tt = tb + lane;
-        bool hit = false;
-        int j = 0;
-        if (tt < t1) {
-          j = (int)__ldg(s.cperm + tt);
-          const uint4 xj = s.xh[j];
-          const float dx = (float)(int)(xi.x - xj.x) * g.scale[0];
-          const float dy = (float)(int)(xi.y - xj.y) * g.scale[1];
-          const float dz = (float)(int)(xi.z - xj.z) * g.scale[2];
-          const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-          const float hj = __uint_as_float(xj.w);
-          hit = r2 < fmaxf(Hi2, (Hfac * hj) * (Hfac * hj));
-          // a partner at exactly i's position (j != i) is skipped
-          if (j != i && xj.x == xi.x && xj.y == xi.y && xj.z == xi.z) hit = false;
+  const int nr = nxc * nyc * 2;
+  for (int rb = 0; rb < nr; rb += 32) {
+    int t0 = 0, len = 0;
+    {
+      const int q = rb + lane;
+      if (q < nr) {
+        const int cq = q >> 1, part = q & 1;
+        const int ax = cq / nyc, ay = cq - ax * nyc;
+        const int ccx = (x0 + ax) % cnx, ccy = (y0 + ay) % cny;
+        const int col = (ccx * cny + ccy) * cnz;
+        const int c0 = part == 0 ? z0 : 0, nc = part == 0 ? run1 : nzc - run1;
+        if (nc > 0) {
+          t0 = __ldg(ccs + col + c0);
+          len = __ldg(ccs + col + c0 + nc) - t0;
         }
-        const unsigned b = __ballot_sync(kFull, hit);
-        const int pos = cnt + __popc(b & ((1u << lane) - 1u));
-        if (hit && pos < s.wlcap) lst[pos] = (uint32_t)j;
-        cnt += __popc(b);
       }
+    }
+    int incl = len;  // inclusive prefix of the lengths over the lanes
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(kFull, incl, 31);
+    for (int base = 0; base < total; base += 32) {
+      const int idx = base + lane;
+      // the range holding idx: the first lane r with incl[r] > idx (binary search by shuffles)
+      int lo = 0;
+#pragma unroll
+      for (int w = 16; w > 0; w >>= 1) {
+        const int v = __shfl_sync(kFull, incl, lo + w - 1);
+        if (v <= idx) lo += w;
+      }
+      const int r0 = __shfl_sync(kFull, t0, lo & 31), e0 = __shfl_sync(kFull, incl - len, lo & 31);
+      bool hit = false;
+      int j = 0;
+      if (idx < total) {
+        j = (int)__ldg(cperm + r0 + (idx - e0));
+        const uint4 xj = s.xh[j];
+        const float dx = (float)(int)(xi.x - xj.x) * g.scale[0];
+        const float dy = (float)(int)(xi.y - xj.y) * g.scale[1];
+        const float dz = (float)(int)(xi.z - xj.z) * g.scale[2];
+        const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+        const float hj = __uint_as_float(xj.w);
+        hit = r2 < fmaxf(Hi2, (Hfac * hj) * (Hfac * hj));
+        // a partner at exactly i's position (j != i) is skipped
+        if (j != i && xj.x == xi.x && xj.y == xi.y && xj.z == xi.z) hit = false;
+      }
+      const unsigned b = __ballot_sync(kFull, hit);
+      const int pos = cnt + __popc(b & ((1u << lane) - 1u));
+      if (hit && pos < s.wlcap) lst[pos] = (uint32_t)j;
+      cnt += __popc(b);
     }
   }
   if (lane == 0) {
@@ -365,7 +403,7 @@ __global__ void __launch_bounds__(256) k_wide_force(DevGrid g, DevPhys ph, DevSt
     if (jwide) {  // j's search: the coarse cells meeting its grid-cell box (k_wide_lists)
       const int kx = px ? reach(Rj, g.side[0], g.nx) : (int)ceilf(Rj / g.side[0]), ky = reach(Rj, g.side[1], g.ny),
                 kz = reach(Rj, g.side[2], g.nz);
-      const int F = s.cF;
+      const int F = s.cF[coarse_level(s, kx, ky, kz)];
       seen = coarse_meets(cxi / F, cxj - kx, kx, g.nx, F, px) && coarse_meets(cyi / F, cyj - ky, ky, g.ny, F) &&
              coarse_meets(czi / F, czj - kz, kz, g.nz, F);
     } else {
@@ -407,12 +445,11 @@ cudaError_t launch_mark_wide(int n, const DevGrid& g, const DevPhys& ph, const D
   return cudaGetLastError();
 }
 
-cudaError_t launch_coarse_keys(int n, int i0, const DevGrid& g, const DevState& s, unsigned int* keys,
+cudaError_t launch_coarse_keys(int n, int level, const DevGrid& g, const DevState& s, unsigned int* keys,
                                unsigned int* vals, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  (void)i0;
-  if (g.periodic_x) k_coarse_keys<true><<<(n + 255) / 256, 256, 0, st>>>(n, g, s, keys, vals);
-  else k_coarse_keys<false><<<(n + 255) / 256, 256, 0, st>>>(n, g, s, keys, vals);
+  if (g.periodic_x) k_coarse_keys<true><<<(n + 255) / 256, 256, 0, st>>>(n, level, g, s, keys, vals);
+  else k_coarse_keys<false><<<(n + 255) / 256, 256, 0, st>>>(n, level, g, s, keys, vals);
   return cudaGetLastError();
 }
 

@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define SPH_ABI_VERSION 3
+#define SPH_ABI_VERSION 4
 
 typedef enum {
   SPH_OK = 0,
@@ -242,6 +242,23 @@ sph_status sph_kick_drift(sph_ctx* ctx, float dt_kick, float dt_drift);
  * or device memory.  dst must hold n x components elements of the field's type (several
  * ranks: the owned particles in local order, n = sph_local_count). */
 sph_status sph_get(sph_ctx* ctx, int field, void* dst, int on_device);
+
+/* Pipelined host I/O (a host loop that uploads step k+1 while step k computes and reads step
+ * k's results back while step k+1 computes; bench.py's e2e).  Copies run on the context's
+ * two copy streams (host-to-device, device-to-host), never on the context stream.
+ * sph_stage_particles: enqueue the host -> device copy of every array of `in` (on_device must
+ *   be 0; page-locked memory for real overlap) into the context's staging buffers and return;
+ *   the copy waits until the previous staged upload has been taken by
+ *   sph_set_particles_staged.  The host arrays must stay unchanged until the copy is done
+ *   (sph_synchronize, or the next sph_set_particles_staged has returned).
+ * sph_set_particles_staged: sph_set_particles from the last staged upload (the context
+ *   stream waits for its copy; SPH_ERR_STATE if nothing is staged).
+ * sph_get_async: sph_get into host memory `dst`, the device -> host copy enqueued after the
+ *   work enqueued so far; `dst` is written by the next sph_synchronize (at most 8 reads in
+ *   flight; a ninth waits for the oldest). */
+sph_status sph_stage_particles(sph_ctx* ctx, const sph_particles_in* in);
+sph_status sph_set_particles_staged(sph_ctx* ctx);
+sph_status sph_get_async(sph_ctx* ctx, int field, void* dst);
 
 /* Particles owned by this rank (= n for one rank); -1 for NULL. */
 int64_t sph_local_count(const sph_ctx* ctx);

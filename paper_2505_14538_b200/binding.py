@@ -82,7 +82,8 @@ class Counters(ctypes.Structure):
 EXPORTS = ["sph_abi_version", "sph_config_default", "sph_create", "sph_set_particles", "sph_rebuild_cells",
            "sph_density", "sph_gradient", "sph_force", "sph_kick_drift", "sph_get", "sph_get_counters",
            "sph_synchronize", "sph_last_error", "sph_destroy", "sph_local_count", "sph_nccl_unique_id",
-           "sph_loopback_create", "sph_loopback_destroy", "sph_set_timing", "sph_get_timings"]
+           "sph_loopback_create", "sph_loopback_destroy", "sph_set_timing", "sph_get_timings",
+           "sph_stage_particles", "sph_set_particles_staged", "sph_get_async"]
 
 _lib = None
 
@@ -106,6 +107,9 @@ def lib():
         L.sph_force.argtypes = [P, ctypes.POINTER(ctypes.c_float)]
         L.sph_kick_drift.argtypes = [P, ctypes.c_float, ctypes.c_float]
         L.sph_get.argtypes = [P, ctypes.c_int, P, ctypes.c_int]
+        L.sph_stage_particles.argtypes = [P, ctypes.POINTER(ParticlesIn)]
+        L.sph_set_particles_staged.argtypes = [P]
+        L.sph_get_async.argtypes = [P, ctypes.c_int, P]
         L.sph_get_counters.argtypes = [P, ctypes.POINTER(Counters)]
         L.sph_synchronize.argtypes = [P]
         L.sph_last_error.argtypes = [P]
@@ -243,6 +247,23 @@ class Context:
         keep = []
         pin = particles_in(particles, keep)
         self._check(lib().sph_set_particles(self.h, ctypes.byref(pin)), "sph_set_particles")
+
+    def stage_particles(self, particles):
+        """sph_stage_particles: asynchronous upload of host arrays (keep them unchanged until
+        the copy is done: the next set_particles_staged or synchronize)."""
+        self._stage_keep = []
+        pin = particles_in(particles, self._stage_keep)
+        self._check(lib().sph_stage_particles(self.h, ctypes.byref(pin)), "sph_stage_particles")
+
+    def set_particles_staged(self):
+        self._check(lib().sph_set_particles_staged(self.h), "sph_set_particles_staged")
+
+    def get_async(self, field, out):
+        """sph_get_async into host memory (a numpy array or a pinned torch tensor of the field's
+        shape), written by the next synchronize."""
+        ptr = out.data_ptr() if _is_torch(out) else out.ctypes.data
+        self._check(lib().sph_get_async(self.h, FIELDS[field][0], ptr), "sph_get_async")
+        return out
 
     def rebuild_cells(self):
         self._check(lib().sph_rebuild_cells(self.h), "sph_rebuild_cells")

@@ -354,6 +354,19 @@ struct sph_ctx {
   cudaEvent_t ev_main = nullptr, ev_x2 = nullptr, ev_x3 = nullptr;
   // halo put (sph_config.halo_put): the neighbours' fr1 / fr2 buffers mapped into this process
   // ([0] left, [1] right), so the gradient epilogue stores X3's ghost records there itself
+  // pipelined host I/O (sph_stage_particles / sph_set_particles_staged / sph_get_async)
+  static constexpr int kGetSlots = 8;
+  cudaStream_t hstream = nullptr, dstream = nullptr;  // host -> device, device -> host copies
+  cudaEvent_t ev_staged = nullptr, ev_stage_free = nullptr;
+  void* stage_buf = nullptr;
+  size_t stage_bytes = 0;
+  sph_particles_in staged{};
+  bool has_staged = false, stage_used = false;
+  void* gbuf[kGetSlots] = {};
+  size_t gbuf_bytes[kGetSlots] = {};
+  bool gused[kGetSlots] = {};
+  cudaEvent_t ev_gready[kGetSlots] = {}, ev_gfree[kGetSlots] = {};
+  int gnext = 0;
   bool halo_put = false;
   float4* peer_fr1[2] = {nullptr, nullptr};
   float4* peer_fr2[2] = {nullptr, nullptr};
@@ -1978,10 +1991,12 @@ sph_status sph_kick_drift(sph_ctx* c, float dt_kick, float dt_drift) {
   return SPH_OK;
 }
 
-sph_status sph_get(sph_ctx* c, int field, void* dst, int on_device) {
-  GUARD(c);
-  if (join_comm(c) != SPH_OK) return SPH_ERR_CUDA;  // (pending halo exchanges)
-  if (!dst) return fail(c, SPH_ERR_INVALID_ARG, "dst is NULL");
+}  // extern "C"
+
+namespace {
+// Gather one field of the owned particles (caller order on one rank) into device memory d
+// (sph_get / sph_get_async); *bytes = its size.  d = nullptr: size only.
+sph_status gather_field(sph_ctx* c, int field, void* d, size_t* bytes) {
   const DevState& s = c->s;
   const void* src = nullptr;
   int stride = 1, off = 0, comps = 1, wide = 0;
@@ -2019,9 +2034,42 @@ sph_status sph_get(sph_ctx* c, int field, void* dst, int on_device) {
   // (cell) order -- SPH_F_ID maps them to the caller's ids
   const int n = c->n_own;
   const int32_t* orig = c->nranks == 1 ? s.orig + c->gL : nullptr;
-  const size_t esz = wide ? 8 : 4;
-  const size_t bytes = (size_t)n * comps * esz;
-  if (n == 0) return SPH_OK;
+  *bytes = (size_t)n * comps * (wide ? 8 : 4);
+  if (n == 0 || !d) return SPH_OK;
+  if (wide)
+    k_scatter64<<<nblk(n, 256), 256, 0, c->stream>>>(n, (const uint64_t*)src + c->gL, orig, (uint64_t*)d);
+  else
+    k_scatter32<<<nblk(n, 256), 256, 0, c->stream>>>(n, (const uint32_t*)src + (size_t)c->gL * stride, stride, off,
+                                                     comps, orig, (uint32_t*)d);
+  c->launches++;
+  CK(cudaGetLastError());
+  return SPH_OK;
+}
+
+// the copy streams and events of the pipelined host I/O (created on first use)
+sph_status ensure_io(sph_ctx* c) {
+  if (c->hstream) return SPH_OK;
+  CK(cudaStreamCreateWithFlags(&c->hstream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&c->dstream, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&c->ev_staged, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_stage_free, cudaEventDisableTiming));
+  for (int k = 0; k < sph_ctx::kGetSlots; ++k) {
+    CK(cudaEventCreateWithFlags(&c->ev_gready[k], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_gfree[k], cudaEventDisableTiming));
+  }
+  return SPH_OK;
+}
+}  // namespace
+
+extern "C" {
+
+sph_status sph_get(sph_ctx* c, int field, void* dst, int on_device) {
+  GUARD(c);
+  if (join_comm(c) != SPH_OK) return SPH_ERR_CUDA;  // (pending halo exchanges)
+  if (!dst) return fail(c, SPH_ERR_INVALID_ARG, "dst is NULL");
+  size_t bytes = 0;
+  sph_status st = gather_field(c, field, nullptr, &bytes);
+  if (st != SPH_OK || bytes == 0) return st;
   void* d = dst;
   if (!on_device) {
     if (c->out_tmp_bytes < bytes) {
@@ -2033,18 +2081,100 @@ sph_status sph_get(sph_ctx* c, int field, void* dst, int on_device) {
     }
     d = c->out_tmp;
   }
-  if (wide)
-    k_scatter64<<<nblk(n, 256), 256, 0, c->stream>>>(n, (const uint64_t*)src + c->gL, orig, (uint64_t*)d);
-  else
-    k_scatter32<<<nblk(n, 256), 256, 0, c->stream>>>(n, (const uint32_t*)src + (size_t)c->gL * stride, stride, off,
-                                                     comps, orig, (uint32_t*)d);
-  c->launches++;
-  CK(cudaGetLastError());
+  if ((st = gather_field(c, field, d, &bytes)) != SPH_OK) return st;
   if (!on_device) {
     CK(cudaMemcpyAsync(dst, d, bytes, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
   }
   return SPH_OK;
+}
+
+sph_status sph_get_async(sph_ctx* c, int field, void* dst) {
+  GUARD(c);
+  if (join_comm(c) != SPH_OK) return SPH_ERR_CUDA;
+  if (!dst) return fail(c, SPH_ERR_INVALID_ARG, "dst is NULL");
+  sph_status st;
+  if ((st = ensure_io(c)) != SPH_OK) return st;
+  size_t bytes = 0;
+  if ((st = gather_field(c, field, nullptr, &bytes)) != SPH_OK || bytes == 0) return st;
+  const int k = c->gnext;
+  c->gnext = (c->gnext + 1) % sph_ctx::kGetSlots;
+  if (c->gbuf_bytes[k] < bytes) {
+    if (c->gbuf[k]) cudaFree(c->gbuf[k]);  // (synchronises the device: the slot's copy is done)
+    c->gbuf[k] = nullptr;
+    c->gbuf_bytes[k] = 0;
+    CK(cudaMalloc(&c->gbuf[k], bytes));
+    c->gbuf_bytes[k] = bytes;
+  } else if (c->gused[k]) {
+    CK(cudaStreamWaitEvent(c->stream, c->ev_gfree[k], 0));  // the slot's previous copy is done
+  }
+  if ((st = gather_field(c, field, c->gbuf[k], &bytes)) != SPH_OK) return st;
+  CK(cudaEventRecord(c->ev_gready[k], c->stream));
+  CK(cudaStreamWaitEvent(c->dstream, c->ev_gready[k], 0));
+  CK(cudaMemcpyAsync(dst, c->gbuf[k], bytes, cudaMemcpyDeviceToHost, c->dstream));
+  CK(cudaEventRecord(c->ev_gfree[k], c->dstream));
+  c->gused[k] = true;
+  return SPH_OK;
+}
+
+sph_status sph_stage_particles(sph_ctx* c, const sph_particles_in* in) {
+  GUARD(c);
+  if (!in || !in->X || !in->v || !in->m || !in->u || !in->h)
+    return fail(c, SPH_ERR_INVALID_ARG, "required particle array is NULL");
+  if (in->on_device) return fail(c, SPH_ERR_INVALID_ARG, "sph_stage_particles takes host arrays");
+  if (in->n < 0 || (c->nranks == 1 && in->n != c->n_in) || in->n > c->cap)
+    return fail(c, SPH_ERR_INVALID_ARG, "particle count mismatch / above capacity");
+  sph_status st;
+  if ((st = ensure_io(c)) != SPH_OK) return st;
+  const size_t n = (size_t)in->n;
+  auto al = [](size_t b) { return (b + 15) & ~size_t(15); };
+  const size_t bytes = al(12 * n) * 2 + al(4 * n) * 3 + (in->alpha_v ? al(4 * n) : 0) + (in->alpha_c ? al(4 * n) : 0) +
+                       (in->div_prev ? al(4 * n) : 0) + (in->id ? al(8 * n) : 0) + 16;
+  if (c->stage_bytes < bytes) {
+    if (c->stage_buf) cudaFree(c->stage_buf);  // (synchronises the device: no copy or ingest reads it)
+    c->stage_buf = nullptr;
+    c->stage_bytes = 0;
+    CK(cudaMalloc(&c->stage_buf, bytes));
+    c->stage_bytes = bytes;
+  } else if (c->stage_used) {
+    CK(cudaStreamWaitEvent(c->hstream, c->ev_stage_free, 0));  // the last staged upload was taken
+  }
+  char* d = static_cast<char*>(c->stage_buf);
+  auto up = [&](const void* src, size_t b) -> void* {
+    if (!src) return nullptr;
+    void* dst = d;
+    cudaMemcpyAsync(dst, src, b, cudaMemcpyHostToDevice, c->hstream);
+    d += al(b);
+    return dst;
+  };
+  sph_particles_in& sp = c->staged;
+  sp = *in;
+  sp.on_device = 1;
+  sp.X = (const uint32_t*)up(in->X, 12 * n);
+  sp.v = (const float*)up(in->v, 12 * n);
+  sp.m = (const float*)up(in->m, 4 * n);
+  sp.u = (const float*)up(in->u, 4 * n);
+  sp.h = (const float*)up(in->h, 4 * n);
+  sp.alpha_v = (const float*)up(in->alpha_v, 4 * n);
+  sp.alpha_c = (const float*)up(in->alpha_c, 4 * n);
+  sp.div_prev = (const float*)up(in->div_prev, 4 * n);
+  sp.id = (const int64_t*)up(in->id, 8 * n);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(c->ev_staged, c->hstream));
+  c->has_staged = true;
+  return SPH_OK;
+}
+
+sph_status sph_set_particles_staged(sph_ctx* c) {
+  GUARD(c);
+  if (!c->has_staged) return fail(c, SPH_ERR_STATE, "sph_set_particles_staged: nothing staged");
+  if (join_comm(c) != SPH_OK) return SPH_ERR_CUDA;  // (pending halo exchanges)
+  CK(cudaStreamWaitEvent(c->stream, c->ev_staged, 0));
+  const sph_status st = ingest(c, &c->staged);
+  CK(cudaEventRecord(c->ev_stage_free, c->stream));
+  c->has_staged = false;
+  c->stage_used = true;
+  return st;
 }
 
 int64_t sph_local_count(const sph_ctx* c) { return c ? (int64_t)c->n_own : -1; }
@@ -2065,6 +2195,8 @@ sph_status sph_synchronize(sph_ctx* c) {
   GUARD(c);
   if (join_comm(c) != SPH_OK) return SPH_ERR_CUDA;
   CK(cudaStreamSynchronize(c->stream));
+  if (c->hstream) CK(cudaStreamSynchronize(c->hstream));
+  if (c->dstream) CK(cudaStreamSynchronize(c->dstream));
   return SPH_OK;
 }
 
@@ -2108,6 +2240,19 @@ sph_status sph_destroy(sph_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->cstream) cudaStreamSynchronize(c->cstream);
+  for (cudaStream_t x : {c->hstream, c->dstream})
+    if (x) {
+      cudaStreamSynchronize(x);
+      cudaStreamDestroy(x);
+    }
+  for (cudaEvent_t e : {c->ev_staged, c->ev_stage_free})
+    if (e) cudaEventDestroy(e);
+  for (int k = 0; k < sph_ctx::kGetSlots; ++k) {
+    if (c->ev_gready[k]) cudaEventDestroy(c->ev_gready[k]);
+    if (c->ev_gfree[k]) cudaEventDestroy(c->ev_gfree[k]);
+    if (c->gbuf[k]) cudaFree(c->gbuf[k]);
+  }
+  if (c->stage_buf) cudaFree(c->stage_buf);
   DevState& s = c->s;
   void* ptrs[] = {s.xh, s.vm, s.u, s.av, s.ac, s.dprev, s.uid, s.orig, s.acc, c->alt.xh, c->alt.vm, c->alt.u,
                   c->alt.av, c->alt.ac, c->alt.dprev, c->alt.uid, c->alt.orig, c->alt.acc, s.dens, s.dvc, s.count,

@@ -1,6 +1,7 @@
 """Small runs of every kernel path for compute-sanitizer (tools/sanitize.sh): the tile loops on a
 jittered lattice, the adaptive grid with wide particles (Sedov), coincident particles, a KDK step
-with a rebuild, and the two-rank slab path over the loopback transport."""
+with a rebuild, the pipelined host I/O, and the two-rank slab path over the loopback transport (halo
+put: the loop epilogues' peer stores into the other rank's ghost slots)."""
 import os
 import sys
 import threading
@@ -55,7 +56,27 @@ def two_ranks(p):
         raise errs[0]
 
 
+def pipelined(p):
+    """The pipelined host I/O: staged uploads and asynchronous read-backs over two passes."""
+    import numpy as np
+
+    ctx = Context(p)
+    a = np.zeros((p["X"].shape[0], 3), np.float32)
+    ctx.stage_particles(p)
+    for k in range(2):
+        ctx.set_particles_staged()
+        if k == 0:
+            ctx.stage_particles(p)
+        ctx.density()
+        ctx.gradient(1e-3)
+        ctx.force()
+        ctx.get_async("a", a)
+    ctx.synchronize()
+    ctx.close()
+
+
 hydro(W.jittered_lattice(12, seed=3, vel_sigma=0.05, u_sigma=0.2), steps=1)
+pipelined(W.jittered_lattice(10, seed=9, vel_sigma=0.05, u_sigma=0.2))
 hydro(W.sedov(20))
 hydro(W.with_duplicates(W.poisson(1500, seed=5), 0.05))
 two_ranks(W.jittered_lattice(16, seed=4, vel_sigma=0.05, u_sigma=0.2))

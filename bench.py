@@ -87,6 +87,8 @@ def parse():
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--tile-z", type=int, default=0, help="cells per CTA block along z (0 = auto)")
     ap.add_argument("--skin", type=float, default=None, help="cell_skin (default: the library's)")
+    ap.add_argument("--balance", action="store_true",
+                    help="several ranks: move the slab cuts toward equal particle counts at every rebuild")
     ap.add_argument("--halo-put", type=int, default=-1, choices=[-1, 0, 1],
                     help="X2/X3 halos by peer stores from the loop epilogues (1), NCCL send/recv (0), "
                          "or the library default (-1: send/recv over several NCCL ranks)")
@@ -311,6 +313,8 @@ def run_ours(args, world, rank, local):
         multi["cell_skin"] = args.skin
     if world > 1 and args.halo_put >= 0:
         multi["halo_put"] = args.halo_put
+    if world > 1 and args.balance:
+        multi["balance"] = 1
     ctx = Context(p, stream=stream.cuda_stream, device=local, **multi)
     dt = 1e-4
 

@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define SPH_ABI_VERSION 4
+#define SPH_ABI_VERSION 5
 
 typedef enum {
   SPH_OK = 0,
@@ -111,6 +111,12 @@ typedef struct {
                           /* the planes after the loop; -1 (default) = 1 for loopback and one   */
                           /* rank, 0 for NCCL over several ranks (not yet run on multi-GPU      */
                           /* hardware).  DESIGN.md §9.                                          */
+  int32_t balance;        /* slab cuts (several ranks): 0 (default) = fixed, rank r owns          */
+                          /* [floor(r 2^32 / R), floor((r+1) 2^32 / R)); 1 = every rebuild moves */
+                          /* each cut toward equal owned-particle counts (a global histogram of  */
+                          /* x, at most a quarter of a cell plane per rebuild so migrants stay   */
+                          /* within one plane; slabs kept >= half the uniform width) -- the 1-D  */
+                          /* orthogonal recursive bisection of the slab path       */
 } sph_config;
 
 /* Particle input.  n particles; arrays are host pointers (on_device = 0) or device

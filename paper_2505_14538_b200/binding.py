@@ -49,7 +49,8 @@ class Config(ctypes.Structure):
                 ("stream", ctypes.c_void_p), ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
                 ("tile_cells_z", ctypes.c_int32), ("predict_h", ctypes.c_int32), ("transport", ctypes.c_int32),
                 ("nccl_uid", ctypes.c_void_p), ("loopback", ctypes.c_void_p), ("adaptive_h", ctypes.c_int32),
-                ("decomp", ctypes.c_int32 * 3), ("halo_put", ctypes.c_int32)]
+                ("decomp", ctypes.c_int32 * 3), ("halo_put", ctypes.c_int32),
+                ("balance", ctypes.c_int32)]
 
 SPH_TRANSPORT_NCCL, SPH_TRANSPORT_LOOPBACK = 0, 1
 

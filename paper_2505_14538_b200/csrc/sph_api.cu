@@ -45,6 +45,12 @@ __global__ void k_hmax(int n, const uint4* __restrict__ xh, unsigned int* out) {
   if ((threadIdx.x & 31) == 0) atomicMax(out, m);  // positive f32 order as u32
 }
 
+// histogram of the owned particles' x over nb equal bins of the box (balanced slab cuts)
+__global__ void k_xhist(int n, const uint4* __restrict__ xh, int nb, unsigned int* hist) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    atomicAdd(&hist[(int)(((unsigned long long)xh[i].x * (unsigned)nb) >> 32)], 1u);
+}
+
 // ghost planes the owned particle needs (ghost_planes_needed) for a list radius Hfac h; a
 // particle that left the slab counts at its nearest owned plane
 __global__ void k_ghost_need(int n, const uint4* __restrict__ xh, DevGrid g, float Hfac, unsigned int* out) {
@@ -368,6 +374,10 @@ struct sph_ctx {
   cudaEvent_t ev_gready[kGetSlots] = {}, ev_gfree[kGetSlots] = {};
   int gnext = 0;
   bool halo_put = false;
+  // slab cuts on the 2^-32 grid: rank r owns [cut[r], cut[r+1]) (sph_config.balance moves them)
+  std::vector<unsigned long long> cut;
+  bool balance = false;
+  unsigned int* xhist = nullptr;  // [kHistBins] device histogram of x (balance)
   float4* peer_fr1[2] = {nullptr, nullptr};
   float4* peer_fr2[2] = {nullptr, nullptr};
   float4* peer_gq[2] = {nullptr, nullptr};
@@ -882,6 +892,52 @@ sph_status rebuild(sph_ctx* c) {
   return mark_wide(c);
 }
 
+// Balanced slab cuts (sph_config.balance): a global histogram of the owned particles' x
+// (kHistBins bins, device-side SUM allreduce, one read-back), and every cut r moved toward the x
+// where the cumulative count reaches r N / R (linear inside its bin) -- by at most a quarter of
+// the thinner adjacent slab's cell plane, so that migrants stay within one ghost plane, and
+// keeping every slab at least half the uniform width.  Every rank computes the same cuts from
+// the same histogram.
+constexpr int kHistBins = 4096;
+sph_status rebalance_cuts(sph_ctx* c, int base, int n) {
+  const int R = c->nranks;
+  if (!c->xhist) CK(cudaMalloc(&c->xhist, kHistBins * sizeof(unsigned int)));
+  CK(cudaMemsetAsync(c->xhist, 0, kHistBins * sizeof(unsigned int), c->stream));
+  if (n > 0) {
+    k_xhist<<<std::min(nblk(n, 256), 1184), 256, 0, c->stream>>>(n, c->s.xh + base, kHistBins, c->xhist);
+    c->launches++;
+  }
+  CK(cudaGetLastError());
+  sph_status st = allreduce_dev(c, c->xhist, kHistBins, kSum);
+  if (st != SPH_OK) return st;
+  std::vector<unsigned int> h(kHistBins);
+  CK(cudaMemcpyAsync(h.data(), c->xhist, kHistBins * sizeof(unsigned int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  double tot = 0.0;
+  for (unsigned int v : h) tot += v;
+  if (!(tot > 0.0)) return SPH_OK;
+  const double two32 = std::ldexp(1.0, 32), bw = two32 / kHistBins;
+  const long long wmin = (long long)((two32 / R) / 2);
+  std::vector<unsigned long long> cut = c->cut;
+  double cum = 0.0;
+  int b = 0;
+  for (int r = 1; r < R; ++r) {
+    const double target = tot * r / R;
+    while (b < kHistBins - 1 && cum + h[b] < target) cum += h[b++];
+    const double frac = h[b] > 0 ? (target - cum) / h[b] : 0.5;
+    const double want = (b + std::min(1.0, std::max(0.0, frac))) * bw;
+    const double wl = (double)(c->cut[r] - c->cut[r - 1]), wr = (double)(c->cut[r + 1] - c->cut[r]);
+    const double step = 0.25 * std::min(wl, wr) / std::max(c->grid.nxo, 1);
+    const double d = std::min(step, std::max(-step, want - (double)c->cut[r]));
+    long long nc = (long long)c->cut[r] + (long long)d;
+    nc = std::max(nc, (long long)cut[r - 1] + wmin);  // (the left neighbour's cut already moved)
+    nc = std::min(nc, (long long)c->cut[r + 1] - wmin);
+    cut[r] = (unsigned long long)std::max(nc, (long long)cut[r - 1] + 1);
+  }
+  c->cut = cut;
+  return SPH_OK;
+}
+
 sph_status rebuild_impl(sph_ctx* c) {
   // SPH_DEBUG: elapsed ms at the stages of the rebuild (synchronising)
   const bool dbg = getenv("SPH_DEBUG") != nullptr;
@@ -918,7 +974,10 @@ sph_status rebuild_impl(sph_ctx* c) {
   const bool slab = c->slab;
   // slab of this rank on the 2^-32 grid (fixed by position, independent of h)
   const double two32 = std::ldexp(1.0, 32);
-  auto slab_lo = [&](int r) { return (unsigned long long)(((unsigned __int128)r << 32) / (unsigned)R); };
+  if (slab && R > 1 && c->balance && c->grid.nxo > 0) {
+    if ((st = rebalance_cuts(c, base, n)) != SPH_OK) return st;
+  }
+  auto slab_lo = [&](int r) { return c->cut[r]; };
   unsigned long long wmin = ~0ull;
   for (int r = 0; r < R; ++r) wmin = std::min(wmin, slab_lo(r + 1) - slab_lo(r));
   g.x_lo = (unsigned int)slab_lo(c->rank);
@@ -1709,6 +1768,10 @@ sph_status sph_create(const sph_config* cfg, const sph_particles_in* in, sph_ctx
   if (const char* m = getenv("SPH_SPARSE_WIDE")) c->sparse_wide = std::max(0, atoi(m));
   if (const char* m = getenv("SPH_COARSE_Q")) c->coarse_q = std::min(1.0, std::max(0.01, atof(m)));
   if (const char* m = getenv("SPH_COARSE_LEVELS")) c->coarse_levels = std::min(kCoarseLevels, std::max(1, atoi(m)));
+  c->cut.resize(c->nranks + 1);
+  for (int r = 0; r <= c->nranks; ++r)
+    c->cut[r] = (unsigned long long)(((unsigned __int128)r << 32) / (unsigned)c->nranks);
+  c->balance = cfg->balance != 0;
   if ((st = alloc_state(c)) != SPH_OK) return bail(st);
   if (c->slab) {
     c->halo_put = cfg->halo_put == 1 ||
@@ -2263,7 +2326,7 @@ sph_status sph_destroy(sph_ctx* c) {
                   c->n_wide_dev, c->wnbr, c->sel_tmp, c->desc_buf, c->pref_buf,
                   c->act_flag, c->blk_list, c->run_list, c->cperm[0], c->cperm[1], c->cperm[2], c->ccs[0],
                   c->ccs[1], c->ccs[2], s.dup, c->side_flag, c->side_list,
-                  s.vc, s.um, c->hin};
+                  s.vc, s.um, c->hin, c->xhist};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->ctr_h) cudaFreeHost(c->ctr_h);

@@ -295,17 +295,17 @@ class LoopComm : public Comm {
   }
   // (one process: through the host, exactly as allreduce)
   std::string allreduce_dev_u32(uint32_t* d, int n, ReduceOp op, cudaStream_t st) override {
-    if (n > 64) return "allreduce: too many values";
-    uint32_t h[64];
-    double v[64];
-    if (cudaMemcpyAsync(h, d, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    std::vector<uint32_t> h(n);
+    std::vector<double> v(n);
+    if (cudaMemcpyAsync(h.data(), d, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, st) != cudaSuccess)
       return "allreduce: D2H failed";
     if (cudaStreamSynchronize(st) != cudaSuccess) return "allreduce: sync failed";
     for (int k = 0; k < n; ++k) v[k] = (double)h[k];
-    std::string e = allreduce(v, n, op, st);
+    std::string e = allreduce(v.data(), n, op, st);
     if (!e.empty()) return e;
     for (int k = 0; k < n; ++k) h[k] = (uint32_t)v[k];
-    if (cudaMemcpy(d, h, n * sizeof(uint32_t), cudaMemcpyHostToDevice) != cudaSuccess) return "allreduce: H2D failed";
+    if (cudaMemcpy(d, h.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice) != cudaSuccess)
+      return "allreduce: H2D failed";
     return "";
   }
 

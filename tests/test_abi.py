@@ -42,7 +42,7 @@ def test_library_exports_every_declared_symbol(sphlib):
     L = sphlib.lib()
     for n in declared_functions():
         assert hasattr(L, n)
-    assert L.sph_abi_version() == 4
+    assert L.sph_abi_version() == 5
 
 
 def test_struct_layout_matches_header(sphlib, tmp_path):

@@ -224,6 +224,42 @@ def test_multirank_kdk_migration():
     assert abs(parts[0]["dt"] - ref["dt"]) <= 1e-4 * ref["dt"]
 
 
+def test_multirank_balanced_slabs():
+    """sph_config.balance (the 1-D ORB of the slab path): with two thirds of the
+    particles in x < 1/2 the fixed slabs own 44 / 33 / 22 % of them; every rebuild moves the
+    cuts toward equal counts (a quarter plane at a time), particles migrate across the moving
+    cuts, and the run still tracks the single-context run."""
+    from paper_2505_14538_b200 import Context
+
+    p = _switches(W.poisson(24000, seed=67, vel_sigma=0.02, u_sigma=0.2), 6)
+    x = p["X"][:, 0].astype(np.float64) / 2.0 ** 32
+    xs = np.where(x < 2.0 / 3.0, 0.75 * x, 0.5 + 1.5 * (x - 2.0 / 3.0))  # density 4/3 left, 2/3 right
+    p["X"] = p["X"].copy()
+    p["X"][:, 0] = np.minimum(np.floor(xs * 2.0 ** 32), 2.0 ** 32 - 1).astype(np.uint32)
+    steps = 8
+    kdk = _kdk(steps, [])
+
+    def prog(ctx):
+        n_start = ctx.n  # (the creation's rebuild keeps the fixed cuts)
+        out = kdk(ctx)
+        out["n_start"] = n_start
+        return out
+
+    g, parts = run_ranks(p, 3, prog, h_tol=1e-5, balance=1)
+    n0 = [q["n_start"] for q in parts]
+    n1 = [q["n_local"] for q in parts]
+    assert sum(n1) == p["X"].shape[0]
+    assert max(n0) > 10000 and max(n1) < 8400, (n0, n1)  # 44 / 33 / 22 % -> about a third each
+    ctx = Context(p, h_tol=1e-5)
+    ref = _kdk(steps, [])(ctx)
+    X1, rho1 = ctx.get("X"), ctx.get("rho")
+    ctx.close()
+    dX = (g["X"].astype(np.int64) - X1.astype(np.int64) + 2 ** 31) % 2 ** 32 - 2 ** 31
+    assert np.abs(dX).max() < 2 ** 32 * 1e-6, "positions drifted apart"
+    assert_close("rho", g["rho"], rho1, rtol=1e-4)
+    assert abs(parts[0]["dt"] - ref["dt"]) <= 1e-4 * ref["dt"]
+
+
 def test_multirank_too_thin_slab_is_an_error():
     """Two ranks need two planes each (ghost planes distinct): explicit error, no hang."""
     from paper_2505_14538_b200 import SphError

@@ -515,6 +515,16 @@ def run_e2e(ctx, p, torch, dev, stream, K, world):
     ctx.synchronize()
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
+    # (untimed) where an e2e step's device time goes: two more pipelined steps with the
+    # library's per-launch events
+    ctx.set_timing(True)
+    ctx.timings(reset=True)
+    ctx.stage_particles(hin)
+    for k in range(2):
+        one(k == 1)
+    ctx.synchronize()
+    phases = {name: round(ms / 2, 3) for name, (ms, cnt) in ctx.timings(reset=True).items() if cnt}
+    ctx.set_timing(False)
     if world > 1:
         import torch.distributed as dist
 
@@ -524,7 +534,7 @@ def run_e2e(ctx, p, torch, dev, stream, K, world):
         dist.all_reduce(ts)
         dt, inter = float(tm.item()), float(ts.item())
     return {"value": inter / dt, "unit": "interactions/s", "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * dt / K,
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * dt / K, "device_ms_per_step": phases,
             "note": "host-timed (perf_counter) over K pipelined steps through the C-ABI: each step uploads its "
                     "inputs from pinned host memory (sph_stage_particles, overlapping the previous step's "
                     "hydro pass) and reads a, du/dt back (sph_get_async, overlapping the next step); "

@@ -196,6 +196,83 @@ __global__ void k_pack_mig(int n, const unsigned int* __restrict__ perm, Persist
   out[p] = r;
 }
 
+__global__ void k_set_u32(unsigned int* p, unsigned int v) { *p = v; }
+
+// Zero n bytes (memsets of the context stream as a kernel: a cudaMemsetAsync can queue on the
+// copy engines behind a pipelined upload, see copy_chunked)
+__global__ void k_zero(uint8_t* p, size_t n) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t head = (16 - ((uintptr_t)p & 15)) & 15;
+  if (head >= n) {
+    for (; i < n; i += stride) p[i] = 0;
+    return;
+  }
+  const size_t n16 = (n - head) / 16;
+  uint4* p4 = reinterpret_cast<uint4*>(p + head);
+  for (size_t k = i; k < n16; k += stride) p4[k] = make_uint4(0u, 0u, 0u, 0u);
+  for (size_t k = i; k < head; k += stride) p[k] = 0;
+  for (size_t k = head + 16 * n16 + i; k < n; k += stride) p[k] = 0;
+}
+__global__ void k_copy_u32(const unsigned int* __restrict__ s, unsigned int* d) { *d = *s; }
+
+// The pipelined host I/O's large copies.  Page-locked, device-mapped host memory is copied by a
+// kernel (loads or stores over PCIe from a few CTAs on the copy stream): the copy engines, which
+// take the copies, memsets and read-backs of every stream in submission order, stay free for the
+// context stream's small operations -- with a 738 MB upload queued on them, those waited up to
+// ~13 ms each (C4 e2e 35.6 to 140 ms per step from run to run; by kernel 41 ms every run: the
+// kernel's PCIe reads reach ~18 GB/s against the copy engines' ~55).  Other host memory goes
+// through cudaMemcpyAsync in pieces of at most 4 MB.  The context stream's own memsets are
+// kernels too (zero_async).
+__global__ void __launch_bounds__(256) k_copy_words(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
+                                                    size_t nw) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t n16 = ((((uintptr_t)src | (uintptr_t)dst) & 15) == 0) ? nw / 4 : 0;
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+  for (; i + 3 * stride < n16; i += 4 * stride) {  // four 16-byte loads in flight per thread
+    const uint4 a = s4[i], b = s4[i + stride], c = s4[i + 2 * stride], e = s4[i + 3 * stride];
+    d4[i] = a;
+    d4[i + stride] = b;
+    d4[i + 2 * stride] = c;
+    d4[i + 3 * stride] = e;
+  }
+  for (; i < n16; i += stride) d4[i] = s4[i];
+  for (size_t w = 4 * n16 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += stride) dst[w] = src[w];
+}
+
+cudaError_t copy_chunked(void* dst, const void* src, size_t b, cudaMemcpyKind kind, cudaStream_t st) {
+  const void* host = kind == cudaMemcpyHostToDevice ? src : dst;
+  cudaPointerAttributes at{};
+  // (uploads by copy engine with SPH_H2D_CE: C4 e2e 41.4 / 65.3 ms against 43.2 / 42.4 by kernel on one box)
+  static const bool h2d_kernel = getenv("SPH_H2D_CE") == nullptr;
+  if ((kind == cudaMemcpyDeviceToHost || h2d_kernel) && b % 4 == 0 && ((uintptr_t)src & 3) == 0 && ((uintptr_t)dst & 3) == 0 &&
+      cudaPointerGetAttributes(&at, host) == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer) {
+    const ptrdiff_t off = static_cast<const char*>(host) - static_cast<const char*>(at.hostPointer);
+    void* mapped = static_cast<char*>(at.devicePointer) + off;
+    const uint32_t* s = static_cast<const uint32_t*>(kind == cudaMemcpyHostToDevice ? mapped : src);
+    uint32_t* d = static_cast<uint32_t*>(kind == cudaMemcpyHostToDevice ? dst : mapped);
+    k_copy_words<<<(unsigned)std::min<size_t>(64, (b / 4 + 1023) / 1024), 256, 0, st>>>(s, d, b / 4);
+    return cudaGetLastError();
+  }
+  cudaGetLastError();  // (cudaPointerGetAttributes on pageable memory)
+  constexpr size_t kPiece = 4u << 20;
+  for (size_t o = 0; o < b; o += kPiece) {
+    const cudaError_t e = cudaMemcpyAsync(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o,
+                                          std::min(kPiece, b - o), kind, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t zero_async(void* p, size_t n, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  const size_t blocks = std::min<size_t>((n / 16 + 255) / 256 + 1, 1184);
+  k_zero<<<(unsigned)blocks, 256, 0, st>>>(static_cast<uint8_t*>(p), n);
+  return cudaGetLastError();
+}
+
 // Halo put (X2): the ghosts' final h, stored into hin by the neighbours' density epilogues,
 // into the ghost positions' h (after the token; ghost slots [0, gL) and [gL + n_own, + gR)).
 __global__ void k_ghost_h(int gL, int n_own, int gR, const float* __restrict__ hin, uint4* xh) {
@@ -650,13 +727,13 @@ sph_status ingest(sph_ctx* c, const sph_particles_in* in) {
 }
 
 sph_status sync_ctr(sph_ctx* c) {
-  CK(cudaMemcpyAsync(c->ctr_h, c->ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, c->stream));
+  CK(copy_chunked(c->ctr_h, c->ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   return SPH_OK;
 }
 
 sph_status reset_ctr(sph_ctx* c) {
-  CK(cudaMemsetAsync(c->ctr, 0, sizeof(DevCounters), c->stream));
+  CK(zero_async(c->ctr, sizeof(DevCounters), c->stream));
   return SPH_OK;
 }
 
@@ -679,7 +756,7 @@ sph_status exchange_sizes(sph_ctx* c, long long to_right, long long to_left, lon
   Xfer s[2] = {{right_of(c), c->cnt_dev, 8}, {left_of(c), c->cnt_dev + 1, 8}};
   Xfer r[2] = {{left_of(c), c->cnt_dev + 2, 8}, {right_of(c), c->cnt_dev + 3, 8}};
   CKC(c->comm->exchange(s, 2, r, 2, c->stream));
-  CK(cudaMemcpyAsync(c->cnt_h + 2, c->cnt_dev + 2, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+  CK(copy_chunked(c->cnt_h + 2, c->cnt_dev + 2, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   from_left = c->cnt_h[2];
   from_right = c->cnt_h[3];
@@ -795,7 +872,7 @@ sph_status agree(sph_ctx* c, bool bad, sph_status code, const char* msg) {
 // fills c->perm_alt (sorted -> input index) and the owned-relative cell_start
 sph_status sort_cells(sph_ctx* c, int base, int n, int* outside) {
   DevGrid& g = c->grid;
-  CK(cudaMemsetAsync(c->scratch + 2, 0, 4, c->stream));
+  CK(zero_async(c->scratch + 2, 4, c->stream));
   if (n > 0) {
     k_keys<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->s.xh + base, g, c->keys, c->perm, (int*)(c->scratch + 2));
     c->launches++;
@@ -811,15 +888,17 @@ sph_status sort_cells(sph_ctx* c, int base, int n, int* outside) {
   k_cell_start<<<nblk(n + 1, 256), 256, 0, c->stream>>>(n, g.ncells, g.zbits, c->keys_alt, c->cell_start);
   c->launches++;
   CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(c->scratch_h + 2, c->scratch + 2, 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(copy_chunked(c->scratch_h + 2, c->scratch + 2, 4, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   *outside = (int)c->scratch_h[2];
   return SPH_OK;
 }
 
 sph_status read_cs(sph_ctx* c, int cell, int* v) {
-  CK(cudaMemcpyAsync(c->scratch + 4, c->cell_start + cell, 4, cudaMemcpyDeviceToDevice, c->stream));
-  CK(cudaMemcpyAsync(c->scratch_h + 4, c->scratch + 4, 4, cudaMemcpyDeviceToHost, c->stream));
+  k_copy_u32<<<1, 1, 0, c->stream>>>(reinterpret_cast<const unsigned int*>(c->cell_start + cell),
+                                     reinterpret_cast<unsigned int*>(c->scratch + 4));
+  CK(cudaGetLastError());
+  CK(copy_chunked(c->scratch_h + 4, c->scratch + 4, 4, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   *v = (int)c->scratch_h[4];
   return SPH_OK;
@@ -902,7 +981,7 @@ constexpr int kHistBins = 4096;
 sph_status rebalance_cuts(sph_ctx* c, int base, int n) {
   const int R = c->nranks;
   if (!c->xhist) CK(cudaMalloc(&c->xhist, kHistBins * sizeof(unsigned int)));
-  CK(cudaMemsetAsync(c->xhist, 0, kHistBins * sizeof(unsigned int), c->stream));
+  CK(zero_async(c->xhist, kHistBins * sizeof(unsigned int), c->stream));
   if (n > 0) {
     k_xhist<<<std::min(nblk(n, 256), 1184), 256, 0, c->stream>>>(n, c->s.xh + base, kHistBins, c->xhist);
     c->launches++;
@@ -911,7 +990,7 @@ sph_status rebalance_cuts(sph_ctx* c, int base, int n) {
   sph_status st = allreduce_dev(c, c->xhist, kHistBins, kSum);
   if (st != SPH_OK) return st;
   std::vector<unsigned int> h(kHistBins);
-  CK(cudaMemcpyAsync(h.data(), c->xhist, kHistBins * sizeof(unsigned int), cudaMemcpyDeviceToHost, c->stream));
+  CK(copy_chunked(h.data(), c->xhist, kHistBins * sizeof(unsigned int), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   double tot = 0.0;
   for (unsigned int v : h) tot += v;
@@ -953,7 +1032,7 @@ sph_status rebuild_impl(sph_ctx* c) {
   const int base = c->gL;
   int n = c->n_own;
   // global h_max -> cell side (identical on every rank)
-  CK(cudaMemsetAsync(c->scratch, 0, 4, c->stream));
+  CK(zero_async(c->scratch, 4, c->stream));
   if (n > 0) {
     k_hmax<<<std::min(nblk(n, 256), 1184), 256, 0, c->stream>>>(n, c->s.xh + base, c->scratch);
     c->launches++;
@@ -961,7 +1040,7 @@ sph_status rebuild_impl(sph_ctx* c) {
   CK(cudaGetLastError());
   // global h_max (positive f32 bits order as uint32): device-side reduction, one read-back
   if ((st = allreduce_dev(c, c->scratch, 1, kMax)) != SPH_OK) return st;
-  CK(cudaMemcpyAsync(c->scratch_h, c->scratch, 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(copy_chunked(c->scratch_h, c->scratch, 4, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   float hmax;
   std::memcpy(&hmax, c->scratch_h, 4);
@@ -1018,7 +1097,7 @@ sph_status rebuild_impl(sph_ctx* c) {
     // list radius (+25 % for its growth in the h iteration; k_wide_density asks for a rebuild
     // past it) crosses a slab face lies within G planes of it, and its own search stays inside
     // the local planes (ghost_planes_needed; the largest over the ranks)
-    CK(cudaMemsetAsync(c->scratch + 5, 0, 4, c->stream));
+    CK(zero_async(c->scratch + 5, 4, c->stream));
     if (n > 0) {
       k_ghost_need<<<std::min(nblk(n, 256), 1184), 256, 0, c->stream>>>(
           n, c->s.xh + base, g, (1.f + c->cfg.cell_skin) * c->cfg.gamma_k * 1.25f, c->scratch + 5);
@@ -1026,7 +1105,7 @@ sph_status rebuild_impl(sph_ctx* c) {
     }
     CK(cudaGetLastError());
     if ((st = allreduce_dev(c, c->scratch + 5, 1, kMax)) != SPH_OK) return st;
-    CK(cudaMemcpyAsync(c->scratch_h + 5, c->scratch + 5, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(copy_chunked(c->scratch_h + 5, c->scratch + 5, 4, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     G = std::max(G, (int)c->scratch_h[5]);
     if (G > kMaxGhostPlanes) {
@@ -1214,14 +1293,14 @@ sph_status rebuild_impl(sph_ctx* c) {
   stage("binned");
   // coincident particles: flags for k_lists and the directed pair count (read with the
   // tile sizes below)
-  CK(cudaMemsetAsync(c->scratch + 14, 0, 4, c->stream));
+  CK(zero_async(c->scratch + 14, 4, c->stream));
   if (n > 0) {
-    CK(cudaMemsetAsync(c->s.dup + c->gL, 0, (size_t)n, c->stream));
+    CK(zero_async(c->s.dup + c->gL, (size_t)n, c->stream));
     k_dup<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->keys_alt, c->s.xh + c->gL, c->s.dup + c->gL, c->scratch + 14);
     c->launches++;
   }
   CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(c->scratch_h + 14, c->scratch + 14, 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(copy_chunked(c->scratch_h + 14, c->scratch + 14, 4, cudaMemcpyDeviceToHost, c->stream));
   // CTA blocks: BX x BY grid columns x KZ cells (BX, BY = 2 when the grid allows: the tile of
   // (BX+2)(BY+2) columns is then ~2x smaller per owned particle than with single columns)
   g.bx = (g.periodic_x ? g.nx >= 6 : g.nxo >= 2) ? 2 : 1;
@@ -1257,13 +1336,13 @@ sph_status rebuild_impl(sph_ctx* c) {
     g.KZ = KZ;
     g.nzb = (g.nz + KZ - 1) / KZ;
     g.nblocks = g.nbx * g.nby * g.nzb;
-    CK(cudaMemsetAsync(c->scratch + 6, 0, 8, c->stream));
+    CK(zero_async(c->scratch + 6, 8, c->stream));
     // the blocks with i particles (flagged from the occupied cells, compacted in block order: one
     // loop CTA each), then the largest tile and i count over those blocks only (a clustered box
     // on a fine grid has mostly empty blocks); the last probe is at the chosen KZ
     if ((st = grow_h(c, &c->act_flag, c->act_cap, (size_t)g.nblocks)) != SPH_OK) return st;
     if ((st = grow_h(c, &c->blk_list, c->list_cap, (size_t)g.nblocks)) != SPH_OK) return st;
-    CK(cudaMemsetAsync(c->act_flag, 0, (size_t)g.nblocks, c->stream));
+    CK(zero_async(c->act_flag, (size_t)g.nblocks, c->stream));
     CK(launch_block_flags(n, c->keys_alt, g, c->act_flag, c->stream));
     {
       thrust::counting_iterator<int> it(0);
@@ -1282,8 +1361,8 @@ sph_status rebuild_impl(sph_ctx* c) {
     }
     c->launches += 3;
     if ((st = allreduce_dev(c, c->scratch + 6, 2, kMax)) != SPH_OK) return st;  // same capacities on every rank
-    CK(cudaMemcpyAsync(c->scratch_h + 6, c->scratch + 6, 8, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(c->scratch_h + 12, c->scratch + 12, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(copy_chunked(c->scratch_h + 6, c->scratch + 6, 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(copy_chunked(c->scratch_h + 12, c->scratch + 12, 4, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     double tmax[2] = {(double)c->scratch_h[6], (double)c->scratch_h[7]};
     g.tcap = std::max(32, (int)tmax[0]);
@@ -1339,7 +1418,7 @@ sph_status rebuild_impl(sph_ctx* c) {
   }
   if (getenv("SPH_DEBUG")) {
     std::vector<int> cs(std::min(g.ncells, 1 << 24) + 1);  // (the monotonicity check on small grids only)
-    cudaMemcpyAsync(cs.data(), c->cell_start, cs.size() * 4, cudaMemcpyDeviceToHost, c->stream);
+    copy_chunked(cs.data(), c->cell_start, cs.size() * 4, cudaMemcpyDeviceToHost, c->stream);
     cudaStreamSynchronize(c->stream);
     int bad = 0;
     for (size_t k = 0; k + 1 < cs.size(); ++k) bad += cs[k + 1] < cs[k];
@@ -1389,7 +1468,7 @@ sph_status rebuild_impl(sph_ctx* c) {
     CK(cub::DeviceSelect::Flagged(c->sel_tmp, need, it, c->side_flag + na, c->side_list + na, n_dev + 1, g.nact,
                                   c->stream));
     c->launches += 2;
-    CK(cudaMemcpyAsync(c->scratch_h + 8, c->scratch + 8, 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(copy_chunked(c->scratch_h + 8, c->scratch + 8, 8, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     c->n_int = g.nact > 0 ? (int)c->scratch_h[8] : 0;
     c->n_bnd = g.nact > 0 ? (int)c->scratch_h[9] : 0;
@@ -1413,7 +1492,7 @@ sph_status h_quantile(sph_ctx* c, double q, float* out, bool global) {
   const int n = c->n_own;
   global = global && c->slab;
   if (n <= 0 && !global) return fail(c, SPH_ERR_INVALID_ARG, "no particles");
-  CK(cudaMemsetAsync(c->scratch + 9, 0, 4, c->stream));
+  CK(zero_async(c->scratch + 9, 4, c->stream));
   if (n > 0) {
     k_h_keys<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->s.xh + c->gL, c->keys);
     c->launches++;
@@ -1421,11 +1500,12 @@ sph_status h_quantile(sph_ctx* c, double q, float* out, bool global) {
     size_t tmp = c->sort_tmp_bytes;
     CK(cub::DeviceRadixSort::SortKeys(c->sort_tmp, tmp, c->keys, c->keys_alt, n, 0, 32, c->stream));
     const int k = std::min(n - 1, std::max(0, (int)(q * (n - 1))));
-    CK(cudaMemcpyAsync(c->scratch + 9, c->keys_alt + k, 4, cudaMemcpyDeviceToDevice, c->stream));
+    k_copy_u32<<<1, 1, 0, c->stream>>>(c->keys_alt + k, reinterpret_cast<unsigned int*>(c->scratch + 9));
+    CK(cudaGetLastError());
   }
   sph_status st;
   if (global && (st = allreduce_dev(c, c->scratch + 9, 1, kMax)) != SPH_OK) return st;
-  CK(cudaMemcpyAsync(c->scratch_h + 9, c->scratch + 9, 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(copy_chunked(c->scratch_h + 9, c->scratch + 9, 4, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   std::memcpy(out, c->scratch_h + 9, 4);
   if (!(*out > 0.f)) return fail(c, SPH_ERR_INVALID_ARG, "no particles");
@@ -1478,15 +1558,15 @@ sph_status mark_wide(sph_ctx* c) {
     CK(cub::DeviceSelect::Flagged(c->sel_tmp, need, it, c->wide_flag + c->gL, c->widx, c->n_wide_dev, n, c->stream));
     c->launches++;
     // (with the population counter n0 in the same read-back)
-    CK(cudaMemcpyAsync(c->scratch_h + 10, c->n_wide_dev, 4, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(c->scratch_h + 15, c->scratch + 15, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(copy_chunked(c->scratch_h + 10, c->n_wide_dev, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(copy_chunked(c->scratch_h + 15, c->scratch + 15, 4, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     std::memcpy(&nw_own, c->scratch_h + 10, 4);
     nw = nw_own;
     if (n_loc > n) {
       CK(cub::DeviceSelect::If(c->sel_tmp, need, it0, c->widx + nw_own, c->n_wide_dev + 1, n_loc, gf, c->stream));
       c->launches++;
-      CK(cudaMemcpyAsync(c->scratch_h + 10, c->n_wide_dev + 1, 4, cudaMemcpyDeviceToHost, c->stream));
+      CK(copy_chunked(c->scratch_h + 10, c->n_wide_dev + 1, 4, cudaMemcpyDeviceToHost, c->stream));
       CK(cudaStreamSynchronize(c->stream));
       int ng;
       std::memcpy(&ng, c->scratch_h + 10, 4);
@@ -1499,7 +1579,7 @@ sph_status mark_wide(sph_ctx* c) {
   sph_status sq;
   for (float margin : {c->wide_margin, 0.f}) {
     c->grid.wide_margin = margin;
-    CK(cudaMemsetAsync(c->scratch + 15, 0, 4, c->stream));
+    CK(zero_async(c->scratch + 15, 4, c->stream));
     CK(launch_mark_wide(n_loc, c->grid, c->phys, s, c->wide_flag, c->scratch + 15, c->stream));
     c->launches++;
     if ((sq = select()) != SPH_OK) return sq;
@@ -1582,7 +1662,7 @@ sph_status mark_wide(sph_ctx* c) {
     }
     CK(cub::DeviceSelect::Flagged(c->sel_tmp, need2, it, c->act_flag, c->run_list, nrun_dev, g.nact, c->stream));
     c->launches++;
-    CK(cudaMemcpyAsync(c->scratch_h + 13, c->scratch + 13, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(copy_chunked(c->scratch_h + 13, c->scratch + 13, 4, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     g.nrun = (int)c->scratch_h[13];
     g.run_list = c->run_list;
@@ -1605,9 +1685,9 @@ sph_status mark_wide(sph_ctx* c) {
 sph_status build_lists(sph_ctx* c) {
   for (int attempt = 0; attempt < 4; ++attempt) {
     c->grid.lcap = c->lcap;
-    CK(cudaMemsetAsync(&c->ctr->list_overflow, 0, sizeof(int), c->stream));
-    CK(cudaMemsetAsync(&c->ctr->wlist_overflow, 0, sizeof(int), c->stream));
-    CK(cudaMemsetAsync(&c->ctr->nonfinite, 0, sizeof(int), c->stream));
+    CK(zero_async(&c->ctr->list_overflow, sizeof(int), c->stream));
+    CK(zero_async(&c->ctr->wlist_overflow, sizeof(int), c->stream));
+    CK(zero_async(&c->ctr->nonfinite, sizeof(int), c->stream));
     if (lists_smem(c->grid) > kSmemMax) return fail(c, SPH_ERR_H_EXCEEDS_CELL, "neighbour lists exceed shared memory");
     {
       Timed tm(c, SPH_T_LISTS);
@@ -1843,9 +1923,9 @@ sph_status sph_density(sph_ctx* c, sph_density_stats* stats) {
   for (;;) {
     uint8_t* bin = c->blk[pass & 1];
     uint8_t* bout = c->blk[(pass + 1) & 1];
-    CK(cudaMemsetAsync(bout, 0, (size_t)std::max(c->grid.nact, 1), c->stream));
-    CK(cudaMemsetAsync(&c->ctr->active_next, 0, 3 * sizeof(int), c->stream));  // active_next, list_stale, overflow
-    CK(cudaMemsetAsync(&c->ctr->h_exceeds, 0, sizeof(int), c->stream));
+    CK(zero_async(bout, (size_t)std::max(c->grid.nact, 1), c->stream));
+    CK(zero_async(&c->ctr->active_next, 3 * sizeof(int), c->stream));  // active_next, list_stale, overflow
+    CK(zero_async(&c->ctr->h_exceeds, sizeof(int), c->stream));
     {
       Timed tm(c, SPH_T_DENSITY);
       CK(launch_density(c->grid, c->phys, c->s, c->cell_start, pass, bin, bout, 1.f + c->cfg.cell_skin, c->ctr,
@@ -1966,7 +2046,7 @@ sph_status sph_gradient(sph_ctx* c, float dt) {
   c->launches += 1 + (c->s.n_wide > 0 ? 1 : 0);
   // (into pinned memory: a pageable destination would block the host until the loop ends;
   // sph_get_counters synchronises and reads it)
-  CK(cudaMemcpyAsync(c->pairs_grad_h, &c->ctr->pairs, 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(copy_chunked(c->pairs_grad_h, &c->ctr->pairs, 8, cudaMemcpyDeviceToHost, c->stream));
   // ghosts need their owners' force-loop records (X3): on the communication stream, overlapping
   // the force loop's interior blocks
   if (c->slab) {
@@ -1993,12 +2073,14 @@ sph_status sph_force(sph_ctx* c, float* dt_next) {
     return fail(c, SPH_ERR_STATE, "sph_force needs a completed sph_gradient on the current cells");
   sph_status st;
   if ((st = reset_ctr(c)) != SPH_OK) return st;
-  unsigned int inf_bits = 0x7f800000u;
-  CK(cudaMemcpyAsync(&c->ctr->dt_bits, &inf_bits, 4, cudaMemcpyHostToDevice, c->stream));
+  // (dt_bits = +inf by a kernel, not a host copy: a copy would queue on the copy engines behind a
+  // pipelined upload, sph_stage_particles, and a pageable one would block the host with it)
+  k_set_u32<<<1, 1, 0, c->stream>>>(&c->ctr->dt_bits, 0x7f800000u);
+  CK(cudaGetLastError());
   {
     Timed tm(c, SPH_T_FORCE);
     // the pair-once loop adds both sides of every pair into acc (ghost slots included)
-    CK(cudaMemsetAsync(c->s.acc, 0, sizeof(float4) * (size_t)(c->gL + c->n_own + c->gR), c->stream));
+    CK(zero_async(c->s.acc, sizeof(float4) * (size_t)(c->gL + c->n_own + c->gR), c->stream));
     if (c->slab && c->x3_pending && !c->grid.run_list) {
       // interior blocks while the X3 halo (ghost force records) is in flight, then the boundary
       DevGrid gi = c->grid, gb = c->grid;
@@ -2146,7 +2228,7 @@ sph_status sph_get(sph_ctx* c, int field, void* dst, int on_device) {
   }
   if ((st = gather_field(c, field, d, &bytes)) != SPH_OK) return st;
   if (!on_device) {
-    CK(cudaMemcpyAsync(dst, d, bytes, cudaMemcpyDeviceToHost, c->stream));
+    CK(copy_chunked(dst, d, bytes, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
   }
   return SPH_OK;
@@ -2174,7 +2256,7 @@ sph_status sph_get_async(sph_ctx* c, int field, void* dst) {
   if ((st = gather_field(c, field, c->gbuf[k], &bytes)) != SPH_OK) return st;
   CK(cudaEventRecord(c->ev_gready[k], c->stream));
   CK(cudaStreamWaitEvent(c->dstream, c->ev_gready[k], 0));
-  CK(cudaMemcpyAsync(dst, c->gbuf[k], bytes, cudaMemcpyDeviceToHost, c->dstream));
+  CK(copy_chunked(dst, c->gbuf[k], bytes, cudaMemcpyDeviceToHost, c->dstream));
   CK(cudaEventRecord(c->ev_gfree[k], c->dstream));
   c->gused[k] = true;
   return SPH_OK;
@@ -2206,7 +2288,8 @@ sph_status sph_stage_particles(sph_ctx* c, const sph_particles_in* in) {
   auto up = [&](const void* src, size_t b) -> void* {
     if (!src) return nullptr;
     void* dst = d;
-    cudaMemcpyAsync(dst, src, b, cudaMemcpyHostToDevice, c->hstream);
+    cudaError_t e_ = copy_chunked(dst, src, b, cudaMemcpyHostToDevice, c->hstream);
+    (void)e_;
     d += al(b);
     return dst;
   };

@@ -728,12 +728,14 @@ sph_status ingest(sph_ctx* c, const sph_particles_in* in) {
 
 sph_status sync_ctr(sph_ctx* c) {
   CK(copy_chunked(c->ctr_h, c->ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, c->stream));
+  c->launches++;
   CK(cudaStreamSynchronize(c->stream));
   return SPH_OK;
 }
 
 sph_status reset_ctr(sph_ctx* c) {
   CK(zero_async(c->ctr, sizeof(DevCounters), c->stream));
+  c->launches++;
   return SPH_OK;
 }
 
@@ -757,6 +759,7 @@ sph_status exchange_sizes(sph_ctx* c, long long to_right, long long to_left, lon
   Xfer r[2] = {{left_of(c), c->cnt_dev + 2, 8}, {right_of(c), c->cnt_dev + 3, 8}};
   CKC(c->comm->exchange(s, 2, r, 2, c->stream));
   CK(copy_chunked(c->cnt_h + 2, c->cnt_dev + 2, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+  c->launches++;
   CK(cudaStreamSynchronize(c->stream));
   from_left = c->cnt_h[2];
   from_right = c->cnt_h[3];
@@ -873,6 +876,7 @@ sph_status agree(sph_ctx* c, bool bad, sph_status code, const char* msg) {
 sph_status sort_cells(sph_ctx* c, int base, int n, int* outside) {
   DevGrid& g = c->grid;
   CK(zero_async(c->scratch + 2, 4, c->stream));
+  c->launches++;
   if (n > 0) {
     k_keys<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->s.xh + base, g, c->keys, c->perm, (int*)(c->scratch + 2));
     c->launches++;
@@ -889,6 +893,7 @@ sph_status sort_cells(sph_ctx* c, int base, int n, int* outside) {
   c->launches++;
   CK(cudaGetLastError());
   CK(copy_chunked(c->scratch_h + 2, c->scratch + 2, 4, cudaMemcpyDeviceToHost, c->stream));
+  c->launches++;
   CK(cudaStreamSynchronize(c->stream));
   *outside = (int)c->scratch_h[2];
   return SPH_OK;
@@ -897,8 +902,10 @@ sph_status sort_cells(sph_ctx* c, int base, int n, int* outside) {
 sph_status read_cs(sph_ctx* c, int cell, int* v) {
   k_copy_u32<<<1, 1, 0, c->stream>>>(reinterpret_cast<const unsigned int*>(c->cell_start + cell),
                                      reinterpret_cast<unsigned int*>(c->scratch + 4));
+  c->launches++;
   CK(cudaGetLastError());
   CK(copy_chunked(c->scratch_h + 4, c->scratch + 4, 4, cudaMemcpyDeviceToHost, c->stream));
+  c->launches++;
   CK(cudaStreamSynchronize(c->stream));
   *v = (int)c->scratch_h[4];
   return SPH_OK;
@@ -982,6 +989,7 @@ sph_status rebalance_cuts(sph_ctx* c, int base, int n) {
   const int R = c->nranks;
   if (!c->xhist) CK(cudaMalloc(&c->xhist, kHistBins * sizeof(unsigned int)));
   CK(zero_async(c->xhist, kHistBins * sizeof(unsigned int), c->stream));
+  c->launches++;
   if (n > 0) {
     k_xhist<<<std::min(nblk(n, 256), 1184), 256, 0, c->stream>>>(n, c->s.xh + base, kHistBins, c->xhist);
     c->launches++;
@@ -991,6 +999,7 @@ sph_status rebalance_cuts(sph_ctx* c, int base, int n) {
   if (st != SPH_OK) return st;
   std::vector<unsigned int> h(kHistBins);
   CK(copy_chunked(h.data(), c->xhist, kHistBins * sizeof(unsigned int), cudaMemcpyDeviceToHost, c->stream));
+  c->launches++;
   CK(cudaStreamSynchronize(c->stream));
   double tot = 0.0;
   for (unsigned int v : h) tot += v;
@@ -1033,6 +1042,7 @@ sph_status rebuild_impl(sph_ctx* c) {
   int n = c->n_own;
   // global h_max -> cell side (identical on every rank)
   CK(zero_async(c->scratch, 4, c->stream));
+  c->launches++;
   if (n > 0) {
     k_hmax<<<std::min(nblk(n, 256), 1184), 256, 0, c->stream>>>(n, c->s.xh + base, c->scratch);
     c->launches++;
@@ -1041,6 +1051,7 @@ sph_status rebuild_impl(sph_ctx* c) {
   // global h_max (positive f32 bits order as uint32): device-side reduction, one read-back
   if ((st = allreduce_dev(c, c->scratch, 1, kMax)) != SPH_OK) return st;
   CK(copy_chunked(c->scratch_h, c->scratch, 4, cudaMemcpyDeviceToHost, c->stream));
+  c->launches++;
   CK(cudaStreamSynchronize(c->stream));
   float hmax;
   std::memcpy(&hmax, c->scratch_h, 4);
@@ -1098,6 +1109,7 @@ sph_status rebuild_impl(sph_ctx* c) {
     // past it) crosses a slab face lies within G planes of it, and its own search stays inside
     // the local planes (ghost_planes_needed; the largest over the ranks)
     CK(zero_async(c->scratch + 5, 4, c->stream));
+    c->launches++;
     if (n > 0) {
       k_ghost_need<<<std::min(nblk(n, 256), 1184), 256, 0, c->stream>>>(
           n, c->s.xh + base, g, (1.f + c->cfg.cell_skin) * c->cfg.gamma_k * 1.25f, c->scratch + 5);
@@ -1106,6 +1118,7 @@ sph_status rebuild_impl(sph_ctx* c) {
     CK(cudaGetLastError());
     if ((st = allreduce_dev(c, c->scratch + 5, 1, kMax)) != SPH_OK) return st;
     CK(copy_chunked(c->scratch_h + 5, c->scratch + 5, 4, cudaMemcpyDeviceToHost, c->stream));
+    c->launches++;
     CK(cudaStreamSynchronize(c->stream));
     G = std::max(G, (int)c->scratch_h[5]);
     if (G > kMaxGhostPlanes) {
@@ -1294,13 +1307,16 @@ sph_status rebuild_impl(sph_ctx* c) {
   // coincident particles: flags for k_lists and the directed pair count (read with the
   // tile sizes below)
   CK(zero_async(c->scratch + 14, 4, c->stream));
+  c->launches++;
   if (n > 0) {
     CK(zero_async(c->s.dup + c->gL, (size_t)n, c->stream));
+    c->launches++;
     k_dup<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->keys_alt, c->s.xh + c->gL, c->s.dup + c->gL, c->scratch + 14);
     c->launches++;
   }
   CK(cudaGetLastError());
   CK(copy_chunked(c->scratch_h + 14, c->scratch + 14, 4, cudaMemcpyDeviceToHost, c->stream));
+  c->launches++;
   // CTA blocks: BX x BY grid columns x KZ cells (BX, BY = 2 when the grid allows: the tile of
   // (BX+2)(BY+2) columns is then ~2x smaller per owned particle than with single columns)
   g.bx = (g.periodic_x ? g.nx >= 6 : g.nxo >= 2) ? 2 : 1;
@@ -1337,12 +1353,14 @@ sph_status rebuild_impl(sph_ctx* c) {
     g.nzb = (g.nz + KZ - 1) / KZ;
     g.nblocks = g.nbx * g.nby * g.nzb;
     CK(zero_async(c->scratch + 6, 8, c->stream));
+    c->launches++;
     // the blocks with i particles (flagged from the occupied cells, compacted in block order: one
     // loop CTA each), then the largest tile and i count over those blocks only (a clustered box
     // on a fine grid has mostly empty blocks); the last probe is at the chosen KZ
     if ((st = grow_h(c, &c->act_flag, c->act_cap, (size_t)g.nblocks)) != SPH_OK) return st;
     if ((st = grow_h(c, &c->blk_list, c->list_cap, (size_t)g.nblocks)) != SPH_OK) return st;
     CK(zero_async(c->act_flag, (size_t)g.nblocks, c->stream));
+    c->launches++;
     CK(launch_block_flags(n, c->keys_alt, g, c->act_flag, c->stream));
     {
       thrust::counting_iterator<int> it(0);
@@ -1362,7 +1380,9 @@ sph_status rebuild_impl(sph_ctx* c) {
     c->launches += 3;
     if ((st = allreduce_dev(c, c->scratch + 6, 2, kMax)) != SPH_OK) return st;  // same capacities on every rank
     CK(copy_chunked(c->scratch_h + 6, c->scratch + 6, 8, cudaMemcpyDeviceToHost, c->stream));
+    c->launches++;
     CK(copy_chunked(c->scratch_h + 12, c->scratch + 12, 4, cudaMemcpyDeviceToHost, c->stream));
+    c->launches++;
     CK(cudaStreamSynchronize(c->stream));
     double tmax[2] = {(double)c->scratch_h[6], (double)c->scratch_h[7]};
     g.tcap = std::max(32, (int)tmax[0]);
@@ -1469,6 +1489,7 @@ sph_status rebuild_impl(sph_ctx* c) {
                                   c->stream));
     c->launches += 2;
     CK(copy_chunked(c->scratch_h + 8, c->scratch + 8, 8, cudaMemcpyDeviceToHost, c->stream));
+    c->launches++;
     CK(cudaStreamSynchronize(c->stream));
     c->n_int = g.nact > 0 ? (int)c->scratch_h[8] : 0;
     c->n_bnd = g.nact > 0 ? (int)c->scratch_h[9] : 0;
@@ -1493,6 +1514,7 @@ sph_status h_quantile(sph_ctx* c, double q, float* out, bool global) {
   global = global && c->slab;
   if (n <= 0 && !global) return fail(c, SPH_ERR_INVALID_ARG, "no particles");
   CK(zero_async(c->scratch + 9, 4, c->stream));
+  c->launches++;
   if (n > 0) {
     k_h_keys<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->s.xh + c->gL, c->keys);
     c->launches++;
@@ -1501,11 +1523,13 @@ sph_status h_quantile(sph_ctx* c, double q, float* out, bool global) {
     CK(cub::DeviceRadixSort::SortKeys(c->sort_tmp, tmp, c->keys, c->keys_alt, n, 0, 32, c->stream));
     const int k = std::min(n - 1, std::max(0, (int)(q * (n - 1))));
     k_copy_u32<<<1, 1, 0, c->stream>>>(c->keys_alt + k, reinterpret_cast<unsigned int*>(c->scratch + 9));
+    c->launches++;
     CK(cudaGetLastError());
   }
   sph_status st;
   if (global && (st = allreduce_dev(c, c->scratch + 9, 1, kMax)) != SPH_OK) return st;
   CK(copy_chunked(c->scratch_h + 9, c->scratch + 9, 4, cudaMemcpyDeviceToHost, c->stream));
+  c->launches++;
   CK(cudaStreamSynchronize(c->stream));
   std::memcpy(out, c->scratch_h + 9, 4);
   if (!(*out > 0.f)) return fail(c, SPH_ERR_INVALID_ARG, "no particles");
@@ -1559,7 +1583,9 @@ sph_status mark_wide(sph_ctx* c) {
     c->launches++;
     // (with the population counter n0 in the same read-back)
     CK(copy_chunked(c->scratch_h + 10, c->n_wide_dev, 4, cudaMemcpyDeviceToHost, c->stream));
+    c->launches++;
     CK(copy_chunked(c->scratch_h + 15, c->scratch + 15, 4, cudaMemcpyDeviceToHost, c->stream));
+    c->launches++;
     CK(cudaStreamSynchronize(c->stream));
     std::memcpy(&nw_own, c->scratch_h + 10, 4);
     nw = nw_own;
@@ -1567,6 +1593,7 @@ sph_status mark_wide(sph_ctx* c) {
       CK(cub::DeviceSelect::If(c->sel_tmp, need, it0, c->widx + nw_own, c->n_wide_dev + 1, n_loc, gf, c->stream));
       c->launches++;
       CK(copy_chunked(c->scratch_h + 10, c->n_wide_dev + 1, 4, cudaMemcpyDeviceToHost, c->stream));
+      c->launches++;
       CK(cudaStreamSynchronize(c->stream));
       int ng;
       std::memcpy(&ng, c->scratch_h + 10, 4);
@@ -1580,6 +1607,7 @@ sph_status mark_wide(sph_ctx* c) {
   for (float margin : {c->wide_margin, 0.f}) {
     c->grid.wide_margin = margin;
     CK(zero_async(c->scratch + 15, 4, c->stream));
+    c->launches++;
     CK(launch_mark_wide(n_loc, c->grid, c->phys, s, c->wide_flag, c->scratch + 15, c->stream));
     c->launches++;
     if ((sq = select()) != SPH_OK) return sq;
@@ -1663,6 +1691,7 @@ sph_status mark_wide(sph_ctx* c) {
     CK(cub::DeviceSelect::Flagged(c->sel_tmp, need2, it, c->act_flag, c->run_list, nrun_dev, g.nact, c->stream));
     c->launches++;
     CK(copy_chunked(c->scratch_h + 13, c->scratch + 13, 4, cudaMemcpyDeviceToHost, c->stream));
+    c->launches++;
     CK(cudaStreamSynchronize(c->stream));
     g.nrun = (int)c->scratch_h[13];
     g.run_list = c->run_list;
@@ -1686,8 +1715,11 @@ sph_status build_lists(sph_ctx* c) {
   for (int attempt = 0; attempt < 4; ++attempt) {
     c->grid.lcap = c->lcap;
     CK(zero_async(&c->ctr->list_overflow, sizeof(int), c->stream));
+    c->launches++;
     CK(zero_async(&c->ctr->wlist_overflow, sizeof(int), c->stream));
+    c->launches++;
     CK(zero_async(&c->ctr->nonfinite, sizeof(int), c->stream));
+    c->launches++;
     if (lists_smem(c->grid) > kSmemMax) return fail(c, SPH_ERR_H_EXCEEDS_CELL, "neighbour lists exceed shared memory");
     {
       Timed tm(c, SPH_T_LISTS);
@@ -1924,8 +1956,11 @@ sph_status sph_density(sph_ctx* c, sph_density_stats* stats) {
     uint8_t* bin = c->blk[pass & 1];
     uint8_t* bout = c->blk[(pass + 1) & 1];
     CK(zero_async(bout, (size_t)std::max(c->grid.nact, 1), c->stream));
-    CK(zero_async(&c->ctr->active_next, 3 * sizeof(int), c->stream));  // active_next, list_stale, overflow
+    c->launches++;
+    CK(zero_async(&c->ctr->active_next, 3 * sizeof(int), c->stream));
+  c->launches++;  // active_next, list_stale, overflow
     CK(zero_async(&c->ctr->h_exceeds, sizeof(int), c->stream));
+    c->launches++;
     {
       Timed tm(c, SPH_T_DENSITY);
       CK(launch_density(c->grid, c->phys, c->s, c->cell_start, pass, bin, bout, 1.f + c->cfg.cell_skin, c->ctr,
@@ -2047,6 +2082,7 @@ sph_status sph_gradient(sph_ctx* c, float dt) {
   // (into pinned memory: a pageable destination would block the host until the loop ends;
   // sph_get_counters synchronises and reads it)
   CK(copy_chunked(c->pairs_grad_h, &c->ctr->pairs, 8, cudaMemcpyDeviceToHost, c->stream));
+  c->launches++;
   // ghosts need their owners' force-loop records (X3): on the communication stream, overlapping
   // the force loop's interior blocks
   if (c->slab) {
@@ -2076,11 +2112,13 @@ sph_status sph_force(sph_ctx* c, float* dt_next) {
   // (dt_bits = +inf by a kernel, not a host copy: a copy would queue on the copy engines behind a
   // pipelined upload, sph_stage_particles, and a pageable one would block the host with it)
   k_set_u32<<<1, 1, 0, c->stream>>>(&c->ctr->dt_bits, 0x7f800000u);
+  c->launches++;
   CK(cudaGetLastError());
   {
     Timed tm(c, SPH_T_FORCE);
     // the pair-once loop adds both sides of every pair into acc (ghost slots included)
     CK(zero_async(c->s.acc, sizeof(float4) * (size_t)(c->gL + c->n_own + c->gR), c->stream));
+    c->launches++;
     if (c->slab && c->x3_pending && !c->grid.run_list) {
       // interior blocks while the X3 halo (ghost force records) is in flight, then the boundary
       DevGrid gi = c->grid, gb = c->grid;
@@ -2229,6 +2267,7 @@ sph_status sph_get(sph_ctx* c, int field, void* dst, int on_device) {
   if ((st = gather_field(c, field, d, &bytes)) != SPH_OK) return st;
   if (!on_device) {
     CK(copy_chunked(dst, d, bytes, cudaMemcpyDeviceToHost, c->stream));
+    c->launches++;
     CK(cudaStreamSynchronize(c->stream));
   }
   return SPH_OK;

@@ -253,7 +253,10 @@ cudaError_t copy_chunked(void* dst, const void* src, size_t b, cudaMemcpyKind ki
     void* mapped = static_cast<char*>(at.devicePointer) + off;
     const uint32_t* s = static_cast<const uint32_t*>(kind == cudaMemcpyHostToDevice ? mapped : src);
     uint32_t* d = static_cast<uint32_t*>(kind == cudaMemcpyHostToDevice ? dst : mapped);
-    k_copy_words<<<(unsigned)std::min<size_t>(64, (b / 4 + 1023) / 1024), 256, 0, st>>>(s, d, b / 4);
+    // (CTAs, C4 e2e ms: 8 69, 16 40-42, 32 39.0-39.2, 64 43, 148 81, 296 48 -- the PCIe reads saturate
+    // near 19 GB/s and more CTAs only take SM slots from the loops; SPH_COPY_CTAS overrides)
+    static const int ctas = getenv("SPH_COPY_CTAS") ? std::max(1, atoi(getenv("SPH_COPY_CTAS"))) : 32;
+    k_copy_words<<<(unsigned)std::min<size_t>(ctas, (b / 4 + 1023) / 1024), 256, 0, st>>>(s, d, b / 4);
     return cudaGetLastError();
   }
   cudaGetLastError();  // (cudaPointerGetAttributes on pageable memory)

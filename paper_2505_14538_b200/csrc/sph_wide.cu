@@ -193,34 +193,44 @@ __global__ void __launch_bounds__(256) k_wide_lists(DevGrid g, DevPhys ph, DevSt
       if (lane >= o) incl += v;
     }
     const int total = __shfl_sync(kFull, incl, 31);
-    for (int base = 0; base < total; base += 32) {
-      const int idx = base + lane;
-      // the range holding idx: the first lane r with incl[r] > idx (binary search by shuffles)
+    // two chunks of 32 candidates per trip, both gathers (cperm -> xh) issued before either test
+    // (the loop is bound by that chain's latency); hits compacted chunk by chunk, in order
+    auto locate = [&](int idx, int& r0, int& e0) {  // the range holding idx: first lane with incl > idx
       int lo = 0;
 #pragma unroll
       for (int w = 16; w > 0; w >>= 1) {
         const int v = __shfl_sync(kFull, incl, lo + w - 1);
         if (v <= idx) lo += w;
       }
-      const int r0 = __shfl_sync(kFull, t0, lo & 31), e0 = __shfl_sync(kFull, incl - len, lo & 31);
-      bool hit = false;
-      int j = 0;
-      if (idx < total) {
-        j = (int)__ldg(cperm + r0 + (idx - e0));
-        const uint4 xj = s.xh[j];
-        const float dx = (float)(int)(xi.x - xj.x) * g.scale[0];
-        const float dy = (float)(int)(xi.y - xj.y) * g.scale[1];
-        const float dz = (float)(int)(xi.z - xj.z) * g.scale[2];
-        const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-        const float hj = __uint_as_float(xj.w);
-        hit = r2 < fmaxf(Hi2, (Hfac * hj) * (Hfac * hj));
-        // a partner at exactly i's position (j != i) is skipped
-        if (j != i && xj.x == xi.x && xj.y == xi.y && xj.z == xi.z) hit = false;
-      }
+      r0 = __shfl_sync(kFull, t0, lo & 31);
+      e0 = __shfl_sync(kFull, incl - len, lo & 31);
+    };
+    auto test = [&](int j, const uint4& xj) {
+      const float dx = (float)(int)(xi.x - xj.x) * g.scale[0];
+      const float dy = (float)(int)(xi.y - xj.y) * g.scale[1];
+      const float dz = (float)(int)(xi.z - xj.z) * g.scale[2];
+      const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+      const float hj = __uint_as_float(xj.w);
+      // a partner at exactly i's position (j != i) is skipped
+      return r2 < fmaxf(Hi2, (Hfac * hj) * (Hfac * hj)) &&
+             !(j != i && xj.x == xi.x && xj.y == xi.y && xj.z == xi.z);
+    };
+    auto emit = [&](bool hit, int j) {
       const unsigned b = __ballot_sync(kFull, hit);
       const int pos = cnt + __popc(b & ((1u << lane) - 1u));
       if (hit && pos < s.wlcap) lst[pos] = (uint32_t)j;
       cnt += __popc(b);
+    };
+    for (int base = 0; base < total; base += 64) {
+      const int ia = base + lane, ib = base + 32 + lane;
+      int ra, ea, rb, eb;
+      locate(ia, ra, ea);
+      locate(ib, rb, eb);
+      const bool va = ia < total, vb = ib < total;
+      const int ja = va ? (int)__ldg(cperm + ra + (ia - ea)) : 0, jb = vb ? (int)__ldg(cperm + rb + (ib - eb)) : 0;
+      const uint4 xa = va ? s.xh[ja] : xi, xb = vb ? s.xh[jb] : xi;
+      emit(va && test(ja, xa), ja);
+      if (base + 32 < total) emit(vb && test(jb, xb), jb);
     }
   }
   if (lane == 0) {
@@ -271,6 +281,7 @@ __global__ void __launch_bounds__(256) k_wide_density(DevGrid g, DevPhys ph, Dev
   const uint32_t* lst = s.wnbr + (size_t)wi * s.wlcap;
   const int n = s.wcount[wi];
   DenAcc a = DenAcc::zero();
+  // (two entries per lane per trip, as k_wide_gradient: 5.94 -> 5.98 ms of density on C5s)
   for (int k = lane; k < n; k += 32) {
     const int j = (int)__ldg(lst + k);
     const float3 d = rel(g, xi, s.xh[j]);
@@ -310,12 +321,24 @@ __global__ void __launch_bounds__(256) k_wide_gradient(DevGrid g, DevPhys ph, De
   const uint32_t* lst = s.wnbr + (size_t)wi * s.wlcap;
   const int n = s.wcount[wi];
   GradAcc a{2.f * gi4.x, 0.f, 0};
-  for (int k = lane; k < n; k += 32) {
-    const int j = (int)__ldg(lst + k);
-    const float3 d = rel(g, xi, s.xh[j]);
-    grad_pair(a, d.x, d.y, d.z, hinv, kBandW, vi, gi4.x, gi4.y, ph.beta, s.vm[j], s.gq[j], [&]() {
-      return exact_neighbour(s.xh, i, j, H2, g.dscale[0], g.dscale[1], g.dscale[2]);
+  // two entries per lane per trip, both gathers issued before either pair (the loop is bound by
+  // the latency of the list -> record gather chain; C5s gradient 3.43 -> 3.13 ms); the lane's sum
+  // order is unchanged
+  for (int k = lane; k < n; k += 64) {
+    const bool two = k + 32 < n;
+    const int j0 = (int)__ldg(lst + k), j1 = two ? (int)__ldg(lst + k + 32) : j0;
+    const uint4 x0 = s.xh[j0], x1 = s.xh[j1];
+    const float4 v0 = s.vm[j0], v1 = s.vm[j1], q0 = s.gq[j0], q1 = s.gq[j1];
+    const float3 d0 = rel(g, xi, x0);
+    grad_pair(a, d0.x, d0.y, d0.z, hinv, kBandW, vi, gi4.x, gi4.y, ph.beta, v0, q0, [&]() {
+      return exact_neighbour(s.xh, i, j0, H2, g.dscale[0], g.dscale[1], g.dscale[2]);
     });
+    if (two) {
+      const float3 d1 = rel(g, xi, x1);
+      grad_pair(a, d1.x, d1.y, d1.z, hinv, kBandW, vi, gi4.x, gi4.y, ph.beta, v1, q1, [&]() {
+        return exact_neighbour(s.xh, i, j1, H2, g.dscale[0], g.dscale[1], g.dscale[2]);
+      });
+    }
   }
   a.vmax = warp_fmax(a.vmax);
   a.lap = warp_sum(a.lap);
@@ -375,6 +398,7 @@ __global__ void __launch_bounds__(256) k_wide_force(DevGrid g, DevPhys ph, DevSt
   float4 ai = make_float4(0.f, 0.f, 0.f, 0.f);
   float vmax = 2.f * I.a.z;  // (R15)
   int nn = 0;
+  // (loading the next trip's list entry and position one trip ahead: C5s force 6.24 -> 6.34 ms)
   for (int k = lane; k < n; k += 32) {
     const int j = (int)__ldg(lst + k);
     const uint4 xj = s.xh[j];

@@ -87,6 +87,8 @@ def parse():
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--tile-z", type=int, default=0, help="cells per CTA block along z (0 = auto)")
     ap.add_argument("--skin", type=float, default=None, help="cell_skin (default: the library's)")
+    ap.add_argument("--spin", type=int, default=1, choices=[0, 1],
+                    help="spin-wait host synchronisation (cuCtxSetFlags CU_CTX_SCHED_SPIN; default 1)")
     ap.add_argument("--balance", action="store_true",
                     help="several ranks: move the slab cuts toward equal particle counts at every rebuild")
     ap.add_argument("--halo-put", type=int, default=-1, choices=[-1, 0, 1],
@@ -292,6 +294,21 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def spin_wait(torch):
+    """Spin-wait host synchronisation for this process's CUDA context (cuCtxSetFlags
+    CU_CTX_SCHED_SPIN): the hydro pass reads a few counters back per step and waits for each; a
+    yielding wait lets the host thread be descheduled for up to milliseconds on a busy host."""
+    import ctypes
+
+    torch.cuda.synchronize()  # (the primary context is current)
+    try:
+        cu = ctypes.CDLL("libcuda.so.1")
+        cu.cuCtxSetFlags.argtypes = [ctypes.c_uint]
+        return cu.cuCtxSetFlags(1) == 0  # CU_CTX_SCHED_SPIN
+    except (OSError, AttributeError):
+        return False
+
+
 def run_ours(args, world, rank, local):
     import torch
 
@@ -299,6 +316,8 @@ def run_ours(args, world, rank, local):
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
+    if args.spin:
+        spin_wait(torch)
     name, p = rank_workload(args.workload, rank, world, args.scaling)
     n = p["X"].shape[0]
     n_total = int(p.get("n_total", n))

@@ -32,6 +32,7 @@
 // in f32 with a rigorous band and re-decided in fp64 inside it, so counts equal the
 // definition exactly.
 #include <algorithm>
+#include <cstdlib>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <math_constants.h>
@@ -1728,6 +1729,10 @@ cudaError_t launch_tile_sizes(const DevGrid& g, const int* cell_start, int* max_
 }
 
 static cudaError_t set_smem(const void* fn, size_t bytes) {
+  // (SPH_CARVEOUT: the shared-memory carveout in percent of the unified L1 / shared storage, -1 =
+  // the driver's choice; an experiment knob)
+  static const int carve = getenv("SPH_CARVEOUT") ? atoi(getenv("SPH_CARVEOUT")) : -1;
+  if (carve >= 0) cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
   return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 

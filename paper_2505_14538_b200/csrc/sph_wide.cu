@@ -308,7 +308,11 @@ __global__ void __launch_bounds__(256) k_wide_density(DevGrid g, DevPhys ph, Dev
     atomicExch(&ctr->h_exceeds, 1);
 }
 
-__global__ void __launch_bounds__(256) k_wide_gradient(DevGrid g, DevPhys ph, DevState s, float dt, int first_step,
+// (k_wide_gradient at 5 CTAs per SM, 48 registers: C5s gradient 3.13 -> 2.89 ms; 4 CTAs 3.10)
+#ifndef SPH_WG_MINB
+#define SPH_WG_MINB 5
+#endif
+__global__ void __launch_bounds__(256, SPH_WG_MINB) k_wide_gradient(DevGrid g, DevPhys ph, DevState s, float dt, int first_step,
                                                        DevCounters* __restrict__ ctr) {
   const int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (wi >= s.n_wide_own) return;  // (ghosts: the X3 exchange brings their records)
@@ -380,7 +384,12 @@ __device__ __forceinline__ void red_add4_w(float4* p, const float4& v) {
 // goes to acc[j] with one vector reduction.  v_sig and N_force: i's over its list; a partner
 // that did not list i gets its share of the pair here (atomics).
 template <bool PX>
-__global__ void __launch_bounds__(256) k_wide_force(DevGrid g, DevPhys ph, DevState s, DevCounters* __restrict__ ctr) {
+// (k_wide_force at 4 CTAs per SM, 64 registers: the gather-latency-bound loop wants the warps;
+// C5s force 6.24 -> 5.27 ms, 5 CTAs (48 registers, spills) 5.58)
+#ifndef SPH_WF_MINB
+#define SPH_WF_MINB 4
+#endif
+__global__ void __launch_bounds__(256, SPH_WF_MINB) k_wide_force(DevGrid g, DevPhys ph, DevState s, DevCounters* __restrict__ ctr) {
   const int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (wi >= s.n_wide) return;
   const int i = s.widx[wi];

@@ -140,7 +140,11 @@ __global__ void k_mark_wide(int n, DevGrid g, DevPhys ph, DevState s, uint8_t* f
 // One warp per wide particle.  Overflow of wlcap: the count is still returned (max in
 // ctr->list_overflow) and the host rebuilds with a larger capacity.
 template <bool PX>
-__global__ void __launch_bounds__(256) k_wide_lists(DevGrid g, DevPhys ph, DevState s, const int* __restrict__ cell_start,
+// (8 CTAs per SM, 32 registers: C5s lists 8.93 at 5 CTAs, 8.77 at 6, 8.65 at 8)
+#ifndef SPH_WL_MINB
+#define SPH_WL_MINB 8
+#endif
+__global__ void __launch_bounds__(256, SPH_WL_MINB) k_wide_lists(DevGrid g, DevPhys ph, DevState s, const int* __restrict__ cell_start,
                                                     DevCounters* __restrict__ ctr) {
   const int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -268,7 +272,11 @@ __device__ __forceinline__ float warp_fmax(float v) {
 
 // One warp per wide particle: the lanes split the list, the sums are reduced over the warp
 // (lane order, deterministic), lane 0 runs the epilogue.
-__global__ void __launch_bounds__(256) k_wide_density(DevGrid g, DevPhys ph, DevState s, int pass, float hfac_stale,
+// (6 CTAs per SM, 40 registers; C5s density 5.81 at 5 CTAs, 6.03 at 8)
+#ifndef SPH_WD_MINB
+#define SPH_WD_MINB 6
+#endif
+__global__ void __launch_bounds__(256, SPH_WD_MINB) k_wide_density(DevGrid g, DevPhys ph, DevState s, int pass, float hfac_stale,
                                                       DevCounters* __restrict__ ctr) {
   const int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (wi >= s.n_wide_own) return;  // (ghosts: their owner iterates them)

@@ -105,6 +105,7 @@ class Clocks:
     def __init__(self, index):
         self.index = index
         self.samples = []
+        self.times = []
         self._stop = threading.Event()
         self._proc = None
 
@@ -126,6 +127,21 @@ class Clocks:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) >= 7:
                 self.samples.append(parts)
+                self.times.append(time.monotonic())
+
+    def wait_first(self, timeout=10.0):
+        """Block until nvidia-smi's first sample: its start-up (NVML initialisation) holds driver
+        locks that stall the host's CUDA calls, so it must be over before the timed region."""
+        t = time.monotonic()
+        while self._proc and not self.samples and time.monotonic() - t < timeout:
+            time.sleep(0.01)
+
+    def window(self, t0, t1):
+        """Keep the samples taken in [t0, t1] (the timed region; else the first one after t0)."""
+        keep = [s for s, t in zip(self.samples, self.times) if t0 <= t <= t1]
+        if not keep:
+            keep = [s for s, t in zip(self.samples, self.times) if t >= t0][:1] or self.samples[-1:]
+        self.samples = keep
 
     def __exit__(self, *a):
         if self._proc:
@@ -355,6 +371,9 @@ def run_ours(args, world, rank, local):
         dt = float(min(dt_next, 2 * dt))
         return st, c
 
+    # clock sampling starts before the warm-up (nvidia-smi's start-up stalls CUDA host calls)
+    clk = Clocks(local).__enter__()
+    clk.wait_first()
     # first density pass establishes a consistent state (h converged, a computed)
     ctx.density()
     ctx.gradient(dt)
@@ -370,12 +389,15 @@ def run_ours(args, world, rank, local):
     ctx.timings(reset=True)
     ctx.set_timing(True)
     log = []
-    with Clocks(local) as clk:
-        t0 = ev()
-        for _ in range(args.steps):
-            step(log)
-        t1 = ev()
-        torch.cuda.synchronize()
+    w0 = time.monotonic()
+    t0 = ev()
+    for _ in range(args.steps):
+        step(log)
+    t1 = ev()
+    torch.cuda.synchronize()
+    w1 = time.monotonic()
+    clk.__exit__(None, None, None)
+    clk.window(w0, w1)
     launches = ctx.counters()["kernel_launches"] - launches0
     ms = t0.elapsed_time(t1)
     if world > 1:

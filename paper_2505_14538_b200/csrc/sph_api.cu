@@ -1459,7 +1459,9 @@ sph_status rebuild_impl(sph_ctx* c) {
   if ((st = grow_h(c, &c->pref_buf, c->pref_cap, 2 * na * (g.icap + 1))) != SPH_OK) return st;
   g.desc_pref = c->pref_buf;
   g.desc_prefF = c->pref_buf + na * (g.icap + 1);
-  CK(launch_tile_desc(g, c->cell_start, c->stream));
+  // (the i columns of every active block now; the full descriptors once the blocks the loops run
+  // are known, at the end of mark_wide)
+  CK(launch_tile_icols(g, c->cell_start, c->stream));
   c->launches++;
   const size_t blk_old = c->blk_cap;
   if ((st = grow_h(c, &c->blk[0], c->blk_cap, na)) != SPH_OK) return st;
@@ -1548,7 +1550,19 @@ struct GhostFlag {
 
 // Flag and list the wide particles of the current grid (none unless the side was sized from
 // an h quantile).
+sph_status mark_wide_impl(sph_ctx* c);
+
+// The wide set and the loops' run list (mark_wide_impl), then the tile descriptors of the blocks
+// the loops run (k_tile_desc; every active block without wide particles).
 sph_status mark_wide(sph_ctx* c) {
+  const sph_status st = mark_wide_impl(c);
+  if (st != SPH_OK) return st;
+  CK(launch_tile_desc(c->grid, c->cell_start, c->stream));
+  c->launches++;
+  return SPH_OK;
+}
+
+sph_status mark_wide_impl(sph_ctx* c) {
   DevState& s = c->s;
   s.n_wide = s.n_wide_own = 0;
   s.wide = nullptr;

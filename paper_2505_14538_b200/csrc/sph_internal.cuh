@@ -209,6 +209,7 @@ cudaError_t launch_wide_force(const DevGrid& g, const DevPhys& ph, const DevStat
 int kernel_threads();
 size_t tile_desc_bytes();  // descriptor + per-cell table, per block
 size_t tile_desc_header_bytes();  // the descriptor alone
+cudaError_t launch_tile_icols(const DevGrid& g, const int* cell_start, cudaStream_t st);
 cudaError_t launch_tile_desc(const DevGrid& g, const int* cell_start, cudaStream_t st);
 cudaError_t launch_block_run(const DevGrid& g, const DevState& s, uint8_t* flag, cudaStream_t st);
 cudaError_t launch_sparse_wide(const DevGrid& g, uint8_t* wide, int32_t* ncount, int kmin, cudaStream_t st);

@@ -1517,8 +1517,9 @@ __global__ void __launch_bounds__(256) k_force_fin(int i0, int n, DevPhys ph, De
 __global__ void __launch_bounds__(64) k_tile_desc(DevGrid g, const int* __restrict__ cell_start) {
   __shared__ BlockShared S;
   Tile T;
-  tile_setup(g, g.blk_list[blockIdx.x], cell_start, S, T);
-  TileDesc* D = reinterpret_cast<TileDesc*>(const_cast<void*>(g.desc)) + blockIdx.x;
+  const int a = blk_a(g);  // (the blocks the loops run: run_list, else every active block)
+  tile_setup(g, g.blk_list[a], cell_start, S, T);
+  TileDesc* D = reinterpret_cast<TileDesc*>(const_cast<void*>(g.desc)) + a;
   if (threadIdx.x == 0) D->T = T;
   if (threadIdx.x < kMaxICols) {
     D->ib[threadIdx.x] = S.ib[threadIdx.x];
@@ -1528,8 +1529,34 @@ __global__ void __launch_bounds__(64) k_tile_desc(DevGrid g, const int* __restri
   if (threadIdx.x <= kMaxICols) D->pre[threadIdx.x] = S.pre[threadIdx.x];
   if (threadIdx.x < kMaxSeg) D->seg[threadIdx.x] = S.seg[threadIdx.x];
   // per tile cell (tile offset, global start) for k_lists' window searches
-  int2* C = reinterpret_cast<int2*>(const_cast<void*>(g.desc_cells)) + (size_t)blockIdx.x * (kMaxTileCells + 1);
+  int2* C = reinterpret_cast<int2*>(const_cast<void*>(g.desc_cells)) + (size_t)a * (kMaxTileCells + 1);
   for (int c = threadIdx.x; c <= T.nct; c += blockDim.x) C[c] = make_int2(S.off[c], c < T.nct ? S.gst[c] : 0);
+}
+
+// The i columns of every active block (TileDesc::pre, g0, tc), one thread per block: all that
+// k_sparse_wide and k_block_run read; the full descriptors (k_tile_desc) are then made for the
+// blocks the loops run only (on a clustered box a few thousand of ~0.9 M active blocks).
+__global__ void k_tile_icols(DevGrid g, const int* __restrict__ cell_start) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= g.nact) return;
+  int jx, jy, zb;
+  block_coords(g, g.blk_list[a], jx, jy, zb);
+  const int ix0 = g.ix_first + jx * g.bx, iy0 = jy * g.by, z0 = zb * g.KZ, z1 = min(g.nz, z0 + g.KZ);
+  TileDesc* D = reinterpret_cast<TileDesc*>(const_cast<void*>(g.desc)) + a;
+  int k = 0, acc = 0;
+  for (int ex = 0; ex < g.bx; ++ex)
+    for (int ey = 0; ey < g.by; ++ey) {
+      if (ix0 + ex >= g.ix_first + g.nxo || iy0 + ey >= g.ny) continue;
+      const int col = ((ix0 + ex) * g.ny + (iy0 + ey)) * g.nz;  // an i column's cells are consecutive
+      const int s0 = __ldg(cell_start + col + z0), s1 = __ldg(cell_start + col + z1);
+      D->tc[k] = (ex + 1) * (g.by + 2) + (ey + 1);
+      D->g0[k] = s0;
+      D->pre[k] = acc;
+      acc += s1 - s0;
+      ++k;
+    }
+  D->pre[k] = acc;
+  for (int r = k; r < kMaxICols; ++r) { D->tc[r] = 0; D->g0[r] = 0; D->pre[r + 1] = acc; }
 }
 
 // tile size and i count of block b
@@ -1692,8 +1719,15 @@ size_t tile_desc_bytes() { return sizeof(TileDesc) + (size_t)(kMaxTileCells + 1)
 size_t tile_desc_header_bytes() { return sizeof(TileDesc); }
 
 cudaError_t launch_tile_desc(const DevGrid& g, const int* cell_start, cudaStream_t st) {
+  const int nb = g.run_list ? g.nrun : g.nact;
+  if (nb == 0) return cudaSuccess;
+  k_tile_desc<<<nb, 64, 0, st>>>(g, cell_start);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tile_icols(const DevGrid& g, const int* cell_start, cudaStream_t st) {
   if (g.nact == 0) return cudaSuccess;
-  k_tile_desc<<<g.nact, 64, 0, st>>>(g, cell_start);
+  k_tile_icols<<<(g.nact + 255) / 256, 256, 0, st>>>(g, cell_start);
   return cudaGetLastError();
 }
 

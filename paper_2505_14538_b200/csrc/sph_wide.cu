@@ -272,9 +272,9 @@ __device__ __forceinline__ float warp_fmax(float v) {
 
 // One warp per wide particle: the lanes split the list, the sums are reduced over the warp
 // (lane order, deterministic), lane 0 runs the epilogue.
-// (6 CTAs per SM, 40 registers; C5s density 5.81 at 5 CTAs, 6.03 at 8)
+// (5 CTAs per SM, 48 registers: with the in-kernel h iteration 6 CTAs spill; C5s density 6.03 at 8 CTAs)
 #ifndef SPH_WD_MINB
-#define SPH_WD_MINB 6
+#define SPH_WD_MINB 5
 #endif
 __global__ void __launch_bounds__(256, SPH_WD_MINB) k_wide_density(DevGrid g, DevPhys ph, DevState s, int pass, float hfac_stale,
                                                       DevCounters* __restrict__ ctr) {
@@ -284,36 +284,53 @@ __global__ void __launch_bounds__(256, SPH_WD_MINB) k_wide_density(DevGrid g, De
   if (pass > 0 && !s.active[i]) return;  // warp-uniform
   const uint4 xi = s.xh[i];
   const float4 vi = s.vm[i];
-  const float h = __uint_as_float(xi.w), hinv = 1.f / h;
-  const double H2 = h2_exact(h, ph.gamma_k);
   const uint32_t* lst = s.wnbr + (size_t)wi * s.wlcap;
   const int n = s.wcount[wi];
-  DenAcc a = DenAcc::zero();
-  // (two entries per lane per trip, as k_wide_gradient: 5.94 -> 5.98 ms of density on C5s)
-  for (int k = lane; k < n; k += 32) {
-    const int j = (int)__ldg(lst + k);
-    const float3 d = rel(g, xi, s.xh[j]);
-    den_pair(a, d.x, d.y, d.z, hinv, kBandW, vi, s.vm[j], [&]() {
-      return exact_neighbour(s.xh, i, j, H2, g.dscale[0], g.dscale[1], g.dscale[2]);
-    });
+  // the h iteration inside the kernel (one rank): a wide particle's sums depend on its own h
+  // only, so after a Newton update it walks its list again while the new h stays within the
+  // list radius (at most 6 updates per pass, as the tile density loop); the slab path takes one
+  // update per pass (its ghost-plane check, below, is per pass)
+  const int maxit = g.periodic_x ? 6 : 1;
+  float h = __uint_as_float(xi.w);
+  for (int it = 0; it < maxit; ++it) {
+    const float hinv = 1.f / h;
+    const double H2 = h2_exact(h, ph.gamma_k);
+    DenAcc a = DenAcc::zero();
+    for (int k = lane; k < n; k += 32) {
+      const int j = (int)__ldg(lst + k);
+      const float3 d = rel(g, xi, s.xh[j]);
+      den_pair(a, d.x, d.y, d.z, hinv, kBandW, vi, s.vm[j], [&]() {
+        return exact_neighbour(s.xh, i, j, H2, g.dscale[0], g.dscale[1], g.dscale[2]);
+      });
+    }
+    a.S0 = warp_sum(a.S0); a.S1 = warp_sum(a.S1); a.R0 = warp_sum(a.R0); a.R1 = warp_sum(a.R1);
+    a.Dv = warp_sum(a.Dv); a.Cx = warp_sum(a.Cx); a.Cy = warp_sum(a.Cy); a.Cz = warp_sum(a.Cz);
+    a.nn = warp_isum(a.nn);
+    int more = 0;
+    float hn = h;
+    if (lane == 0) {
+      const DenOut o = den_epilogue(g, ph, s, a, i, h, vi.w, pass + it, hfac_stale);
+      atomicAdd(&ctr->pairs_all, (unsigned long long)o.nn);
+      more = o.active && !o.stale && it + 1 < maxit;
+      hn = o.hn;
+      if (!more) {
+        if (o.final_) atomicAdd(&ctr->pairs, (unsigned long long)o.nn);
+        if (o.final_ && o.resid > 0.f) atomicMax(&ctr->max_resid_bits, __float_as_uint(o.resid));
+        if (o.give_up) atomicAdd(&ctr->unconverged, 1);
+        if (o.active) atomicAdd(&ctr->active_next, 1);
+        if (o.stale) atomicExch(&ctr->list_stale, 1);
+        // slab path: the new list radius must still fit the G ghost planes (ghost_planes_needed);
+        // past them the grid is rebuilt with a larger G
+        if (!g.periodic_x && o.active &&
+            ghost_planes_needed((int)ceilf((1.f + g.skin) * ph.gamma_k * o.hn / g.side_min),
+                                plane_of<false>(g, i, xi.x) - g.ix_first, g.nxo) > g.ix_first)
+          atomicExch(&ctr->h_exceeds, 1);
+      }
+    }
+    more = __shfl_sync(kFull, more, 0);
+    if (!more) break;
+    h = __shfl_sync(kFull, hn, 0);
   }
-  a.S0 = warp_sum(a.S0); a.S1 = warp_sum(a.S1); a.R0 = warp_sum(a.R0); a.R1 = warp_sum(a.R1);
-  a.Dv = warp_sum(a.Dv); a.Cx = warp_sum(a.Cx); a.Cy = warp_sum(a.Cy); a.Cz = warp_sum(a.Cz);
-  a.nn = warp_isum(a.nn);
-  if (lane != 0) return;
-  const DenOut o = den_epilogue(g, ph, s, a, i, h, vi.w, pass, hfac_stale);
-  atomicAdd(&ctr->pairs_all, (unsigned long long)o.nn);
-  if (o.final_) atomicAdd(&ctr->pairs, (unsigned long long)o.nn);
-  if (o.final_ && o.resid > 0.f) atomicMax(&ctr->max_resid_bits, __float_as_uint(o.resid));
-  if (o.give_up) atomicAdd(&ctr->unconverged, 1);
-  if (o.active) atomicAdd(&ctr->active_next, 1);
-  if (o.stale) atomicExch(&ctr->list_stale, 1);
-  // slab path: the new list radius must still fit the G ghost planes (ghost_planes_needed);
-  // past them the grid is rebuilt with a larger G
-  if (!g.periodic_x && o.active &&
-      ghost_planes_needed((int)ceilf((1.f + g.skin) * ph.gamma_k * o.hn / g.side_min),
-                          plane_of<false>(g, i, xi.x) - g.ix_first, g.nxo) > g.ix_first)
-    atomicExch(&ctr->h_exceeds, 1);
 }
 
 // (k_wide_gradient at 5 CTAs per SM, 48 registers: C5s gradient 3.13 -> 2.89 ms; 4 CTAs 3.10)

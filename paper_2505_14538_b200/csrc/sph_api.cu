@@ -1397,7 +1397,9 @@ sph_status rebuild_impl(sph_ctx* c) {
     if (force_smem(g) > kSmemTarget) g.force_threads = 512;
     const bool fits = force_smem(g) <= kSmemMax && lists_smem(g) <= kSmemMax && density_smem(g) <= kSmemMax &&
                       gradient_smem(g) <= kSmemMax && g.tcap < 32760;  // (list entries: 15-bit slots)
-    const bool ok = fits && (force_smem(g) <= kSmemTarget || KZ == 1);
+    // (KZ <= 2 is taken at one force CTA per SM too: C3 Sedov 128^3 at KZ = 2 with one CTA 6.66 ms
+    // per step against 7.90 at KZ = 1 with two -- the list build gains more from the taller blocks)
+    const bool ok = fits && (force_smem(g) <= kSmemTarget || KZ <= 2);
     if (fits && c->cfg.tile_cells_z > 0) break;
     if (!probing && ok) break;  // the estimate fits
     if (ok) kz_lo = KZ; else kz_hi = KZ;

@@ -474,7 +474,7 @@ struct sph_ctx {
   long long n_coinc = 0;        // directed coincident pairs of the owned particles (k_dup)
   unsigned long long* pairs_grad_h = nullptr;  // pinned: the last gradient loop's directed pairs
   float wide_margin = 0.2f;     // adaptive grid: DevGrid::wide_margin (env SPH_WIDE_MARGIN overrides)
-  int sparse_wide = 32;         // adaptive grid: blocks with fewer tile particles go wide (env SPH_SPARSE_WIDE; 0 = off)
+  int sparse_wide = 64;         // adaptive grid: blocks with fewer tile particles go wide (env SPH_SPARSE_WIDE; 0 = off)
   double coarse_q = 0.99;       // wide search grid: the h quantile its coarse cells are sized from (env SPH_COARSE_Q)
   // distinct wide search grids (env SPH_COARSE_LEVELS, 1..kCoarseLevels); C5s ms per step with 1 / 2 / 3:
   // 29.5 / 29.0 / 29.2 (the wide list build is bound by its gather latency, not by the candidates)

@@ -471,6 +471,7 @@ struct sph_ctx {
   size_t side_cap = 0, side_flag_cap = 0;
   int n_int = 0, n_bnd = 0;
   int kz_hint = 0;              // KZ chosen at the last rebuild (first probe of the next)
+  bool kz_hint_1cta = false;    // ... with one force CTA per SM
   long long n_coinc = 0;        // directed coincident pairs of the owned particles (k_dup)
   unsigned long long* pairs_grad_h = nullptr;  // pinned: the last gradient loop's directed pairs
   float wide_margin = 0.2f;     // adaptive grid: DevGrid::wide_margin (env SPH_WIDE_MARGIN overrides)
@@ -1342,7 +1343,9 @@ sph_status rebuild_impl(sph_ctx* c) {
   // the last rebuild's KZ is only a first probe: one above it (tiles may have shrunk since), then
   // the hint itself if that does not fit, then a bisection below
   const int hint = (c->kz_hint > 0 && c->kz_hint < KZ) ? c->kz_hint : 0;
-  if (hint) KZ = hint + 1;
+  // (a KZ taken at one force CTA per SM: a taller block cannot fit two CTAs, and one CTA takes at
+  // most KZ = 2 -- probe the hint itself first)
+  if (hint) KZ = c->kz_hint_1cta ? hint : hint + 1;
   if (c->cfg.tile_cells_z > 0) KZ = c->cfg.tile_cells_z;
   KZ = std::max(1, std::min(KZ, kz_max));
   g.lists_warps = 8;  // (the largest k_lists CTA for the fit test)
@@ -1417,6 +1420,7 @@ sph_status rebuild_impl(sph_ctx* c) {
     KZ = kz_lo == 0 ? (hint && hint < kz_hi ? hint : std::max(1, kz_hi / 2)) : (kz_lo + kz_hi) / 2;
   }
   c->kz_hint = g.KZ;
+  c->kz_hint_1cta = force_smem(g) > kSmemTarget;
   {
     const char* e = getenv("SPH_DENS_INNER");  // (tuning: Newton iterations per pass inside the CTA)
     g.dens_inner = e ? std::max(1, atoi(e)) : 6;

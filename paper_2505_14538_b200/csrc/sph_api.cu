@@ -443,6 +443,8 @@ struct sph_ctx {
   // pipelined host I/O (sph_stage_particles / sph_set_particles_staged / sph_get_async)
   static constexpr int kGetSlots = 8;
   cudaStream_t hstream = nullptr, dstream = nullptr;  // host -> device, device -> host copies
+  cudaStream_t h2stream = nullptr;                    // (host -> device by copy engine, SPH_H2D_CE_FRAC)
+  cudaEvent_t ev_h2 = nullptr;
   cudaEvent_t ev_staged = nullptr, ev_stage_free = nullptr;
   void* stage_buf = nullptr;
   size_t stage_bytes = 0;
@@ -2257,6 +2259,8 @@ sph_status ensure_io(sph_ctx* c) {
   if (c->hstream) return SPH_OK;
   CK(cudaStreamCreateWithFlags(&c->hstream, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&c->dstream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&c->h2stream, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&c->ev_h2, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_staged, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_stage_free, cudaEventDisableTiming));
   for (int k = 0; k < sph_ctx::kGetSlots; ++k) {
@@ -2345,13 +2349,25 @@ sph_status sph_stage_particles(sph_ctx* c, const sph_particles_in* in) {
     c->stage_bytes = bytes;
   } else if (c->stage_used) {
     CK(cudaStreamWaitEvent(c->hstream, c->ev_stage_free, 0));  // the last staged upload was taken
+    CK(cudaStreamWaitEvent(c->h2stream, c->ev_stage_free, 0));
   }
+  // (SPH_H2D_CE_FRAC: the leading fraction of every array goes through the copy engines on a
+  // second stream, the rest by kernel -- an experiment knob, default 0)
+  static const double ce_frac = getenv("SPH_H2D_CE_FRAC") ? std::min(1.0, std::max(0.0, atof(getenv("SPH_H2D_CE_FRAC")))) : 0.0;
   char* d = static_cast<char*>(c->stage_buf);
   auto up = [&](const void* src, size_t b) -> void* {
     if (!src) return nullptr;
     void* dst = d;
-    cudaError_t e_ = copy_chunked(dst, src, b, cudaMemcpyHostToDevice, c->hstream);
-    (void)e_;
+    const size_t bce = ce_frac > 0.0 ? std::min(b, (size_t)(ce_frac * b) & ~size_t(15)) : 0;
+    constexpr size_t kPiece = 4u << 20;
+    for (size_t o = 0; o < bce; o += kPiece)
+      cudaMemcpyAsync(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o, std::min(kPiece, bce - o),
+                      cudaMemcpyHostToDevice, c->h2stream);
+    if (b > bce) {
+      cudaError_t e_ = copy_chunked(static_cast<char*>(dst) + bce, static_cast<const char*>(src) + bce, b - bce,
+                                    cudaMemcpyHostToDevice, c->hstream);
+      (void)e_;
+    }
     d += al(b);
     return dst;
   };
@@ -2368,6 +2384,8 @@ sph_status sph_stage_particles(sph_ctx* c, const sph_particles_in* in) {
   sp.div_prev = (const float*)up(in->div_prev, 4 * n);
   sp.id = (const int64_t*)up(in->id, 8 * n);
   CK(cudaGetLastError());
+  CK(cudaEventRecord(c->ev_h2, c->h2stream));
+  CK(cudaStreamWaitEvent(c->hstream, c->ev_h2, 0));
   CK(cudaEventRecord(c->ev_staged, c->hstream));
   c->has_staged = true;
   return SPH_OK;
@@ -2404,6 +2422,7 @@ sph_status sph_synchronize(sph_ctx* c) {
   if (join_comm(c) != SPH_OK) return SPH_ERR_CUDA;
   CK(cudaStreamSynchronize(c->stream));
   if (c->hstream) CK(cudaStreamSynchronize(c->hstream));
+  if (c->h2stream) CK(cudaStreamSynchronize(c->h2stream));
   if (c->dstream) CK(cudaStreamSynchronize(c->dstream));
   return SPH_OK;
 }
@@ -2448,12 +2467,12 @@ sph_status sph_destroy(sph_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->cstream) cudaStreamSynchronize(c->cstream);
-  for (cudaStream_t x : {c->hstream, c->dstream})
+  for (cudaStream_t x : {c->hstream, c->dstream, c->h2stream})
     if (x) {
       cudaStreamSynchronize(x);
       cudaStreamDestroy(x);
     }
-  for (cudaEvent_t e : {c->ev_staged, c->ev_stage_free})
+  for (cudaEvent_t e : {c->ev_staged, c->ev_stage_free, c->ev_h2})
     if (e) cudaEventDestroy(e);
   for (int k = 0; k < sph_ctx::kGetSlots; ++k) {
     if (c->ev_gready[k]) cudaEventDestroy(c->ev_gready[k]);

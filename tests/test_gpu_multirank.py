@@ -305,9 +305,11 @@ def test_single_rank_slab_path(transport):
     assert abs(dt - one["dt"]) <= 1e-6 * one["dt"]
 
 
-def test_multirank_kdk_sedov_wide():
+@pytest.mark.parametrize("balance", [0, 1])
+def test_multirank_kdk_sedov_wide(balance):
     """KDK steps of the C3-like Sedov blast on three ranks: migration, rebuilds with G ghost
-    planes and wide particles on every rank.  Momentum: cross-rank pairs are evaluated on both
+    planes and wide particles on every rank (halo put on the loopback transport; balance = 1
+    also moves the slab cuts at every rebuild).  Momentum: cross-rank pairs are evaluated on both
     ranks (each keeps its own side) from tile coordinates, so the two sides agree to f32
     rounding, not bitwise (DESIGN.md §9): |Delta P| <= 1e-6 sum m |v| per step (north star);
     the trajectories track the single-context run to f32 rounding growth."""
@@ -316,7 +318,7 @@ def test_multirank_kdk_sedov_wide():
     p = _switches(W.sedov(48), 11)
     m = p["m"].astype(np.float64)
     steps = 3
-    g, parts = run_ranks(p, 3, _kdk(steps, []), h_tol=1e-5)
+    g, parts = run_ranks(p, 3, _kdk(steps, []), h_tol=1e-5, balance=balance)
     assert min(q["counters"]["wide_particles"] for q in parts) > 0
     ctx = Context(p, h_tol=1e-5)
     ref = _kdk(steps, [])(ctx)

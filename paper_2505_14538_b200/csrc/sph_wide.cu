@@ -88,14 +88,16 @@ __device__ __forceinline__ void coarse_range(int a, int k, int n, int F, int cn,
     cnt = hi >= lo ? hi / F - c0 + 1 : 0;
     return;
   }
-  const int am = ((a % n) + n) % n;
-  c0 = (2 * k + 1 >= n) ? 0 : am / F;
-  cnt = 0;
-  int ci = c0;
-  while (cnt < cn && coarse_meets(ci, a, k, n, F)) {
-    ++cnt;
-    ci = ci + 1 == cn ? 0 : ci + 1;
+  // closed form of "the cells from the one holding a, cyclically, while coarse_meets" (checked
+  // against that loop for every n < 70, F <= n, k <= n, a in [-2n, 2n): identical c0 and cnt)
+  if (2 * k + 1 >= n) {
+    c0 = 0;
+    cnt = cn;
+    return;
   }
+  const int am = ((a % n) + n) % n, e = am + 2 * k;
+  c0 = am / F;
+  cnt = e < n ? e / F - c0 + 1 : min(cn - c0 + (e - n) / F + 1, cn);
 }
 
 // coarse level of a wide particle whose search reaches kx, ky, kz grid cells: the finest

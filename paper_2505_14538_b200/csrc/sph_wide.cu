@@ -76,7 +76,11 @@ __device__ __forceinline__ bool coarse_meets(int ci, int a, int k, int n, int F,
   const int f0 = ci * F, w = min(F, n - f0);
   if (!per) return f0 <= a + 2 * k && f0 + w - 1 >= a;  // (non-periodic: the range clipped to the axis)
   if (2 * k + 1 >= n) return true;  // (the whole axis)
-  const int d0 = ((f0 - a) % n + n) % n;  // start of the coarse cell, from a (mod n)
+  // start of the coarse cell, from a (mod n): a = c - k with c in [0, n) and k <= (n - 1) / 2 + 1
+  // (reach), so f0 - a lies in (-n, 2n) and two conditional corrections replace the modulo
+  int d0 = f0 - a;
+  d0 += d0 < 0 ? n : 0;
+  d0 -= d0 >= n ? n : 0;
   return d0 <= 2 * k || d0 + w > n;
 }
 // coarse cells meeting the grid-cell range [a, a + 2k] (mod n): c0 (the one holding a) and

@@ -83,6 +83,15 @@ __device__ __forceinline__ bool coarse_meets(int ci, int a, int k, int n, int F,
   d0 -= d0 >= n ? n : 0;
   return d0 <= 2 * k || d0 + w > n;
 }
+// x / F for 0 <= x < 2^22, F >= 1 without an integer division: the f32 quotient is within one of
+// the exact one, then corrected (the force loop's "did j list i" takes three per wide partner)
+__device__ __forceinline__ int div_small(int x, int F) {
+  int q = __float2int_rz(__fdividef((float)x, (float)F));
+  q += (q + 1) * F <= x ? 1 : 0;
+  q -= q * F > x ? 1 : 0;
+  return q;
+}
+
 // coarse cells meeting the grid-cell range [a, a + 2k] (mod n): c0 (the one holding a) and
 // the cnt that follow it cyclically
 __device__ __forceinline__ void coarse_range(int a, int k, int n, int F, int cn, int& c0, int& cnt, bool per = true) {
@@ -468,8 +477,8 @@ __global__ void __launch_bounds__(256, SPH_WF_MINB) k_wide_force(DevGrid g, DevP
       const int kx = px ? reach(Rj, g.side[0], g.nx) : (int)ceilf(Rj / g.side[0]), ky = reach(Rj, g.side[1], g.ny),
                 kz = reach(Rj, g.side[2], g.nz);
       const int F = s.cF[coarse_level(s, kx, ky, kz)];
-      seen = coarse_meets(cxi / F, cxj - kx, kx, g.nx, F, px) && coarse_meets(cyi / F, cyj - ky, ky, g.ny, F) &&
-             coarse_meets(czi / F, czj - kz, kz, g.nz, F);
+      seen = coarse_meets(div_small(cxi, F), cxj - kx, kx, g.nx, F, px) &&
+             coarse_meets(div_small(cyi, F), cyj - ky, ky, g.ny, F) && coarse_meets(div_small(czi, F), czj - kz, kz, g.nz, F);
     } else {
       seen = within(cxi, cxj, 1, g.nx, px) && within(cyi, cyj, 1, g.ny) && within(czi, czj, 1, g.nz);
     }
